@@ -1,0 +1,250 @@
+/*
+ * splat_b200.h — C-ABI drop-in boundary for the Mini-Splatting2 optimisation hot path
+ * (tile-based differentiable Gaussian rasterizer, blending-weight importance, depth
+ * rendering + unprojection) implemented as hand-written sm_100a CUDA kernels.
+ *
+ * Every entry point replaces one reference C++ function (paths relative to
+ * /root/reference/proj):
+ *
+ *   splat_render                 <- render<float>              include/splat/rasterizer.hpp:72-76
+ *                                                               src/rasterizer.cpp:175-182
+ *   splat_accumulate_importance  <- accumulate_importance<float> rasterizer.hpp:79-82,
+ *                                                               rasterizer.cpp:184-193
+ *   splat_render_backward        <- render_backward<float>     include/splat/gradients.hpp:52-56,
+ *                                                               src/gradients.cpp:45-222
+ *   splat_l1_loss                <- l1_loss<float>             include/splat/loss.hpp:9-10,
+ *                                                               src/loss.cpp:63-76
+ *   splat_render_backward_l1     <- l1_loss + render_backward fused (trainer.cpp:228-239 with
+ *                                   lambda_dssim = 0)
+ *   splat_adam_step              <- OptimState::step           include/splat/optimizer.hpp:41,
+ *                                                               src/optimizer.cpp:40-71
+ *   splat_depth_unproject        <- depth_reinitialize unprojection loop src/densify.cpp:207-222
+ *   splat_project_debug / splat_tiles_debug <- project<float> (rasterizer.cpp:10-90) and
+ *                                   detail::bin_tiles (rasterizer.hpp:156-174), exposed for
+ *                                   bit-exact checks of rects, sort keys, lists and ranges.
+ *
+ * Conventions (mirroring the reference):
+ *   - Gaussian storage is the reference's GaussianSetT<float> layout: centers [N][3],
+ *     log_scales [N][3], rotations [N][4] (w,x,y,z), opacity_logits [N], sh [N][48]
+ *     coefficient-major (sh[k*3+c]).
+ *   - Images are H x W x C row-major, channel-interleaved (types.hpp:24-52).
+ *   - Pointers named *_dev are device memory; everything else is host memory.
+ *   - All calls are asynchronous on the context stream unless documented otherwise.
+ *   - Exceptions of the reference map to status codes: std::invalid_argument ->
+ *     SPLAT_ERR_INVALID_ARGUMENT, std::logic_error -> SPLAT_ERR_LOGIC,
+ *     std::runtime_error -> SPLAT_ERR_RUNTIME.  splat_last_error() returns the message.
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPLAT_SH_COEFFS 16
+#define SPLAT_SH_VALUES 48
+#define SPLAT_GRAD_FLOATS 59 /* 3 + 3 + 4 + 1 + 48 floats per Gaussian */
+
+typedef enum splat_status {
+    SPLAT_OK = 0,
+    SPLAT_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    SPLAT_ERR_LOGIC = 2,            /* std::logic_error (arrays / rows out of sync) */
+    SPLAT_ERR_RUNTIME = 3,          /* std::runtime_error (e.g. no valid depth pixel) */
+    SPLAT_ERR_CUDA = 4,
+    SPLAT_ERR_OUT_OF_MEMORY = 5,
+    SPLAT_ERR_NO_FORWARD_STATE = 6  /* fused/reuse call without a matching forward */
+} splat_status;
+
+/* Mirrors CameraT<float> (camera.hpp:12-22). rotation is row-major world->camera. */
+typedef struct splat_camera {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float rotation[9];
+    float translation[3];
+    float znear, zfar;
+} splat_camera;
+
+/* Mirrors RasterConfig (rasterizer.hpp:17-25) field for field. */
+typedef struct splat_raster_config {
+    int32_t tile_size;          /* 16 */
+    int32_t apply_thresholds;   /* 1; 0 = exact mode (no gates, full-image rects) */
+    double transmittance_min;   /* 1e-4 */
+    double contribution_min;    /* 1/255 */
+    double alpha_max;           /* 0.99 */
+    double lowpass;             /* 0.3 */
+    double radius_sigmas;       /* 3.0 */
+} splat_raster_config;
+
+/* GaussianSetT<float> (gaussian_set.hpp:60-81) as plain arrays. */
+typedef struct splat_gaussians {
+    const float* centers;        /* [n][3] */
+    const float* log_scales;     /* [n][3] */
+    const float* rotations;      /* [n][4] (w,x,y,z) */
+    const float* opacity_logits; /* [n] */
+    const float* sh;             /* [n][48] coefficient-major */
+    int32_t n;
+    int32_t active_sh_degree;
+} splat_gaussians;
+
+/* RenderOutput<float> (rasterizer.hpp:43-51); every field may be NULL. */
+typedef struct splat_render_outputs {
+    float* color;            /* [H][W][3] */
+    float* alpha;            /* [H][W] */
+    float* depth;            /* [H][W] */
+    float* transmittance;    /* [H][W] */
+    int32_t* max_contributor;/* [H][W], -1 = background */
+} splat_render_outputs;
+
+/* ImportanceReport<float> (rasterizer.hpp:54-61). */
+typedef struct splat_importance_outputs {
+    float* importance;        /* [n] sum of blend weights */
+    float* max_weight;        /* [n] */
+    int32_t* max_pixel_count; /* [n] */
+} splat_importance_outputs;
+
+/* ParamGrads<float> (gradients.hpp:14-46). */
+typedef struct splat_param_grads {
+    float* d_centers;        /* [n][3] */
+    float* d_log_scales;     /* [n][3] */
+    float* d_rotations;      /* [n][4] */
+    float* d_opacity_logits; /* [n] */
+    float* d_sh;             /* [n][48] */
+    float* grad2d_accum;     /* [n] (may be NULL) */
+    int32_t* grad2d_count;   /* [n] (may be NULL) */
+} splat_param_grads;
+
+/* AdamConfig + LrSchedule (optimizer.hpp:12-32). */
+typedef struct splat_adam_config {
+    double beta1, beta2, eps;
+    double lr_init, lr_final;
+    int32_t max_steps;
+    int32_t _pad;
+    double scene_extent;
+    double lr_sh_dc, lr_sh_rest, lr_opacity, lr_scale, lr_rotation;
+} splat_adam_config;
+
+/* Parameter groups for splat_adam_step's group_mask. */
+#define SPLAT_GROUP_CENTERS   1u
+#define SPLAT_GROUP_SCALES    2u
+#define SPLAT_GROUP_ROTATIONS 4u
+#define SPLAT_GROUP_OPACITY   8u
+#define SPLAT_GROUP_SH        16u
+#define SPLAT_GROUP_ALL       31u
+
+/* Mutable parameter pointers (device) for the optimizer. */
+typedef struct splat_params_mut {
+    float* centers;
+    float* log_scales;
+    float* rotations;
+    float* opacity_logits;
+    float* sh;
+    int32_t n;
+    int32_t active_sh_degree;
+} splat_params_mut;
+
+/* Adam moments, same layout as the parameters (optimizer.hpp:69-76). */
+typedef struct splat_adam_moments {
+    float *m_centers, *v_centers;
+    float *m_log_scales, *v_log_scales;
+    float *m_rotations, *v_rotations;
+    float *m_opacity, *v_opacity;
+    float *m_sh, *v_sh;
+} splat_adam_moments;
+
+/* Pixel validity rule for splat_depth_unproject. */
+#define SPLAT_DEPTH_RULE_ARGMAX 0 /* max_contributor >= 0 (densify.cpp:216) */
+#define SPLAT_DEPTH_RULE_ALPHA  1 /* accumulated alpha > alpha_threshold (BASELINE cfg 2) */
+
+typedef struct splat_ctx splat_ctx;
+
+/* ---- context ------------------------------------------------------------------------ */
+int splat_ctx_create(int device, splat_ctx** out);
+int splat_ctx_destroy(splat_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL = legacy default. */
+int splat_ctx_set_stream(splat_ctx* ctx, void* cuda_stream);
+int splat_sync(splat_ctx* ctx);
+const char* splat_last_error(const splat_ctx* ctx);
+/* Number of kernels this context launched since creation (for bench accounting). */
+int64_t splat_kernel_launches(const splat_ctx* ctx);
+
+/* ---- forward ------------------------------------------------------------------------ */
+/* render<float>: g/mask/out are device pointers; background is host float[3]. The context
+ * keeps the forward state (sorted tile lists, projected records, per-pixel T_final and last
+ * contributor) for a following splat_render_backward(reuse_forward=1) / _l1 / unproject.
+ * report may be NULL (render without ImportanceReport). */
+int splat_render(splat_ctx* ctx, const splat_gaussians* g_dev, const splat_camera* cam,
+                 const splat_raster_config* cfg, const uint8_t* mask_dev,
+                 const float background[3], const splat_render_outputs* out_dev,
+                 const splat_importance_outputs* report_dev);
+
+int splat_accumulate_importance(splat_ctx* ctx, const splat_gaussians* g_dev,
+                                const splat_camera* cam, const splat_raster_config* cfg,
+                                const uint8_t* mask_dev,
+                                const splat_importance_outputs* report_dev);
+
+/* ---- backward ----------------------------------------------------------------------- */
+/* render_backward<float>. accumulate=0 zeroes grads first (reference returns fresh
+ * ParamGrads); accumulate=1 adds (ParamGrads::add, gradients.hpp:35-45). reuse_forward=1
+ * reuses the state of the immediately preceding splat_render on the same inputs. */
+int splat_render_backward(splat_ctx* ctx, const splat_gaussians* g_dev,
+                          const splat_camera* cam, const splat_raster_config* cfg,
+                          const float* d_color_dev, const uint8_t* mask_dev,
+                          const float background[3], const splat_param_grads* grads_dev,
+                          int accumulate, int reuse_forward);
+
+/* l1_loss<float>: loss_dev (device float scalar) may be NULL, grad_dev may be NULL. */
+int splat_l1_loss(splat_ctx* ctx, const float* a_dev, const float* b_dev, int64_t count,
+                  float* grad_dev, float* loss_dev);
+
+/* Fused L1 + backward against target_dev, using the colour of the preceding splat_render
+ * (which must have run on the same inputs). loss_dev may be NULL. */
+int splat_render_backward_l1(splat_ctx* ctx, const splat_gaussians* g_dev,
+                             const splat_camera* cam, const splat_raster_config* cfg,
+                             const float* target_dev, const uint8_t* mask_dev,
+                             const float background[3], const splat_param_grads* grads_dev,
+                             int accumulate, float* loss_dev);
+
+/* ---- optimizer ---------------------------------------------------------------------- */
+/* OptimState::step. *step_count is the host-side step counter t (read, then incremented),
+ * exactly as OptimState::t_ (optimizer.cpp:45-47). Groups not in group_mask are left
+ * untouched; quaternion renormalisation (optimizer.cpp:69) runs iff
+ * SPLAT_GROUP_ROTATIONS is in the mask. */
+int splat_adam_step(splat_ctx* ctx, const splat_params_mut* params_dev,
+                    const splat_param_grads* grads_dev, const splat_adam_moments* moments_dev,
+                    const splat_adam_config* cfg, int32_t* step_count, uint32_t group_mask);
+
+/* ---- depth unprojection ------------------------------------------------------------- */
+/* For the preceding splat_render: every valid pixel (rule) whose raster index satisfies
+ * (view_index*H*W + pixel + seed) % stride == 0 is unprojected to
+ * cam.center() + depth * cam.ray_direction(px, py) (densify.cpp:213-220). Points are
+ * written compacted in raster order: points_dev [capacity][3], pixel_dev [capacity].
+ * *count_dev receives the number of selected pixels (may exceed capacity: nothing is
+ * written past capacity). stride = 1 selects every valid pixel. */
+int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule,
+                          float alpha_threshold, int64_t view_index, int32_t stride,
+                          int64_t seed, float* points_dev, int32_t* pixel_dev,
+                          int64_t capacity, int32_t* count_dev);
+
+/* ---- bit-exact debug views of the preceding forward (host outputs, synchronous) ------ */
+/* n_survivors / n_pairs of the last forward. */
+int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs,
+                         int32_t* tiles_x, int32_t* tiles_y);
+/* Per Gaussian (index order): rect[4] = x0,x1,y0,y1 (0,0,0,0 when culled), radius,
+ * depth bits, survivor flag. Any pointer may be NULL. */
+int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* depth,
+                        uint8_t* survivor, float* mean2d, float* conic, float* color,
+                        float* opacity);
+/* Sorted pairs: key_tile[p], gaussian[p] for p < n_pairs (per-tile lists, depth-ordered),
+ * ranges[2*t] = start, ranges[2*t+1] = end, depth_order[r] = r-th survivor (by
+ * (depth, index)). Any pointer may be NULL. */
+int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int32_t* ranges,
+                      int32_t* depth_order);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLAT_B200_H */

@@ -1,0 +1,351 @@
+// oracle/ref_capi.cpp — C interface over the reference's OWN hot-path code.
+//
+// TEST INFRASTRUCTURE ONLY.  Built by oracle/Makefile into oracle/_ref/libsplat_ref*.so from
+// /root/reference/proj/src/*.cpp compiled in place (never copied) against the Eigen-subset
+// shim in oracle/compat.  Exposes the splat_oracle.h interface with the ref_ prefix so the
+// tests can run the reference itself next to the C restatement (oracle/splat_oracle.c) and
+// the CUDA kernels, plus a few reference-only entry points (Adam from fresh moments,
+// depth_reinitialize) used to pin the restatement.
+#define ORACLE_FN(name) ref_##name
+#include "splat_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "splat/densify.hpp"
+#include "splat/gradients.hpp"
+#include "splat/loss.hpp"
+#include "splat/optimizer.hpp"
+#include "splat/rasterizer.hpp"
+#include "splat/simplify.hpp"
+#include "splat/visibility.hpp"
+
+using namespace splat;
+
+namespace {
+
+std::string g_err;
+
+int map_exception(const std::exception& e, int code) {
+    g_err = e.what();
+    return code;
+}
+
+#define REF_TRY try {
+#define REF_CATCH                                                        \
+    }                                                                    \
+    catch (const std::invalid_argument& e) {                             \
+        return map_exception(e, SPLAT_ERR_INVALID_ARGUMENT);             \
+    }                                                                    \
+    catch (const std::logic_error& e) {                                  \
+        return map_exception(e, SPLAT_ERR_LOGIC);                        \
+    }                                                                    \
+    catch (const std::runtime_error& e) {                                \
+        return map_exception(e, SPLAT_ERR_RUNTIME);                      \
+    }                                                                    \
+    catch (const std::exception& e) {                                    \
+        return map_exception(e, SPLAT_ERR_RUNTIME);                      \
+    }
+
+GaussianSet to_set(const splat_gaussians* g) {
+    GaussianSet s;
+    s.active_sh_degree = g->active_sh_degree;
+    s.resize(g->n);
+    for (int i = 0; i < g->n; ++i) {
+        s.centers[i] = Vec3f(g->centers[3 * i], g->centers[3 * i + 1], g->centers[3 * i + 2]);
+        s.log_scales[i] = Vec3f(g->log_scales[3 * i], g->log_scales[3 * i + 1], g->log_scales[3 * i + 2]);
+        s.rotations[i] = Vec4f(g->rotations[4 * i], g->rotations[4 * i + 1], g->rotations[4 * i + 2],
+                               g->rotations[4 * i + 3]);
+        s.opacity_logits[i] = g->opacity_logits[i];
+    }
+    if (g->n > 0) std::memcpy(s.sh.data(), g->sh, sizeof(float) * 48 * static_cast<size_t>(g->n));
+    return s;
+}
+
+Camera to_cam(const splat_camera* c) {
+    Camera cam;
+    cam.width = c->width;
+    cam.height = c->height;
+    cam.fx = c->fx;
+    cam.fy = c->fy;
+    cam.cx = c->cx;
+    cam.cy = c->cy;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) cam.rotation(i, j) = c->rotation[i * 3 + j];
+    cam.translation = Vec3f(c->translation[0], c->translation[1], c->translation[2]);
+    cam.znear = c->znear;
+    cam.zfar = c->zfar;
+    return cam;
+}
+
+RasterConfig to_cfg(const splat_raster_config* c) {
+    RasterConfig r;
+    r.tile_size = c->tile_size;
+    r.transmittance_min = c->transmittance_min;
+    r.contribution_min = c->contribution_min;
+    r.alpha_max = c->alpha_max;
+    r.lowpass = c->lowpass;
+    r.radius_sigmas = c->radius_sigmas;
+    r.apply_thresholds = c->apply_thresholds != 0;
+    return r;
+}
+
+std::vector<char> to_mask(const uint8_t* m, int n) {
+    std::vector<char> v(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) v[i] = static_cast<char>(m[i]);
+    return v;
+}
+
+AdamConfig to_adam(const splat_adam_config* c) {
+    AdamConfig a;
+    a.beta1 = c->beta1;
+    a.beta2 = c->beta2;
+    a.eps = c->eps;
+    a.position.lr_init = c->lr_init;
+    a.position.lr_final = c->lr_final;
+    a.position.max_steps = c->max_steps;
+    a.scene_extent = c->scene_extent;
+    a.lr_sh_dc = c->lr_sh_dc;
+    a.lr_sh_rest = c->lr_sh_rest;
+    a.lr_opacity = c->lr_opacity;
+    a.lr_scale = c->lr_scale;
+    a.lr_rotation = c->lr_rotation;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+float ref_exp(float x) { return std::exp(x); }
+
+int ref_project(const splat_gaussians* g, const splat_camera* c, const splat_raster_config* cf,
+                const uint8_t* mask, int32_t* n_survivors, int32_t* order, int32_t* rect,
+                int32_t* radius, float* depth, float* mean2d, float* conic, float* color,
+                float* opacity) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    const Camera cam = to_cam(c);
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    const auto proj = project<float>(set, cam, to_cfg(cf), mask ? &mv : nullptr);
+    *n_survivors = static_cast<int32_t>(proj.size());
+    for (size_t r = 0; r < proj.size(); ++r) {
+        const auto& pg = proj[r];
+        const int i = pg.index;
+        if (order) order[r] = i;
+        if (rect) {
+            rect[4 * i] = pg.x0;
+            rect[4 * i + 1] = pg.x1;
+            rect[4 * i + 2] = pg.y0;
+            rect[4 * i + 3] = pg.y1;
+        }
+        if (radius) radius[i] = pg.radius;
+        if (depth) depth[i] = pg.depth_mean;
+        if (mean2d) {
+            mean2d[2 * i] = pg.mean2d[0];
+            mean2d[2 * i + 1] = pg.mean2d[1];
+        }
+        if (conic)
+            for (int k = 0; k < 3; ++k) conic[3 * i + k] = pg.conic[k];
+        if (color)
+            for (int k = 0; k < 3; ++k) color[3 * i + k] = pg.color[k];
+        if (opacity) opacity[i] = pg.opacity;
+    }
+    return 0;
+    REF_CATCH
+}
+
+int ref_tiles(const splat_gaussians* g, const splat_camera* c, const splat_raster_config* cf,
+              const uint8_t* mask, int64_t* n_pairs, int32_t* ranges, int32_t* gaussian,
+              int64_t capacity) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    const Camera cam = to_cam(c);
+    cam.validate();
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    const RasterConfig cfg = to_cfg(cf);
+    const auto proj = project<float>(set, cam, cfg, mask ? &mv : nullptr);
+    const auto grid = detail::bin_tiles(proj, cam.width, cam.height, cfg.tile_size);
+    int64_t total = 0;
+    for (size_t t = 0; t < grid.lists.size(); ++t) {
+        if (ranges) {
+            ranges[2 * t] = static_cast<int32_t>(total);
+            ranges[2 * t + 1] = static_cast<int32_t>(total + grid.lists[t].size());
+        }
+        total += static_cast<int64_t>(grid.lists[t].size());
+    }
+    *n_pairs = total;
+    if (gaussian && capacity >= total) {
+        int64_t k = 0;
+        for (const auto& list : grid.lists)
+            for (int pos : list) gaussian[k++] = proj[pos].index;
+    }
+    return 0;
+    REF_CATCH
+}
+
+int ref_render(const splat_gaussians* g, const splat_camera* c, const splat_raster_config* cf,
+               const uint8_t* mask, const float bg[3], float* color, float* alpha, float* depth,
+               float* transmittance, int32_t* max_contributor, float* importance,
+               float* max_weight, int32_t* max_pixel_count, int64_t* stats) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    const Camera cam = to_cam(c);
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    ImportanceReport<float> report;
+    const bool want_report = importance || max_weight || max_pixel_count;
+    const auto out = render<float>(set, cam, to_cfg(cf), mask ? &mv : nullptr,
+                                   Vec3f(bg[0], bg[1], bg[2]), want_report ? &report : nullptr);
+    const size_t hw = static_cast<size_t>(cam.width) * cam.height;
+    if (color) std::memcpy(color, out.color.data.data(), sizeof(float) * hw * 3);
+    if (alpha) std::memcpy(alpha, out.alpha.data.data(), sizeof(float) * hw);
+    if (depth) std::memcpy(depth, out.depth.data.data(), sizeof(float) * hw);
+    if (transmittance) std::memcpy(transmittance, out.transmittance.data.data(), sizeof(float) * hw);
+    if (max_contributor) std::memcpy(max_contributor, out.max_contributor.data(), sizeof(int32_t) * hw);
+    if (importance) std::memcpy(importance, report.importance.data(), sizeof(float) * g->n);
+    if (max_weight) std::memcpy(max_weight, report.max_weight.data(), sizeof(float) * g->n);
+    if (max_pixel_count)
+        std::memcpy(max_pixel_count, report.max_pixel_count.data(), sizeof(int32_t) * g->n);
+    if (stats) stats[0] = stats[1] = -1;
+    return 0;
+    REF_CATCH
+}
+
+int ref_accumulate_importance(const splat_gaussians* g, const splat_camera* c,
+                              const splat_raster_config* cf, const uint8_t* mask,
+                              float* importance, float* max_weight, int32_t* max_pixel_count) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    const auto rep = accumulate_importance<float>(set, to_cam(c), to_cfg(cf), mask ? &mv : nullptr);
+    std::memcpy(importance, rep.importance.data(), sizeof(float) * g->n);
+    std::memcpy(max_weight, rep.max_weight.data(), sizeof(float) * g->n);
+    std::memcpy(max_pixel_count, rep.max_pixel_count.data(), sizeof(int32_t) * g->n);
+    return 0;
+    REF_CATCH
+}
+
+int ref_render_backward(const splat_gaussians* g, const splat_camera* c,
+                        const splat_raster_config* cf, const float* d_color, const uint8_t* mask,
+                        const float bg[3], float* d_centers, float* d_log_scales,
+                        float* d_rotations, float* d_opacity, float* d_sh, float* grad2d_accum,
+                        int32_t* grad2d_count) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    const Camera cam = to_cam(c);
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    Imagef dc(cam.width, cam.height, 3);
+    std::memcpy(dc.data.data(), d_color, sizeof(float) * dc.data.size());
+    const auto gr = render_backward<float>(set, cam, to_cfg(cf), dc, mask ? &mv : nullptr,
+                                           Vec3f(bg[0], bg[1], bg[2]));
+    for (int i = 0; i < g->n; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            d_centers[3 * i + k] = gr.d_centers[i][k];
+            d_log_scales[3 * i + k] = gr.d_log_scales[i][k];
+        }
+        for (int k = 0; k < 4; ++k) d_rotations[4 * i + k] = gr.d_rotations[i][k];
+        d_opacity[i] = gr.d_opacity_logits[i];
+        if (grad2d_accum) grad2d_accum[i] = gr.grad2d_accum[i];
+        if (grad2d_count) grad2d_count[i] = gr.grad2d_count[i];
+    }
+    if (g->n > 0) std::memcpy(d_sh, gr.d_sh.data(), sizeof(float) * 48 * static_cast<size_t>(g->n));
+    return 0;
+    REF_CATCH
+}
+
+float ref_l1_loss(const float* a, const float* b, int64_t count, float* grad) {
+    Imagef ia(static_cast<int>(count), 1, 1), ib(static_cast<int>(count), 1, 1), ig;
+    std::memcpy(ia.data.data(), a, sizeof(float) * count);
+    std::memcpy(ib.data.data(), b, sizeof(float) * count);
+    const float l = l1_loss<float>(ia, ib, grad ? &ig : nullptr);
+    if (grad) std::memcpy(grad, ig.data.data(), sizeof(float) * count);
+    return l;
+}
+
+double ref_lr_at(const splat_adam_config* cfg, int32_t step) {
+    return to_adam(cfg).position.at(step);
+}
+
+// `steps` reference OptimState::step calls from fresh (zero) moments with the same grads.
+int ref_adam_steps(float* centers, float* log_scales, float* rotations, float* opacity_logits,
+                   float* sh, int32_t n, const float* d_centers, const float* d_log_scales,
+                   const float* d_rotations, const float* d_opacity, const float* d_sh,
+                   const splat_adam_config* cfg, int32_t steps) {
+    REF_TRY
+    splat_gaussians gv{centers, log_scales, rotations, opacity_logits, sh, n, 3};
+    GaussianSet set = to_set(&gv);
+    ParamGrads<float> gr;
+    gr.resize_zero(n);
+    for (int i = 0; i < n; ++i) {
+        gr.d_centers[i] = Vec3f(d_centers[3 * i], d_centers[3 * i + 1], d_centers[3 * i + 2]);
+        gr.d_log_scales[i] = Vec3f(d_log_scales[3 * i], d_log_scales[3 * i + 1], d_log_scales[3 * i + 2]);
+        gr.d_rotations[i] = Vec4f(d_rotations[4 * i], d_rotations[4 * i + 1], d_rotations[4 * i + 2],
+                                  d_rotations[4 * i + 3]);
+        gr.d_opacity_logits[i] = d_opacity[i];
+    }
+    if (n > 0) std::memcpy(gr.d_sh.data(), d_sh, sizeof(float) * 48 * static_cast<size_t>(n));
+    OptimState opt(to_adam(cfg), n);
+    for (int s = 0; s < steps; ++s) opt.step(set, gr);
+    for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            centers[3 * i + k] = set.centers[i][k];
+            log_scales[3 * i + k] = set.log_scales[i][k];
+        }
+        for (int k = 0; k < 4; ++k) rotations[4 * i + k] = set.rotations[i][k];
+        opacity_logits[i] = set.opacity_logits[i];
+    }
+    if (n > 0) std::memcpy(sh, set.sh.data(), sizeof(float) * 48 * static_cast<size_t>(n));
+    return 0;
+    REF_CATCH
+}
+
+// depth_reinitialize (densify.cpp:197-253) over one view; writes the fresh set's centers
+// (a seeded permutation of the unprojected pool when sample_count >= pool size).
+int ref_depth_reinitialize(const splat_gaussians* g, const splat_camera* c,
+                           const splat_raster_config* cf, const float* image,
+                           int32_t sample_count, uint32_t seed, float* centers_out,
+                           int32_t* count_out) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    const Camera cam = to_cam(c);
+    Imagef img(cam.width, cam.height, 3);
+    std::memcpy(img.data.data(), image, sizeof(float) * img.data.size());
+    std::mt19937 rng(seed);
+    const GaussianSet fresh = depth_reinitialize(set, {cam}, {img}, sample_count, to_cfg(cf), rng);
+    *count_out = fresh.size();
+    for (int i = 0; i < fresh.size(); ++i)
+        for (int k = 0; k < 3; ++k) centers_out[3 * i + k] = fresh.centers[i][k];
+    return 0;
+    REF_CATCH
+}
+
+// global_importance (simplify.cpp:13-34) over several views: fp64 Σ importance and Σ counts.
+int ref_global_importance(const splat_gaussians* g, const splat_camera* cams, int32_t n_cams,
+                          const splat_raster_config* cf, double* accum_weight,
+                          int32_t* intersections) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<Camera> cv;
+    for (int k = 0; k < n_cams; ++k) cv.push_back(to_cam(&cams[k]));
+    const auto gi = global_importance(set, cv, to_cfg(cf));
+    for (int i = 0; i < g->n; ++i) {
+        accum_weight[i] = gi.accum_weight[i];
+        intersections[i] = gi.intersections[i];
+    }
+    return 0;
+    REF_CATCH
+}
+
+}  // extern "C"

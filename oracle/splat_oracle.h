@@ -1,0 +1,97 @@
+/*
+ * splat_oracle.h — CPU parity oracle for the Mini-Splatting2 rasterizer hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load the oracle libraries (liboracle, oracle/_ref).  The
+ * product path (paper_2411_12788_b200/) never calls into this directory.
+ *
+ * Two implementations export this same C interface:
+ *   - oracle/splat_oracle.c   : a plain-C restatement of the reference algorithm, function by
+ *                               function (symbols prefixed oracle_);
+ *   - oracle/ref_capi.cpp     : the reference's OWN sources (/root/reference/proj/src), compiled
+ *                               in place against oracle/compat/Eigen (symbols prefixed ref_),
+ *                               built into oracle/_ref/ by oracle/Makefile.
+ * The restatement is pinned against the reference build (bitwise, tests/test_oracle_pin.py)
+ * and against the reference's own known-answer tests (tests/golden/).
+ *
+ * Exp modes: liboracle.so / libsplat_ref.so use splat_expf (include/splat_expf.h), the
+ * exp the CUDA kernels use ("mode B", bit-exact parity); liboracle_libm.so /
+ * libsplat_ref_libm.so use glibc expf ("mode A", the reference exactly as shipped).
+ */
+#ifndef SPLAT_ORACLE_H
+#define SPLAT_ORACLE_H
+
+#include "splat_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef ORACLE_FN
+#define ORACLE_FN(name) oracle_##name
+#endif
+
+const char* ORACLE_FN(last_error)(void);
+
+/* project<float> (rasterizer.cpp:10-90), results scattered per Gaussian index.
+ * order[r] = index of the r-th survivor in (depth, index) order; *n_survivors its length. */
+int ORACLE_FN(project)(const splat_gaussians* g, const splat_camera* cam,
+                       const splat_raster_config* cfg, const uint8_t* mask,
+                       int32_t* n_survivors, int32_t* order, int32_t* rect, int32_t* radius,
+                       float* depth, float* mean2d, float* conic, float* color, float* opacity);
+
+/* detail::bin_tiles (rasterizer.hpp:156-174) as CSR over Gaussian indices:
+ * ranges[2t], ranges[2t+1] = [start, end) into gaussian[]. *n_pairs always receives P;
+ * gaussian is written only when capacity >= P (pass capacity 0 to query). */
+int ORACLE_FN(tiles)(const splat_gaussians* g, const splat_camera* cam,
+                     const splat_raster_config* cfg, const uint8_t* mask, int64_t* n_pairs,
+                     int32_t* ranges, int32_t* gaussian, int64_t capacity);
+
+/* render<float> with optional ImportanceReport (rasterizer.cpp:96-182). Any output may be
+ * NULL. stats (nullable, int64[2]) receives list visits V and committed blends C. */
+int ORACLE_FN(render)(const splat_gaussians* g, const splat_camera* cam,
+                      const splat_raster_config* cfg, const uint8_t* mask, const float bg[3],
+                      float* color, float* alpha, float* depth, float* transmittance,
+                      int32_t* max_contributor, float* importance, float* max_weight,
+                      int32_t* max_pixel_count, int64_t* stats);
+
+/* render_backward<float> (gradients.cpp:45-222). Grad arrays are overwritten (fresh
+ * ParamGrads). grad2d_accum / grad2d_count may be NULL. */
+int ORACLE_FN(render_backward)(const splat_gaussians* g, const splat_camera* cam,
+                               const splat_raster_config* cfg, const float* d_color,
+                               const uint8_t* mask, const float bg[3], float* d_centers,
+                               float* d_log_scales, float* d_rotations, float* d_opacity,
+                               float* d_sh, float* grad2d_accum, int32_t* grad2d_count);
+
+/* l1_loss<float> (loss.cpp:63-76). grad may be NULL. */
+float ORACLE_FN(l1_loss)(const float* a, const float* b, int64_t count, float* grad);
+
+/* OptimState::step (optimizer.cpp:40-71) on arrays; params/moments updated in place.
+ * Groups outside group_mask are skipped; rotations are renormalised iff rotations are in
+ * the mask (all groups = the reference exactly). */
+int ORACLE_FN(adam_step)(float* centers, float* log_scales, float* rotations,
+                         float* opacity_logits, float* sh, int32_t n, const float* d_centers,
+                         const float* d_log_scales, const float* d_rotations,
+                         const float* d_opacity, const float* d_sh, float* m, float* v,
+                         const splat_adam_config* cfg, int32_t* step_count,
+                         uint32_t group_mask);
+
+/* LrSchedule::at (optimizer.cpp:8-12). */
+double ORACLE_FN(lr_at)(const splat_adam_config* cfg, int32_t step);
+
+/* depth_reinitialize unprojection (densify.cpp:207-222) over one rendered view, with the
+ * selection rule of splat_depth_unproject (include/splat_b200.h). */
+int ORACLE_FN(unproject)(const splat_camera* cam, const int32_t* max_contributor,
+                         const float* alpha, const float* depth, int rule,
+                         float alpha_threshold, int64_t view_index, int32_t stride,
+                         int64_t seed, float* points, int32_t* pixel, int64_t capacity,
+                         int64_t* count);
+
+/* The exp the library was built with (splat_expf or glibc expf). */
+float ORACLE_FN(exp)(float x);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLAT_ORACLE_H */

@@ -1,0 +1,247 @@
+"""Test-side loader for the CPU parity oracles (oracle/liboracle*.so, oracle/_ref/libsplat_ref*.so).
+
+TEST INFRASTRUCTURE: imported only by tests/, __graft_entry__.smoke() and bench.py's CPU legs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_2411_12788_b200.capi import AdamConfig, Camera, Gaussians, RasterConfig
+
+ROOT = Path(__file__).resolve().parents[1]
+ORACLE_DIR = ROOT / "oracle"
+LIBS = {
+    ("oracle", "B"): ORACLE_DIR / "liboracle.so",
+    ("oracle", "A"): ORACLE_DIR / "liboracle_libm.so",
+    ("ref", "B"): ORACLE_DIR / "_ref" / "libsplat_ref.so",
+    ("ref", "A"): ORACLE_DIR / "_ref" / "libsplat_ref_libm.so",
+}
+
+fp = C.POINTER(C.c_float)
+ip = C.POINTER(C.c_int32)
+u8p = C.POINTER(C.c_uint8)
+i64p = C.POINTER(C.c_int64)
+
+
+def build_oracle() -> None:
+    """(Re)build the oracle libraries (and oracle/_ref when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "all"], check=True)
+
+
+def available(kind: str, mode: str = "B") -> bool:
+    return LIBS[(kind, mode)].exists()
+
+
+def _ptr(a, t=fp):
+    if a is None:
+        return t()
+    return a.ctypes.data_as(t)
+
+
+class GaussiansView:
+    """Keeps numpy arrays alive while a Gaussians struct points at them."""
+
+    def __init__(self, s):
+        self.arrays = [np.ascontiguousarray(x, dtype=np.float32) for x in
+                       (s.centers, s.log_scales, s.rotations, s.opacity_logits, s.sh)]
+        c, ls, r, o, sh = self.arrays
+        self.struct = Gaussians(_ptr(c), _ptr(ls), _ptr(r), _ptr(o), _ptr(sh), s.n,
+                                s.active_sh_degree)
+
+
+class OracleLib:
+    """One oracle implementation (C restatement or the reference build) in one exp mode."""
+
+    def __init__(self, kind: str = "oracle", mode: str = "B"):
+        self.kind, self.mode = kind, mode
+        path = LIBS[(kind, mode)]
+        if not path.exists():
+            build_oracle()
+        self.lib = C.CDLL(str(path))
+        p = kind + "_"
+        self.p = p
+        L = self.lib
+        G, CAM, CFG = C.POINTER(Gaussians), C.POINTER(Camera), C.POINTER(RasterConfig)
+        getattr(L, p + "last_error").restype = C.c_char_p
+        getattr(L, p + "project").argtypes = [G, CAM, CFG, u8p, ip, ip, ip, ip, fp, fp, fp, fp, fp]
+        getattr(L, p + "tiles").argtypes = [G, CAM, CFG, u8p, i64p, ip, ip, C.c_int64]
+        getattr(L, p + "render").argtypes = [G, CAM, CFG, u8p, fp, fp, fp, fp, fp, ip, fp, fp, ip, i64p]
+        getattr(L, p + "render_backward").argtypes = [G, CAM, CFG, fp, u8p, fp, fp, fp, fp, fp, fp, fp, ip]
+        getattr(L, p + "l1_loss").argtypes = [fp, fp, C.c_int64, fp]
+        getattr(L, p + "l1_loss").restype = C.c_float
+        getattr(L, p + "lr_at").argtypes = [C.POINTER(AdamConfig), C.c_int32]
+        getattr(L, p + "lr_at").restype = C.c_double
+        getattr(L, p + "exp").argtypes = [C.c_float]
+        getattr(L, p + "exp").restype = C.c_float
+        for fn in ("project", "tiles", "render", "render_backward"):
+            getattr(L, p + fn).restype = C.c_int
+        if kind == "oracle":
+            getattr(L, p + "adam_step").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp, fp, fp,
+                                          C.POINTER(AdamConfig), ip, C.c_uint32]
+            getattr(L, p + "unproject").argtypes = [CAM, ip, fp, fp, C.c_int, C.c_float, C.c_int64, C.c_int32,
+                                          C.c_int64, fp, ip, C.c_int64, i64p]
+        else:
+            getattr(L, p + "adam_steps").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp,
+                                           C.POINTER(AdamConfig), C.c_int32]
+            getattr(L, p + "depth_reinitialize").argtypes = [G, CAM, CFG, fp, C.c_int32, C.c_uint32, fp, ip]
+            getattr(L, p + "global_importance").argtypes = [G, CAM, C.c_int32, CFG, C.POINTER(C.c_double), ip]
+
+    def fn(self, name):
+        return getattr(self.lib, self.p + name)
+
+    def check(self, rc):
+        if rc != 0:
+            msg = self.fn("last_error")().decode()
+            raise RuntimeError(f"{self.p}: status {rc}: {msg}")
+
+    def exp(self, x: float) -> float:
+        return self.fn("exp")(x)
+
+    # ---- wrappers returning numpy --------------------------------------------------------
+    def project(self, s, cam, cfg=None, mask=None):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        n = s.n
+        out = dict(order=np.zeros(max(n, 1), np.int32), rect=np.zeros((max(n, 1), 4), np.int32),
+                   radius=np.zeros(max(n, 1), np.int32), depth=np.zeros(max(n, 1), np.float32),
+                   mean2d=np.zeros((max(n, 1), 2), np.float32), conic=np.zeros((max(n, 1), 3), np.float32),
+                   color=np.zeros((max(n, 1), 3), np.float32), opacity=np.zeros(max(n, 1), np.float32))
+        ns = C.c_int32(0)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        self.check(self.fn("project")(C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(m, u8p),
+                                      C.byref(ns), _ptr(out["order"], ip), _ptr(out["rect"], ip),
+                                      _ptr(out["radius"], ip), _ptr(out["depth"]), _ptr(out["mean2d"]),
+                                      _ptr(out["conic"]), _ptr(out["color"]), _ptr(out["opacity"])))
+        out = {k: v[:n] for k, v in out.items()}
+        out["order"] = out["order"][: ns.value]
+        out["n_survivors"] = ns.value
+        return out
+
+    def tiles(self, s, cam, cfg=None, mask=None):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        tx = (cam.width + cfg.tile_size - 1) // cfg.tile_size
+        ty = (cam.height + cfg.tile_size - 1) // cfg.tile_size
+        ranges = np.zeros((tx * ty, 2), np.int32)
+        npairs = C.c_int64(0)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        self.check(self.fn("tiles")(C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(m, u8p),
+                                    C.byref(npairs), _ptr(ranges, ip), ip(), 0))
+        gauss = np.zeros(max(npairs.value, 1), np.int32)
+        self.check(self.fn("tiles")(C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(m, u8p),
+                                    C.byref(npairs), _ptr(ranges, ip), _ptr(gauss, ip), npairs.value))
+        return dict(ranges=ranges, gaussian=gauss[: npairs.value], n_pairs=npairs.value,
+                    tiles_x=tx, tiles_y=ty)
+
+    def render(self, s, cam, cfg=None, mask=None, bg=(0.0, 0.0, 0.0), report=True):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        h, w, n = cam.height, cam.width, s.n
+        o = dict(color=np.zeros((h, w, 3), np.float32), alpha=np.zeros((h, w), np.float32),
+                 depth=np.zeros((h, w), np.float32), transmittance=np.zeros((h, w), np.float32),
+                 max_contributor=np.zeros((h, w), np.int32))
+        r = dict(importance=np.zeros(max(n, 1), np.float32), max_weight=np.zeros(max(n, 1), np.float32),
+                 max_pixel_count=np.zeros(max(n, 1), np.int32)) if report else {}
+        stats = np.zeros(2, np.int64)
+        bgv = np.asarray(bg, np.float32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        self.check(self.fn("render")(
+            C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(m, u8p), _ptr(bgv),
+            _ptr(o["color"]), _ptr(o["alpha"]), _ptr(o["depth"]), _ptr(o["transmittance"]),
+            _ptr(o["max_contributor"], ip), _ptr(r.get("importance")), _ptr(r.get("max_weight")),
+            _ptr(r.get("max_pixel_count"), ip), _ptr(stats, i64p)))
+        o.update({k: v[:n] for k, v in r.items()})
+        o["visits"], o["commits"] = int(stats[0]), int(stats[1])
+        return o
+
+    def render_backward(self, s, cam, d_color, cfg=None, mask=None, bg=(0.0, 0.0, 0.0)):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        n = max(s.n, 1)
+        g = dict(d_centers=np.zeros((n, 3), np.float32), d_log_scales=np.zeros((n, 3), np.float32),
+                 d_rotations=np.zeros((n, 4), np.float32), d_opacity_logits=np.zeros(n, np.float32),
+                 d_sh=np.zeros((n, 48), np.float32), grad2d_accum=np.zeros(n, np.float32),
+                 grad2d_count=np.zeros(n, np.int32))
+        dc = np.ascontiguousarray(d_color, np.float32)
+        bgv = np.asarray(bg, np.float32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        self.check(self.fn("render_backward")(
+            C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(dc), _ptr(m, u8p), _ptr(bgv),
+            _ptr(g["d_centers"]), _ptr(g["d_log_scales"]), _ptr(g["d_rotations"]),
+            _ptr(g["d_opacity_logits"]), _ptr(g["d_sh"]), _ptr(g["grad2d_accum"]),
+            _ptr(g["grad2d_count"], ip)))
+        return {k: v[: s.n] for k, v in g.items()}
+
+    def l1_loss(self, a, b, want_grad=True):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        grad = np.zeros_like(a) if want_grad else None
+        loss = self.fn("l1_loss")(_ptr(a), _ptr(b), a.size, _ptr(grad))
+        return float(loss), grad
+
+    def lr_at(self, cfg, step):
+        return self.fn("lr_at")(C.byref(cfg), step)
+
+    def adam_step(self, s, grads, m, v, cfg, step, group_mask=31):
+        """oracle_adam_step in place on copies; returns (set, m, v, step)."""
+        s = s.copy()
+        m = np.ascontiguousarray(m, np.float32).copy()
+        v = np.ascontiguousarray(v, np.float32).copy()
+        st = C.c_int32(step)
+        gr = {k: np.ascontiguousarray(grads[k], np.float32) for k in
+              ("d_centers", "d_log_scales", "d_rotations", "d_opacity_logits", "d_sh")}
+        self.check(self.fn("adam_step")(
+            _ptr(s.centers), _ptr(s.log_scales), _ptr(s.rotations), _ptr(s.opacity_logits), _ptr(s.sh),
+            s.n, _ptr(gr["d_centers"]), _ptr(gr["d_log_scales"]), _ptr(gr["d_rotations"]),
+            _ptr(gr["d_opacity_logits"]), _ptr(gr["d_sh"]), _ptr(m), _ptr(v), C.byref(cfg),
+            C.byref(st), group_mask))
+        return s, m, v, st.value
+
+    def adam_steps(self, s, grads, cfg, steps):
+        """ref_adam_steps: `steps` reference OptimState::step calls from zero moments."""
+        s = s.copy()
+        gr = {k: np.ascontiguousarray(grads[k], np.float32) for k in
+              ("d_centers", "d_log_scales", "d_rotations", "d_opacity_logits", "d_sh")}
+        self.check(self.fn("adam_steps")(
+            _ptr(s.centers), _ptr(s.log_scales), _ptr(s.rotations), _ptr(s.opacity_logits), _ptr(s.sh),
+            s.n, _ptr(gr["d_centers"]), _ptr(gr["d_log_scales"]), _ptr(gr["d_rotations"]),
+            _ptr(gr["d_opacity_logits"]), _ptr(gr["d_sh"]), C.byref(cfg), steps))
+        return s
+
+    def unproject(self, cam, max_contributor, alpha, depth, rule=0, alpha_threshold=0.5,
+                  view_index=0, stride=1, seed=0):
+        hw = cam.width * cam.height
+        pts = np.zeros((hw, 3), np.float32)
+        pix = np.zeros(hw, np.int32)
+        cnt = C.c_int64(0)
+        mc = np.ascontiguousarray(max_contributor, np.int32)
+        al = np.ascontiguousarray(alpha, np.float32)
+        dp = np.ascontiguousarray(depth, np.float32)
+        self.check(self.fn("unproject")(C.byref(cam), _ptr(mc, ip), _ptr(al), _ptr(dp), rule,
+                                        alpha_threshold, view_index, stride, seed, _ptr(pts),
+                                        _ptr(pix, ip), hw, C.byref(cnt)))
+        return pts[: cnt.value], pix[: cnt.value]
+
+    def depth_reinitialize(self, s, cam, image, sample_count, seed=0, cfg=None):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        out = np.zeros((cam.width * cam.height, 3), np.float32)
+        cnt = C.c_int32(0)
+        img = np.ascontiguousarray(image, np.float32)
+        self.check(self.fn("depth_reinitialize")(C.byref(gv.struct), C.byref(cam), C.byref(cfg),
+                                                 _ptr(img), sample_count, seed, _ptr(out), C.byref(cnt)))
+        return out[: cnt.value]
+
+    def global_importance(self, s, cams, cfg=None):
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        arr = (Camera * len(cams))(*cams)
+        acc = np.zeros(s.n, np.float64)
+        cnt = np.zeros(s.n, np.int32)
+        self.check(self.fn("global_importance")(C.byref(gv.struct), arr, len(cams), C.byref(cfg),
+                                                acc.ctypes.data_as(C.POINTER(C.c_double)), _ptr(cnt, ip)))
+        return acc, cnt
