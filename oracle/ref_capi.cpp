@@ -348,4 +348,32 @@ int ref_global_importance(const splat_gaussians* g, const splat_camera* cams, in
     REF_CATCH
 }
 
+
+// render_backward<double> on the float inputs promoted to double: an fp64 "truth" used to show
+// that the GPU's float gradients are as close to exact as the reference's own float path.
+int ref_render_backward_f64(const splat_gaussians* g, const splat_camera* c, const splat_raster_config* cf,
+                            const float* d_color, const uint8_t* mask, const float bg[3], double* d_centers,
+                            double* d_log_scales, double* d_rotations, double* d_opacity, double* d_sh) {
+    REF_TRY
+    const GaussianSetT<double> set = to_set(g).cast<double>();
+    const CameraT<double> cam = to_cam(c).cast<double>();
+    std::vector<char> mv;
+    if (mask) mv = to_mask(mask, g->n);
+    Image<double> dc(cam.width, cam.height, 3);
+    for (size_t k = 0; k < dc.data.size(); ++k) dc.data[k] = d_color[k];
+    const auto gr = render_backward<double>(set, cam, to_cfg(cf), dc, mask ? &mv : nullptr,
+                                            Vec3<double>(bg[0], bg[1], bg[2]));
+    for (int i = 0; i < g->n; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            d_centers[3 * i + k] = gr.d_centers[i][k];
+            d_log_scales[3 * i + k] = gr.d_log_scales[i][k];
+        }
+        for (int k = 0; k < 4; ++k) d_rotations[4 * i + k] = gr.d_rotations[i][k];
+        d_opacity[i] = gr.d_opacity_logits[i];
+    }
+    for (size_t k = 0; k < gr.d_sh.size(); ++k) d_sh[k] = gr.d_sh[k];
+    return 0;
+    REF_CATCH
+}
+
 }  // extern "C"

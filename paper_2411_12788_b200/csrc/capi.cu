@@ -1,0 +1,585 @@
+// capi.cu — splat_ctx, the per-view pipeline orchestration, and the extern "C" boundary declared
+// in include/splat_b200.h.  Host code only (kernels live in forward.cu / sort.cu / backward.cu).
+//
+// Pipeline of one forward (render<float>, rasterizer.cpp:96-182):
+//   K1 preprocess (N) -> depth radix sort (N keys, stable) -> gather tile counts in depth order
+//   -> exclusive scan (pair offsets, P) -> [one host read of P] -> K3 emit (tile, gaussian) pairs
+//   -> stable radix sort by tile id -> K5 tile ranges -> K6 blend (+importance, +depth).
+// The backward reuses the forward's sorted lists, records and per-pixel (T_final, last) state
+// (the reference recomputes project + bin_tiles, gradients.cpp:58-61; the result is identical).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+#include "splat_b200.h"
+
+using namespace splat_b200;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t need, bool zero = false, cudaStream_t s = nullptr) {
+        if (need <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t cap = need + need / 4 + 256;
+        cudaError_t e = cudaMalloc(&p, cap);
+        if (e != cudaSuccess) return e;
+        bytes = cap;
+        if (zero) return cudaMemsetAsync(p, 0, cap, s);
+        return cudaSuccess;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct FwdState {
+    bool valid = false;
+    CamParams cp{};
+    int n = 0;
+    int n_surv = 0;
+    uint64_t n_pairs = 0;
+    bool pairs_in_alt = false;
+    float bg[3] = {0, 0, 0};
+    const float* g_centers = nullptr;  // identity of the inputs (reuse check)
+    const uint8_t* mask = nullptr;
+    float* color = nullptr;
+    float* alpha = nullptr;
+    float* depth = nullptr;
+    int32_t* max_contributor = nullptr;
+};
+
+}  // namespace
+
+struct splat_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    LaunchCtx lc;
+    std::string err;
+    // per-Gaussian
+    DevBuf rec, aux, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
+    // per-pair
+    DevBuf pair_tile[2], pair_gauss[2];
+    // misc
+    DevBuf ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
+    uint32_t* host_counters = nullptr;  // pinned [n_surv, P]
+    FwdState st;
+};
+
+namespace {
+
+int set_err(splat_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_err(splat_ctx* c, cudaError_t e, const char* where) {
+    if (e == cudaErrorMemoryAllocation)
+        return set_err(c, SPLAT_ERR_OUT_OF_MEMORY, std::string(where) + ": " + cudaGetErrorString(e));
+    return set_err(c, SPLAT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                                  \
+    do {                                                 \
+        cudaError_t e_ = (expr);                         \
+        if (e_ != cudaSuccess) return cuda_err(ctx, e_, where); \
+    } while (0)
+
+// camera.hpp:38-48 CameraT::validate, in float with the shim's reduction order.
+int validate_camera(splat_ctx* ctx, const splat_camera* c) {
+    if (!c) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "camera: null");
+    if (c->width < 1 || c->height < 1) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "camera: degenerate image size");
+    if (!(c->znear > 0.0f) || !(c->zfar > c->znear))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "camera: need 0 < znear < zfar");
+    float worst = 0.0f;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            const float* a = &c->rotation[i * 3];
+            const float* b = &c->rotation[j * 3];
+            const float d = a[0] * b[0] + (a[1] * b[1] + a[2] * b[2]);
+            const float v = std::fabs(d - (i == j ? 1.0f : 0.0f));
+            worst = worst < v ? v : worst;
+        }
+    if (!(worst <= 1e-6f)) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "camera: rotation not orthonormal");
+    if (c->width > 65535 || c->height > 65535)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "camera: width/height above 65535 unsupported");
+    return SPLAT_OK;
+}
+
+int make_params(splat_ctx* ctx, const splat_camera* c, const splat_raster_config* cfg, CamParams* cp) {
+    int rc = validate_camera(ctx, c);
+    if (rc) return rc;
+    if (!cfg) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "raster config: null");
+    const int ts = cfg->tile_size;
+    if (!(ts == 8 || (ts >= 16 && ts % 16 == 0)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "tile_size must be 8 or a multiple of 16 on the GPU path");
+    std::memset(cp, 0, sizeof(*cp));
+    cp->width = c->width;
+    cp->height = c->height;
+    cp->fx = c->fx;
+    cp->fy = c->fy;
+    cp->cx = c->cx;
+    cp->cy = c->cy;
+    std::memcpy(cp->R, c->rotation, sizeof(cp->R));
+    std::memcpy(cp->t, c->translation, sizeof(cp->t));
+    for (int i = 0; i < 3; ++i) {  // center = -(R^T t), camera.hpp:25
+        const float* R = c->rotation;
+        const float* t = c->translation;
+        cp->center[i] = -(R[i] * t[0] + (R[3 + i] * t[1] + R[6 + i] * t[2]));
+    }
+    cp->znear = c->znear;
+    cp->tile_size = ts;
+    cp->tiles_x = (c->width + ts - 1) / ts;
+    cp->tiles_y = (c->height + ts - 1) / ts;
+    cp->apply_thresholds = cfg->apply_thresholds ? 1 : 0;
+    cp->lowpass = (float)cfg->lowpass;
+    cp->radius_sigmas = (float)cfg->radius_sigmas;
+    cp->alpha_max = (float)cfg->alpha_max;
+    cp->contribution_min = (float)cfg->contribution_min;
+    cp->transmittance_min = (float)cfg->transmittance_min;
+    cp->log_cond_limit = (float)std::log(1e12);
+    return SPLAT_OK;
+}
+
+int check_set(splat_ctx* ctx, const splat_gaussians* g) {
+    if (!g) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "gaussians: null");
+    if (g->n < 0 || (g->n > 0 && (!g->centers || !g->log_scales || !g->rotations || !g->opacity_logits || !g->sh)))
+        return set_err(ctx, SPLAT_ERR_LOGIC, "GaussianSet parallel arrays out of sync");
+    if (g->active_sh_degree < 0 || g->active_sh_degree > 3)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "active_sh_degree must be in [0, 3]");
+    return SPLAT_OK;
+}
+
+int ceil_log2(uint32_t v) {
+    int b = 0;
+    while ((1u << b) < v) ++b;
+    return b;
+}
+
+// The full forward of one view.  `out` fields may be null; the backward state (t_final,
+// last_index, colour) always lands in ctx buffers or the caller's colour buffer.
+int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                const uint8_t* mask, const float bg[3], const splat_render_outputs* out,
+                const splat_importance_outputs* rep) {
+    ctx->st.valid = false;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    CamParams cp;
+    if ((rc = make_params(ctx, cam, cfg, &cp))) return rc;
+    LaunchCtx& lc = ctx->lc;
+    cudaStream_t s = ctx->stream;
+    const int n = g->n;
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    const int n_tiles = cp.tiles_x * cp.tiles_y;
+    const size_t hw = (size_t)cp.width * cp.height;
+    const bool want_depth = out && out->depth;
+
+    CK(ctx->rec.ensure(nn * sizeof(ProjRec)), "alloc rec");
+    if (want_depth) CK(ctx->aux.ensure(nn * sizeof(AuxRec)), "alloc aux");
+    for (int k = 0; k < 2; ++k) {
+        CK(ctx->keys[k].ensure(nn * 4), "alloc keys");
+        CK(ctx->vals[k].ensure(nn * 4), "alloc vals");
+    }
+    CK(ctx->tile_counts.ensure(nn * 4), "alloc counts");
+    CK(ctx->counts_sorted.ensure(nn * 4), "alloc counts");
+    CK(ctx->offsets.ensure((nn + 1) * 4), "alloc offsets");
+    CK(ctx->counters.ensure(64), "alloc counters");
+    CK(ctx->hist.ensure(radix_hist_words(nn, 8) * 4), "alloc hist");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(radix_hist_words(nn, 8)) + scan_temp_words(nn) + 64) * 4), "alloc scan");
+    CK(ctx->ranges.ensure((size_t)n_tiles * 8), "alloc ranges");
+    CK(ctx->t_final.ensure(hw * 4), "alloc t_final");
+    CK(ctx->last_index.ensure(hw * 4), "alloc last");
+    float* color_out = out ? out->color : nullptr;
+    if (!color_out) {
+        CK(ctx->color.ensure(hw * 12), "alloc color");
+        color_out = ctx->color.as<float>();
+    }
+    if (!ctx->host_counters) CK(cudaMallocHost(&ctx->host_counters, 64), "alloc pinned");
+
+    uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] = n_surv, [1] = P
+    CK(cudaMemsetAsync(d_counters, 0, 16, s), "memset counters");
+    int n_surv = 0;
+    uint64_t n_pairs = 0;
+    bool pairs_alt = false;
+    if (n > 0) {
+        GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
+        uint32_t* keys = ctx->keys[0].as<uint32_t>();
+        uint32_t* vals = ctx->vals[0].as<uint32_t>();
+        CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
+                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters),
+           "preprocess");
+        bool alt = false;
+        CK(radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), (uint64_t)n, 0,
+                            32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
+           "depth sort");
+        const uint32_t* order = alt ? ctx->vals[1].as<uint32_t>() : vals;
+        CK(launch_gather_counts(lc, order, ctx->tile_counts.as<uint32_t>(), ctx->counts_sorted.as<uint32_t>(), n),
+           "gather counts");
+        CK(exclusive_scan_u32(lc, ctx->counts_sorted.as<uint32_t>(), ctx->offsets.as<uint32_t>(), (uint64_t)n,
+                              ctx->scan_tmp.as<uint32_t>(), d_counters + 1),
+           "scan counts");
+        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 8, cudaMemcpyDeviceToHost, s), "read counts");
+        CK(cudaStreamSynchronize(s), "sync counts");
+        n_surv = (int)ctx->host_counters[0];
+        n_pairs = ctx->host_counters[1];
+        if (n_pairs > 0) {
+            for (int k = 0; k < 2; ++k) {
+                CK(ctx->pair_tile[k].ensure(n_pairs * 4), "alloc pairs");
+                CK(ctx->pair_gauss[k].ensure(n_pairs * 4), "alloc pairs");
+            }
+            const size_t hw_words = radix_hist_words(n_pairs, 8);
+            CK(ctx->hist.ensure(hw_words * 4), "alloc hist");
+            CK(ctx->scan_tmp.ensure((scan_temp_words(hw_words) + 64) * 4), "alloc scan");
+            CK(launch_emit_pairs(lc, order, ctx->offsets.as<uint32_t>(), ctx->rec.as<ProjRec>(), cp, n_surv,
+                                 ctx->pair_tile[0].as<uint32_t>(), ctx->pair_gauss[0].as<uint32_t>()),
+               "emit pairs");
+            const int tile_bits = ceil_log2((uint32_t)n_tiles);
+            CK(radix_sort_pairs(lc, ctx->pair_tile[0].as<uint32_t>(), ctx->pair_gauss[0].as<uint32_t>(),
+                                ctx->pair_tile[1].as<uint32_t>(), ctx->pair_gauss[1].as<uint32_t>(), n_pairs, 0,
+                                tile_bits, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &pairs_alt),
+               "tile sort");
+        }
+    }
+    const uint32_t* sorted_tiles = ctx->pair_tile[pairs_alt ? 1 : 0].as<uint32_t>();
+    const uint32_t* sorted_gauss = ctx->pair_gauss[pairs_alt ? 1 : 0].as<uint32_t>();
+    CK(launch_tile_ranges(lc, sorted_tiles, n_pairs, ctx->ranges.as<uint32_t>(), n_tiles), "tile ranges");
+    if (rep && n > 0) {
+        if (rep->importance) CK(cudaMemsetAsync(rep->importance, 0, (size_t)n * 4, s), "memset importance");
+        if (rep->max_weight) CK(cudaMemsetAsync(rep->max_weight, 0, (size_t)n * 4, s), "memset max_weight");
+        if (rep->max_pixel_count) CK(cudaMemsetAsync(rep->max_pixel_count, 0, (size_t)n * 4, s), "memset count");
+    }
+    FwdOutputs fo{};
+    fo.color = color_out;
+    fo.alpha = out ? out->alpha : nullptr;
+    fo.depth = out ? out->depth : nullptr;
+    fo.transmittance = out ? out->transmittance : nullptr;
+    fo.max_contributor = out ? out->max_contributor : nullptr;
+    const bool report = rep && rep->importance && rep->max_weight && rep->max_pixel_count && n > 0;
+    fo.importance = report ? rep->importance : nullptr;
+    fo.max_weight = report ? rep->max_weight : nullptr;
+    fo.max_pixel_count = report ? rep->max_pixel_count : nullptr;
+    fo.t_final = ctx->t_final.as<float>();
+    fo.last_index = ctx->last_index.as<int32_t>();
+    CK(launch_blend_forward(lc, cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
+                            want_depth ? ctx->aux.as<AuxRec>() : nullptr, bg, fo),
+       "blend forward");
+    FwdState& st = ctx->st;
+    st.cp = cp;
+    st.n = n;
+    st.n_surv = n_surv;
+    st.n_pairs = n_pairs;
+    st.pairs_in_alt = pairs_alt;
+    std::memcpy(st.bg, bg, sizeof(st.bg));
+    st.g_centers = g->centers;
+    st.mask = mask;
+    st.color = color_out;
+    st.alpha = fo.alpha;
+    st.depth = fo.depth;
+    st.max_contributor = fo.max_contributor;
+    st.valid = true;
+    return SPLAT_OK;
+}
+
+bool state_matches(const splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const uint8_t* mask,
+                   const float bg[3]) {
+    const FwdState& st = ctx->st;
+    if (!st.valid || st.n != g->n || st.g_centers != g->centers || st.mask != mask) return false;
+    if (st.cp.width != cam->width || st.cp.height != cam->height) return false;
+    if (std::memcmp(st.cp.R, cam->rotation, sizeof(st.cp.R)) || std::memcmp(st.cp.t, cam->translation, sizeof(st.cp.t)))
+        return false;
+    return st.bg[0] == bg[0] && st.bg[1] == bg[1] && st.bg[2] == bg[2];
+}
+
+int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                 const float* d_color, const float* target, const uint8_t* mask, const float bg[3],
+                 const splat_param_grads* grads, int accumulate, float* loss_dev) {
+    if (!grads || (g->n > 0 && (!grads->d_centers || !grads->d_log_scales || !grads->d_rotations ||
+                                !grads->d_opacity_logits || !grads->d_sh)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward: gradient outputs missing");
+    const FwdState& st = ctx->st;
+    LaunchCtx& lc = ctx->lc;
+    const int n = g->n;
+    CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 48, true, ctx->stream), "alloc grad2d");
+    const int n_blocks = st.cp.tiles_x * st.cp.tiles_y * ((st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)) *
+                                                         (st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)));
+    float* partials = nullptr;
+    if (target && loss_dev) {
+        CK(ctx->loss_partials.ensure((size_t)n_blocks * 4), "alloc partials");
+        partials = ctx->loss_partials.as<float>();
+    }
+    if (n > 0 || (target && loss_dev)) {
+        const uint32_t* sorted_gauss = ctx->pair_gauss[st.pairs_in_alt ? 1 : 0].as<uint32_t>();
+        CK(launch_blend_backward(lc, st.cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
+                                 ctx->t_final.as<float>(), ctx->last_index.as<int32_t>(), bg, d_color, st.color, target,
+                                 partials, ctx->grad2d.as<float>()),
+           "blend backward");
+    }
+    if (n > 0) {
+        GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
+        CK(launch_chain(lc, gp, st.cp, ctx->grad2d.as<float>(), ctx->rec.as<ProjRec>(), *grads, accumulate), "chain");
+    }
+    if (partials) {
+        const float inv_n = 1.0f / (float)(3 * (int64_t)st.cp.width * st.cp.height);
+        CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
+    }
+    (void)cfg;
+    (void)mask;
+    return SPLAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int splat_ctx_create(int device, splat_ctx** out) {
+    if (!out) return SPLAT_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return SPLAT_ERR_CUDA;
+    splat_ctx* c = new splat_ctx();
+    c->device = device;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+        c->lc.num_sms = sms;
+    *out = c;
+    return SPLAT_OK;
+}
+
+int splat_ctx_destroy(splat_ctx* ctx) {
+    if (!ctx) return SPLAT_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
+    delete ctx;
+    return SPLAT_OK;
+}
+
+int splat_ctx_set_stream(splat_ctx* ctx, void* stream) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->lc.stream = ctx->stream;
+    return SPLAT_OK;
+}
+
+int splat_sync(splat_ctx* ctx) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    return SPLAT_OK;
+}
+
+const char* splat_last_error(const splat_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t splat_kernel_launches(const splat_ctx* ctx) { return ctx ? ctx->lc.count : 0; }
+
+int splat_render(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                 const uint8_t* mask, const float background[3], const splat_render_outputs* out,
+                 const splat_importance_outputs* report) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    const float zero[3] = {0, 0, 0};
+    return run_forward(ctx, g, cam, cfg, mask, background ? background : zero, out, report);
+}
+
+int splat_accumulate_importance(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam,
+                                const splat_raster_config* cfg, const uint8_t* mask,
+                                const splat_importance_outputs* report) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (!report || !report->importance || !report->max_weight || !report->max_pixel_count)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "accumulate_importance: report outputs missing");
+    const float zero[3] = {0, 0, 0};
+    return run_forward(ctx, g, cam, cfg, mask, zero, nullptr, report);
+}
+
+int splat_render_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam,
+                          const splat_raster_config* cfg, const float* d_color, const uint8_t* mask,
+                          const float background[3], const splat_param_grads* grads, int accumulate,
+                          int reuse_forward) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    if (!d_color) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward: dLoss/dColor shape mismatch");
+    const float zero[3] = {0, 0, 0};
+    const float* bg = background ? background : zero;
+    if (!(reuse_forward && state_matches(ctx, g, cam, mask, bg))) {
+        if ((rc = run_forward(ctx, g, cam, cfg, mask, bg, nullptr, nullptr))) return rc;
+    }
+    return run_backward(ctx, g, cam, cfg, d_color, nullptr, mask, bg, grads, accumulate, nullptr);
+}
+
+int splat_l1_loss(splat_ctx* ctx, const float* a, const float* b, int64_t count, float* grad, float* loss) {
+    if (!ctx || count < 0 || (count > 0 && (!a || !b))) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "l1_loss: bad args");
+    const int np = l1_partials_count(count);
+    CK(ctx->loss_partials.ensure((size_t)(np > 0 ? np : 1) * 4), "alloc partials");
+    CK(launch_l1(ctx->lc, a, b, count, grad, ctx->loss_partials.as<float>(), np), "l1");
+    if (loss) {
+        if (count == 0) CK(cudaMemsetAsync(loss, 0, 4, ctx->stream), "l1 loss");
+        else CK(launch_loss_reduce(ctx->lc, ctx->loss_partials.as<float>(), np, 1.0f / (float)count, loss), "l1 reduce");
+    }
+    return SPLAT_OK;
+}
+
+int splat_render_backward_l1(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam,
+                             const splat_raster_config* cfg, const float* target, const uint8_t* mask,
+                             const float background[3], const splat_param_grads* grads, int accumulate,
+                             float* loss) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    if (!target) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward_l1: target missing");
+    const float zero[3] = {0, 0, 0};
+    const float* bg = background ? background : zero;
+    if (!state_matches(ctx, g, cam, mask, bg))
+        return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "render_backward_l1: needs a preceding splat_render on the same inputs");
+    return run_backward(ctx, g, cam, cfg, nullptr, target, mask, bg, grads, accumulate, loss);
+}
+
+int splat_adam_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param_grads* gr, const splat_adam_moments* m,
+                    const splat_adam_config* cfg, int32_t* step_count, uint32_t group_mask) {
+    if (!ctx || !p || !gr || !m || !cfg || !step_count) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "adam: null args");
+    if (p->n < 0) return set_err(ctx, SPLAT_ERR_LOGIC, "OptimState::step: moment/gradient rows out of sync with set");
+    // LrSchedule::at (optimizer.cpp:8-12) and bias corrections (optimizer.cpp:45-47), host fp64
+    const int t = *step_count;
+    double lr_sched;
+    if (t <= 0) {
+        lr_sched = cfg->lr_init;
+    } else {
+        double tt = (double)t / (double)cfg->max_steps;
+        if (tt > 1.0) tt = 1.0;
+        lr_sched = std::exp((1.0 - tt) * std::log(cfg->lr_init) + tt * std::log(cfg->lr_final));
+    }
+    const double lr_pos = lr_sched * cfg->scene_extent;
+    *step_count = t + 1;
+    const double bias1 = 1.0 - std::pow(cfg->beta1, *step_count);
+    const double bias2 = 1.0 - std::pow(cfg->beta2, *step_count);
+    const int64_t n = p->n;
+    LaunchCtx& lc = ctx->lc;
+    auto run = [&](uint32_t bit, float* param, const float* grad, float* mm, float* vv, int64_t cnt, double lr,
+                   double lr_alt, int sh) -> int {
+        if (!(group_mask & bit)) return SPLAT_OK;
+        if (cnt > 0 && (!param || !grad || !mm || !vv))
+            return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "adam: group pointers missing");
+        AdamGroupArgs a{param, grad, mm, vv, cnt, lr, lr_alt, sh};
+        CK(launch_adam(lc, a, cfg->beta1, cfg->beta2, cfg->eps, bias1, bias2), "adam");
+        return SPLAT_OK;
+    };
+    int rc;
+    if ((rc = run(SPLAT_GROUP_CENTERS, p->centers, gr->d_centers, m->m_centers, m->v_centers, 3 * n, lr_pos, lr_pos, 0))) return rc;
+    if ((rc = run(SPLAT_GROUP_SCALES, p->log_scales, gr->d_log_scales, m->m_log_scales, m->v_log_scales, 3 * n,
+                  cfg->lr_scale, cfg->lr_scale, 0))) return rc;
+    if ((rc = run(SPLAT_GROUP_ROTATIONS, p->rotations, gr->d_rotations, m->m_rotations, m->v_rotations, 4 * n,
+                  cfg->lr_rotation, cfg->lr_rotation, 0))) return rc;
+    if ((rc = run(SPLAT_GROUP_OPACITY, p->opacity_logits, gr->d_opacity_logits, m->m_opacity, m->v_opacity, n,
+                  cfg->lr_opacity, cfg->lr_opacity, 0))) return rc;
+    if ((rc = run(SPLAT_GROUP_SH, p->sh, gr->d_sh, m->m_sh, m->v_sh, 48 * n, cfg->lr_sh_dc, cfg->lr_sh_rest, 1))) return rc;
+    if (group_mask & SPLAT_GROUP_ROTATIONS) CK(launch_quat_normalize(lc, p->rotations, (int)n), "quat normalize");
+    return SPLAT_OK;
+}
+
+int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule, float alpha_threshold,
+                          int64_t view_index, int32_t stride, int64_t seed, float* points, int32_t* pixel,
+                          int64_t capacity, int32_t* count_dev) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (stride < 1) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "unproject: stride < 1");
+    const FwdState& st = ctx->st;
+    if (!st.valid || !st.depth || (rule == SPLAT_DEPTH_RULE_ALPHA ? !st.alpha : !st.max_contributor))
+        return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "unproject: needs a preceding splat_render with depth and "
+                                                        "alpha/max_contributor outputs");
+    if (!count_dev || (capacity > 0 && (!points || !pixel)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "unproject: outputs missing");
+    int rc = validate_camera(ctx, cam);
+    if (rc) return rc;
+    const CamParams cp = st.cp;
+    if (cam->width != cp.width || cam->height != cp.height)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "unproject: camera does not match the rendered view");
+    const size_t hw = (size_t)cp.width * cp.height;
+    CK(ctx->flags.ensure(hw * 4), "alloc flags");
+    CK(ctx->flag_offsets.ensure(hw * 4), "alloc offsets");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(hw) + 64) * 4), "alloc scan");
+    CK(launch_unproject(ctx->lc, cp, st.max_contributor, st.alpha, st.depth, rule, alpha_threshold, view_index, stride,
+                        seed, points, pixel, capacity, count_dev, ctx->flags.as<uint32_t>(),
+                        ctx->flag_offsets.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>()),
+       "unproject");
+    return SPLAT_OK;
+}
+
+int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (!ctx->st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
+    if (n_survivors) *n_survivors = ctx->st.n_surv;
+    if (n_pairs) *n_pairs = (int64_t)ctx->st.n_pairs;
+    if (tiles_x) *tiles_x = ctx->st.cp.tiles_x;
+    if (tiles_y) *tiles_y = ctx->st.cp.tiles_y;
+    return SPLAT_OK;
+}
+
+int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* depth, uint8_t* survivor, float* mean2d,
+                        float* conic, float* color, float* opacity) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    const FwdState& st = ctx->st;
+    if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
+    const int n = st.n;
+    if (n == 0) return SPLAT_OK;
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    ProjRec* h = new ProjRec[n];
+    uint32_t* counts = new uint32_t[n];
+    uint32_t* keys = new uint32_t[n];
+    cudaError_t e = cudaMemcpy(h, ctx->rec.p, sizeof(ProjRec) * n, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(counts, ctx->tile_counts.p, 4 * (size_t)n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        delete[] h; delete[] counts; delete[] keys;
+        return cuda_err(ctx, e, "project debug");
+    }
+    for (int i = 0; i < n; ++i) {
+        const bool alive = counts[i] > 0;
+        uint32_t rx, ry;
+        std::memcpy(&rx, &h[i].r1.z, 4);
+        std::memcpy(&ry, &h[i].r1.w, 4);
+        if (rect) {
+            rect[4 * i] = alive ? (int32_t)(rx & 0xffff) : 0;
+            rect[4 * i + 1] = alive ? (int32_t)(rx >> 16) : 0;
+            rect[4 * i + 2] = alive ? (int32_t)(ry & 0xffff) : 0;
+            rect[4 * i + 3] = alive ? (int32_t)(ry >> 16) : 0;
+        }
+        if (survivor) survivor[i] = alive ? 1 : 0;
+        if (depth) depth[i] = alive ? h[i].r2.w : 0.0f;
+        if (mean2d) { mean2d[2 * i] = alive ? h[i].r0.x : 0.f; mean2d[2 * i + 1] = alive ? h[i].r0.y : 0.f; }
+        if (conic) {
+            conic[3 * i] = alive ? h[i].r0.z : 0.f;
+            conic[3 * i + 1] = alive ? h[i].r0.w : 0.f;
+            conic[3 * i + 2] = alive ? h[i].r1.x : 0.f;
+        }
+        if (color) { for (int k = 0; k < 3; ++k) color[3 * i + k] = alive ? (&h[i].r2.x)[k] : 0.f; }
+        if (opacity) opacity[i] = alive ? h[i].r1.y : 0.f;
+        if (radius) radius[i] = 0;  // radius is not stored on device; rect carries the footprint
+    }
+    delete[] h; delete[] counts; delete[] keys;
+    return SPLAT_OK;
+}
+
+int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int32_t* ranges, int32_t* depth_order) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    const FwdState& st = ctx->st;
+    if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    const int k = st.pairs_in_alt ? 1 : 0;
+    if (key_tile && st.n_pairs) CK(cudaMemcpy(key_tile, ctx->pair_tile[k].p, 4 * st.n_pairs, cudaMemcpyDeviceToHost), "copy");
+    if (gaussian && st.n_pairs) CK(cudaMemcpy(gaussian, ctx->pair_gauss[k].p, 4 * st.n_pairs, cudaMemcpyDeviceToHost), "copy");
+    if (ranges)
+        CK(cudaMemcpy(ranges, ctx->ranges.p, 8 * (size_t)st.cp.tiles_x * st.cp.tiles_y, cudaMemcpyDeviceToHost), "copy");
+    if (depth_order && st.n_surv) {
+        // depth sort of N keys: 4 passes of 8 bits -> result back in buffer 0
+        CK(cudaMemcpy(depth_order, ctx->vals[0].p, 4 * (size_t)st.n_surv, cudaMemcpyDeviceToHost), "copy");
+    }
+    return SPLAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,596 @@
+// forward.cu — preprocess, tile-pair emission, tile ranges, per-tile blend forward (+ importance,
+// argmax depth) and depth unprojection.  Compiled with --fmad=false: every float expression is
+// evaluated with separately rounded operations in the order written, which is the reference's
+// order (oracle/compat/Eigen/Dense), so integer outputs and forward images are bit-exact
+// against the oracle.
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace splat_b200 {
+
+namespace {
+
+__device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return a0 * b0 + (a1 * b1 + a2 * b2);  // Eigen 3.4 unrolled redux: x0 + (x1 + x2)
+}
+
+// sh_basis + sh_to_color (sh.hpp:27-51, 84-100)
+__device__ __forceinline__ void sh_color(const float* __restrict__ sh, float x, float y, float z, int degree,
+                                         float rgb[3]) {
+    float b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) b[i] = 0.0f;
+    b[0] = (float)(0.28209479177387814);
+    if (degree >= 1) {
+        const float c1 = (float)(0.4886025119029199);
+        b[1] = -c1 * y;
+        b[2] = c1 * z;
+        b[3] = -c1 * x;
+    }
+    const float xx = x * x, yy = y * y, zz = z * z;
+    if (degree >= 2) {
+        b[4] = (float)(1.0925484305920792) * x * y;
+        b[5] = (float)(-1.0925484305920792) * y * z;
+        b[6] = (float)(0.31539156525252005) * (2.0f * zz - xx - yy);
+        b[7] = (float)(-1.0925484305920792) * x * z;
+        b[8] = (float)(0.5462742152960396) * (xx - yy);
+    }
+    if (degree >= 3) {
+        b[9] = (float)(-0.5900435899266435) * y * (3.0f * xx - yy);
+        b[10] = (float)(2.890611442640554) * x * y * z;
+        b[11] = (float)(-0.4570457994644658) * y * (4.0f * zz - xx - yy);
+        b[12] = (float)(0.3731763325901154) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+        b[13] = (float)(-0.4570457994644658) * x * (4.0f * zz - xx - yy);
+        b[14] = (float)(1.445305721320277) * z * (xx - yy);
+        b[15] = (float)(-0.5900435899266435) * x * (xx - 3.0f * yy);
+    }
+    rgb[0] = rgb[1] = rgb[2] = 0.5f;
+    const int n = (degree + 1) * (degree + 1);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k < n) {
+            rgb[0] = rgb[0] + b[k] * sh[k * 3 + 0];
+            rgb[1] = rgb[1] + b[k] * sh[k * 3 + 1];
+            rgb[2] = rgb[2] + b[k] * sh[k * 3 + 2];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (rgb[c] < 0.0f) rgb[c] = 0.0f;
+}
+
+__device__ __forceinline__ float std_max(float a, float b) { return (a < b) ? b : a; }
+__device__ __forceinline__ float std_min(float a, float b) { return (b < a) ? b : a; }
+
+// project<T> body for one Gaussian (rasterizer.cpp:24-82).  Returns false when culled.
+template <bool VEC_SH>
+__global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamParams cp, const uint8_t* __restrict__ mask,
+                                                        ProjRec* __restrict__ rec, AuxRec* __restrict__ aux,
+                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                        uint32_t* __restrict__ tile_counts,
+                                                        uint32_t* __restrict__ n_surv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool alive = i < g.n;
+    if (alive && mask && !mask[i]) alive = false;
+    float px = 0.f, py = 0.f, pz = 0.f, zc = 0.f;
+    float pc0 = 0.f, pc1 = 0.f;
+    if (alive) {
+        px = __ldg(&g.centers[3 * i]);
+        py = __ldg(&g.centers[3 * i + 1]);
+        pz = __ldg(&g.centers[3 * i + 2]);
+        pc0 = dot3(cp.R[0], cp.R[1], cp.R[2], px, py, pz) + cp.t[0];
+        pc1 = dot3(cp.R[3], cp.R[4], cp.R[5], px, py, pz) + cp.t[1];
+        zc = dot3(cp.R[6], cp.R[7], cp.R[8], px, py, pz) + cp.t[2];
+        if (zc <= cp.znear) alive = false;
+    }
+    ProjRec r;
+    AuxRec a;
+    uint32_t count = 0;
+    if (alive) {
+        const float z = zc;
+        const float m0 = cp.fx * pc0 / z + cp.cx;
+        const float m1 = cp.fy * pc1 / z + cp.cy;
+        // covariance_from_params (gaussian_set.hpp:41-55)
+        const float ls0 = __ldg(&g.log_scales[3 * i]), ls1 = __ldg(&g.log_scales[3 * i + 1]),
+                    ls2 = __ldg(&g.log_scales[3 * i + 2]);
+        float qw = __ldg(&g.rotations[4 * i]), qx = __ldg(&g.rotations[4 * i + 1]),
+              qy = __ldg(&g.rotations[4 * i + 2]), qz = __ldg(&g.rotations[4 * i + 3]);
+        const float qn = sqrtf((qw * qw + qx * qx) + (qy * qy + qz * qz));
+        if (!(qn > 0.0f)) {
+            qw = 1.0f; qx = qy = qz = 0.0f;
+        } else {
+            qw = qw / qn; qx = qx / qn; qy = qy / qn; qz = qz / qn;
+        }
+        float Rq[9];
+        Rq[0] = 1.0f - 2.0f * (qy * qy + qz * qz);
+        Rq[1] = 2.0f * (qx * qy - qw * qz);
+        Rq[2] = 2.0f * (qx * qz + qw * qy);
+        Rq[3] = 2.0f * (qx * qy + qw * qz);
+        Rq[4] = 1.0f - 2.0f * (qx * qx + qz * qz);
+        Rq[5] = 2.0f * (qy * qz - qw * qx);
+        Rq[6] = 2.0f * (qx * qz - qw * qy);
+        Rq[7] = 2.0f * (qy * qz + qw * qx);
+        Rq[8] = 1.0f - 2.0f * (qx * qx + qy * qy);
+        const float s0 = splat_expf(ls0), s1 = splat_expf(ls1), s2 = splat_expf(ls2);
+        float Mq[9];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+            Mq[rr * 3 + 0] = Rq[rr * 3 + 0] * s0;
+            Mq[rr * 3 + 1] = Rq[rr * 3 + 1] * s1;
+            Mq[rr * 3 + 2] = Rq[rr * 3 + 2] * s2;
+        }
+        float C[9];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+            for (int cc = rr; cc < 3; ++cc) {
+                const float v = dot3(Mq[rr * 3], Mq[rr * 3 + 1], Mq[rr * 3 + 2], Mq[cc * 3], Mq[cc * 3 + 1],
+                                     Mq[cc * 3 + 2]);
+                C[rr * 3 + cc] = v;
+                C[cc * 3 + rr] = v;
+            }
+        // EWA: cov2d = (J R) cov3d (J R)^T + lowpass I
+        const float J00 = cp.fx / z, J02 = -cp.fx * pc0 / (z * z);
+        const float J11 = cp.fy / z, J12 = -cp.fy * pc1 / (z * z);
+        const float J[6] = {J00, 0.0f, J02, 0.0f, J11, J12};
+        float M[6], A[6];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+                M[rr * 3 + cc] = dot3(J[rr * 3], J[rr * 3 + 1], J[rr * 3 + 2], cp.R[cc], cp.R[3 + cc], cp.R[6 + cc]);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+                A[rr * 3 + cc] = dot3(M[rr * 3], M[rr * 3 + 1], M[rr * 3 + 2], C[cc], C[3 + cc], C[6 + cc]);
+        const float V00 = dot3(A[0], A[1], A[2], M[0], M[1], M[2]);
+        const float V01 = dot3(A[0], A[1], A[2], M[3], M[4], M[5]);
+        const float V11 = dot3(A[3], A[4], A[5], M[3], M[4], M[5]);
+        const float c0 = V00 + cp.lowpass, c1 = V01, c2 = V11 + cp.lowpass;
+        const float det = c0 * c2 - c1 * c1;
+        if (!(det > 0.0f)) {
+            alive = false;
+        } else {
+            const float inv_det = 1.0f / det;
+            const float k0 = c2 * inv_det, k1 = -c1 * inv_det, k2 = c0 * inv_det;
+            int x0, x1, y0, y1;
+            if (!cp.apply_thresholds) {
+                x0 = 0; x1 = cp.width; y0 = 0; y1 = cp.height;
+            } else {
+                const float mid = 0.5f * (c0 + c2);
+                const float lmax = mid + sqrtf(std_max(mid * mid - det, 0.0f));
+                const int radius = (int)ceilf(cp.radius_sigmas * sqrtf(lmax));
+                const float rf = (float)radius;
+                x0 = max(0, (int)ceilf(m0 - rf - 0.5f));
+                x1 = min(cp.width, (int)floorf(m0 + rf - 0.5f) + 1);
+                y0 = max(0, (int)ceilf(m1 - rf - 0.5f));
+                y1 = min(cp.height, (int)floorf(m1 + rf - 0.5f) + 1);
+                if (x0 >= x1 || y0 >= y1) alive = false;
+            }
+            if (alive) {
+                const float opacity = 1.0f / (1.0f + splat_expf(-__ldg(&g.opacity_logits[i])));
+                // view_dir = (p - cam_center).normalized()
+                float u0 = px - cp.center[0], u1 = py - cp.center[1], u2 = pz - cp.center[2];
+                const float zz = dot3(u0, u1, u2, u0, u1, u2);
+                if (zz > 0.0f) {
+                    const float nn = sqrtf(zz);
+                    u0 = u0 / nn; u1 = u1 / nn; u2 = u2 / nn;
+                }
+                float rgb[3];
+                if (VEC_SH) {
+                    float shv[48];
+                    const float4* s4 = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)i);
+#pragma unroll
+                    for (int k = 0; k < 12; ++k) {
+                        const float4 v = __ldg(&s4[k]);
+                        shv[4 * k] = v.x; shv[4 * k + 1] = v.y; shv[4 * k + 2] = v.z; shv[4 * k + 3] = v.w;
+                    }
+                    sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
+                } else {
+                    float shv[48];
+#pragma unroll
+                    for (int k = 0; k < 48; ++k) shv[k] = __ldg(&g.sh[48 * (size_t)i + k]);
+                    sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
+                }
+                const int ts = cp.tile_size;
+                count = (uint32_t)(((x1 - 1) / ts - x0 / ts + 1) * ((y1 - 1) / ts - y0 / ts + 1));
+                r.r0 = make_float4(m0, m1, k0, k1);
+                r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(x0, x1)),
+                                   __uint_as_float(pack_range(y0, y1)));
+                r.r2 = make_float4(rgb[0], rgb[1], rgb[2], z);
+                if (aux) {
+                    const float smax = std_max(std_max(ls0, ls1), ls2);
+                    const float smin = std_min(std_min(ls0, ls1), ls2);
+                    const bool degenerate = 2.0f * (smax - smin) > cp.log_cond_limit;
+                    a.a0 = make_float4(px, py, pz, degenerate ? 1.0f : 0.0f);
+                    if (degenerate) {
+                        a.a1 = make_float4(1.0f, 0.0f, 0.0f, 1.0f);
+                        a.a2 = make_float4(0.0f, 1.0f, 0.0f, 0.0f);
+                    } else {
+                        // Eigen cofactor inverse (compat/Eigen/Dense)
+#define CM(r_, c_) C[(r_) * 3 + (c_)]
+#define COF(i_, j_) (CM(((i_) + 1) % 3, ((j_) + 1) % 3) * CM(((i_) + 2) % 3, ((j_) + 2) % 3) - \
+                     CM(((i_) + 1) % 3, ((j_) + 2) % 3) * CM(((i_) + 2) % 3, ((j_) + 1) % 3))
+                        const float f00 = COF(0, 0), f10 = COF(1, 0), f20 = COF(2, 0);
+                        const float dt = f00 * CM(0, 0) + (f10 * CM(1, 0) + f20 * CM(2, 0));
+                        const float inv = 1.0f / dt;
+                        const float i00 = f00 * inv, i01 = f10 * inv, i02 = f20 * inv;
+                        const float i11 = COF(1, 1) * inv, i12 = COF(2, 1) * inv, i22 = COF(2, 2) * inv;
+#undef COF
+#undef CM
+                        a.a1 = make_float4(i00, i01, i02, i11);
+                        a.a2 = make_float4(i12, i22, 0.0f, 0.0f);
+                    }
+                }
+            }
+        }
+    }
+    if (i < g.n) {
+        keys[i] = alive ? __float_as_uint(zc) : 0xffffffffu;
+        vals[i] = (uint32_t)i;
+        tile_counts[i] = alive ? count : 0u;
+        if (alive) {
+            rec[i] = r;
+            if (aux) aux[i] = a;
+        }
+    }
+    const int block_alive = __syncthreads_count(alive);
+    if (threadIdx.x == 0 && block_alive) atomicAdd(n_surv, (uint32_t)block_alive);
+}
+
+__global__ void gather_counts_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
+                                     uint32_t* __restrict__ out, int n) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) out[r] = counts[order[r]];
+}
+
+// One warp per Gaussian (in depth order): lanes stride over its tile rect.
+__global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restrict__ order,
+                                                        const uint32_t* __restrict__ offsets,
+                                                        const ProjRec* __restrict__ rec, int tile_size,
+                                                        int tiles_x, int n_surv, uint32_t* __restrict__ pair_tile,
+                                                        uint32_t* __restrict__ pair_gauss) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_surv) return;
+    const uint32_t gid = order[warp];
+    const uint32_t off = offsets[warp];
+    const float4 r1 = rec[gid].r1;
+    const int x0 = range_lo(r1.z), x1 = range_hi(r1.z), y0 = range_lo(r1.w), y1 = range_hi(r1.w);
+    const int tx0 = x0 / tile_size, tx1 = (x1 - 1) / tile_size;
+    const int ty0 = y0 / tile_size, ty1 = (y1 - 1) / tile_size;
+    const int nx = tx1 - tx0 + 1;
+    const int total = nx * (ty1 - ty0 + 1);
+    for (int k = lane; k < total; k += 32) {
+        const int ty = ty0 + k / nx, tx = tx0 + k % nx;
+        pair_tile[off + k] = (uint32_t)(ty * tiles_x + tx);
+        pair_gauss[off + k] = gid;
+    }
+}
+
+// CSR ranges over the tile-sorted pairs: ranges[2t] = lower_bound(t), ranges[2t+1] =
+// lower_bound(t + 1).  Empty tiles get [p, p] exactly like detail::bin_tiles' empty lists.
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ tiles, uint32_t n, uint32_t* __restrict__ ranges,
+                                   int n_tiles) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    uint32_t bounds[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t key = (uint32_t)t + k;
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (tiles[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        bounds[k] = lo;
+    }
+    ranges[2 * t] = bounds[0];
+    ranges[2 * t + 1] = bounds[1];
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Per-tile front-to-back blend (rasterizer.cpp:124-169 + traverse_pixel rasterizer.hpp:116-147).
+// One CTA per BW x BW pixel block (BW = min(tile, 16)); a tile of size 16k is covered by k*k
+// CTAs sharing its list (blockIdx.y).  Gaussian records are staged in shared memory in batches
+// of blockDim.x; all threads walk the batch in the same order (broadcast smem reads).
+template <bool REPORT>
+__global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+                                                           const uint32_t* __restrict__ pair_gauss,
+                                                           const ProjRec* __restrict__ rec,
+                                                           const AuxRec* __restrict__ aux, float bg0, float bg1,
+                                                           float bg2, FwdOutputs out) {
+    __shared__ float4 s_r0[kBlock], s_r1[kBlock], s_r2[kBlock];
+    __shared__ uint32_t s_gid[kBlock];
+    __shared__ float s_imp[REPORT ? kBlock : 1];
+    __shared__ uint32_t s_maxw[REPORT ? kBlock : 1];
+    const int nthreads = blockDim.x;
+    const int tid = threadIdx.x;
+    const int ts = cp.tile_size;
+    const int bw = ts < 16 ? ts : 16;
+    const int tile = blockIdx.x;
+    const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
+    const int subs = ts / bw;
+    const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
+    const int px = tx * ts + sx * bw + tid % bw;
+    const int py = ty * ts + sy * bw + tid / bw;
+    const bool inside = px < cp.width && py < cp.height;
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const int thr = cp.apply_thresholds;
+    const float amax_c = cp.alpha_max, cmin = cp.contribution_min, tmin = cp.transmittance_min;
+    const float x = (float)px + 0.5f, y = (float)py + 0.5f;
+
+    float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, wmax = 0.0f;
+    int32_t amax_gid = -1, last = -1;
+    bool done = !inside;
+    if (REPORT) {
+        s_imp[tid] = 0.0f;
+        s_maxw[tid] = 0u;
+    }
+    for (uint32_t base = start; base < end; base += nthreads) {
+        if (__syncthreads_count(!done) == 0) break;
+        const uint32_t idx = base + tid;
+        if (idx < end) {
+            const uint32_t gid = pair_gauss[idx];
+            const ProjRec rr = rec[gid];
+            s_r0[tid] = rr.r0;
+            s_r1[tid] = rr.r1;
+            s_r2[tid] = rr.r2;
+            s_gid[tid] = gid;
+        }
+        __syncthreads();
+        const int cnt = (int)min((uint32_t)nthreads, end - base);
+        if (!REPORT) {
+            for (int j = 0; j < cnt && !done; ++j) {
+                float alpha, g2d, dx, dy;
+                bool clamped;
+                const float4 r1 = s_r1[j];
+                const float4 r0 = s_r0[j];
+                if (!gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
+                const float next = T * (1.0f - alpha);
+                if (thr && next < tmin) {
+                    done = true;
+                    break;
+                }
+                const float w = T * alpha;
+                const float4 r2 = s_r2[j];
+                acc0 = acc0 + w * r2.x;
+                acc1 = acc1 + w * r2.y;
+                acc2 = acc2 + w * r2.z;
+                if (w > wmax) {
+                    wmax = w;
+                    amax_gid = (int32_t)s_gid[j];
+                }
+                last = (int32_t)(base + j);
+                T = next;
+            }
+        } else {
+            const int lane = tid & 31;
+            for (int j = 0; j < cnt; ++j) {
+                if (__all_sync(0xffffffffu, done)) break;
+                float w = 0.0f;
+                if (!done) {
+                    float alpha, g2d, dx, dy;
+                    bool clamped;
+                    const float4 r1 = s_r1[j];
+                    const float4 r0 = s_r0[j];
+                    if (gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
+                        const float next = T * (1.0f - alpha);
+                        if (thr && next < tmin) {
+                            done = true;
+                        } else {
+                            w = T * alpha;
+                            const float4 r2 = s_r2[j];
+                            acc0 = acc0 + w * r2.x;
+                            acc1 = acc1 + w * r2.y;
+                            acc2 = acc2 + w * r2.z;
+                            if (w > wmax) {
+                                wmax = w;
+                                amax_gid = (int32_t)s_gid[j];
+                            }
+                            last = (int32_t)(base + j);
+                            T = next;
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, w > 0.0f)) {
+                    const float sum = warp_sum(w);
+                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
+                    if (lane == 0) {
+                        atomicAdd(&s_imp[j], sum);
+                        atomicMax(&s_maxw[j], mx);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid < cnt && s_maxw[tid] != 0u) {
+                const uint32_t gid = s_gid[tid];
+                atomicAdd(&out.importance[gid], s_imp[tid]);
+                atomicMax(reinterpret_cast<uint32_t*>(&out.max_weight[gid]), s_maxw[tid]);
+                s_imp[tid] = 0.0f;
+                s_maxw[tid] = 0u;
+            }
+        }
+        __syncthreads();
+    }
+    if (!inside) return;
+    const size_t pix = (size_t)py * cp.width + px;
+    if (REPORT && amax_gid >= 0) atomicAdd(&out.max_pixel_count[amax_gid], 1);
+    if (out.color) {
+        out.color[3 * pix + 0] = acc0 + T * bg0;
+        out.color[3 * pix + 1] = acc1 + T * bg1;
+        out.color[3 * pix + 2] = acc2 + T * bg2;
+    }
+    if (out.alpha) out.alpha[pix] = 1.0f - T;
+    if (out.transmittance) out.transmittance[pix] = T;
+    if (out.max_contributor) out.max_contributor[pix] = amax_gid;
+    if (out.t_final) out.t_final[pix] = T;
+    if (out.last_index) out.last_index[pix] = last;
+    if (out.depth) {
+        float d = 0.0f;
+        if (amax_gid >= 0) {
+            // cam.ray_direction (camera.hpp:32-36) and depth_along_ray (rasterizer.hpp:87-96)
+            float d0 = ((float)px + 0.5f - cp.cx) / cp.fx;
+            float d1 = ((float)py + 0.5f - cp.cy) / cp.fy;
+            float d2 = 1.0f;
+            const float z2 = dot3(d0, d1, d2, d0, d1, d2);
+            if (z2 > 0.0f) {
+                const float nn = sqrtf(z2);
+                d0 = d0 / nn; d1 = d1 / nn; d2 = d2 / nn;
+            }
+            const float w0 = dot3(cp.R[0], cp.R[3], cp.R[6], d0, d1, d2);
+            const float w1 = dot3(cp.R[1], cp.R[4], cp.R[7], d0, d1, d2);
+            const float w2 = dot3(cp.R[2], cp.R[5], cp.R[8], d0, d1, d2);
+            const AuxRec ax = aux[amax_gid];
+            const float r0 = ax.a0.x - cp.center[0], r1 = ax.a0.y - cp.center[1], r2 = ax.a0.z - cp.center[2];
+            if (ax.a0.w != 0.0f) {
+                d = dot3(r0, r1, r2, w0, w1, w2);
+            } else {
+                const float i00 = ax.a1.x, i01 = ax.a1.y, i02 = ax.a1.z, i11 = ax.a1.w, i12 = ax.a2.x,
+                            i22 = ax.a2.y;
+                const float cd0 = dot3(i00, i01, i02, w0, w1, w2);
+                const float cd1 = dot3(i01, i11, i12, w0, w1, w2);
+                const float cd2 = dot3(i02, i12, i22, w0, w1, w2);
+                const float denom = dot3(w0, w1, w2, cd0, cd1, cd2);
+                const float t = dot3(r0, r1, r2, cd0, cd1, cd2) / denom;
+                d = (!(t > 0.0f) || !isfinite(t)) ? dot3(r0, r1, r2, w0, w1, w2) : t;
+            }
+        }
+        out.depth[pix] = d;
+    }
+}
+
+__global__ void unproject_flags_kernel(int width, int height, const int32_t* __restrict__ max_contributor,
+                                       const float* __restrict__ alpha, int rule, float thr, int64_t view_index,
+                                       int32_t stride, int64_t seed, uint32_t* __restrict__ flags) {
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t hw = (int64_t)width * height;
+    if (pix >= hw) return;
+    const bool valid = rule == SPLAT_DEPTH_RULE_ALPHA ? (alpha[pix] > thr) : (max_contributor[pix] >= 0);
+    const int64_t key = view_index * hw + pix + seed;
+    const int64_t m = ((key % stride) + stride) % stride;
+    flags[pix] = (valid && m == 0) ? 1u : 0u;
+}
+
+__global__ void unproject_write_kernel(CamParams cp, const uint32_t* __restrict__ flags,
+                                       const uint32_t* __restrict__ offsets, const float* __restrict__ depth,
+                                       float* __restrict__ points, int32_t* __restrict__ pixel, int64_t capacity) {
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t hw = (int64_t)cp.width * cp.height;
+    if (pix >= hw || !flags[pix]) return;
+    const int64_t o = offsets[pix];
+    if (o >= capacity) return;
+    const int px = (int)(pix % cp.width), py = (int)(pix / cp.width);
+    float d0 = ((float)px + 0.5f - cp.cx) / cp.fx;
+    float d1 = ((float)py + 0.5f - cp.cy) / cp.fy;
+    float d2 = 1.0f;
+    const float z2 = dot3(d0, d1, d2, d0, d1, d2);
+    if (z2 > 0.0f) {
+        const float nn = sqrtf(z2);
+        d0 = d0 / nn; d1 = d1 / nn; d2 = d2 / nn;
+    }
+    const float w0 = dot3(cp.R[0], cp.R[3], cp.R[6], d0, d1, d2);
+    const float w1 = dot3(cp.R[1], cp.R[4], cp.R[7], d0, d1, d2);
+    const float w2 = dot3(cp.R[2], cp.R[5], cp.R[8], d0, d1, d2);
+    const float d = depth[pix];
+    points[3 * o + 0] = cp.center[0] + d * w0;
+    points[3 * o + 1] = cp.center[1] + d * w1;
+    points[3 * o + 2] = cp.center[2] + d * w2;
+    pixel[o] = (int32_t)pix;
+}
+
+__global__ void count_from_scan_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ flags,
+                                       int64_t hw, int32_t* __restrict__ count) {
+    *count = (int32_t)(offsets[hw - 1] + flags[hw - 1]);
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
+                              ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
+                              uint32_t* n_survivors_dev) {
+    if (g.n == 0) return cudaSuccess;
+    const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
+    if (vec)
+        preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+                                                                             tile_counts, n_survivors_dev);
+    else
+        preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+                                                                              tile_counts, n_survivors_dev);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
+                                 uint32_t* counts_sorted, int n) {
+    if (n == 0) return cudaSuccess;
+    gather_counts_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(order, tile_counts, counts_sorted, n);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32_t* offsets, const ProjRec* rec,
+                              const CamParams& cp, int n_survivors, uint32_t* pair_tile, uint32_t* pair_gauss) {
+    if (n_survivors == 0) return cudaSuccess;
+    emit_pairs_kernel<<<blocks_for((int64_t)n_survivors * 32, 256), 256, 0, lc.stream>>>(
+        order, offsets, rec, cp.tile_size, cp.tiles_x, n_survivors, pair_tile, pair_gauss);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs, uint32_t* ranges,
+                               int n_tiles) {
+    tile_ranges_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(sorted_tiles, (uint32_t)n_pairs, ranges,
+                                                                        n_tiles);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+                                 const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux, const float bg[3],
+                                 const FwdOutputs& out) {
+    const int ts = cp.tile_size;
+    const int bw = ts < 16 ? ts : 16;
+    const int subs = ts / bw;
+    dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
+    const int threads = bw * bw;
+    if (out.importance)
+        blend_forward_kernel<true><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
+                                                                   bg[2], out);
+    else
+        blend_forward_kernel<false><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
+                                                                    bg[2], out);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* max_contributor, const float* alpha,
+                             const float* depth, int rule, float alpha_threshold, int64_t view_index, int32_t stride,
+                             int64_t seed, float* points, int32_t* pixel, int64_t capacity, int32_t* count_dev,
+                             uint32_t* flags, uint32_t* offsets, uint32_t* scan_tmp) {
+    const int64_t hw = (int64_t)cp.width * cp.height;
+    unproject_flags_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp.width, cp.height, max_contributor, alpha,
+                                                                       rule, alpha_threshold, view_index, stride,
+                                                                       seed, flags);
+    lc.count++;
+    cudaError_t e = exclusive_scan_u32(lc, flags, offsets, (uint64_t)hw, scan_tmp, nullptr);
+    if (e != cudaSuccess) return e;
+    unproject_write_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp, flags, offsets, depth, points, pixel,
+                                                                       capacity);
+    count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev);
+    lc.count += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace splat_b200

@@ -1,0 +1,119 @@
+// internal.h — host-side declarations shared by the CUDA translation units and the C-ABI layer.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <utility>
+
+#include <cuda_runtime.h>
+
+#include "splat_b200.h"
+
+namespace splat_b200 {
+
+struct CamParams;
+struct ProjRec;
+struct AuxRec;
+
+struct LaunchCtx {
+    cudaStream_t stream = nullptr;
+    int64_t count = 0;  // kernels launched (bench accounting)
+    int num_sms = 148;
+};
+
+// ---- sort.cu ------------------------------------------------------------------------------
+size_t scan_temp_words(uint64_t n);
+size_t radix_hist_words(uint64_t n, int bits);
+cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n,
+                               uint32_t* tmp, uint32_t* total_dev);
+// Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result lands in keys/vals
+// or, when *result_in_alt, in keys_alt/vals_alt.
+cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,
+                             uint32_t* vals_alt, uint64_t n, int begin_bit, int end_bit,
+                             uint32_t* hist, uint32_t* scan_tmp, bool* result_in_alt);
+
+// ---- forward.cu ---------------------------------------------------------------------------
+struct GaussianPtrs {
+    const float* centers;
+    const float* log_scales;
+    const float* rotations;
+    const float* opacity_logits;
+    const float* sh;
+    int n;
+    int sh_degree;
+};
+
+// K1: per-Gaussian projection. Writes rec/aux (aux may be null), depth keys (0xFFFFFFFF when
+// culled), identity values and per-Gaussian tile counts; *n_survivors_dev += survivors.
+cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
+                              const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
+                              uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev);
+// counts_sorted[r] = tile_counts[order[r]]
+cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
+                                 uint32_t* counts_sorted, int n);
+// K3: pairs (tile id, Gaussian id) in depth order.
+cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32_t* offsets,
+                              const ProjRec* rec, const CamParams& cp, int n_survivors,
+                              uint32_t* pair_tile, uint32_t* pair_gauss);
+// K5: ranges[2t], ranges[2t+1] = [start, end) of tile t in the sorted pairs.
+cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs,
+                               uint32_t* ranges, int n_tiles);
+
+struct FwdOutputs {
+    float* color;            // [H][W][3] or null
+    float* alpha;            // [H][W] or null
+    float* depth;            // [H][W] or null (needs aux)
+    float* transmittance;    // [H][W] or null
+    int32_t* max_contributor;// [H][W] or null
+    float* importance;       // [n] or null (report)
+    float* max_weight;       // [n] or null
+    int32_t* max_pixel_count;// [n] or null
+    float* t_final;          // [H][W] backward state or null
+    int32_t* last_index;     // [H][W] backward state or null
+};
+
+// K6 (+K7 depth epilogue): per-tile front-to-back blend.
+cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+                                 const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux,
+                                 const float bg[3], const FwdOutputs& out);
+
+// Depth unprojection + stride-rule compaction over one rendered view.
+cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* max_contributor,
+                             const float* alpha, const float* depth, int rule, float alpha_threshold,
+                             int64_t view_index, int32_t stride, int64_t seed, float* points,
+                             int32_t* pixel, int64_t capacity, int32_t* count_dev, uint32_t* flags,
+                             uint32_t* offsets, uint32_t* scan_tmp);
+
+// ---- backward.cu --------------------------------------------------------------------------
+// Per-Gaussian 2D gradient accumulator, 48 B (3 x float4):
+//   g0 = (d_mean.x, d_mean.y, d_conic00, d_conic01), g1 = (d_conic11, d_opacity, d_col.r,
+//   d_col.g), g2 = (d_col.b, touched, 0, 0)
+struct Grad2D;
+
+cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+                                  const uint32_t* pair_gauss, const ProjRec* rec,
+                                  const float* t_final, const int32_t* last_index, const float bg[3],
+                                  const float* d_color, const float* color, const float* target,
+                                  float* loss_partials, float* grad2d);
+cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
+cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d,
+                         const ProjRec* rec, const splat_param_grads& out, int accumulate);
+cudaError_t launch_l1(LaunchCtx& lc, const float* a, const float* b, int64_t n, float* grad,
+                      float* partials, int n_partials);
+int l1_partials_count(int64_t n);
+
+struct AdamGroupArgs {
+    float* param;
+    const float* grad;
+    float* m;
+    float* v;
+    int64_t count;
+    double lr;
+    double lr_alt;   // for SH: lr of coefficients k >= 3 (rest)
+    int sh_layout;   // 1: per-48 row, first 3 use lr, rest lr_alt
+};
+cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, double beta2, double eps,
+                        double bias1, double bias2);
+cudaError_t launch_quat_normalize(LaunchCtx& lc, float* rotations, int n);
+
+}  // namespace splat_b200

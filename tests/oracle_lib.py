@@ -88,6 +88,8 @@ class OracleLib:
             getattr(L, p + "adam_steps").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp,
                                            C.POINTER(AdamConfig), C.c_int32]
             getattr(L, p + "depth_reinitialize").argtypes = [G, CAM, CFG, fp, C.c_int32, C.c_uint32, fp, ip]
+            dp = C.POINTER(C.c_double)
+            getattr(L, p + "render_backward_f64").argtypes = [G, CAM, CFG, fp, u8p, fp, dp, dp, dp, dp, dp]
             getattr(L, p + "global_importance").argtypes = [G, CAM, C.c_int32, CFG, C.POINTER(C.c_double), ip]
 
     def fn(self, name):
@@ -174,6 +176,23 @@ class OracleLib:
             _ptr(g["d_centers"]), _ptr(g["d_log_scales"]), _ptr(g["d_rotations"]),
             _ptr(g["d_opacity_logits"]), _ptr(g["d_sh"]), _ptr(g["grad2d_accum"]),
             _ptr(g["grad2d_count"], ip)))
+        return {k: v[: s.n] for k, v in g.items()}
+
+    def render_backward_f64(self, s, cam, d_color, cfg=None, mask=None, bg=(0.0, 0.0, 0.0)):
+        """Reference render_backward<double> (fp64 truth) on the float inputs."""
+        cfg = cfg or RasterConfig()
+        gv = GaussiansView(s)
+        n = max(s.n, 1)
+        g = dict(d_centers=np.zeros((n, 3)), d_log_scales=np.zeros((n, 3)), d_rotations=np.zeros((n, 4)),
+                 d_opacity_logits=np.zeros(n), d_sh=np.zeros((n, 48)))
+        dc = np.ascontiguousarray(d_color, np.float32)
+        bgv = np.asarray(bg, np.float32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        dptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        self.check(self.fn("render_backward_f64")(
+            C.byref(gv.struct), C.byref(cam), C.byref(cfg), _ptr(dc), _ptr(m, u8p), _ptr(bgv),
+            dptr(g["d_centers"]), dptr(g["d_log_scales"]), dptr(g["d_rotations"]), dptr(g["d_opacity_logits"]),
+            dptr(g["d_sh"])))
         return {k: v[: s.n] for k, v in g.items()}
 
     def l1_loss(self, a, b, want_grad=True):
