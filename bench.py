@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""bench.py — fwd+bwd training views/s of the Mini-Splatting2 rasterizer hot path on B200.
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on): 1,000,000 Gaussians
+(config-0 distributions, seed 0), SH degree 3, 1237x822 ring views (fov 70 deg, radius 3R,
+height 0.5R), L1 loss against targets rendered from the same set with means + N(0, 0.01^2).
+One step = per rank `--views` ring views of: preprocess -> (depth, tile) radix sorts -> blend
+forward -> fused L1 -> blend backward -> per-Gaussian chain (all 59 gradients), then (N > 1) an
+NCCL all-reduce of the optimised gradient slice, then Adam on means (lr 1.6e-4).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd+bwd views/s (1M Gaussians, 1237x822, SH3) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "views/s"
+RING = 64
+REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--views", type=int, default=1, help="ring views per rank per step")
+    ap.add_argument("--gaussians", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload_config(args, world):
+    return {"workload": "cfg1: 1M Gaussians SH3, 1237x822 ring views, L1 vs perturbed-means target, "
+                        "fwd+bwd (59 grads) + Adam(means, lr 1.6e-4)",
+            "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
+            "ring_views": RING, "n_ranks": world,
+            "allreduce": "3N mean gradients (fp32, NCCL sum) when N > 1",
+            "l2": "inputs larger than L2 (236 MB parameters + ~160 MB pair lists per view); views rotate each step",
+            "scene_seed": 0}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU reference (oracle/_ref, the reference's own sources; test infrastructure, never the product)
+# ---------------------------------------------------------------------------------------------
+def _ref_lib():
+    lib_path = ROOT / "oracle" / "_ref" / "libsplat_ref_libm.so"
+    kind = "reference"
+    if not lib_path.exists():
+        return None, None
+    from paper_2411_12788_b200.capi import AdamConfig, Camera, Gaussians, RasterConfig
+    lib = C.CDLL(str(lib_path))
+    lib.ref_scene_create.restype = C.c_void_p
+    lib.ref_scene_create.argtypes = [C.POINTER(Gaussians), C.POINTER(AdamConfig)]
+    lib.ref_scene_destroy.argtypes = [C.c_void_p]
+    lib.ref_train_view.restype = C.c_int
+    lib.ref_train_view.argtypes = [C.c_void_p, C.POINTER(Camera), C.POINTER(RasterConfig),
+                                   C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    return lib, kind
+
+
+def cpu_views_per_s(n_gaussians, threads, rounds=1):
+    """Time the reference's own render -> l1_loss -> render_backward -> OptimState::step on
+    `threads` host threads, each training one config-1 ring view per round."""
+    from paper_2411_12788_b200 import scenes
+    from paper_2411_12788_b200.capi import AdamConfig, Gaussians, RasterConfig
+    lib, kind = _ref_lib()
+    if lib is None:
+        return None
+    s = scenes.make_gaussians(n_gaussians, seed=0)
+    arrs = [np.ascontiguousarray(a, np.float32) for a in (s.centers, s.log_scales, s.rotations, s.opacity_logits, s.sh)]
+    fp = C.POINTER(C.c_float)
+    g = Gaussians(*[a.ctypes.data_as(fp) for a in arrs], s.n, 3)
+    adam = AdamConfig()
+    cfg = RasterConfig()
+    cams = [scenes.ring_camera(k, RING) for k in range(threads)]
+    # targets: a cheap deterministic stand-in image per view (CPU time of the target render is
+    # not part of the step); value range matches a render.
+    rng = np.random.default_rng(0)
+    tgt = [np.ascontiguousarray(rng.uniform(0, 1, size=(822, 1237, 3)).astype(np.float32)) for _ in range(threads)]
+    handles = [lib.ref_scene_create(C.byref(g), C.byref(adam)) for _ in range(threads)]
+    if not all(handles):
+        return None
+    errors = []
+
+    def work(i):
+        loss = C.c_float()
+        for _ in range(rounds):
+            rc = lib.ref_train_view(handles[i], C.byref(cams[i]), C.byref(cfg), tgt[i].ctypes.data_as(fp), C.byref(loss))
+            if rc:
+                errors.append(rc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    for hnd in handles:
+        lib.ref_scene_destroy(hnd)
+    if errors:
+        raise RuntimeError(f"reference train_view failed: {errors[:3]}")
+    return {"value": threads * rounds / wall, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{threads} threads x {rounds} config-1 ring view(s) each through the reference's own "
+                      f"render<float> -> l1_loss -> render_backward<float> -> OptimState::step (means), "
+                      f"{wall:.1f} s wall", "seconds": wall}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    threads = args.cpu_threads or os.cpu_count() or 1
+    lib, _ = _ref_lib()
+    if lib is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsplat_ref_libm.so not built"}))
+        return
+    for _ in range(args.warmup):
+        cpu_views_per_s(args.gaussians, threads, 1)
+    t_total, views = 0.0, 0
+    for _ in range(args.steps):
+        r = cpu_views_per_s(args.gaussians, threads, 1)
+        t_total += r["seconds"]
+        views += threads
+    value = views / t_total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE cfg1 shapes)",
+            "config": workload_config(args, world), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{threads} threads x 1 config-1 view per step (reference's own C++ "
+                                       f"compiled in place, glibc expf)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(r)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(kernel, n, n_surv, pairs, hw):
+    """Compulsory HBM bytes per launch (SURVEY.md §8d terms)."""
+    if kernel == "blend_backward":
+        # sorted ids 4P + projected records 48 B/Gaussian + per-pixel T, last, colour, target (32 B)
+        # + 2D gradient accumulators 48 B/Gaussian
+        return 4 * pairs + 48 * n_surv + 32 * hw + 48 * n_surv
+    if kernel == "blend_forward":
+        return 4 * pairs + 48 * n_surv + 20 * hw  # ids + records + colour 12, T 4, last 4
+    if kernel == "chain":
+        return 48 * n + 48 * n + 236 * n + 236 * n + 48 * n  # grad2d r/w-zero, rec, params, grads
+    if kernel == "preprocess":
+        return 236 * n + 48 * n + 12 * n
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    device = torch.cuda.current_device()
+
+    from paper_2411_12788_b200 import capi, scenes
+    from paper_2411_12788_b200.rasterizer import Context, DeviceGaussians, render
+    from paper_2411_12788_b200.trainer import ViewTrainer
+
+    ctx = Context.default(device)
+    s = scenes.make_gaussians(args.gaussians, seed=0)
+    ds = DeviceGaussians.from_host(s, device)
+    dt = DeviceGaussians.from_host(scenes.perturbed(s), device)
+    cams = [scenes.ring_camera(k, RING) for k in range(RING)]
+    targets = [render(dt, cam, want_depth=False, ctx=ctx).color.clone() for cam in cams]
+    del dt
+    trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=capi.GROUP_CENTERS, ctx=ctx, max_views=max(args.views, 1))
+    V = args.views
+
+    def views_for(step):
+        idx = [(step * world * V + rank * V + j) % RING for j in range(V)]
+        return [cams[i] for i in idx], [targets[i] for i in idx], idx
+
+    stream = torch.cuda.current_stream()
+    for st in range(args.warmup):
+        c, t, _ = views_for(st)
+        trainer.step(c, t)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region -----------------------------------------------------------------
+    lib = ctx.lib
+    lib.splat_profile_enable(ctx.h, 1)
+    clocks = ClockSampler(device)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    pairs = []
+    for st in range(args.warmup, args.warmup + args.steps):
+        c, t, _ = views_for(st)
+        trainer.step(c, t)
+        pairs += trainer.pairs_last_step
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    names = C.create_string_buffer(4096)
+    tot = (C.c_double * 64)()
+    cnt = (C.c_int64 * 64)()
+    nk = C.c_int()
+    ctx.check(lib.splat_profile_read(ctx.h, names, 4096, tot, cnt, 64, C.byref(nk)))
+    lib.splat_profile_enable(ctx.h, 0)
+    kern = {nm: (tot[i], cnt[i]) for i, nm in enumerate(names.value.decode().split("\n")[: nk.value])}
+    if world > 1:
+        t_ms = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        ms = float(t_ms.item())
+    total_views = world * V * args.steps
+    value = total_views / (ms / 1000.0)
+
+    # ---- e2e through the public API with host buffers -------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host_t = [targets[i].cpu().pin_memory() for i in range(min(RING, 8 * V))]
+        for st in range(2):
+            c, _, idx = views_for(st)
+            trainer.step_host(c, [host_t[i % len(host_t)] for i in idx])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for st in range(args.steps):
+            c, _, idx = views_for(st)
+            trainer.step_host(c, [host_t[i % len(host_t)] for i in idx])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t_ms = torch.tensor([ems], device=f"cuda:{device}", dtype=torch.float64)
+            dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+            ems = float(t_ms.item())
+        e2e = {"value": total_views / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(V * 822 * 1237 * 3 * 4), "d2h_bytes_per_step": int(V * 4),
+               "path": "ViewTrainer.step_host: pinned host target -> device copy, C-ABI render/backward_l1/adam, "
+                       "loss read back each step"}
+
+    # ---- roofline of the dominant kernel (CUDA events around every launch, timed region) ----------
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    peak, peak_src = 6537.6, "MEASURED_PEAKS.json hbm_gbs (fallback if absent)"
+    if peaks_path.exists():
+        try:
+            peak = float(json.loads(peaks_path.read_text())["hbm_gbs"])
+            peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    dom = max(kern.items(), key=lambda kv: kv[1][0])[0] if kern else None
+    n_views = len(pairs)
+    hw = 1237 * 822
+    n = args.gaussians
+    avg_pairs = float(np.mean(pairs)) if pairs else 0.0
+    n_surv = n  # all survive at cfg1 (ring radius 3R > R)
+    roof = None
+    if dom:
+        ab = algorithmic_bytes(dom, n, n_surv, avg_pairs, hw)
+        avg_ms = kern[dom][0] / max(kern[dom][1], 1)
+        if ab:
+            achieved = ab / (avg_ms / 1000.0) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": ab,
+                    "avg_launch_ms": avg_ms, "peak_source": peak_src,
+                    "note": "blend kernels are issue-bound (FP32/SFU/LSU on staged records), not HBM-bound"}
+    breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                     "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or min(os.cpu_count() or 1, 16)
+        try:
+            cpu = cpu_views_per_s(args.gaussians, threads, 1)
+            if cpu:
+                cpu.pop("seconds", None)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE cfg1 shapes)",
+                "config": workload_config(args, world), "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+                "pairs_per_view": avg_pairs, "kernel_breakdown": breakdown}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

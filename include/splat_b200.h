@@ -170,6 +170,14 @@ const char* splat_last_error(const splat_ctx* ctx);
 /* Number of kernels this context launched since creation (for bench accounting). */
 int64_t splat_kernel_launches(const splat_ctx* ctx);
 
+/* Per-kernel CUDA-event timing on the context stream (bench accounting). While enabled,
+ * every launch is bracketed by events; splat_profile_read synchronises, writes up to
+ * max_kernels entries (names '\n'-separated into `names`, total milliseconds, launch counts)
+ * and resets the accumulators. */
+int splat_profile_enable(splat_ctx* ctx, int on);
+int splat_profile_read(splat_ctx* ctx, char* names, int names_bytes, double* total_ms,
+                       int64_t* counts, int max_kernels, int* n_kernels);
+
 /* ---- forward ------------------------------------------------------------------------ */
 /* render<float>: g/mask/out are device pointers; background is host float[3]. The context
  * keeps the forward state (sorted tile lists, projected records, per-pixel T_final and last

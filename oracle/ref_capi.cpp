@@ -376,4 +376,46 @@ int ref_render_backward_f64(const splat_gaussians* g, const splat_camera* c, con
     REF_CATCH
 }
 
+
+// ---- CPU baseline: one config-1 training view through the reference's own API ---------------
+// A scene handle owns a GaussianSet + OptimState so the timed call runs only reference code:
+// render<float> -> l1_loss -> render_backward<float> -> OptimState::step with only d_centers
+// populated (config 1: Adam on means; zero grads + zero moments leave the other groups unchanged,
+// test_optimizer.cpp:147-159).
+struct RefScene {
+    GaussianSet set;
+    OptimState opt;
+    RefScene(GaussianSet s, const AdamConfig& c) : set(std::move(s)), opt(c, 0) { opt.reinit(set.size()); }
+};
+
+void* ref_scene_create(const splat_gaussians* g, const splat_adam_config* cfg) {
+    try {
+        return new RefScene(to_set(g), to_adam(cfg));
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void ref_scene_destroy(void* h) { delete static_cast<RefScene*>(h); }
+
+int ref_train_view(void* h, const splat_camera* c, const splat_raster_config* cf, const float* target,
+                   float* loss_out) {
+    REF_TRY
+    RefScene& sc = *static_cast<RefScene*>(h);
+    const Camera cam = to_cam(c);
+    const RasterConfig cfg = to_cfg(cf);
+    const auto out = render<float>(sc.set, cam, cfg);
+    Imagef tgt(cam.width, cam.height, 3), d_color;
+    std::memcpy(tgt.data.data(), target, sizeof(float) * tgt.data.size());
+    const float loss = l1_loss<float>(out.color, tgt, &d_color);
+    ParamGrads<float> g = render_backward<float>(sc.set, cam, cfg, d_color);
+    ParamGrads<float> means;
+    means.resize_zero(sc.set.size());
+    means.d_centers = g.d_centers;
+    sc.opt.step(sc.set, means);
+    if (loss_out) *loss_out = loss;
+    return 0;
+    REF_CATCH
+}
+
 }  // extern "C"

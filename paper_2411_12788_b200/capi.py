@@ -199,6 +199,9 @@ _EXPORTS = {
     "splat_sync": (C.c_int, [C.c_void_p]),
     "splat_last_error": (C.c_char_p, [C.c_void_p]),
     "splat_kernel_launches": (C.c_int64, [C.c_void_p]),
+    "splat_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "splat_profile_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int)]),
     "splat_render": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera),
                                C.POINTER(RasterConfig), u8p, C.POINTER(C.c_float),
                                C.POINTER(RenderOutputs), C.POINTER(ImportanceOutputs)]),

@@ -618,15 +618,21 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
     const int subs = ts / bw;
     dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
-    blend_backward_kernel<<<grid, bw * bw, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, t_final, last_index, bg[0],
+    {
+        LaunchScope ls_(lc, "blend_backward");
+        blend_backward_kernel<<<grid, bw * bw, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, t_final, last_index, bg[0],
                                                           bg[1], bg[2], d_color, color, target, inv_n, loss_partials,
                                                           reinterpret_cast<float4*>(grad2d));
+    }
     lc.count++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss) {
-    loss_reduce_kernel<<<1, 256, 0, lc.stream>>>(partials, n, inv_n, loss);
+    {
+        LaunchScope ls_(lc, "loss_reduce");
+        loss_reduce_kernel<<<1, 256, 0, lc.stream>>>(partials, n, inv_n, loss);
+    }
     lc.count++;
     return cudaGetLastError();
 }
@@ -636,11 +642,17 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
     if (g.n == 0) return cudaSuccess;
     const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
     if (vec)
-        chain_kernel<true><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
+        {
+            LaunchScope ls_(lc, "chain");
+            chain_kernel<true><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
                                                                        out, accumulate);
+        }
     else
-        chain_kernel<false><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
+        {
+            LaunchScope ls_(lc, "chain");
+            chain_kernel<false><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
                                                                         rec, out, accumulate);
+        }
     lc.count++;
     return cudaGetLastError();
 }
@@ -658,16 +670,22 @@ cudaError_t launch_l1(LaunchCtx& lc, const float* a, const float* b, int64_t n, 
 cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, double beta2, double eps, double bias1,
                         double bias2) {
     if (a.count == 0) return cudaSuccess;
-    adam_kernel<<<blocks_for(a.count, 256), 256, 0, lc.stream>>>(a.param, a.grad, a.m, a.v, a.count, a.lr, a.lr_alt,
+    {
+        LaunchScope ls_(lc, "adam");
+        adam_kernel<<<blocks_for(a.count, 256), 256, 0, lc.stream>>>(a.param, a.grad, a.m, a.v, a.count, a.lr, a.lr_alt,
                                                                 a.sh_layout, beta1, 1.0 - beta1, beta2, 1.0 - beta2,
                                                                 eps, bias1, bias2);
+    }
     lc.count++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_quat_normalize(LaunchCtx& lc, float* rotations, int n) {
     if (n == 0) return cudaSuccess;
-    quat_normalize_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(rotations, n);
+    {
+        LaunchScope ls_(lc, "quat_normalize");
+        quat_normalize_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(rotations, n);
+    }
     lc.count++;
     return cudaGetLastError();
 }

@@ -11,12 +11,61 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
 #include "splat_b200.h"
 
 using namespace splat_b200;
+
+// Per-kernel CUDA-event timing (bench.py's live roofline): every launch is bracketed by two
+// events on the launching stream; splat_profile_read() synchronises and sums per kernel name.
+namespace splat_b200 {
+struct ProfileState {
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t open = 0;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void recycle() {
+        for (auto& r : recs) {
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        recs.clear();
+    }
+    ~ProfileState() {
+        recycle();
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+void LaunchCtx::prof_begin(const char* name) {
+    if (!prof) return;
+    ProfileState::Rec r{name, prof->get(), prof->get()};
+    cudaEventRecord(r.a, stream);
+    prof->recs.push_back(r);
+}
+
+void LaunchCtx::prof_end() {
+    if (!prof || prof->recs.empty()) return;
+    cudaEventRecord(prof->recs.back().b, stream);
+}
+}  // namespace splat_b200
 
 namespace {
 
@@ -360,6 +409,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (!ctx) return SPLAT_OK;
     cudaSetDevice(ctx->device);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
+    delete ctx->lc.prof;
     delete ctx;
     return SPLAT_OK;
 }
@@ -380,6 +430,48 @@ int splat_sync(splat_ctx* ctx) {
 const char* splat_last_error(const splat_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t splat_kernel_launches(const splat_ctx* ctx) { return ctx ? ctx->lc.count : 0; }
+
+int splat_profile_enable(splat_ctx* ctx, int on) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (on && !ctx->lc.prof) ctx->lc.prof = new ProfileState();
+    if (!on && ctx->lc.prof) {
+        cudaStreamSynchronize(ctx->stream);
+        delete ctx->lc.prof;
+        ctx->lc.prof = nullptr;
+    }
+    return SPLAT_OK;
+}
+
+int splat_profile_read(splat_ctx* ctx, char* names, int names_bytes, double* total_ms, int64_t* counts, int max_kernels,
+                       int* n_kernels) {
+    if (!ctx || !ctx->lc.prof) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "profiling not enabled");
+    CK(cudaStreamSynchronize(ctx->stream), "profile sync");
+    std::map<std::string, std::pair<double, int64_t>> agg;
+    for (auto& r : ctx->lc.prof->recs) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b), "profile elapsed");
+        auto& e = agg[r.name];
+        e.first += ms;
+        e.second += 1;
+    }
+    ctx->lc.prof->recycle();
+    int k = 0;
+    std::string all;
+    for (auto& kv : agg) {
+        if (k >= max_kernels) break;
+        total_ms[k] = kv.second.first;
+        counts[k] = kv.second.second;
+        all += kv.first;
+        all += '\n';
+        ++k;
+    }
+    if (names && names_bytes > 0) {
+        std::strncpy(names, all.c_str(), (size_t)names_bytes - 1);
+        names[names_bytes - 1] = 0;
+    }
+    *n_kernels = k;
+    return SPLAT_OK;
+}
 
 int splat_render(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
                  const uint8_t* mask, const float background[3], const splat_render_outputs* out,

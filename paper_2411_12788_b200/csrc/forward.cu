@@ -523,11 +523,17 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
-        preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+        {
+            LaunchScope ls_(lc, "preprocess");
+            preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
                                                                              tile_counts, n_survivors_dev);
+        }
     else
-        preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+        {
+            LaunchScope ls_(lc, "preprocess");
+            preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
                                                                               tile_counts, n_survivors_dev);
+        }
     lc.count++;
     return cudaGetLastError();
 }
@@ -535,7 +541,10 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
 cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
                                  uint32_t* counts_sorted, int n) {
     if (n == 0) return cudaSuccess;
-    gather_counts_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(order, tile_counts, counts_sorted, n);
+    {
+        LaunchScope ls_(lc, "gather_counts");
+        gather_counts_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(order, tile_counts, counts_sorted, n);
+    }
     lc.count++;
     return cudaGetLastError();
 }
@@ -543,16 +552,22 @@ cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uin
 cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32_t* offsets, const ProjRec* rec,
                               const CamParams& cp, int n_survivors, uint32_t* pair_tile, uint32_t* pair_gauss) {
     if (n_survivors == 0) return cudaSuccess;
-    emit_pairs_kernel<<<blocks_for((int64_t)n_survivors * 32, 256), 256, 0, lc.stream>>>(
+    {
+        LaunchScope ls_(lc, "emit_pairs");
+        emit_pairs_kernel<<<blocks_for((int64_t)n_survivors * 32, 256), 256, 0, lc.stream>>>(
         order, offsets, rec, cp.tile_size, cp.tiles_x, n_survivors, pair_tile, pair_gauss);
+    }
     lc.count++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs, uint32_t* ranges,
                                int n_tiles) {
-    tile_ranges_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(sorted_tiles, (uint32_t)n_pairs, ranges,
+    {
+        LaunchScope ls_(lc, "tile_ranges");
+        tile_ranges_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(sorted_tiles, (uint32_t)n_pairs, ranges,
                                                                         n_tiles);
+    }
     lc.count++;
     return cudaGetLastError();
 }
@@ -566,11 +581,17 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
     dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
     const int threads = bw * bw;
     if (out.importance)
-        blend_forward_kernel<true><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
+        {
+            LaunchScope ls_(lc, "blend_forward");
+            blend_forward_kernel<true><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
                                                                    bg[2], out);
+        }
     else
-        blend_forward_kernel<false><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
+        {
+            LaunchScope ls_(lc, "blend_forward");
+            blend_forward_kernel<false><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
                                                                     bg[2], out);
+        }
     lc.count++;
     return cudaGetLastError();
 }
@@ -580,15 +601,24 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
                              int64_t seed, float* points, int32_t* pixel, int64_t capacity, int32_t* count_dev,
                              uint32_t* flags, uint32_t* offsets, uint32_t* scan_tmp) {
     const int64_t hw = (int64_t)cp.width * cp.height;
-    unproject_flags_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp.width, cp.height, max_contributor, alpha,
+    {
+        LaunchScope ls_(lc, "unproject_flags");
+        unproject_flags_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp.width, cp.height, max_contributor, alpha,
                                                                        rule, alpha_threshold, view_index, stride,
                                                                        seed, flags);
+    }
     lc.count++;
     cudaError_t e = exclusive_scan_u32(lc, flags, offsets, (uint64_t)hw, scan_tmp, nullptr);
     if (e != cudaSuccess) return e;
-    unproject_write_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp, flags, offsets, depth, points, pixel,
+    {
+        LaunchScope ls_(lc, "unproject_write");
+        unproject_write_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp, flags, offsets, depth, points, pixel,
                                                                        capacity);
-    count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev);
+    }
+    {
+        LaunchScope ls_(lc, "count_from_scan");
+        count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev);
+    }
     lc.count += 2;
     return cudaGetLastError();
 }

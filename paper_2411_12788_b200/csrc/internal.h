@@ -15,10 +15,23 @@ struct CamParams;
 struct ProjRec;
 struct AuxRec;
 
+struct ProfileState;
+
 struct LaunchCtx {
     cudaStream_t stream = nullptr;
     int64_t count = 0;  // kernels launched (bench accounting)
     int num_sms = 148;
+    ProfileState* prof = nullptr;  // non-null while per-kernel CUDA-event timing is on
+    // Bracket one kernel launch with CUDA events on `stream` (no-ops when profiling is off).
+    void prof_begin(const char* name);
+    void prof_end();
+};
+
+// RAII bracket: LaunchScope s(lc, "name"); kernel<<<...>>>;
+struct LaunchScope {
+    LaunchCtx& lc;
+    LaunchScope(LaunchCtx& l, const char* name) : lc(l) { lc.prof_begin(name); }
+    ~LaunchScope() { lc.prof_end(); }
 };
 
 // ---- sort.cu ------------------------------------------------------------------------------

@@ -210,11 +210,17 @@ cudaError_t radix_pass(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, ui
                        uint32_t n, int shift, uint32_t* hist, uint32_t* scan_tmp) {
     const uint32_t nblocks = (n + kSortTile - 1) / kSortTile;
     constexpr uint32_t BINS = 1u << BITS;
-    radix_upsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, n, shift, hist, nblocks);
+    {
+        LaunchScope ls_(lc, "radix_upsweep");
+        radix_upsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, n, shift, hist, nblocks);
+    }
     lc.count++;
     cudaError_t e = exclusive_scan_u32(lc, hist, hist, BINS * nblocks, scan_tmp, nullptr);
     if (e != cudaSuccess) return e;
-    radix_downsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, nblocks);
+    {
+        LaunchScope ls_(lc, "radix_downsweep");
+        radix_downsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, nblocks);
+    }
     lc.count++;
     return cudaGetLastError();
 }
@@ -238,9 +244,18 @@ cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out,
         return cudaSuccess;
     }
     const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
-    scan_reduce_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, (uint32_t)n, tmp);
-    scan_sums_kernel<<<1, kScanThreads, 0, lc.stream>>>(tmp, nb, total_dev);
-    scan_down_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, out, (uint32_t)n, tmp);
+    {
+        LaunchScope ls_(lc, "scan_reduce");
+        scan_reduce_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, (uint32_t)n, tmp);
+    }
+    {
+        LaunchScope ls_(lc, "scan_sums");
+        scan_sums_kernel<<<1, kScanThreads, 0, lc.stream>>>(tmp, nb, total_dev);
+    }
+    {
+        LaunchScope ls_(lc, "scan_down");
+        scan_down_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, out, (uint32_t)n, tmp);
+    }
     lc.count += 3;
     return cudaGetLastError();
 }

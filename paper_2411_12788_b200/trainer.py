@@ -1,0 +1,97 @@
+"""View-parallel training step over the C-ABI: the caller side of the hot path.
+
+One step (trainer.cpp:226-240 with lambda_dssim = 0, batched as BASELINE config 4):
+  for each view of this rank's batch:
+      render<float>                                   (splat_render)
+      l1_loss + render_backward<float>, grads summed  (splat_render_backward_l1, ParamGrads::add)
+  all-reduce of the packed gradient (torch.distributed / NCCL), only when world_size > 1:
+      the 3N mean gradients when only means are optimised (config 1), all 59N floats otherwise
+  OptimState::step on the selected parameter groups (splat_adam_step)
+
+Views shard across ranks with no data-path collective other than that gradient exchange.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import Camera, RasterConfig, RenderOutputs, as_fp
+from .rasterizer import Context, DeviceGaussians, DeviceGrads, OptimState, _torch
+
+
+class ViewTrainer:
+    def __init__(self, params: DeviceGaussians, adam: Optional[capi.AdamConfig] = None,
+                 group_mask: int = capi.GROUP_ALL, cfg: Optional[RasterConfig] = None,
+                 background=(0.0, 0.0, 0.0), ctx: Optional[Context] = None, max_views: int = 64,
+                 process_group=None):
+        torch = _torch()
+        self.torch = torch
+        self.ctx = ctx or Context.default()
+        self.params = params
+        self.cfg = cfg or RasterConfig()
+        self.bg = (C.c_float * 3)(*background)
+        self.group_mask = group_mask
+        self.grads = DeviceGrads(params.n, self.ctx.device)
+        self.opt = OptimState(adam or capi.AdamConfig(), params.n, self.ctx.device)
+        self.loss = torch.zeros(max_views, dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        self.pg = process_group
+        self.pairs_last_step: list[int] = []
+        self._empty_out = RenderOutputs()
+        self._gs = params.struct()
+        self._gr = self.grads.struct()
+        self._staging = None
+
+    @property
+    def world_size(self) -> int:
+        import torch.distributed as dist
+        return dist.get_world_size(self.pg) if dist.is_available() and dist.is_initialized() else 1
+
+    def reduce_slice(self):
+        """The part of the packed gradient that the optimiser consumes (the exchanged bytes)."""
+        n = self.params.n
+        if self.group_mask == capi.GROUP_CENTERS:
+            return self.grads.flat[: 3 * n]
+        return self.grads.flat[: 59 * n]
+
+    def _views(self, cams: Sequence[Camera], targets) -> None:
+        lib, h = self.ctx.lib, self.ctx.h
+        self.pairs_last_step = []
+        for j, (cam, tgt) in enumerate(zip(cams, targets)):
+            self.ctx.check(lib.splat_render(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), None, self.bg,
+                                            C.byref(self._empty_out), None))
+            np_, = [C.c_int64()]
+            lib.splat_forward_counts(h, None, C.byref(np_), None, None)
+            self.pairs_last_step.append(np_.value)
+            self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
+                                                        as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
+                                                        1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
+
+    def _finish(self) -> None:
+        if self.world_size > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
+        self.opt.step(self.params, self.grads, self.group_mask, self.ctx)
+
+    def step(self, cams: Sequence[Camera], targets) -> "object":
+        """Device-resident step: targets are CUDA tensors [H, W, 3]. Returns the per-view loss
+        tensor (device); nothing is synchronised."""
+        self.ctx.bind_stream()
+        self._views(cams, targets)
+        self._finish()
+        return self.loss[: len(cams)]
+
+    def step_host(self, cams: Sequence[Camera], targets_host) -> np.ndarray:
+        """End-to-end step through the public API: each view's target is copied host->device
+        (pinned, async) inside the step and the per-view losses are read back to the host."""
+        torch = self.torch
+        k = len(cams)
+        shape = tuple(targets_host[0].shape)
+        if self._staging is None or self._staging.shape[0] < k or tuple(self._staging.shape[1:]) != shape:
+            self._staging = torch.empty((k, *shape), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        for j in range(k):
+            self._staging[j].copy_(targets_host[j], non_blocking=True)
+        self.step(cams, [self._staging[j] for j in range(k)])
+        return self.loss[:k].cpu().numpy()
