@@ -24,6 +24,7 @@ SOURCES = {
     "forward.cu": ["--fmad=false"],
     "sort.cu": [],
     "backward.cu": [],
+    "chain.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                                                             float4* __restrict__ grad2d) {
     __shared__ float4 s_r0[kBlock], s_r1[kBlock], s_r2[kBlock];
     __shared__ uint32_t s_gid[kBlock];
+    __shared__ int s_idx[kBlock];
+    __shared__ int s_wcnt[kBlock / 32];
     __shared__ float s_g[kBlock * kGradStride];
     __shared__ float s_red[kBlock / 32];
     __shared__ int s_maxlast[kBlock / 32];
@@ -93,15 +95,17 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
     const int subs = ts / bw;
     const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
-    const int px = tx * ts + sx * bw + tid % bw;
-    const int py = ty * ts + sy * bw + tid / bw;
+    const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
+    const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
+    const int px = bx0 + tid % bw;
+    const int py = by0 + tid / bw;
     const bool inside = px < cp.width && py < cp.height;
     const size_t pix = inside ? (size_t)py * cp.width + px : 0;
 
     float dL0 = 0.f, dL1 = 0.f, dL2 = 0.f;
+    float l = 0.0f;
     if (inside) {
         if (target) {
-            float l = 0.0f;
             float* dl[3] = {&dL0, &dL1, &dL2};
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -109,21 +113,18 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                 l += fabsf(dd);
                 *dl[c] = dd > 0.0f ? inv_n : (dd < 0.0f ? -inv_n : 0.0f);
             }
-            if (loss_partials) {
-                const float ws = warp_sum(l);
-                if (lane == 0) s_red[warp] = ws;
-            }
         } else {
             dL0 = d_color[3 * pix];
             dL1 = d_color[3 * pix + 1];
             dL2 = d_color[3 * pix + 2];
         }
-    } else if (target && loss_partials) {
-        const float ws = warp_sum(0.0f);
+    }
+    if (target && loss_partials) {
+        const float ws = warp_sum(l);
         if (lane == 0) s_red[warp] = ws;
     }
     const int my_last = inside ? last_index[pix] : -1;
-    const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(my_last + 1)) - 1;
+    const int wl = (int)__reduce_max_sync(0xffffffffu, (unsigned)(my_last + 1)) - 1;
     if (lane == 0) s_maxlast[warp] = wl;
     __syncthreads();
     if (target && loss_partials && tid == 0) {
@@ -143,23 +144,14 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     float b0 = bg0, b1 = bg1, b2 = bg2;
 
     for (int hi = block_last + 1; hi > (int)start; hi -= nthreads) {
-        const int lo = max((int)start, hi - nthreads);
-        const int cnt = hi - lo;
-        if (tid < cnt) {
-            const uint32_t gid = pair_gauss[hi - 1 - tid];
-            const ProjRec rr = rec[gid];
-            s_r0[tid] = rr.r0;
-            s_r1[tid] = rr.r1;
-            s_r2[tid] = rr.r2;
-            s_gid[tid] = gid;
-#pragma unroll
-            for (int k = 0; k < kGradSlots; ++k) s_g[tid * kGradStride + k] = 0.0f;
-        }
+        const int count = min(nthreads, hi - (int)start);
+        const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1,
+                                    s_r0, s_r1, s_r2, s_gid, s_idx, s_wcnt);
+        for (int k = tid; k < cnt * kGradStride; k += nthreads) s_g[k] = 0.0f;
         __syncthreads();
-        // samples above this warp's last commit are skipped by the whole warp
-        const int jstart = max(0, hi - 1 - wl);
-        for (int j = jstart; j < cnt; ++j) {
-            const int idx = hi - 1 - j;
+        for (int j = 0; j < cnt; ++j) {
+            const int idx = s_idx[j];
+            if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
             float v[10];
 #pragma unroll
             for (int k = 0; k < 10; ++k) v[k] = 0.0f;
@@ -210,321 +202,6 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
             atomicAdd(dst + 2, make_float4(gs[8], gs[9], 0.0f, 0.0f));
         }
         __syncthreads();
-    }
-}
-
-__device__ __forceinline__ void sh_basis_all(float x, float y, float z, int degree, float bs[16]) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) bs[i] = 0.0f;
-    bs[0] = (float)0.28209479177387814;
-    if (degree < 1) return;
-    const float c1 = (float)0.4886025119029199;
-    bs[1] = -c1 * y;
-    bs[2] = c1 * z;
-    bs[3] = -c1 * x;
-    if (degree < 2) return;
-    const float xx = x * x, yy = y * y, zz = z * z;
-    bs[4] = (float)1.0925484305920792 * x * y;
-    bs[5] = (float)-1.0925484305920792 * y * z;
-    bs[6] = (float)0.31539156525252005 * (2.0f * zz - xx - yy);
-    bs[7] = (float)-1.0925484305920792 * x * z;
-    bs[8] = (float)0.5462742152960396 * (xx - yy);
-    if (degree < 3) return;
-    bs[9] = (float)-0.5900435899266435 * y * (3.0f * xx - yy);
-    bs[10] = (float)2.890611442640554 * x * y * z;
-    bs[11] = (float)-0.4570457994644658 * y * (4.0f * zz - xx - yy);
-    bs[12] = (float)0.3731763325901154 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-    bs[13] = (float)-0.4570457994644658 * x * (4.0f * zz - xx - yy);
-    bs[14] = (float)1.445305721320277 * z * (xx - yy);
-    bs[15] = (float)-0.5900435899266435 * x * (xx - 3.0f * yy);
-}
-
-// sh_basis_grad (sh.hpp:55-79) contracted with coef[k]: returns sum_k coef[k] * d basis_k / d dir.
-__device__ __forceinline__ void sh_dir_grad(float x, float y, float z, int degree, const float coef[16], float g[3]) {
-    g[0] = g[1] = g[2] = 0.0f;
-    if (degree < 1) return;
-    const float c1 = (float)0.4886025119029199;
-    g[1] += -c1 * coef[1];
-    g[2] += c1 * coef[2];
-    g[0] += -c1 * coef[3];
-    if (degree < 2) return;
-    const float xx = x * x, yy = y * y, zz = z * z;
-    const float C20 = (float)1.0925484305920792, C21 = (float)-1.0925484305920792, C22 = (float)0.31539156525252005,
-                C23 = (float)-1.0925484305920792, C24 = (float)0.5462742152960396;
-    g[0] += coef[4] * C20 * y;  g[1] += coef[4] * C20 * x;
-    g[1] += coef[5] * C21 * z;  g[2] += coef[5] * C21 * y;
-    g[0] += coef[6] * C22 * (-2.0f * x); g[1] += coef[6] * C22 * (-2.0f * y); g[2] += coef[6] * C22 * (4.0f * z);
-    g[0] += coef[7] * C23 * z;  g[2] += coef[7] * C23 * x;
-    g[0] += coef[8] * C24 * (2.0f * x); g[1] += coef[8] * C24 * (-2.0f * y);
-    if (degree < 3) return;
-    const float C30 = (float)-0.5900435899266435, C31 = (float)2.890611442640554, C32 = (float)-0.4570457994644658,
-                C33 = (float)0.3731763325901154, C34 = (float)-0.4570457994644658, C35 = (float)1.445305721320277,
-                C36 = (float)-0.5900435899266435;
-    g[0] += coef[9] * C30 * (6.0f * x * y); g[1] += coef[9] * C30 * (3.0f * xx - 3.0f * yy);
-    g[0] += coef[10] * C31 * (y * z); g[1] += coef[10] * C31 * (x * z); g[2] += coef[10] * C31 * (x * y);
-    g[0] += coef[11] * C32 * (-2.0f * x * y); g[1] += coef[11] * C32 * (4.0f * zz - xx - 3.0f * yy);
-    g[2] += coef[11] * C32 * (8.0f * y * z);
-    g[0] += coef[12] * C33 * (-6.0f * x * z); g[1] += coef[12] * C33 * (-6.0f * y * z);
-    g[2] += coef[12] * C33 * (6.0f * zz - 3.0f * xx - 3.0f * yy);
-    g[0] += coef[13] * C34 * (4.0f * zz - 3.0f * xx - yy); g[1] += coef[13] * C34 * (-2.0f * x * y);
-    g[2] += coef[13] * C34 * (8.0f * x * z);
-    g[0] += coef[14] * C35 * (2.0f * x * z); g[1] += coef[14] * C35 * (-2.0f * y * z); g[2] += coef[14] * C35 * (xx - yy);
-    g[0] += coef[15] * C36 * (3.0f * xx - 3.0f * yy); g[1] += coef[15] * C36 * (-6.0f * x * y);
-}
-
-// Per-Gaussian geometric chain (gradients.cpp:127-220).  Untouched Gaussians get exact zeros
-// (or nothing when accumulating).  The 2D accumulator is re-zeroed as it is consumed.
-template <bool VEC>
-__global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
-                                                   const ProjRec* __restrict__ rec, splat_param_grads out,
-                                                   int accumulate) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
-    const float4 g0 = grad2d[3 * (size_t)i], g1 = grad2d[3 * (size_t)i + 1], g2 = grad2d[3 * (size_t)i + 2];
-    const bool touched = g2.y > 0.0f;
-    if (!touched) {
-        if (!accumulate) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                out.d_centers[3 * (size_t)i + k] = 0.0f;
-                out.d_log_scales[3 * (size_t)i + k] = 0.0f;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) out.d_rotations[4 * (size_t)i + k] = 0.0f;
-            out.d_opacity_logits[i] = 0.0f;
-            if (VEC) {
-                float4* d4 = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)i);
-#pragma unroll
-                for (int k = 0; k < 12; ++k) d4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-                for (int k = 0; k < 48; ++k) out.d_sh[48 * (size_t)i + k] = 0.0f;
-            }
-            if (out.grad2d_accum) out.grad2d_accum[i] = 0.0f;
-            if (out.grad2d_count) out.grad2d_count[i] = 0;
-        }
-        return;
-    }
-    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    grad2d[3 * (size_t)i] = zero4;
-    grad2d[3 * (size_t)i + 1] = zero4;
-    grad2d[3 * (size_t)i + 2] = zero4;
-
-    const float dmx = g0.x, dmy = g0.y, dq00 = g0.z, dq01 = g0.w, dq11 = g1.x, dopac = g1.y;
-    const float dcol[3] = {g1.z, g1.w, g2.x};
-    const ProjRec pr = rec[i];
-    const float k0 = pr.r0.z, k1 = pr.r0.w, k2 = pr.r1.x, opacity = pr.r1.y;
-
-    // dV = -Q dQ Q  (conic = inverse(cov2d)), dQ symmetric with off-diagonal dq01
-    const float n00 = -(k0 * dq00 + k1 * dq01), n01 = -(k0 * dq01 + k1 * dq11);
-    const float n10 = -(k1 * dq00 + k2 * dq01), n11 = -(k1 * dq01 + k2 * dq11);
-    const float dV00 = n00 * k0 + n01 * k1, dV01 = n00 * k1 + n01 * k2;
-    const float dV10 = n10 * k0 + n11 * k1, dV11 = n10 * k1 + n11 * k2;
-
-    const float px = g.centers[3 * (size_t)i], py = g.centers[3 * (size_t)i + 1], pz = g.centers[3 * (size_t)i + 2];
-    const float* R = cp.R;
-    const float pc0 = R[0] * px + R[1] * py + R[2] * pz + cp.t[0];
-    const float pc1 = R[3] * px + R[4] * py + R[5] * pz + cp.t[1];
-    const float z = R[6] * px + R[7] * py + R[8] * pz + cp.t[2];
-    const float iz = 1.0f / z, iz2 = iz * iz;
-    const float J00 = cp.fx * iz, J02 = -cp.fx * pc0 * iz2, J11 = cp.fy * iz, J12 = -cp.fy * pc1 * iz2;
-    float M[6];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        M[c] = J00 * R[c] + J02 * R[6 + c];
-        M[3 + c] = J11 * R[3 + c] + J12 * R[6 + c];
-    }
-    // covariance
-    float qw = g.rotations[4 * (size_t)i], qx = g.rotations[4 * (size_t)i + 1], qy = g.rotations[4 * (size_t)i + 2],
-          qz = g.rotations[4 * (size_t)i + 3];
-    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-    float qh[4];
-    if (!(qn > 0.0f)) {
-        qh[0] = 1.0f; qh[1] = qh[2] = qh[3] = 0.0f;
-    } else {
-        qh[0] = qw / qn; qh[1] = qx / qn; qh[2] = qy / qn; qh[3] = qz / qn;
-    }
-    const float w_ = qh[0], x_ = qh[1], y_ = qh[2], z_ = qh[3];
-    float Rq[9];
-    Rq[0] = 1.0f - 2.0f * (y_ * y_ + z_ * z_);
-    Rq[1] = 2.0f * (x_ * y_ - w_ * z_);
-    Rq[2] = 2.0f * (x_ * z_ + w_ * y_);
-    Rq[3] = 2.0f * (x_ * y_ + w_ * z_);
-    Rq[4] = 1.0f - 2.0f * (x_ * x_ + z_ * z_);
-    Rq[5] = 2.0f * (y_ * z_ - w_ * x_);
-    Rq[6] = 2.0f * (x_ * z_ - w_ * y_);
-    Rq[7] = 2.0f * (y_ * z_ + w_ * x_);
-    Rq[8] = 1.0f - 2.0f * (x_ * x_ + y_ * y_);
-    const float sc[3] = {splat_expf(g.log_scales[3 * (size_t)i]), splat_expf(g.log_scales[3 * (size_t)i + 1]),
-                         splat_expf(g.log_scales[3 * (size_t)i + 2])};
-    float M3[9], C[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) M3[r * 3 + c] = Rq[r * 3 + c] * sc[c];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            C[r * 3 + c] = M3[r * 3] * M3[c * 3] + M3[r * 3 + 1] * M3[c * 3 + 1] + M3[r * 3 + 2] * M3[c * 3 + 2];
-    // d_cov3d = M^T dV M
-    float D[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const float p0 = M[r] * dV00 + M[3 + r] * dV10;
-        const float p1 = M[r] * dV01 + M[3 + r] * dV11;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) D[r * 3 + c] = p0 * M[c] + p1 * M[3 + c];
-    }
-    // dM = 2 dV M cov3d ; dJ = dM R^T
-    float E[6], F[6];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        E[c] = 2.0f * (dV00 * M[c] + dV01 * M[3 + c]);
-        E[3 + c] = 2.0f * (dV10 * M[c] + dV11 * M[3 + c]);
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            F[r * 3 + c] = E[r * 3] * C[c] + E[r * 3 + 1] * C[3 + c] + E[r * 3 + 2] * C[6 + c];
-    float dJ[6];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            dJ[r * 3 + c] = F[r * 3] * R[c * 3] + F[r * 3 + 1] * R[c * 3 + 1] + F[r * 3 + 2] * R[c * 3 + 2];
-    float dp0 = dJ[2] * (-cp.fx * iz2);
-    float dp1 = dJ[5] * (-cp.fy * iz2);
-    float dp2 = dJ[0] * (-cp.fx * iz2) + dJ[2] * (2.0f * cp.fx * pc0 * iz2 * iz) + dJ[4] * (-cp.fy * iz2) +
-                dJ[5] * (2.0f * cp.fy * pc1 * iz2 * iz);
-    dp0 += dmx * cp.fx * iz;
-    dp1 += dmy * cp.fy * iz;
-    dp2 += dmx * (-cp.fx * pc0 * iz2) + dmy * (-cp.fy * pc1 * iz2);
-    float dc0 = R[0] * dp0 + R[3] * dp1 + R[6] * dp2;
-    float dc1 = R[1] * dp0 + R[4] * dp1 + R[7] * dp2;
-    float dc2 = R[2] * dp0 + R[5] * dp1 + R[8] * dp2;
-    // scales / rotation: dM3 = 2 D M3, dR = dM3 diag(s)
-    float G[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            G[r * 3 + c] = 2.0f * (D[r * 3] * M3[c] + D[r * 3 + 1] * M3[3 + c] + D[r * 3 + 2] * M3[6 + c]);
-    float dls[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) dls[k] = (Rq[k] * G[k] + Rq[3 + k] * G[3 + k] + Rq[6 + k] * G[6 + k]) * sc[k];
-    float H[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) H[r * 3 + c] = G[r * 3 + c] * sc[c];
-    // d q_hat = sum(dR .* dR/dq_k), quat_rotation_jacobians (gradients.cpp:25-41)
-    float dqh[4];
-    dqh[0] = 2.0f * (-z_ * H[1] + y_ * H[2] + z_ * H[3] - x_ * H[5] - y_ * H[6] + x_ * H[7]);
-    dqh[1] = 2.0f * (y_ * H[1] + z_ * H[2] + y_ * H[3] - 2.0f * x_ * H[4] - w_ * H[5] + z_ * H[6] + w_ * H[7] -
-                     2.0f * x_ * H[8]);
-    dqh[2] = 2.0f * (-2.0f * y_ * H[0] + x_ * H[1] + w_ * H[2] + x_ * H[3] + z_ * H[5] - w_ * H[6] + z_ * H[7] -
-                     2.0f * y_ * H[8]);
-    dqh[3] = 2.0f * (-2.0f * z_ * H[0] - w_ * H[1] + x_ * H[2] + w_ * H[3] - 2.0f * z_ * H[4] + y_ * H[5] +
-                     x_ * H[6] + y_ * H[7]);
-    float drot[4] = {0.f, 0.f, 0.f, 0.f};
-    if (qn > 1e-12f) {
-        const float qd = qh[0] * dqh[0] + qh[1] * dqh[1] + qh[2] * dqh[2] + qh[3] * dqh[3];
-        const float iq = 1.0f / qn;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) drot[k] = (dqh[k] - qh[k] * qd) * iq;
-    }
-    const float dlogit = dopac * opacity * (1.0f - opacity);
-    // SH (gradients.cpp:192-219)
-    const float u0 = px - cp.center[0], u1 = py - cp.center[1], u2 = pz - cp.center[2];
-    const float len = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
-    const float il = 1.0f / len;
-    const float d0 = u0 * il, d1 = u1 * il, d2 = u2 * il;
-    const int deg = g.sh_degree;
-    const int nco = (deg + 1) * (deg + 1);
-    float bs[16];
-    sh_basis_all(d0, d1, d2, deg, bs);
-    float shv[48];
-    if (VEC) {
-        const float4* s4 = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)i);
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            const float4 vv = s4[k];
-            shv[4 * k] = vv.x; shv[4 * k + 1] = vv.y; shv[4 * k + 2] = vv.z; shv[4 * k + 3] = vv.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < 48; ++k) shv[k] = g.sh[48 * (size_t)i + k];
-    }
-    float rgb[3] = {0.5f, 0.5f, 0.5f};
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if (k < nco) {
-            rgb[0] += bs[k] * shv[3 * k];
-            rgb[1] += bs[k] * shv[3 * k + 1];
-            rgb[2] += bs[k] * shv[3 * k + 2];
-        }
-    float dc[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) dc[c] = rgb[c] < 0.0f ? 0.0f : dcol[c];
-    float dsh[48];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const bool on = k < nco;
-        dsh[3 * k] = on ? bs[k] * dc[0] : 0.0f;
-        dsh[3 * k + 1] = on ? bs[k] * dc[1] : 0.0f;
-        dsh[3 * k + 2] = on ? bs[k] * dc[2] : 0.0f;
-    }
-    if (deg > 0) {
-        float coef[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            coef[k] = (k >= 1 && k < nco) ? dc[0] * shv[3 * k] + dc[1] * shv[3 * k + 1] + dc[2] * shv[3 * k + 2] : 0.0f;
-        float gd[3];
-        sh_dir_grad(d0, d1, d2, deg, coef, gd);
-        const float dd = d0 * gd[0] + d1 * gd[1] + d2 * gd[2];
-        dc0 += (gd[0] - d0 * dd) * il;
-        dc1 += (gd[1] - d1 * dd) * il;
-        dc2 += (gd[2] - d2 * dd) * il;
-    }
-    const float dmn = sqrtf(dmx * dmx + dmy * dmy);
-    const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i;
-    if (accumulate) {
-        out.d_centers[i3] += dc0; out.d_centers[i3 + 1] += dc1; out.d_centers[i3 + 2] += dc2;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) out.d_log_scales[i3 + k] += dls[k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) out.d_rotations[i4 + k] += drot[k];
-        out.d_opacity_logits[i] += dlogit;
-        if (VEC) {
-            float4* d4 = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)i);
-#pragma unroll
-            for (int k = 0; k < 12; ++k) {
-                float4 o = d4[k];
-                o.x += dsh[4 * k]; o.y += dsh[4 * k + 1]; o.z += dsh[4 * k + 2]; o.w += dsh[4 * k + 3];
-                d4[k] = o;
-            }
-        } else {
-            for (int k = 0; k < 48; ++k) out.d_sh[48 * (size_t)i + k] += dsh[k];
-        }
-        if (out.grad2d_accum) out.grad2d_accum[i] += dmn;
-        if (out.grad2d_count) out.grad2d_count[i] += 1;
-    } else {
-        out.d_centers[i3] = dc0; out.d_centers[i3 + 1] = dc1; out.d_centers[i3 + 2] = dc2;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) out.d_log_scales[i3 + k] = dls[k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) out.d_rotations[i4 + k] = drot[k];
-        out.d_opacity_logits[i] = dlogit;
-        if (VEC) {
-            float4* d4 = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)i);
-#pragma unroll
-            for (int k = 0; k < 12; ++k) d4[k] = make_float4(dsh[4 * k], dsh[4 * k + 1], dsh[4 * k + 2], dsh[4 * k + 3]);
-        } else {
-            for (int k = 0; k < 48; ++k) out.d_sh[48 * (size_t)i + k] = dsh[k];
-        }
-        if (out.grad2d_accum) out.grad2d_accum[i] = dmn;
-        if (out.grad2d_count) out.grad2d_count[i] = 1;
     }
 }
 
@@ -633,26 +310,6 @@ cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, floa
         LaunchScope ls_(lc, "loss_reduce");
         loss_reduce_kernel<<<1, 256, 0, lc.stream>>>(partials, n, inv_n, loss);
     }
-    lc.count++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d, const ProjRec* rec,
-                         const splat_param_grads& out, int accumulate) {
-    if (g.n == 0) return cudaSuccess;
-    const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
-    if (vec)
-        {
-            LaunchScope ls_(lc, "chain");
-            chain_kernel<true><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
-                                                                       out, accumulate);
-        }
-    else
-        {
-            LaunchScope ls_(lc, "chain");
-            chain_kernel<false><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
-                                                                        rec, out, accumulate);
-        }
     lc.count++;
     return cudaGetLastError();
 }

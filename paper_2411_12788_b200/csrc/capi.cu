@@ -117,7 +117,7 @@ struct splat_ctx {
     LaunchCtx lc;
     std::string err;
     // per-Gaussian
-    DevBuf rec, aux, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
+    DevBuf rec, aux, depth, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
     DevBuf pair_tile[2], pair_gauss[2];
     // misc
@@ -241,6 +241,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         CK(ctx->vals[k].ensure(nn * 4), "alloc vals");
     }
     CK(ctx->tile_counts.ensure(nn * 4), "alloc counts");
+    CK(ctx->depth.ensure(nn * 4), "alloc depth");
     CK(ctx->counts_sorted.ensure(nn * 4), "alloc counts");
     CK(ctx->offsets.ensure((nn + 1) * 4), "alloc offsets");
     CK(ctx->counters.ensure(64), "alloc counters");
@@ -266,7 +267,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* keys = ctx->keys[0].as<uint32_t>();
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
-                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters),
+                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>()),
            "preprocess");
         bool alt = false;
         CK(radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), (uint64_t)n, 0,
@@ -623,11 +624,12 @@ int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* d
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     ProjRec* h = new ProjRec[n];
     uint32_t* counts = new uint32_t[n];
-    uint32_t* keys = new uint32_t[n];
+    float* depths = new float[n];
     cudaError_t e = cudaMemcpy(h, ctx->rec.p, sizeof(ProjRec) * n, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(depths, ctx->depth.p, 4 * (size_t)n, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(counts, ctx->tile_counts.p, 4 * (size_t)n, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
-        delete[] h; delete[] counts; delete[] keys;
+        delete[] h; delete[] counts; delete[] depths;
         return cuda_err(ctx, e, "project debug");
     }
     for (int i = 0; i < n; ++i) {
@@ -642,7 +644,7 @@ int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* d
             rect[4 * i + 3] = alive ? (int32_t)(ry >> 16) : 0;
         }
         if (survivor) survivor[i] = alive ? 1 : 0;
-        if (depth) depth[i] = alive ? h[i].r2.w : 0.0f;
+        if (depth) depth[i] = alive ? depths[i] : 0.0f;
         if (mean2d) { mean2d[2 * i] = alive ? h[i].r0.x : 0.f; mean2d[2 * i + 1] = alive ? h[i].r0.y : 0.f; }
         if (conic) {
             conic[3 * i] = alive ? h[i].r0.z : 0.f;
@@ -653,7 +655,7 @@ int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* d
         if (opacity) opacity[i] = alive ? h[i].r1.y : 0.f;
         if (radius) radius[i] = 0;  // radius is not stored on device; rect carries the footprint
     }
-    delete[] h; delete[] counts; delete[] keys;
+    delete[] h; delete[] counts; delete[] depths;
     return SPLAT_OK;
 }
 

@@ -1,0 +1,381 @@
+// chain.cu — per-Gaussian 2D -> 3D gradient chain (K10, gradients.cpp:127-220).
+//
+// Compiled with --fmad=false and written in the reference's operation order (the order fixed by
+// oracle/compat/Eigen/Dense: halving reductions, left-associative products), so that for equal
+// 2D inputs (d_mean2d, d_conic, d_opacity, d_colour) it produces the reference's float results bit
+// for bit.  The only GPU-vs-reference gradient difference left is then the summation order of the
+// per-pixel contributions in blend_backward.  One thread per Gaussian; ~1 kFLOP each (3% of a
+// step), so exactness here is free.
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace splat_b200 {
+
+namespace {
+
+__device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return a0 * b0 + (a1 * b1 + a2 * b2);
+}
+
+// sh_basis (sh.hpp:27-51)
+__device__ __forceinline__ void sh_basis_all(float x, float y, float z, int degree, float b[16]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) b[i] = 0.0f;
+    b[0] = (float)0.28209479177387814;
+    if (degree < 1) return;
+    const float c1 = (float)0.4886025119029199;
+    b[1] = -c1 * y;
+    b[2] = c1 * z;
+    b[3] = -c1 * x;
+    if (degree < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    b[4] = (float)1.0925484305920792 * x * y;
+    b[5] = (float)-1.0925484305920792 * y * z;
+    b[6] = (float)0.31539156525252005 * (2.0f * zz - xx - yy);
+    b[7] = (float)-1.0925484305920792 * x * z;
+    b[8] = (float)0.5462742152960396 * (xx - yy);
+    if (degree < 3) return;
+    b[9] = (float)-0.5900435899266435 * y * (3.0f * xx - yy);
+    b[10] = (float)2.890611442640554 * x * y * z;
+    b[11] = (float)-0.4570457994644658 * y * (4.0f * zz - xx - yy);
+    b[12] = (float)0.3731763325901154 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = (float)-0.4570457994644658 * x * (4.0f * zz - xx - yy);
+    b[14] = (float)1.445305721320277 * z * (xx - yy);
+    b[15] = (float)-0.5900435899266435 * x * (xx - 3.0f * yy);
+}
+
+// sh_basis_grad (sh.hpp:55-79): g[k] = d basis_k / d dir
+__device__ __forceinline__ void sh_basis_grad_all(float x, float y, float z, int degree, float g[16][3]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) g[k][0] = g[k][1] = g[k][2] = 0.0f;
+    if (degree < 1) return;
+    const float c1 = (float)0.4886025119029199;
+    g[1][1] = -c1;
+    g[2][2] = c1;
+    g[3][0] = -c1;
+    if (degree < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+#define SET3(k, C, a, b, c) { const float cc_ = (float)(C); g[k][0] = cc_ * (a); g[k][1] = cc_ * (b); g[k][2] = cc_ * (c); }
+    SET3(4, 1.0925484305920792, y, x, 0.0f)
+    SET3(5, -1.0925484305920792, 0.0f, z, y)
+    SET3(6, 0.31539156525252005, -2.0f * x, -2.0f * y, 4.0f * z)
+    SET3(7, -1.0925484305920792, z, 0.0f, x)
+    SET3(8, 0.5462742152960396, 2.0f * x, -2.0f * y, 0.0f)
+    if (degree < 3) return;
+    SET3(9, -0.5900435899266435, 6.0f * x * y, 3.0f * xx - 3.0f * yy, 0.0f)
+    SET3(10, 2.890611442640554, y * z, x * z, x * y)
+    SET3(11, -0.4570457994644658, -2.0f * x * y, 4.0f * zz - xx - 3.0f * yy, 8.0f * y * z)
+    SET3(12, 0.3731763325901154, -6.0f * x * z, -6.0f * y * z, 6.0f * zz - 3.0f * xx - 3.0f * yy)
+    SET3(13, -0.4570457994644658, 4.0f * zz - 3.0f * xx - yy, -2.0f * x * y, 8.0f * x * z)
+    SET3(14, 1.445305721320277, 2.0f * x * z, -2.0f * y * z, xx - yy)
+    SET3(15, -0.5900435899266435, 3.0f * xx - 3.0f * yy, -6.0f * x * y, 0.0f)
+#undef SET3
+}
+
+__device__ __forceinline__ void normalized_quat(float w, float x, float y, float z, float q[4]) {
+    const float n = sqrtf((w * w + x * x) + (y * y + z * z));
+    if (!(n > 0.0f)) {
+        q[0] = 1.0f; q[1] = q[2] = q[3] = 0.0f;
+        return;
+    }
+    q[0] = w / n; q[1] = x / n; q[2] = y / n; q[3] = z / n;
+}
+
+__device__ __forceinline__ void rotation_from_quat(const float qr[4], float r[9]) {
+    float q[4];
+    normalized_quat(qr[0], qr[1], qr[2], qr[3], q);
+    const float w = q[0], x = q[1], y = q[2], z = q[3];
+    r[0] = 1.0f - 2.0f * (y * y + z * z);
+    r[1] = 2.0f * (x * y - w * z);
+    r[2] = 2.0f * (x * z + w * y);
+    r[3] = 2.0f * (x * y + w * z);
+    r[4] = 1.0f - 2.0f * (x * x + z * z);
+    r[5] = 2.0f * (y * z - w * x);
+    r[6] = 2.0f * (x * z - w * y);
+    r[7] = 2.0f * (y * z + w * x);
+    r[8] = 1.0f - 2.0f * (x * x + y * y);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
+                                                   const ProjRec* __restrict__ rec, splat_param_grads out,
+                                                   int accumulate) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const float4 g0 = grad2d[3 * (size_t)i], g1 = grad2d[3 * (size_t)i + 1], g2 = grad2d[3 * (size_t)i + 2];
+    const bool touched = g2.y > 0.0f;
+    const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i, i48 = 48 * (size_t)i;
+    if (!touched) {
+        if (!accumulate) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                out.d_centers[i3 + k] = 0.0f;
+                out.d_log_scales[i3 + k] = 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out.d_rotations[i4 + k] = 0.0f;
+            out.d_opacity_logits[i] = 0.0f;
+            if (VEC) {
+                float4* d4 = reinterpret_cast<float4*>(out.d_sh + i48);
+#pragma unroll
+                for (int k = 0; k < 12; ++k) d4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                for (int k = 0; k < 48; ++k) out.d_sh[i48 + k] = 0.0f;
+            }
+            if (out.grad2d_accum) out.grad2d_accum[i] = 0.0f;
+            if (out.grad2d_count) out.grad2d_count[i] = 0;
+        }
+        return;
+    }
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    grad2d[3 * (size_t)i] = zero4;
+    grad2d[3 * (size_t)i + 1] = zero4;
+    grad2d[3 * (size_t)i + 2] = zero4;
+
+    const float dm0 = g0.x, dm1 = g0.y;
+    const float dQ[4] = {g0.z, g0.w, g0.w, g1.x};  // row-major (00, 01, 10, 11); 01 == 10
+    const float dopac = g1.y;
+    const float dcol[3] = {g1.z, g1.w, g2.x};
+    const ProjRec pr = rec[i];
+    const float k0 = pr.r0.z, k1 = pr.r0.w, k2 = pr.r1.x, opacity = pr.r1.y;
+
+    const float gaccum = sqrtf(dm0 * dm0 + dm1 * dm1);
+    // dV = (-Q) dQ Q
+    const float Qn[4] = {-k0, -k1, -k1, -k2};
+    const float Q[4] = {k0, k1, k1, k2};
+    float N[4], dV[4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) N[r * 2 + c] = Qn[r * 2] * dQ[c] + Qn[r * 2 + 1] * dQ[2 + c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) dV[r * 2 + c] = N[r * 2] * Q[c] + N[r * 2 + 1] * Q[2 + c];
+
+    const float p0 = g.centers[i3], p1 = g.centers[i3 + 1], p2 = g.centers[i3 + 2];
+    const float* Rc = cp.R;
+    const float fx = cp.fx, fy = cp.fy;
+    const float pc0 = dot3(Rc[0], Rc[1], Rc[2], p0, p1, p2) + cp.t[0];
+    const float pc1 = dot3(Rc[3], Rc[4], Rc[5], p0, p1, p2) + cp.t[1];
+    const float z = dot3(Rc[6], Rc[7], Rc[8], p0, p1, p2) + cp.t[2];
+    const float J[6] = {fx / z, 0.0f, -fx * pc0 / (z * z), 0.0f, fy / z, -fy * pc1 / (z * z)};
+    float Mm[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Mm[r * 3 + c] = dot3(J[r * 3], J[r * 3 + 1], J[r * 3 + 2], Rc[c], Rc[3 + c], Rc[6 + c]);
+    // covariance_from_params
+    const float qraw[4] = {g.rotations[i4], g.rotations[i4 + 1], g.rotations[i4 + 2], g.rotations[i4 + 3]};
+    const float ls[3] = {g.log_scales[i3], g.log_scales[i3 + 1], g.log_scales[i3 + 2]};
+    float Rq0[9];
+    rotation_from_quat(qraw, Rq0);
+    const float sc[3] = {splat_expf(ls[0]), splat_expf(ls[1]), splat_expf(ls[2])};
+    float m3[9], C[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m3[r * 3 + c] = Rq0[r * 3 + c] * sc[c];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = r; c < 3; ++c) {
+            const float v = dot3(m3[r * 3], m3[r * 3 + 1], m3[r * 3 + 2], m3[c * 3], m3[c * 3 + 1], m3[c * 3 + 2]);
+            C[r * 3 + c] = v;
+            C[c * 3 + r] = v;
+        }
+    // d_cov3d = M^T dV M
+    float P[6], D[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) P[r * 2 + c] = Mm[0 * 3 + r] * dV[0 * 2 + c] + Mm[1 * 3 + r] * dV[1 * 2 + c];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) D[r * 3 + c] = P[r * 2] * Mm[0 * 3 + c] + P[r * 2 + 1] * Mm[1 * 3 + c];
+    // dM = 2 dV M cov3d ; dJ = dM R^T
+    float dV2[4], E[6], F[6], dJ[6];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dV2[k] = 2.0f * dV[k];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) E[r * 3 + c] = dV2[r * 2] * Mm[0 * 3 + c] + dV2[r * 2 + 1] * Mm[1 * 3 + c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[r * 3 + c] = dot3(E[r * 3], E[r * 3 + 1], E[r * 3 + 2], C[c], C[3 + c], C[6 + c]);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            dJ[r * 3 + c] = dot3(F[r * 3], F[r * 3 + 1], F[r * 3 + 2], Rc[c * 3], Rc[c * 3 + 1], Rc[c * 3 + 2]);
+    float dp[3] = {0.0f, 0.0f, 0.0f};
+    dp[0] += dJ[2] * (-fx / (z * z));
+    dp[1] += dJ[5] * (-fy / (z * z));
+    dp[2] += dJ[0] * (-fx / (z * z)) + dJ[2] * (2.0f * fx * pc0 / (z * z * z)) + dJ[4] * (-fy / (z * z)) +
+             dJ[5] * (2.0f * fy * pc1 / (z * z * z));
+    dp[0] += dm0 * fx / z;
+    dp[1] += dm1 * fy / z;
+    dp[2] += dm0 * (-fx * pc0 / (z * z)) + dm1 * (-fy * pc1 / (z * z));
+    float dcen[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dcen[k] = dot3(Rc[k], Rc[3 + k], Rc[6 + k], dp[0], dp[1], dp[2]);
+    // M3 = R(q_hat) diag(s); note rotation_from_quat normalises q_hat again (gradients.cpp:173-174)
+    float qh[4], Rq[9], M3[9], D2[9], G[9], H[9];
+    normalized_quat(qraw[0], qraw[1], qraw[2], qraw[3], qh);
+    rotation_from_quat(qh, Rq);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) M3[r * 3 + c] = Rq[r * 3 + c] * sc[c];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) D2[k] = 2.0f * D[k];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            G[r * 3 + c] = dot3(D2[r * 3], D2[r * 3 + 1], D2[r * 3 + 2], M3[c], M3[3 + c], M3[6 + c]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) H[r * 3 + c] = G[r * 3 + c] * sc[c];
+    float dls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dls[k] = dot3(Rq[k], Rq[3 + k], Rq[6 + k], G[k], G[3 + k], G[6 + k]) * sc[k];
+    const float w_ = qh[0], x_ = qh[1], y_ = qh[2], z_ = qh[3];
+    const float dRq[4][9] = {{0.0f, -z_, y_, z_, 0.0f, -x_, -y_, x_, 0.0f},
+                             {0.0f, y_, z_, y_, -2.0f * x_, -w_, z_, w_, -2.0f * x_},
+                             {-2.0f * y_, x_, w_, x_, 0.0f, z_, -w_, z_, -2.0f * y_},
+                             {-2.0f * z_, -w_, x_, w_, -2.0f * z_, y_, x_, y_, 0.0f}};
+    float dqh[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float e[9];  // column-major element order of H .* (2 dR/dq_k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int r = 0; r < 3; ++r) e[c * 3 + r] = H[r * 3 + c] * (dRq[k][r * 3 + c] * 2.0f);
+        dqh[k] = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + (e[7] + e[8])));
+    }
+    float drot[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float qn = sqrtf((qraw[0] * qraw[0] + qraw[1] * qraw[1]) + (qraw[2] * qraw[2] + qraw[3] * qraw[3]));
+    const bool rot_ok = qn > 1e-12f;
+    if (rot_ok) {
+        const float qd = (qh[0] * dqh[0] + qh[1] * dqh[1]) + (qh[2] * dqh[2] + qh[3] * dqh[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) drot[k] = (dqh[k] - qh[k] * qd) / qn;
+    }
+    const float dlogit = dopac * opacity * (1.0f - opacity);
+    // SH (gradients.cpp:192-219)
+    const float u0 = p0 - cp.center[0], u1 = p1 - cp.center[1], u2 = p2 - cp.center[2];
+    const float len = sqrtf(dot3(u0, u1, u2, u0, u1, u2));
+    const float dir0 = u0 / len, dir1 = u1 / len, dir2 = u2 / len;
+    const int deg = g.sh_degree;
+    const int nco = (deg + 1) * (deg + 1);
+    float basis[16];
+    sh_basis_all(dir0, dir1, dir2, deg, basis);
+    float shv[48];
+    if (VEC) {
+        const float4* s4 = reinterpret_cast<const float4*>(g.sh + i48);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            const float4 vv = s4[k];
+            shv[4 * k] = vv.x; shv[4 * k + 1] = vv.y; shv[4 * k + 2] = vv.z; shv[4 * k + 3] = vv.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 48; ++k) shv[k] = g.sh[i48 + k];
+    }
+    float rgb[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (k < nco) {
+            rgb[0] = rgb[0] + basis[k] * shv[3 * k];
+            rgb[1] = rgb[1] + basis[k] * shv[3 * k + 1];
+            rgb[2] = rgb[2] + basis[k] * shv[3 * k + 2];
+        }
+    float dc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dc[c] = rgb[c] < 0.0f ? 0.0f : dcol[c];
+    float dsh[48];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const bool on = k < nco;
+        dsh[3 * k] = on ? basis[k] * dc[0] : 0.0f;
+        dsh[3 * k + 1] = on ? basis[k] * dc[1] : 0.0f;
+        dsh[3 * k + 2] = on ? basis[k] * dc[2] : 0.0f;
+    }
+    if (deg > 0) {
+        float gb[16][3];
+        sh_basis_grad_all(dir0, dir1, dir2, deg, gb);
+        float dd[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+            if (k < nco) {
+                float coef = 0.0f;
+                coef = coef + dc[0] * shv[3 * k];
+                coef = coef + dc[1] * shv[3 * k + 1];
+                coef = coef + dc[2] * shv[3 * k + 2];
+                dd[0] = dd[0] + gb[k][0] * coef;
+                dd[1] = dd[1] + gb[k][1] * coef;
+                dd[2] = dd[2] + gb[k][2] * coef;
+            }
+        }
+        const float ddot = dot3(dir0, dir1, dir2, dd[0], dd[1], dd[2]);
+        dcen[0] = dcen[0] + (dd[0] - dir0 * ddot) / len;
+        dcen[1] = dcen[1] + (dd[1] - dir1 * ddot) / len;
+        dcen[2] = dcen[2] + (dd[2] - dir2 * ddot) / len;
+    }
+    // write (fresh ParamGrads: 0 + x; accumulate: existing + x, ParamGrads::add)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float bc = accumulate ? out.d_centers[i3 + k] : 0.0f;
+        const float bs = accumulate ? out.d_log_scales[i3 + k] : 0.0f;
+        out.d_centers[i3 + k] = bc + dcen[k];
+        out.d_log_scales[i3 + k] = bs + dls[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float br = accumulate ? out.d_rotations[i4 + k] : 0.0f;
+        out.d_rotations[i4 + k] = br + drot[k];
+    }
+    out.d_opacity_logits[i] = (accumulate ? out.d_opacity_logits[i] : 0.0f) + dlogit;
+    if (VEC) {
+        float4* d4 = reinterpret_cast<float4*>(out.d_sh + i48);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            float4 o = accumulate ? d4[k] : zero4;
+            o.x = o.x + dsh[4 * k]; o.y = o.y + dsh[4 * k + 1]; o.z = o.z + dsh[4 * k + 2]; o.w = o.w + dsh[4 * k + 3];
+            d4[k] = o;
+        }
+    } else {
+        for (int k = 0; k < 48; ++k) out.d_sh[i48 + k] = (accumulate ? out.d_sh[i48 + k] : 0.0f) + dsh[k];
+    }
+    if (out.grad2d_accum) out.grad2d_accum[i] = (accumulate ? out.grad2d_accum[i] : 0.0f) + gaccum;
+    if (out.grad2d_count) out.grad2d_count[i] = (accumulate ? out.grad2d_count[i] : 0) + 1;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d, const ProjRec* rec,
+                         const splat_param_grads& out, int accumulate) {
+    if (g.n == 0) return cudaSuccess;
+    const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
+    LaunchScope ls(lc, "chain");
+    if (vec)
+        chain_kernel<true><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
+                                                                       out, accumulate);
+    else
+        chain_kernel<false><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
+                                                                        rec, out, accumulate);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+}  // namespace splat_b200

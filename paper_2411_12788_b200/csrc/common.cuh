@@ -84,10 +84,90 @@ __device__ __forceinline__ bool gate_sample(const float4& r0, const float4& r1, 
     return true;
 }
 
+// Exactness-preserving block cull.  The Gaussian can pass the alpha gate somewhere in the pixel
+// block [bx0, bx1) x [by0, by1) only if (a) its pixel rect meets the block and (b) the maximum of
+// power = -q(dx, dy) / 2 over the block's pixel centres reaches cut = ln(cmin / opacity) - 1e-3
+// (r2.w, written by preprocess; -inf in exact mode).  (b) bounds the discrete maximum by the
+// continuous one over the box of pixel centres: q is a positive-definite quadratic, so its
+// minimum over a box is 0 when the box holds the origin and otherwise lies on an edge, where it
+// is a clamped 1-D vertex.  The 1e-3 margin in the exponent dwarfs every rounding involved (q is
+// evaluated to ~1e-6 relative, splat_expf to 1 ulp), so a culled sample would have been skipped
+// by the per-pixel gate anyway: the committed set, and every output bit, are unchanged.
+__device__ __forceinline__ bool may_contribute(const float4& r0, const float4& r1, float cut, int bx0, int bx1,
+                                               int by0, int by1) {
+    const int X0 = max(range_lo(r1.z), bx0), X1 = min(range_hi(r1.z), bx1);
+    const int Y0 = max(range_lo(r1.w), by0), Y1 = min(range_hi(r1.w), by1);
+    if (X0 >= X1 || Y0 >= Y1) return false;
+    if (!(cut > -INFINITY)) return true;
+    // dx = mean.x - (px + 0.5) over px in [X0, X1 - 1]
+    const float dxl = r0.x - ((float)X1 - 0.5f), dxh = r0.x - ((float)X0 + 0.5f);
+    const float dyl = r0.y - ((float)Y1 - 0.5f), dyh = r0.y - ((float)Y0 + 0.5f);
+    float qmin = 0.0f;
+    const bool inside = dxl <= 0.0f && dxh >= 0.0f && dyl <= 0.0f && dyh >= 0.0f;
+    if (!inside) {
+        const float a = r0.z, b = r0.w, c = r1.x;
+        // q minus a rounding bound proportional to the magnitudes of its terms: the per-pixel
+        // gate evaluates the same quadratic in another order, and for elongated Gaussians the
+        // terms cancel (|terms| >> q), so the cull must not trust q beyond ~1e-5 of sum |terms|.
+        auto q_lo = [&](float dx, float dy) {
+            const float t0 = a * dx * dx, t1 = 2.0f * b * dx * dy, t2 = c * dy * dy;
+            return (t0 + t1 + t2) - 1e-5f * (t0 + fabsf(t1) + t2);
+        };
+        const float ia = 1.0f / a, ic = 1.0f / c;
+        const float y_at_xl = fminf(fmaxf(-b * dxl * ic, dyl), dyh);
+        const float y_at_xh = fminf(fmaxf(-b * dxh * ic, dyl), dyh);
+        const float x_at_yl = fminf(fmaxf(-b * dyl * ia, dxl), dxh);
+        const float x_at_yh = fminf(fmaxf(-b * dyh * ia, dxl), dxh);
+        qmin = fminf(fminf(q_lo(dxl, y_at_xl), q_lo(dxh, y_at_xh)), fminf(q_lo(x_at_yl, dyl), q_lo(x_at_yh, dyh)));
+    }
+    return -0.5f * qmin >= cut;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// Stage one batch of list entries [idx_of(0), ...) in shared memory, keeping only Gaussians that
+// pass the exact block cull (common.cuh may_contribute); order is preserved by a ballot/prefix
+// compaction.  Returns the number of staged entries.  s_idx keeps each entry's absolute position
+// in the sorted pair array (the "list position" of the reference).
+template <typename IdxFn>
+__device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32_t* __restrict__ pair_gauss,
+                                           const ProjRec* __restrict__ rec, int bx0, int bx1, int by0, int by1,
+                                           float4* s_r0, float4* s_r1, float4* s_r2, uint32_t* s_gid, int* s_idx,
+                                           int* s_wcnt) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    bool keep = false;
+    ProjRec rr;
+    uint32_t gid = 0;
+    int idx = 0;
+    if (tid < count) {
+        idx = idx_of(tid);
+        gid = pair_gauss[idx];
+        rr = rec[gid];
+        keep = may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_wcnt[warp] = __popc(m);
+    __syncthreads();
+    int off = 0, total = 0;
+    for (int w = 0; w < nwarps; ++w) {
+        const int c = s_wcnt[w];
+        off += w < warp ? c : 0;
+        total += c;
+    }
+    if (keep) {
+        const int pos = off + __popc(m & lanemask_lt());
+        s_r0[pos] = rr.r0;
+        s_r1[pos] = rr.r1;
+        s_r2[pos] = rr.r2;
+        s_gid[pos] = gid;
+        s_idx[pos] = idx;
+    }
+    __syncthreads();
+    return total;
 }
 
 }  // namespace splat_b200

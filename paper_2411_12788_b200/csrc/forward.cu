@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                                                         ProjRec* __restrict__ rec, AuxRec* __restrict__ aux,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ tile_counts,
-                                                        uint32_t* __restrict__ n_surv) {
+                                                        uint32_t* __restrict__ n_surv, float* __restrict__ depth_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = i < g.n;
     if (alive && mask && !mask[i]) alive = false;
@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                 r.r0 = make_float4(m0, m1, k0, k1);
                 r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(x0, x1)),
                                    __uint_as_float(pack_range(y0, y1)));
-                r.r2 = make_float4(rgb[0], rgb[1], rgb[2], z);
+                // block-cull threshold (common.cuh may_contribute): ln(cmin / opacity) - 1e-3
+                const float cut = cp.apply_thresholds ? logf(cp.contribution_min / opacity) - 1e-3f : -INFINITY;
+                r.r2 = make_float4(rgb[0], rgb[1], rgb[2], cut);
                 if (aux) {
                     const float smax = std_max(std_max(ls0, ls1), ls2);
                     const float smin = std_min(std_min(ls0, ls1), ls2);
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
         keys[i] = alive ? __float_as_uint(zc) : 0xffffffffu;
         vals[i] = (uint32_t)i;
         tile_counts[i] = alive ? count : 0u;
+        depth_out[i] = alive ? zc : 0.0f;
         if (alive) {
             rec[i] = r;
             if (aux) aux[i] = a;
@@ -301,8 +304,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // Per-tile front-to-back blend (rasterizer.cpp:124-169 + traverse_pixel rasterizer.hpp:116-147).
 // One CTA per BW x BW pixel block (BW = min(tile, 16)); a tile of size 16k is covered by k*k
-// CTAs sharing its list (blockIdx.y).  Gaussian records are staged in shared memory in batches
-// of blockDim.x; all threads walk the batch in the same order (broadcast smem reads).
+// CTAs sharing its list (blockIdx.y).  The tile list is walked in batches of blockDim.x entries;
+// each batch is culled to the Gaussians that can reach the alpha floor inside the block and
+// staged in shared memory, and all threads walk it in the same order (broadcast reads).
 template <bool REPORT>
 __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
@@ -311,6 +315,8 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                                                            float bg2, FwdOutputs out) {
     __shared__ float4 s_r0[kBlock], s_r1[kBlock], s_r2[kBlock];
     __shared__ uint32_t s_gid[kBlock];
+    __shared__ int s_idx[kBlock];
+    __shared__ int s_wcnt[kBlock / 32];
     __shared__ float s_imp[REPORT ? kBlock : 1];
     __shared__ uint32_t s_maxw[REPORT ? kBlock : 1];
     const int nthreads = blockDim.x;
@@ -321,8 +327,10 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
     const int subs = ts / bw;
     const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
-    const int px = tx * ts + sx * bw + tid % bw;
-    const int py = ty * ts + sy * bw + tid / bw;
+    const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
+    const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
+    const int px = bx0 + tid % bw;
+    const int py = by0 + tid / bw;
     const bool inside = px < cp.width && py < cp.height;
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
     const int thr = cp.apply_thresholds;
@@ -336,91 +344,84 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
         s_imp[tid] = 0.0f;
         s_maxw[tid] = 0u;
     }
-    for (uint32_t base = start; base < end; base += nthreads) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t idx = base + tid;
-        if (idx < end) {
-            const uint32_t gid = pair_gauss[idx];
-            const ProjRec rr = rec[gid];
-            s_r0[tid] = rr.r0;
-            s_r1[tid] = rr.r1;
-            s_r2[tid] = rr.r2;
-            s_gid[tid] = gid;
-        }
-        __syncthreads();
-        const int cnt = (int)min((uint32_t)nthreads, end - base);
-        if (!REPORT) {
-            for (int j = 0; j < cnt && !done; ++j) {
-                float alpha, g2d, dx, dy;
-                bool clamped;
-                const float4 r1 = s_r1[j];
-                const float4 r0 = s_r0[j];
-                if (!gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
-                const float next = T * (1.0f - alpha);
-                if (thr && next < tmin) {
-                    done = true;
-                    break;
-                }
-                const float w = T * alpha;
-                const float4 r2 = s_r2[j];
-                acc0 = acc0 + w * r2.x;
-                acc1 = acc1 + w * r2.y;
-                acc2 = acc2 + w * r2.z;
-                if (w > wmax) {
-                    wmax = w;
-                    amax_gid = (int32_t)s_gid[j];
-                }
-                last = (int32_t)(base + j);
-                T = next;
-            }
-        } else {
-            const int lane = tid & 31;
-            for (int j = 0; j < cnt; ++j) {
-                if (__all_sync(0xffffffffu, done)) break;
-                float w = 0.0f;
-                if (!done) {
+    if (bx0 < bx1 && by0 < by1) {
+        for (uint32_t base = start; base < end; base += nthreads) {
+            if (__syncthreads_count(!done) == 0) break;
+            const int cnt = stage_batch([&](int t) { return (int)(base + t); }, (int)min((uint32_t)nthreads, end - base),
+                                        pair_gauss, rec, bx0, bx1, by0, by1, s_r0, s_r1, s_r2, s_gid, s_idx, s_wcnt);
+            if (!REPORT) {
+                for (int j = 0; j < cnt && !done; ++j) {
                     float alpha, g2d, dx, dy;
                     bool clamped;
                     const float4 r1 = s_r1[j];
                     const float4 r0 = s_r0[j];
-                    if (gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
-                        const float next = T * (1.0f - alpha);
-                        if (thr && next < tmin) {
-                            done = true;
-                        } else {
-                            w = T * alpha;
-                            const float4 r2 = s_r2[j];
-                            acc0 = acc0 + w * r2.x;
-                            acc1 = acc1 + w * r2.y;
-                            acc2 = acc2 + w * r2.z;
-                            if (w > wmax) {
-                                wmax = w;
-                                amax_gid = (int32_t)s_gid[j];
+                    if (!gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
+                    const float next = T * (1.0f - alpha);
+                    if (thr && next < tmin) {
+                        done = true;
+                        break;
+                    }
+                    const float w = T * alpha;
+                    const float4 r2 = s_r2[j];
+                    acc0 = acc0 + w * r2.x;
+                    acc1 = acc1 + w * r2.y;
+                    acc2 = acc2 + w * r2.z;
+                    if (w > wmax) {
+                        wmax = w;
+                        amax_gid = (int32_t)s_gid[j];
+                    }
+                    last = s_idx[j];
+                    T = next;
+                }
+            } else {
+                const int lane = tid & 31;
+                for (int j = 0; j < cnt; ++j) {
+                    if (__all_sync(0xffffffffu, done)) break;
+                    float w = 0.0f;
+                    if (!done) {
+                        float alpha, g2d, dx, dy;
+                        bool clamped;
+                        const float4 r1 = s_r1[j];
+                        const float4 r0 = s_r0[j];
+                        if (gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
+                            const float next = T * (1.0f - alpha);
+                            if (thr && next < tmin) {
+                                done = true;
+                            } else {
+                                w = T * alpha;
+                                const float4 r2 = s_r2[j];
+                                acc0 = acc0 + w * r2.x;
+                                acc1 = acc1 + w * r2.y;
+                                acc2 = acc2 + w * r2.z;
+                                if (w > wmax) {
+                                    wmax = w;
+                                    amax_gid = (int32_t)s_gid[j];
+                                }
+                                last = s_idx[j];
+                                T = next;
                             }
-                            last = (int32_t)(base + j);
-                            T = next;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, w > 0.0f)) {
+                        const float sum = warp_sum(w);
+                        const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
+                        if (lane == 0) {
+                            atomicAdd(&s_imp[j], sum);
+                            atomicMax(&s_maxw[j], mx);
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, w > 0.0f)) {
-                    const float sum = warp_sum(w);
-                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
-                    if (lane == 0) {
-                        atomicAdd(&s_imp[j], sum);
-                        atomicMax(&s_maxw[j], mx);
-                    }
+                __syncthreads();
+                if (tid < cnt && s_maxw[tid] != 0u) {
+                    const uint32_t gid = s_gid[tid];
+                    atomicAdd(&out.importance[gid], s_imp[tid]);
+                    atomicMax(reinterpret_cast<uint32_t*>(&out.max_weight[gid]), s_maxw[tid]);
+                    s_imp[tid] = 0.0f;
+                    s_maxw[tid] = 0u;
                 }
             }
             __syncthreads();
-            if (tid < cnt && s_maxw[tid] != 0u) {
-                const uint32_t gid = s_gid[tid];
-                atomicAdd(&out.importance[gid], s_imp[tid]);
-                atomicMax(reinterpret_cast<uint32_t*>(&out.max_weight[gid]), s_maxw[tid]);
-                s_imp[tid] = 0.0f;
-                s_maxw[tid] = 0u;
-            }
         }
-        __syncthreads();
     }
     if (!inside) return;
     const size_t pix = (size_t)py * cp.width + px;
@@ -519,20 +520,20 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
-                              uint32_t* n_survivors_dev) {
+                              uint32_t* n_survivors_dev, float* depth_out) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                             tile_counts, n_survivors_dev);
+                                                                             tile_counts, n_survivors_dev, depth_out);
         }
     else
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                              tile_counts, n_survivors_dev);
+                                                                              tile_counts, n_survivors_dev, depth_out);
         }
     lc.count++;
     return cudaGetLastError();

@@ -60,7 +60,8 @@ struct GaussianPtrs {
 // culled), identity values and per-Gaussian tile counts; *n_survivors_dev += survivors.
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
-                              uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev);
+                              uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
+                              float* depth_out);
 // counts_sorted[r] = tile_counts[order[r]]
 cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
                                  uint32_t* counts_sorted, int n);
