@@ -25,6 +25,7 @@ SOURCES = {
     "sort.cu": [],
     "backward.cu": [],
     "chain.cu": ["--fmad=false"],
+    "binning.cu": [],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

@@ -14,7 +14,6 @@ namespace splat_b200 {
 
 namespace {
 
-constexpr int kGradSlots = 10;   // 9 gradient values + touched count per staged Gaussian
 constexpr int kGradStride = 10;  // smem row stride (floats): conflict-free lane->value scatter
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -1,0 +1,281 @@
+// binning.cu — per-tile lists (detail::bin_tiles, rasterizer.hpp:156-174) built without sorting
+// the P (tile, Gaussian) pairs.
+//
+// The reference pushes every depth-sorted Gaussian into each tile its pixel rect touches, so a
+// tile's list is "the Gaussians covering it, in (depth, index) order".  A stable radix sort of P
+// pairs by tile reproduces that but moves ~16 B x P x 2 passes.  Instead:
+//   1. emit (supertile, Gaussian) pairs in depth order — a supertile is 4 x 4 tiles, so Ps ~ P/10;
+//   2. stable radix sort of the Ps pairs by supertile (one or two small passes);
+//   3. split every supertile list into segments of kSeg entries; a count pass gives, per
+//      (tile, segment), how many entries of the segment cover the tile; an exclusive scan of those
+//      counts laid out tile-major / segment-minor gives every (tile, segment) its output offset;
+//   4. an emit pass re-walks each segment in order and writes each Gaussian id into the lists of
+//      the tiles it covers at offset + (rank among the segment's earlier entries covering that
+//      tile), the rank coming from one warp ballot per tile of the supertile.
+// Stability at every step makes each list exactly the reference's, and only P x 4 B are written.
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace splat_b200 {
+
+namespace {
+
+constexpr int kST = 4;              // supertile side in tiles
+constexpr int kSTT = kST * kST;     // tiles per supertile
+constexpr int kSeg = 1024;          // entries per segment of a supertile list
+constexpr int kBinThreads = 256;
+
+struct TileRect {
+    int tx0, tx1, ty0, ty1;  // inclusive tile range of a Gaussian's pixel rect
+};
+
+__device__ __forceinline__ TileRect tile_rect(const float4& r1, int ts) {
+    TileRect t;
+    t.tx0 = range_lo(r1.z) / ts;
+    t.tx1 = (range_hi(r1.z) - 1) / ts;
+    t.ty0 = range_lo(r1.w) / ts;
+    t.ty1 = (range_hi(r1.w) - 1) / ts;
+    return t;
+}
+
+// (supertile, Gaussian) pairs in depth order: one thread per survivor.
+__global__ void __launch_bounds__(256) emit_st_pairs_kernel(const uint32_t* __restrict__ order,
+                                                           const uint32_t* __restrict__ offsets,
+                                                           const ProjRec* __restrict__ rec, int ts, int st_x,
+                                                           int n_surv, uint32_t* __restrict__ st_key,
+                                                           uint32_t* __restrict__ st_gauss) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_surv) return;
+    const uint32_t gid = order[r];
+    uint32_t o = offsets[r];
+    const TileRect t = tile_rect(rec[gid].r1, ts);
+    for (int sy = t.ty0 / kST; sy <= t.ty1 / kST; ++sy)
+        for (int sx = t.tx0 / kST; sx <= t.tx1 / kST; ++sx) {
+            st_key[o] = (uint32_t)(sy * st_x + sx);
+            st_gauss[o] = gid;
+            ++o;
+        }
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
+// total).  One CTA of kBinThreads threads.
+template <typename F>
+__device__ void cta_scan(int n, F val, uint32_t* __restrict__ out, uint32_t* s_warp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t carry = 0;
+    for (int base = 0; base < n; base += kBinThreads) {
+        const int i = base + tid;
+        const uint32_t v = i < n ? val(i) : 0u;
+        const uint32_t inc = warp_incl_scan(v, lane);
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+        for (int w = 0; w < kBinThreads / 32; ++w) {
+            off += w < warp ? s_warp[w] : 0u;
+            tot += s_warp[w];
+        }
+        if (i < n) out[i] = carry + off + inc - v;
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) out[n] = carry;
+}
+
+// seg_start[st] = first segment id of supertile st (exclusive scan of ceil(len / kSeg));
+// tile_base[t] = first slot of tile t in the (tile, segment) count array.
+__global__ void __launch_bounds__(kBinThreads) seg_setup_kernel(const uint32_t* __restrict__ st_ranges, int n_st,
+                                                               int tiles_x, int tiles_y, int st_x,
+                                                               uint32_t* __restrict__ seg_start,
+                                                               uint32_t* __restrict__ tile_base) {
+    __shared__ uint32_t s_warp[kBinThreads / 32];
+    auto nseg = [&](int st) {
+        const uint32_t len = st_ranges[2 * st + 1] - st_ranges[2 * st];
+        return (len + kSeg - 1) / kSeg;
+    };
+    cta_scan(n_st, nseg, seg_start, s_warp);
+    cta_scan(tiles_x * tiles_y,
+             [&](int t) {
+                 const int tx = t % tiles_x, ty = t / tiles_x;
+                 return nseg((ty / kST) * st_x + tx / kST);
+             },
+             tile_base, s_warp);
+}
+
+// Count (EMIT = false) or emit (EMIT = true) pass over one segment of one supertile list.
+template <bool EMIT>
+__global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
+    const uint32_t* __restrict__ st_ranges, const uint32_t* __restrict__ seg_start, int n_st,
+    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ st_gauss, const ProjRec* __restrict__ rec,
+    int ts, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ slots, uint32_t* __restrict__ pair_gauss) {
+    __shared__ uint32_t s_wc[kBinThreads / 32][kSTT];
+    __shared__ uint32_t s_run[kSTT];
+    __shared__ uint32_t s_base[kSTT];
+    const int b = blockIdx.x;
+    if (b >= (int)seg_start[n_st]) return;
+    int lo_st = 0, hi_st = n_st;  // largest st with seg_start[st] <= b
+    while (hi_st - lo_st > 1) {
+        const int mid = (lo_st + hi_st) >> 1;
+        if (seg_start[mid] <= (uint32_t)b) lo_st = mid;
+        else hi_st = mid;
+    }
+    const int st = lo_st;
+    const int seg = b - (int)seg_start[st];
+    const uint32_t st_end = st_ranges[2 * st + 1];
+    const uint32_t lo = st_ranges[2 * st] + (uint32_t)seg * kSeg;
+    const uint32_t hi = min(lo + (uint32_t)kSeg, st_end);
+    const int tx_base = (st % st_x) * kST, ty_base = (st / st_x) * kST;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < kSTT) {
+        s_run[tid] = 0;
+        if (EMIT) {
+            const int tx = tx_base + (tid % kST), ty = ty_base + (tid / kST);
+            s_base[tid] = (tx < tiles_x && ty < tiles_y) ? slots[tile_base[ty * tiles_x + tx] + seg] : 0u;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = lanemask_lt();
+    for (uint32_t c = lo; c < hi; c += kBinThreads) {
+        const uint32_t e = c + tid;
+        uint32_t gid = 0, cover = 0;
+        if (e < hi) {
+            gid = st_gauss[e];
+            const TileRect t = tile_rect(rec[gid].r1, ts);
+            const int lx0 = max(t.tx0 - tx_base, 0), lx1 = min(t.tx1 - tx_base, kST - 1);
+            const int ly0 = max(t.ty0 - ty_base, 0), ly1 = min(t.ty1 - ty_base, kST - 1);
+            for (int ly = ly0; ly <= ly1; ++ly)
+                for (int lx = lx0; lx <= lx1; ++lx) cover |= 1u << (ly * kST + lx);
+        }
+        uint32_t rank[kSTT];
+#pragma unroll
+        for (int f = 0; f < kSTT; ++f) {
+            const unsigned m = __ballot_sync(0xffffffffu, (cover >> f) & 1u);
+            rank[f] = __popc(m & lt);
+            if (lane == 0) s_wc[warp][f] = __popc(m);
+        }
+        __syncthreads();
+        if (EMIT && cover) {
+#pragma unroll
+            for (int f = 0; f < kSTT; ++f) {
+                if ((cover >> f) & 1u) {
+                    uint32_t pre = 0;
+                    for (int w = 0; w < warp; ++w) pre += s_wc[w][f];
+                    pair_gauss[s_base[f] + s_run[f] + pre + rank[f]] = gid;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < kSTT) {
+            uint32_t tot = 0;
+            for (int w = 0; w < kBinThreads / 32; ++w) tot += s_wc[w][tid];
+            s_run[tid] += tot;
+        }
+        __syncthreads();
+    }
+    if (!EMIT && tid < kSTT) {
+        const int tx = tx_base + (tid % kST), ty = ty_base + (tid / kST);
+        if (tx < tiles_x && ty < tiles_y) slots[tile_base[ty * tiles_x + tx] + seg] = s_run[tid];
+    }
+}
+
+// ranges[t] = [scanned[tile_base[t]], scanned[tile_base[t + 1]])
+__global__ void ranges_from_slots_kernel(const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_base,
+                                         int n_tiles, uint32_t* __restrict__ ranges) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    ranges[2 * t] = scanned[tile_base[t]];
+    ranges[2 * t + 1] = scanned[tile_base[t + 1]];
+}
+
+// supertile ranges over the st-sorted keys (lower bounds)
+__global__ void key_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ ranges,
+                                  int n_keys) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_keys) return;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t key = (uint32_t)t + k;
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (keys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        ranges[2 * t + k] = lo;
+    }
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+int supertile_side() { return kST; }
+size_t bin_segment_upper(uint64_t st_pairs, int n_st) { return (size_t)(st_pairs / kSeg + n_st + 1); }
+
+cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
+    const int n_st = a.st_x * a.st_y;
+    const int n_tiles = a.tiles_x * a.tiles_y;
+    if (a.n_surv > 0) {
+        LaunchScope s(lc, "emit_st_pairs");
+        emit_st_pairs_kernel<<<blocks_for(a.n_surv, 256), 256, 0, lc.stream>>>(a.order, a.st_offsets, a.rec, a.tile_size,
+                                                                             a.st_x, a.n_surv, a.st_key[0],
+                                                                             a.st_gauss[0]);
+        lc.count++;
+    }
+    bool alt = false;
+    cudaError_t e = radix_sort_pairs(lc, a.st_key[0], a.st_gauss[0], a.st_key[1], a.st_gauss[1], a.st_pairs, 0,
+                                     a.st_bits, a.hist, a.scan_tmp, &alt);
+    if (e != cudaSuccess) return e;
+    const uint32_t* keys = a.st_key[alt ? 1 : 0];
+    const uint32_t* gauss = a.st_gauss[alt ? 1 : 0];
+    {
+        LaunchScope s(lc, "st_ranges");
+        key_ranges_kernel<<<blocks_for(n_st, 256), 256, 0, lc.stream>>>(keys, (uint32_t)a.st_pairs, a.st_ranges, n_st);
+        lc.count++;
+    }
+    {
+        LaunchScope s(lc, "seg_setup");
+        seg_setup_kernel<<<1, kBinThreads, 0, lc.stream>>>(a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, a.seg_start,
+                                                          a.tile_base);
+        lc.count++;
+    }
+    const size_t segs = bin_segment_upper(a.st_pairs, n_st);
+    const size_t n_slots = segs * kSTT + 1;
+    e = cudaMemsetAsync(a.slots, 0, n_slots * 4, lc.stream);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope s(lc, "bin_count");
+        bin_segments_kernel<false><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
+            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rec, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
+            a.slots, nullptr);
+        lc.count++;
+    }
+    e = exclusive_scan_u32(lc, a.slots, a.slots, n_slots, a.scan_tmp, nullptr);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope s(lc, "tile_ranges");
+        ranges_from_slots_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(a.slots, a.tile_base, n_tiles,
+                                                                                  a.ranges);
+        lc.count++;
+    }
+    {
+        LaunchScope s(lc, "bin_emit");
+        bin_segments_kernel<true><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
+            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rec, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
+            a.slots, a.pair_gauss);
+        lc.count++;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace splat_b200

@@ -119,7 +119,7 @@ struct splat_ctx {
     // per-Gaussian
     DevBuf rec, aux, depth, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
-    DevBuf pair_tile[2], pair_gauss[2];
+    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_ranges, seg_start, tile_base, slots;
     // misc
     DevBuf ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, P]
@@ -258,10 +258,10 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     if (!ctx->host_counters) CK(cudaMallocHost(&ctx->host_counters, 64), "alloc pinned");
 
     uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] = n_surv, [1] = P
-    CK(cudaMemsetAsync(d_counters, 0, 16, s), "memset counters");
+    CK(cudaMemsetAsync(d_counters, 0, 16, s), "memset counters");  // [0] survivors [1] Ps [2] P
     int n_surv = 0;
     uint64_t n_pairs = 0;
-    bool pairs_alt = false;
+    const bool pairs_alt = false;
     if (n > 0) {
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
         uint32_t* keys = ctx->keys[0].as<uint32_t>();
@@ -279,31 +279,57 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         CK(exclusive_scan_u32(lc, ctx->counts_sorted.as<uint32_t>(), ctx->offsets.as<uint32_t>(), (uint64_t)n,
                               ctx->scan_tmp.as<uint32_t>(), d_counters + 1),
            "scan counts");
-        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 8, cudaMemcpyDeviceToHost, s), "read counts");
+        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
         CK(cudaStreamSynchronize(s), "sync counts");
         n_surv = (int)ctx->host_counters[0];
-        n_pairs = ctx->host_counters[1];
-        if (n_pairs > 0) {
-            for (int k = 0; k < 2; ++k) {
-                CK(ctx->pair_tile[k].ensure(n_pairs * 4), "alloc pairs");
-                CK(ctx->pair_gauss[k].ensure(n_pairs * 4), "alloc pairs");
-            }
-            const size_t hw_words = radix_hist_words(n_pairs, 8);
-            CK(ctx->hist.ensure(hw_words * 4), "alloc hist");
-            CK(ctx->scan_tmp.ensure((scan_temp_words(hw_words) + 64) * 4), "alloc scan");
-            CK(launch_emit_pairs(lc, order, ctx->offsets.as<uint32_t>(), ctx->rec.as<ProjRec>(), cp, n_surv,
-                                 ctx->pair_tile[0].as<uint32_t>(), ctx->pair_gauss[0].as<uint32_t>()),
-               "emit pairs");
-            const int tile_bits = ceil_log2((uint32_t)n_tiles);
-            CK(radix_sort_pairs(lc, ctx->pair_tile[0].as<uint32_t>(), ctx->pair_gauss[0].as<uint32_t>(),
-                                ctx->pair_tile[1].as<uint32_t>(), ctx->pair_gauss[1].as<uint32_t>(), n_pairs, 0,
-                                tile_bits, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &pairs_alt),
-               "tile sort");
+        const uint64_t st_pairs = ctx->host_counters[1];
+        n_pairs = ctx->host_counters[2];
+        const int sts = supertile_side();
+        const int st_x = (cp.tiles_x + sts - 1) / sts, st_y = (cp.tiles_y + sts - 1) / sts;
+        const int n_st = st_x * st_y;
+        for (int k = 0; k < 2; ++k) {
+            CK(ctx->st_key[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
+            CK(ctx->st_gauss[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
         }
+        CK(ctx->pair_gauss[0].ensure(n_pairs * 4 + 4), "alloc pairs");
+        CK(ctx->st_ranges.ensure((size_t)n_st * 8), "alloc st ranges");
+        CK(ctx->seg_start.ensure(((size_t)n_st + 1) * 4), "alloc seg");
+        CK(ctx->tile_base.ensure(((size_t)n_tiles + 1) * 4), "alloc tile base");
+        const size_t n_slots = bin_segment_upper(st_pairs, n_st) * 16 + 1;
+        CK(ctx->slots.ensure(n_slots * 4), "alloc slots");
+        const size_t hwords = radix_hist_words(st_pairs, 8);
+        CK(ctx->hist.ensure(hwords * 4), "alloc hist");
+        CK(ctx->scan_tmp.ensure((scan_temp_words(hwords > n_slots ? hwords : n_slots) + 64) * 4), "alloc scan");
+        BinningArgs ba{};
+        ba.order = order;
+        ba.st_offsets = ctx->offsets.as<uint32_t>();
+        ba.rec = ctx->rec.as<ProjRec>();
+        ba.n_surv = n_surv;
+        ba.st_pairs = st_pairs;
+        ba.tile_size = cp.tile_size;
+        ba.tiles_x = cp.tiles_x;
+        ba.tiles_y = cp.tiles_y;
+        ba.st_x = st_x;
+        ba.st_y = st_y;
+        ba.st_bits = ceil_log2((uint32_t)n_st);
+        for (int k = 0; k < 2; ++k) {
+            ba.st_key[k] = ctx->st_key[k].as<uint32_t>();
+            ba.st_gauss[k] = ctx->st_gauss[k].as<uint32_t>();
+        }
+        ba.st_ranges = ctx->st_ranges.as<uint32_t>();
+        ba.seg_start = ctx->seg_start.as<uint32_t>();
+        ba.tile_base = ctx->tile_base.as<uint32_t>();
+        ba.slots = ctx->slots.as<uint32_t>();
+        ba.ranges = ctx->ranges.as<uint32_t>();
+        ba.pair_gauss = ctx->pair_gauss[0].as<uint32_t>();
+        ba.hist = ctx->hist.as<uint32_t>();
+        ba.scan_tmp = ctx->scan_tmp.as<uint32_t>();
+        CK(launch_binning(lc, ba), "binning");
+    } else {
+        CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_tiles * 8, s), "memset ranges");
+        CK(ctx->pair_gauss[0].ensure(4), "alloc pairs");
     }
-    const uint32_t* sorted_tiles = ctx->pair_tile[pairs_alt ? 1 : 0].as<uint32_t>();
-    const uint32_t* sorted_gauss = ctx->pair_gauss[pairs_alt ? 1 : 0].as<uint32_t>();
-    CK(launch_tile_ranges(lc, sorted_tiles, n_pairs, ctx->ranges.as<uint32_t>(), n_tiles), "tile ranges");
+    const uint32_t* sorted_gauss = ctx->pair_gauss[0].as<uint32_t>();
     if (rep && n > 0) {
         if (rep->importance) CK(cudaMemsetAsync(rep->importance, 0, (size_t)n * 4, s), "memset importance");
         if (rep->max_weight) CK(cudaMemsetAsync(rep->max_weight, 0, (size_t)n * 4, s), "memset max_weight");
@@ -665,7 +691,18 @@ int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int3
     if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     const int k = st.pairs_in_alt ? 1 : 0;
-    if (key_tile && st.n_pairs) CK(cudaMemcpy(key_tile, ctx->pair_tile[k].p, 4 * st.n_pairs, cudaMemcpyDeviceToHost), "copy");
+    const int n_tiles = st.cp.tiles_x * st.cp.tiles_y;
+    if (key_tile && st.n_pairs) {  // the tile id of each list entry, from the CSR ranges
+        uint32_t* r = new uint32_t[2 * (size_t)n_tiles];
+        cudaError_t e = cudaMemcpy(r, ctx->ranges.p, 8 * (size_t)n_tiles, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            delete[] r;
+            return cuda_err(ctx, e, "copy ranges");
+        }
+        for (int t = 0; t < n_tiles; ++t)
+            for (uint32_t p = r[2 * t]; p < r[2 * t + 1] && p < st.n_pairs; ++p) key_tile[p] = t;
+        delete[] r;
+    }
     if (gaussian && st.n_pairs) CK(cudaMemcpy(gaussian, ctx->pair_gauss[k].p, 4 * st.n_pairs, cudaMemcpyDeviceToHost), "copy");
     if (ranges)
         CK(cudaMemcpy(ranges, ctx->ranges.p, 8 * (size_t)st.cp.tiles_x * st.cp.tiles_y, cudaMemcpyDeviceToHost), "copy");

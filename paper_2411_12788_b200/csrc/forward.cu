@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
     }
     ProjRec r;
     AuxRec a;
-    uint32_t count = 0;
+    uint32_t count = 0, tiles = 0;
     if (alive) {
         const float z = zc;
         const float m0 = cp.fx * pc0 / z + cp.cx;
@@ -196,7 +196,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                     sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
                 }
                 const int ts = cp.tile_size;
-                count = (uint32_t)(((x1 - 1) / ts - x0 / ts + 1) * ((y1 - 1) / ts - y0 / ts + 1));
+                const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts, ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
+                tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+                count = (uint32_t)((tx1 / 4 - tx0 / 4 + 1) * (ty1 / 4 - ty0 / 4 + 1));  // supertiles
                 r.r0 = make_float4(m0, m1, k0, k1);
                 r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(x0, x1)),
                                    __uint_as_float(pack_range(y0, y1)));
@@ -240,8 +242,18 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
             if (aux) aux[i] = a;
         }
     }
+    __shared__ uint32_t s_pairs[8];
+    uint32_t wp = tiles;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
+    if ((threadIdx.x & 31) == 0) s_pairs[threadIdx.x >> 5] = wp;
     const int block_alive = __syncthreads_count(alive);
-    if (threadIdx.x == 0 && block_alive) atomicAdd(n_surv, (uint32_t)block_alive);
+    if (threadIdx.x == 0 && block_alive) {
+        uint32_t bp = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) bp += s_pairs[w];
+        atomicAdd(n_surv, (uint32_t)block_alive);
+        atomicAdd(n_surv + 2, bp);
+    }
 }
 
 __global__ void gather_counts_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,

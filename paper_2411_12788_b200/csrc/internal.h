@@ -57,7 +57,8 @@ struct GaussianPtrs {
 };
 
 // K1: per-Gaussian projection. Writes rec/aux (aux may be null), depth keys (0xFFFFFFFF when
-// culled), identity values and per-Gaussian tile counts; *n_survivors_dev += survivors.
+// culled), identity values and per-Gaussian SUPERTILE counts (0 = culled);
+// counters[0] += survivors, counters[2] += tile pairs P.
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
@@ -72,6 +73,29 @@ cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32
 // K5: ranges[2t], ranges[2t+1] = [start, end) of tile t in the sorted pairs.
 cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs,
                                uint32_t* ranges, int n_tiles);
+
+// ---- binning.cu ---------------------------------------------------------------------------
+struct BinningArgs {
+    const uint32_t* order;       // survivors in (depth, index) order
+    const uint32_t* st_offsets;  // exclusive scan of supertile counts in depth order
+    const ProjRec* rec;
+    int n_surv;
+    uint64_t st_pairs;
+    int tile_size, tiles_x, tiles_y, st_x, st_y, st_bits;
+    uint32_t* st_key[2];
+    uint32_t* st_gauss[2];
+    uint32_t* st_ranges;   // [2 * n_st]
+    uint32_t* seg_start;   // [n_st + 1]
+    uint32_t* tile_base;   // [n_tiles + 1]
+    uint32_t* slots;       // [bin_segment_upper * 16 + 1]
+    uint32_t* ranges;      // [2 * n_tiles] out
+    uint32_t* pair_gauss;  // [P] out: per-tile lists of Gaussian ids
+    uint32_t* hist;
+    uint32_t* scan_tmp;
+};
+int supertile_side();
+size_t bin_segment_upper(uint64_t st_pairs, int n_st);
+cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a);
 
 struct FwdOutputs {
     float* color;            // [H][W][3] or null
