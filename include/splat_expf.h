@@ -79,4 +79,25 @@ SPLAT_HD float splat_expf(float x) {
     return splat_mul(splat_mul(p, s1), s2);
 }
 
+/* splat_expf without the special cases, for arguments whose k = rint(x / ln2) lies in
+ * [-126, 127] (x in [-87.3, 88.0]): there 2^k is a normal float, so p * 2^k is the exact value
+ * rounded once — the same single rounding the two-step scaling of splat_expf performs — and the
+ * result is bit-identical to splat_expf (checked exhaustively over [-87.3, 0] by
+ * tests/test_expf.py).  The blend kernels use it after the `power >= cut` test, which confines
+ * the argument to [ln(cmin) - 1e-3, 0]. */
+SPLAT_HD float splat_expf_core(float x) {
+    const float kf = rintf(splat_mul(x, 1.44269502162933349609375f));
+    float r = splat_fma(kf, -0.693145751953125f, x);
+    r = splat_fma(kf, -1.428606765330187045037746429443359375e-06f, r);
+    float p = 1.98412698412698412698e-4f;
+    p = splat_fma(p, r, 1.38888888888888888889e-3f);
+    p = splat_fma(p, r, 8.33333333333333333333e-3f);
+    p = splat_fma(p, r, 4.16666666666666666667e-2f);
+    p = splat_fma(p, r, 1.66666666666666666667e-1f);
+    p = splat_fma(p, r, 0.5f);
+    p = splat_fma(p, r, 1.0f);
+    p = splat_fma(p, r, 1.0f);
+    return splat_mul(p, splat_bits_to_float((uint32_t)((int)kf + 127) << 23));
+}
+
 #endif /* SPLAT_EXPF_H */

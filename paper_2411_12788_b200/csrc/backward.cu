@@ -68,6 +68,7 @@ __device__ __forceinline__ float warp_transpose_reduce10(const float v[10], int 
 // per-Gaussian accumulator with three float4 atomics per (CTA, Gaussian).
 // With target != nullptr, dL/dC = sign(C - target)/n (l1_loss, loss.cpp:63-76) is fused in and
 // the CTA's L1 partial sum is written to loss_partials[block].
+template <bool THR>
 __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                             const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
@@ -136,9 +137,11 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     const uint32_t start = ranges[2 * tile];
     if (block_last < (int)start) return;  // nothing committed in this block
 
-    const int thr = cp.apply_thresholds;
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
+    const uint32_t mybits = (1u << (tid % bw)) | (1u << (16 + tid / bw));
+    const int rpw = 32 / bw;
+    const uint32_t wrows = (((1u << rpw) - 1u) << (warp * rpw)) << 16;
     float T = inside ? t_final[pix] : 1.0f;
     float b0 = bg0, b1 = bg1, b2 = bg2;
 
@@ -151,6 +154,8 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
         for (int j = 0; j < cnt; ++j) {
             const int idx = s_idx[j];
             if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
+            const float4 r1 = s_r1[j];
+            if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (warp-uniform)
             float v[10];
 #pragma unroll
             for (int k = 0; k < 10; ++k) v[k] = 0.0f;
@@ -158,8 +163,8 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
             if (idx <= my_last) {
                 float alpha, g2d, dx, dy;
                 bool clamped;
-                const float4 r0 = s_r0[j], r1 = s_r1[j];
-                if (gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
+                const float4 r0 = s_r0[j];
+                if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
                     committed = true;
                     const float4 r2 = s_r2[j];
                     const float one_m_a = 1.0f - alpha;
@@ -296,9 +301,14 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
     {
         LaunchScope ls_(lc, "blend_backward");
-        blend_backward_kernel<<<grid, bw * bw, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, t_final, last_index, bg[0],
-                                                          bg[1], bg[2], d_color, color, target, inv_n, loss_partials,
-                                                          reinterpret_cast<float4*>(grad2d));
+        if (cp.apply_thresholds)
+            blend_backward_kernel<true><<<grid, bw * bw, 0, lc.stream>>>(
+                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n,
+                loss_partials, reinterpret_cast<float4*>(grad2d));
+        else
+            blend_backward_kernel<false><<<grid, bw * bw, 0, lc.stream>>>(
+                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n,
+                loss_partials, reinterpret_cast<float4*>(grad2d));
     }
     lc.count++;
     return cudaGetLastError();

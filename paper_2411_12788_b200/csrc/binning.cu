@@ -31,26 +31,26 @@ struct TileRect {
     int tx0, tx1, ty0, ty1;  // inclusive tile range of a Gaussian's pixel rect
 };
 
-__device__ __forceinline__ TileRect tile_rect(const float4& r1, int ts) {
+__device__ __forceinline__ TileRect tile_rect(uint2 r, int ts) {
     TileRect t;
-    t.tx0 = range_lo(r1.z) / ts;
-    t.tx1 = (range_hi(r1.z) - 1) / ts;
-    t.ty0 = range_lo(r1.w) / ts;
-    t.ty1 = (range_hi(r1.w) - 1) / ts;
+    t.tx0 = (int)(r.x & 0xffffu) / ts;
+    t.tx1 = ((int)(r.x >> 16) - 1) / ts;
+    t.ty0 = (int)(r.y & 0xffffu) / ts;
+    t.ty1 = ((int)(r.y >> 16) - 1) / ts;
     return t;
 }
 
 // (supertile, Gaussian) pairs in depth order: one thread per survivor.
 __global__ void __launch_bounds__(256) emit_st_pairs_kernel(const uint32_t* __restrict__ order,
                                                            const uint32_t* __restrict__ offsets,
-                                                           const ProjRec* __restrict__ rec, int ts, int st_x,
+                                                           const uint2* __restrict__ rect_ref, int ts, int st_x,
                                                            int n_surv, uint32_t* __restrict__ st_key,
                                                            uint32_t* __restrict__ st_gauss) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_surv) return;
     const uint32_t gid = order[r];
     uint32_t o = offsets[r];
-    const TileRect t = tile_rect(rec[gid].r1, ts);
+    const TileRect t = tile_rect(rect_ref[gid], ts);
     for (int sy = t.ty0 / kST; sy <= t.ty1 / kST; ++sy)
         for (int sx = t.tx0 / kST; sx <= t.tx1 / kST; ++sx) {
             st_key[o] = (uint32_t)(sy * st_x + sx);
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kBinThreads) seg_setup_kernel(const uint32_t* 
 template <bool EMIT>
 __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
     const uint32_t* __restrict__ st_ranges, const uint32_t* __restrict__ seg_start, int n_st,
-    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ st_gauss, const ProjRec* __restrict__ rec,
+    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ st_gauss, const uint2* __restrict__ rect_ref,
     int ts, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ slots, uint32_t* __restrict__ pair_gauss) {
     __shared__ uint32_t s_wc[kBinThreads / 32][kSTT];
     __shared__ uint32_t s_run[kSTT];
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
         uint32_t gid = 0, cover = 0;
         if (e < hi) {
             gid = st_gauss[e];
-            const TileRect t = tile_rect(rec[gid].r1, ts);
+            const TileRect t = tile_rect(rect_ref[gid], ts);
             const int lx0 = max(t.tx0 - tx_base, 0), lx1 = min(t.tx1 - tx_base, kST - 1);
             const int ly0 = max(t.ty0 - ty_base, 0), ly1 = min(t.ty1 - ty_base, kST - 1);
             for (int ly = ly0; ly <= ly1; ++ly)
@@ -227,7 +227,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     const int n_tiles = a.tiles_x * a.tiles_y;
     if (a.n_surv > 0) {
         LaunchScope s(lc, "emit_st_pairs");
-        emit_st_pairs_kernel<<<blocks_for(a.n_surv, 256), 256, 0, lc.stream>>>(a.order, a.st_offsets, a.rec, a.tile_size,
+        emit_st_pairs_kernel<<<blocks_for(a.n_surv, 256), 256, 0, lc.stream>>>(a.order, a.st_offsets, a.rect_ref, a.tile_size,
                                                                              a.st_x, a.n_surv, a.st_key[0],
                                                                              a.st_gauss[0]);
         lc.count++;
@@ -256,7 +256,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     {
         LaunchScope s(lc, "bin_count");
         bin_segments_kernel<false><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
-            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rec, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
+            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rect_ref, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
             a.slots, nullptr);
         lc.count++;
     }
@@ -271,7 +271,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     {
         LaunchScope s(lc, "bin_emit");
         bin_segments_kernel<true><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
-            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rec, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
+            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rect_ref, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
             a.slots, a.pair_gauss);
         lc.count++;
     }

@@ -117,7 +117,7 @@ struct splat_ctx {
     LaunchCtx lc;
     std::string err;
     // per-Gaussian
-    DevBuf rec, aux, depth, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
+    DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
     DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_ranges, seg_start, tile_base, slots;
     // misc
@@ -242,6 +242,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     }
     CK(ctx->tile_counts.ensure(nn * 4), "alloc counts");
     CK(ctx->depth.ensure(nn * 4), "alloc depth");
+    CK(ctx->rect_ref.ensure(nn * 8), "alloc rects");
     CK(ctx->counts_sorted.ensure(nn * 4), "alloc counts");
     CK(ctx->offsets.ensure((nn + 1) * 4), "alloc offsets");
     CK(ctx->counters.ensure(64), "alloc counters");
@@ -267,7 +268,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* keys = ctx->keys[0].as<uint32_t>();
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
-                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>()),
+                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>()),
            "preprocess");
         bool alt = false;
         CK(radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), (uint64_t)n, 0,
@@ -303,7 +304,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         BinningArgs ba{};
         ba.order = order;
         ba.st_offsets = ctx->offsets.as<uint32_t>();
-        ba.rec = ctx->rec.as<ProjRec>();
+        ba.rect_ref = ctx->rect_ref.as<uint2>();
         ba.n_surv = n_surv;
         ba.st_pairs = st_pairs;
         ba.tile_size = cp.tile_size;
@@ -651,18 +652,18 @@ int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* d
     ProjRec* h = new ProjRec[n];
     uint32_t* counts = new uint32_t[n];
     float* depths = new float[n];
+    uint2* rects = new uint2[n];
     cudaError_t e = cudaMemcpy(h, ctx->rec.p, sizeof(ProjRec) * n, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(depths, ctx->depth.p, 4 * (size_t)n, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(rects, ctx->rect_ref.p, 8 * (size_t)n, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(counts, ctx->tile_counts.p, 4 * (size_t)n, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
-        delete[] h; delete[] counts; delete[] depths;
+        delete[] h; delete[] counts; delete[] depths; delete[] rects;
         return cuda_err(ctx, e, "project debug");
     }
     for (int i = 0; i < n; ++i) {
         const bool alive = counts[i] > 0;
-        uint32_t rx, ry;
-        std::memcpy(&rx, &h[i].r1.z, 4);
-        std::memcpy(&ry, &h[i].r1.w, 4);
+        const uint32_t rx = rects[i].x, ry = rects[i].y;
         if (rect) {
             rect[4 * i] = alive ? (int32_t)(rx & 0xffff) : 0;
             rect[4 * i + 1] = alive ? (int32_t)(rx >> 16) : 0;
@@ -681,7 +682,7 @@ int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* d
         if (opacity) opacity[i] = alive ? h[i].r1.y : 0.f;
         if (radius) radius[i] = 0;  // radius is not stored on device; rect carries the footprint
     }
-    delete[] h; delete[] counts; delete[] depths;
+    delete[] h; delete[] counts; delete[] depths; delete[] rects;
     return SPLAT_OK;
 }
 

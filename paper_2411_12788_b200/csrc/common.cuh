@@ -19,8 +19,12 @@ constexpr int kBlock = 256;  // threads per tile CTA (16 x 16 pixels)
 
 // Projected Gaussian record, 48 B (3 x float4), indexed by Gaussian id:
 //   r0 = (mean2d.x, mean2d.y, conic0, conic1)
-//   r1 = (conic2, opacity, rect x0 | x1 << 16, rect y0 | y1 << 16)
-//   r2 = (color.r, color.g, color.b, depth)
+//   r1 = (conic2, opacity, eff x0 | x1 << 16, eff y0 | y1 << 16)
+//   r2 = (color.r, color.g, color.b, cut)
+// The effective rect is the reference pixel rect (rasterizer.cpp:63-68) intersected with the
+// bounding box of the ellipse where alpha can reach the contribution floor; cut = ln(cmin /
+// opacity) - 1e-3 (-inf in exact mode).  The reference rect itself (which defines the tile lists)
+// is kept in a separate uint2 array for binning.
 struct __align__(16) ProjRec {
     float4 r0, r1, r2;
 };
@@ -53,16 +57,17 @@ __device__ __forceinline__ int range_lo(float f) { return (int)(__float_as_uint(
 __device__ __forceinline__ int range_hi(float f) { return (int)(__float_as_uint(f) >> 16); }
 
 // Per-sample gate of traverse_pixel (rasterizer.hpp:125-143), shared by the forward and the
-// backward so both see identical alphas.  Returns false when the sample is skipped (outside
-// the rect, power > 0, or alpha below the contribution floor).  The T-break test is left to
-// the caller (it needs T).  All arithmetic is explicitly rounded: no FMA contraction.
-__device__ __forceinline__ bool gate_sample(const float4& r0, const float4& r1, int px, int py,
-                                            float x, float y, int thresholds, float alpha_max,
-                                            float contribution_min, float& alpha, float& g2d,
+// backward so both see identical alphas.  r1 is the STAGED record (stage_batch): r1.z holds the
+// block-relative pixel masks of the effective rect (columns in bits 0-15, rows in 16-31) and r1.w
+// the cut.  Returns false when the sample is skipped: outside the rect, power > 0, power below the
+// cut (alpha would be below the floor), or alpha below the contribution floor.  The extra skips
+// only ever drop samples the reference skips too (see may_contribute / preprocess), and all
+// arithmetic deciding the committed set is explicitly rounded: no FMA contraction.
+template <bool THR>
+__device__ __forceinline__ bool gate_sample(const float4& r0, const float4& r1, uint32_t mybits, float x, float y,
+                                            float alpha_max, float contribution_min, float& alpha, float& g2d,
                                             bool& clamped, float& dx, float& dy) {
-    const float rx = r1.z, ry = r1.w;
-    if (px < range_lo(rx) || px >= range_hi(rx) || py < range_lo(ry) || py >= range_hi(ry))
-        return false;
+    if ((__float_as_uint(r1.z) & mybits) != mybits) return false;
     dx = __fsub_rn(r0.x, x);
     dy = __fsub_rn(r0.y, y);
     // power = -0.5 * (c0 dx dx + c2 dy dy) - c1 dx dy
@@ -71,15 +76,19 @@ __device__ __forceinline__ bool gate_sample(const float4& r0, const float4& r1, 
     const float m = __fmul_rn(-0.5f, __fadd_rn(a, b));
     const float power = __fsub_rn(m, __fmul_rn(__fmul_rn(r0.w, dx), dy));
     if (power > 0.0f) return false;
-    g2d = splat_expf(power);
-    alpha = __fmul_rn(r1.y, g2d);
     clamped = false;
-    if (thresholds) {
+    if (THR) {
+        if (power < r1.w) return false;
+        g2d = splat_expf_core(power);  // argument in [cut, 0]: bit-identical to splat_expf
+        alpha = __fmul_rn(r1.y, g2d);
         if (alpha > alpha_max) {
             alpha = alpha_max;
             clamped = true;
         }
         if (alpha < contribution_min) return false;
+    } else {
+        g2d = splat_expf(power);
+        alpha = __fmul_rn(r1.y, g2d);
     }
     return true;
 }
@@ -160,8 +169,13 @@ __device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32
     }
     if (keep) {
         const int pos = off + __popc(m & lanemask_lt());
+        // block-relative masks of the effective rect: bit lx = column bx0 + lx, bit 16 + ly = row
+        const int X0 = max(range_lo(rr.r1.z), bx0) - bx0, X1 = min(range_hi(rr.r1.z), bx1) - bx0;
+        const int Y0 = max(range_lo(rr.r1.w), by0) - by0, Y1 = min(range_hi(rr.r1.w), by1) - by0;
+        const uint32_t cols = ((1u << X1) - 1u) & ~((1u << X0) - 1u);
+        const uint32_t rows = ((1u << Y1) - 1u) & ~((1u << Y0) - 1u);
         s_r0[pos] = rr.r0;
-        s_r1[pos] = rr.r1;
+        s_r1[pos] = make_float4(rr.r1.x, rr.r1.y, __uint_as_float(cols | (rows << 16)), rr.r2.w);
         s_r2[pos] = rr.r2;
         s_gid[pos] = gid;
         s_idx[pos] = idx;

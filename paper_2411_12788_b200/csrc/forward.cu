@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                                                         ProjRec* __restrict__ rec, AuxRec* __restrict__ aux,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ tile_counts,
-                                                        uint32_t* __restrict__ n_surv, float* __restrict__ depth_out) {
+                                                        uint32_t* __restrict__ n_surv, float* __restrict__ depth_out,
+                                                        uint2* __restrict__ rect_ref) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool alive = i < g.n;
     if (alive && mask && !mask[i]) alive = false;
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
     }
     ProjRec r;
     AuxRec a;
+    uint2 ref_rect = make_uint2(0u, 0u);
     uint32_t count = 0, tiles = 0;
     if (alive) {
         const float z = zc;
@@ -202,9 +204,33 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                 r.r0 = make_float4(m0, m1, k0, k1);
                 r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(x0, x1)),
                                    __uint_as_float(pack_range(y0, y1)));
-                // block-cull threshold (common.cuh may_contribute): ln(cmin / opacity) - 1e-3
+                // cut = ln(cmin / opacity) - 1e-3: below it alpha cannot reach the floor
                 const float cut = cp.apply_thresholds ? logf(cp.contribution_min / opacity) - 1e-3f : -INFINITY;
+                // Effective rect for blending: the reference rect intersected with the bounding box
+                // of the ellipse power >= cut, i.e. |dx| <= sqrt(-2 cut cov2d_xx) (the conic is the
+                // inverse of cov2d); 1e-4 relative + 0.01 px of slack cover every rounding.
+                int ex0 = x0, ex1 = x1, ey0 = y0, ey1 = y1;
+                if (cp.apply_thresholds) {
+                    if (!(cut < 0.0f)) {
+                        ex1 = ex0;
+                        ey1 = ey0;
+                    } else {
+                        const float Q = -2.0f * cut;
+                        const float rx = sqrtf(Q * c0) * 1.0001f + 0.01f;
+                        const float ry = sqrtf(Q * c2) * 1.0001f + 0.01f;
+                        ex0 = max(x0, (int)ceilf(m0 - rx - 0.5f));
+                        ex1 = min(x1, (int)floorf(m0 + rx - 0.5f) + 1);
+                        ey0 = max(y0, (int)ceilf(m1 - ry - 0.5f));
+                        ey1 = min(y1, (int)floorf(m1 + ry - 0.5f) + 1);
+                        if (ex1 < ex0) ex1 = ex0;
+                        if (ey1 < ey0) ey1 = ey0;
+                    }
+                }
+                r.r0 = make_float4(m0, m1, k0, k1);
+                r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(ex0, ex1)),
+                                   __uint_as_float(pack_range(ey0, ey1)));
                 r.r2 = make_float4(rgb[0], rgb[1], rgb[2], cut);
+                ref_rect = make_uint2(pack_range(x0, x1), pack_range(y0, y1));
                 if (aux) {
                     const float smax = std_max(std_max(ls0, ls1), ls2);
                     const float smin = std_min(std_min(ls0, ls1), ls2);
@@ -237,6 +263,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
         vals[i] = (uint32_t)i;
         tile_counts[i] = alive ? count : 0u;
         depth_out[i] = alive ? zc : 0.0f;
+        rect_ref[i] = ref_rect;
         if (alive) {
             rec[i] = r;
             if (aux) aux[i] = a;
@@ -319,7 +346,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // CTAs sharing its list (blockIdx.y).  The tile list is walked in batches of blockDim.x entries;
 // each batch is culled to the Gaussians that can reach the alpha floor inside the block and
 // staged in shared memory, and all threads walk it in the same order (broadcast reads).
-template <bool REPORT>
+template <bool REPORT, bool THR>
 __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
@@ -345,9 +372,12 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
     const int py = by0 + tid / bw;
     const bool inside = px < cp.width && py < cp.height;
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    const int thr = cp.apply_thresholds;
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min, tmin = cp.transmittance_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
+    // this pixel's bits in the staged masks, and this warp's rows (32 / bw rows per warp)
+    const uint32_t mybits = (1u << (tid % bw)) | (1u << (16 + tid / bw));
+    const int rpw = 32 / bw;
+    const uint32_t wrows = (((1u << rpw) - 1u) << ((threadIdx.x >> 5) * rpw)) << 16;
 
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, wmax = 0.0f;
     int32_t amax_gid = -1, last = -1;
@@ -366,10 +396,11 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                     float alpha, g2d, dx, dy;
                     bool clamped;
                     const float4 r1 = s_r1[j];
+                    if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
                     const float4 r0 = s_r0[j];
-                    if (!gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
+                    if (!gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
                     const float next = T * (1.0f - alpha);
-                    if (thr && next < tmin) {
+                    if (THR && next < tmin) {
                         done = true;
                         break;
                     }
@@ -390,14 +421,15 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                 for (int j = 0; j < cnt; ++j) {
                     if (__all_sync(0xffffffffu, done)) break;
                     float w = 0.0f;
+                    const float4 r1 = s_r1[j];
+                    if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
                     if (!done) {
                         float alpha, g2d, dx, dy;
                         bool clamped;
-                        const float4 r1 = s_r1[j];
                         const float4 r0 = s_r0[j];
-                        if (gate_sample(r0, r1, px, py, x, y, thr, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
+                        if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
                             const float next = T * (1.0f - alpha);
-                            if (thr && next < tmin) {
+                            if (THR && next < tmin) {
                                 done = true;
                             } else {
                                 w = T * alpha;
@@ -532,20 +564,20 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
-                              uint32_t* n_survivors_dev, float* depth_out) {
+                              uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                             tile_counts, n_survivors_dev, depth_out);
+                                                                             tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
     else
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                              tile_counts, n_survivors_dev, depth_out);
+                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
     lc.count++;
     return cudaGetLastError();
@@ -593,18 +625,17 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
     const int subs = ts / bw;
     dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
     const int threads = bw * bw;
-    if (out.importance)
-        {
-            LaunchScope ls_(lc, "blend_forward");
-            blend_forward_kernel<true><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
-                                                                   bg[2], out);
-        }
-    else
-        {
-            LaunchScope ls_(lc, "blend_forward");
-            blend_forward_kernel<false><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1],
-                                                                    bg[2], out);
-        }
+    LaunchScope ls_(lc, "blend_forward");
+#define BLEND_FWD(R, T) blend_forward_kernel<R, T><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, \
+                                                                                   bg[0], bg[1], bg[2], out)
+    if (out.importance) {
+        if (cp.apply_thresholds) BLEND_FWD(true, true);
+        else BLEND_FWD(true, false);
+    } else {
+        if (cp.apply_thresholds) BLEND_FWD(false, true);
+        else BLEND_FWD(false, false);
+    }
+#undef BLEND_FWD
     lc.count++;
     return cudaGetLastError();
 }

@@ -62,7 +62,7 @@ struct GaussianPtrs {
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
-                              float* depth_out);
+                              float* depth_out, uint2* rect_ref);
 // counts_sorted[r] = tile_counts[order[r]]
 cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
                                  uint32_t* counts_sorted, int n);
@@ -78,7 +78,7 @@ cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint
 struct BinningArgs {
     const uint32_t* order;       // survivors in (depth, index) order
     const uint32_t* st_offsets;  // exclusive scan of supertile counts in depth order
-    const ProjRec* rec;
+    const uint2* rect_ref;  // reference pixel rects (x0 | x1 << 16, y0 | y1 << 16)
     int n_surv;
     uint64_t st_pairs;
     int tile_size, tiles_x, tiles_y, st_x, st_y, st_bits;
