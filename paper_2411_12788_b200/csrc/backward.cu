@@ -79,10 +79,7 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                                                             const float* __restrict__ target, float inv_n,
                                                             float* __restrict__ loss_partials,
                                                             float4* __restrict__ grad2d) {
-    __shared__ float4 s_r0[kBlock], s_r1[kBlock], s_r2[kBlock];
-    __shared__ uint32_t s_gid[kBlock];
-    __shared__ int s_idx[kBlock];
-    __shared__ int s_wcnt[kBlock / 32];
+    __shared__ StageSmem sm;
     __shared__ float s_g[kBlock * kGradStride];
     __shared__ float s_red[kBlock / 32];
     __shared__ int s_maxlast[kBlock / 32];
@@ -142,19 +139,20 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     const uint32_t mybits = (1u << (tid % bw)) | (1u << (16 + tid / bw));
     const int rpw = 32 / bw;
     const uint32_t wrows = (((1u << rpw) - 1u) << (warp * rpw)) << 16;
+    const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
+    const uint32_t a_idx = smem_base(sm.idx), a_g = smem_base(s_g);
     float T = inside ? t_final[pix] : 1.0f;
     float b0 = bg0, b1 = bg1, b2 = bg2;
 
     for (int hi = block_last + 1; hi > (int)start; hi -= nthreads) {
         const int count = min(nthreads, hi - (int)start);
-        const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1,
-                                    s_r0, s_r1, s_r2, s_gid, s_idx, s_wcnt);
+        const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1, sm);
         for (int k = tid; k < cnt * kGradStride; k += nthreads) s_g[k] = 0.0f;
         __syncthreads();
         for (int j = 0; j < cnt; ++j) {
-            const int idx = s_idx[j];
+            const int idx = (int)lds_u32(a_idx + 4u * j);
             if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
-            const float4 r1 = s_r1[j];
+            const float4 r1 = lds_f4(a_r1 + 16u * j);
             if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (warp-uniform)
             float v[10];
 #pragma unroll
@@ -163,12 +161,12 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
             if (idx <= my_last) {
                 float alpha, g2d, dx, dy;
                 bool clamped;
-                const float4 r0 = s_r0[j];
+                const float4 r0 = lds_f4(a_r0 + 16u * j);
                 if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
                     committed = true;
-                    const float4 r2 = s_r2[j];
+                    const float4 r2 = lds_f4(a_r2 + 16u * j);
                     const float one_m_a = 1.0f - alpha;
-                    const float t_before = T / one_m_a;
+                    const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
                     const float w = t_before * alpha;
                     v[6] = w * dL0;
                     v[7] = w * dL1;
@@ -194,13 +192,16 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
             if (__any_sync(0xffffffffu, committed)) {
                 int which;
                 const float s = warp_transpose_reduce10(v, lane, &which);
-                if (which >= 0 && s != 0.0f) atomicAdd(&s_g[j * kGradStride + which], s);
+                if (which >= 0 && s != 0.0f) {
+                    const uint32_t a = a_g + 4u * (uint32_t)(j * kGradStride + which);
+                    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(a), "f"(s) : "memory");
+                }
             }
         }
         __syncthreads();
         if (tid < cnt && s_g[tid * kGradStride + 9] > 0.0f) {
             const float* gs = &s_g[tid * kGradStride];
-            float4* dst = grad2d + 3 * (size_t)s_gid[tid];
+            float4* dst = grad2d + 3 * (size_t)sm.gid[tid];
             atomicAdd(dst + 0, make_float4(gs[0], gs[1], gs[2], gs[3]));
             atomicAdd(dst + 1, make_float4(gs[4], gs[5], gs[6], gs[7]));
             atomicAdd(dst + 2, make_float4(gs[8], gs[9], 0.0f, 0.0f));

@@ -142,11 +142,45 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // pass the exact block cull (common.cuh may_contribute); order is preserved by a ballot/prefix
 // compaction.  Returns the number of staged entries.  s_idx keeps each entry's absolute position
 // in the sorted pair array (the "list position" of the reference).
+// 32-bit shared-window loads.  nvcc re-derives the shared window base (S2R SR_CgaCtaId + LEA)
+// inside hot loops when it addresses __shared__ arrays by name; taking the base once as a 32-bit
+// shared address, laundered through an empty asm so it stays in a register, and loading with
+// ld.shared keeps the inner loops free of that overhead.
+__device__ __forceinline__ uint32_t smem_base(const void* p) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("" : "+r"(a));
+    return a;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// Shared-memory staging area of one batch (one per CTA).
+struct StageSmem {
+    float4 r0[kBlock];
+    float4 r1[kBlock];
+    float4 r2[kBlock];
+    uint32_t gid[kBlock];
+    int idx[kBlock];
+    int wcnt[kBlock / 32];
+};
+
+// Stage one batch of list entries in shared memory, keeping only Gaussians that pass the exact
+// block cull (may_contribute); order is preserved by a ballot/prefix compaction.  Returns the
+// number of staged entries.  sm.idx keeps each entry's absolute position in the sorted pair
+// array (the reference's list position); sm.r1 is rewritten to (conic2, opacity, pixel masks of
+// the effective rect relative to the block, cut) for gate_sample.
 template <typename IdxFn>
 __device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32_t* __restrict__ pair_gauss,
                                            const ProjRec* __restrict__ rec, int bx0, int bx1, int by0, int by1,
-                                           float4* s_r0, float4* s_r1, float4* s_r2, uint32_t* s_gid, int* s_idx,
-                                           int* s_wcnt) {
+                                           StageSmem& sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     bool keep = false;
     ProjRec rr;
@@ -159,26 +193,25 @@ __device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32
         keep = may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1);
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_wcnt[warp] = __popc(m);
+    if (lane == 0) sm.wcnt[warp] = __popc(m);
     __syncthreads();
     int off = 0, total = 0;
     for (int w = 0; w < nwarps; ++w) {
-        const int c = s_wcnt[w];
+        const int c = sm.wcnt[w];
         off += w < warp ? c : 0;
         total += c;
     }
     if (keep) {
         const int pos = off + __popc(m & lanemask_lt());
-        // block-relative masks of the effective rect: bit lx = column bx0 + lx, bit 16 + ly = row
         const int X0 = max(range_lo(rr.r1.z), bx0) - bx0, X1 = min(range_hi(rr.r1.z), bx1) - bx0;
         const int Y0 = max(range_lo(rr.r1.w), by0) - by0, Y1 = min(range_hi(rr.r1.w), by1) - by0;
         const uint32_t cols = ((1u << X1) - 1u) & ~((1u << X0) - 1u);
         const uint32_t rows = ((1u << Y1) - 1u) & ~((1u << Y0) - 1u);
-        s_r0[pos] = rr.r0;
-        s_r1[pos] = make_float4(rr.r1.x, rr.r1.y, __uint_as_float(cols | (rows << 16)), rr.r2.w);
-        s_r2[pos] = rr.r2;
-        s_gid[pos] = gid;
-        s_idx[pos] = idx;
+        sm.r0[pos] = rr.r0;
+        sm.r1[pos] = make_float4(rr.r1.x, rr.r1.y, __uint_as_float(cols | (rows << 16)), rr.r2.w);
+        sm.r2[pos] = rr.r2;
+        sm.gid[pos] = gid;
+        sm.idx[pos] = idx;
     }
     __syncthreads();
     return total;

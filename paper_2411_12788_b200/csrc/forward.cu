@@ -352,10 +352,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                                                            const ProjRec* __restrict__ rec,
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
                                                            float bg2, FwdOutputs out) {
-    __shared__ float4 s_r0[kBlock], s_r1[kBlock], s_r2[kBlock];
-    __shared__ uint32_t s_gid[kBlock];
-    __shared__ int s_idx[kBlock];
-    __shared__ int s_wcnt[kBlock / 32];
+    __shared__ StageSmem sm;
     __shared__ float s_imp[REPORT ? kBlock : 1];
     __shared__ uint32_t s_maxw[REPORT ? kBlock : 1];
     const int nthreads = blockDim.x;
@@ -379,6 +376,8 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
     const int rpw = 32 / bw;
     const uint32_t wrows = (((1u << rpw) - 1u) << ((threadIdx.x >> 5) * rpw)) << 16;
 
+    const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
+    const uint32_t a_gid = smem_base(sm.gid), a_idx = smem_base(sm.idx);
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, wmax = 0.0f;
     int32_t amax_gid = -1, last = -1;
     bool done = !inside;
@@ -390,14 +389,14 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
         for (uint32_t base = start; base < end; base += nthreads) {
             if (__syncthreads_count(!done) == 0) break;
             const int cnt = stage_batch([&](int t) { return (int)(base + t); }, (int)min((uint32_t)nthreads, end - base),
-                                        pair_gauss, rec, bx0, bx1, by0, by1, s_r0, s_r1, s_r2, s_gid, s_idx, s_wcnt);
+                                        pair_gauss, rec, bx0, bx1, by0, by1, sm);
             if (!REPORT) {
                 for (int j = 0; j < cnt && !done; ++j) {
                     float alpha, g2d, dx, dy;
                     bool clamped;
-                    const float4 r1 = s_r1[j];
+                    const float4 r1 = lds_f4(a_r1 + 16u * j);
                     if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
-                    const float4 r0 = s_r0[j];
+                    const float4 r0 = lds_f4(a_r0 + 16u * j);
                     if (!gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
                     const float next = T * (1.0f - alpha);
                     if (THR && next < tmin) {
@@ -405,15 +404,15 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                         break;
                     }
                     const float w = T * alpha;
-                    const float4 r2 = s_r2[j];
+                    const float4 r2 = lds_f4(a_r2 + 16u * j);
                     acc0 = acc0 + w * r2.x;
                     acc1 = acc1 + w * r2.y;
                     acc2 = acc2 + w * r2.z;
                     if (w > wmax) {
                         wmax = w;
-                        amax_gid = (int32_t)s_gid[j];
+                        amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
                     }
-                    last = s_idx[j];
+                    last = (int32_t)lds_u32(a_idx + 4u * j);
                     T = next;
                 }
             } else {
@@ -421,27 +420,27 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                 for (int j = 0; j < cnt; ++j) {
                     if (__all_sync(0xffffffffu, done)) break;
                     float w = 0.0f;
-                    const float4 r1 = s_r1[j];
+                    const float4 r1 = lds_f4(a_r1 + 16u * j);
                     if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
                     if (!done) {
                         float alpha, g2d, dx, dy;
                         bool clamped;
-                        const float4 r0 = s_r0[j];
+                        const float4 r0 = lds_f4(a_r0 + 16u * j);
                         if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
                             const float next = T * (1.0f - alpha);
                             if (THR && next < tmin) {
                                 done = true;
                             } else {
                                 w = T * alpha;
-                                const float4 r2 = s_r2[j];
+                                const float4 r2 = lds_f4(a_r2 + 16u * j);
                                 acc0 = acc0 + w * r2.x;
                                 acc1 = acc1 + w * r2.y;
                                 acc2 = acc2 + w * r2.z;
                                 if (w > wmax) {
                                     wmax = w;
-                                    amax_gid = (int32_t)s_gid[j];
+                                    amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
                                 }
-                                last = s_idx[j];
+                                last = (int32_t)lds_u32(a_idx + 4u * j);
                                 T = next;
                             }
                         }
@@ -457,7 +456,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                 }
                 __syncthreads();
                 if (tid < cnt && s_maxw[tid] != 0u) {
-                    const uint32_t gid = s_gid[tid];
+                    const uint32_t gid = sm.gid[tid];
                     atomicAdd(&out.importance[gid], s_imp[tid]);
                     atomicMax(reinterpret_cast<uint32_t*>(&out.max_weight[gid]), s_maxw[tid]);
                     s_imp[tid] = 0.0f;
