@@ -94,8 +94,11 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
     const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
     const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
-    const int px = bx0 + tid % bw;
-    const int py = by0 + tid / bw;
+    // pixel of this thread: warps own compact patches (8 x 4 for 16 x 16 blocks, 8 x 4 for 8 x 8)
+    const int lx = ((tid >> 5) & ((bw >> 3) - 1)) * 8 + (tid & 7);
+    const int ly = ((tid >> 5) / (bw >> 3)) * 4 + ((tid & 31) >> 3);
+    const int px = bx0 + lx;
+    const int py = by0 + ly;
     const bool inside = px < cp.width && py < cp.height;
     const size_t pix = inside ? (size_t)py * cp.width + px : 0;
 
@@ -136,9 +139,8 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
 
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
-    const uint32_t mybits = (1u << (tid % bw)) | (1u << (16 + tid / bw));
-    const int rpw = 32 / bw;
-    const uint32_t wrows = (((1u << rpw) - 1u) << (warp * rpw)) << 16;
+    const uint32_t mybits = (1u << lx) | (1u << (16 + ly));
+    const uint32_t wcols = 0xffu << (lx & ~7), wrows = 0xfu << (16 + (ly & ~3));
     const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
     const uint32_t a_idx = smem_base(sm.idx), a_g = smem_base(s_g);
     float T = inside ? t_final[pix] : 1.0f;
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
             const int idx = (int)lds_u32(a_idx + 4u * j);
             if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
             const float4 r1 = lds_f4(a_r1 + 16u * j);
-            if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (warp-uniform)
+            if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
             float v[10];
 #pragma unroll
             for (int k = 0; k < 10; ++k) v[k] = 0.0f;

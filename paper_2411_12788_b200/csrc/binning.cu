@@ -112,15 +112,22 @@ __global__ void __launch_bounds__(kBinThreads) seg_setup_kernel(const uint32_t* 
              tile_base, s_warp);
 }
 
-// Count (EMIT = false) or emit (EMIT = true) pass over one segment of one supertile list.
+// Count (EMIT = false) or emit (EMIT = true) pass over one segment of one supertile list.  The
+// segment is walked in chunks of kBinThreads entries; per local tile f, a warp ballot gives each
+// entry its rank among the chunk's entries covering f.  Emitted ids are staged per tile in shared
+// memory and written out as contiguous runs (coalesced), since a tile's entries of one chunk are
+// consecutive in its list.
 template <bool EMIT>
 __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
     const uint32_t* __restrict__ st_ranges, const uint32_t* __restrict__ seg_start, int n_st,
     const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ st_gauss, const uint2* __restrict__ rect_ref,
     int ts, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ slots, uint32_t* __restrict__ pair_gauss) {
-    __shared__ uint32_t s_wc[kBinThreads / 32][kSTT];
+    constexpr int kWarpsB = kBinThreads / 32;
+    __shared__ uint32_t s_wc[kWarpsB][kSTT];   // per-warp counts, then exclusive prefixes over warps
+    __shared__ uint32_t s_tot[kSTT + 1];       // chunk totals per tile, then exclusive prefix over tiles
     __shared__ uint32_t s_run[kSTT];
     __shared__ uint32_t s_base[kSTT];
+    __shared__ uint32_t s_out[EMIT ? kSTT * kBinThreads : 1];
     const int b = blockIdx.x;
     if (b >= (int)seg_start[n_st]) return;
     int lo_st = 0, hi_st = n_st;  // largest st with seg_start[st] <= b
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
             const TileRect t = tile_rect(rect_ref[gid], ts);
             const int lx0 = max(t.tx0 - tx_base, 0), lx1 = min(t.tx1 - tx_base, kST - 1);
             const int ly0 = max(t.ty0 - ty_base, 0), ly1 = min(t.ty1 - ty_base, kST - 1);
-            for (int ly = ly0; ly <= ly1; ++ly)
-                for (int lx = lx0; lx <= lx1; ++lx) cover |= 1u << (ly * kST + lx);
+            const uint32_t row = ((1u << (lx1 + 1)) - 1u) & ~((1u << lx0) - 1u);
+            for (int ly = ly0; ly <= ly1; ++ly) cover |= row << (ly * kST);
         }
         uint32_t rank[kSTT];
 #pragma unroll
@@ -164,21 +171,46 @@ __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
             if (lane == 0) s_wc[warp][f] = __popc(m);
         }
         __syncthreads();
-        if (EMIT && cover) {
+        if (tid < kSTT) {  // exclusive prefix over warps per tile; chunk total per tile
+            uint32_t run = 0;
 #pragma unroll
-            for (int f = 0; f < kSTT; ++f) {
-                if ((cover >> f) & 1u) {
-                    uint32_t pre = 0;
-                    for (int w = 0; w < warp; ++w) pre += s_wc[w][f];
-                    pair_gauss[s_base[f] + s_run[f] + pre + rank[f]] = gid;
-                }
+            for (int w = 0; w < kWarpsB; ++w) {
+                const uint32_t cw = s_wc[w][tid];
+                s_wc[w][tid] = run;
+                run += cw;
             }
+            s_tot[tid] = run;
         }
         __syncthreads();
-        if (tid < kSTT) {
-            uint32_t tot = 0;
-            for (int w = 0; w < kBinThreads / 32; ++w) tot += s_wc[w][tid];
-            s_run[tid] += tot;
+        if (EMIT) {
+            if (cover) {
+#pragma unroll
+                for (int f = 0; f < kSTT; ++f)
+                    if ((cover >> f) & 1u) s_out[f * kBinThreads + s_wc[warp][f] + rank[f]] = gid;
+            }
+            if (tid == 0) {  // exclusive prefix of the chunk totals over tiles (flat run layout)
+                uint32_t acc = 0;
+                for (int f = 0; f < kSTT; ++f) {
+                    const uint32_t t = s_tot[f];
+                    s_tot[f] = acc;
+                    acc += t;
+                }
+                s_tot[kSTT] = acc;
+            }
+            __syncthreads();
+            const uint32_t total = s_tot[kSTT];
+            for (uint32_t q = tid; q < total; q += kBinThreads) {
+                int f = 0;  // tile of flat index q: last f with s_tot[f] <= q
+#pragma unroll
+                for (int step = kSTT / 2; step > 0; step >>= 1)
+                    if (f + step < kSTT && s_tot[f + step] <= q) f += step;
+                const uint32_t i = q - s_tot[f];
+                pair_gauss[s_base[f] + s_run[f] + i] = s_out[f * kBinThreads + i];
+            }
+            __syncthreads();
+            if (tid < kSTT) s_run[tid] += s_tot[tid + 1] - s_tot[tid];
+        } else {
+            if (tid < kSTT) s_run[tid] += s_tot[tid];
         }
         __syncthreads();
     }

@@ -275,11 +275,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
                             32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
            "depth sort");
         const uint32_t* order = alt ? ctx->vals[1].as<uint32_t>() : vals;
-        CK(launch_gather_counts(lc, order, ctx->tile_counts.as<uint32_t>(), ctx->counts_sorted.as<uint32_t>(), n),
-           "gather counts");
-        CK(exclusive_scan_u32(lc, ctx->counts_sorted.as<uint32_t>(), ctx->offsets.as<uint32_t>(), (uint64_t)n,
-                              ctx->scan_tmp.as<uint32_t>(), d_counters + 1),
-           "scan counts");
+        CK(exclusive_scan_gather_u32(lc, ctx->tile_counts.as<uint32_t>(), order, ctx->offsets.as<uint32_t>(),
+                                     (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), d_counters + 1),
+           "scan supertile counts");
         CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
         CK(cudaStreamSynchronize(s), "sync counts");
         n_surv = (int)ctx->host_counters[0];

@@ -365,16 +365,19 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
     const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
     const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
     const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
-    const int px = bx0 + tid % bw;
-    const int py = by0 + tid / bw;
+    // pixel of this thread: warps own compact patches (8 x 4 for 16 x 16 blocks, 8 x 4 for 8 x 8)
+    const int lx = ((tid >> 5) & ((bw >> 3) - 1)) * 8 + (tid & 7);
+    const int ly = ((tid >> 5) / (bw >> 3)) * 4 + ((tid & 31) >> 3);
+    const int px = bx0 + lx;
+    const int py = by0 + ly;
     const bool inside = px < cp.width && py < cp.height;
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min, tmin = cp.transmittance_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
     // this pixel's bits in the staged masks, and this warp's rows (32 / bw rows per warp)
-    const uint32_t mybits = (1u << (tid % bw)) | (1u << (16 + tid / bw));
-    const int rpw = 32 / bw;
-    const uint32_t wrows = (((1u << rpw) - 1u) << ((threadIdx.x >> 5) * rpw)) << 16;
+    const uint32_t mybits = (1u << lx) | (1u << (16 + ly));
+    // this warp's columns and rows in the staged masks: skip an entry when either misses
+    const uint32_t wcols = 0xffu << (lx & ~7), wrows = 0xfu << (16 + (ly & ~3));
 
     const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
     const uint32_t a_gid = smem_base(sm.gid), a_idx = smem_base(sm.idx);
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                     float alpha, g2d, dx, dy;
                     bool clamped;
                     const float4 r1 = lds_f4(a_r1 + 16u * j);
-                    if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
+                    if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
                     const float4 r0 = lds_f4(a_r0 + 16u * j);
                     if (!gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
                     const float next = T * (1.0f - alpha);
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const 
                     if (__all_sync(0xffffffffu, done)) break;
                     float w = 0.0f;
                     const float4 r1 = lds_f4(a_r1 + 16u * j);
-                    if (!(__float_as_uint(r1.z) & wrows)) continue;  // no row of this warp (uniform)
+                    if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
                     if (!done) {
                         float alpha, g2d, dx, dy;
                         bool clamped;

@@ -39,6 +39,9 @@ size_t scan_temp_words(uint64_t n);
 size_t radix_hist_words(uint64_t n, int bits);
 cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n,
                                uint32_t* tmp, uint32_t* total_dev);
+// out[i] = sum_{r < i} in[idx[r]] (gather fused into the single-pass scan)
+cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const uint32_t* idx, uint32_t* out,
+                                      uint64_t n, uint32_t* tmp, uint32_t* total_dev);
 // Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result lands in keys/vals
 // or, when *result_in_alt, in keys_alt/vals_alt.
 cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,

@@ -1,16 +1,22 @@
-// sort.cu — device-wide exclusive scan and stable LSD radix sort (hand-written, sm_100a).
+// sort.cu — single-pass exclusive scan and Onesweep-style stable LSD radix sort (hand-written,
+// sm_100a).
 //
 // Replaces the reference's std::sort of ProjectedGaussian by (depth_mean, index)
-// (rasterizer.cpp:85-88) and the push_back binning of detail::bin_tiles
-// (rasterizer.hpp:156-174).  The per-tile lists come out of two stable sorts:
-//   1. the N depth keys (IEEE bits of depth_mean > 0, monotone as uint32; culled Gaussians
-//      carry 0xFFFFFFFF) with Gaussian ids as values, in index order  -> (depth, index) order;
-//   2. the P (tile id, Gaussian id) pairs, emitted in that depth order, by tile id only.
-// Stability of both passes reproduces the reference lists exactly.
+// (rasterizer.cpp:85-88).  The N depth keys (IEEE bits of depth_mean > 0, monotone as uint32;
+// culled Gaussians carry 0xFFFFFFFF) are sorted stably with the Gaussian ids as values, in index
+// order, which yields exactly the reference's (depth, index) order; the same sort orders the
+// (supertile, Gaussian) pairs of binning.cu.
 //
-// Radix pass = upsweep (per-CTA digit histogram, digit-major) + exclusive scan of the histogram
-// + downsweep (warp-synchronous stable ranking with __match_any_sync, scatter).  4096 keys per
-// CTA (256 threads x 16), digits of up to 8 bits.
+// Scan: one kernel.  Tiles of 4096 items take their tile id from an atomic counter (so every
+// predecessor is already running: forward progress without relying on block scheduling order),
+// publish their aggregate, then look back over predecessors' (flag, value) words (decoupled
+// look-back) for the exclusive prefix.
+//
+// Radix sort: one histogram kernel computes the digit histograms of every pass in a single read
+// of the keys; then each pass is one kernel: tiles rank their keys per warp with __match_any_sync
+// (stable), publish per-digit tile counts, look back per digit (one thread per digit) for the
+// tile's global digit offsets, and scatter.  2 + passes launches per sort instead of 5 per pass.
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -20,16 +26,39 @@ namespace splat_b200 {
 
 namespace {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;  // 4096
+constexpr int kWarps = kThreads / 32;
 
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
-constexpr int kSortWarps = kSortThreads / 32;
+// 64-bit look-back words: bits 62-63 flag (1 aggregate, 2 inclusive prefix), low bits value.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v, int lane) {
+// 32-bit look-back words for the per-digit radix status: bits 30-31 flag, low 30 bits value.
+constexpr uint32_t kFlagAgg32 = 1u << 30;
+constexpr uint32_t kFlagInc32 = 2u << 30;
+constexpr uint32_t kValMask32 = (1u << 30) - 1;
+
+__device__ __forceinline__ void st_relaxed64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
@@ -38,142 +67,156 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v, int lane) {
     return v;
 }
 
-// Block-wide exclusive scan of one value per thread; returns the block total in *total.
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
-    __shared__ uint32_t s_warp[kScanThreads / 32];
+// Block-wide exclusive scan of one value per thread (kThreads threads); *total gets the sum.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* s_warp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t inc = warp_inclusive_scan(v, lane);
+    const uint32_t inc = warp_incl_scan(v, lane);
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
-        w = warp_inclusive_scan(w, lane);
-        if (lane < kScanThreads / 32) s_warp[lane] = w;
-    }
-    __syncthreads();
-    const uint32_t warp_off = warp > 0 ? s_warp[warp - 1] : 0u;
-    *total = s_warp[kScanThreads / 32 - 1];
-    __syncthreads();
-    return warp_off + inc - v;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in,
-                                                                    uint32_t n,
-                                                                    uint32_t* __restrict__ block_sums) {
-    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-    uint32_t s = 0;
+    uint32_t off = 0, tot = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
-        if (i < n) s += in[i];
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_warp[w];
+        off += w < warp ? c : 0u;
+        tot += c;
     }
-    uint32_t total;
-    block_exclusive_scan(s, &total);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+    *total = tot;
+    __syncthreads();
+    return off + inc - v;
 }
 
-// Single CTA: exclusive scan of the block sums in place; writes the grand total.
-__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(uint32_t* __restrict__ sums,
-                                                                  uint32_t nblocks,
-                                                                  uint32_t* __restrict__ total_out) {
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < nblocks; base += kScanThreads) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t v = i < nblocks ? sums[i] : 0u;
-        uint32_t total;
-        const uint32_t ex = block_exclusive_scan(v, &total);
-        if (i < nblocks) sums[i] = carry + ex;
-        carry += total;
-    }
-    if (threadIdx.x == 0 && total_out) *total_out = carry;
-}
-
-// Each thread owns kScanItems consecutive elements (blocked arrangement) for a local serial
-// scan, then a block scan of the thread totals.
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* __restrict__ in,
-                                                                  uint32_t* __restrict__ out, uint32_t n,
-                                                                  const uint32_t* __restrict__ block_offs) {
-    __shared__ uint32_t s_data[kScanTile];
-    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+// ---- single-pass scan -------------------------------------------------------------------------
+// tmp layout (u64 words): [0] tile counter, [1 + t] look-back word of tile t.
+template <bool GATHER>
+__global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t* __restrict__ in,
+                                                                const uint32_t* __restrict__ idx,
+                                                                uint32_t* __restrict__ out, uint64_t n,
+                                                                uint64_t* __restrict__ tmp,
+                                                                uint32_t* __restrict__ total_out) {
+    __shared__ uint32_t s_data[kTile];
+    __shared__ uint32_t s_warp[kWarps];
+    __shared__ uint64_t s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned long long*>(tmp), 1ull);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * kTile;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const int li = k * kScanThreads + threadIdx.x;
+    for (int k = 0; k < kItems; ++k) {
+        const int li = k * kThreads + threadIdx.x;
         const uint64_t i = base + li;
-        s_data[li] = i < n ? in[i] : 0u;
+        s_data[li] = i < n ? (GATHER ? in[idx[i]] : in[i]) : 0u;
     }
     __syncthreads();
-    uint32_t local[kScanItems];
+    uint32_t local[kItems];
     uint32_t s = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < kItems; ++k) {
         local[k] = s;
-        s += s_data[threadIdx.x * kScanItems + k];
+        s += s_data[threadIdx.x * kItems + k];
     }
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan(s, &total) + block_offs[blockIdx.x];
+    uint32_t agg;
+    const uint32_t ex = block_exclusive_scan(s, &agg, s_warp);
+    uint64_t* status = tmp + 1;
+    if (threadIdx.x < 32) {  // warp-cooperative look-back: 32 predecessors per round trip
+        const int lane = threadIdx.x;
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_relaxed64(&status[0], kFlagInc | agg);
+        } else {
+            if (lane == 0) st_relaxed64(&status[tile], kFlagAgg | agg);
+            int64_t hi_p = (int64_t)tile - 1;
+            while (true) {
+                const int64_t p = hi_p - lane;
+                const uint64_t w = p >= 0 ? ld_relaxed64(&status[p]) : kFlagInc;
+                if (__any_sync(0xffffffffu, (w >> 62) == 0)) continue;
+                const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+                const int first_inc = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+                uint64_t v = lane <= first_inc ? (w & kValMask) : 0ull;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) s_data[threadIdx.x * kScanItems + k] = ex + local[k];
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (inc) break;
+                hi_p -= 32;
+            }
+            if (lane == 0) st_relaxed64(&status[tile], kFlagInc | (prefix + agg));
+        }
+        if (lane == 0) {
+            s_prefix = prefix;
+            const uint64_t ntiles = (n + kTile - 1) / kTile;
+            if (total_out && tile == ntiles - 1) *total_out = (uint32_t)(prefix + agg);
+        }
+    }
+    __syncthreads();
+    const uint32_t off = (uint32_t)s_prefix + ex;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) s_data[threadIdx.x * kItems + k] = off + local[k];
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const int li = k * kScanThreads + threadIdx.x;
+    for (int k = 0; k < kItems; ++k) {
+        const int li = k * kThreads + threadIdx.x;
         const uint64_t i = base + li;
         if (i < n) out[i] = s_data[li];
     }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(kSortThreads) radix_upsweep_kernel(const uint32_t* __restrict__ keys,
-                                                                      uint32_t n, int shift,
-                                                                      uint32_t* __restrict__ hist,
-                                                                      uint32_t nblocks) {
-    constexpr int BINS = 1 << BITS;
-    __shared__ uint32_t s_hist[kSortWarps][BINS];
-    for (int i = threadIdx.x; i < kSortWarps * BINS; i += kSortThreads) (&s_hist[0][0])[i] = 0u;
+// ---- radix sort -------------------------------------------------------------------------------
+// Digit histograms of all passes (passes x 256 bins, digit width `bits`) in one read.
+__global__ void __launch_bounds__(kThreads) radix_histogram_kernel(const uint32_t* __restrict__ keys, uint64_t n,
+                                                                  int begin_bit, int bits, int passes,
+                                                                  uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_hist[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_hist[0][0])[i] = 0u;
     __syncthreads();
-    const int warp = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
-    for (int k = 0; k < kSortItems; ++k) {
-        const uint64_t i = base + (uint64_t)k * kSortThreads + threadIdx.x;
-        if (i < n) atomicAdd(&s_hist[warp][(keys[i] >> shift) & (BINS - 1)], 1u);
+    const uint32_t mask = (1u << bits) - 1u;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kThreads) {
+        const uint32_t k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (begin_bit + p * bits)) & mask], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < BINS; d += kSortThreads) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) s += s_hist[w][d];
-        hist[(uint64_t)d * nblocks + blockIdx.x] = s;
+    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
+        const uint32_t v = (&s_hist[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
     }
 }
 
+// One stable pass.  status: [ntiles][BINS] look-back words (zeroed); counter: tile id counter.
 template <int BITS>
-__global__ void __launch_bounds__(kSortThreads) radix_downsweep_kernel(
-    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-    const uint32_t* __restrict__ offs, uint32_t nblocks) {
+__global__ void __launch_bounds__(kThreads) radix_onesweep_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ hist,
+    uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
     constexpr int BINS = 1 << BITS;
-    constexpr int PER_WARP = kSortTile / kSortWarps;  // 512 consecutive keys per warp
-    __shared__ uint32_t s_cnt[kSortWarps][BINS];
-    for (int i = threadIdx.x; i < kSortWarps * BINS; i += kSortThreads) (&s_cnt[0][0])[i] = 0u;
+    constexpr int PER_WARP = kTile / kWarps;  // 512 consecutive keys per warp
+    __shared__ uint32_t s_cnt[kWarps][BINS];
+    __shared__ uint32_t s_glob[BINS];
+    __shared__ uint32_t s_warp[kWarps];
+    __shared__ uint32_t s_tile;
+    for (int i = threadIdx.x; i < kWarps * BINS; i += kThreads) (&s_cnt[0][0])[i] = 0u;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    {  // global exclusive digit offsets of this pass
+        uint32_t tot;
+        const uint32_t v = threadIdx.x < BINS ? hist[threadIdx.x] : 0u;
+        const uint32_t ex = block_exclusive_scan(v, &tot, s_warp);  // contains __syncthreads
+        if (threadIdx.x < BINS) s_glob[threadIdx.x] = ex;
+    }
+    const uint32_t tile = s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t wbase = (uint64_t)blockIdx.x * kSortTile + (uint64_t)warp * PER_WARP;
-    uint32_t k[kSortItems], v[kSortItems];
+    const uint64_t wbase = (uint64_t)tile * kTile + (uint64_t)warp * PER_WARP;
+    uint32_t k[kItems], v[kItems];
 #pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
+    for (int r = 0; r < kItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         k[r] = i < n ? keys_in[i] : 0u;
         v[r] = i < n ? vals_in[i] : 0u;
     }
     __syncthreads();
     const unsigned lt = lanemask_lt();
-    uint32_t rank[kSortItems];
+    uint32_t rank[kItems];
 #pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
+    for (int r = 0; r < kItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         const bool valid = i < n;
         const uint32_t d = (k[r] >> shift) & (BINS - 1);
-        // invalid lanes get unique non-digit labels so they form singleton groups
         const uint32_t label = valid ? d : (0x80000000u | (uint32_t)lane);
         const unsigned peers = __match_any_sync(0xffffffffu, label);
         const uint32_t old = valid ? s_cnt[warp][d] : 0u;
@@ -183,18 +226,56 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep_kernel(
         rank[r] = old + __popc(peers & lt);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < BINS; d += kSortThreads) {
-        uint32_t run = offs[(uint64_t)d * nblocks + blockIdx.x];
+    for (int d = threadIdx.x; d < BINS; d += kThreads) {
+        uint32_t c = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t c = s_cnt[w][d];
+        for (int w = 0; w < kWarps; ++w) c += s_cnt[w][d];
+        uint32_t* st = status + (uint64_t)tile * BINS + d;
+        uint32_t prefix = 0;
+        if (tile == 0) {
+            st_relaxed32(st, kFlagInc32 | c);
+        } else {
+            st_relaxed32(st, kFlagAgg32 | c);
+            // windowed look-back: kWin predecessors per round trip instead of one
+            constexpr int kWin = 16;
+            int64_t hi_p = (int64_t)tile - 1;
+            while (true) {
+                uint32_t w[kWin];
+#pragma unroll
+                for (int q = 0; q < kWin; ++q) {
+                    const int64_t p = hi_p - q;
+                    w[q] = p >= 0 ? ld_relaxed32(status + (uint64_t)p * BINS + d) : kFlagInc32;
+                }
+                bool ready = true;
+#pragma unroll
+                for (int q = 0; q < kWin; ++q) ready &= (w[q] >> 30) != 0;
+                if (!ready) continue;
+                uint32_t acc = 0;
+                bool done = false;
+#pragma unroll
+                for (int q = 0; q < kWin; ++q) {
+                    if (!done) {
+                        acc += w[q] & kValMask32;
+                        done = (w[q] >> 30) == 2;
+                    }
+                }
+                prefix += acc;
+                if (done) break;
+                hi_p -= kWin;
+            }
+            st_relaxed32(st, kFlagInc32 | (prefix + c));
+        }
+        uint32_t run = s_glob[d] + prefix;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t cw = s_cnt[w][d];
             s_cnt[w][d] = run;
-            run += c;
+            run += cw;
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
+    for (int r = 0; r < kItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         if (i < n) {
             const uint32_t d = (k[r] >> shift) & (BINS - 1);
@@ -206,90 +287,92 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep_kernel(
 }
 
 template <int BITS>
-cudaError_t radix_pass(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
-                       uint32_t n, int shift, uint32_t* hist, uint32_t* scan_tmp) {
-    const uint32_t nblocks = (n + kSortTile - 1) / kSortTile;
-    constexpr uint32_t BINS = 1u << BITS;
-    {
-        LaunchScope ls_(lc, "radix_upsweep");
-        radix_upsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, n, shift, hist, nblocks);
-    }
-    lc.count++;
-    cudaError_t e = exclusive_scan_u32(lc, hist, hist, BINS * nblocks, scan_tmp, nullptr);
-    if (e != cudaSuccess) return e;
-    {
-        LaunchScope ls_(lc, "radix_downsweep");
-        radix_downsweep_kernel<BITS><<<nblocks, kSortThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, nblocks);
-    }
-    lc.count++;
-    return cudaGetLastError();
+void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n,
+                     int shift, const uint32_t* hist, uint32_t* status, uint32_t* counter) {
+    const uint32_t ntiles = (n + kTile - 1) / kTile;
+    radix_onesweep_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, status, counter);
 }
 
 }  // namespace
 
 size_t scan_temp_words(uint64_t n) {
-    const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-    return (size_t)nb + 1;
+    const uint64_t nt = (n + kTile - 1) / kTile;
+    return (size_t)(2 * (nt + 1) + 2);  // u64 counter + u64 status per tile, in 32-bit words
 }
 
 size_t radix_hist_words(uint64_t n, int bits) {
-    const uint64_t nb = (n + kSortTile - 1) / kSortTile;
-    return (size_t)(nb << bits);
+    (void)bits;
+    const uint64_t nt = (n + kTile - 1) / kTile;
+    return (size_t)(4 * 256 + 4 + 4 * nt * 256);  // hist [4][256] + counters [4] + status [4][nt][256]
 }
 
-cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n,
-                               uint32_t* tmp, uint32_t* total_dev) {
+cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tmp,
+                               uint32_t* total_dev) {
+    return exclusive_scan_gather_u32(lc, in, nullptr, out, n, tmp, total_dev);
+}
+
+cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const uint32_t* idx, uint32_t* out,
+                                      uint64_t n, uint32_t* tmp, uint32_t* total_dev) {
     if (n == 0) {
         if (total_dev) return cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), lc.stream);
         return cudaSuccess;
     }
-    const uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
-    {
-        LaunchScope ls_(lc, "scan_reduce");
-        scan_reduce_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, (uint32_t)n, tmp);
-    }
-    {
-        LaunchScope ls_(lc, "scan_sums");
-        scan_sums_kernel<<<1, kScanThreads, 0, lc.stream>>>(tmp, nb, total_dev);
-    }
-    {
-        LaunchScope ls_(lc, "scan_down");
-        scan_down_kernel<<<nb, kScanThreads, 0, lc.stream>>>(in, out, (uint32_t)n, tmp);
-    }
-    lc.count += 3;
+    const uint64_t nt = (n + kTile - 1) / kTile;
+    cudaError_t e = cudaMemsetAsync(tmp, 0, 8 * (nt + 1), lc.stream);
+    if (e != cudaSuccess) return e;
+    LaunchScope s(lc, "scan");
+    uint64_t* t64 = reinterpret_cast<uint64_t*>(tmp);
+    if (idx)
+        scan_lookback_kernel<true><<<(unsigned)nt, kThreads, 0, lc.stream>>>(in, idx, out, n, t64, total_dev);
+    else
+        scan_lookback_kernel<false><<<(unsigned)nt, kThreads, 0, lc.stream>>>(in, idx, out, n, t64, total_dev);
+    lc.count++;
     return cudaGetLastError();
 }
 
-cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,
-                             uint32_t* vals_alt, uint64_t n, int begin_bit, int end_bit, uint32_t* hist,
-                             uint32_t* scan_tmp, bool* result_in_alt) {
+cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                             uint64_t n, int begin_bit, int end_bit, uint32_t* hist, uint32_t* scan_tmp,
+                             bool* result_in_alt) {
+    (void)scan_tmp;
     *result_in_alt = false;
     if (n == 0 || end_bit <= begin_bit) return cudaSuccess;
-    uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     const int total = end_bit - begin_bit;
     const int passes = (total + 7) / 8;
     const int bits = (total + passes - 1) / passes;  // balanced digits, <= 8
-    int shift = begin_bit;
+    const uint64_t nt = (n + kTile - 1) / kTile;
+    uint32_t* counters = hist + 4 * 256;
+    uint32_t* status = counters + 4;
+    cudaError_t e = cudaMemsetAsync(hist, 0, 4 * (size_t)(4 * 256 + 4 + (size_t)passes * nt * 256), lc.stream);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope s(lc, "radix_histogram");
+        const unsigned grid =
+            (unsigned)std::min<uint64_t>((n + kThreads * 8 - 1) / (kThreads * 8), (uint64_t)lc.num_sms * 4);
+        radix_histogram_kernel<<<grid, kThreads, 0, lc.stream>>>(keys, n, begin_bit, bits, passes, hist);
+        lc.count++;
+    }
+    uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     for (int p = 0; p < passes; ++p) {
-        const int b = (shift + bits <= end_bit) ? bits : end_bit - shift;
-        cudaError_t e;
-        switch (b) {
-            case 1: e = radix_pass<1>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 2: e = radix_pass<2>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 3: e = radix_pass<3>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 4: e = radix_pass<4>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 5: e = radix_pass<5>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 6: e = radix_pass<6>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            case 7: e = radix_pass<7>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
-            default: e = radix_pass<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, hist, scan_tmp); break;
+        const int shift = begin_bit + p * bits;
+        const uint32_t* h = hist + 256 * p;
+        uint32_t* st = status + (size_t)p * nt * 256;
+        LaunchScope s(lc, "radix_onesweep");
+        switch (bits) {
+            case 1: launch_onesweep<1>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 2: launch_onesweep<2>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 3: launch_onesweep<3>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 4: launch_onesweep<4>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 5: launch_onesweep<5>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 6: launch_onesweep<6>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 7: launch_onesweep<7>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            default: launch_onesweep<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
         }
-        if (e != cudaSuccess) return e;
+        lc.count++;
         std::swap(ki, ko);
         std::swap(vi, vo);
         *result_in_alt = !*result_in_alt;
-        shift += b;
     }
-    return cudaSuccess;
+    return cudaGetLastError();
 }
 
 }  // namespace splat_b200
