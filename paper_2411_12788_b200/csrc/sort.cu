@@ -28,8 +28,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096
+constexpr int kTile = kThreads * kItems;  // 4096 (scan)
 constexpr int kWarps = kThreads / 32;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kThreads * kSortItems;  // 2048 (radix passes: more CTAs, fewer registers)
 
 // 64-bit look-back words: bits 62-63 flag (1 aggregate, 2 inclusive prefix), low bits value.
 constexpr uint64_t kFlagAgg = 1ull << 62;
@@ -164,8 +166,8 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
 __global__ void __launch_bounds__(kThreads) radix_histogram_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                                                                   int begin_bit, int bits, int passes,
                                                                   uint32_t* __restrict__ hist) {
-    __shared__ uint32_t s_hist[4][256];
-    for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_hist[0][0])[i] = 0u;
+    __shared__ uint32_t s_hist[4][512];
+    for (int i = threadIdx.x; i < 4 * 512; i += kThreads) (&s_hist[0][0])[i] = 0u;
     __syncthreads();
     const uint32_t mask = (1u << bits) - 1u;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kThreads) {
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(kThreads) radix_histogram_kernel(const uint32_
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (begin_bit + p * bits)) & mask], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
+    for (int i = threadIdx.x; i < passes * 512; i += kThreads) {
         const uint32_t v = (&s_hist[0][0])[i];
         if (v) atomicAdd(&hist[i], v);
     }
@@ -186,34 +188,54 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_kernel(
     uint32_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ hist,
     uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
     constexpr int BINS = 1 << BITS;
-    constexpr int PER_WARP = kTile / kWarps;  // 512 consecutive keys per warp
+    constexpr int PER_WARP = kSortTile / kWarps;  // consecutive keys per warp
     __shared__ uint32_t s_cnt[kWarps][BINS];
     __shared__ uint32_t s_glob[BINS];
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint32_t s_tile;
+    // A pass whose digit is the same for every key (one histogram bin holds all n keys, e.g. the
+    // exponent byte of depths within one binade) is the identity permutation: copy.
+    bool trivial = false;
+    for (int d = threadIdx.x; d < BINS; d += kThreads) trivial |= hist[d] == n;
+    if (__syncthreads_or(trivial)) {
+        const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+        for (int r = threadIdx.x; r < kSortTile; r += kThreads) {
+            const uint64_t i = base + r;
+            if (i < n) {
+                keys_out[i] = keys_in[i];
+                vals_out[i] = vals_in[i];
+            }
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < kWarps * BINS; i += kThreads) (&s_cnt[0][0])[i] = 0u;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
-    {  // global exclusive digit offsets of this pass
-        uint32_t tot;
-        const uint32_t v = threadIdx.x < BINS ? hist[threadIdx.x] : 0u;
-        const uint32_t ex = block_exclusive_scan(v, &tot, s_warp);  // contains __syncthreads
-        if (threadIdx.x < BINS) s_glob[threadIdx.x] = ex;
+    {  // global exclusive digit offsets of this pass (BINS <= 2 * kThreads)
+        uint32_t tot0, tot1;
+        const uint32_t v0 = threadIdx.x < BINS ? hist[threadIdx.x] : 0u;
+        const uint32_t ex0 = block_exclusive_scan(v0, &tot0, s_warp);
+        if (threadIdx.x < BINS) s_glob[threadIdx.x] = ex0;
+        if (BINS > kThreads) {
+            const uint32_t v1 = threadIdx.x + kThreads < BINS ? hist[threadIdx.x + kThreads] : 0u;
+            const uint32_t ex1 = block_exclusive_scan(v1, &tot1, s_warp);
+            if (threadIdx.x + kThreads < BINS) s_glob[threadIdx.x + kThreads] = tot0 + ex1;
+        }
     }
     const uint32_t tile = s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t wbase = (uint64_t)tile * kTile + (uint64_t)warp * PER_WARP;
-    uint32_t k[kItems], v[kItems];
+    const uint64_t wbase = (uint64_t)tile * kSortTile + (uint64_t)warp * PER_WARP;
+    uint32_t k[kSortItems], v[kSortItems];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         k[r] = i < n ? keys_in[i] : 0u;
         v[r] = i < n ? vals_in[i] : 0u;
     }
     __syncthreads();
     const unsigned lt = lanemask_lt();
-    uint32_t rank[kItems];
+    uint32_t rank[kSortItems];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         const bool valid = i < n;
         const uint32_t d = (k[r] >> shift) & (BINS - 1);
@@ -275,7 +297,7 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_kernel(
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         if (i < n) {
             const uint32_t d = (k[r] >> shift) & (BINS - 1);
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_kernel(
 template <int BITS>
 void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n,
                      int shift, const uint32_t* hist, uint32_t* status, uint32_t* counter) {
-    const uint32_t ntiles = (n + kTile - 1) / kTile;
+    const uint32_t ntiles = (n + kSortTile - 1) / kSortTile;
     radix_onesweep_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, status, counter);
 }
 
@@ -302,8 +324,8 @@ size_t scan_temp_words(uint64_t n) {
 
 size_t radix_hist_words(uint64_t n, int bits) {
     (void)bits;
-    const uint64_t nt = (n + kTile - 1) / kTile;
-    return (size_t)(4 * 256 + 4 + 4 * nt * 256);  // hist [4][256] + counters [4] + status [4][nt][256]
+    const uint64_t nt = (n + kSortTile - 1) / kSortTile;
+    return (size_t)(4 * 512 + 4 + 4 * nt * 512);  // hist [4][512] + counters [4] + status [4][nt][512]
 }
 
 cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tmp,
@@ -337,12 +359,12 @@ cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint
     *result_in_alt = false;
     if (n == 0 || end_bit <= begin_bit) return cudaSuccess;
     const int total = end_bit - begin_bit;
-    const int passes = (total + 7) / 8;
-    const int bits = (total + passes - 1) / passes;  // balanced digits, <= 8
-    const uint64_t nt = (n + kTile - 1) / kTile;
-    uint32_t* counters = hist + 4 * 256;
+    const int passes = total <= 9 ? 1 : (total + 7) / 8;  // one 9-bit pass for small key ranges
+    const int bits = (total + passes - 1) / passes;       // balanced digits, <= 9
+    const uint64_t nt = (n + kSortTile - 1) / kSortTile;
+    uint32_t* counters = hist + 4 * 512;
     uint32_t* status = counters + 4;
-    cudaError_t e = cudaMemsetAsync(hist, 0, 4 * (size_t)(4 * 256 + 4 + (size_t)passes * nt * 256), lc.stream);
+    cudaError_t e = cudaMemsetAsync(hist, 0, 4 * (size_t)(4 * 512 + 4 + (size_t)passes * nt * 512), lc.stream);
     if (e != cudaSuccess) return e;
     {
         LaunchScope s(lc, "radix_histogram");
@@ -354,8 +376,8 @@ cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint
     uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     for (int p = 0; p < passes; ++p) {
         const int shift = begin_bit + p * bits;
-        const uint32_t* h = hist + 256 * p;
-        uint32_t* st = status + (size_t)p * nt * 256;
+        const uint32_t* h = hist + 512 * p;
+        uint32_t* st = status + (size_t)p * nt * 512;
         LaunchScope s(lc, "radix_onesweep");
         switch (bits) {
             case 1: launch_onesweep<1>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
@@ -365,7 +387,8 @@ cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint
             case 5: launch_onesweep<5>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
             case 6: launch_onesweep<6>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
             case 7: launch_onesweep<7>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            default: launch_onesweep<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 8: launch_onesweep<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            default: launch_onesweep<9>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
         }
         lc.count++;
         std::swap(ki, ko);
