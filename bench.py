@@ -246,8 +246,10 @@ def run_ours(args):
     trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=capi.GROUP_CENTERS, ctx=ctx, max_views=max(args.views, 1))
     V = args.views
 
+    from paper_2411_12788_b200.trainer import views_for as _views_for
+
     def views_for(step):
-        idx = [(step * world * V + rank * V + j) % RING for j in range(V)]
+        idx = _views_for(step, rank, world, V, RING)
         return [cams[i] for i in idx], [targets[i] for i in idx], idx
 
     stream = torch.cuda.current_stream()

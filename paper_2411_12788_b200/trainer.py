@@ -22,6 +22,26 @@ from .capi import Camera, RasterConfig, RenderOutputs, as_fp
 from .rasterizer import Context, DeviceGaussians, DeviceGrads, OptimState, _torch
 
 
+def views_for(step: int, rank: int, world: int, views_per_rank: int, ring: int) -> list[int]:
+    """Ring-view indices rank `rank` trains at `step`: consecutive blocks of `views_per_rank`,
+    rank-major within the step, wrapping around the ring (SURVEY.md §8e partitioning)."""
+    base = step * world * views_per_rank + rank * views_per_rank
+    return [(base + j) % ring for j in range(views_per_rank)]
+
+
+def pack_grads(g: dict) -> np.ndarray:
+    """ParamGrads as the packed all-reduce buffer [centers 3N | scales 3N | rot 4N | opac N | sh 48N]."""
+    return np.concatenate([np.asarray(g[k], np.float32).reshape(-1) for k in
+                           ("d_centers", "d_log_scales", "d_rotations", "d_opacity_logits", "d_sh")])
+
+
+def unpack_grads(flat: np.ndarray, n: int) -> dict:
+    o = np.cumsum([0, 3 * n, 3 * n, 4 * n, n, 48 * n])
+    return dict(d_centers=flat[o[0]:o[1]].reshape(n, 3), d_log_scales=flat[o[1]:o[2]].reshape(n, 3),
+                d_rotations=flat[o[2]:o[3]].reshape(n, 4), d_opacity_logits=flat[o[3]:o[4]],
+                d_sh=flat[o[4]:o[5]].reshape(n, 48))
+
+
 class ViewTrainer:
     def __init__(self, params: DeviceGaussians, adam: Optional[capi.AdamConfig] = None,
                  group_mask: int = capi.GROUP_ALL, cfg: Optional[RasterConfig] = None,
@@ -62,7 +82,7 @@ class ViewTrainer:
         for j, (cam, tgt) in enumerate(zip(cams, targets)):
             self.ctx.check(lib.splat_render(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), None, self.bg,
                                             C.byref(self._empty_out), None))
-            np_, = [C.c_int64()]
+            np_ = C.c_int64()
             lib.splat_forward_counts(h, None, C.byref(np_), None, None)
             self.pairs_last_step.append(np_.value)
             self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),

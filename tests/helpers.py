@@ -71,3 +71,26 @@ def small_scene(n=300, seed=5, w=64, h=48, dist=3.0, sh_degree=3):
 
 def exact_cfg():
     return RasterConfig(apply_thresholds=0)
+
+
+def load_golden(path):
+    """A tests/golden fixture -> (set, cam, cfg, bg, mask, d_color, data)."""
+    from paper_2411_12788_b200.capi import Camera
+    d = dict(np.load(path))
+    s = scenes.GaussianSet(d["centers"], d["log_scales"], d["rotations"], d["opacity_logits"], d["sh"],
+                           int(d["sh_degree"]))
+    cam = Camera()
+    cam.width, cam.height = (int(x) for x in d["cam_wh"])
+    cam.fx, cam.fy, cam.cx, cam.cy, cam.znear, cam.zfar = (float(x) for x in d["cam_intr"])
+    for i in range(9):
+        cam.rotation[i] = float(d["cam_R"][i])
+    for i in range(3):
+        cam.translation[i] = float(d["cam_t"][i])
+    c = d["cfg"]
+    cfg = RasterConfig(tile_size=int(c[0]), apply_thresholds=int(c[1]), transmittance_min=float(c[2]),
+                       contribution_min=float(c[3]), alpha_max=float(c[4]), lowpass=float(c[5]),
+                       radius_sigmas=float(c[6]))
+    return s, cam, cfg, tuple(float(x) for x in d["bg"]), d.get("mask"), d["d_color"], d
+
+
+GOLDEN = sorted((__import__("pathlib").Path(__file__).resolve().parent / "golden").glob("*.npz"))

@@ -1,0 +1,57 @@
+"""The shared exponential (include/splat_expf.h): accuracy, and splat_expf_core == splat_expf on
+the range the blend kernels use it for."""
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+SRC = r'''
+#include "splat_expf.h"
+#include <stdio.h>
+#include <stdlib.h>
+int main(void) {
+    long n = 0, over1ulp = 0, core_diff = 0;
+    /* every 61st float in [-103.9, 88.7]; exhaustive for core on every 7th float in [-87.3, 0] */
+    for (uint32_t u = 0; u < 0xFFFFFFFFu - 61; u += 61) {
+        float x; memcpy(&x, &u, 4);
+        if (!(x > -103.9f && x < 88.7f)) continue;
+        ++n;
+        float a = splat_expf(x);
+        float r = (float)exp((double)x);
+        int32_t ia, ir; memcpy(&ia, &a, 4); memcpy(&ir, &r, 4);
+        if (r != 0 && abs(ia - ir) > 1) ++over1ulp;
+    }
+    for (uint32_t u = 0x80000000u; u <= 0xC2AE9999u; u += 7) {
+        float x; memcpy(&x, &u, 4);
+        if (!(x >= -87.3f)) continue;
+        float a = splat_expf(x), b = splat_expf_core(x);
+        if (memcmp(&a, &b, 4)) ++core_diff;
+    }
+    printf("%ld %ld %ld\n", n, over1ulp, core_diff);
+    return 0;
+}
+'''
+
+
+def test_splat_expf_accuracy_and_core(tmp_path):
+    c = tmp_path / "t.c"
+    c.write_text(SRC)
+    exe = tmp_path / "t"
+    subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off", f"-I{ROOT / 'include'}", str(c), "-o", str(exe), "-lm"],
+                   check=True)
+    n, over, core = (int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split())
+    assert n > 10_000_000
+    assert over == 0, f"{over} samples off by more than 1 ulp"
+    assert core == 0, f"splat_expf_core differs from splat_expf on {core} samples"
+
+
+def test_oracle_exp_modes():
+    import sys
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import OracleLib
+    b, a = OracleLib("oracle", "B"), OracleLib("oracle", "A")
+    xs = np.linspace(-20, 5, 20001, dtype=np.float32)
+    gb = np.array([b.exp(float(x)) for x in xs], np.float32)
+    ga = np.array([a.exp(float(x)) for x in xs], np.float32)
+    assert np.all(np.abs(gb.view(np.int32) - ga.view(np.int32)) <= 1)
