@@ -37,8 +37,8 @@ REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_powe
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--views", type=int, default=1, help="ring views per rank per step")
     ap.add_argument("--gaussians", type=int, default=1_000_000)
@@ -167,7 +167,7 @@ class ClockSampler:
         q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -253,6 +253,10 @@ def run_ours(args):
         return [cams[i] for i in idx], [targets[i] for i in idx], idx
 
     stream = torch.cuda.current_stream()
+    # clocks are sampled from the start of the warm-up (GPU under the same load) to the end of the
+    # timed region
+    clocks = ClockSampler(device)
+    clocks.start()
     for st in range(args.warmup):
         c, t, _ = views_for(st)
         trainer.step(c, t)
@@ -261,9 +265,6 @@ def run_ours(args):
     # ---- device-timed region -----------------------------------------------------------------
     lib = ctx.lib
     lib.splat_profile_enable(ctx.h, 1)
-    clocks = ClockSampler(device)
-    clocks.start()
-    time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

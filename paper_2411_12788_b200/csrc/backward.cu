@@ -14,7 +14,6 @@ namespace splat_b200 {
 
 namespace {
 
-constexpr int kGradStride = 10;  // smem row stride (floats): conflict-free lane->value scatter
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -22,50 +21,43 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// Transpose-reduce of 10 per-lane values across the warp in 12 shuffles (instead of 50):
-// every level exchanges the half a lane does not keep.  On return, lane l holds the warp total
-// of value index *which, or *which = -1 when l holds padding / a duplicate.
-__device__ __forceinline__ float warp_transpose_reduce10(const float v[10], int lane, int* which) {
-    const bool a = lane & 16, b = lane & 8, c = lane & 4, d = lane & 2;
+// Transpose-reduce of 12 per-lane values (four groups of 3) across the warp in 18 shuffles
+// (a butterfly would take 60): the first two levels exchange the half a lane does not keep, the
+// last three reduce the 3 remaining values.  On return, lanes 0, 8, 16, 24 hold the warp totals of
+// groups 0, 1, 2, 3 (values 3g .. 3g+2) in out[0..2].
+__device__ __forceinline__ void warp_reduce12(const float v[12], int lane, float out[3]) {
+    const bool a = lane & 16, b = lane & 8;
     float u[6];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        const float send = a ? v[i] : v[5 + i];
-        const float keep = a ? v[5 + i] : v[i];
+    for (int i = 0; i < 6; ++i) {
+        const float send = a ? v[i] : v[6 + i];
+        const float keep = a ? v[6 + i] : v[i];
         u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    u[5] = 0.0f;
-    float w[4];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const float send = b ? u[i] : u[3 + i];
         const float keep = b ? u[3 + i] : u[i];
-        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-    w[3] = 0.0f;
-    float x[2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float send = c ? w[i] : w[2 + i];
-        const float keep = c ? w[2 + i] : w[i];
-        x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    const float send = d ? x[0] : x[1];
-    float y = (d ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
-    y += __shfl_xor_sync(0xffffffffu, y, 1);
-    const int oc = (c ? 2 : 0) + (d ? 1 : 0);
-    const int local = (b ? 3 : 0) + oc;
-    const bool valid = !(lane & 1) && local < 5 && oc < 3;
-    *which = valid ? (a ? 5 : 0) + local : -1;
-    return y;
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
+}
+
+__device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float z, float w) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
+                 : "memory");
 }
 
 // Blend backward (gradients.cpp:73-123): per pixel, walk the tile list back to front from the
 // pixel's last committed sample, re-evaluating the forward gates; b = colour behind the sample
 // (normalised), exactly the reference recursion; T_before = T_after / (1 - alpha).
 // Per staged Gaussian the 9 per-pixel contributions (d_mean2d 2, d_conic 3 (01 = 10),
-// d_opacity, d_colour 3) are warp-reduced, accumulated in shared memory, and flushed to the
-// per-Gaussian accumulator with three float4 atomics per (CTA, Gaussian).
+// d_opacity, d_colour 3) plus a commit count are warp-reduced and added straight to the
+// per-Gaussian accumulator with four red.global.add.v4.f32 per (warp, Gaussian): no shared
+// accumulation, no flush barrier.
 // With target != nullptr, dL/dC = sign(C - target)/n (l1_loss, loss.cpp:63-76) is fused in and
 // the CTA's L1 partial sum is written to loss_partials[block].
 template <bool THR>
@@ -80,7 +72,6 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                                                             float* __restrict__ loss_partials,
                                                             float4* __restrict__ grad2d) {
     __shared__ StageSmem sm;
-    __shared__ float s_g[kBlock * kGradStride];
     __shared__ float s_red[kBlock / 32];
     __shared__ int s_maxlast[kBlock / 32];
     const int nthreads = blockDim.x;
@@ -142,23 +133,22 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     const uint32_t mybits = (1u << lx) | (1u << (16 + ly));
     const uint32_t wcols = 0xffu << (lx & ~7), wrows = 0xfu << (16 + (ly & ~3));
     const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
-    const uint32_t a_idx = smem_base(sm.idx), a_g = smem_base(s_g);
+    const uint32_t a_idx = smem_base(sm.idx), a_gid = smem_base(sm.gid);
     float T = inside ? t_final[pix] : 1.0f;
     float b0 = bg0, b1 = bg1, b2 = bg2;
 
     for (int hi = block_last + 1; hi > (int)start; hi -= nthreads) {
         const int count = min(nthreads, hi - (int)start);
         const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1, sm);
-        for (int k = tid; k < cnt * kGradStride; k += nthreads) s_g[k] = 0.0f;
-        __syncthreads();
         for (int j = 0; j < cnt; ++j) {
             const int idx = (int)lds_u32(a_idx + 4u * j);
             if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
             const float4 r1 = lds_f4(a_r1 + 16u * j);
             if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
-            float v[10];
+            // v: (dmean.x, dmean.y, dconic00 | dconic01, dconic11, dopacity | dcolour rgb | commits)
+            float v[12];
 #pragma unroll
-            for (int k = 0; k < 10; ++k) v[k] = 0.0f;
+            for (int k = 0; k < 12; ++k) v[k] = 0.0f;
             bool committed = false;
             if (idx <= my_last) {
                 float alpha, g2d, dx, dy;
@@ -192,23 +182,15 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                 }
             }
             if (__any_sync(0xffffffffu, committed)) {
-                int which;
-                const float s = warp_transpose_reduce10(v, lane, &which);
-                if (which >= 0 && s != 0.0f) {
-                    const uint32_t a = a_g + 4u * (uint32_t)(j * kGradStride + which);
-                    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(a), "f"(s) : "memory");
+                float r[3];
+                warp_reduce12(v, lane, r);
+                if ((lane & 7) == 0) {
+                    const uint32_t gid = lds_u32(a_gid + 4u * j);
+                    red_add_v4(grad2d + 4 * (size_t)gid + (lane >> 3), r[0], r[1], r[2], 0.0f);
                 }
             }
         }
-        __syncthreads();
-        if (tid < cnt && s_g[tid * kGradStride + 9] > 0.0f) {
-            const float* gs = &s_g[tid * kGradStride];
-            float4* dst = grad2d + 3 * (size_t)sm.gid[tid];
-            atomicAdd(dst + 0, make_float4(gs[0], gs[1], gs[2], gs[3]));
-            atomicAdd(dst + 1, make_float4(gs[4], gs[5], gs[6], gs[7]));
-            atomicAdd(dst + 2, make_float4(gs[8], gs[9], 0.0f, 0.0f));
-        }
-        __syncthreads();
+        __syncthreads();  // the next batch overwrites the staging area
     }
 }
 

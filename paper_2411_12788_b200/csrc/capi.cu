@@ -385,7 +385,7 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     const FwdState& st = ctx->st;
     LaunchCtx& lc = ctx->lc;
     const int n = g->n;
-    CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 48, true, ctx->stream), "alloc grad2d");
+    CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 64, true, ctx->stream), "alloc grad2d");
     const int n_blocks = st.cp.tiles_x * st.cp.tiles_y * ((st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)) *
                                                          (st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)));
     float* partials = nullptr;

@@ -104,8 +104,11 @@ __global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp
                                                    int accumulate) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.n) return;
-    const float4 g0 = grad2d[3 * (size_t)i], g1 = grad2d[3 * (size_t)i + 1], g2 = grad2d[3 * (size_t)i + 2];
-    const bool touched = g2.y > 0.0f;
+    // accumulator (blend_backward): g0 = (dmean.x, dmean.y, dconic00), g1 = (dconic01, dconic11,
+    // dopacity), g2 = d colour, g3.x = number of committed (warp, pixel) samples
+    const float4 g0 = grad2d[4 * (size_t)i], g1 = grad2d[4 * (size_t)i + 1], g2 = grad2d[4 * (size_t)i + 2],
+                 g3 = grad2d[4 * (size_t)i + 3];
+    const bool touched = g3.x > 0.0f;
     const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i, i48 = 48 * (size_t)i;
     if (!touched) {
         if (!accumulate) {
@@ -130,14 +133,13 @@ __global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp
         return;
     }
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    grad2d[3 * (size_t)i] = zero4;
-    grad2d[3 * (size_t)i + 1] = zero4;
-    grad2d[3 * (size_t)i + 2] = zero4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) grad2d[4 * (size_t)i + k] = zero4;
 
     const float dm0 = g0.x, dm1 = g0.y;
-    const float dQ[4] = {g0.z, g0.w, g0.w, g1.x};  // row-major (00, 01, 10, 11); 01 == 10
-    const float dopac = g1.y;
-    const float dcol[3] = {g1.z, g1.w, g2.x};
+    const float dQ[4] = {g0.z, g1.x, g1.x, g1.y};  // row-major (00, 01, 10, 11); 01 == 10
+    const float dopac = g1.z;
+    const float dcol[3] = {g2.x, g2.y, g2.z};
     const ProjRec pr = rec[i];
     const float k0 = pr.r0.z, k1 = pr.r0.w, k2 = pr.r1.x, opacity = pr.r1.y;
 

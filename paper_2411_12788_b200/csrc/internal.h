@@ -126,9 +126,9 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
                              uint32_t* offsets, uint32_t* scan_tmp);
 
 // ---- backward.cu --------------------------------------------------------------------------
-// Per-Gaussian 2D gradient accumulator, 48 B (3 x float4):
-//   g0 = (d_mean.x, d_mean.y, d_conic00, d_conic01), g1 = (d_conic11, d_opacity, d_col.r,
-//   d_col.g), g2 = (d_col.b, touched, 0, 0)
+// Per-Gaussian 2D gradient accumulator, 64 B (4 x float4, w unused):
+//   g0 = (d_mean.x, d_mean.y, d_conic00), g1 = (d_conic01, d_conic11, d_opacity),
+//   g2 = d_colour, g3.x = committed samples (touched flag)
 struct Grad2D;
 
 cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
