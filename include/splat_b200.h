@@ -236,6 +236,25 @@ int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule,
                           int64_t seed, float* points_dev, int32_t* pixel_dev,
                           int64_t capacity, int32_t* count_dev);
 
+/* ---- importance over views (BASELINE config 3) ------------------------------------- */
+/* After splat_accumulate_importance for view k: bitmask_dev[(n+31)/32] (may be NULL) gets bit i
+ * set iff max_weight[i] > threshold (the config-3 visibility rule), and the running
+ * global_importance (simplify.cpp:13-34) is updated: accum_dev[i] += (double)importance[i],
+ * counts_dev[i] += max_pixel_count[i] (either may be NULL).  Views added in call order give the
+ * reference's fp64 sums for the same per-view importance. */
+int splat_visibility_update(splat_ctx* ctx, const splat_importance_outputs* report_dev, int32_t n,
+                            float threshold, uint32_t* bitmask_dev, double* accum_dev,
+                            int64_t* counts_dev);
+
+/* ---- primitives (exposed for tests and microbenchmarks) ------------------------------ */
+/* Stable LSD radix sort of (keys, vals) on key bits [begin_bit, end_bit), n pairs, device
+ * pointers; the result lands in keys/vals or, when *result_in_alt, in keys_alt/vals_alt. */
+int splat_sort_pairs(splat_ctx* ctx, uint32_t* keys_dev, uint32_t* vals_dev, uint32_t* keys_alt_dev,
+                     uint32_t* vals_alt_dev, int64_t n, int begin_bit, int end_bit, int* result_in_alt);
+/* Exclusive prefix sum of n uint32 (in place allowed); total_dev may be NULL. */
+int splat_exclusive_scan(splat_ctx* ctx, const uint32_t* in_dev, uint32_t* out_dev, int64_t n,
+                         uint32_t* total_dev);
+
 /* ---- bit-exact debug views of the preceding forward (host outputs, synchronous) ------ */
 /* n_survivors / n_pairs of the last forward. */
 int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs,

@@ -26,6 +26,7 @@ SOURCES = {
     "backward.cu": [],
     "chain.cu": ["--fmad=false"],
     "binning.cu": [],
+    "importance.cu": [],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

@@ -220,6 +220,11 @@ _EXPORTS = {
                                   C.POINTER(C.c_int32), C.c_uint32]),
     "splat_depth_unproject": (C.c_int, [C.c_void_p, C.POINTER(Camera), C.c_int, C.c_float,
                                         C.c_int64, C.c_int32, C.c_int64, fp, ip, C.c_int64, ip]),
+    "splat_visibility_update": (C.c_int, [C.c_void_p, C.POINTER(ImportanceOutputs), C.c_int32, C.c_float,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]),
+    "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                   C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "splat_forward_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "splat_project_debug": (C.c_int, [C.c_void_p, ip, ip, fp, u8p, fp, fp, fp, fp]),

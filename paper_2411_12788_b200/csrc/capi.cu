@@ -30,7 +30,7 @@ struct ProfileState {
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
-    size_t open = 0;
+    std::vector<size_t> open;  // stack of open records (scopes nest: a radix pass contains a scan)
     cudaEvent_t get() {
         if (!pool.empty()) {
             cudaEvent_t e = pool.back();
@@ -47,6 +47,7 @@ struct ProfileState {
             pool.push_back(r.b);
         }
         recs.clear();
+        open.clear();
     }
     ~ProfileState() {
         recycle();
@@ -58,12 +59,14 @@ void LaunchCtx::prof_begin(const char* name) {
     if (!prof) return;
     ProfileState::Rec r{name, prof->get(), prof->get()};
     cudaEventRecord(r.a, stream);
+    prof->open.push_back(prof->recs.size());
     prof->recs.push_back(r);
 }
 
 void LaunchCtx::prof_end() {
-    if (!prof || prof->recs.empty()) return;
-    cudaEventRecord(prof->recs.back().b, stream);
+    if (!prof || prof->open.empty()) return;
+    cudaEventRecord(prof->recs[prof->open.back()].b, stream);
+    prof->open.pop_back();
 }
 }  // namespace splat_b200
 
@@ -626,6 +629,38 @@ int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule, flo
                         seed, points, pixel, capacity, count_dev, ctx->flags.as<uint32_t>(),
                         ctx->flag_offsets.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>()),
        "unproject");
+    return SPLAT_OK;
+}
+
+int splat_visibility_update(splat_ctx* ctx, const splat_importance_outputs* rep, int32_t n, float threshold,
+                            uint32_t* bitmask, double* accum, int64_t* counts) {
+    if (!ctx || !rep || n < 0 || (n > 0 && (!rep->importance || !rep->max_weight || !rep->max_pixel_count)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "visibility_update: bad args");
+    CK(launch_visibility_update(ctx->lc, rep->importance, rep->max_weight, rep->max_pixel_count, n, threshold,
+                                bitmask, accum, counts),
+       "visibility_update");
+    return SPLAT_OK;
+}
+
+int splat_sort_pairs(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                     int begin_bit, int end_bit, int* result_in_alt) {
+    if (!ctx || n < 0 || begin_bit < 0 || end_bit > 32 || !result_in_alt)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "sort_pairs: bad args");
+    const size_t hw = radix_hist_words((uint64_t)(n > 0 ? n : 1), 8);
+    CK(ctx->hist.ensure(hw * 4), "alloc hist");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(hw) + 64) * 4), "alloc scan");
+    bool alt = false;
+    CK(radix_sort_pairs(ctx->lc, keys, vals, keys_alt, vals_alt, (uint64_t)n, begin_bit, end_bit,
+                        ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
+       "sort_pairs");
+    *result_in_alt = alt ? 1 : 0;
+    return SPLAT_OK;
+}
+
+int splat_exclusive_scan(splat_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total) {
+    if (!ctx || n < 0) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "exclusive_scan: bad args");
+    CK(ctx->scan_tmp.ensure((scan_temp_words((uint64_t)n) + 64) * 4), "alloc scan");
+    CK(exclusive_scan_u32(ctx->lc, in, out, (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), total), "exclusive_scan");
     return SPLAT_OK;
 }
 

@@ -98,11 +98,15 @@ __device__ __forceinline__ void rotation_from_quat(const float qr[4], float r[9]
     r[8] = 1.0f - 2.0f * (x * x + y * y);
 }
 
+constexpr int kChainThreads = 128;
+constexpr int kShRow = 13;  // float4 per staged SH row (12 + 1 pad: conflict-free LDS/STS.128)
+
+// One Gaussian.  With VEC, its SH row is read from and its SH gradient row written to s_sh (the
+// caller copies rows in and out); untouched Gaussians leave a zero gradient row.
 template <bool VEC>
-__global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
-                                                   const ProjRec* __restrict__ rec, splat_param_grads out,
-                                                   int accumulate) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
+                                          const ProjRec* __restrict__ rec, splat_param_grads out, int accumulate,
+                                          int i, float4* s_sh) {
     if (i >= g.n) return;
     // accumulator (blend_backward): g0 = (dmean.x, dmean.y, dconic00), g1 = (dconic01, dconic11,
     // dopacity), g2 = d colour, g3.x = number of committed (warp, pixel) samples
@@ -120,15 +124,14 @@ __global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp
 #pragma unroll
             for (int k = 0; k < 4; ++k) out.d_rotations[i4 + k] = 0.0f;
             out.d_opacity_logits[i] = 0.0f;
-            if (VEC) {
-                float4* d4 = reinterpret_cast<float4*>(out.d_sh + i48);
-#pragma unroll
-                for (int k = 0; k < 12; ++k) d4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
+            if (!VEC)
                 for (int k = 0; k < 48; ++k) out.d_sh[i48 + k] = 0.0f;
-            }
             if (out.grad2d_accum) out.grad2d_accum[i] = 0.0f;
             if (out.grad2d_count) out.grad2d_count[i] = 0;
+        }
+        if (VEC) {  // zero gradient row (copied out / added by the caller)
+#pragma unroll
+            for (int k = 0; k < 12; ++k) s_sh[threadIdx.x * kShRow + k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         return;
     }
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp
     sh_basis_all(dir0, dir1, dir2, deg, basis);
     float shv[48];
     if (VEC) {
-        const float4* s4 = reinterpret_cast<const float4*>(g.sh + i48);
+        const float4* s4 = &s_sh[threadIdx.x * kShRow];
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
             const float4 vv = s4[k];
@@ -346,19 +349,47 @@ __global__ void __launch_bounds__(128) chain_kernel(GaussianPtrs g, CamParams cp
         out.d_rotations[i4 + k] = br + drot[k];
     }
     out.d_opacity_logits[i] = (accumulate ? out.d_opacity_logits[i] : 0.0f) + dlogit;
-    if (VEC) {
-        float4* d4 = reinterpret_cast<float4*>(out.d_sh + i48);
+    if (VEC) {  // the fresh gradient row; the caller writes (or adds) it coalesced
+        float4* d4 = &s_sh[threadIdx.x * kShRow];
 #pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            float4 o = accumulate ? d4[k] : zero4;
-            o.x = o.x + dsh[4 * k]; o.y = o.y + dsh[4 * k + 1]; o.z = o.z + dsh[4 * k + 2]; o.w = o.w + dsh[4 * k + 3];
-            d4[k] = o;
-        }
+        for (int k = 0; k < 12; ++k) d4[k] = make_float4(dsh[4 * k], dsh[4 * k + 1], dsh[4 * k + 2], dsh[4 * k + 3]);
     } else {
         for (int k = 0; k < 48; ++k) out.d_sh[i48 + k] = (accumulate ? out.d_sh[i48 + k] : 0.0f) + dsh[k];
     }
     if (out.grad2d_accum) out.grad2d_accum[i] = (accumulate ? out.grad2d_accum[i] : 0.0f) + gaccum;
     if (out.grad2d_count) out.grad2d_count[i] = (accumulate ? out.grad2d_count[i] : 0) + 1;
+}
+
+// The SH rows (192 B in, 192 B of gradients out per Gaussian) move between HBM and shared memory
+// with coalesced float4 copies; the per-thread chain reads / writes its row in shared memory.
+template <bool VEC>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
+                                                             const ProjRec* __restrict__ rec, splat_param_grads out,
+                                                             int accumulate) {
+    __shared__ float4 s_sh[VEC ? kChainThreads * kShRow : 1];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int base = blockIdx.x * kChainThreads;
+    const int cnt = min(kChainThreads, g.n - base);
+    if (VEC) {
+        const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)base);
+        for (int q = threadIdx.x; q < cnt * 12; q += kChainThreads) s_sh[(q / 12) * kShRow + q % 12] = __ldg(src + q);
+        __syncthreads();
+    }
+    chain_one<VEC>(g, cp, grad2d, rec, out, accumulate, i, s_sh);
+    if (VEC) {
+        __syncthreads();
+        float4* dst = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)base);
+        for (int q = threadIdx.x; q < cnt * 12; q += kChainThreads) {
+            const float4 d = s_sh[(q / 12) * kShRow + q % 12];
+            if (accumulate) {
+                float4 o = dst[q];
+                o.x = o.x + d.x; o.y = o.y + d.y; o.z = o.z + d.z; o.w = o.w + d.w;
+                dst[q] = o;
+            } else {
+                dst[q] = d;
+            }
+        }
+    }
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -371,10 +402,10 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
     const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
     LaunchScope ls(lc, "chain");
     if (vec)
-        chain_kernel<true><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
+        chain_kernel<true><<<blocks_for(g.n, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
                                                                        out, accumulate);
     else
-        chain_kernel<false><<<blocks_for(g.n, 128), 128, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
+        chain_kernel<false><<<blocks_for(g.n, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
                                                                         rec, out, accumulate);
     lc.count++;
     return cudaGetLastError();

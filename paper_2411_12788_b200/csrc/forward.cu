@@ -64,15 +64,27 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, float x, 
 __device__ __forceinline__ float std_max(float a, float b) { return (a < b) ? b : a; }
 __device__ __forceinline__ float std_min(float a, float b) { return (b < a) ? b : a; }
 
-// project<T> body for one Gaussian (rasterizer.cpp:24-82).  Returns false when culled.
+constexpr int kPreThreads = 128;
+constexpr int kShRow = 13;  // float4 per staged SH row (12 + 1 pad: conflict-free LDS.128)
+
+// project<T> body for one Gaussian (rasterizer.cpp:24-82).  With VEC_SH the block first copies its
+// Gaussians' 192-byte SH rows into shared memory with coalesced float4 loads.
 template <bool VEC_SH>
-__global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamParams cp, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g, CamParams cp, const uint8_t* __restrict__ mask,
                                                         ProjRec* __restrict__ rec, AuxRec* __restrict__ aux,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ tile_counts,
                                                         uint32_t* __restrict__ n_surv, float* __restrict__ depth_out,
                                                         uint2* __restrict__ rect_ref) {
+    __shared__ float4 s_sh[VEC_SH ? kPreThreads * kShRow : 1];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (VEC_SH) {
+        const int base = blockIdx.x * kPreThreads;
+        const int cnt = min(kPreThreads, g.n - base);
+        const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)base);
+        for (int q = threadIdx.x; q < cnt * 12; q += kPreThreads) s_sh[(q / 12) * kShRow + q % 12] = __ldg(src + q);
+        __syncthreads();
+    }
     bool alive = i < g.n;
     if (alive && mask && !mask[i]) alive = false;
     float px = 0.f, py = 0.f, pz = 0.f, zc = 0.f;
@@ -184,10 +196,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(GaussianPtrs g, CamPara
                 float rgb[3];
                 if (VEC_SH) {
                     float shv[48];
-                    const float4* s4 = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)i);
+                    const float4* s4 = &s_sh[threadIdx.x * kShRow];
 #pragma unroll
                     for (int k = 0; k < 12; ++k) {
-                        const float4 v = __ldg(&s4[k]);
+                        const float4 v = s4[k];
                         shv[4 * k] = v.x; shv[4 * k + 1] = v.y; shv[4 * k + 2] = v.z; shv[4 * k + 3] = v.w;
                     }
                     sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
@@ -572,13 +584,13 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
     if (vec)
         {
             LaunchScope ls_(lc, "preprocess");
-            preprocess_kernel<true><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+            preprocess_kernel<true><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
     else
         {
             LaunchScope ls_(lc, "preprocess");
-            preprocess_kernel<false><<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
+            preprocess_kernel<false><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
                                                                               tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
     lc.count++;

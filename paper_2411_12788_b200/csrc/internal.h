@@ -125,6 +125,11 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
                              int32_t* pixel, int64_t capacity, int32_t* count_dev, uint32_t* flags,
                              uint32_t* offsets, uint32_t* scan_tmp);
 
+// ---- importance.cu ------------------------------------------------------------------------
+cudaError_t launch_visibility_update(LaunchCtx& lc, const float* importance, const float* max_weight,
+                                     const int32_t* max_count, int n, float threshold, uint32_t* bitmask,
+                                     double* accum, int64_t* counts);
+
 // ---- backward.cu --------------------------------------------------------------------------
 // Per-Gaussian 2D gradient accumulator, 64 B (4 x float4, w unused):
 //   g0 = (d_mean.x, d_mean.y, d_conic00), g1 = (d_conic01, d_conic11, d_opacity),

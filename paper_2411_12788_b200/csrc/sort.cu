@@ -308,11 +308,105 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_kernel(
     }
 }
 
+// Reduce-then-scan variant of one pass, for passes with many tiles (the Onesweep look-back chain
+// grows with the tile count): per-tile digit counts (digit-major), the single-pass scan over that
+// matrix, then the same stable ranking + scatter with the scanned offsets.
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) radix_tile_counts_kernel(const uint32_t* __restrict__ keys, uint32_t n,
+                                                                    int shift, uint32_t* __restrict__ counts,
+                                                                    uint32_t ntiles) {
+    constexpr int BINS = 1 << BITS;
+    __shared__ uint32_t s_hist[kWarps][BINS];
+    for (int i = threadIdx.x; i < kWarps * BINS; i += kThreads) (&s_hist[0][0])[i] = 0u;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint64_t i = base + (uint64_t)r * kThreads + threadIdx.x;
+        if (i < n) atomicAdd(&s_hist[warp][(keys[i] >> shift) & (BINS - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < BINS; d += kThreads) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) c += s_hist[w][d];
+        counts[(uint64_t)d * ntiles + blockIdx.x] = c;
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) radix_scatter_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ offs, uint32_t ntiles) {
+    constexpr int BINS = 1 << BITS;
+    constexpr int PER_WARP = kSortTile / kWarps;
+    __shared__ uint32_t s_cnt[kWarps][BINS];
+    for (int i = threadIdx.x; i < kWarps * BINS; i += kThreads) (&s_cnt[0][0])[i] = 0u;
+    const uint32_t tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t wbase = (uint64_t)tile * kSortTile + (uint64_t)warp * PER_WARP;
+    uint32_t k[kSortItems], v[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        k[r] = i < n ? keys_in[i] : 0u;
+        v[r] = i < n ? vals_in[i] : 0u;
+    }
+    __syncthreads();
+    const unsigned lt = lanemask_lt();
+    uint32_t rank[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t d = (k[r] >> shift) & (BINS - 1);
+        const uint32_t label = valid ? d : (0x80000000u | (uint32_t)lane);
+        const unsigned peers = __match_any_sync(0xffffffffu, label);
+        const uint32_t old = valid ? s_cnt[warp][d] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) s_cnt[warp][d] = old + __popc(peers);
+        __syncwarp();
+        rank[r] = old + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < BINS; d += kThreads) {
+        uint32_t run = offs[(uint64_t)d * ntiles + tile];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t cw = s_cnt[w][d];
+            s_cnt[w][d] = run;
+            run += cw;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        if (i < n) {
+            const uint32_t d = (k[r] >> shift) & (BINS - 1);
+            const uint32_t pos = s_cnt[warp][d] + rank[r];
+            keys_out[pos] = k[r];
+            vals_out[pos] = v[r];
+        }
+    }
+}
+
+constexpr uint32_t kOnesweepMaxTiles = 640;  // above this, the look-back chain costs more than a scan
+
 template <int BITS>
 void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n,
-                     int shift, const uint32_t* hist, uint32_t* status, uint32_t* counter) {
+                     int shift, const uint32_t* hist, uint32_t* status, uint32_t* counter, uint32_t* scan_tmp) {
     const uint32_t ntiles = (n + kSortTile - 1) / kSortTile;
-    radix_onesweep_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, status, counter);
+    if (ntiles <= kOnesweepMaxTiles) {
+        radix_onesweep_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, status, counter);
+        return;
+    }
+    uint32_t* counts = status;  // [BINS][ntiles] fits in the pass's status area
+    radix_tile_counts_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, n, shift, counts, ntiles);
+    exclusive_scan_u32(lc, counts, counts, (uint64_t)ntiles << BITS, scan_tmp, nullptr);
+    radix_scatter_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, counts, ntiles);
+    lc.count += 2;
 }
 
 }  // namespace
@@ -355,7 +449,6 @@ cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const u
 cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                              uint64_t n, int begin_bit, int end_bit, uint32_t* hist, uint32_t* scan_tmp,
                              bool* result_in_alt) {
-    (void)scan_tmp;
     *result_in_alt = false;
     if (n == 0 || end_bit <= begin_bit) return cudaSuccess;
     const int total = end_bit - begin_bit;
@@ -380,15 +473,15 @@ cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint
         uint32_t* st = status + (size_t)p * nt * 512;
         LaunchScope s(lc, "radix_onesweep");
         switch (bits) {
-            case 1: launch_onesweep<1>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 2: launch_onesweep<2>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 3: launch_onesweep<3>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 4: launch_onesweep<4>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 5: launch_onesweep<5>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 6: launch_onesweep<6>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 7: launch_onesweep<7>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            case 8: launch_onesweep<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
-            default: launch_onesweep<9>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p); break;
+            case 1: launch_onesweep<1>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 2: launch_onesweep<2>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 3: launch_onesweep<3>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 4: launch_onesweep<4>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 5: launch_onesweep<5>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 6: launch_onesweep<6>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 7: launch_onesweep<7>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            case 8: launch_onesweep<8>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
+            default: launch_onesweep<9>(lc, ki, vi, ko, vo, (uint32_t)n, shift, h, st, counters + p, scan_tmp); break;
         }
         lc.count++;
         std::swap(ki, ko);

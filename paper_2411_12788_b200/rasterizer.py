@@ -435,3 +435,63 @@ def project_debug(n: int, ctx: Optional[Context] = None) -> dict:
                                           color.ctypes.data_as(capi.fp), opac.ctypes.data_as(capi.fp)))
     return dict(rect=rect[:n], depth=depth[:n], survivor=surv[:n].astype(bool), mean2d=mean2d[:n], conic=conic[:n],
                 color=color[:n], opacity=opac[:n])
+
+
+def visibility_pass(set_, cams, cfg: Optional[RasterConfig] = None, threshold: float = 1e-3,
+                    ctx: Optional[Context] = None):
+    """BASELINE config 3 over views: accumulate_importance per view (rasterizer.cpp:184-193), the
+    per-view visibility bitmask (max blend weight > threshold) and global_importance
+    (simplify.cpp:13-34: fp64 sum of importance, sum of argmax counts, views in order).
+    Returns (masks [views, ceil(n/32)] uint32 words, accum_weight float64 [n], intersections int64 [n])
+    as torch CUDA tensors."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    cfg = cfg or RasterConfig()
+    ds, _ = _device_set(set_, ctx.device)
+    n = ds.n
+    dev = f"cuda:{ctx.device}"
+    words = (n + 31) // 32
+    masks = torch.zeros((len(cams), max(words, 1)), dtype=torch.int32, device=dev)
+    accum = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+    counts = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    r = dict(importance=torch.zeros(max(n, 1), dtype=torch.float32, device=dev),
+             max_weight=torch.zeros(max(n, 1), dtype=torch.float32, device=dev),
+             max_pixel_count=torch.zeros(max(n, 1), dtype=torch.int32, device=dev))
+    rep = ImportanceOutputs(as_fp(r["importance"].data_ptr()), as_fp(r["max_weight"].data_ptr()),
+                            as_ip(r["max_pixel_count"].data_ptr()))
+    ctx.bind_stream()
+    g = ds.struct()
+    for k, cam in enumerate(cams):
+        ctx.check(ctx.lib.splat_accumulate_importance(ctx.h, C.byref(g), C.byref(cam), C.byref(cfg), None,
+                                                      C.byref(rep)))
+        ctx.check(ctx.lib.splat_visibility_update(ctx.h, C.byref(rep), n, threshold, masks[k].data_ptr(),
+                                                  accum.data_ptr(), counts.data_ptr()))
+    return masks, accum[:n], counts[:n]
+
+
+def unpack_mask(words, n: int) -> np.ndarray:
+    """uint32 bitmask words -> bool [n] (bit i of word i // 32)."""
+    w = np.asarray(words).astype(np.uint32)
+    bits = (w[:, None] >> np.arange(32, dtype=np.uint32)[None, :]) & 1
+    return bits.reshape(-1)[:n].astype(bool)
+
+
+def depth_points(set_, cams, cfg: Optional[RasterConfig] = None, rule: int = capi.DEPTH_RULE_ALPHA,
+                 alpha_threshold: float = 0.5, stride: int = 4, seed: int = 0, ctx: Optional[Context] = None):
+    """BASELINE config 2 (aggressive densification's depth pass, densify.cpp:207-222): per view,
+    render depth + alpha, select pixels with alpha > alpha_threshold (or argmax >= 0) and
+    (view * H * W + pixel + seed) % stride == 0, unproject them.  Returns (points [k, 3],
+    view [k], pixel [k]) as torch CUDA tensors, views in order, pixels in raster order."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    cfg = cfg or RasterConfig()
+    ds, _ = _device_set(set_, ctx.device)
+    pts, views, pixels = [], [], []
+    for k, cam in enumerate(cams):
+        render(ds, cam, cfg, ctx=ctx, want_depth=True)
+        p, px, cnt = unproject_depth(cam, rule=rule, alpha_threshold=alpha_threshold, view_index=k, stride=stride,
+                                     seed=seed, ctx=ctx)
+        pts.append(p.clone())
+        pixels.append(px.clone())
+        views.append(torch.full((p.shape[0],), k, dtype=torch.int32, device=p.device))
+    return torch.cat(pts), torch.cat(views), torch.cat(pixels)
