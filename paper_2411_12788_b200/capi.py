@@ -241,7 +241,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # SPLAT_B200_LIB selects an alternative build of the same library (tuning experiments)
+    p = Path(path) if path else Path(os.environ.get("SPLAT_B200_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -60,8 +60,8 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
 // accumulation, no flush barrier.
 // With target != nullptr, dL/dC = sign(C - target)/n (l1_loss, loss.cpp:63-76) is fused in and
 // the CTA's L1 partial sum is written to loss_partials[block].
-template <bool THR>
-__global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+template <bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                             const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
                                                             const float* __restrict__ t_final,
@@ -71,20 +71,22 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
                                                             const float* __restrict__ target, float inv_n,
                                                             float* __restrict__ loss_partials,
                                                             float4* __restrict__ grad2d) {
-    __shared__ StageSmem sm;
-    __shared__ float s_red[kBlock / 32];
-    __shared__ int s_maxlast[kBlock / 32];
+    __shared__ StageSmem<BW * BH> sm;
+    __shared__ float s_red[BW * BH / 32];
+    __shared__ int s_maxlast[BW * BH / 32];
     const int nthreads = blockDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = nthreads >> 5;
     const int ts = cp.tile_size;
-    const int bw = ts < 16 ? ts : 16;
-    const int tile = blockIdx.x;
+    constexpr int bw = BW;
+    // sub-blocks of one tile are adjacent in the grid, so the tile's list and records are
+    // re-read from L2 while still hot
+    const int subs_x = ts / BW, nsub = subs_x * (ts / BH);
+    const int tile = (int)blockIdx.x / nsub, sub = (int)blockIdx.x - tile * nsub;
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
-    const int subs = ts / bw;
-    const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
-    const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
-    const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
+    const int sx = sub % subs_x, sy = sub / subs_x;
+    const int bx0 = tx * ts + sx * BW, by0 = ty * ts + sy * BH;
+    const int bx1 = min(bx0 + BW, cp.width), by1 = min(by0 + BH, cp.height);
     // pixel of this thread: warps own compact patches (8 x 4 for 16 x 16 blocks, 8 x 4 for 8 x 8)
     const int lx = ((tid >> 5) & ((bw >> 3) - 1)) * 8 + (tid & 7);
     const int ly = ((tid >> 5) / (bw >> 3)) * 4 + ((tid & 31) >> 3);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(256) blend_backward_kernel(CamParams cp, const
     if (target && loss_partials && tid == 0) {
         float s = 0.0f;
         for (int w = 0; w < nwarps; ++w) s += s_red[w];
-        loss_partials[blockIdx.y * gridDim.x + blockIdx.x] = s;
+        loss_partials[blockIdx.x] = s;
     }
     int block_last = -1;
     for (int w = 0; w < nwarps; ++w) block_last = max(block_last, s_maxlast[w]);
@@ -223,18 +225,30 @@ __global__ void __launch_bounds__(kL1Threads) l1_kernel(const float* __restrict_
     }
 }
 
-// Deterministic final sum (fixed order, fp64 accumulation).
-__global__ void loss_reduce_kernel(const float* __restrict__ partials, int n, float inv_n, float* __restrict__ loss) {
-    __shared__ double s[256];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += (double)partials[i];
-    s[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
-        __syncthreads();
+// Deterministic final sum (fixed order, fp64 accumulation).  1024 threads, 4 independent
+// accumulators per thread so the partial loads are in flight together.
+constexpr int kLossThreads = 1024;
+__global__ void __launch_bounds__(kLossThreads) loss_reduce_kernel(const float* __restrict__ partials, int n,
+                                                                   float inv_n, float* __restrict__ loss) {
+    __shared__ double s[kLossThreads / 32];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = threadIdx.x;
+    for (; i + 3 * kLossThreads < n; i += 4 * kLossThreads) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] += (double)partials[i + k * kLossThreads];
     }
-    if (threadIdx.x == 0) *loss = (float)s[0] * inv_n;
+    for (int k = 0; i < n; i += kLossThreads, ++k) acc[k & 3] += (double)partials[i];
+    double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = s[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) *loss = (float)v * inv_n;
+    }
 }
 
 // adam_delta (optimizer.cpp:29-36) with every fp64 operation explicitly rounded (no DFMA), so
@@ -280,20 +294,24 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const int32_t* last_index, const float bg[3], const float* d_color,
                                   const float* color, const float* target, float* loss_partials, float* grad2d) {
     const int ts = cp.tile_size;
-    const int bw = ts < 16 ? ts : 16;
-    const int subs = ts / bw;
-    dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
+    const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
     {
         LaunchScope ls_(lc, "blend_backward");
-        if (cp.apply_thresholds)
-            blend_backward_kernel<true><<<grid, bw * bw, 0, lc.stream>>>(
-                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n,
-                loss_partials, reinterpret_cast<float4*>(grad2d));
-        else
-            blend_backward_kernel<false><<<grid, bw * bw, 0, lc.stream>>>(
-                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n,
-                loss_partials, reinterpret_cast<float4*>(grad2d));
+#define BLEND_BWD_SHAPE(T, W, H)                                                                                   \
+    blend_backward_kernel<T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, t_final, last_index, \
+                                                                  bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
+                                                                  loss_partials, reinterpret_cast<float4*>(grad2d))
+#define BLEND_BWD(T)                                             \
+    do {                                                         \
+        if (cp.block_w == 16) BLEND_BWD_SHAPE(T, 16, 16);        \
+        else if (cp.block_h == 8) BLEND_BWD_SHAPE(T, 8, 8);      \
+        else BLEND_BWD_SHAPE(T, 8, 4);                           \
+    } while (0)
+        if (cp.apply_thresholds) BLEND_BWD(true);
+        else BLEND_BWD(false);
+#undef BLEND_BWD
+#undef BLEND_BWD_SHAPE
     }
     lc.count++;
     return cudaGetLastError();
@@ -302,7 +320,7 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss) {
     {
         LaunchScope ls_(lc, "loss_reduce");
-        loss_reduce_kernel<<<1, 256, 0, lc.stream>>>(partials, n, inv_n, loss);
+        loss_reduce_kernel<<<1, kLossThreads, 0, lc.stream>>>(partials, n, inv_n, loss);
     }
     lc.count++;
     return cudaGetLastError();

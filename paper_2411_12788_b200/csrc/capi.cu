@@ -8,6 +8,7 @@
 // The backward reuses the forward's sorted lists, records and per-pixel (T_final, last) state
 // (the reference recomputes project + bin_tiles, gradients.cpp:58-61; the result is identical).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -169,6 +170,17 @@ int validate_camera(splat_ctx* ctx, const splat_camera* c) {
     return SPLAT_OK;
 }
 
+// Blend CTA pixel block (SPLAT_BLEND_BLOCK = 16x16 | 8x8 | 8x4; default 8x8): returns w * 100 + h.
+static int blend_block_shape() {
+    static const int shape = [] {
+        const char* e = std::getenv("SPLAT_BLEND_BLOCK");
+        if (e && std::strcmp(e, "16x16") == 0) return 1616;
+        if (e && std::strcmp(e, "8x4") == 0) return 804;
+        return 808;
+    }();
+    return shape;
+}
+
 int make_params(splat_ctx* ctx, const splat_camera* c, const splat_raster_config* cfg, CamParams* cp) {
     int rc = validate_camera(ctx, c);
     if (rc) return rc;
@@ -192,6 +204,11 @@ int make_params(splat_ctx* ctx, const splat_camera* c, const splat_raster_config
     }
     cp->znear = c->znear;
     cp->tile_size = ts;
+    {
+        const int shape = blend_block_shape();
+        cp->block_w = ts < 16 ? 8 : shape / 100;
+        cp->block_h = ts < 16 ? (shape % 100 == 4 ? 4 : 8) : shape % 100;
+    }
     cp->tiles_x = (c->width + ts - 1) / ts;
     cp->tiles_y = (c->height + ts - 1) / ts;
     cp->apply_thresholds = cfg->apply_thresholds ? 1 : 0;
@@ -389,8 +406,8 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     LaunchCtx& lc = ctx->lc;
     const int n = g->n;
     CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 64, true, ctx->stream), "alloc grad2d");
-    const int n_blocks = st.cp.tiles_x * st.cp.tiles_y * ((st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)) *
-                                                         (st.cp.tile_size / (st.cp.tile_size < 16 ? st.cp.tile_size : 16)));
+    const int n_blocks =
+        st.cp.tiles_x * st.cp.tiles_y * (st.cp.tile_size / st.cp.block_w) * (st.cp.tile_size / st.cp.block_h);
     float* partials = nullptr;
     if (target && loss_dev) {
         CK(ctx->loss_partials.ensure((size_t)n_blocks * 4), "alloc partials");

@@ -45,6 +45,7 @@ struct CamParams {
     float center[3];  // -(R^T t), computed on the host in the reference's order
     float znear;
     int tile_size, tiles_x, tiles_y;
+    int block_w, block_h;  // pixel block of one blend CTA (16x16, 8x8 or 8x4; divides the tile)
     int apply_thresholds;
     float lowpass, radius_sigmas, alpha_max, contribution_min, transmittance_min;
     float log_cond_limit;  // float(log(1e12))
@@ -163,13 +164,14 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 }
 
 // Shared-memory staging area of one batch (one per CTA).
+template <int CAP>
 struct StageSmem {
-    float4 r0[kBlock];
-    float4 r1[kBlock];
-    float4 r2[kBlock];
-    uint32_t gid[kBlock];
-    int idx[kBlock];
-    int wcnt[kBlock / 32];
+    float4 r0[CAP];
+    float4 r1[CAP];
+    float4 r2[CAP];
+    uint32_t gid[CAP];
+    int idx[CAP];
+    int wcnt[(CAP + 31) / 32];
 };
 
 // Stage one batch of list entries in shared memory, keeping only Gaussians that pass the exact
@@ -177,10 +179,10 @@ struct StageSmem {
 // number of staged entries.  sm.idx keeps each entry's absolute position in the sorted pair
 // array (the reference's list position); sm.r1 is rewritten to (conic2, opacity, pixel masks of
 // the effective rect relative to the block, cut) for gate_sample.
-template <typename IdxFn>
+template <int CAP, typename IdxFn>
 __device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32_t* __restrict__ pair_gauss,
                                            const ProjRec* __restrict__ rec, int bx0, int bx1, int by0, int by1,
-                                           StageSmem& sm) {
+                                           StageSmem<CAP>& sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     bool keep = false;
     ProjRec rr;

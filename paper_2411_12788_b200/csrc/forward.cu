@@ -358,25 +358,27 @@ __device__ __forceinline__ float warp_sum(float v) {
 // CTAs sharing its list (blockIdx.y).  The tile list is walked in batches of blockDim.x entries;
 // each batch is culled to the Gaussians that can reach the alpha floor inside the block and
 // staged in shared memory, and all threads walk it in the same order (broadcast reads).
-template <bool REPORT, bool THR>
-__global__ void __launch_bounds__(256) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+template <bool REPORT, bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
                                                            float bg2, FwdOutputs out) {
-    __shared__ StageSmem sm;
-    __shared__ float s_imp[REPORT ? kBlock : 1];
-    __shared__ uint32_t s_maxw[REPORT ? kBlock : 1];
+    __shared__ StageSmem<BW * BH> sm;
+    __shared__ float s_imp[REPORT ? BW * BH : 1];
+    __shared__ uint32_t s_maxw[REPORT ? BW * BH : 1];
     const int nthreads = blockDim.x;
     const int tid = threadIdx.x;
     const int ts = cp.tile_size;
-    const int bw = ts < 16 ? ts : 16;
-    const int tile = blockIdx.x;
+    constexpr int bw = BW;
+    // sub-blocks of one tile are adjacent in the grid, so the tile's list and records are
+    // re-read from L2 while still hot
+    const int subs_x = ts / BW, nsub = subs_x * (ts / BH);
+    const int tile = (int)blockIdx.x / nsub, sub = (int)blockIdx.x - tile * nsub;
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
-    const int subs = ts / bw;
-    const int sx = blockIdx.y % subs, sy = blockIdx.y / subs;
-    const int bx0 = tx * ts + sx * bw, by0 = ty * ts + sy * bw;
-    const int bx1 = min(bx0 + bw, cp.width), by1 = min(by0 + bw, cp.height);
+    const int sx = sub % subs_x, sy = sub / subs_x;
+    const int bx0 = tx * ts + sx * BW, by0 = ty * ts + sy * BH;
+    const int bx1 = min(bx0 + BW, cp.width), by1 = min(by0 + BH, cp.height);
     // pixel of this thread: warps own compact patches (8 x 4 for 16 x 16 blocks, 8 x 4 for 8 x 8)
     const int lx = ((tid >> 5) & ((bw >> 3) - 1)) * 8 + (tid & 7);
     const int ly = ((tid >> 5) / (bw >> 3)) * 4 + ((tid & 31) >> 3);
@@ -635,13 +637,16 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
                                  const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux, const float bg[3],
                                  const FwdOutputs& out) {
     const int ts = cp.tile_size;
-    const int bw = ts < 16 ? ts : 16;
-    const int subs = ts / bw;
-    dim3 grid((unsigned)(cp.tiles_x * cp.tiles_y), (unsigned)(subs * subs));
-    const int threads = bw * bw;
+    const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     LaunchScope ls_(lc, "blend_forward");
-#define BLEND_FWD(R, T) blend_forward_kernel<R, T><<<grid, threads, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, \
-                                                                                   bg[0], bg[1], bg[2], out)
+#define BLEND_FWD_SHAPE(R, T, W, H) \
+    blend_forward_kernel<R, T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out)
+#define BLEND_FWD(R, T)                                                        \
+    do {                                                                       \
+        if (cp.block_w == 16) BLEND_FWD_SHAPE(R, T, 16, 16);                   \
+        else if (cp.block_h == 8) BLEND_FWD_SHAPE(R, T, 8, 8);                 \
+        else BLEND_FWD_SHAPE(R, T, 8, 4);                                      \
+    } while (0)
     if (out.importance) {
         if (cp.apply_thresholds) BLEND_FWD(true, true);
         else BLEND_FWD(true, false);
@@ -649,6 +654,7 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
         if (cp.apply_thresholds) BLEND_FWD(false, true);
         else BLEND_FWD(false, false);
     }
+#undef BLEND_FWD_SHAPE
 #undef BLEND_FWD
     lc.count++;
     return cudaGetLastError();
