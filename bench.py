@@ -37,8 +37,10 @@ REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_powe
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--profile-steps", type=int, default=20,
+                    help="extra steps after the timed region, with per-kernel CUDA events (breakdown/roofline)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--views", type=int, default=1, help="ring views per rank per step")
     ap.add_argument("--gaussians", type=int, default=1_000_000)
@@ -158,12 +160,18 @@ def run_reference_arm(args):
 # our arm
 # ---------------------------------------------------------------------------------------------
 class ClockSampler:
+    """nvidia-smi clock / throttle-reason sampling (every 50 ms) around the timed region.
+
+    start() waits for the first sample so the sampler is live before the timed region; stop()
+    summarises the samples taken inside [t0, t1] (monotonic seconds, the timed region), falling
+    back to the samples nearest to it when the region is shorter than the sampling period."""
+
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.lines = []
 
-    def start(self):
+    def start(self, wait_s=5.0):
         q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
@@ -173,34 +181,50 @@ class ClockSampler:
             self.t.start()
         except OSError:
             self.proc = None
+            return
+        t_end = time.monotonic() + wait_s
+        while not self.lines and time.monotonic() < t_end:
+            time.sleep(0.01)
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.monotonic(), ln.strip()))
 
-    def stop(self):
+    def stop(self, t0, t1):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)  # one more period so the sample covering t1 arrives
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        for ln in self.lines:
+        parsed = []
+        for ts, ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 3 + len(REASONS):
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                parsed.append((ts, float(parts[0]), float(parts[1]),
+                               {r for r, v in zip(REASONS, parts[3:]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for r, v in zip(REASONS, parts[3:]):
-                if v.lower().startswith("active"):
-                    reasons.add(r)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        inside = [p for p in parsed if t0 <= p[0] <= t1 + 0.05]
+        sel = inside or sorted(parsed, key=lambda p: min(abs(p[0] - t0), abs(p[0] - t1)))[:2]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        reasons = set().union(*(p[3] for p in sel))
+        return {"sm_mhz": float(np.median([p[1] for p in sel])), "sm_max_mhz": sel[-1][2], "reasons": sorted(reasons),
+                "samples": len(sel), "samples_in_timed_region": len(inside)}
+
+
+def ncu_summary(kernel):
+    """The committed ncu --set full summary of `kernel` (profiles/ncu_summary.json), if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(p.read_text())["kernels"].get(kernel)
+    except Exception:
+        return None
 
 
 def algorithmic_bytes(kernel, n, n_surv, pairs, hw):
@@ -253,8 +277,6 @@ def run_ours(args):
         return [cams[i] for i in idx], [targets[i] for i in idx], idx
 
     stream = torch.cuda.current_stream()
-    # clocks are sampled from the start of the warm-up (GPU under the same load) to the end of the
-    # timed region
     clocks = ClockSampler(device)
     clocks.start()
     for st in range(args.warmup):
@@ -264,25 +286,35 @@ def run_ours(args):
 
     # ---- device-timed region -----------------------------------------------------------------
     lib = ctx.lib
-    lib.splat_profile_enable(ctx.h, 1)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.monotonic()
     ev0.record(stream)
-    pairs = []
+    pairs, survivors = [], []
     for st in range(args.warmup, args.warmup + args.steps):
         c, t, _ = views_for(st)
         trainer.step(c, t)
         pairs += trainer.pairs_last_step
+        survivors += trainer.survivors_last_step
     ev1.record(stream)
     torch.cuda.synchronize()
+    t_wall1 = time.monotonic()
     if world > 1:
         dist.barrier()
     launches = ctx.launches() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop(t_wall0, t_wall1)
     ms = ev0.elapsed_time(ev1)
+
+    # ---- per-kernel breakdown: a separate profiled pass (CUDA events around every launch) ------
+    lib.splat_profile_enable(ctx.h, 1)
+    p_steps = max(1, args.profile_steps)
+    for st in range(args.warmup + args.steps, args.warmup + args.steps + p_steps):
+        c, t, _ = views_for(st)
+        trainer.step(c, t)
+    torch.cuda.synchronize()
     names = C.create_string_buffer(4096)
     tot = (C.c_double * 64)()
     cnt = (C.c_int64 * 64)()
@@ -338,7 +370,7 @@ def run_ours(args):
     hw = 1237 * 822
     n = args.gaussians
     avg_pairs = float(np.mean(pairs)) if pairs else 0.0
-    n_surv = n  # all survive at cfg1 (ring radius 3R > R)
+    n_surv = float(np.mean(survivors)) if survivors else n
     roof = None
     if dom:
         ab = algorithmic_bytes(dom, n, n_surv, avg_pairs, hw)
@@ -349,7 +381,11 @@ def run_ours(args):
                     "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": ab,
                     "avg_launch_ms": avg_ms, "peak_source": peak_src,
                     "note": "blend kernels are issue-bound (FP32/SFU/LSU on staged records), not HBM-bound"}
-    breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+            ncu = ncu_summary(dom)
+            if ncu:
+                roof["traffic"] = ncu.get("dram_bytes_per_launch")
+                roof["ncu"] = ncu
+    breakdown = {k: {"ms_per_step": v[0] / p_steps, "launches_per_step": v[1] / p_steps,
                      "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
 
     cpu = None
@@ -368,7 +404,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE cfg1 shapes)",
                 "config": workload_config(args, world), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
-                "pairs_per_view": avg_pairs, "kernel_breakdown": breakdown}
+                "pairs_per_view": avg_pairs, "survivors_per_view": n_surv, "kernel_breakdown": breakdown}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

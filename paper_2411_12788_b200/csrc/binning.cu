@@ -4,8 +4,14 @@
 // The reference pushes every depth-sorted Gaussian into each tile its pixel rect touches, so a
 // tile's list is "the Gaussians covering it, in (depth, index) order".  A stable radix sort of P
 // pairs by tile reproduces that but moves ~16 B x P x 2 passes.  Instead:
-//   1. emit (supertile, Gaussian) pairs in depth order — a supertile is 4 x 4 tiles, so Ps ~ P/10;
-//   2. stable radix sort of the Ps pairs by supertile (one or two small passes);
+//   1-2. supertile lists (a supertile is 4 x 4 tiles, so Ps ~ P/6), stable in depth order, by a
+//      chunked counting sort with no pair array and no radix pass: the depth-ordered survivors
+//      are cut into chunks of kStChunk; one warp per chunk counts its entries per supertile
+//      (st_chunk_kernel<false>), an exclusive scan over the counts laid out supertile-major /
+//      chunk-minor gives every (supertile, chunk) its output offset, and the same warp re-walks
+//      the chunk writing each Gaussian id at offset + (rank among the chunk's earlier entries of
+//      that supertile), ranks from __match_any_sync over the flattened (Gaussian, supertile)
+//      entries.  (Fallback for > kStMaxSmem supertiles: emit pairs + stable radix sort.)
 //   3. split every supertile list into segments of kSeg entries; a count pass gives, per
 //      (tile, segment), how many entries of the segment cover the tile; an exclusive scan of those
 //      counts laid out tile-major / segment-minor gives every (tile, segment) its output offset;
@@ -26,6 +32,8 @@ constexpr int kST = 4;              // supertile side in tiles
 constexpr int kSTT = kST * kST;     // tiles per supertile
 constexpr int kSeg = 1024;          // entries per segment of a supertile list
 constexpr int kBinThreads = 256;
+constexpr int kStChunk = 128;       // depth-ordered survivors per chunk of the supertile pass
+constexpr int kStMaxSmem = 6144;    // supertiles the chunked pass keeps in shared memory
 
 struct TileRect {
     int tx0, tx1, ty0, ty1;  // inclusive tile range of a Gaussian's pixel rect
@@ -66,6 +74,97 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
         if (lane >= o) v += u;
     }
     return v;
+}
+
+// Supertile pass over one chunk of depth-ordered survivors, one warp per chunk.  The chunk's
+// Gaussians are flattened, 32 at a time, into (Gaussian, supertile) entries in (depth, raster)
+// order; every window of 32 entries is ranked per supertile with __match_any_sync, and a
+// per-supertile running count in shared memory carries the rank across windows.
+//   EMIT = false: cnt[st * nchunks + c] = entries of chunk c in supertile st.
+//   EMIT = true:  cnt holds the exclusive scan of those counts; writes st_gauss[offset + rank].
+template <bool EMIT>
+__global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict__ order,
+                                                      const uint2* __restrict__ rect_ref, int n_surv, int ts,
+                                                      int st_x, int n_st, int nchunks, uint32_t* __restrict__ cnt,
+                                                      uint32_t* __restrict__ st_gauss) {
+    extern __shared__ uint32_t s_run[];  // [n_st]
+    const int c = blockIdx.x, lane = threadIdx.x;
+    for (int st = lane; st < n_st; st += 32) s_run[st] = EMIT ? cnt[(size_t)st * nchunks + c] : 0u;
+    if (!EMIT && c == 0 && lane == 0) cnt[(size_t)n_st * nchunks] = 0u;  // scan slot of the total
+    __syncwarp();
+    const int g0 = c * kStChunk, g1 = min(g0 + kStChunk, n_surv);
+    const unsigned lt = lanemask_lt();
+    // the whole chunk's ids and rects are loaded up front (two dependent round trips per chunk)
+    constexpr int kPer = kStChunk / 32;
+    uint32_t gids[kPer];
+    uint2 rects[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int r = g0 + k * 32 + lane;
+        gids[k] = r < g1 ? order[r] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int r = g0 + k * 32 + lane;
+        rects[k] = r < g1 ? rect_ref[gids[k]] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int r = g0 + k * 32 + lane;
+        const uint32_t gid = gids[k];
+        int sx0 = 0, sy0 = 0, w = 1, m = 0;
+        if (r < g1) {
+            const TileRect t = tile_rect(rects[k], ts);
+            sx0 = t.tx0 / kST;
+            sy0 = t.ty0 / kST;
+            w = t.tx1 / kST - sx0 + 1;
+            m = w * (t.ty1 / kST - sy0 + 1);
+        }
+        if (!EMIT) {  // counts are order-free: shared-memory atomics per entry
+            for (int q = 0; q < m; ++q) atomicAdd(&s_run[(sy0 + q / w) * st_x + sx0 + q % w], 1u);
+            continue;
+        }
+        if (!__any_sync(0xffffffffu, m > 0)) continue;
+        const int inc = (int)warp_incl_scan((uint32_t)m, lane);
+        const int off = inc - m;
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        for (int e0 = 0; e0 < total; e0 += 32) {
+            const int e = e0 + lane;
+            const bool valid = e < total;
+            int owner = 0;  // last lane whose entries start at or before e
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+                if (__shfl_sync(0xffffffffu, off, owner + step) <= e) owner += step;
+            const int q = e - __shfl_sync(0xffffffffu, off, owner);
+            const int ow = __shfl_sync(0xffffffffu, w, owner);
+            const int st = (__shfl_sync(0xffffffffu, sy0, owner) + q / ow) * st_x + __shfl_sync(0xffffffffu, sx0, owner) +
+                           q % ow;
+            const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
+            const unsigned grp = __match_any_sync(0xffffffffu, valid ? st : -1);
+            const int leader = __ffs(grp) - 1;
+            uint32_t base = 0;
+            if (valid && lane == leader) {
+                base = s_run[st];
+                s_run[st] = base + (uint32_t)__popc(grp);
+            }
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (valid) st_gauss[base + __popc(grp & lt)] = ogid;
+            __syncwarp();
+        }
+    }
+    if (!EMIT) {
+        __syncwarp();
+        for (int st = lane; st < n_st; st += 32) cnt[(size_t)st * nchunks + c] = s_run[st];
+    }
+}
+
+// st_ranges[st] = [scanned[st * nchunks], scanned[(st + 1) * nchunks])
+__global__ void st_ranges_from_chunks_kernel(const uint32_t* __restrict__ scanned, int n_st, int nchunks,
+                                             uint32_t* __restrict__ ranges) {
+    const int st = blockIdx.x * blockDim.x + threadIdx.x;
+    if (st >= n_st) return;
+    ranges[2 * st] = scanned[(size_t)st * nchunks];
+    ranges[2 * st + 1] = scanned[(size_t)(st + 1) * nchunks];
 }
 
 // Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
@@ -254,26 +353,62 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 int supertile_side() { return kST; }
 size_t bin_segment_upper(uint64_t st_pairs, int n_st) { return (size_t)(st_pairs / kSeg + n_st + 1); }
 
+bool st_chunked(int n_st) { return n_st <= kStMaxSmem; }
+int st_chunks(int n_surv) { return n_surv > kStChunk ? (n_surv + kStChunk - 1) / kStChunk : 1; }
+size_t st_chunk_words(int n_surv, int n_st) { return (size_t)n_st * st_chunks(n_surv) + 1; }
+
 cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     const int n_st = a.st_x * a.st_y;
     const int n_tiles = a.tiles_x * a.tiles_y;
-    if (a.n_surv > 0) {
-        LaunchScope s(lc, "emit_st_pairs");
-        emit_st_pairs_kernel<<<blocks_for(a.n_surv, 256), 256, 0, lc.stream>>>(a.order, a.st_offsets, a.rect_ref, a.tile_size,
-                                                                             a.st_x, a.n_surv, a.st_key[0],
-                                                                             a.st_gauss[0]);
-        lc.count++;
-    }
-    bool alt = false;
-    cudaError_t e = radix_sort_pairs(lc, a.st_key[0], a.st_gauss[0], a.st_key[1], a.st_gauss[1], a.st_pairs, 0,
-                                     a.st_bits, a.hist, a.scan_tmp, &alt);
-    if (e != cudaSuccess) return e;
-    const uint32_t* keys = a.st_key[alt ? 1 : 0];
-    const uint32_t* gauss = a.st_gauss[alt ? 1 : 0];
-    {
-        LaunchScope s(lc, "st_ranges");
-        key_ranges_kernel<<<blocks_for(n_st, 256), 256, 0, lc.stream>>>(keys, (uint32_t)a.st_pairs, a.st_ranges, n_st);
-        lc.count++;
+    const uint32_t* gauss;
+    cudaError_t e;
+    if (st_chunked(n_st)) {
+        const int nchunks = st_chunks(a.n_surv);
+        const size_t smem = (size_t)n_st * 4;
+        if (smem > 48 * 1024) {
+            cudaFuncSetAttribute(st_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(st_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        }
+        {
+            LaunchScope s(lc, "st_count");
+            st_chunk_kernel<false><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, a.tile_size, a.st_x,
+                                                                     n_st, nchunks, a.st_cnt, nullptr);
+            lc.count++;
+        }
+        e = exclusive_scan_u32(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.scan_tmp, nullptr);
+        if (e != cudaSuccess) return e;
+        {
+            LaunchScope s(lc, "st_emit");
+            st_chunk_kernel<true><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, a.tile_size, a.st_x,
+                                                                    n_st, nchunks, a.st_cnt, a.st_gauss[0]);
+            lc.count++;
+        }
+        {
+            LaunchScope s(lc, "st_ranges");
+            st_ranges_from_chunks_kernel<<<blocks_for(n_st, 256), 256, 0, lc.stream>>>(a.st_cnt, n_st, nchunks,
+                                                                                      a.st_ranges);
+            lc.count++;
+        }
+        gauss = a.st_gauss[0];
+    } else {
+        if (a.n_surv > 0) {
+            LaunchScope s(lc, "emit_st_pairs");
+            emit_st_pairs_kernel<<<blocks_for(a.n_surv, 256), 256, 0, lc.stream>>>(
+                a.order, a.st_offsets, a.rect_ref, a.tile_size, a.st_x, a.n_surv, a.st_key[0], a.st_gauss[0]);
+            lc.count++;
+        }
+        bool alt = false;
+        e = radix_sort_pairs(lc, a.st_key[0], a.st_gauss[0], a.st_key[1], a.st_gauss[1], a.st_pairs, 0, a.st_bits,
+                             a.hist, a.scan_tmp, &alt);
+        if (e != cudaSuccess) return e;
+        const uint32_t* keys = a.st_key[alt ? 1 : 0];
+        gauss = a.st_gauss[alt ? 1 : 0];
+        {
+            LaunchScope s(lc, "st_ranges");
+            key_ranges_kernel<<<blocks_for(n_st, 256), 256, 0, lc.stream>>>(keys, (uint32_t)a.st_pairs, a.st_ranges,
+                                                                           n_st);
+            lc.count++;
+        }
     }
     {
         LaunchScope s(lc, "seg_setup");

@@ -123,10 +123,11 @@ struct splat_ctx {
     // per-Gaussian
     DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
-    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_ranges, seg_start, tile_base, slots;
+    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_ranges, seg_start, tile_base, slots;
     // misc
-    DevBuf ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
-    uint32_t* host_counters = nullptr;  // pinned [n_surv, P]
+    DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
+    uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
+    cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     FwdState st;
 };
 
@@ -277,6 +278,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         color_out = ctx->color.as<float>();
     }
     if (!ctx->host_counters) CK(cudaMallocHost(&ctx->host_counters, 64), "alloc pinned");
+    if (!ctx->ev_counts) CK(cudaEventCreateWithFlags(&ctx->ev_counts, cudaEventDisableTiming), "event");
 
     uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] = n_surv, [1] = P
     CK(cudaMemsetAsync(d_counters, 0, 16, s), "memset counters");  // [0] survivors [1] Ps [2] P
@@ -290,35 +292,45 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>()),
            "preprocess");
+        // The host needs [n_surv, Ps, P] (sizes and allocations below); they are final after
+        // preprocess, so the copy is queued before the depth sort and the host waits only for
+        // it: the sort runs while the rest of the view is enqueued.
+        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
+        CK(cudaEventRecord(ctx->ev_counts, s), "record counts");
         bool alt = false;
         CK(radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), (uint64_t)n, 0,
                             32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
            "depth sort");
         const uint32_t* order = alt ? ctx->vals[1].as<uint32_t>() : vals;
-        CK(exclusive_scan_gather_u32(lc, ctx->tile_counts.as<uint32_t>(), order, ctx->offsets.as<uint32_t>(),
-                                     (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), d_counters + 1),
-           "scan supertile counts");
-        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
-        CK(cudaStreamSynchronize(s), "sync counts");
-        n_surv = (int)ctx->host_counters[0];
-        const uint64_t st_pairs = ctx->host_counters[1];
-        n_pairs = ctx->host_counters[2];
         const int sts = supertile_side();
         const int st_x = (cp.tiles_x + sts - 1) / sts, st_y = (cp.tiles_y + sts - 1) / sts;
         const int n_st = st_x * st_y;
-        for (int k = 0; k < 2; ++k) {
-            CK(ctx->st_key[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
+        const bool chunked = st_chunked(n_st);
+        if (!chunked)  // fallback supertile pass: pair offsets in depth order
+            CK(exclusive_scan_gather_u32(lc, ctx->tile_counts.as<uint32_t>(), order, ctx->offsets.as<uint32_t>(),
+                                         (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), nullptr),
+               "scan supertile counts");
+        CK(cudaEventSynchronize(ctx->ev_counts), "sync counts");
+        n_surv = (int)ctx->host_counters[0];
+        const uint64_t st_pairs = ctx->host_counters[1];
+        n_pairs = ctx->host_counters[2];
+        for (int k = 0; k < (chunked ? 1 : 2); ++k) {
+            if (!chunked) CK(ctx->st_key[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
             CK(ctx->st_gauss[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
         }
+        const size_t st_words = chunked ? st_chunk_words(n_surv, n_st) : 1;
+        if (chunked) CK(ctx->st_cnt.ensure(st_words * 4), "alloc st counts");
         CK(ctx->pair_gauss[0].ensure(n_pairs * 4 + 4), "alloc pairs");
         CK(ctx->st_ranges.ensure((size_t)n_st * 8), "alloc st ranges");
         CK(ctx->seg_start.ensure(((size_t)n_st + 1) * 4), "alloc seg");
         CK(ctx->tile_base.ensure(((size_t)n_tiles + 1) * 4), "alloc tile base");
         const size_t n_slots = bin_segment_upper(st_pairs, n_st) * 16 + 1;
         CK(ctx->slots.ensure(n_slots * 4), "alloc slots");
-        const size_t hwords = radix_hist_words(st_pairs, 8);
-        CK(ctx->hist.ensure(hwords * 4), "alloc hist");
-        CK(ctx->scan_tmp.ensure((scan_temp_words(hwords > n_slots ? hwords : n_slots) + 64) * 4), "alloc scan");
+        const size_t hwords = chunked ? 0 : radix_hist_words(st_pairs, 8);
+        if (!chunked) CK(ctx->hist.ensure(hwords * 4), "alloc hist");
+        size_t scan_n = hwords > n_slots ? hwords : n_slots;
+        scan_n = scan_n > st_words ? scan_n : st_words;
+        CK(ctx->scan_tmp.ensure((scan_temp_words(scan_n) + 64) * 4), "alloc scan");
         BinningArgs ba{};
         ba.order = order;
         ba.st_offsets = ctx->offsets.as<uint32_t>();
@@ -335,6 +347,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
             ba.st_key[k] = ctx->st_key[k].as<uint32_t>();
             ba.st_gauss[k] = ctx->st_gauss[k].as<uint32_t>();
         }
+        ba.st_cnt = ctx->st_cnt.as<uint32_t>();
         ba.st_ranges = ctx->st_ranges.as<uint32_t>();
         ba.seg_start = ctx->seg_start.as<uint32_t>();
         ba.tile_base = ctx->tile_base.as<uint32_t>();
@@ -422,7 +435,10 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     }
     if (n > 0) {
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
-        CK(launch_chain(lc, gp, st.cp, ctx->grad2d.as<float>(), ctx->rec.as<ProjRec>(), *grads, accumulate), "chain");
+        CK(ctx->chain_list.ensure(((size_t)st.n_surv + 2) * 4), "alloc chain list");
+        CK(launch_chain(lc, gp, st.cp, ctx->grad2d.as<float>(), ctx->rec.as<ProjRec>(), *grads, accumulate, st.n_surv,
+                        ctx->chain_list.as<uint32_t>()),
+           "chain");
     }
     if (partials) {
         const float inv_n = 1.0f / (float)(3 * (int64_t)st.cp.width * st.cp.height);
@@ -455,6 +471,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (!ctx) return SPLAT_OK;
     cudaSetDevice(ctx->device);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
+    if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
     delete ctx->lc.prof;
     delete ctx;
     return SPLAT_OK;

@@ -106,7 +106,7 @@ constexpr int kShRow = 13;  // float4 per staged SH row (12 + 1 pad: conflict-fr
 template <bool VEC>
 __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
                                           const ProjRec* __restrict__ rec, splat_param_grads out, int accumulate,
-                                          int i, float4* s_sh) {
+                                          int i, float4* s_sh, int row) {
     if (i >= g.n) return;
     // accumulator (blend_backward): g0 = (dmean.x, dmean.y, dconic00), g1 = (dconic01, dconic11,
     // dopacity), g2 = d colour, g3.x = number of committed (warp, pixel) samples
@@ -131,7 +131,7 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
         }
         if (VEC) {  // zero gradient row (copied out / added by the caller)
 #pragma unroll
-            for (int k = 0; k < 12; ++k) s_sh[threadIdx.x * kShRow + k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < 12; ++k) s_sh[row * kShRow + k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         return;
     }
@@ -285,7 +285,7 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     sh_basis_all(dir0, dir1, dir2, deg, basis);
     float shv[48];
     if (VEC) {
-        const float4* s4 = &s_sh[threadIdx.x * kShRow];
+        const float4* s4 = &s_sh[row * kShRow];
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
             const float4 vv = s4[k];
@@ -350,7 +350,7 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     }
     out.d_opacity_logits[i] = (accumulate ? out.d_opacity_logits[i] : 0.0f) + dlogit;
     if (VEC) {  // the fresh gradient row; the caller writes (or adds) it coalesced
-        float4* d4 = &s_sh[threadIdx.x * kShRow];
+        float4* d4 = &s_sh[row * kShRow];
 #pragma unroll
         for (int k = 0; k < 12; ++k) d4[k] = make_float4(dsh[4 * k], dsh[4 * k + 1], dsh[4 * k + 2], dsh[4 * k + 3]);
     } else {
@@ -360,34 +360,86 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     if (out.grad2d_count) out.grad2d_count[i] = (accumulate ? out.grad2d_count[i] : 0) + 1;
 }
 
-// The SH rows (192 B in, 192 B of gradients out per Gaussian) move between HBM and shared memory
-// with coalesced float4 copies; the per-thread chain reads / writes its row in shared memory.
-template <bool VEC>
+// Plain one-thread-per-Gaussian chain (SH pointers not 16-byte aligned).
 __global__ void __launch_bounds__(kChainThreads) chain_kernel(GaussianPtrs g, CamParams cp, float4* __restrict__ grad2d,
                                                              const ProjRec* __restrict__ rec, splat_param_grads out,
                                                              int accumulate) {
-    __shared__ float4 s_sh[VEC ? kChainThreads * kShRow : 1];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int base = blockIdx.x * kChainThreads;
-    const int cnt = min(kChainThreads, g.n - base);
-    if (VEC) {
-        const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)base);
-        for (int q = threadIdx.x; q < cnt * 12; q += kChainThreads) s_sh[(q / 12) * kShRow + q % 12] = __ldg(src + q);
-        __syncthreads();
+    chain_one<false>(g, cp, grad2d, rec, out, accumulate, i, nullptr, 0);
+}
+
+// Zero count floats from p, cooperatively by one warp (float4 stores when p is 16-byte aligned).
+__device__ __forceinline__ void zero_span_warp(float* p, int count, int lane) {
+    int head = 0;
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        const int n4 = count >> 2;
+        float4* p4 = reinterpret_cast<float4*>(p);
+        for (int q = lane; q < n4; q += 32) p4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        head = n4 << 2;
     }
-    chain_one<VEC>(g, cp, grad2d, rec, out, accumulate, i, s_sh);
-    if (VEC) {
-        __syncthreads();
-        float4* dst = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)base);
-        for (int q = threadIdx.x; q < cnt * 12; q += kChainThreads) {
-            const float4 d = s_sh[(q / 12) * kShRow + q % 12];
-            if (accumulate) {
-                float4 o = dst[q];
-                o.x = o.x + d.x; o.y = o.y + d.y; o.z = o.z + d.z; o.w = o.w + d.w;
-                dst[q] = o;
-            } else {
-                dst[q] = d;
-            }
+    for (int q = head + lane; q < count; q += 32) p[q] = 0.0f;
+}
+
+// Only Gaussians some pixel committed ("touched": a fraction of the survivors) need the chain.
+// Pass 1 lists them (warp-aggregated append; list order is irrelevant, every Gaussian's chain is
+// independent) and, for a fresh gradient, writes the zero gradients of all others with
+// coalesced stores.  Pass 2 runs the chain on the list with every lane busy; each thread stages
+// its own 192-byte SH row in shared memory with float4 loads and writes its gradient row back
+// the same way.
+__global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __restrict__ grad2d, int n,
+                                                            splat_param_grads out, int accumulate,
+                                                            uint32_t* __restrict__ list) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool touched = i < n && grad2d[4 * (size_t)i + 3].x > 0.0f;
+    const unsigned m = __ballot_sync(0xffffffffu, touched);
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(list, (uint32_t)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (touched) list[1 + base + __popc(m & lanemask_lt())] = (uint32_t)i;
+    }
+    if (accumulate) return;  // nothing to add for untouched Gaussians
+    // Every gradient of the warp's 32 Gaussians is zeroed here (touched ones are overwritten by
+    // pass 2): each array's span for the warp is contiguous, so the warp writes it with float4
+    // stores (full sectors only).
+    const int w0 = i - lane;
+    const int rows = min(32, n - w0);
+    if (rows <= 0) return;
+    zero_span_warp(out.d_centers + 3 * (size_t)w0, 3 * rows, lane);
+    zero_span_warp(out.d_log_scales + 3 * (size_t)w0, 3 * rows, lane);
+    zero_span_warp(out.d_rotations + 4 * (size_t)w0, 4 * rows, lane);
+    zero_span_warp(out.d_opacity_logits + (size_t)w0, rows, lane);
+    zero_span_warp(out.d_sh + 48 * (size_t)w0, 48 * rows, lane);
+    if (out.grad2d_accum) zero_span_warp(out.grad2d_accum + (size_t)w0, rows, lane);
+    if (out.grad2d_count && lane < rows) out.grad2d_count[w0 + lane] = 0;
+}
+
+__global__ void __launch_bounds__(kChainThreads) chain_touched_kernel(GaussianPtrs g, CamParams cp,
+                                                                     float4* __restrict__ grad2d,
+                                                                     const ProjRec* __restrict__ rec,
+                                                                     splat_param_grads out, int accumulate,
+                                                                     const uint32_t* __restrict__ list) {
+    __shared__ float4 s_sh[kChainThreads * kShRow];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int)list[0]) return;
+    const int i = (int)list[1 + t];
+    const int row = threadIdx.x;
+    const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)i);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) s_sh[row * kShRow + k] = __ldg(src + k);
+    chain_one<true>(g, cp, grad2d, rec, out, accumulate, i, s_sh, row);
+    float4* dst = reinterpret_cast<float4*>(out.d_sh + 48 * (size_t)i);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const float4 d = s_sh[row * kShRow + k];
+        if (accumulate) {
+            float4 o = dst[k];
+            o.x = o.x + d.x; o.y = o.y + d.y; o.z = o.z + d.z; o.w = o.w + d.w;
+            dst[k] = o;
+        } else {
+            dst[k] = d;
         }
     }
 }
@@ -397,17 +449,29 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 }  // namespace
 
 cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d, const ProjRec* rec,
-                         const splat_param_grads& out, int accumulate) {
+                         const splat_param_grads& out, int accumulate, int n_surv, uint32_t* list) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
-    LaunchScope ls(lc, "chain");
-    if (vec)
-        chain_kernel<true><<<blocks_for(g.n, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d), rec,
-                                                                       out, accumulate);
-    else
-        chain_kernel<false><<<blocks_for(g.n, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, reinterpret_cast<float4*>(grad2d),
-                                                                        rec, out, accumulate);
-    lc.count++;
+    float4* g2 = reinterpret_cast<float4*>(grad2d);
+    if (!vec) {
+        LaunchScope ls(lc, "chain");
+        chain_kernel<<<blocks_for(g.n, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, g2, rec, out, accumulate);
+        lc.count++;
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaMemsetAsync(list, 0, 4, lc.stream);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope ls(lc, "chain_compact");
+        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out, accumulate, list);
+        lc.count++;
+    }
+    if (n_surv > 0) {
+        LaunchScope ls(lc, "chain");
+        chain_touched_kernel<<<blocks_for(n_surv, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, g2, rec, out,
+                                                                                               accumulate, list);
+        lc.count++;
+    }
     return cudaGetLastError();
 }
 

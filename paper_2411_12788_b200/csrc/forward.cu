@@ -281,16 +281,26 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
             if (aux) aux[i] = a;
         }
     }
-    __shared__ uint32_t s_pairs[8];
-    uint32_t wp = tiles;
+    __shared__ uint32_t s_pairs[8], s_st[8];
+    uint32_t wp = tiles, ws = alive ? count : 0u;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(0xffffffffu, wp, o);
-    if ((threadIdx.x & 31) == 0) s_pairs[threadIdx.x >> 5] = wp;
+    for (int o = 16; o > 0; o >>= 1) {
+        wp += __shfl_xor_sync(0xffffffffu, wp, o);
+        ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_pairs[threadIdx.x >> 5] = wp;
+        s_st[threadIdx.x >> 5] = ws;
+    }
     const int block_alive = __syncthreads_count(alive);
     if (threadIdx.x == 0 && block_alive) {
-        uint32_t bp = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) bp += s_pairs[w];
+        uint32_t bp = 0, bs = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            bp += s_pairs[w];
+            bs += s_st[w];
+        }
         atomicAdd(n_surv, (uint32_t)block_alive);
+        atomicAdd(n_surv + 1, bs);
         atomicAdd(n_surv + 2, bp);
     }
 }

@@ -61,7 +61,7 @@ struct GaussianPtrs {
 
 // K1: per-Gaussian projection. Writes rec/aux (aux may be null), depth keys (0xFFFFFFFF when
 // culled), identity values and per-Gaussian SUPERTILE counts (0 = culled);
-// counters[0] += survivors, counters[2] += tile pairs P.
+// counters[0] += survivors, counters[1] += supertile pairs Ps, counters[2] += tile pairs P.
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
@@ -85,8 +85,9 @@ struct BinningArgs {
     int n_surv;
     uint64_t st_pairs;
     int tile_size, tiles_x, tiles_y, st_x, st_y, st_bits;
-    uint32_t* st_key[2];
-    uint32_t* st_gauss[2];
+    uint32_t* st_key[2];    // fallback path only
+    uint32_t* st_gauss[2];  // [0]: supertile lists (chunked path); both: sort ping-pong (fallback)
+    uint32_t* st_cnt;       // [st_chunk_words] chunked path: (supertile, chunk) counts / offsets
     uint32_t* st_ranges;   // [2 * n_st]
     uint32_t* seg_start;   // [n_st + 1]
     uint32_t* tile_base;   // [n_tiles + 1]
@@ -98,6 +99,11 @@ struct BinningArgs {
 };
 int supertile_side();
 size_t bin_segment_upper(uint64_t st_pairs, int n_st);
+// Chunked supertile pass (no pair sort) when the supertile count fits shared memory; otherwise
+// the fallback needs st_offsets (exclusive scan of supertile counts in depth order) and st_key.
+bool st_chunked(int n_st);
+int st_chunks(int n_surv);
+size_t st_chunk_words(int n_surv, int n_st);
 cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a);
 
 struct FwdOutputs {
@@ -142,8 +148,10 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const float* d_color, const float* color, const float* target,
                                   float* loss_partials, float* grad2d);
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
+// K10 chain.  list: scratch of n_surv + 1 words (touched-Gaussian list; touched <= survivors).
 cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d,
-                         const ProjRec* rec, const splat_param_grads& out, int accumulate);
+                         const ProjRec* rec, const splat_param_grads& out, int accumulate, int n_surv,
+                         uint32_t* list);
 cudaError_t launch_l1(LaunchCtx& lc, const float* a, const float* b, int64_t n, float* grad,
                       float* partials, int n_partials);
 int l1_partials_count(int64_t n);

@@ -59,6 +59,7 @@ class ViewTrainer:
         self.loss = torch.zeros(max_views, dtype=torch.float32, device=f"cuda:{self.ctx.device}")
         self.pg = process_group
         self.pairs_last_step: list[int] = []
+        self.survivors_last_step: list[int] = []
         self._empty_out = RenderOutputs()
         self._gs = params.struct()
         self._gr = self.grads.struct()
@@ -79,12 +80,14 @@ class ViewTrainer:
     def _views(self, cams: Sequence[Camera], targets) -> None:
         lib, h = self.ctx.lib, self.ctx.h
         self.pairs_last_step = []
+        self.survivors_last_step = []
         for j, (cam, tgt) in enumerate(zip(cams, targets)):
             self.ctx.check(lib.splat_render(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), None, self.bg,
                                             C.byref(self._empty_out), None))
-            np_ = C.c_int64()
-            lib.splat_forward_counts(h, None, C.byref(np_), None, None)
+            ns_, np_ = C.c_int64(), C.c_int64()
+            lib.splat_forward_counts(h, C.byref(ns_), C.byref(np_), None, None)
             self.pairs_last_step.append(np_.value)
+            self.survivors_last_step.append(ns_.value)
             self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
                                                         as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
                                                         1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
