@@ -235,8 +235,10 @@ def algorithmic_bytes(kernel, n, n_surv, pairs, hw):
         return 4 * pairs + 48 * n_surv + 32 * hw + 48 * n_surv
     if kernel == "blend_forward":
         return 4 * pairs + 48 * n_surv + 20 * hw  # ids + records + colour 12, T 4, last 4
+    if kernel == "chain_compact":
+        return 16 * n + 236 * n + 4 * n  # commit counts read, every gradient row zeroed, touched list
     if kernel == "chain":
-        return 48 * n + 48 * n + 236 * n + 236 * n + 48 * n  # grad2d r/w-zero, rec, params, grads
+        return None  # touched Gaussians only: ~650 B each (params, rec, grad2d, gradients)
     if kernel == "preprocess":
         return 236 * n + 48 * n + 12 * n
     return None
