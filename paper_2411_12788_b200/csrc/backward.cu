@@ -61,7 +61,7 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
 // With target != nullptr, dL/dC = sign(C - target)/n (l1_loss, loss.cpp:63-76) is fused in and
 // the CTA's L1 partial sum is written to loss_partials[block].
 template <bool THR, int BW, int BH>
-__global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+__device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
                                                             const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
                                                             const float* __restrict__ t_final,
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, c
     // sub-blocks of one tile are adjacent in the grid, so the tile's list and records are
     // re-read from L2 while still hot
     const int subs_x = ts / BW, nsub = subs_x * (ts / BH);
-    const int tile = (int)blockIdx.x / nsub, sub = (int)blockIdx.x - tile * nsub;
+    const int tile = bid / nsub, sub = bid - tile * nsub;
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
     const int sx = sub % subs_x, sy = sub / subs_x;
     const int bx0 = tx * ts + sx * BW, by0 = ty * ts + sy * BH;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, c
     if (target && loss_partials && tid == 0) {
         float s = 0.0f;
         for (int w = 0; w < nwarps; ++w) s += s_red[w];
-        loss_partials[blockIdx.x] = s;
+        loss_partials[bid] = s;
     }
     int block_last = -1;
     for (int w = 0; w < nwarps; ++w) block_last = max(block_last, s_maxlast[w]);
@@ -193,6 +193,42 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, c
             }
         }
         __syncthreads();  // the next batch overwrites the staging area
+    }
+}
+
+template <bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+                                                            const uint32_t* __restrict__ pair_gauss,
+                                                            const ProjRec* __restrict__ rec,
+                                                            const float* __restrict__ t_final,
+                                                            const int32_t* __restrict__ last_index, float bg0,
+                                                            float bg1, float bg2, const float* __restrict__ d_color,
+                                                            const float* __restrict__ color,
+                                                            const float* __restrict__ target, float inv_n,
+                                                            float* __restrict__ loss_partials,
+                                                            float4* __restrict__ grad2d) {
+    blend_backward_block<THR, BW, BH>((int)blockIdx.x, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
+}
+
+template <bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_backward_persistent(CamParams cp, const uint32_t* __restrict__ ranges,
+                                                            const uint32_t* __restrict__ pair_gauss,
+                                                            const ProjRec* __restrict__ rec,
+                                                            const float* __restrict__ t_final,
+                                                            const int32_t* __restrict__ last_index, float bg0,
+                                                            float bg1, float bg2, const float* __restrict__ d_color,
+                                                            const float* __restrict__ color,
+                                                            const float* __restrict__ target, float inv_n,
+                                                            float* __restrict__ loss_partials,
+                                                            float4* __restrict__ grad2d, int nblocks, int* __restrict__ counter) {
+    __shared__ int s_bid;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_bid = atomicAdd(counter, 1);
+        __syncthreads();
+        const int b = s_bid;
+        if (b >= nblocks) break;
+        blend_backward_block<THR, BW, BH>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
     }
 }
 
@@ -298,10 +334,23 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
     {
         LaunchScope ls_(lc, "blend_backward");
-#define BLEND_BWD_SHAPE(T, W, H)                                                                                   \
-    blend_backward_kernel<T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, t_final, last_index, \
-                                                                  bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
-                                                                  loss_partials, reinterpret_cast<float4*>(grad2d))
+#define BLEND_BWD_SHAPE(T, W, H)                                                                                  \
+    do {                                                                                                          \
+        if (lc.persistent_blend && lc.work_counters) {                                                            \
+            static int per_sm = 0;                                                                                \
+            if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_backward_persistent<T, W, H>, \
+                                                                      W * H, 0);                                  \
+            const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                              \
+            cudaMemsetAsync(lc.work_counters + 1, 0, 4, lc.stream);                                               \
+            blend_backward_persistent<T, W, H><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(                  \
+                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
+                loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);              \
+        } else {                                                                                                  \
+            blend_backward_kernel<T, W, H><<<grid, W * H, 0, lc.stream>>>(                                       \
+                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
+                loss_partials, reinterpret_cast<float4*>(grad2d));                                                \
+        }                                                                                                         \
+    } while (0)
 #define BLEND_BWD(T)                                             \
     do {                                                         \
         if (cp.block_w == 16) BLEND_BWD_SHAPE(T, 16, 16);        \

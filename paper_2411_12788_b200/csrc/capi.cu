@@ -463,6 +463,14 @@ int splat_ctx_create(int device, splat_ctx** out) {
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         c->lc.num_sms = sms;
+    if (cudaMalloc(&c->lc.work_counters, 16 * sizeof(int)) != cudaSuccess) {
+        delete c;
+        return SPLAT_ERR_OUT_OF_MEMORY;
+    }
+    {
+        const char* e = std::getenv("SPLAT_BLEND_PERSISTENT");
+        c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
+    }
     *out = c;
     return SPLAT_OK;
 }
@@ -472,6 +480,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
+    if (ctx->lc.work_counters) cudaFree(ctx->lc.work_counters);
     delete ctx->lc.prof;
     delete ctx;
     return SPLAT_OK;

@@ -369,7 +369,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // each batch is culled to the Gaussians that can reach the alpha floor inside the block and
 // staged in shared memory, and all threads walk it in the same order (broadcast reads).
 template <bool REPORT, bool THR, int BW, int BH>
-__global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+__device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, co
     // sub-blocks of one tile are adjacent in the grid, so the tile's list and records are
     // re-read from L2 while still hot
     const int subs_x = ts / BW, nsub = subs_x * (ts / BH);
-    const int tile = (int)blockIdx.x / nsub, sub = (int)blockIdx.x - tile * nsub;
+    const int tile = bid / nsub, sub = bid - tile * nsub;
     const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
     const int sx = sub % subs_x, sy = sub / subs_x;
     const int bx0 = tx * ts + sx * BW, by0 = ty * ts + sy * BH;
@@ -540,6 +540,34 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, co
     }
 }
 
+template <bool REPORT, bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+                                                           const uint32_t* __restrict__ pair_gauss,
+                                                           const ProjRec* __restrict__ rec,
+                                                           const AuxRec* __restrict__ aux, float bg0, float bg1,
+                                                           float bg2, FwdOutputs out) {
+    blend_forward_block<REPORT, THR, BW, BH>((int)blockIdx.x, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
+}
+
+// Persistent variant: one wave of CTAs pulls pixel blocks from a work counter (no CTA launch /
+// retire gaps between blocks, occupancy stays at the register limit through the whole kernel).
+template <bool REPORT, bool THR, int BW, int BH>
+__global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp, const uint32_t* __restrict__ ranges,
+                                                           const uint32_t* __restrict__ pair_gauss,
+                                                           const ProjRec* __restrict__ rec,
+                                                           const AuxRec* __restrict__ aux, float bg0, float bg1,
+                                                           float bg2, FwdOutputs out, int nblocks, int* __restrict__ counter) {
+    __shared__ int s_bid;
+    for (;;) {
+        __syncthreads();  // the previous block's shared-memory reads are done
+        if (threadIdx.x == 0) s_bid = atomicAdd(counter, 1);
+        __syncthreads();
+        const int b = s_bid;
+        if (b >= nblocks) break;
+        blend_forward_block<REPORT, THR, BW, BH>(b, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
+    }
+}
+
 __global__ void unproject_flags_kernel(int width, int height, const int32_t* __restrict__ max_contributor,
                                        const float* __restrict__ alpha, int rule, float thr, int64_t view_index,
                                        int32_t stride, int64_t seed, uint32_t* __restrict__ flags) {
@@ -649,8 +677,21 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
     const int ts = cp.tile_size;
     const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     LaunchScope ls_(lc, "blend_forward");
-#define BLEND_FWD_SHAPE(R, T, W, H) \
-    blend_forward_kernel<R, T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out)
+#define BLEND_FWD_SHAPE(R, T, W, H)                                                                              \
+    do {                                                                                                         \
+        if (lc.persistent_blend && lc.work_counters) {                                                           \
+            static int per_sm = 0;                                                                               \
+            if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_forward_persistent<R, T, W, H>, \
+                                                                      W * H, 0);                                 \
+            const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                             \
+            cudaMemsetAsync(lc.work_counters, 0, 4, lc.stream);                                                  \
+            blend_forward_persistent<R, T, W, H><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(               \
+                cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters);       \
+        } else {                                                                                                 \
+            blend_forward_kernel<R, T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], \
+                                                                           bg[1], bg[2], out);                   \
+        }                                                                                                        \
+    } while (0)
 #define BLEND_FWD(R, T)                                                        \
     do {                                                                       \
         if (cp.block_w == 16) BLEND_FWD_SHAPE(R, T, 16, 16);                   \

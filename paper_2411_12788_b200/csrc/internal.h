@@ -21,6 +21,8 @@ struct LaunchCtx {
     cudaStream_t stream = nullptr;
     int64_t count = 0;  // kernels launched (bench accounting)
     int num_sms = 148;
+    int* work_counters = nullptr;  // device ints for persistent-CTA work queues ([0] fwd, [1] bwd)
+    bool persistent_blend = true;  // blend kernels as persistent CTAs pulling pixel blocks
     ProfileState* prof = nullptr;  // non-null while per-kernel CUDA-event timing is on
     // Bracket one kernel launch with CUDA events on `stream` (no-ops when profiling is off).
     void prof_begin(const char* name);
