@@ -5,6 +5,7 @@
 // backward reconstructs T_before = T_after / (1 - alpha) instead of storing per-sample T.
 // The gates themselves are replayed bit-exactly (gate_sample uses explicit _rn intrinsics), so
 // the set of committed samples is identical to the forward's.  FMA contraction is allowed here.
+#include <climits>
 #include <cstdint>
 
 #include "common.cuh"
@@ -42,6 +43,35 @@ __device__ __forceinline__ void warp_reduce12(const float v[12], int lane, float
     }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
+}
+
+// The same transpose reduction for 24 values (two entries x four groups of 3) in 27 shuffles: on
+// return lanes 4g (g = 0..7) hold the warp totals of values 3g .. 3g+2 in out[0..2].
+__device__ __forceinline__ void warp_reduce24(const float v[24], int lane, float out[3]) {
+    const bool a = lane & 16, b = lane & 8, c = lane & 4;
+    float u[12], w[6];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+        const float send = a ? v[i] : v[12 + i];
+        const float keep = a ? v[12 + i] : v[i];
+        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const float send = b ? u[i] : u[6 + i];
+        const float keep = b ? u[6 + i] : u[i];
+        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float send = c ? w[i] : w[3 + i];
+        const float keep = c ? w[3 + i] : w[i];
+        out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1)
 #pragma unroll
         for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
 }
@@ -142,53 +172,69 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
     for (int hi = block_last + 1; hi > (int)start; hi -= nthreads) {
         const int count = min(nthreads, hi - (int)start);
         const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1, sm);
-        for (int j = 0; j < cnt; ++j) {
-            const int idx = (int)lds_u32(a_idx + 4u * j);
-            if (idx > wl) continue;  // above every commit of this warp (warp-uniform)
-            const float4 r1 = lds_f4(a_r1 + 16u * j);
-            if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
+        // Two staged entries per iteration: their gates are independent instruction streams (the
+        // branch-free gate), the per-pixel recursion then commits them in list order (j first: the
+        // batch is staged back to front), and one 24-value transpose reduction serves both.
+        for (int j = 0; j < cnt; j += 2) {
+            const bool has_b = j + 1 < cnt;
+            const uint32_t jb = has_b ? (uint32_t)(j + 1) : (uint32_t)j;
+            const int idx_a = (int)lds_u32(a_idx + 4u * j);
+            const int idx_b = has_b ? (int)lds_u32(a_idx + 4u * jb) : INT_MAX;
+            const float4 r1a = lds_f4(a_r1 + 16u * j);
+            const float4 r1b = lds_f4(a_r1 + 16u * jb);
+            const uint32_t ma = __float_as_uint(r1a.z), mb = __float_as_uint(r1b.z);
+            // warp-uniform: above every commit of this warp, or the effective rect misses its patch
+            const bool wa = idx_a <= wl && (ma & wrows) && (ma & wcols);
+            const bool wb = idx_b <= wl && (mb & wrows) && (mb & wcols);
+            if (!wa && !wb) continue;
+            const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
+            float alpha_a, g_a, dxa, dya, alpha_b, g_b, dxb, dyb;
+            bool cl_a, cl_b;
+            bool ga = gate_sample_nb<THR>(r0a, r1a, mybits, x, y, amax_c, cmin, alpha_a, g_a, cl_a, dxa, dya);
+            bool gb = gate_sample_nb<THR>(r0b, r1b, mybits, x, y, amax_c, cmin, alpha_b, g_b, cl_b, dxb, dyb);
+            ga = ga && wa && idx_a <= my_last;
+            gb = gb && wb && idx_b <= my_last;
             // v: (dmean.x, dmean.y, dconic00 | dconic01, dconic11, dopacity | dcolour rgb | commits)
-            float v[12];
+            // for entry a in v[0..11], entry b in v[12..23]
+            float v[24];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) v[k] = 0.0f;
-            bool committed = false;
-            if (idx <= my_last) {
-                float alpha, g2d, dx, dy;
-                bool clamped;
-                const float4 r0 = lds_f4(a_r0 + 16u * j);
-                if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
-                    committed = true;
-                    const float4 r2 = lds_f4(a_r2 + 16u * j);
-                    const float one_m_a = 1.0f - alpha;
-                    const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
-                    const float w = t_before * alpha;
-                    v[6] = w * dL0;
-                    v[7] = w * dL1;
-                    v[8] = w * dL2;
-                    const float da = t_before * (dL0 * (r2.x - b0) + dL1 * (r2.y - b1) + dL2 * (r2.z - b2));
-                    if (!clamped) {
-                        v[5] = da * g2d;
-                        const float dpower = da * r1.y * g2d;
-                        v[0] = dpower * (-(r0.z * dx + r0.w * dy));
-                        v[1] = dpower * (-(r1.x * dy + r0.w * dx));
-                        const float hp = -0.5f * dpower;
-                        v[2] = hp * dx * dx;
-                        v[3] = hp * dx * dy;
-                        v[4] = hp * dy * dy;
-                    }
-                    v[9] = 1.0f;
-                    b0 = alpha * r2.x + one_m_a * b0;
-                    b1 = alpha * r2.y + one_m_a * b1;
-                    b2 = alpha * r2.z + one_m_a * b2;
-                    T = t_before;
+            for (int k = 0; k < 24; ++k) v[k] = 0.0f;
+            auto commit = [&](float* vv, const float4& r0, const float4& r1, const float4& r2, float alpha, float g2d,
+                              bool clamped, float dx, float dy) {
+                const float one_m_a = 1.0f - alpha;
+                const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
+                const float w = t_before * alpha;
+                vv[6] = w * dL0;
+                vv[7] = w * dL1;
+                vv[8] = w * dL2;
+                const float da = t_before * (dL0 * (r2.x - b0) + dL1 * (r2.y - b1) + dL2 * (r2.z - b2));
+                if (!clamped) {
+                    vv[5] = da * g2d;
+                    const float dpower = da * r1.y * g2d;
+                    vv[0] = dpower * (-(r0.z * dx + r0.w * dy));
+                    vv[1] = dpower * (-(r1.x * dy + r0.w * dx));
+                    const float hp = -0.5f * dpower;
+                    vv[2] = hp * dx * dx;
+                    vv[3] = hp * dx * dy;
+                    vv[4] = hp * dy * dy;
                 }
-            }
-            if (__any_sync(0xffffffffu, committed)) {
+                vv[9] = 1.0f;
+                b0 = alpha * r2.x + one_m_a * b0;
+                b1 = alpha * r2.y + one_m_a * b1;
+                b2 = alpha * r2.z + one_m_a * b2;
+                T = t_before;
+            };
+            if (ga) commit(v, r0a, r1a, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
+            if (gb) commit(v + 12, r0b, r1b, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+            const bool any_a = __any_sync(0xffffffffu, ga), any_b = __any_sync(0xffffffffu, gb);
+            if (any_a || any_b) {
                 float r[3];
-                warp_reduce12(v, lane, r);
-                if ((lane & 7) == 0) {
-                    const uint32_t gid = lds_u32(a_gid + 4u * j);
-                    red_add_v4(grad2d + 4 * (size_t)gid + (lane >> 3), r[0], r[1], r[2], 0.0f);
+                warp_reduce24(v, lane, r);
+                const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
+                const bool mine = (lane & 3) == 0 && (grp < 4 ? any_a : any_b);
+                if (mine) {
+                    const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
+                    red_add_v4(grad2d + 4 * (size_t)gid + (grp & 3), r[0], r[1], r[2], 0.0f);
                 }
             }
         }

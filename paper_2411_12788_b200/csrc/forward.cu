@@ -418,29 +418,60 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
             const int cnt = stage_batch([&](int t) { return (int)(base + t); }, (int)min((uint32_t)nthreads, end - base),
                                         pair_gauss, rec, bx0, bx1, by0, by1, sm);
             if (!REPORT) {
-                for (int j = 0; j < cnt && !done; ++j) {
-                    float alpha, g2d, dx, dy;
+                // Two staged entries per iteration: independent branch-free gates, then the
+                // per-pixel recursion commits them in list order.
+                for (int j = 0; j < cnt && !done; j += 2) {
+                    const bool has_b = j + 1 < cnt;
+                    const uint32_t jb = has_b ? (uint32_t)(j + 1) : (uint32_t)j;
+                    const float4 r1a = lds_f4(a_r1 + 16u * j);
+                    const float4 r1b = lds_f4(a_r1 + 16u * jb);
+                    const uint32_t ma = __float_as_uint(r1a.z), mb = __float_as_uint(r1b.z);
+                    const bool wa = (ma & wrows) && (ma & wcols);  // warp-uniform: rect meets the patch
+                    const bool wb = has_b && (mb & wrows) && (mb & wcols);
+                    if (!wa && !wb) continue;
+                    const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
+                    float alpha_a, alpha_b, g2d, dx, dy;
                     bool clamped;
-                    const float4 r1 = lds_f4(a_r1 + 16u * j);
-                    if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
-                    const float4 r0 = lds_f4(a_r0 + 16u * j);
-                    if (!gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) continue;
-                    const float next = T * (1.0f - alpha);
-                    if (THR && next < tmin) {
-                        done = true;
-                        break;
+                    const bool ga = gate_sample_nb<THR>(r0a, r1a, mybits, x, y, amax_c, cmin, alpha_a, g2d, clamped, dx,
+                                                        dy) && wa;
+                    const bool gb = gate_sample_nb<THR>(r0b, r1b, mybits, x, y, amax_c, cmin, alpha_b, g2d, clamped, dx,
+                                                        dy) && wb;
+                    if (ga) {
+                        const float next = T * (1.0f - alpha_a);
+                        if (THR && next < tmin) {
+                            done = true;
+                            break;
+                        }
+                        const float w = T * alpha_a;
+                        const float4 r2 = lds_f4(a_r2 + 16u * j);
+                        acc0 = acc0 + w * r2.x;
+                        acc1 = acc1 + w * r2.y;
+                        acc2 = acc2 + w * r2.z;
+                        if (w > wmax) {
+                            wmax = w;
+                            amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
+                        }
+                        last = (int32_t)lds_u32(a_idx + 4u * j);
+                        T = next;
                     }
-                    const float w = T * alpha;
-                    const float4 r2 = lds_f4(a_r2 + 16u * j);
-                    acc0 = acc0 + w * r2.x;
-                    acc1 = acc1 + w * r2.y;
-                    acc2 = acc2 + w * r2.z;
-                    if (w > wmax) {
-                        wmax = w;
-                        amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
+                    if (gb) {
+                        const float next = T * (1.0f - alpha_b);
+                        if (THR && next < tmin) {
+                            done = true;
+                            break;
+                        }
+                        const float w = T * alpha_b;
+                        const float4 r2 = lds_f4(a_r2 + 16u * jb);
+                        acc0 = acc0 + w * r2.x;
+                        acc1 = acc1 + w * r2.y;
+                        acc2 = acc2 + w * r2.z;
+                        if (w > wmax) {
+                            wmax = w;
+                            amax_gid = (int32_t)lds_u32(a_gid + 4u * jb);
+                        }
+                        last = (int32_t)lds_u32(a_idx + 4u * jb);
+                        T = next;
                     }
-                    last = (int32_t)lds_u32(a_idx + 4u * j);
-                    T = next;
                 }
             } else {
                 const int lane = tid & 31;
