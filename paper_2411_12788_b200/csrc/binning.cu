@@ -158,31 +158,27 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
     }
 }
 
-// st_ranges[st] = [scanned[st * nchunks], scanned[(st + 1) * nchunks])
-__global__ void st_ranges_from_chunks_kernel(const uint32_t* __restrict__ scanned, int n_st, int nchunks,
-                                             uint32_t* __restrict__ ranges) {
-    const int st = blockIdx.x * blockDim.x + threadIdx.x;
-    if (st >= n_st) return;
-    ranges[2 * st] = scanned[(size_t)st * nchunks];
-    ranges[2 * st + 1] = scanned[(size_t)(st + 1) * nchunks];
-}
 
 // Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
 // total).  One CTA of kBinThreads threads.
-template <typename F>
+// Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
+// total).  One CTA of T threads.
+template <int T, typename F>
 __device__ void cta_scan(int n, F val, uint32_t* __restrict__ out, uint32_t* s_warp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t carry = 0;
-    for (int base = 0; base < n; base += kBinThreads) {
+    for (int base = 0; base < n; base += T) {
         const int i = base + tid;
         const uint32_t v = i < n ? val(i) : 0u;
         const uint32_t inc = warp_incl_scan(v, lane);
         if (lane == 31) s_warp[warp] = inc;
         __syncthreads();
         uint32_t off = 0, tot = 0;
-        for (int w = 0; w < kBinThreads / 32; ++w) {
-            off += w < warp ? s_warp[w] : 0u;
-            tot += s_warp[w];
+#pragma unroll 8
+        for (int w = 0; w < T / 32; ++w) {
+            const uint32_t c = s_warp[w];
+            off += w < warp ? c : 0u;
+            tot += c;
         }
         if (i < n) out[i] = carry + off + inc - v;
         carry += tot;
@@ -191,24 +187,49 @@ __device__ void cta_scan(int n, F val, uint32_t* __restrict__ out, uint32_t* s_w
     if (tid == 0) out[n] = carry;
 }
 
-// seg_start[st] = first segment id of supertile st (exclusive scan of ceil(len / kSeg));
+constexpr int kSetupThreads = 1024;
+constexpr int kSetupSmemSt = 16384;  // supertiles whose segment counts fit shared memory
+
+// One CTA: (chunked path) supertile ranges from the scanned (supertile, chunk) counts; segment
+// counts per supertile; seg_start = their exclusive scan; seg_st[s] = supertile of segment s;
 // tile_base[t] = first slot of tile t in the (tile, segment) count array.
-__global__ void __launch_bounds__(kBinThreads) seg_setup_kernel(const uint32_t* __restrict__ st_ranges, int n_st,
-                                                               int tiles_x, int tiles_y, int st_x,
-                                                               uint32_t* __restrict__ seg_start,
-                                                               uint32_t* __restrict__ tile_base) {
-    __shared__ uint32_t s_warp[kBinThreads / 32];
+__global__ void __launch_bounds__(kSetupThreads) seg_setup_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
+                                                                 uint32_t* __restrict__ st_ranges, int n_st,
+                                                                 int tiles_x, int tiles_y, int st_x,
+                                                                 uint32_t* __restrict__ seg_start,
+                                                                 uint32_t* __restrict__ seg_st,
+                                                                 uint32_t* __restrict__ tile_base) {
+    extern __shared__ uint32_t s_nseg[];  // [n_st] when n_st <= kSetupSmemSt
+    __shared__ uint32_t s_warp[kSetupThreads / 32];
+    const bool in_smem = n_st <= kSetupSmemSt;
+    for (int st = threadIdx.x; st < n_st; st += kSetupThreads) {
+        uint32_t lo, hi;
+        if (st_cnt) {
+            lo = st_cnt[(size_t)st * nchunks];
+            hi = st_cnt[(size_t)(st + 1) * nchunks];
+            st_ranges[2 * st] = lo;
+            st_ranges[2 * st + 1] = hi;
+        } else {
+            lo = st_ranges[2 * st];
+            hi = st_ranges[2 * st + 1];
+        }
+        if (in_smem) s_nseg[st] = (hi - lo + kSeg - 1) / kSeg;
+    }
+    __syncthreads();
     auto nseg = [&](int st) {
-        const uint32_t len = st_ranges[2 * st + 1] - st_ranges[2 * st];
-        return (len + kSeg - 1) / kSeg;
+        if (in_smem) return s_nseg[st];
+        return (st_ranges[2 * st + 1] - st_ranges[2 * st] + kSeg - 1) / kSeg;
     };
-    cta_scan(n_st, nseg, seg_start, s_warp);
-    cta_scan(tiles_x * tiles_y,
-             [&](int t) {
-                 const int tx = t % tiles_x, ty = t / tiles_x;
-                 return nseg((ty / kST) * st_x + tx / kST);
-             },
-             tile_base, s_warp);
+    cta_scan<kSetupThreads>(n_st, nseg, seg_start, s_warp);
+    __syncthreads();
+    for (int st = threadIdx.x; st < n_st; st += kSetupThreads)
+        for (uint32_t q = seg_start[st]; q < seg_start[st + 1]; ++q) seg_st[q] = (uint32_t)st;
+    cta_scan<kSetupThreads>(tiles_x * tiles_y,
+                            [&](int t) {
+                                const int tx = t % tiles_x, ty = t / tiles_x;
+                                return nseg((ty / kST) * st_x + tx / kST);
+                            },
+                            tile_base, s_warp);
 }
 
 // Count (EMIT = false) or emit (EMIT = true) pass over one segment of one supertile list.  The
@@ -229,13 +250,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
     __shared__ uint32_t s_out[EMIT ? kSTT * kBinThreads : 1];
     const int b = blockIdx.x;
     if (b >= (int)seg_start[n_st]) return;
-    int lo_st = 0, hi_st = n_st;  // largest st with seg_start[st] <= b
-    while (hi_st - lo_st > 1) {
-        const int mid = (lo_st + hi_st) >> 1;
-        if (seg_start[mid] <= (uint32_t)b) lo_st = mid;
-        else hi_st = mid;
-    }
-    const int st = lo_st;
+    const int st = (int)seg_start[n_st + 1 + b];  // seg_st (seg_setup)
     const int seg = b - (int)seg_start[st];
     const uint32_t st_end = st_ranges[2 * st + 1];
     const uint32_t lo = st_ranges[2 * st] + (uint32_t)seg * kSeg;
@@ -287,27 +302,16 @@ __global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
                 for (int f = 0; f < kSTT; ++f)
                     if ((cover >> f) & 1u) s_out[f * kBinThreads + s_wc[warp][f] + rank[f]] = gid;
             }
-            if (tid == 0) {  // exclusive prefix of the chunk totals over tiles (flat run layout)
-                uint32_t acc = 0;
-                for (int f = 0; f < kSTT; ++f) {
-                    const uint32_t t = s_tot[f];
-                    s_tot[f] = acc;
-                    acc += t;
-                }
-                s_tot[kSTT] = acc;
-            }
             __syncthreads();
-            const uint32_t total = s_tot[kSTT];
-            for (uint32_t q = tid; q < total; q += kBinThreads) {
-                int f = 0;  // tile of flat index q: last f with s_tot[f] <= q
+            // tile f's entries of this chunk are consecutive in its list: warp w copies tiles w, w + 8
 #pragma unroll
-                for (int step = kSTT / 2; step > 0; step >>= 1)
-                    if (f + step < kSTT && s_tot[f + step] <= q) f += step;
-                const uint32_t i = q - s_tot[f];
-                pair_gauss[s_base[f] + s_run[f] + i] = s_out[f * kBinThreads + i];
+            for (int f = warp; f < kSTT; f += kWarpsB) {
+                const uint32_t tot = s_tot[f];
+                uint32_t* dst = pair_gauss + s_base[f] + s_run[f];
+                for (uint32_t i = lane; i < tot; i += 32) dst[i] = s_out[f * kBinThreads + i];
             }
             __syncthreads();
-            if (tid < kSTT) s_run[tid] += s_tot[tid + 1] - s_tot[tid];
+            if (tid < kSTT) s_run[tid] += s_tot[tid];
         } else {
             if (tid < kSTT) s_run[tid] += s_tot[tid];
         }
@@ -383,12 +387,6 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
                                                                     n_st, nchunks, a.st_cnt, a.st_gauss[0]);
             lc.count++;
         }
-        {
-            LaunchScope s(lc, "st_ranges");
-            st_ranges_from_chunks_kernel<<<blocks_for(n_st, 256), 256, 0, lc.stream>>>(a.st_cnt, n_st, nchunks,
-                                                                                      a.st_ranges);
-            lc.count++;
-        }
         gauss = a.st_gauss[0];
     } else {
         if (a.n_surv > 0) {
@@ -412,8 +410,13 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     }
     {
         LaunchScope s(lc, "seg_setup");
-        seg_setup_kernel<<<1, kBinThreads, 0, lc.stream>>>(a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, a.seg_start,
-                                                          a.tile_base);
+        const bool chunked = st_chunked(n_st);
+        const size_t smem = n_st <= kSetupSmemSt ? (size_t)n_st * 4 : 0;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(seg_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        seg_setup_kernel<<<1, kSetupThreads, smem, lc.stream>>>(chunked ? a.st_cnt : nullptr, st_chunks(a.n_surv),
+                                                                a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x,
+                                                                a.seg_start, a.seg_start + n_st + 1, a.tile_base);
         lc.count++;
     }
     const size_t segs = bin_segment_upper(a.st_pairs, n_st);

@@ -322,7 +322,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         if (chunked) CK(ctx->st_cnt.ensure(st_words * 4), "alloc st counts");
         CK(ctx->pair_gauss[0].ensure(n_pairs * 4 + 4), "alloc pairs");
         CK(ctx->st_ranges.ensure((size_t)n_st * 8), "alloc st ranges");
-        CK(ctx->seg_start.ensure(((size_t)n_st + 1) * 4), "alloc seg");
+        CK(ctx->seg_start.ensure(((size_t)n_st + 1 + bin_segment_upper(st_pairs, n_st)) * 4), "alloc seg");
         CK(ctx->tile_base.ensure(((size_t)n_tiles + 1) * 4), "alloc tile base");
         const size_t n_slots = bin_segment_upper(st_pairs, n_st) * 16 + 1;
         CK(ctx->slots.ensure(n_slots * 4), "alloc slots");

@@ -91,7 +91,7 @@ struct BinningArgs {
     uint32_t* st_gauss[2];  // [0]: supertile lists (chunked path); both: sort ping-pong (fallback)
     uint32_t* st_cnt;       // [st_chunk_words] chunked path: (supertile, chunk) counts / offsets
     uint32_t* st_ranges;   // [2 * n_st]
-    uint32_t* seg_start;   // [n_st + 1]
+    uint32_t* seg_start;   // [n_st + 1] segment starts, then [bin_segment_upper] supertile of each segment
     uint32_t* tile_base;   // [n_tiles + 1]
     uint32_t* slots;       // [bin_segment_upper * 16 + 1]
     uint32_t* ranges;      // [2 * n_tiles] out
