@@ -79,79 +79,120 @@ def _ref_lib():
     return lib, kind
 
 
-def cpu_views_per_s(n_gaussians, threads, rounds=1):
-    """Time the reference's own render -> l1_loss -> render_backward -> OptimState::step on
-    `threads` host threads, each training one config-1 ring view per round."""
-    from paper_2411_12788_b200 import scenes
-    from paper_2411_12788_b200.capi import AdamConfig, Gaussians, RasterConfig
-    lib, kind = _ref_lib()
-    if lib is None:
-        return None
-    s = scenes.make_gaussians(n_gaussians, seed=0)
-    arrs = [np.ascontiguousarray(a, np.float32) for a in (s.centers, s.log_scales, s.rotations, s.opacity_logits, s.sh)]
-    fp = C.POINTER(C.c_float)
-    g = Gaussians(*[a.ctypes.data_as(fp) for a in arrs], s.n, 3)
-    adam = AdamConfig()
-    cfg = RasterConfig()
-    cams = [scenes.ring_camera(k, RING) for k in range(threads)]
-    # targets: a cheap deterministic stand-in image per view (CPU time of the target render is
-    # not part of the step); value range matches a render.
-    rng = np.random.default_rng(0)
-    tgt = [np.ascontiguousarray(rng.uniform(0, 1, size=(822, 1237, 3)).astype(np.float32)) for _ in range(threads)]
-    handles = [lib.ref_scene_create(C.byref(g), C.byref(adam)) for _ in range(threads)]
-    if not all(handles):
-        return None
-    errors = []
+class CpuReference:
+    """The reference's own render -> l1_loss -> render_backward -> OptimState::step (means) on
+    `threads` host threads (oracle/_ref, compiled in place from the reference's sources), each
+    training one config-1 ring view per round on its own copy of the scene."""
 
-    def work(i):
-        loss = C.c_float()
-        for _ in range(rounds):
-            rc = lib.ref_train_view(handles[i], C.byref(cams[i]), C.byref(cfg), tgt[i].ctypes.data_as(fp), C.byref(loss))
+    def __init__(self, n_gaussians, threads):
+        from paper_2411_12788_b200 import scenes
+        from paper_2411_12788_b200.capi import AdamConfig, Gaussians, RasterConfig
+        self.lib, self.kind = _ref_lib()
+        if self.lib is None:
+            raise RuntimeError("oracle/_ref/libsplat_ref_libm.so not built")
+        s = scenes.make_gaussians(n_gaussians, seed=0)
+        self.arrs = [np.ascontiguousarray(a, np.float32) for a in (s.centers, s.log_scales, s.rotations,
+                                                                   s.opacity_logits, s.sh)]
+        fp = C.POINTER(C.c_float)
+        g = Gaussians(*[a.ctypes.data_as(fp) for a in self.arrs], s.n, 3)
+        adam = AdamConfig()
+        self.cfg = RasterConfig()
+        self.threads = threads
+        self.cams = [scenes.ring_camera(k, RING) for k in range(threads)]
+        # targets: a cheap deterministic stand-in image per view (the target render is not part of
+        # the step); value range matches a render.
+        rng = np.random.default_rng(0)
+        self.tgt = [np.ascontiguousarray(rng.uniform(0, 1, size=(822, 1237, 3)).astype(np.float32))
+                    for _ in range(threads)]
+        self.handles = [self.lib.ref_scene_create(C.byref(g), C.byref(adam)) for _ in range(threads)]
+        if not all(self.handles):
+            self.close()
+            raise RuntimeError("reference scene allocation failed")
+
+    def round(self):
+        """One view per thread, all threads in parallel; returns the wall seconds."""
+        fp = C.POINTER(C.c_float)
+        errors = []
+
+        def work(i):
+            loss = C.c_float()
+            rc = self.lib.ref_train_view(self.handles[i], C.byref(self.cams[i]), C.byref(self.cfg),
+                                         self.tgt[i].ctypes.data_as(fp), C.byref(loss))
             if rc:
                 errors.append(rc)
 
-    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    t0 = time.perf_counter()
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    wall = time.perf_counter() - t0
-    for hnd in handles:
-        lib.ref_scene_destroy(hnd)
-    if errors:
-        raise RuntimeError(f"reference train_view failed: {errors[:3]}")
-    return {"value": threads * rounds / wall, "unit": UNIT, "cores": threads, "kind": kind,
+        th = [threading.Thread(target=work, args=(i,)) for i in range(self.threads)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        wall = time.perf_counter() - t0
+        if errors:
+            raise RuntimeError(f"reference train_view failed: {errors[:3]}")
+        return wall
+
+    def close(self):
+        for hnd in self.handles:
+            if hnd:
+                self.lib.ref_scene_destroy(hnd)
+        self.handles = []
+
+
+def cpu_threads_default(args, cap):
+    return args.cpu_threads or max(1, min(os.cpu_count() or 1, cap))
+
+
+def cpu_views_per_s(n_gaussians, threads, rounds=1):
+    """Bounded CPU-baseline sample: `rounds` rounds of one view per thread."""
+    ref = CpuReference(n_gaussians, threads)
+    try:
+        wall = sum(ref.round() for _ in range(rounds))
+    finally:
+        ref.close()
+    return {"value": threads * rounds / wall, "unit": UNIT, "cores": threads, "kind": ref.kind,
             "sample": f"{threads} threads x {rounds} config-1 ring view(s) each through the reference's own "
                       f"render<float> -> l1_loss -> render_backward<float> -> OptimState::step (means), "
                       f"{wall:.1f} s wall", "seconds": wall}
 
 
+REF_BUDGET_S = 150.0  # whole reference arm: warm-up + timed rounds
+
+
 def run_reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref) on the host cores, same
+    metric/config as our arm.  Each step is one round of one config-1 view per host thread (a
+    bounded sample of the workload); the number of timed steps is capped so the whole arm ends
+    within REF_BUDGET_S, and the line reports the steps actually timed."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    threads = args.cpu_threads or os.cpu_count() or 1
+    threads = cpu_threads_default(args, 64)
     lib, _ = _ref_lib()
     if lib is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsplat_ref_libm.so not built"}))
         return
-    for _ in range(args.warmup):
-        cpu_views_per_s(args.gaussians, threads, 1)
-    t_total, views = 0.0, 0
-    for _ in range(args.steps):
-        r = cpu_views_per_s(args.gaussians, threads, 1)
-        t_total += r["seconds"]
-        views += threads
+    t_start = time.perf_counter()
+    ref = CpuReference(args.gaussians, threads)
+    try:
+        first = ref.round() if args.warmup > 0 else None  # one untimed warm-up round bounds the rest
+        per = first if first else 6.0
+        steps = max(1, min(args.steps, int((REF_BUDGET_S - (time.perf_counter() - t_start)) / per)))
+        t_total = sum(ref.round() for _ in range(steps))
+    finally:
+        ref.close()
+    views = threads * steps
     value = views / t_total
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": 1 if args.warmup > 0 else 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": 1000 * t_total / steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE cfg1 shapes)",
             "config": workload_config(args, world), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{threads} threads x 1 config-1 view per step (reference's own C++ "
-                                       f"compiled in place, glibc expf)"},
+                             "sample": f"{threads} threads x 1 config-1 view per step, {steps} timed step(s) "
+                                       f"(capped to a {REF_BUDGET_S:.0f} s arm); the reference's own C++ "
+                                       f"compiled in place, glibc expf"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -392,7 +433,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = args.cpu_threads or min(os.cpu_count() or 1, 16)
+        threads = cpu_threads_default(args, 16)
         try:
             cpu = cpu_views_per_s(args.gaussians, threads, 1)
             if cpu:

@@ -102,6 +102,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
                                                             float* __restrict__ loss_partials,
                                                             float4* __restrict__ grad2d) {
     __shared__ StageSmem<BW * BH> sm;
+    __shared__ StageRaw<BW * BH> raw;
     __shared__ float s_red[BW * BH / 32];
     __shared__ int s_maxlast[BW * BH / 32];
     const int nthreads = blockDim.x;
@@ -169,9 +170,15 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
     float T = inside ? t_final[pix] : 1.0f;
     float b0 = bg0, b1 = bg1, b2 = bg2;
 
-    for (int hi = block_last + 1; hi > (int)start; hi -= nthreads) {
-        const int count = min(nthreads, hi - (int)start);
-        const int cnt = stage_batch([&](int t) { return hi - 1 - t; }, count, pair_gauss, rec, bx0, bx1, by0, by1, sm);
+    auto pos = [&](int b, int t) -> int {
+        const int i = block_last - b * nthreads - t;
+        return i >= (int)start ? i : -1;
+    };
+    StagePipe<BW * BH, decltype(pos)> pipe(pos, pair_gauss, rec, &raw);
+    pipe.start();
+    const int nb = (block_last + 1 - (int)start + nthreads - 1) / nthreads;
+    for (int b = 0; b < nb; ++b) {
+        const int cnt = pipe.stage(b, true, bx0, bx1, by0, by1, sm);
         // Two staged entries per iteration: their gates are independent instruction streams (the
         // branch-free gate), the per-pixel recursion then commits them in list order (j first: the
         // batch is staged back to front), and one 24-value transpose reduction serves both.
@@ -238,8 +245,9 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
                 }
             }
         }
-        __syncthreads();  // the next batch overwrites the staging area
+        // the next stage() starts with a barrier before it overwrites the staging area
     }
+    pipe.finish();
 }
 
 template <bool THR, int BW, int BH>

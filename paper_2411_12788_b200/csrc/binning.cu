@@ -12,13 +12,15 @@
 //      the chunk writing each Gaussian id at offset + (rank among the chunk's earlier entries of
 //      that supertile), ranks from __match_any_sync over the flattened (Gaussian, supertile)
 //      entries.  (Fallback for > kStMaxSmem supertiles: emit pairs + stable radix sort.)
-//   3. split every supertile list into segments of kSeg entries; a count pass gives, per
-//      (tile, segment), how many entries of the segment cover the tile; an exclusive scan of those
-//      counts laid out tile-major / segment-minor gives every (tile, segment) its output offset;
-//   4. an emit pass re-walks each segment in order and writes each Gaussian id into the lists of
-//      the tiles it covers at offset + (rank among the segment's earlier entries covering that
-//      tile), the rank coming from one warp ballot per tile of the supertile.
-// Stability at every step makes each list exactly the reference's, and only P x 4 B are written.
+//   3. per-tile lists from the supertile lists: every supertile list entry carries its 16-bit
+//      tile cover (written by step 2); the lists are cut into fixed-size pieces, a count pass
+//      gives per (piece, tile) counts, and an emit pass ranks each entry per tile by warp ballots
+//      + a scan over the piece's warps and writes contiguous runs.  No global scan: every tile
+//      list of supertile s lives in a fixed-capacity slot (a tile's list is a sub-list of its
+//      supertile's list, so L_s entries suffice): tile f of s starts at 16 lo_s + f L_s, and
+//      ranges[t] = [start, start + count).
+// Stability at every step makes each list exactly the reference's, and only P x 4 B are written
+// (into a 16 Ps-entry capacity; the debug getter compacts the lists to CSR for the bit-exact checks).
 #include <cstdint>
 
 #include "common.cuh"
@@ -30,8 +32,7 @@ namespace {
 
 constexpr int kST = 4;              // supertile side in tiles
 constexpr int kSTT = kST * kST;     // tiles per supertile
-constexpr int kSeg = 1024;          // entries per segment of a supertile list
-constexpr int kBinThreads = 256;
+constexpr int kL2Threads = 512;     // level-2 CTA: one per piece of a supertile list
 constexpr int kStChunk = 128;       // depth-ordered survivors per chunk of the supertile pass
 constexpr int kStMaxSmem = 6144;    // supertiles the chunked pass keeps in shared memory
 
@@ -46,6 +47,32 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r, int ts) {
     t.ty0 = (int)(r.y & 0xffffu) / ts;
     t.ty1 = ((int)(r.y >> 16) - 1) / ts;
     return t;
+}
+
+// Same, for a power-of-two tile size (shift; rect bounds are >= 0 and x1 > x0 >= 0 on survivors).
+__device__ __forceinline__ TileRect tile_rect_shift(uint2 r, int sh) {
+    TileRect t;
+    t.tx0 = (int)(r.x & 0xffffu) >> sh;
+    t.tx1 = ((int)(r.x >> 16) - 1) >> sh;
+    t.ty0 = (int)(r.y & 0xffffu) >> sh;
+    t.ty1 = ((int)(r.y >> 16) - 1) >> sh;
+    return t;
+}
+
+__device__ __forceinline__ TileRect tile_rect_any(uint2 r, int ts, int sh) {
+    return sh >= 0 ? tile_rect_shift(r, sh) : tile_rect(r, ts);
+}
+
+// Tiles of supertile (sx, sy) that the inclusive tile rect covers, as 16 bits (bit 4 ly + lx).
+__device__ __forceinline__ uint32_t cover16(int tx0, int tx1, int ty0, int ty1, int sx, int sy) {
+    const int lx0 = max(tx0 - sx * kST, 0), lx1 = min(tx1 - sx * kST, kST - 1);
+    const int ly0 = max(ty0 - sy * kST, 0), ly1 = min(ty1 - sy * kST, kST - 1);
+    if (lx0 > lx1 || ly0 > ly1) return 0u;
+    const uint32_t row = ((2u << lx1) - 1u) & ~((1u << lx0) - 1u);
+    const uint32_t rows = ((2u << ly1) - 1u) & ~((1u << ly0) - 1u);
+    // bit ly of rows -> nibble ly: multiplying the 4-bit row by sum 16^ly places one copy per row
+    const uint32_t spread = (rows & 1u) | ((rows & 2u) << 3) | ((rows & 4u) << 6) | ((rows & 8u) << 9);
+    return row * spread;
 }
 
 // (supertile, Gaussian) pairs in depth order: one thread per survivor.
@@ -85,8 +112,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 template <bool EMIT>
 __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict__ order,
                                                       const uint2* __restrict__ rect_ref, int n_surv, int ts,
-                                                      int st_x, int n_st, int nchunks, uint32_t* __restrict__ cnt,
-                                                      uint32_t* __restrict__ st_gauss) {
+                                                      int ts_shift, int st_x, int n_st, int nchunks,
+                                                      uint32_t* __restrict__ cnt, uint32_t* __restrict__ st_gauss,
+                                                      uint16_t* __restrict__ st_cover) {
     extern __shared__ uint32_t s_run[];  // [n_st]
     const int c = blockIdx.x, lane = threadIdx.x;
     for (int st = lane; st < n_st; st += 32) s_run[st] = EMIT ? cnt[(size_t)st * nchunks + c] : 0u;
@@ -113,12 +141,15 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
         const int r = g0 + k * 32 + lane;
         const uint32_t gid = gids[k];
         int sx0 = 0, sy0 = 0, w = 1, m = 0;
+        uint32_t ptx = 0, pty = 0;  // (tx0 | tx1 << 16), (ty0 | ty1 << 16)
         if (r < g1) {
-            const TileRect t = tile_rect(rects[k], ts);
+            const TileRect t = tile_rect_any(rects[k], ts, ts_shift);
             sx0 = t.tx0 / kST;
             sy0 = t.ty0 / kST;
             w = t.tx1 / kST - sx0 + 1;
             m = w * (t.ty1 / kST - sy0 + 1);
+            ptx = (uint32_t)t.tx0 | ((uint32_t)t.tx1 << 16);
+            pty = (uint32_t)t.ty0 | ((uint32_t)t.ty1 << 16);
         }
         if (!EMIT) {  // counts are order-free: shared-memory atomics per entry
             for (int q = 0; q < m; ++q) atomicAdd(&s_run[(sy0 + q / w) * st_x + sx0 + q % w], 1u);
@@ -137,9 +168,11 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
                 if (__shfl_sync(0xffffffffu, off, owner + step) <= e) owner += step;
             const int q = e - __shfl_sync(0xffffffffu, off, owner);
             const int ow = __shfl_sync(0xffffffffu, w, owner);
-            const int st = (__shfl_sync(0xffffffffu, sy0, owner) + q / ow) * st_x + __shfl_sync(0xffffffffu, sx0, owner) +
-                           q % ow;
+            const int esx = __shfl_sync(0xffffffffu, sx0, owner) + q % ow;
+            const int esy = __shfl_sync(0xffffffffu, sy0, owner) + q / ow;
+            const int st = esy * st_x + esx;
             const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
+            const uint32_t optx = __shfl_sync(0xffffffffu, ptx, owner), opty = __shfl_sync(0xffffffffu, pty, owner);
             const unsigned grp = __match_any_sync(0xffffffffu, valid ? st : -1);
             const int leader = __ffs(grp) - 1;
             uint32_t base = 0;
@@ -148,7 +181,12 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
                 s_run[st] = base + (uint32_t)__popc(grp);
             }
             base = __shfl_sync(0xffffffffu, base, leader);
-            if (valid) st_gauss[base + __popc(grp & lt)] = ogid;
+            if (valid) {
+                const uint32_t o = base + __popc(grp & lt);
+                st_gauss[o] = ogid;
+                st_cover[o] = (uint16_t)cover16((int)(optx & 0xffffu), (int)(optx >> 16), (int)(opty & 0xffffu),
+                                                (int)(opty >> 16), esx, esy);
+            }
             __syncwarp();
         }
     }
@@ -159,177 +197,175 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
 }
 
 
-// Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
-// total).  One CTA of kBinThreads threads.
-// Block-wide exclusive scan of `n` values produced by `val(i)`, written to out[0..n] (out[n] =
-// total).  One CTA of T threads.
-template <int T, typename F>
-__device__ void cta_scan(int n, F val, uint32_t* __restrict__ out, uint32_t* s_warp) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t carry = 0;
-    for (int base = 0; base < n; base += T) {
-        const int i = base + tid;
-        const uint32_t v = i < n ? val(i) : 0u;
-        const uint32_t inc = warp_incl_scan(v, lane);
-        if (lane == 31) s_warp[warp] = inc;
-        __syncthreads();
-        uint32_t off = 0, tot = 0;
-#pragma unroll 8
-        for (int w = 0; w < T / 32; ++w) {
-            const uint32_t c = s_warp[w];
-            off += w < warp ? c : 0u;
-            tot += c;
-        }
-        if (i < n) out[i] = carry + off + inc - v;
-        carry += tot;
-        __syncthreads();
-    }
-    if (tid == 0) out[n] = carry;
+// ---- level 2 -----------------------------------------------------------------------------------
+// Every supertile list is cut into pieces of kPiece entries.  Piece ids need no scan: supertile s
+// owns ids [g(s), g(s+1)) with g(s) = floor(lo_s / kPiece) + s (strictly increasing, and its
+// ceil(L_s / kPiece) pieces fit), so a tiny map kernel writes the id -> supertile table.  Each
+// list entry carries its 16-bit tile cover (written by the level-1 emit), so level 2 reads only
+// coalesced (id, cover) pairs:
+//   bin_count: per piece, entries covering each of the 16 tiles (ballots);
+//   bin_emit:  per piece, the tile offsets of its earlier pieces (<= a few dozen counts), the
+//              ranks of its entries per tile from ballots + a scan over (slice, warp) in shared
+//              memory, and one store instruction per (slice, warp, tile) writing a contiguous
+//              run of the tile's list.
+constexpr int kPiece = 2048;
+constexpr int kPieceK = kPiece / kL2Threads;  // entries per thread
+constexpr uint32_t kNoPiece = 0xffffffffu;
+
+// lo_s: start of supertile s's list (s in [0, n_st]) in the concatenated supertile lists.
+__device__ __forceinline__ uint32_t st_lo(const uint32_t* __restrict__ st_cnt, int nchunks,
+                                          const uint32_t* __restrict__ st_ranges, int n_st, int s) {
+    if (st_cnt) return st_cnt[(size_t)s * nchunks];
+    return s < n_st ? st_ranges[2 * s] : st_ranges[2 * n_st - 1];
 }
 
-constexpr int kSetupThreads = 1024;
-constexpr int kSetupSmemSt = 16384;  // supertiles whose segment counts fit shared memory
-
-// One CTA: (chunked path) supertile ranges from the scanned (supertile, chunk) counts; segment
-// counts per supertile; seg_start = their exclusive scan; seg_st[s] = supertile of segment s;
-// tile_base[t] = first slot of tile t in the (tile, segment) count array.
-__global__ void __launch_bounds__(kSetupThreads) seg_setup_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
-                                                                 uint32_t* __restrict__ st_ranges, int n_st,
-                                                                 int tiles_x, int tiles_y, int st_x,
-                                                                 uint32_t* __restrict__ seg_start,
-                                                                 uint32_t* __restrict__ seg_st,
-                                                                 uint32_t* __restrict__ tile_base) {
-    extern __shared__ uint32_t s_nseg[];  // [n_st] when n_st <= kSetupSmemSt
-    __shared__ uint32_t s_warp[kSetupThreads / 32];
-    const bool in_smem = n_st <= kSetupSmemSt;
-    for (int st = threadIdx.x; st < n_st; st += kSetupThreads) {
-        uint32_t lo, hi;
-        if (st_cnt) {
-            lo = st_cnt[(size_t)st * nchunks];
-            hi = st_cnt[(size_t)(st + 1) * nchunks];
-            st_ranges[2 * st] = lo;
-            st_ranges[2 * st + 1] = hi;
-        } else {
-            lo = st_ranges[2 * st];
-            hi = st_ranges[2 * st + 1];
+// One thread per supertile: piece_st[id] for its id range; empty ranges for empty supertiles.
+__global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges,
+                               int n_st, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ piece_st,
+                               uint32_t* __restrict__ ranges) {
+    const int st = blockIdx.x * blockDim.x + threadIdx.x;
+    if (st >= n_st) return;
+    const uint32_t lo = st_lo(st_cnt, nchunks, st_ranges, n_st, st);
+    const uint32_t hi = st_lo(st_cnt, nchunks, st_ranges, n_st, st + 1);
+    const uint32_t g0 = lo / kPiece + (uint32_t)st, g1 = hi / kPiece + (uint32_t)st + 1u;
+    const uint32_t np = (hi - lo + kPiece - 1) / kPiece;
+    for (uint32_t id = g0; id < g1; ++id) piece_st[id] = id - g0 < np ? (uint32_t)st : kNoPiece;
+    if (hi == lo) {
+        const int tx_base = (st % st_x) * kST, ty_base = (st / st_x) * kST;
+        for (int f = 0; f < kSTT; ++f) {
+            const int tx = tx_base + (f % kST), ty = ty_base + (f / kST);
+            if (tx < tiles_x && ty < tiles_y) {
+                ranges[2 * (ty * tiles_x + tx)] = kSTT * lo;
+                ranges[2 * (ty * tiles_x + tx) + 1] = kSTT * lo;
+            }
         }
-        if (in_smem) s_nseg[st] = (hi - lo + kSeg - 1) / kSeg;
     }
-    __syncthreads();
-    auto nseg = [&](int st) {
-        if (in_smem) return s_nseg[st];
-        return (st_ranges[2 * st + 1] - st_ranges[2 * st] + kSeg - 1) / kSeg;
-    };
-    cta_scan<kSetupThreads>(n_st, nseg, seg_start, s_warp);
-    __syncthreads();
-    for (int st = threadIdx.x; st < n_st; st += kSetupThreads)
-        for (uint32_t q = seg_start[st]; q < seg_start[st + 1]; ++q) seg_st[q] = (uint32_t)st;
-    cta_scan<kSetupThreads>(tiles_x * tiles_y,
-                            [&](int t) {
-                                const int tx = t % tiles_x, ty = t / tiles_x;
-                                return nseg((ty / kST) * st_x + tx / kST);
-                            },
-                            tile_base, s_warp);
 }
 
-// Count (EMIT = false) or emit (EMIT = true) pass over one segment of one supertile list.  The
-// segment is walked in chunks of kBinThreads entries; per local tile f, a warp ballot gives each
-// entry its rank among the chunk's entries covering f.  Emitted ids are staged per tile in shared
-// memory and written out as contiguous runs (coalesced), since a tile's entries of one chunk are
-// consecutive in its list.
-template <bool EMIT>
-__global__ void __launch_bounds__(kBinThreads) bin_segments_kernel(
-    const uint32_t* __restrict__ st_ranges, const uint32_t* __restrict__ seg_start, int n_st,
-    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ st_gauss, const uint2* __restrict__ rect_ref,
-    int ts, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ slots, uint32_t* __restrict__ pair_gauss) {
-    constexpr int kWarpsB = kBinThreads / 32;
-    __shared__ uint32_t s_wc[kWarpsB][kSTT];   // per-warp counts, then exclusive prefixes over warps
-    __shared__ uint32_t s_tot[kSTT + 1];       // chunk totals per tile, then exclusive prefix over tiles
-    __shared__ uint32_t s_run[kSTT];
-    __shared__ uint32_t s_base[kSTT];
-    __shared__ uint32_t s_out[EMIT ? kSTT * kBinThreads : 1];
-    const int b = blockIdx.x;
-    if (b >= (int)seg_start[n_st]) return;
-    const int st = (int)seg_start[n_st + 1 + b];  // seg_st (seg_setup)
-    const int seg = b - (int)seg_start[st];
-    const uint32_t st_end = st_ranges[2 * st + 1];
-    const uint32_t lo = st_ranges[2 * st] + (uint32_t)seg * kSeg;
-    const uint32_t hi = min(lo + (uint32_t)kSeg, st_end);
-    const int tx_base = (st % st_x) * kST, ty_base = (st / st_x) * kST;
+struct PieceInfo {
+    int st;
+    uint32_t p, lo_s, hi_s, lo, hi;
+};
+
+__device__ __forceinline__ bool piece_info(uint32_t id, const uint32_t* __restrict__ piece_st,
+                                           const uint32_t* __restrict__ st_cnt, int nchunks,
+                                           const uint32_t* __restrict__ st_ranges, int n_st, PieceInfo& pi) {
+    const uint32_t st = piece_st[id];
+    if (st == kNoPiece) return false;
+    pi.st = (int)st;
+    pi.lo_s = st_lo(st_cnt, nchunks, st_ranges, n_st, pi.st);
+    pi.hi_s = st_lo(st_cnt, nchunks, st_ranges, n_st, pi.st + 1);
+    pi.p = id - (pi.lo_s / kPiece + st);
+    pi.lo = pi.lo_s + pi.p * kPiece;
+    pi.hi = min(pi.lo + (uint32_t)kPiece, pi.hi_s);
+    return true;
+}
+
+__global__ void __launch_bounds__(kL2Threads) bin_count_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
+                                                              const uint32_t* __restrict__ st_ranges, int n_st,
+                                                              const uint32_t* __restrict__ piece_st,
+                                                              const uint16_t* __restrict__ st_cover,
+                                                              uint32_t* __restrict__ piece_cnt) {
+    __shared__ uint32_t s_cnt[kSTT];
+    PieceInfo pi;
+    if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < kSTT) s_cnt[tid] = 0u;
+    uint32_t cv[kPieceK];
+#pragma unroll
+    for (int k = 0; k < kPieceK; ++k) {
+        const uint32_t e = pi.lo + k * kL2Threads + tid;
+        cv[k] = e < pi.hi ? (uint32_t)st_cover[e] : 0u;
+    }
+    uint32_t mine = 0;  // lane f: this warp's entries covering tile f
+#pragma unroll
+    for (int f = 0; f < kSTT; ++f) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < kPieceK; ++k) c += __popc(__ballot_sync(0xffffffffu, (cv[k] >> f) & 1u));
+        if (lane == f) mine = c;
+    }
+    __syncthreads();
+    if (lane < kSTT && mine) atomicAdd(&s_cnt[lane], mine);
+    __syncthreads();
+    if (tid < kSTT) piece_cnt[(size_t)blockIdx.x * kSTT + tid] = s_cnt[tid];
+}
+
+__global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
+    const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges, int n_st,
+    const uint32_t* __restrict__ piece_st, const uint32_t* __restrict__ piece_cnt,
+    const uint32_t* __restrict__ st_gauss, const uint16_t* __restrict__ st_cover, int tiles_x, int tiles_y, int st_x,
+    uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges) {
+    constexpr int kW = kL2Threads / 32;
+    __shared__ uint32_t s_c[kPieceK][kW][kSTT];    // (slice k, warp) entries covering tile f, then their list position
+    __shared__ uint32_t s_prefix[kSTT];
+    PieceInfo pi;
+    if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < kSTT) {
-        s_run[tid] = 0;
-        if (EMIT) {
-            const int tx = tx_base + (tid % kST), ty = ty_base + (tid / kST);
-            s_base[tid] = (tx < tiles_x && ty < tiles_y) ? slots[tile_base[ty * tiles_x + tx] + seg] : 0u;
+    const uint32_t cap = pi.hi_s - pi.lo_s;  // capacity of every tile list of this supertile
+    if (tid < kSTT) {  // counts of this supertile's earlier pieces
+        const uint32_t id0 = pi.lo_s / kPiece + (uint32_t)pi.st;
+        uint32_t pre = 0;
+        for (uint32_t q = 0; q < pi.p; ++q) pre += piece_cnt[(size_t)(id0 + q) * kSTT + tid];
+        s_prefix[tid] = pre;
+    }
+    uint32_t gid[kPieceK], cv[kPieceK];
+#pragma unroll
+    for (int k = 0; k < kPieceK; ++k) {
+        const uint32_t e = pi.lo + k * kL2Threads + tid;
+        const bool ok = e < pi.hi;
+        gid[k] = ok ? st_gauss[e] : 0u;
+        cv[k] = ok ? (uint32_t)st_cover[e] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kPieceK; ++k)
+#pragma unroll
+        for (int f = 0; f < kSTT; ++f) {
+            const unsigned m = __ballot_sync(0xffffffffu, (cv[k] >> f) & 1u);
+            if (lane == f) s_c[k][warp][f] = __popc(m);
+        }
+    __syncthreads();
+    {   // warp f: exclusive scan of tile f's counts over the 64 (slice, warp) positions in entry order
+        static_assert(kPieceK * kW == 64 && kW == kSTT, "scan layout assumes 16 warps x 4 slices");
+        const int f = warp;
+        uint32_t* col = &s_c[0][0][0];
+        const int q0 = 2 * lane, q1 = 2 * lane + 1;
+        const uint32_t v0 = col[q0 * kSTT + f], v1 = col[q1 * kSTT + f];
+        const uint32_t inc = warp_incl_scan(v0 + v1, lane);
+        const uint32_t list0 = (uint32_t)kSTT * pi.lo_s + (uint32_t)f * cap;
+        const uint32_t base = list0 + s_prefix[f];
+        col[q0 * kSTT + f] = base + inc - v0 - v1;
+        col[q1 * kSTT + f] = base + inc - v1;
+        if (lane == 31 && pi.hi == pi.hi_s) {  // last piece: the tile's range
+            const int tx = (pi.st % st_x) * kST + (f % kST), ty = (pi.st / st_x) * kST + (f / kST);
+            if (tx < tiles_x && ty < tiles_y) {
+                const int t = ty * tiles_x + tx;
+                ranges[2 * t] = list0;
+                ranges[2 * t + 1] = base + inc;
+            }
         }
     }
     __syncthreads();
     const unsigned lt = lanemask_lt();
-    for (uint32_t c = lo; c < hi; c += kBinThreads) {
-        const uint32_t e = c + tid;
-        uint32_t gid = 0, cover = 0;
-        if (e < hi) {
-            gid = st_gauss[e];
-            const TileRect t = tile_rect(rect_ref[gid], ts);
-            const int lx0 = max(t.tx0 - tx_base, 0), lx1 = min(t.tx1 - tx_base, kST - 1);
-            const int ly0 = max(t.ty0 - ty_base, 0), ly1 = min(t.ty1 - ty_base, kST - 1);
-            const uint32_t row = ((1u << (lx1 + 1)) - 1u) & ~((1u << lx0) - 1u);
-            for (int ly = ly0; ly <= ly1; ++ly) cover |= row << (ly * kST);
-        }
-        uint32_t rank[kSTT];
+#pragma unroll
+    for (int k = 0; k < kPieceK; ++k)
 #pragma unroll
         for (int f = 0; f < kSTT; ++f) {
-            const unsigned m = __ballot_sync(0xffffffffu, (cover >> f) & 1u);
-            rank[f] = __popc(m & lt);
-            if (lane == 0) s_wc[warp][f] = __popc(m);
+            const bool on = (cv[k] >> f) & 1u;
+            const unsigned m = __ballot_sync(0xffffffffu, on);
+            if (on) pair_gauss[s_c[k][warp][f] + __popc(m & lt)] = gid[k];
         }
-        __syncthreads();
-        if (tid < kSTT) {  // exclusive prefix over warps per tile; chunk total per tile
-            uint32_t run = 0;
-#pragma unroll
-            for (int w = 0; w < kWarpsB; ++w) {
-                const uint32_t cw = s_wc[w][tid];
-                s_wc[w][tid] = run;
-                run += cw;
-            }
-            s_tot[tid] = run;
-        }
-        __syncthreads();
-        if (EMIT) {
-            if (cover) {
-#pragma unroll
-                for (int f = 0; f < kSTT; ++f)
-                    if ((cover >> f) & 1u) s_out[f * kBinThreads + s_wc[warp][f] + rank[f]] = gid;
-            }
-            __syncthreads();
-            // tile f's entries of this chunk are consecutive in its list: warp w copies tiles w, w + 8
-#pragma unroll
-            for (int f = warp; f < kSTT; f += kWarpsB) {
-                const uint32_t tot = s_tot[f];
-                uint32_t* dst = pair_gauss + s_base[f] + s_run[f];
-                for (uint32_t i = lane; i < tot; i += 32) dst[i] = s_out[f * kBinThreads + i];
-            }
-            __syncthreads();
-            if (tid < kSTT) s_run[tid] += s_tot[tid];
-        } else {
-            if (tid < kSTT) s_run[tid] += s_tot[tid];
-        }
-        __syncthreads();
-    }
-    if (!EMIT && tid < kSTT) {
-        const int tx = tx_base + (tid % kST), ty = ty_base + (tid / kST);
-        if (tx < tiles_x && ty < tiles_y) slots[tile_base[ty * tiles_x + tx] + seg] = s_run[tid];
-    }
 }
 
-// ranges[t] = [scanned[tile_base[t]], scanned[tile_base[t + 1]])
-__global__ void ranges_from_slots_kernel(const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_base,
-                                         int n_tiles, uint32_t* __restrict__ ranges) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tiles) return;
-    ranges[2 * t] = scanned[tile_base[t]];
-    ranges[2 * t + 1] = scanned[tile_base[t + 1]];
+// Fallback path (supertile lists from the pair sort): covers from the rects.
+__global__ void st_cover_kernel(const uint32_t* __restrict__ st_key, const uint32_t* __restrict__ st_gauss,
+                                const uint2* __restrict__ rect_ref, uint32_t n, int ts, int ts_shift, int st_x,
+                                uint16_t* __restrict__ st_cover) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const TileRect t = tile_rect_any(rect_ref[st_gauss[i]], ts, ts_shift);
+    const int st = (int)st_key[i];
+    st_cover[i] = (uint16_t)cover16(t.tx0, t.tx1, t.ty0, t.ty1, st % st_x, st / st_x);
 }
 
 // supertile ranges over the st-sorted keys (lower bounds)
@@ -355,7 +391,8 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 }  // namespace
 
 int supertile_side() { return kST; }
-size_t bin_segment_upper(uint64_t st_pairs, int n_st) { return (size_t)(st_pairs / kSeg + n_st + 1); }
+size_t bin_l2_pieces(uint64_t st_pairs, int n_st) { return (size_t)(st_pairs / kPiece + n_st); }
+size_t bin_l2_words(uint64_t st_pairs, int n_st) { return bin_l2_pieces(st_pairs, n_st) * (1 + kSTT) + 1; }
 
 bool st_chunked(int n_st) { return n_st <= kStMaxSmem; }
 int st_chunks(int n_surv) { return n_surv > kStChunk ? (n_surv + kStChunk - 1) / kStChunk : 1; }
@@ -366,6 +403,12 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     const int n_tiles = a.tiles_x * a.tiles_y;
     const uint32_t* gauss;
     cudaError_t e;
+    const int ts = a.tile_size;
+    int ts_shift = -1;
+    if ((ts & (ts - 1)) == 0) {
+        ts_shift = 0;
+        while ((1 << ts_shift) < ts) ++ts_shift;
+    }
     if (st_chunked(n_st)) {
         const int nchunks = st_chunks(a.n_surv);
         const size_t smem = (size_t)n_st * 4;
@@ -375,16 +418,17 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
         }
         {
             LaunchScope s(lc, "st_count");
-            st_chunk_kernel<false><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, a.tile_size, a.st_x,
-                                                                     n_st, nchunks, a.st_cnt, nullptr);
+            st_chunk_kernel<false><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, ts, ts_shift,
+                                                                     a.st_x, n_st, nchunks, a.st_cnt, nullptr, nullptr);
             lc.count++;
         }
         e = exclusive_scan_u32(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.scan_tmp, nullptr);
         if (e != cudaSuccess) return e;
         {
             LaunchScope s(lc, "st_emit");
-            st_chunk_kernel<true><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, a.tile_size, a.st_x,
-                                                                    n_st, nchunks, a.st_cnt, a.st_gauss[0]);
+            st_chunk_kernel<true><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, ts, ts_shift,
+                                                                    a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
+                                                                    a.st_cover);
             lc.count++;
         }
         gauss = a.st_gauss[0];
@@ -407,44 +451,40 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
                                                                            n_st);
             lc.count++;
         }
+        if (a.st_pairs > 0) {
+            LaunchScope s(lc, "st_cover");
+            st_cover_kernel<<<blocks_for((int64_t)a.st_pairs, 256), 256, 0, lc.stream>>>(
+                keys, gauss, a.rect_ref, (uint32_t)a.st_pairs, ts, ts_shift, a.st_x, a.st_cover);
+            lc.count++;
+        }
     }
     {
-        LaunchScope s(lc, "seg_setup");
-        const bool chunked = st_chunked(n_st);
-        const size_t smem = n_st <= kSetupSmemSt ? (size_t)n_st * 4 : 0;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(seg_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        seg_setup_kernel<<<1, kSetupThreads, smem, lc.stream>>>(chunked ? a.st_cnt : nullptr, st_chunks(a.n_surv),
-                                                                a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x,
-                                                                a.seg_start, a.seg_start + n_st + 1, a.tile_base);
-        lc.count++;
+        const uint32_t* cnt = st_chunked(n_st) ? a.st_cnt : nullptr;
+        const int nch = st_chunks(a.n_surv);
+        const uint32_t np = (uint32_t)bin_l2_pieces(a.st_pairs, n_st);
+        uint32_t* piece_st = a.l2_tmp;
+        uint32_t* piece_cnt = a.l2_tmp + np;
+        {
+            LaunchScope s(lc, "bin_map");
+            bin_map_kernel<<<blocks_for(n_st, 128), 128, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, a.tiles_x,
+                                                                         a.tiles_y, a.st_x, piece_st, a.ranges);
+            lc.count++;
+        }
+        if (np > 0) {
+            {
+                LaunchScope s(lc, "bin_count");
+                bin_count_kernel<<<np, kL2Threads, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, piece_st, a.st_cover,
+                                                                   piece_cnt);
+                lc.count++;
+            }
+            LaunchScope s(lc, "bin_emit");
+            bin_emit_kernel<<<np, kL2Threads, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, piece_st, piece_cnt, gauss,
+                                                              a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss,
+                                                              a.ranges);
+            lc.count++;
+        }
     }
-    const size_t segs = bin_segment_upper(a.st_pairs, n_st);
-    const size_t n_slots = segs * kSTT + 1;
-    e = cudaMemsetAsync(a.slots, 0, n_slots * 4, lc.stream);
-    if (e != cudaSuccess) return e;
-    {
-        LaunchScope s(lc, "bin_count");
-        bin_segments_kernel<false><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
-            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rect_ref, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
-            a.slots, nullptr);
-        lc.count++;
-    }
-    e = exclusive_scan_u32(lc, a.slots, a.slots, n_slots, a.scan_tmp, nullptr);
-    if (e != cudaSuccess) return e;
-    {
-        LaunchScope s(lc, "tile_ranges");
-        ranges_from_slots_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(a.slots, a.tile_base, n_tiles,
-                                                                                  a.ranges);
-        lc.count++;
-    }
-    {
-        LaunchScope s(lc, "bin_emit");
-        bin_segments_kernel<true><<<(unsigned)segs, kBinThreads, 0, lc.stream>>>(
-            a.st_ranges, a.seg_start, n_st, a.tile_base, gauss, a.rect_ref, a.tile_size, a.tiles_x, a.tiles_y, a.st_x,
-            a.slots, a.pair_gauss);
-        lc.count++;
-    }
+    (void)n_tiles;
     return cudaGetLastError();
 }
 

@@ -7,6 +7,7 @@
 //   -> stable radix sort by tile id -> K5 tile ranges -> K6 blend (+importance, +depth).
 // The backward reuses the forward's sorted lists, records and per-pixel (T_final, last) state
 // (the reference recomputes project + bin_tiles, gradients.cpp:58-61; the result is identical).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -123,7 +124,7 @@ struct splat_ctx {
     // per-Gaussian
     DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
-    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_ranges, seg_start, tile_base, slots;
+    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_ranges, l2_tmp, st_cover;
     // misc
     DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
@@ -320,16 +321,15 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         }
         const size_t st_words = chunked ? st_chunk_words(n_surv, n_st) : 1;
         if (chunked) CK(ctx->st_cnt.ensure(st_words * 4), "alloc st counts");
-        CK(ctx->pair_gauss[0].ensure(n_pairs * 4 + 4), "alloc pairs");
+        if (tile_list_capacity(st_pairs) >= (size_t)UINT32_MAX)
+            return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "too many tile-Gaussian pairs for 32-bit list offsets");
+        CK(ctx->pair_gauss[0].ensure(tile_list_capacity(st_pairs) * 4 + 4), "alloc pairs");
         CK(ctx->st_ranges.ensure((size_t)n_st * 8), "alloc st ranges");
-        CK(ctx->seg_start.ensure(((size_t)n_st + 1 + bin_segment_upper(st_pairs, n_st)) * 4), "alloc seg");
-        CK(ctx->tile_base.ensure(((size_t)n_tiles + 1) * 4), "alloc tile base");
-        const size_t n_slots = bin_segment_upper(st_pairs, n_st) * 16 + 1;
-        CK(ctx->slots.ensure(n_slots * 4), "alloc slots");
+        CK(ctx->l2_tmp.ensure(bin_l2_words(st_pairs, n_st) * 4), "alloc binning scratch");
+        CK(ctx->st_cover.ensure(st_pairs * 2 + 4), "alloc st cover");
         const size_t hwords = chunked ? 0 : radix_hist_words(st_pairs, 8);
         if (!chunked) CK(ctx->hist.ensure(hwords * 4), "alloc hist");
-        size_t scan_n = hwords > n_slots ? hwords : n_slots;
-        scan_n = scan_n > st_words ? scan_n : st_words;
+        const size_t scan_n = hwords > st_words ? hwords : st_words;
         CK(ctx->scan_tmp.ensure((scan_temp_words(scan_n) + 64) * 4), "alloc scan");
         BinningArgs ba{};
         ba.order = order;
@@ -349,9 +349,8 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         }
         ba.st_cnt = ctx->st_cnt.as<uint32_t>();
         ba.st_ranges = ctx->st_ranges.as<uint32_t>();
-        ba.seg_start = ctx->seg_start.as<uint32_t>();
-        ba.tile_base = ctx->tile_base.as<uint32_t>();
-        ba.slots = ctx->slots.as<uint32_t>();
+        ba.l2_tmp = ctx->l2_tmp.as<uint32_t>();
+        ba.st_cover = ctx->st_cover.as<uint16_t>();
         ba.ranges = ctx->ranges.as<uint32_t>();
         ba.pair_gauss = ctx->pair_gauss[0].as<uint32_t>();
         ba.hist = ctx->hist.as<uint32_t>();
@@ -769,20 +768,30 @@ int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int3
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     const int k = st.pairs_in_alt ? 1 : 0;
     const int n_tiles = st.cp.tiles_x * st.cp.tiles_y;
-    if (key_tile && st.n_pairs) {  // the tile id of each list entry, from the CSR ranges
-        uint32_t* r = new uint32_t[2 * (size_t)n_tiles];
-        cudaError_t e = cudaMemcpy(r, ctx->ranges.p, 8 * (size_t)n_tiles, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) {
-            delete[] r;
-            return cuda_err(ctx, e, "copy ranges");
-        }
-        for (int t = 0; t < n_tiles; ++t)
-            for (uint32_t p = r[2 * t]; p < r[2 * t + 1] && p < st.n_pairs; ++p) key_tile[p] = t;
-        delete[] r;
+    // Device lists live in a capacity layout ([start, end) per tile); report them compacted to
+    // CSR in tile order, which is detail::bin_tiles' per-tile lists concatenated.
+    std::vector<uint32_t> r(2 * (size_t)n_tiles);
+    CK(cudaMemcpy(r.data(), ctx->ranges.p, 8 * (size_t)n_tiles, cudaMemcpyDeviceToHost), "copy ranges");
+    std::vector<uint32_t> lists;
+    if ((key_tile || gaussian) && st.n_pairs) {
+        uint32_t hi = 0;
+        for (int t = 0; t < n_tiles; ++t) hi = std::max(hi, r[2 * t + 1]);
+        lists.resize(hi);
+        if (hi) CK(cudaMemcpy(lists.data(), ctx->pair_gauss[k].p, 4 * (size_t)hi, cudaMemcpyDeviceToHost), "copy lists");
     }
-    if (gaussian && st.n_pairs) CK(cudaMemcpy(gaussian, ctx->pair_gauss[k].p, 4 * st.n_pairs, cudaMemcpyDeviceToHost), "copy");
-    if (ranges)
-        CK(cudaMemcpy(ranges, ctx->ranges.p, 8 * (size_t)st.cp.tiles_x * st.cp.tiles_y, cudaMemcpyDeviceToHost), "copy");
+    uint64_t p = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+        const uint32_t b = r[2 * t], e = r[2 * t + 1];
+        if (ranges) {
+            ranges[2 * t] = (int32_t)p;
+            ranges[2 * t + 1] = (int32_t)(p + (e - b));
+        }
+        for (uint32_t q = b; q < e && p < st.n_pairs; ++q, ++p) {
+            if (key_tile) key_tile[p] = t;
+            if (gaussian) gaussian[p] = (int32_t)lists[q];
+        }
+        if (p >= st.n_pairs) p = st.n_pairs;
+    }
     if (depth_order && st.n_surv) {
         // depth sort of N keys: 4 passes of 8 bits -> result back in buffer 0
         CK(cudaMemcpy(depth_order, ctx->vals[0].p, 4 * (size_t)st.n_surv, cudaMemcpyDeviceToHost), "copy");

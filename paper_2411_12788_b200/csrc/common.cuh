@@ -249,4 +249,109 @@ __device__ __forceinline__ int stage_batch(IdxFn idx_of, int count, const uint32
     return total;
 }
 
+
+// ---- pipelined staging ------------------------------------------------------------------------
+// stage_batch gathers each batch with two dependent round trips (list entry -> Gaussian id ->
+// 48-byte record) right before the batch is needed, so every batch starts with the whole CTA
+// stalled on L2.  StagePipe overlaps that latency with the previous batch's blending: while batch
+// b is blended, batch b+1's records are already copied into a raw shared buffer by cp.async
+// (their ids were loaded one batch earlier) and batch b+2's ids are in flight into registers.
+// stage() then only culls + compacts from shared memory.  Same staged content, same order.
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int CAP>
+struct StageRaw {
+    float4 r[CAP][3];  // one raw ProjRec per thread slot
+};
+
+// PosFn pos(b, t): list position of thread t's entry in batch b, or -1 when batch b has no entry t.
+template <int CAP, typename PosFn>
+struct StagePipe {
+    PosFn pos;
+    const uint32_t* __restrict__ pair_gauss;
+    const ProjRec* __restrict__ rec;
+    StageRaw<CAP>* raw;
+    int idx_f;       // entry whose record is in flight to raw (batch b)
+    uint32_t gid_f;
+    int idx_n;       // entry of batch b + 1, id loaded into gid_n
+    uint32_t gid_n;
+
+    __device__ __forceinline__ StagePipe(PosFn p, const uint32_t* pg, const ProjRec* rc, StageRaw<CAP>* rw)
+        : pos(p), pair_gauss(pg), rec(rc), raw(rw) {}
+
+    __device__ __forceinline__ void launch_copy() {
+        if (idx_f >= 0) {
+            const float4* src = reinterpret_cast<const float4*>(rec + gid_f);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&raw->r[threadIdx.x][0]);
+            cp_async16(dst, src);
+            cp_async16(dst + 16u, src + 1);
+            cp_async16(dst + 32u, src + 2);
+        }
+        cp_async_commit();
+    }
+
+    // Batch 0 in flight, batch 1's ids loading.
+    __device__ __forceinline__ void start() {
+        const int t = threadIdx.x;
+        idx_f = pos(0, t);
+        gid_f = idx_f >= 0 ? pair_gauss[idx_f] : 0u;
+        launch_copy();
+        idx_n = pos(1, t);
+        gid_n = idx_n >= 0 ? __ldg(pair_gauss + idx_n) : 0u;
+    }
+
+    // Stage batch b (whose records are in flight): cull + compact into sm, then launch batch
+    // b+1's copies and batch b+2's id loads.  Returns the staged count, or -1 when no thread of
+    // the CTA is `active` (every thread gets the same answer; nothing is staged then).
+    __device__ __forceinline__ int stage(int b, bool active, int bx0, int bx1, int by0, int by1, StageSmem<CAP>& sm) {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+        cp_async_wait_all();
+        // raw is complete and visible; every thread is done reading the previous staging area
+        if (__syncthreads_count(active) == 0) return -1;
+        bool keep = false;
+        ProjRec rr;
+        if (idx_f >= 0) {
+            rr.r0 = raw->r[tid][0];
+            rr.r1 = raw->r[tid][1];
+            rr.r2 = raw->r[tid][2];
+            keep = may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) sm.wcnt[warp] = __popc(m);
+        __syncthreads();
+        int off = 0, total = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            const int c = sm.wcnt[w];
+            off += w < warp ? c : 0;
+            total += c;
+        }
+        if (keep) {
+            const int p = off + __popc(m & lanemask_lt());
+            const int X0 = max(range_lo(rr.r1.z), bx0) - bx0, X1 = min(range_hi(rr.r1.z), bx1) - bx0;
+            const int Y0 = max(range_lo(rr.r1.w), by0) - by0, Y1 = min(range_hi(rr.r1.w), by1) - by0;
+            const uint32_t cols = ((1u << X1) - 1u) & ~((1u << X0) - 1u);
+            const uint32_t rows = ((1u << Y1) - 1u) & ~((1u << Y0) - 1u);
+            sm.r0[p] = rr.r0;
+            sm.r1[p] = make_float4(rr.r1.x, rr.r1.y, __uint_as_float(cols | (rows << 16)), rr.r2.w);
+            sm.r2[p] = rr.r2;
+            sm.gid[p] = gid_f;
+            sm.idx[p] = idx_f;
+        }
+        __syncthreads();  // staged batch visible; raw reads done
+        idx_f = idx_n;
+        gid_f = gid_n;
+        launch_copy();
+        idx_n = pos(b + 2, tid);
+        gid_n = idx_n >= 0 ? __ldg(pair_gauss + idx_n) : 0u;
+        return total;
+    }
+
+    // No copy may still be writing raw when the CTA moves on (persistent kernels reuse it).
+    __device__ __forceinline__ void finish() { cp_async_wait_all(); }
+};
+
 }  // namespace splat_b200

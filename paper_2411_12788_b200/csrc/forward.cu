@@ -375,6 +375,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
                                                            float bg2, FwdOutputs out) {
     __shared__ StageSmem<BW * BH> sm;
+    __shared__ StageRaw<BW * BH> raw;
     __shared__ float s_imp[REPORT ? BW * BH : 1];
     __shared__ uint32_t s_maxw[REPORT ? BW * BH : 1];
     const int nthreads = blockDim.x;
@@ -412,11 +413,17 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
         s_imp[tid] = 0.0f;
         s_maxw[tid] = 0u;
     }
-    if (bx0 < bx1 && by0 < by1) {
-        for (uint32_t base = start; base < end; base += nthreads) {
-            if (__syncthreads_count(!done) == 0) break;
-            const int cnt = stage_batch([&](int t) { return (int)(base + t); }, (int)min((uint32_t)nthreads, end - base),
-                                        pair_gauss, rec, bx0, bx1, by0, by1, sm);
+    if (bx0 < bx1 && by0 < by1 && start < end) {
+        auto pos = [&](int b, int t) -> int {
+            const uint32_t i = start + (uint32_t)b * (uint32_t)nthreads + (uint32_t)t;
+            return i < end ? (int)i : -1;
+        };
+        StagePipe<BW * BH, decltype(pos)> pipe(pos, pair_gauss, rec, &raw);
+        pipe.start();
+        const int nb = (int)((end - start + (uint32_t)nthreads - 1u) / (uint32_t)nthreads);
+        for (int b = 0; b < nb; ++b) {
+            const int cnt = pipe.stage(b, !done, bx0, bx1, by0, by1, sm);
+            if (cnt < 0) break;
             if (!REPORT) {
                 // Two staged entries per iteration: independent branch-free gates, then the
                 // per-pixel recursion commits them in list order.
@@ -521,8 +528,9 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                     s_maxw[tid] = 0u;
                 }
             }
-            __syncthreads();
+            // the next stage() starts with a barrier: staged entries stay until every warp is done
         }
+        pipe.finish();
     }
     if (!inside) return;
     const size_t pix = (size_t)py * cp.width + px;

@@ -91,16 +91,18 @@ struct BinningArgs {
     uint32_t* st_gauss[2];  // [0]: supertile lists (chunked path); both: sort ping-pong (fallback)
     uint32_t* st_cnt;       // [st_chunk_words] chunked path: (supertile, chunk) counts / offsets
     uint32_t* st_ranges;   // [2 * n_st]
-    uint32_t* seg_start;   // [n_st + 1] segment starts, then [bin_segment_upper] supertile of each segment
-    uint32_t* tile_base;   // [n_tiles + 1]
-    uint32_t* slots;       // [bin_segment_upper * 16 + 1]
-    uint32_t* ranges;      // [2 * n_tiles] out
-    uint32_t* pair_gauss;  // [P] out: per-tile lists of Gaussian ids
+    uint16_t* st_cover;     // [st_pairs] tile cover (16 bits) of each supertile list entry
+    uint32_t* l2_tmp;      // [bin_l2_words] level-2 piece map and per-piece tile counts
+    uint32_t* ranges;      // [2 * n_tiles] out: [start, end) of each tile's list in pair_gauss
+    uint32_t* pair_gauss;  // [16 * st_pairs] out: per-tile lists of Gaussian ids (capacity layout)
     uint32_t* hist;
     uint32_t* scan_tmp;
 };
 int supertile_side();
-size_t bin_segment_upper(uint64_t st_pairs, int n_st);
+// Capacity (entries) of the per-tile list buffer: every tile of supertile s gets L_s slots.
+size_t bin_l2_pieces(uint64_t st_pairs, int n_st);
+size_t bin_l2_words(uint64_t st_pairs, int n_st);
+inline size_t tile_list_capacity(uint64_t st_pairs) { return (size_t)st_pairs * 16; }
 // Chunked supertile pass (no pair sort) when the supertile count fits shared memory; otherwise
 // the fallback needs st_offsets (exclusive scan of supertile counts in depth order) and st_key.
 bool st_chunked(int n_st);

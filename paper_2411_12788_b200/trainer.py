@@ -77,7 +77,9 @@ class ViewTrainer:
             return self.grads.flat[: 3 * n]
         return self.grads.flat[: 59 * n]
 
-    def _views(self, cams: Sequence[Camera], targets) -> None:
+    def _views(self, cams: Sequence[Camera], targets, ready=None) -> None:
+        """`ready[j]` (optional): an event the backward of view j waits for (its target's H2D
+        copy), so the copy overlaps that view's forward."""
         lib, h = self.ctx.lib, self.ctx.h
         self.pairs_last_step = []
         self.survivors_last_step = []
@@ -88,6 +90,8 @@ class ViewTrainer:
             lib.splat_forward_counts(h, C.byref(ns_), C.byref(np_), None, None)
             self.pairs_last_step.append(np_.value)
             self.survivors_last_step.append(ns_.value)
+            if ready is not None:
+                self.torch.cuda.current_stream().wait_event(ready[j])
             self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
                                                         as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
                                                         1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
@@ -98,23 +102,33 @@ class ViewTrainer:
             dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
         self.opt.step(self.params, self.grads, self.group_mask, self.ctx)
 
-    def step(self, cams: Sequence[Camera], targets) -> "object":
+    def step(self, cams: Sequence[Camera], targets, ready=None) -> "object":
         """Device-resident step: targets are CUDA tensors [H, W, 3]. Returns the per-view loss
         tensor (device); nothing is synchronised."""
         self.ctx.bind_stream()
-        self._views(cams, targets)
+        self._views(cams, targets, ready)
         self._finish()
         return self.loss[: len(cams)]
 
     def step_host(self, cams: Sequence[Camera], targets_host) -> np.ndarray:
         """End-to-end step through the public API: each view's target is copied host->device
-        (pinned, async) inside the step and the per-view losses are read back to the host."""
+        (pinned, async) inside the step and the per-view losses are read back to the host.
+
+        The copies run on a side stream and each view's backward waits only for its own target,
+        so the H2D transfer overlaps that view's forward (preprocess, sort, binning, blend)."""
         torch = self.torch
         k = len(cams)
         shape = tuple(targets_host[0].shape)
         if self._staging is None or self._staging.shape[0] < k or tuple(self._staging.shape[1:]) != shape:
             self._staging = torch.empty((k, *shape), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
-        for j in range(k):
-            self._staging[j].copy_(targets_host[j], non_blocking=True)
-        self.step(cams, [self._staging[j] for j in range(k)])
+            self._copy_stream = torch.cuda.Stream(device=self.ctx.device)
+            self._copy_events = [torch.cuda.Event() for _ in range(k)]
+        compute = torch.cuda.current_stream(self.ctx.device)
+        cs = self._copy_stream
+        cs.wait_stream(compute)  # the staging buffer is free once the previous step's backward ran
+        with torch.cuda.stream(cs):
+            for j in range(k):
+                self._staging[j].copy_(targets_host[j], non_blocking=True)
+                self._copy_events[j].record(cs)
+        self.step(cams, [self._staging[j] for j in range(k)], ready=self._copy_events[:k])
         return self.loss[:k].cpu().numpy()
