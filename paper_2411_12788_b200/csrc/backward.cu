@@ -12,6 +12,9 @@
 #include "internal.h"
 
 namespace splat_b200 {
+#ifdef SPLAT_STATS
+__device__ unsigned long long g_bstats[8];
+#endif
 
 namespace {
 
@@ -234,6 +237,20 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
             if (ga) commit(v, r0a, r1a, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
             if (gb) commit(v + 12, r0b, r1b, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
             const bool any_a = __any_sync(0xffffffffu, ga), any_b = __any_sync(0xffffffffu, gb);
+#ifdef SPLAT_STATS
+            {
+                const unsigned el_a = __ballot_sync(0xffffffffu, wa && idx_a <= my_last);
+                const unsigned el_b = __ballot_sync(0xffffffffu, wb && idx_b <= my_last);
+                const unsigned ca = __ballot_sync(0xffffffffu, ga), cb = __ballot_sync(0xffffffffu, gb);
+                if (lane == 0) {
+                    atomicAdd(&g_bstats[0], (unsigned long long)(wa + wb));
+                    atomicAdd(&g_bstats[1], (unsigned long long)(any_a + any_b));
+                    atomicAdd(&g_bstats[2], (unsigned long long)(__popc(el_a) + __popc(el_b)));
+                    atomicAdd(&g_bstats[3], (unsigned long long)(__popc(ca) + __popc(cb)));
+                    atomicAdd(&g_bstats[4], 1ull);
+                }
+            }
+#endif
             if (any_a || any_b) {
                 float r[3];
                 warp_reduce24(v, lane, r);
@@ -248,6 +265,190 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
         // the next stage() starts with a barrier before it overwrites the staging area
     }
     pipe.finish();
+}
+
+// Two pixels per thread: one warp per 8 x 8 block, lane (lx, ly) owns pixels (lx, ly) ["A", top
+// half] and (lx, ly + 4) ["B", bottom half].  The per-pixel recursion and gates are those of
+// blend_backward_block; per staged pair of entries the two pixels' contributions are added in
+// registers before ONE 24-value warp reduction, which now covers 64 pixels (half the reduction
+// work per pixel), and the two pixel chains are independent instruction streams.  Entries whose
+// effective rect misses a half skip that half's gates (warp-uniform).
+struct PixBwd {
+    float T, b0, b1, b2, dL0, dL1, dL2, x, y;
+    int last;
+    uint32_t bits;
+};
+
+template <bool THR>
+__device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
+                                                         const uint32_t* __restrict__ pair_gauss,
+                                                         const ProjRec* __restrict__ rec,
+                                                         const float* __restrict__ t_final,
+                                                         const int32_t* __restrict__ last_index, float bg0, float bg1,
+                                                         float bg2, const float* __restrict__ d_color,
+                                                         const float* __restrict__ color,
+                                                         const float* __restrict__ target, float inv_n,
+                                                         float* __restrict__ loss_partials,
+                                                         float4* __restrict__ grad2d) {
+    constexpr int BW = 8, BH = 8;
+    __shared__ StageSmem<32> sm;
+    __shared__ StageRaw<32> raw;
+    const int lane = threadIdx.x;
+    const int ts = cp.tile_size;
+    const int subs_x = ts / BW, nsub = subs_x * (ts / BH);
+    const int tile = bid / nsub, sub = bid - tile * nsub;
+    const int tx = tile % cp.tiles_x, ty = tile / cp.tiles_x;
+    const int sx = sub % subs_x, sy = sub / subs_x;
+    const int bx0 = tx * ts + sx * BW, by0 = ty * ts + sy * BH;
+    const int bx1 = min(bx0 + BW, cp.width), by1 = min(by0 + BH, cp.height);
+    const int lx = lane & 7, ly = lane >> 3;
+    PixBwd P[2];
+    float l = 0.0f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int px = bx0 + lx, py = by0 + ly + 4 * h;
+        const bool inside = px < cp.width && py < cp.height;
+        const size_t pix = inside ? (size_t)py * cp.width + px : 0;
+        PixBwd& q = P[h];
+        q.dL0 = q.dL1 = q.dL2 = 0.0f;
+        if (inside) {
+            if (target) {
+                const float d0 = color[3 * pix] - target[3 * pix];
+                const float d1 = color[3 * pix + 1] - target[3 * pix + 1];
+                const float d2 = color[3 * pix + 2] - target[3 * pix + 2];
+                l += fabsf(d0) + fabsf(d1) + fabsf(d2);
+                q.dL0 = d0 > 0.0f ? inv_n : (d0 < 0.0f ? -inv_n : 0.0f);
+                q.dL1 = d1 > 0.0f ? inv_n : (d1 < 0.0f ? -inv_n : 0.0f);
+                q.dL2 = d2 > 0.0f ? inv_n : (d2 < 0.0f ? -inv_n : 0.0f);
+            } else {
+                q.dL0 = d_color[3 * pix];
+                q.dL1 = d_color[3 * pix + 1];
+                q.dL2 = d_color[3 * pix + 2];
+            }
+        }
+        q.last = inside ? last_index[pix] : -1;
+        q.T = inside ? t_final[pix] : 1.0f;
+        q.b0 = bg0;
+        q.b1 = bg1;
+        q.b2 = bg2;
+        q.x = (float)px + 0.5f;
+        q.y = (float)py + 0.5f;
+        q.bits = (1u << lx) | (1u << (16 + ly + 4 * h));
+    }
+    if (target && loss_partials) {
+        const float ws = warp_sum(l);
+        if (lane == 0) loss_partials[bid] = ws;
+    }
+    const int wlA = (int)__reduce_max_sync(0xffffffffu, (unsigned)(P[0].last + 1)) - 1;
+    const int wlB = (int)__reduce_max_sync(0xffffffffu, (unsigned)(P[1].last + 1)) - 1;
+    const int block_last = max(wlA, wlB);
+    const uint32_t start = ranges[2 * tile];
+    if (block_last < (int)start) return;  // nothing committed in this block
+
+    const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
+    constexpr uint32_t kRowsA = 0xfu << 16, kRowsB = 0xf0u << 16;
+    const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
+    const uint32_t a_idx = smem_base(sm.idx), a_gid = smem_base(sm.gid);
+
+    auto pos = [&](int b, int t) -> int {
+        const int i = block_last - b * 32 - t;
+        return i >= (int)start ? i : -1;
+    };
+    StagePipe<32, decltype(pos)> pipe(pos, pair_gauss, rec, &raw);
+    pipe.start();
+    const int nb = (block_last + 1 - (int)start + 31) / 32;
+    for (int b = 0; b < nb; ++b) {
+        const int cnt = pipe.stage(b, true, bx0, bx1, by0, by1, sm);
+        for (int j = 0; j < cnt; j += 2) {
+            const bool has_b = j + 1 < cnt;
+            const uint32_t jb = has_b ? (uint32_t)(j + 1) : (uint32_t)j;
+            const int idx_a = (int)lds_u32(a_idx + 4u * j);
+            const int idx_b = has_b ? (int)lds_u32(a_idx + 4u * jb) : INT_MAX;
+            const float4 r1a = lds_f4(a_r1 + 16u * j);
+            const float4 r1b = lds_f4(a_r1 + 16u * jb);
+            const uint32_t ma = __float_as_uint(r1a.z), mb = __float_as_uint(r1b.z);
+            // warp-uniform per half: above every commit of the half, or the rect misses the half
+            const bool waA = idx_a <= wlA && (ma & kRowsA), waB = idx_a <= wlB && (ma & kRowsB);
+            const bool wbA = idx_b <= wlA && (mb & kRowsA), wbB = idx_b <= wlB && (mb & kRowsB);
+            if (!(waA || waB || wbA || wbB)) continue;
+            const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
+            float v[24];
+#pragma unroll
+            for (int k = 0; k < 24; ++k) v[k] = 0.0f;
+            bool anyc_a = false, anyc_b = false;
+            auto commit = [&](float* vv, PixBwd& q, const float4& r0, const float4& r1, const float4& r2, float alpha,
+                              float g2d, bool clamped, float dx, float dy) {
+                const float one_m_a = 1.0f - alpha;
+                const float t_before = __fdividef(q.T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
+                const float w = t_before * alpha;
+                vv[6] += w * q.dL0;
+                vv[7] += w * q.dL1;
+                vv[8] += w * q.dL2;
+                const float da = t_before * (q.dL0 * (r2.x - q.b0) + q.dL1 * (r2.y - q.b1) + q.dL2 * (r2.z - q.b2));
+                if (!clamped) {
+                    vv[5] += da * g2d;
+                    const float dpower = da * r1.y * g2d;
+                    vv[0] += dpower * (-(r0.z * dx + r0.w * dy));
+                    vv[1] += dpower * (-(r1.x * dy + r0.w * dx));
+                    const float hp = -0.5f * dpower;
+                    vv[2] += hp * dx * dx;
+                    vv[3] += hp * dx * dy;
+                    vv[4] += hp * dy * dy;
+                }
+                vv[9] += 1.0f;
+                q.b0 = alpha * r2.x + one_m_a * q.b0;
+                q.b1 = alpha * r2.y + one_m_a * q.b1;
+                q.b2 = alpha * r2.z + one_m_a * q.b2;
+                q.T = t_before;
+            };
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const bool wa = h == 0 ? waA : waB, wb = h == 0 ? wbA : wbB;
+                if (!(wa || wb)) continue;
+                PixBwd& q = P[h];
+                float alpha_a, g_a, dxa, dya, alpha_b, g_b, dxb, dyb;
+                bool cl_a, cl_b;
+                bool ga = gate_sample_nb<THR>(r0a, r1a, q.bits, q.x, q.y, amax_c, cmin, alpha_a, g_a, cl_a, dxa, dya);
+                bool gb = gate_sample_nb<THR>(r0b, r1b, q.bits, q.x, q.y, amax_c, cmin, alpha_b, g_b, cl_b, dxb, dyb);
+                ga = ga && wa && idx_a <= q.last;
+                gb = gb && wb && idx_b <= q.last;
+                if (ga) commit(v, q, r0a, r1a, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
+                if (gb) commit(v + 12, q, r0b, r1b, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+                anyc_a |= ga;
+                anyc_b |= gb;
+            }
+            const bool any_a = __any_sync(0xffffffffu, anyc_a), any_b = __any_sync(0xffffffffu, anyc_b);
+            if (any_a || any_b) {
+                float r[3];
+                warp_reduce24(v, lane, r);
+                const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
+                const bool mine = (lane & 3) == 0 && (grp < 4 ? any_a : any_b);
+                if (mine) {
+                    const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
+                    red_add_v4(grad2d + 4 * (size_t)gid + (grp & 3), r[0], r[1], r[2], 0.0f);
+                }
+            }
+        }
+    }
+    pipe.finish();
+}
+
+template <bool THR>
+__global__ void __launch_bounds__(32) blend_backward_px2_persistent(
+    CamParams cp, const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ pair_gauss,
+    const ProjRec* __restrict__ rec, const float* __restrict__ t_final, const int32_t* __restrict__ last_index,
+    float bg0, float bg1, float bg2, const float* __restrict__ d_color, const float* __restrict__ color,
+    const float* __restrict__ target, float inv_n, float* __restrict__ loss_partials, float4* __restrict__ grad2d,
+    int nblocks, int* __restrict__ counter) {
+    for (;;) {
+        int b = 0;
+        if (threadIdx.x == 0) b = atomicAdd(counter, 1);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= nblocks) break;
+        blend_backward_block_px2<THR>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color,
+                                      color, target, inv_n, loss_partials, grad2d);
+        __syncwarp();
+    }
 }
 
 template <bool THR, int BW, int BH>
@@ -320,24 +521,30 @@ __global__ void __launch_bounds__(kL1Threads) l1_kernel(const float* __restrict_
 constexpr int kLossThreads = 1024;
 __global__ void __launch_bounds__(kLossThreads) loss_reduce_kernel(const float* __restrict__ partials, int n,
                                                                    float inv_n, float* __restrict__ loss) {
+    // one CTA; 16 independent loads in flight per thread, fp64 accumulation (order fixed by n)
     __shared__ double s[kLossThreads / 32];
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int i = threadIdx.x;
-    for (; i + 3 * kLossThreads < n; i += 4 * kLossThreads) {
+    constexpr int kU = 16;
+    double acc = 0.0;
+    for (int base = 0; base < n; base += kLossThreads * kU) {
+        float v[kU];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] += (double)partials[i + k * kLossThreads];
+        for (int k = 0; k < kU; ++k) {
+            const int i = base + k * kLossThreads + threadIdx.x;
+            v[k] = i < n ? partials[i] : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) acc += (double)v[k];
     }
-    for (int k = 0; i < n; i += kLossThreads, ++k) acc[k & 3] += (double)partials[i];
-    double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    double w = acc;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = w;
     __syncthreads();
     if (threadIdx.x < 32) {
-        v = s[threadIdx.x];
+        w = threadIdx.x < kLossThreads / 32 ? s[threadIdx.x] : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) *loss = (float)v * inv_n;
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (threadIdx.x == 0) *loss = (float)w * inv_n;
     }
 }
 
@@ -411,7 +618,25 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
         else if (cp.block_h == 8) BLEND_BWD_SHAPE(T, 8, 8);      \
         else BLEND_BWD_SHAPE(T, 8, 4);                           \
     } while (0)
-        if (cp.apply_thresholds) BLEND_BWD(true);
+        if (lc.bwd_px2 && cp.block_w == 8 && cp.block_h == 8 && lc.work_counters) {
+            static int per_sm[2] = {0, 0};
+            const int k = cp.apply_thresholds ? 1 : 0;
+            if (!per_sm[k]) {
+                if (k) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], blend_backward_px2_persistent<true>, 32, 0);
+                else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], blend_backward_px2_persistent<false>, 32, 0);
+            }
+            unsigned pg = (unsigned)(lc.num_sms * (per_sm[k] > 0 ? per_sm[k] : 1));
+            if (pg > grid) pg = grid;
+            cudaMemsetAsync(lc.work_counters + 1, 0, 4, lc.stream);
+            if (k)
+                blend_backward_px2_persistent<true><<<pg, 32, 0, lc.stream>>>(
+                    cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
+                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);
+            else
+                blend_backward_px2_persistent<false><<<pg, 32, 0, lc.stream>>>(
+                    cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
+                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);
+        } else if (cp.apply_thresholds) BLEND_BWD(true);
         else BLEND_BWD(false);
 #undef BLEND_BWD
 #undef BLEND_BWD_SHAPE
@@ -463,3 +688,19 @@ cudaError_t launch_quat_normalize(LaunchCtx& lc, float* rotations, int n) {
 }
 
 }  // namespace splat_b200
+
+extern "C" int splat_debug_bstats(unsigned long long* out, int reset) {
+#ifdef SPLAT_STATS
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, splat_b200::g_bstats, sizeof(unsigned long long) * 8) != cudaSuccess) return 3;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(splat_b200::g_bstats, z, sizeof(z));
+    }
+    return 0;
+#else
+    (void)out;
+    (void)reset;
+    return -1;
+#endif
+}

@@ -469,6 +469,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
     {
         const char* e = std::getenv("SPLAT_BLEND_PERSISTENT");
         c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
+        const char* e2 = std::getenv("SPLAT_BWD_PX2");
+        c->lc.bwd_px2 = !(e2 && std::strcmp(e2, "0") == 0);
     }
     *out = c;
     return SPLAT_OK;

@@ -133,11 +133,10 @@ __device__ __forceinline__ bool gate_sample_nb(const float4& r0, const float4& r
 // is a clamped 1-D vertex.  The 1e-3 margin in the exponent dwarfs every rounding involved (q is
 // evaluated to ~1e-6 relative, splat_expf to 1 ulp), so a culled sample would have been skipped
 // by the per-pixel gate anyway: the committed set, and every output bit, are unchanged.
-__device__ __forceinline__ bool may_contribute(const float4& r0, const float4& r1, float cut, int bx0, int bx1,
-                                               int by0, int by1) {
-    const int X0 = max(range_lo(r1.z), bx0), X1 = min(range_hi(r1.z), bx1);
-    const int Y0 = max(range_lo(r1.w), by0), Y1 = min(range_hi(r1.w), by1);
-    if (X0 >= X1 || Y0 >= Y1) return false;
+// (b) alone, over the pixel box [X0, X1) x [Y0, Y1) (non-empty): r0 = (mean, conic0, conic1), c =
+// conic2.
+__device__ __forceinline__ bool quad_box_reaches(const float4& r0, float c, float cut, int X0, int X1, int Y0,
+                                                 int Y1) {
     if (!(cut > -INFINITY)) return true;
     // dx = mean.x - (px + 0.5) over px in [X0, X1 - 1]
     const float dxl = r0.x - ((float)X1 - 0.5f), dxh = r0.x - ((float)X0 + 0.5f);
@@ -145,7 +144,7 @@ __device__ __forceinline__ bool may_contribute(const float4& r0, const float4& r
     float qmin = 0.0f;
     const bool inside = dxl <= 0.0f && dxh >= 0.0f && dyl <= 0.0f && dyh >= 0.0f;
     if (!inside) {
-        const float a = r0.z, b = r0.w, c = r1.x;
+        const float a = r0.z, b = r0.w;
         // q minus a rounding bound proportional to the magnitudes of its terms: the per-pixel
         // gate evaluates the same quadratic in another order, and for elongated Gaussians the
         // terms cancel (|terms| >> q), so the cull must not trust q beyond ~1e-5 of sum |terms|.
@@ -161,6 +160,14 @@ __device__ __forceinline__ bool may_contribute(const float4& r0, const float4& r
         qmin = fminf(fminf(q_lo(dxl, y_at_xl), q_lo(dxh, y_at_xh)), fminf(q_lo(x_at_yl, dyl), q_lo(x_at_yh, dyh)));
     }
     return -0.5f * qmin >= cut;
+}
+
+__device__ __forceinline__ bool may_contribute(const float4& r0, const float4& r1, float cut, int bx0, int bx1,
+                                               int by0, int by1) {
+    const int X0 = max(range_lo(r1.z), bx0), X1 = min(range_hi(r1.z), bx1);
+    const int Y0 = max(range_lo(r1.w), by0), Y1 = min(range_hi(r1.w), by1);
+    if (X0 >= X1 || Y0 >= Y1) return false;
+    return quad_box_reaches(r0, r1.x, cut, X0, X1, Y0, Y1);
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

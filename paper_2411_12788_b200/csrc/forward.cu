@@ -9,6 +9,11 @@
 #include "internal.h"
 
 namespace splat_b200 {
+#ifdef SPLAT_STATS
+// Instrumented builds only (tools/stats_build.sh): forward traversal counters, read with
+// splat_debug_stats.
+__device__ unsigned long long g_stats[8];
+#endif
 
 namespace {
 
@@ -424,6 +429,12 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
         for (int b = 0; b < nb; ++b) {
             const int cnt = pipe.stage(b, !done, bx0, bx1, by0, by1, sm);
             if (cnt < 0) break;
+#ifdef SPLAT_STATS
+            if (tid == 0) {
+                atomicAdd(&g_stats[4], (unsigned long long)cnt);
+                atomicAdd(&g_stats[6], (unsigned long long)min((uint32_t)nthreads, end - start - (uint32_t)b * nthreads));
+            }
+#endif
             if (!REPORT) {
                 // Two staged entries per iteration: independent branch-free gates, then the
                 // per-pixel recursion commits them in list order.
@@ -443,6 +454,27 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                                                         dy) && wa;
                     const bool gb = gate_sample_nb<THR>(r0b, r1b, mybits, x, y, amax_c, cmin, alpha_b, g2d, clamped, dx,
                                                         dy) && wb;
+#ifdef SPLAT_STATS
+                    {
+                        auto patch_ok = [&](const float4& r0, const float4& r1, uint32_t msk) {
+                            const uint32_t cols = msk & wcols & 0xffffu, rows = (msk & wrows) >> 16;
+                            if (!cols || !rows) return false;
+                            const int X0 = __ffs(cols) - 1, X1 = 32 - __clz(cols);
+                            const int Y0 = __ffs(rows) - 1, Y1 = 32 - __clz(rows);
+                            return quad_box_reaches(r0, r1.x, r1.w, bx0 + X0, bx0 + X1, by0 + Y0, by0 + Y1);
+                        };
+                        const bool pa = wa && patch_ok(r0a, r1a, ma), pb = wb && patch_ok(r0b, r1b, mb);
+                        const unsigned am = __activemask();
+                        const bool anya = __any_sync(am, ga), anyb = __any_sync(am, gb);
+                        if ((tid & 31) == __ffs(am) - 1) {
+                            atomicAdd(&g_stats[0], (unsigned long long)(wa + wb));
+                            atomicAdd(&g_stats[1], (unsigned long long)((wa && !pa) + (wb && !pb)));
+                            atomicAdd(&g_stats[2], (unsigned long long)(anya + anyb));
+                            atomicAdd(&g_stats[3], (unsigned long long)((pa && !anya) + (pb && !anyb)));
+                            atomicAdd(&g_stats[5], (unsigned long long)__popc(am));
+                        }
+                    }
+#endif
                     if (ga) {
                         const float next = T * (1.0f - alpha_a);
                         if (THR && next < tmin) {
@@ -778,3 +810,20 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
 }
 
 }  // namespace splat_b200
+
+// Instrumented builds: copy (and with reset != 0, zero) the forward traversal counters.
+extern "C" int splat_debug_stats(unsigned long long* out, int reset) {
+#ifdef SPLAT_STATS
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, splat_b200::g_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return 3;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(splat_b200::g_stats, z, sizeof(z));
+    }
+    return 0;
+#else
+    (void)out;
+    (void)reset;
+    return -1;
+#endif
+}

@@ -23,6 +23,7 @@ struct LaunchCtx {
     int num_sms = 148;
     int* work_counters = nullptr;  // device ints for persistent-CTA work queues ([0] fwd, [1] bwd)
     bool persistent_blend = true;  // blend kernels as persistent CTAs pulling pixel blocks
+    bool bwd_px2 = true;           // 8 x 8 backward: one warp, two pixels per thread
     ProfileState* prof = nullptr;  // non-null while per-kernel CUDA-event timing is on
     // Bracket one kernel launch with CUDA events on `stream` (no-ops when profiling is off).
     void prof_begin(const char* name);

@@ -17,6 +17,7 @@
 // (stable), publish per-digit tile counts, look back per digit (one thread per digit) for the
 // tile's global digit offsets, and scatter.  2 + passes launches per sort instead of 5 per pass.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -392,13 +393,20 @@ __global__ void __launch_bounds__(kThreads) radix_scatter_kernel(
     }
 }
 
-constexpr uint32_t kOnesweepMaxTiles = 640;  // above this, the look-back chain costs more than a scan
+// Above this many tiles the Onesweep look-back chain costs more than a reduce-then-scan pass.
+static uint32_t onesweep_max_tiles() {
+    static uint32_t v = [] {
+        const char* e = std::getenv("SPLAT_ONESWEEP_MAX");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 640u;
+    }();
+    return v;
+}
 
 template <int BITS>
 void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n,
                      int shift, const uint32_t* hist, uint32_t* status, uint32_t* counter, uint32_t* scan_tmp) {
     const uint32_t ntiles = (n + kSortTile - 1) / kSortTile;
-    if (ntiles <= kOnesweepMaxTiles) {
+    if (ntiles <= onesweep_max_tiles()) {
         radix_onesweep_kernel<BITS><<<ntiles, kThreads, 0, lc.stream>>>(ki, vi, ko, vo, n, shift, hist, status, counter);
         return;
     }
