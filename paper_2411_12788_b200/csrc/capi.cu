@@ -129,6 +129,12 @@ struct splat_ctx {
     DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
+    // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
+    // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
+    // view's blend forward (ev_fwd_start) and joined before the chain (ev_zero).
+    cudaStream_t zstream = nullptr;
+    cudaEvent_t ev_fwd_start = nullptr, ev_zero = nullptr;
+    bool fwd_start_recorded = false;
     FwdState st;
 };
 
@@ -250,6 +256,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     if ((rc = make_params(ctx, cam, cfg, &cp))) return rc;
     LaunchCtx& lc = ctx->lc;
     cudaStream_t s = ctx->stream;
+    ctx->fwd_start_recorded = false;
     const int n = g->n;
     const size_t nn = (size_t)(n > 0 ? n : 1);
     const int n_tiles = cp.tiles_x * cp.tiles_y;
@@ -378,6 +385,10 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     fo.max_pixel_count = report ? rep->max_pixel_count : nullptr;
     fo.t_final = ctx->t_final.as<float>();
     fo.last_index = ctx->last_index.as<int32_t>();
+    // the gradient zero-fill of a following backward may start here: it then overlaps the blend
+    // kernels (issue-bound) rather than the latency-bound sort and binning
+    CK(cudaEventRecord(ctx->ev_fwd_start, s), "record forward start");
+    ctx->fwd_start_recorded = true;
     CK(launch_blend_forward(lc, cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
                             want_depth ? ctx->aux.as<AuxRec>() : nullptr, bg, fo),
        "blend forward");
@@ -418,6 +429,20 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     LaunchCtx& lc = ctx->lc;
     const int n = g->n;
     CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 64, true, ctx->stream), "alloc grad2d");
+    const bool zero_async = !accumulate && n > 0 && ctx->fwd_start_recorded;
+    if (zero_async) {
+        cudaStream_t z = ctx->zstream;
+        CK(cudaStreamWaitEvent(z, ctx->ev_fwd_start, 0), "zero wait");
+        const size_t nn = (size_t)n;
+        CK(cudaMemsetAsync(grads->d_centers, 0, 12 * nn, z), "zero grads");
+        CK(cudaMemsetAsync(grads->d_log_scales, 0, 12 * nn, z), "zero grads");
+        CK(cudaMemsetAsync(grads->d_rotations, 0, 16 * nn, z), "zero grads");
+        CK(cudaMemsetAsync(grads->d_opacity_logits, 0, 4 * nn, z), "zero grads");
+        CK(cudaMemsetAsync(grads->d_sh, 0, 192 * nn, z), "zero grads");
+        if (grads->grad2d_accum) CK(cudaMemsetAsync(grads->grad2d_accum, 0, 4 * nn, z), "zero grads");
+        if (grads->grad2d_count) CK(cudaMemsetAsync(grads->grad2d_count, 0, 4 * nn, z), "zero grads");
+        CK(cudaEventRecord(ctx->ev_zero, z), "zero done");
+    }
     const int n_blocks =
         st.cp.tiles_x * st.cp.tiles_y * (st.cp.tile_size / st.cp.block_w) * (st.cp.tile_size / st.cp.block_h);
     float* partials = nullptr;
@@ -435,8 +460,9 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     if (n > 0) {
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
         CK(ctx->chain_list.ensure(((size_t)st.n_surv + 2) * 4), "alloc chain list");
+        if (zero_async) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_zero, 0), "zero join");
         CK(launch_chain(lc, gp, st.cp, ctx->grad2d.as<float>(), ctx->rec.as<ProjRec>(), *grads, accumulate, st.n_surv,
-                        ctx->chain_list.as<uint32_t>()),
+                        ctx->chain_list.as<uint32_t>(), zero_async),
            "chain");
     }
     if (partials) {
@@ -466,6 +492,13 @@ int splat_ctx_create(int device, splat_ctx** out) {
         delete c;
         return SPLAT_ERR_OUT_OF_MEMORY;
     }
+    if (cudaStreamCreateWithFlags(&c->zstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fwd_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_zero, cudaEventDisableTiming) != cudaSuccess) {
+        cudaFree(c->lc.work_counters);
+        delete c;
+        return SPLAT_ERR_CUDA;
+    }
     {
         const char* e = std::getenv("SPLAT_BLEND_PERSISTENT");
         c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
@@ -482,6 +515,12 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
     if (ctx->lc.work_counters) cudaFree(ctx->lc.work_counters);
+    if (ctx->ev_fwd_start) cudaEventDestroy(ctx->ev_fwd_start);
+    if (ctx->ev_zero) cudaEventDestroy(ctx->ev_zero);
+    if (ctx->zstream) {
+        cudaStreamSynchronize(ctx->zstream);
+        cudaStreamDestroy(ctx->zstream);
+    }
     delete ctx->lc.prof;
     delete ctx;
     return SPLAT_OK;

@@ -387,20 +387,30 @@ __device__ __forceinline__ void zero_span_warp(float* p, int count, int lane) {
 // its own 192-byte SH row in shared memory with float4 loads and writes its gradient row back
 // the same way.
 __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __restrict__ grad2d, int n,
-                                                            splat_param_grads out, int accumulate,
+                                                            splat_param_grads out, int zero_untouched,
                                                             uint32_t* __restrict__ list) {
+    // one list append (atomic) per CTA: a single counter takes ~1 ns per atomic, so per-warp
+    // appends would serialise ~n/32 of them
+    __shared__ uint32_t s_wc[8];
+    __shared__ uint32_t s_base;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool touched = i < n && grad2d[4 * (size_t)i + 3].x > 0.0f;
     const unsigned m = __ballot_sync(0xffffffffu, touched);
-    if (m) {
-        const int leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(list, (uint32_t)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (touched) list[1 + base + __popc(m & lanemask_lt())] = (uint32_t)i;
+    if (lane == 0) s_wc[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t c = s_wc[w];
+            s_wc[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(list, tot) : 0u;
     }
-    if (accumulate) return;  // nothing to add for untouched Gaussians
+    __syncthreads();
+    if (touched) list[1 + s_base + s_wc[warp] + __popc(m & lanemask_lt())] = (uint32_t)i;
+    if (!zero_untouched) return;  // accumulating, or the rows are already zero
     // Every gradient of the warp's 32 Gaussians is zeroed here (touched ones are overwritten by
     // pass 2): each array's span for the warp is contiguous, so the warp writes it with float4
     // stores (full sectors only).
@@ -449,7 +459,8 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 }  // namespace
 
 cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d, const ProjRec* rec,
-                         const splat_param_grads& out, int accumulate, int n_surv, uint32_t* list) {
+                         const splat_param_grads& out, int accumulate, int n_surv, uint32_t* list,
+                         bool prezeroed) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = ((reinterpret_cast<uintptr_t>(g.sh) | reinterpret_cast<uintptr_t>(out.d_sh)) & 15u) == 0;
     float4* g2 = reinterpret_cast<float4*>(grad2d);
@@ -463,7 +474,8 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
     if (e != cudaSuccess) return e;
     {
         LaunchScope ls(lc, "chain_compact");
-        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out, accumulate, list);
+        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out,
+                                                                          !accumulate && !prezeroed, list);
         lc.count++;
     }
     if (n_surv > 0) {

@@ -154,9 +154,11 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   float* loss_partials, float* grad2d);
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
 // K10 chain.  list: scratch of n_surv + 1 words (touched-Gaussian list; touched <= survivors).
+// prezeroed: a fresh (accumulate = 0) gradient whose rows were already zero-filled (side stream);
+// only touched rows are written.
 cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, float* grad2d,
                          const ProjRec* rec, const splat_param_grads& out, int accumulate, int n_surv,
-                         uint32_t* list);
+                         uint32_t* list, bool prezeroed = false);
 cudaError_t launch_l1(LaunchCtx& lc, const float* a, const float* b, int64_t n, float* grad,
                       float* partials, int n_partials);
 int l1_partials_count(int64_t n);
