@@ -245,6 +245,12 @@ int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule,
 int splat_visibility_update(splat_ctx* ctx, const splat_importance_outputs* report_dev, int32_t n,
                             float threshold, uint32_t* bitmask_dev, double* accum_dev,
                             int64_t* counts_dev);
+/* The same, plus max_all_dev[i] = max(max_all_dev[i], max_weight[i]) (may be NULL): the
+ * per-Gaussian maximum blending weight over all views so far (the quantity the view-parallel
+ * pass max-reduces across ranks). */
+int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* report_dev, int32_t n,
+                                float threshold, uint32_t* bitmask_dev, double* accum_dev,
+                                int64_t* counts_dev, float* max_all_dev);
 
 /* ---- primitives (exposed for tests and microbenchmarks) ------------------------------ */
 /* Stable LSD radix sort of (keys, vals) on key bits [begin_bit, end_bit), n pairs, device

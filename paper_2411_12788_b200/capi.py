@@ -222,6 +222,8 @@ _EXPORTS = {
                                         C.c_int64, C.c_int32, C.c_int64, fp, ip, C.c_int64, ip]),
     "splat_visibility_update": (C.c_int, [C.c_void_p, C.POINTER(ImportanceOutputs), C.c_int32, C.c_float,
                                           C.c_void_p, C.c_void_p, C.c_void_p]),
+    "splat_visibility_update_max": (C.c_int, [C.c_void_p, C.POINTER(ImportanceOutputs), C.c_int32, C.c_float,
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

@@ -715,14 +715,19 @@ int splat_depth_unproject(splat_ctx* ctx, const splat_camera* cam, int rule, flo
     return SPLAT_OK;
 }
 
-int splat_visibility_update(splat_ctx* ctx, const splat_importance_outputs* rep, int32_t n, float threshold,
-                            uint32_t* bitmask, double* accum, int64_t* counts) {
+int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* rep, int32_t n, float threshold,
+                                uint32_t* bitmask, double* accum, int64_t* counts, float* max_all) {
     if (!ctx || !rep || n < 0 || (n > 0 && (!rep->importance || !rep->max_weight || !rep->max_pixel_count)))
         return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "visibility_update: bad args");
     CK(launch_visibility_update(ctx->lc, rep->importance, rep->max_weight, rep->max_pixel_count, n, threshold,
-                                bitmask, accum, counts),
+                                bitmask, accum, counts, max_all),
        "visibility_update");
     return SPLAT_OK;
+}
+
+int splat_visibility_update(splat_ctx* ctx, const splat_importance_outputs* rep, int32_t n, float threshold,
+                            uint32_t* bitmask, double* accum, int64_t* counts) {
+    return splat_visibility_update_max(ctx, rep, n, threshold, bitmask, accum, counts, nullptr);
 }
 
 int splat_sort_pairs(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,

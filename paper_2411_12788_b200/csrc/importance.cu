@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(256) visibility_update_kernel(const float* __r
                                                                const int32_t* __restrict__ max_count, int n,
                                                                float threshold, uint32_t* __restrict__ bitmask,
                                                                double* __restrict__ accum,
-                                                               int64_t* __restrict__ counts) {
+                                                               int64_t* __restrict__ counts,
+                                                               float* __restrict__ max_all) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool in = i < n;
     const bool vis = in && max_weight[i] > threshold;
@@ -31,17 +32,19 @@ __global__ void __launch_bounds__(256) visibility_update_kernel(const float* __r
     if (!in) return;
     if (accum) accum[i] += (double)importance[i];
     if (counts) counts[i] += max_count[i];
+    if (max_all) max_all[i] = fmaxf(max_all[i], max_weight[i]);
 }
 
 }  // namespace
 
 cudaError_t launch_visibility_update(LaunchCtx& lc, const float* importance, const float* max_weight,
                                      const int32_t* max_count, int n, float threshold, uint32_t* bitmask,
-                                     double* accum, int64_t* counts) {
+                                     double* accum, int64_t* counts, float* max_all) {
     if (n == 0) return cudaSuccess;
     LaunchScope s(lc, "visibility_update");
     visibility_update_kernel<<<(unsigned)((n + 255) / 256), 256, 0, lc.stream>>>(importance, max_weight, max_count, n,
-                                                                               threshold, bitmask, accum, counts);
+                                                                               threshold, bitmask, accum, counts,
+                                                                               max_all);
     lc.count++;
     return cudaGetLastError();
 }

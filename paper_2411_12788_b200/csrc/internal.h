@@ -139,7 +139,7 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
 // ---- importance.cu ------------------------------------------------------------------------
 cudaError_t launch_visibility_update(LaunchCtx& lc, const float* importance, const float* max_weight,
                                      const int32_t* max_count, int n, float threshold, uint32_t* bitmask,
-                                     double* accum, int64_t* counts);
+                                     double* accum, int64_t* counts, float* max_all = nullptr);
 
 // ---- backward.cu --------------------------------------------------------------------------
 // Per-Gaussian 2D gradient accumulator, 64 B (4 x float4, w unused):

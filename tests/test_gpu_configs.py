@@ -113,3 +113,23 @@ def test_config4_batched_step_all_parameters(oracle):
         d = np.abs(a - b)
         assert d.max() <= 4 * lr + 1e-6, k
         assert (d > 1e-3 * lr).mean() < 1e-3, f"{k}: {(d > 1e-3 * lr).mean():.2e} of elements off"
+
+
+def test_view_parallel_passes_single_rank_match(oracle):
+    """multiview.visibility_pass_views / depth_points_views (the NCCL view-parallel passes) on one
+    rank equal the plain passes; the max blend weight over views equals the oracle's."""
+    from paper_2411_12788_b200 import multiview as MV
+    s = scenes.make_gaussians(20_000, seed=4)
+    cams = [_ring(k, 4) for k in range(4)]
+    masks, accum, counts, mx = MV.visibility_pass_views(s, cams)
+    m0, a0, c0 = R.visibility_pass(s, cams)
+    assert_bitwise(masks.cpu().numpy(), m0.cpu().numpy(), "view-parallel masks")
+    # per-view importance is an atomic float sum (order varies run to run): tolerance, not bits
+    assert np.allclose(accum.cpu().numpy(), a0.cpu().numpy(), rtol=1e-5, atol=1e-9), "view-parallel accum"
+    assert_bitwise(counts.cpu().numpy(), c0.cpu().numpy(), "view-parallel counts")
+    want = np.max(np.stack([oracle.render(s, c)["max_weight"] for c in cams]), 0)
+    assert_bitwise(mx.cpu().numpy(), want, "max blend weight over views")
+    p, v, x = MV.depth_points_views(s, cams, stride=3, seed=1)
+    p0, v0, x0 = R.depth_points(s, cams, stride=3, seed=1)
+    for a, b, what in ((p, p0, "points"), (v, v0, "views"), (x, x0, "pixels")):
+        assert_bitwise(a.cpu().numpy(), b.cpu().numpy(), f"view-parallel {what}")
