@@ -16,7 +16,9 @@ def short(name):
 
 
 def main(path):
-    rows = [r for r in csv.DictReader(open(path)) if r.get("Metric Name") == "gpu__time_duration.sum"]
+    lines = open(path).read().splitlines()
+    head = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))  # skip program / ncu chatter
+    rows = [r for r in csv.DictReader(lines[head:]) if r.get("Metric Name") == "gpu__time_duration.sum"]
     agg = OrderedDict()
     for r in rows:
         v = float(r["Metric Value"].replace(",", ""))

@@ -18,8 +18,8 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 
 NAME_MAP = [  # (regex on the demangled ncu kernel name, bench launch name)
-    (r"blend_backward_kernel", "blend_backward"),
-    (r"blend_forward_kernel", "blend_forward"),
+    (r"blend_backward", "blend_backward"),
+    (r"blend_forward", "blend_forward"),
     (r"chain_touched_kernel", "chain"),
     (r"chain_compact_kernel", "chain_compact"),
     (r"chain_kernel", "chain"),
@@ -27,8 +27,9 @@ NAME_MAP = [  # (regex on the demangled ncu kernel name, bench launch name)
     (r"adam_kernel", "adam"),
     (r"st_chunk_kernel<(\(bool\))?0", "st_count"),
     (r"st_chunk_kernel<(\(bool\))?1", "st_emit"),
-    (r"bin_segments_kernel<(\(bool\))?0", "bin_count"),
-    (r"bin_segments_kernel<(\(bool\))?1", "bin_emit"),
+    (r"bin_count_kernel", "bin_count"),
+    (r"bin_emit_kernel", "bin_emit"),
+    (r"bin_map_kernel", "bin_map"),
     (r"radix_onesweep_kernel", "radix_onesweep"),
     (r"radix_histogram_kernel", "radix_histogram"),
     (r"scan_lookback_kernel", "scan"),
@@ -107,8 +108,7 @@ def summarise(reps):
 def main(reps):
     kernels = summarise(reps)
     path = HERE / "ncu_summary.json"
-    old = json.loads(path.read_text()) if path.exists() else {"kernels": {}}
-    old["kernels"].update(kernels)
+    old = {"kernels": kernels, "sources": [Path(r).name for r in reps]}
     old["note"] = ("ncu --set full --clock-control none captures (cold caches, serialised replays): use shares and "
                    "per-launch DRAM bytes, not absolute times; regenerate with profiles/summarize_ncu.py")
     path.write_text(json.dumps(old, indent=1, sort_keys=True) + "\n")
