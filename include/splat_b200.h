@@ -252,6 +252,67 @@ int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* 
                                 float threshold, uint32_t* bitmask_dev, double* accum_dev,
                                 int64_t* counts_dev, float* max_all_dev);
 
+/* ---- densification and simplification on device ---------- */
+/* These run every few hundred iterations; each synchronises the context stream once or twice
+ * to read back the scalars the reference's control flow branches on. */
+
+/* quantile_threshold (quantile.hpp:16-28) over the entries of values_dev[n] selected by
+ * sel_dev[i] != 0 (NULL: all entries): the (1 - keep_q) linear-interpolation order statistic,
+ * computed in double from the two neighbouring sorted values.  *count_out = selected entries.
+ * SPLAT_ERR_INVALID_ARGUMENT for an empty selection or keep_q outside (0, 1), as the reference
+ * throws std::invalid_argument. */
+int splat_quantile_threshold(splat_ctx* ctx, const float* values_dev, const uint8_t* sel_dev, int32_t n,
+                             double keep_q, float* tau_out, int32_t* count_out);
+int splat_quantile_threshold_f64(splat_ctx* ctx, const double* values_dev, const uint8_t* sel_dev, int32_t n,
+                                 double keep_q, double* tau_out, int32_t* count_out);
+
+/* build_masks (visibility.cpp:9-37), one view: from that view's accumulate_importance
+ * importance_dev[n], mask_dev[n] = importance > tau with tau the keep_q quantile over the
+ * strictly positive importances; when nothing exceeds tau every positive entry is kept; all
+ * zero when nothing is positive.  The byte mask is what splat_render / accumulate_importance
+ * take as `mask` (VisibilityTable::mask_for). */
+int splat_visibility_mask(splat_ctx* ctx, const float* importance_dev, int32_t n, double keep_q, uint8_t* mask_dev);
+
+/* identify_critical (densify.cpp:32-103) from the per-view statistics accumulated by
+ * splat_visibility_update_max over the views: best_weight_dev (max over views of max_weight),
+ * max_count_sum_dev (sum over views of max_pixel_count: > 0 iff "ever the max contributor")
+ * and summed_importance_dev (fp64).  MaxWeight: critical = ever_max && best > tau (tau the keep_q
+ * quantile over the ever_max candidates, keep-all edge rule); the other criteria take the same
+ * count of Gaussians by score, descending, ties by index: opacity (float sigmoid), summed
+ * importance, or caller-drawn random_scores_dev (the reference draws uniform doubles from its
+ * std::mt19937).  critical_dev[n] bytes (0/1); *count_out = CriticalSelection::count. */
+#define SPLAT_CRITERION_RANDOM 0
+#define SPLAT_CRITERION_OPACITY 1
+#define SPLAT_CRITERION_ACCUM_WEIGHT 2
+#define SPLAT_CRITERION_MAX_WEIGHT 3
+int splat_identify_critical(splat_ctx* ctx, const splat_gaussians* g, const float* best_weight_dev,
+                            const int64_t* max_count_sum_dev, const double* summed_importance_dev, int criterion,
+                            double keep_q, const double* random_scores_dev, uint8_t* critical_dev,
+                            int32_t* count_out);
+
+/* aggressive_clone + apply_densify_plan (densify.cpp:105-130, 159-195), in place: p holds p->n
+ * rows in arrays with room for `capacity` rows.  Every critical row with opacity > 1e-7 gets
+ * alpha_new = 1 - sqrt(1 - alpha) (alpha clamped to 1 - 1e-7), opacity logit(alpha_new) and
+ * log-scales + ln(k)/2, and an identical copy is appended, in index order.
+ * moment_source_dev[new n]: old row for Adam moments, -1 = zeroed (both copies of a clone and
+ * every appended row).  *n_out = new row count.  SPLAT_ERR_INVALID_ARGUMENT when capacity is too
+ * small (*n_out then = the rows needed; nothing is modified). */
+int splat_aggressive_clone(splat_ctx* ctx, const splat_params_mut* p, int64_t capacity, const uint8_t* critical_dev,
+                           int32_t* moment_source_dev, int32_t* n_out);
+
+/* importance_prune (simplify.cpp:94-107): kept_dev = ascending indices with
+ * importance > tau (select_above_quantile over all n entries, keep-all edge rule);
+ * *n_kept = their count.  Follow with splat_gather_rows (GaussianSet::select) and, for Adam,
+ * the same gather of the moments (OptimState::keep). */
+int splat_importance_prune(splat_ctx* ctx, const double* importance_dev, int32_t n, double keep_q, int32_t* kept_dev,
+                           int32_t* n_kept);
+
+/* Row gather: dst[r][c] = src[source[r]][c] for r < n_rows, c < width; source[r] < 0 gives a zero
+ * row (OptimState::remap, optimizer.cpp:73-108; GaussianSet::select, gaussian_set.hpp:96-110).
+ * src and dst must not overlap. */
+int splat_gather_rows(splat_ctx* ctx, const float* src_dev, int32_t width, const int32_t* source_dev, int32_t n_rows,
+                      float* dst_dev);
+
 /* ---- primitives (exposed for tests and microbenchmarks) ------------------------------ */
 /* Stable LSD radix sort of (keys, vals) on key bits [begin_bit, end_bit), n pairs, device
  * pointers; the result lands in keys/vals or, when *result_in_alt, in keys_alt/vals_alt. */

@@ -100,4 +100,80 @@ SPLAT_HD float splat_expf_core(float x) {
     return splat_mul(p, splat_bits_to_float((uint32_t)((int)kf + 127) << 23));
 }
 
+SPLAT_HD float splat_add(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+
+SPLAT_HD float splat_sub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+
+SPLAT_HD float splat_div(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fdiv_rn(a, b);
+#else
+    return a / b;
+#endif
+}
+
+SPLAT_HD uint32_t splat_float_to_bits(float f) {
+#if defined(__CUDA_ARCH__)
+    return __float_as_uint(f);
+#else
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+#endif
+}
+
+/* The one natural logarithm shared by the CUDA kernels and the mode-B oracle (the reference
+ * calls std::log(float) in aggressive_clone and logit, densify.cpp:116-121, types.hpp:63-65).
+ * The classic fdlibm/FreeBSD logf scheme: x = 2^k (1 + f) with 1 + f in [sqrt(2)/2, sqrt(2)),
+ * s = f / (2 + f), log(1 + f) = f - (f^2/2 - s (f^2/2 + R(s^2))) with the published minimax
+ * coefficients, and k ln2 split hi/lo.  Only correctly rounded +, -, *, / (no contraction), so
+ * gcc and nvcc agree bit for bit.  Accuracy: < 1 ulp (tests/test_expf.py). */
+SPLAT_HD float splat_logf(float x) {
+    const float ln2_hi = 6.9313812256e-01f, ln2_lo = 9.0580006145e-06f;
+    const float Lg1 = 6.6666662693e-01f, Lg2 = 4.0000972152e-01f, Lg3 = 2.8498786688e-01f,
+                Lg4 = 2.4279078841e-01f;
+    uint32_t ix = splat_float_to_bits(x);
+    int k = 0;
+    if (ix < 0x00800000u || (ix >> 31)) {          /* x < 2^-126 (subnormal or 0) or negative */
+        if ((ix & 0x7fffffffu) == 0) return splat_bits_to_float(0xff800000u); /* -inf */
+        if (ix >> 31) return splat_bits_to_float(0x7fc00000u);                 /* NaN */
+        k -= 25;
+        x = splat_mul(x, 33554432.0f);            /* 2^25: exact */
+        ix = splat_float_to_bits(x);
+    } else if (ix >= 0x7f800000u) {
+        return x;                                  /* +inf or NaN */
+    } else if (ix == 0x3f800000u) {
+        return 0.0f;
+    }
+    k += (int)(ix >> 23) - 127;
+    ix &= 0x007fffffu;
+    const uint32_t i = (ix + (0x95f64u << 3)) & 0x800000u;   /* mantissa above sqrt(2): halve */
+    x = splat_bits_to_float(ix | (i ^ 0x3f800000u));
+    k += (int)(i >> 23);
+    const float f = splat_sub(x, 1.0f);
+    const float s = splat_div(f, splat_add(2.0f, f));
+    const float dk = (float)k;
+    const float z = splat_mul(s, s);
+    const float w = splat_mul(z, z);
+    const float t1 = splat_mul(w, splat_add(Lg2, splat_mul(w, Lg4)));
+    const float t2 = splat_mul(z, splat_add(Lg1, splat_mul(w, Lg3)));
+    const float R = splat_add(t2, t1);
+    const float hfsq = splat_mul(splat_mul(0.5f, f), f);
+    /* dk*ln2_hi - ((hfsq - (s*(hfsq+R) + dk*ln2_lo)) - f) */
+    const float inner = splat_add(splat_mul(s, splat_add(hfsq, R)), splat_mul(dk, ln2_lo));
+    return splat_sub(splat_mul(dk, ln2_hi), splat_sub(splat_sub(hfsq, inner), f));
+}
+
 #endif /* SPLAT_EXPF_H */

@@ -418,4 +418,95 @@ int ref_train_view(void* h, const splat_camera* c, const splat_raster_config* cf
     REF_CATCH
 }
 
+// ---- densification / simplification, the reference's own functions ---------
+
+// The uniform draws identify_critical's Random criterion makes from a fresh std::mt19937(seed)
+// (densify.cpp:78-81), exported so the restatement and the GPU can be fed the same scores.
+int ref_random_scores(uint32_t seed, int32_t n, double* out) {
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    for (int i = 0; i < n; ++i) out[i] = u(rng);
+    return 0;
+}
+
+// identify_critical (densify.cpp:32-103); masks: optional [n_cams][n] bytes (VisibilityTable).
+int ref_identify_critical_views(const splat_gaussians* g, const splat_camera* cams, int32_t n_cams,
+                                const splat_raster_config* cf, int criterion, double keep_q, uint32_t seed,
+                                const uint8_t* masks, uint8_t* critical, int32_t* count) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<Camera> cv;
+    for (int k = 0; k < n_cams; ++k) cv.push_back(to_cam(&cams[k]));
+    VisibilityTable table;
+    if (masks) {
+        table.gaussian_count = g->n;
+        for (int k = 0; k < n_cams; ++k)
+            table.masks.emplace_back(masks + (size_t)k * g->n, masks + (size_t)(k + 1) * g->n);
+    }
+    std::mt19937 rng(seed);
+    const IdentCriterion crit = criterion == SPLAT_CRITERION_RANDOM    ? IdentCriterion::Random
+                                : criterion == SPLAT_CRITERION_OPACITY ? IdentCriterion::Opacity
+                                : criterion == SPLAT_CRITERION_ACCUM_WEIGHT ? IdentCriterion::AccumWeight
+                                                                            : IdentCriterion::MaxWeight;
+    const CriticalSelection sel = identify_critical(set, cv, crit, keep_q, to_cfg(cf), rng, masks ? &table : nullptr);
+    for (int i = 0; i < g->n; ++i) critical[i] = sel.critical[i] ? 1 : 0;
+    *count = sel.count;
+    return 0;
+    REF_CATCH
+}
+
+// aggressive_clone + apply_densify_plan (densify.cpp:105-130, 159-195): the applied set written
+// to the output arrays (capacity rows), moment_source, new row count.
+int ref_aggressive_clone_apply(const splat_gaussians* g, const uint8_t* critical, float* centers, float* log_scales,
+                         float* rotations, float* opacity_logits, float* sh, int64_t capacity,
+                         int32_t* moment_source, int32_t* n_out) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<char> crit(critical, critical + g->n);
+    const DensifyPlan plan = aggressive_clone(set, crit);
+    const DensifyApplied out = apply_densify_plan(set, plan);
+    const int m = out.set.size();
+    *n_out = m;
+    if (m > capacity) throw std::invalid_argument("ref_aggressive_clone: capacity");
+    for (int i = 0; i < m; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            centers[3 * i + c] = out.set.centers[i][c];
+            log_scales[3 * i + c] = out.set.log_scales[i][c];
+        }
+        for (int c = 0; c < 4; ++c) rotations[4 * i + c] = out.set.rotations[i][c];
+        opacity_logits[i] = out.set.opacity_logits[i];
+        moment_source[i] = out.moment_source[i];
+    }
+    if (m > 0) std::memcpy(sh, out.set.sh.data(), sizeof(float) * 48 * static_cast<size_t>(m));
+    return 0;
+    REF_CATCH
+}
+
+// build_masks (visibility.cpp:9-37): masks [n_cams][n] bytes.
+int ref_build_masks(const splat_gaussians* g, const splat_camera* cams, int32_t n_cams, const splat_raster_config* cf,
+                    double keep_q, uint8_t* masks) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<Camera> cv;
+    for (int k = 0; k < n_cams; ++k) cv.push_back(to_cam(&cams[k]));
+    const VisibilityTable t = build_masks(set, cv, keep_q, to_cfg(cf));
+    for (int k = 0; k < n_cams; ++k)
+        for (int i = 0; i < g->n; ++i) masks[(size_t)k * g->n + i] = t.masks[k][i] ? 1 : 0;
+    return 0;
+    REF_CATCH
+}
+
+// importance_prune (simplify.cpp:94-107) on a set of n rows: the kept indices.
+int ref_importance_prune_set(const splat_gaussians* g, const double* importance, double keep_q, int32_t* kept,
+                         int32_t* n_kept) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<double> imp(importance, importance + g->n);
+    const SimplifyResult r = importance_prune(set, imp, keep_q);
+    for (size_t k = 0; k < r.kept.size(); ++k) kept[k] = r.kept[k];
+    *n_kept = static_cast<int32_t>(r.kept.size());
+    return 0;
+    REF_CATCH
+}
+
 }  // extern "C"

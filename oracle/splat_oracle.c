@@ -19,8 +19,10 @@
 
 #ifdef ORACLE_USE_LIBM_EXP
 #define EXP expf
+#define LOG logf
 #else
 #define EXP splat_expf
+#define LOG splat_logf
 #endif
 
 static char g_err[256];
@@ -859,3 +861,207 @@ int ORACLE_FN(unproject)(const splat_camera* cam, const int32_t* max_contributor
     *count = cnt;
     return 0;
 }
+
+/* ---- densification and simplification ----------------- */
+static int cmp_f32(const void* a, const void* b) {
+    const float x = *(const float*)a, y = *(const float*)b;
+    return (x > y) - (x < y);
+}
+static int cmp_f64(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+
+/* quantile_threshold (quantile.hpp:16-28): sort, linear interpolation in double. */
+int ORACLE_FN(quantile_threshold)(const float* values, const uint8_t* sel, int32_t n, double keep_q, float* tau,
+                                  int32_t* count) {
+    if (!(keep_q > 0.0 && keep_q < 1.0)) return fail(SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: keep_q");
+    float* v = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    int32_t m = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (!sel || sel[i]) v[m++] = values[i];
+    if (count) *count = m;
+    if (m == 0) {
+        free(v);
+        return fail(SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: empty input");
+    }
+    qsort(v, (size_t)m, sizeof(float), cmp_f32);
+    const double q = 1.0 - keep_q;
+    const double h = q * (double)(m - 1);
+    const size_t lo = (size_t)floor(h);
+    const size_t hi = lo + 1 < (size_t)m - 1 ? lo + 1 : (size_t)m - 1;
+    const double frac = h - (double)lo;
+    *tau = (float)((double)v[lo] + frac * ((double)v[hi] - (double)v[lo]));
+    free(v);
+    return 0;
+}
+
+int ORACLE_FN(quantile_threshold_f64)(const double* values, const uint8_t* sel, int32_t n, double keep_q,
+                                      double* tau, int32_t* count) {
+    if (!(keep_q > 0.0 && keep_q < 1.0)) return fail(SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: keep_q");
+    double* v = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int32_t m = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (!sel || sel[i]) v[m++] = values[i];
+    if (count) *count = m;
+    if (m == 0) {
+        free(v);
+        return fail(SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: empty input");
+    }
+    qsort(v, (size_t)m, sizeof(double), cmp_f64);
+    const double q = 1.0 - keep_q;
+    const double h = q * (double)(m - 1);
+    const size_t lo = (size_t)floor(h);
+    const size_t hi = lo + 1 < (size_t)m - 1 ? lo + 1 : (size_t)m - 1;
+    const double frac = h - (double)lo;
+    *tau = v[lo] + frac * (v[hi] - v[lo]);
+    free(v);
+    return 0;
+}
+
+/* build_masks, one view (visibility.cpp:15-35). */
+int ORACLE_FN(visibility_mask)(const float* importance, int32_t n, double keep_q, uint8_t* mask) {
+    uint8_t* pos = (uint8_t*)malloc((size_t)(n > 0 ? n : 1));
+    int any_pos = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        pos[i] = importance[i] > 0.0f;
+        any_pos |= pos[i];
+        mask[i] = 0;
+    }
+    if (any_pos) {
+        float tau;
+        int rc = ORACLE_FN(quantile_threshold)(importance, pos, n, keep_q, &tau, NULL);
+        if (rc) {
+            free(pos);
+            return rc;
+        }
+        int any = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            mask[i] = importance[i] > tau;
+            any |= mask[i];
+        }
+        if (!any)
+            for (int32_t i = 0; i < n; ++i) mask[i] = importance[i] > 0.0f;
+    }
+    free(pos);
+    return 0;
+}
+
+typedef struct {
+    double score;
+    int32_t idx;
+} scored_t;
+static int cmp_scored(const void* a, const void* b) { /* densify.cpp:96-99: score desc, index asc */
+    const scored_t* x = (const scored_t*)a;
+    const scored_t* y = (const scored_t*)b;
+    if (x->score != y->score) return x->score > y->score ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+/* identify_critical (densify.cpp:32-103) from the per-view statistics (best weight = max over
+ * views of max_weight, max_count_sum > 0 = ever the max contributor, fp64 summed importance). */
+int ORACLE_FN(identify_critical)(const splat_gaussians* g, const float* best, const int64_t* max_count_sum,
+                                 const double* summed, int criterion, double keep_q, const double* random,
+                                 uint8_t* critical, int32_t* count_out) {
+    const int32_t n = g->n;
+    *count_out = 0;
+    uint8_t* ever = (uint8_t*)malloc((size_t)(n > 0 ? n : 1));
+    int32_t m = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        ever[i] = max_count_sum[i] > 0;
+        m += ever[i];
+        critical[i] = 0;
+    }
+    if (m == 0) {
+        free(ever);
+        return 0;
+    }
+    float tau;
+    int rc = ORACLE_FN(quantile_threshold)(best, ever, n, keep_q, &tau, NULL);
+    if (rc) {
+        free(ever);
+        return rc;
+    }
+    int32_t count = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (ever[i] && best[i] > tau) ++count;
+    const int keep_all = count == 0;
+    if (keep_all) count = m;
+    *count_out = count;
+    if (criterion == SPLAT_CRITERION_MAX_WEIGHT) {
+        for (int32_t i = 0; i < n; ++i) critical[i] = ever[i] && (keep_all || best[i] > tau);
+        free(ever);
+        return 0;
+    }
+    scored_t* sc = (scored_t*)malloc(sizeof(scored_t) * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        double s;
+        if (criterion == SPLAT_CRITERION_OPACITY)
+            s = (double)sigmoidf_(g->opacity_logits[i]);
+        else if (criterion == SPLAT_CRITERION_ACCUM_WEIGHT)
+            s = summed[i];
+        else
+            s = random[i];
+        sc[i].score = s;
+        sc[i].idx = i;
+    }
+    qsort(sc, (size_t)n, sizeof(scored_t), cmp_scored);
+    for (int32_t r = 0; r < count; ++r) critical[sc[r].idx] = 1;
+    free(sc);
+    free(ever);
+    return 0;
+}
+
+/* aggressive_clone + apply_densify_plan (densify.cpp:105-130, 159-195) on arrays with room for
+ * capacity rows; same contract as splat_aggressive_clone. */
+int ORACLE_FN(aggressive_clone)(float* centers, float* log_scales, float* rotations, float* opacity_logits, float* sh,
+                                int32_t n, int64_t capacity, const uint8_t* critical, int32_t* moment_source,
+                                int32_t* n_out) {
+    int32_t clones = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (critical[i] && sigmoidf_(opacity_logits[i]) > 1e-7f) ++clones;
+    *n_out = n + clones;
+    if ((int64_t)n + clones > capacity) return fail(SPLAT_ERR_INVALID_ARGUMENT, "aggressive_clone: capacity");
+    const float sqrt2 = sqrtf(2.f);
+    int32_t j = n;
+    for (int32_t i = 0; i < n; ++i) {
+        if (moment_source) moment_source[i] = i;
+        if (!critical[i]) continue;
+        float alpha = sigmoidf_(opacity_logits[i]);
+        if (alpha <= 1e-7f) continue;
+        alpha = fmin_std(alpha, 1.f - 1e-7f);
+        const float alpha_new = 1.f - sqrtf(1.f - alpha);
+        const float denom = 2.f * alpha_new - alpha_new * alpha_new / sqrt2;
+        const float k = (alpha * alpha) / (denom * denom);
+        const float shift = 0.5f * LOG(k);
+        const float logit_new = LOG(alpha_new / (1.f - alpha_new)); /* logit, types.hpp:63-65 */
+        opacity_logits[i] = logit_new;
+        for (int c = 0; c < 3; ++c) log_scales[3 * i + c] = log_scales[3 * i + c] + shift;
+        if (moment_source) {
+            moment_source[i] = -1;
+            moment_source[j] = -1;
+        }
+        memcpy(centers + 3 * (size_t)j, centers + 3 * (size_t)i, 12);
+        memcpy(log_scales + 3 * (size_t)j, log_scales + 3 * (size_t)i, 12);
+        memcpy(rotations + 4 * (size_t)j, rotations + 4 * (size_t)i, 16);
+        opacity_logits[j] = logit_new;
+        memcpy(sh + 48 * (size_t)j, sh + 48 * (size_t)i, 192);
+        ++j;
+    }
+    return 0;
+}
+
+/* importance_prune (simplify.cpp:94-107): kept = ascending indices selected by
+ * select_above_quantile (quantile.hpp:33-46). */
+int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep_q, int32_t* kept, int32_t* n_kept) {
+    double tau;
+    int rc = ORACLE_FN(quantile_threshold_f64)(importance, NULL, n, keep_q, &tau, NULL);
+    if (rc) return rc;
+    int32_t k = 0, any = 0;
+    for (int32_t i = 0; i < n; ++i) any |= importance[i] > tau;
+    for (int32_t i = 0; i < n; ++i)
+        if (!any || importance[i] > tau) kept[k++] = i;
+    *n_kept = k;
+    return 0;
+}
+

@@ -87,6 +87,20 @@ int ORACLE_FN(unproject)(const splat_camera* cam, const int32_t* max_contributor
                          int64_t seed, float* points, int32_t* pixel, int64_t capacity,
                          int64_t* count);
 
+/* ---- densification / simplification (contracts as in splat_b200.h) ---- */
+int ORACLE_FN(quantile_threshold)(const float* values, const uint8_t* sel, int32_t n, double keep_q, float* tau,
+                                  int32_t* count);
+int ORACLE_FN(quantile_threshold_f64)(const double* values, const uint8_t* sel, int32_t n, double keep_q,
+                                      double* tau, int32_t* count);
+int ORACLE_FN(visibility_mask)(const float* importance, int32_t n, double keep_q, uint8_t* mask);
+int ORACLE_FN(identify_critical)(const splat_gaussians* g, const float* best, const int64_t* max_count_sum,
+                                 const double* summed, int criterion, double keep_q, const double* random,
+                                 uint8_t* critical, int32_t* count_out);
+int ORACLE_FN(aggressive_clone)(float* centers, float* log_scales, float* rotations, float* opacity_logits, float* sh,
+                                int32_t n, int64_t capacity, const uint8_t* critical, int32_t* moment_source,
+                                int32_t* n_out);
+int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep_q, int32_t* kept, int32_t* n_kept);
+
 /* The exp the library was built with (splat_expf or glibc expf). */
 float ORACLE_FN(exp)(float x);
 

@@ -27,6 +27,7 @@ SOURCES = {
     "chain.cu": ["--fmad=false"],
     "binning.cu": [],
     "importance.cu": [],
+    "densify.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

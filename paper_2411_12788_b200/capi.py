@@ -39,6 +39,9 @@ fp = C.POINTER(C.c_float)
 ip = C.POINTER(C.c_int32)
 u8p = C.POINTER(C.c_uint8)
 
+# identify_critical criteria (include/splat_b200.h SPLAT_CRITERION_*, densify.hpp:15)
+CRITERION_RANDOM, CRITERION_OPACITY, CRITERION_ACCUM_WEIGHT, CRITERION_MAX_WEIGHT = 0, 1, 2, 3
+
 
 class Camera(C.Structure):
     """splat_camera — CameraT<float> (camera.hpp:12-22); rotation row-major world->camera."""
@@ -224,6 +227,18 @@ _EXPORTS = {
                                           C.c_void_p, C.c_void_p, C.c_void_p]),
     "splat_visibility_update_max": (C.c_int, [C.c_void_p, C.POINTER(ImportanceOutputs), C.c_int32, C.c_float,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "splat_quantile_threshold": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                                           C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
+    "splat_quantile_threshold_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                                               C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+    "splat_visibility_mask": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p]),
+    "splat_identify_critical": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
+    "splat_aggressive_clone": (C.c_int, [C.c_void_p, C.POINTER(ParamsMut), C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_int32)]),
+    "splat_importance_prune": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
+                                         C.POINTER(C.c_int32)]),
+    "splat_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

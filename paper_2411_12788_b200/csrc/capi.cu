@@ -127,6 +127,8 @@ struct splat_ctx {
     DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_ranges, l2_tmp, st_cover;
     // misc
     DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
+    // densify / simplify scratch (separate from the forward's buffers)
+    DevBuf dkey[2], dval[2], dhi, dflags, doffsets, dscalar;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
@@ -407,6 +409,119 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     st.max_contributor = fo.max_contributor;
     st.valid = true;
     return SPLAT_OK;
+}
+
+// ---- densify / simplify helpers ------------------------------------------
+// Order statistic support: the selected values' orderable keys sorted ascending on device;
+// returns (via *m) the selected count and leaves vals (original indices) in sorted order in
+// ctx->dval[*alt].  64-bit keys (double) sort the low word, then stably the high word.
+int sorted_selection(splat_ctx* ctx, const void* values, bool f64, const uint8_t* sel, int32_t n, int32_t* m_out,
+                     int* alt_out) {
+    LaunchCtx& lc = ctx->lc;
+    cudaStream_t s = ctx->stream;
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    for (int k = 0; k < 2; ++k) {
+        CK(ctx->dkey[k].ensure(nn * 4), "alloc keys");
+        CK(ctx->dval[k].ensure(nn * 4), "alloc vals");
+    }
+    CK(ctx->dhi.ensure(nn * 4), "alloc keys");
+    CK(ctx->dflags.ensure(nn * 4), "alloc flags");
+    CK(ctx->doffsets.ensure((nn + 1) * 4), "alloc offsets");
+    CK(ctx->dscalar.ensure(64), "alloc scalar");
+    CK(ctx->hist.ensure(radix_hist_words(nn, 8) * 4), "alloc hist");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(std::max(nn, radix_hist_words(nn, 8))) + 64) * 4), "alloc scan");
+    uint32_t m = (uint32_t)n;
+    if (sel && n > 0) {
+        CK(launch_flags_from_bytes(lc, sel, n, ctx->dflags.as<uint32_t>()), "flags");
+        uint32_t* total = ctx->dscalar.as<uint32_t>();
+        CK(exclusive_scan_u32(lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), (uint64_t)n,
+                              ctx->scan_tmp.as<uint32_t>(), total),
+           "scan");
+        CK(cudaMemcpyAsync(&m, total, 4, cudaMemcpyDeviceToHost, s), "read count");
+        CK(cudaStreamSynchronize(s), "sync");
+    }
+    *m_out = (int32_t)m;
+    *alt_out = 0;
+    if (m == 0) return SPLAT_OK;
+    uint32_t* k0 = ctx->dkey[0].as<uint32_t>();
+    uint32_t* v0 = ctx->dval[0].as<uint32_t>();
+    if (!f64) {
+        CK(launch_select_keys_f32(lc, static_cast<const float*>(values), sel, n, ctx->doffsets.as<uint32_t>(), k0, v0),
+           "select keys");
+        bool alt = false;
+        CK(radix_sort_pairs(lc, k0, v0, ctx->dkey[1].as<uint32_t>(), ctx->dval[1].as<uint32_t>(), m, 0, 32,
+                            ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
+           "sort");
+        *alt_out = alt ? 1 : 0;
+        return SPLAT_OK;
+    }
+    uint32_t* hi = ctx->dhi.as<uint32_t>();
+    CK(launch_select_keys_f64(lc, static_cast<const double*>(values), sel, n, ctx->doffsets.as<uint32_t>(), k0, hi, v0),
+       "select keys");
+    bool alt = false;
+    CK(radix_sort_pairs(lc, k0, v0, ctx->dkey[1].as<uint32_t>(), ctx->dval[1].as<uint32_t>(), m, 0, 32,
+                        ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
+       "sort lo");
+    const int a = alt ? 1 : 0;
+    // high words in the current order: gather by the original index (select_keys wrote hi at the
+    // compacted position; the original -> compacted map is doffsets, so gather via a second copy)
+    // simpler: rebuild the high words of the sorted entries from the values themselves
+    uint32_t* vcur = ctx->dval[a].as<uint32_t>();
+    uint32_t* kcur = ctx->dkey[a].as<uint32_t>();
+    CK(launch_select_keys_f64(lc, static_cast<const double*>(values), nullptr, n, nullptr, ctx->dkey[1 - a].as<uint32_t>(),
+                              hi, ctx->dval[1 - a].as<uint32_t>()),
+       "all keys");  // hi[i] = high word of values[i] for every original index i
+    CK(launch_gather_u32(lc, hi, vcur, (int)m, kcur), "gather hi");
+    bool alt2 = false;
+    CK(radix_sort_pairs(lc, kcur, vcur, ctx->dkey[1 - a].as<uint32_t>(), ctx->dval[1 - a].as<uint32_t>(), m, 0, 32,
+                        ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt2),
+       "sort hi");
+    *alt_out = alt2 ? 1 - a : a;
+    return SPLAT_OK;
+}
+
+// quantile_threshold's interpolation (quantile.hpp:22-27) from the sorted selection.
+template <typename T>
+int quantile_from_sorted(splat_ctx* ctx, const T* values, int32_t m, int alt, double keep_q, T* tau) {
+    const double q = 1.0 - keep_q;
+    const double h = q * (double)(m - 1);
+    const size_t lo = (size_t)std::floor(h);
+    const size_t hi = std::min(lo + 1, (size_t)m - 1);
+    const double frac = h - (double)lo;
+    uint32_t idx[2];
+    const uint32_t* order = ctx->dval[alt].as<uint32_t>();
+    CK(cudaMemcpyAsync(&idx[0], order + lo, 4, cudaMemcpyDeviceToHost, ctx->stream), "read order");
+    CK(cudaMemcpyAsync(&idx[1], order + hi, 4, cudaMemcpyDeviceToHost, ctx->stream), "read order");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    T v[2];
+    CK(cudaMemcpy(&v[0], values + idx[0], sizeof(T), cudaMemcpyDeviceToHost), "read value");
+    CK(cudaMemcpy(&v[1], values + idx[1], sizeof(T), cudaMemcpyDeviceToHost), "read value");
+    *tau = static_cast<T>(static_cast<double>(v[0]) + frac * (static_cast<double>(v[1]) - static_cast<double>(v[0])));
+    return SPLAT_OK;
+}
+
+template <typename T>
+int quantile_threshold_impl(splat_ctx* ctx, const T* values, const uint8_t* sel, int32_t n, double keep_q, T* tau,
+                            int32_t* count) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (!(keep_q > 0.0 && keep_q < 1.0))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: keep_q must be in (0,1)");
+    if (n < 0 || (n > 0 && !values)) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: bad args");
+    int32_t m = 0;
+    int alt = 0;
+    int rc = sorted_selection(ctx, values, sizeof(T) == 8, sel, n, &m, &alt);
+    if (rc) return rc;
+    if (count) *count = m;
+    if (m == 0) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: empty input");
+    return quantile_from_sorted(ctx, values, m, alt, keep_q, tau);
+}
+
+uint32_t read_u32(splat_ctx* ctx, const uint32_t* dev, int* rc) {
+    uint32_t v = 0;
+    cudaError_t e = cudaMemcpyAsync(&v, dev, 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    *rc = e == cudaSuccess ? SPLAT_OK : cuda_err(ctx, e, "read scalar");
+    return v;
 }
 
 bool state_matches(const splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const uint8_t* mask,
@@ -842,6 +957,171 @@ int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int3
         // depth sort of N keys: 4 passes of 8 bits -> result back in buffer 0
         CK(cudaMemcpy(depth_order, ctx->vals[0].p, 4 * (size_t)st.n_surv, cudaMemcpyDeviceToHost), "copy");
     }
+    return SPLAT_OK;
+}
+
+int splat_quantile_threshold(splat_ctx* ctx, const float* values, const uint8_t* sel, int32_t n, double keep_q,
+                             float* tau_out, int32_t* count_out) {
+    if (!tau_out) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: null output");
+    return quantile_threshold_impl(ctx, values, sel, n, keep_q, tau_out, count_out);
+}
+
+int splat_quantile_threshold_f64(splat_ctx* ctx, const double* values, const uint8_t* sel, int32_t n, double keep_q,
+                                 double* tau_out, int32_t* count_out) {
+    if (!tau_out) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: null output");
+    return quantile_threshold_impl(ctx, values, sel, n, keep_q, tau_out, count_out);
+}
+
+int splat_visibility_mask(splat_ctx* ctx, const float* importance, int32_t n, double keep_q, uint8_t* mask) {
+    if (!ctx || n < 0 || (n > 0 && (!importance || !mask)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "visibility_mask: bad args");
+    if (n == 0) return SPLAT_OK;
+    // positives (visibility.cpp:17-20)
+    CK(ctx->dflags.ensure((size_t)n * 4), "alloc");
+    CK(ctx->dscalar.ensure(64), "alloc");
+    CK(launch_count_above_f32(ctx->lc, importance, nullptr, n, 0.0f, ctx->dscalar.as<uint32_t>()), "count");
+    int rc = 0;
+    const uint32_t pos = read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    if (rc) return rc;
+    if (pos == 0) {
+        CK(cudaMemsetAsync(mask, 0, (size_t)n, ctx->stream), "zero mask");
+        return SPLAT_OK;
+    }
+    // selection = importance > 0, as bytes, via the mask buffer itself
+    CK(launch_visibility_mask(ctx->lc, importance, n, 0.0f, 0, mask), "positive mask");
+    float tau = 0.0f;
+    int32_t m = 0;
+    rc = quantile_threshold_impl(ctx, importance, mask, n, keep_q, &tau, &m);
+    if (rc) return rc;
+    CK(launch_count_above_f32(ctx->lc, importance, nullptr, n, tau, ctx->dscalar.as<uint32_t>()), "count");
+    const uint32_t above = read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    if (rc) return rc;
+    CK(launch_visibility_mask(ctx->lc, importance, n, tau, above == 0 ? 1 : 0, mask), "mask");
+    return SPLAT_OK;
+}
+
+int splat_identify_critical(splat_ctx* ctx, const splat_gaussians* g, const float* best, const int64_t* max_count,
+                            const double* summed, int criterion, double keep_q, const double* random,
+                            uint8_t* critical, int32_t* count_out) {
+    if (!ctx || !g || !critical || !count_out || !best || !max_count)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "identify_critical: bad args");
+    if (criterion < SPLAT_CRITERION_RANDOM || criterion > SPLAT_CRITERION_MAX_WEIGHT)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "identify_critical: unknown criterion");
+    if ((criterion == SPLAT_CRITERION_ACCUM_WEIGHT && !summed) || (criterion == SPLAT_CRITERION_RANDOM && !random) ||
+        (criterion == SPLAT_CRITERION_OPACITY && !g->opacity_logits))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "identify_critical: criterion input missing");
+    const int n = g->n;
+    *count_out = 0;
+    if (n <= 0) return SPLAT_OK;
+    CK(cudaMemsetAsync(critical, 0, (size_t)n, ctx->stream), "zero critical");
+    // candidates: ever the max contributor (densify.cpp:57-60); the selection bytes reuse `critical`
+    CK(launch_ever_max(ctx->lc, max_count, n, critical), "ever max");
+    float tau = 0.0f;
+    int32_t m = 0;
+    int alt = 0;
+    int rc = sorted_selection(ctx, best, false, critical, n, &m, &alt);
+    if (rc) return rc;
+    if (m == 0) {  // no candidates: empty selection, count 0 (densify.cpp:63)
+        CK(cudaMemsetAsync(critical, 0, (size_t)n, ctx->stream), "zero critical");
+        return SPLAT_OK;
+    }
+    if (!(keep_q > 0.0 && keep_q < 1.0))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quantile_threshold: keep_q must be in (0,1)");
+    if ((rc = quantile_from_sorted(ctx, best, m, alt, keep_q, &tau))) return rc;
+    CK(ctx->dscalar.ensure(64), "alloc");
+    CK(launch_count_above_f32(ctx->lc, best, critical, n, tau, ctx->dscalar.as<uint32_t>()), "count");
+    int32_t count = (int32_t)read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    if (rc) return rc;
+    const bool keep_all = count == 0;
+    if (keep_all) count = m;
+    *count_out = count;
+    if (criterion == SPLAT_CRITERION_MAX_WEIGHT) {
+        CK(launch_maxweight_critical(ctx->lc, best, max_count, n, tau, keep_all ? 1 : 0, critical), "critical");
+        return SPLAT_OK;
+    }
+    // score order, descending, ties by index (densify.cpp:96-101): stable LSD over the 64-bit
+    // inverted keys (low word, then high word)
+    LaunchCtx& lc = ctx->lc;
+    const size_t nn = (size_t)n;
+    for (int k = 0; k < 2; ++k) {
+        CK(ctx->dkey[k].ensure(nn * 4), "alloc");
+        CK(ctx->dval[k].ensure(nn * 4), "alloc");
+    }
+    CK(ctx->dhi.ensure(nn * 4), "alloc");
+    uint32_t* hi = ctx->dhi.as<uint32_t>();
+    CK(launch_score_keys(lc, criterion, g->opacity_logits, summed, random, n, ctx->dkey[0].as<uint32_t>(), hi,
+                         ctx->dval[0].as<uint32_t>()),
+       "score keys");
+    bool a1 = false;
+    CK(radix_sort_pairs(lc, ctx->dkey[0].as<uint32_t>(), ctx->dval[0].as<uint32_t>(), ctx->dkey[1].as<uint32_t>(),
+                        ctx->dval[1].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(),
+                        &a1),
+       "sort lo");
+    const int a = a1 ? 1 : 0;
+    CK(launch_gather_u32(lc, hi, ctx->dval[a].as<uint32_t>(), n, ctx->dkey[a].as<uint32_t>()), "gather hi");
+    bool a2 = false;
+    CK(radix_sort_pairs(lc, ctx->dkey[a].as<uint32_t>(), ctx->dval[a].as<uint32_t>(), ctx->dkey[1 - a].as<uint32_t>(),
+                        ctx->dval[1 - a].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(),
+                        ctx->scan_tmp.as<uint32_t>(), &a2),
+       "sort hi");
+    const int fin = a2 ? 1 - a : a;
+    CK(cudaMemsetAsync(critical, 0, (size_t)n, ctx->stream), "zero critical");
+    CK(launch_mark_first(lc, ctx->dval[fin].as<uint32_t>(), count, critical), "mark");
+    return SPLAT_OK;
+}
+
+int splat_aggressive_clone(splat_ctx* ctx, const splat_params_mut* p, int64_t capacity, const uint8_t* critical,
+                           int32_t* moment_source, int32_t* n_out) {
+    if (!ctx || !p || !n_out || (p->n > 0 && (!critical || !p->centers || !p->log_scales || !p->rotations ||
+                                               !p->opacity_logits || !p->sh)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "aggressive_clone: bad args");
+    const int n = p->n;
+    *n_out = n;
+    if (n <= 0) return SPLAT_OK;
+    CK(ctx->dflags.ensure((size_t)n * 4), "alloc");
+    CK(ctx->doffsets.ensure(((size_t)n + 1) * 4), "alloc");
+    CK(ctx->dscalar.ensure(64), "alloc");
+    CK(ctx->scan_tmp.ensure((scan_temp_words((uint64_t)n) + 64) * 4), "alloc");
+    CK(launch_clone_flags(ctx->lc, p->opacity_logits, critical, n, ctx->dflags.as<uint32_t>()), "clone flags");
+    CK(exclusive_scan_u32(ctx->lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), (uint64_t)n,
+                          ctx->scan_tmp.as<uint32_t>(), ctx->dscalar.as<uint32_t>()),
+       "clone scan");
+    int rc = 0;
+    const uint32_t clones = read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    if (rc) return rc;
+    const int64_t need = (int64_t)n + clones;
+    *n_out = (int32_t)need;
+    if (need > capacity) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "aggressive_clone: capacity too small");
+    CK(launch_clone_apply(ctx->lc, *p, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), n, moment_source),
+       "clone apply");
+    return SPLAT_OK;
+}
+
+int splat_importance_prune(splat_ctx* ctx, const double* importance, int32_t n, double keep_q, int32_t* kept,
+                           int32_t* n_kept) {
+    if (!ctx || !n_kept || n < 0 || (n > 0 && (!importance || !kept)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "importance_prune: bad args");
+    double tau = 0.0;
+    int32_t m = 0;
+    int rc = quantile_threshold_impl(ctx, importance, nullptr, n, keep_q, &tau, &m);  // throws on n == 0 too
+    if (rc) return rc;
+    CK(launch_count_above_f64(ctx->lc, importance, nullptr, n, tau, ctx->dscalar.as<uint32_t>()), "count");
+    const uint32_t above = read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    if (rc) return rc;
+    CK(launch_keep_flags(ctx->lc, importance, n, tau, above == 0 ? 1 : 0, ctx->dflags.as<uint32_t>()), "keep");
+    CK(exclusive_scan_u32(ctx->lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), (uint64_t)n,
+                          ctx->scan_tmp.as<uint32_t>(), ctx->dscalar.as<uint32_t>()),
+       "keep scan");
+    CK(launch_compact_index(ctx->lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), n, kept), "compact");
+    *n_kept = (int32_t)read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    return rc;
+}
+
+int splat_gather_rows(splat_ctx* ctx, const float* src, int32_t width, const int32_t* source, int32_t n_rows,
+                      float* dst) {
+    if (!ctx || width <= 0 || n_rows < 0 || (n_rows > 0 && (!src || !source || !dst)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "gather_rows: bad args");
+    CK(launch_gather_rows(ctx->lc, src, width, source, n_rows, dst), "gather rows");
     return SPLAT_OK;
 }
 

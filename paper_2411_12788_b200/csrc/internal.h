@@ -177,4 +177,29 @@ cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, dou
                         double bias1, double bias2);
 cudaError_t launch_quat_normalize(LaunchCtx& lc, float* rotations, int n);
 
+// densify.cu: selection keys, counts, masks, critical flags, clone, gathers.
+cudaError_t launch_select_keys_f32(LaunchCtx& lc, const float* v, const uint8_t* sel, int n, const uint32_t* offsets,
+                                   uint32_t* key, uint32_t* vals);
+cudaError_t launch_select_keys_f64(LaunchCtx& lc, const double* v, const uint8_t* sel, int n,
+                                   const uint32_t* offsets, uint32_t* key_lo, uint32_t* key_hi, uint32_t* vals);
+cudaError_t launch_flags_from_bytes(LaunchCtx& lc, const uint8_t* sel, int n, uint32_t* flags);
+cudaError_t launch_gather_u32(LaunchCtx& lc, const uint32_t* src, const uint32_t* idx, int n, uint32_t* dst);
+cudaError_t launch_count_above_f32(LaunchCtx& lc, const float* v, const uint8_t* sel, int n, float tau, uint32_t* out);
+cudaError_t launch_count_above_f64(LaunchCtx& lc, const double* v, const uint8_t* sel, int n, double tau,
+                                   uint32_t* out);
+cudaError_t launch_visibility_mask(LaunchCtx& lc, const float* imp, int n, float tau, int keep_all, uint8_t* mask);
+cudaError_t launch_maxweight_critical(LaunchCtx& lc, const float* best, const int64_t* max_count, int n, float tau,
+                                      int keep_all, uint8_t* critical);
+cudaError_t launch_ever_max(LaunchCtx& lc, const int64_t* max_count, int n, uint8_t* ever);
+cudaError_t launch_score_keys(LaunchCtx& lc, int criterion, const float* logits, const double* summed,
+                              const double* random, int n, uint32_t* key_lo, uint32_t* key_hi, uint32_t* vals);
+cudaError_t launch_mark_first(LaunchCtx& lc, const uint32_t* order, int count, uint8_t* critical);
+cudaError_t launch_clone_flags(LaunchCtx& lc, const float* logits, const uint8_t* critical, int n, uint32_t* flags);
+cudaError_t launch_clone_apply(LaunchCtx& lc, const splat_params_mut& p, const uint32_t* flags, const uint32_t* rank,
+                               int n, int32_t* moment_source);
+cudaError_t launch_keep_flags(LaunchCtx& lc, const double* v, int n, double tau, int keep_all, uint32_t* flags);
+cudaError_t launch_compact_index(LaunchCtx& lc, const uint32_t* flags, const uint32_t* offsets, int n, int32_t* out);
+cudaError_t launch_gather_rows(LaunchCtx& lc, const float* src, int width, const int32_t* source, int n_rows,
+                               float* dst);
+
 }  // namespace splat_b200

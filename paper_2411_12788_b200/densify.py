@@ -1,0 +1,214 @@
+"""On-device densification and simplification, mirroring the
+reference's API over the C-ABI (include/splat_b200.h):
+
+  build_masks          visibility.cpp:9-37       per-view quantile masks (VisibilityTable)
+  view_statistics      densify.cpp:41-53         max blend weight / ever-max / summed importance
+  identify_critical    densify.cpp:32-103        MaxWeight, Opacity, AccumWeight, Random criteria
+  aggressive_clone     densify.cpp:105-130 + apply_densify_plan densify.cpp:159-195
+  importance_prune     simplify.cpp:94-107       select_above_quantile on global importance
+  select / remap       gaussian_set.hpp:96-110, OptimState::remap optimizer.cpp:73-108
+  quantile_threshold   quantile.hpp:16-28
+
+Everything per Gaussian runs in CUDA (csrc/densify.cu + the radix sort); the host reads back
+only the scalars the reference's control flow branches on.  No CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+from . import capi
+from .capi import ImportanceOutputs, RasterConfig, as_fp, as_ip
+from .rasterizer import Context, DeviceGaussians, OptimState, _device_set, _torch
+
+CRITERIA = {"random": capi.CRITERION_RANDOM, "opacity": capi.CRITERION_OPACITY,
+            "accum-weight": capi.CRITERION_ACCUM_WEIGHT, "max-weight": capi.CRITERION_MAX_WEIGHT}
+
+
+def _crit(criterion) -> int:
+    """ident_criterion_from_string (densify.cpp:14-20) or an int."""
+    if isinstance(criterion, str):
+        if criterion not in CRITERIA:
+            raise ValueError(f"unknown identification criterion: {criterion}")
+        return CRITERIA[criterion]
+    return int(criterion)
+
+
+def quantile_threshold(values, keep_q: float, sel=None, ctx: Optional[Context] = None):
+    """quantile_threshold over a CUDA float32 / float64 tensor (entries with sel != 0). Returns
+    (tau, selected count)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    ctx.bind_stream()
+    cnt = C.c_int32()
+    sp = sel.data_ptr() if sel is not None else None
+    if values.dtype == torch.float64:
+        tau = C.c_double()
+        ctx.check(ctx.lib.splat_quantile_threshold_f64(ctx.h, values.data_ptr(), sp, values.numel(), keep_q,
+                                                       C.byref(tau), C.byref(cnt)))
+    else:
+        tau = C.c_float()
+        ctx.check(ctx.lib.splat_quantile_threshold(ctx.h, values.data_ptr(), sp, values.numel(), keep_q,
+                                                   C.byref(tau), C.byref(cnt)))
+    return tau.value, cnt.value
+
+
+class _Report:
+    def __init__(self, n, dev):
+        torch = _torch()
+        self.importance = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+        self.max_weight = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+        self.max_pixel_count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        self.struct = ImportanceOutputs(as_fp(self.importance.data_ptr()), as_fp(self.max_weight.data_ptr()),
+                                        as_ip(self.max_pixel_count.data_ptr()))
+
+
+def build_masks(set_, cams: Sequence[capi.Camera], keep_q: float, cfg: Optional[RasterConfig] = None,
+                ctx: Optional[Context] = None):
+    """build_masks: [views, n] uint8 CUDA tensor, row k = VisibilityTable::mask_for(k)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    cfg = cfg or RasterConfig()
+    ds, _ = _device_set(set_, ctx.device)
+    n, dev = ds.n, f"cuda:{ctx.device}"
+    masks = torch.zeros((len(cams), max(n, 1)), dtype=torch.uint8, device=dev)
+    rep = _Report(n, dev)
+    g = ds.struct()
+    ctx.bind_stream()
+    for k, cam in enumerate(cams):
+        ctx.check(ctx.lib.splat_accumulate_importance(ctx.h, C.byref(g), C.byref(cam), C.byref(cfg), None,
+                                                      C.byref(rep.struct)))
+        ctx.check(ctx.lib.splat_visibility_mask(ctx.h, rep.importance.data_ptr(), n, keep_q, masks[k].data_ptr()))
+    return masks[:, :n]
+
+
+def view_statistics(set_, cams: Sequence[capi.Camera], cfg: Optional[RasterConfig] = None, masks=None,
+                    ctx: Optional[Context] = None):
+    """The per-view folds identify_critical makes (densify.cpp:41-53): (best_weight f32 = max over
+    views of max_weight, max_count_sum i64 (> 0 iff ever the max contributor), summed importance
+    f64), with optional per-view masks ([views, n] uint8 CUDA, as VisibilityTable)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    cfg = cfg or RasterConfig()
+    ds, _ = _device_set(set_, ctx.device)
+    n, dev = ds.n, f"cuda:{ctx.device}"
+    best = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    summed = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+    rep = _Report(n, dev)
+    g = ds.struct()
+    ctx.bind_stream()
+    for k, cam in enumerate(cams):
+        mp = capi.as_u8p(masks[k].data_ptr()) if masks is not None else None
+        ctx.check(ctx.lib.splat_accumulate_importance(ctx.h, C.byref(g), C.byref(cam), C.byref(cfg), mp,
+                                                      C.byref(rep.struct)))
+        ctx.check(ctx.lib.splat_visibility_update_max(ctx.h, C.byref(rep.struct), n, 0.0, None, summed.data_ptr(),
+                                                      cnt.data_ptr(), best.data_ptr()))
+    return best[:n], cnt[:n], summed[:n]
+
+
+def identify_critical(set_, cams: Sequence[capi.Camera], criterion="max-weight", keep_q: float = 0.5,
+                      cfg: Optional[RasterConfig] = None, random_scores=None, masks=None, stats=None,
+                      ctx: Optional[Context] = None):
+    """identify_critical.  Returns (critical uint8 CUDA tensor [n], CriticalSelection::count).
+    random_scores: float64 CUDA tensor [n] for the Random criterion (the reference draws them from
+    its std::mt19937).  stats: precomputed view_statistics (e.g. gathered across ranks by
+    multiview.importance_views)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    ds, _ = _device_set(set_, ctx.device)
+    c = _crit(criterion)
+    best, cnt, summed = stats if stats is not None else view_statistics(ds, cams, cfg, masks, ctx)
+    crit = torch.zeros(max(ds.n, 1), dtype=torch.uint8, device=f"cuda:{ctx.device}")
+    count = C.c_int32()
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_identify_critical(ctx.h, C.byref(ds.struct()), best.data_ptr(), cnt.data_ptr(),
+                                              summed.data_ptr(), c, keep_q,
+                                              random_scores.data_ptr() if random_scores is not None else None,
+                                              crit.data_ptr(), C.byref(count)))
+    return crit[:ds.n], count.value
+
+
+def _grow(params: DeviceGaussians, capacity: int) -> DeviceGaussians:
+    """Copy of params in a layout with room for `capacity` rows (first params.n rows filled)."""
+    out = DeviceGaussians(capacity, params.active_sh_degree, params.flat.device.index or 0)
+    n = params.n
+    out.centers[:n].copy_(params.centers)
+    out.log_scales[:n].copy_(params.log_scales)
+    out.rotations[:n].copy_(params.rotations)
+    out.opacity_logits[:n].copy_(params.opacity_logits)
+    out.sh[:n].copy_(params.sh)
+    return out
+
+
+def aggressive_clone(params: DeviceGaussians, critical, ctx: Optional[Context] = None):
+    """aggressive_clone + apply_densify_plan.  Returns (new DeviceGaussians, moment_source int32
+    CUDA tensor) — feed moment_source to OptimState.remap."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    ctx.bind_stream()
+    n = params.n
+    n_out = C.c_int32()
+    dev = f"cuda:{ctx.device}"
+    # the row count the plan needs (the call returns it without modifying anything when short)
+    rc = ctx.lib.splat_aggressive_clone(ctx.h, C.byref(params.mut()), n, critical.data_ptr(), None, C.byref(n_out))
+    if rc not in (0, 1):
+        ctx.check(rc)
+    need = n_out.value
+    grown = _grow(params, need) if need > n else params
+    p = grown.mut()
+    p.n = n
+    ms = torch.empty(max(need, 1), dtype=torch.int32, device=dev)
+    ctx.check(ctx.lib.splat_aggressive_clone(ctx.h, C.byref(p), need, critical.data_ptr(), ms.data_ptr(),
+                                             C.byref(n_out)))
+    return grown, ms[:need]
+
+
+def select(params: DeviceGaussians, keep, n_rows: Optional[int] = None, ctx: Optional[Context] = None):
+    """GaussianSetT::select with a CUDA int32 index tensor (or the first n_rows when keep is None)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    if keep is None:
+        keep = torch.arange(n_rows, dtype=torch.int32, device=params.flat.device)
+    m = int(keep.numel())
+    out = DeviceGaussians(m, params.active_sh_degree, params.flat.device.index or 0)
+    ctx.bind_stream()
+    for src, dst, w in ((params.centers, out.centers, 3), (params.log_scales, out.log_scales, 3),
+                        (params.rotations, out.rotations, 4), (params.opacity_logits, out.opacity_logits, 1),
+                        (params.sh, out.sh, 48)):
+        ctx.check(ctx.lib.splat_gather_rows(ctx.h, src.data_ptr(), w, keep.data_ptr(), m, dst.data_ptr()))
+    return out
+
+
+def remap(opt: OptimState, source, ctx: Optional[Context] = None) -> None:
+    """OptimState::remap (optimizer.cpp:73-108): row r of every moment array takes old row
+    source[r]; source[r] < 0 gives zero moments.  OptimState::keep is remap with kept indices."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    n_old, n_new = opt.n, int(source.numel())
+    dev = opt.m.device
+    m = torch.zeros(max(59 * n_new, 1), dtype=torch.float32, device=dev)
+    v = torch.zeros(max(59 * n_new, 1), dtype=torch.float32, device=dev)
+    ctx.bind_stream()
+    o_old = o_new = 0
+    for w in (3, 3, 4, 1, 48):
+        for src, dst in ((opt.m, m), (opt.v, v)):
+            ctx.check(ctx.lib.splat_gather_rows(ctx.h, src.data_ptr() + 4 * o_old, w, source.data_ptr(), n_new,
+                                                dst.data_ptr() + 4 * o_new))
+        o_old += w * n_old
+        o_new += w * n_new
+    opt.m, opt.v, opt.n = m, v, n_new
+
+
+def importance_prune(params: DeviceGaussians, importance, keep_q: float, ctx: Optional[Context] = None):
+    """importance_prune on a float64 CUDA importance tensor (e.g. global importance).  Returns
+    (kept DeviceGaussians, kept indices int32 CUDA tensor)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    n = params.n
+    kept = torch.empty(max(n, 1), dtype=torch.int32, device=params.flat.device)
+    nk = C.c_int32()
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_importance_prune(ctx.h, importance.data_ptr(), n, keep_q, kept.data_ptr(), C.byref(nk)))
+    kept = kept[: nk.value]
+    return select(params, kept, ctx=ctx), kept

@@ -84,6 +84,13 @@ class OracleLib:
                                           C.POINTER(AdamConfig), ip, C.c_uint32]
             getattr(L, p + "unproject").argtypes = [CAM, ip, fp, fp, C.c_int, C.c_float, C.c_int64, C.c_int32,
                                           C.c_int64, fp, ip, C.c_int64, i64p]
+            dp = C.POINTER(C.c_double)
+            getattr(L, p + "quantile_threshold").argtypes = [fp, u8p, C.c_int32, C.c_double, fp, ip]
+            getattr(L, p + "quantile_threshold_f64").argtypes = [dp, u8p, C.c_int32, C.c_double, dp, ip]
+            getattr(L, p + "visibility_mask").argtypes = [fp, C.c_int32, C.c_double, u8p]
+            getattr(L, p + "identify_critical").argtypes = [G, fp, i64p, dp, C.c_int, C.c_double, dp, u8p, ip]
+            getattr(L, p + "aggressive_clone").argtypes = [fp, fp, fp, fp, fp, C.c_int32, C.c_int64, u8p, ip, ip]
+            getattr(L, p + "importance_prune").argtypes = [dp, C.c_int32, C.c_double, ip, ip]
         else:
             getattr(L, p + "adam_steps").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp,
                                            C.POINTER(AdamConfig), C.c_int32]
@@ -91,6 +98,12 @@ class OracleLib:
             dp = C.POINTER(C.c_double)
             getattr(L, p + "render_backward_f64").argtypes = [G, CAM, CFG, fp, u8p, fp, dp, dp, dp, dp, dp]
             getattr(L, p + "global_importance").argtypes = [G, CAM, C.c_int32, CFG, C.POINTER(C.c_double), ip]
+            getattr(L, p + "random_scores").argtypes = [C.c_uint32, C.c_int32, dp]
+            getattr(L, p + "identify_critical_views").argtypes = [G, CAM, C.c_int32, CFG, C.c_int, C.c_double,
+                                                                  C.c_uint32, u8p, u8p, ip]
+            getattr(L, p + "aggressive_clone_apply").argtypes = [G, u8p, fp, fp, fp, fp, fp, C.c_int64, ip, ip]
+            getattr(L, p + "build_masks").argtypes = [G, CAM, C.c_int32, CFG, C.c_double, u8p]
+            getattr(L, p + "importance_prune_set").argtypes = [G, dp, C.c_double, ip, ip]
 
     def fn(self, name):
         return getattr(self.lib, self.p + name)
@@ -264,3 +277,109 @@ class OracleLib:
         self.check(self.fn("global_importance")(C.byref(gv.struct), arr, len(cams), C.byref(cfg),
                                                 acc.ctypes.data_as(C.POINTER(C.c_double)), _ptr(cnt, ip)))
         return acc, cnt
+
+    # ---- densification / simplification -----------------------------------
+    def quantile_threshold(self, values, keep_q, sel=None):
+        v = np.ascontiguousarray(values)
+        sel = None if sel is None else np.ascontiguousarray(sel, np.uint8)
+        cnt = C.c_int32()
+        if v.dtype == np.float64:
+            tau = C.c_double()
+            self.check(self.fn("quantile_threshold_f64")(_ptr(v, C.POINTER(C.c_double)), _ptr(sel, u8p), v.size,
+                                                         keep_q, C.byref(tau), C.byref(cnt)))
+        else:
+            v = v.astype(np.float32)
+            tau = C.c_float()
+            self.check(self.fn("quantile_threshold")(_ptr(v), _ptr(sel, u8p), v.size, keep_q, C.byref(tau),
+                                                     C.byref(cnt)))
+        return tau.value, cnt.value
+
+    def visibility_mask(self, importance, keep_q):
+        imp = np.ascontiguousarray(importance, np.float32)
+        mask = np.zeros(imp.size, np.uint8)
+        self.check(self.fn("visibility_mask")(_ptr(imp), imp.size, keep_q, _ptr(mask, u8p)))
+        return mask
+
+    def view_statistics(self, s, cams, cfg=None, masks=None):
+        """Per-view accumulate_importance folded into (best weight, max-count sum, fp64 summed)."""
+        best = np.zeros(s.n, np.float32)
+        cnt = np.zeros(s.n, np.int64)
+        summed = np.zeros(s.n, np.float64)
+        for k, cam in enumerate(cams):
+            r = self.render(s, cam, cfg, mask=None if masks is None else masks[k])
+            best = np.maximum(best, r["max_weight"])
+            cnt += r["max_pixel_count"]
+            summed += r["importance"].astype(np.float64)
+        return best, cnt, summed
+
+    def identify_critical(self, s, best, max_count_sum, summed, criterion, keep_q, random=None):
+        gv = GaussiansView(s)
+        best = np.ascontiguousarray(best, np.float32)
+        mc = np.ascontiguousarray(max_count_sum, np.int64)
+        sm = np.ascontiguousarray(summed, np.float64)
+        rnd = None if random is None else np.ascontiguousarray(random, np.float64)
+        crit = np.zeros(s.n, np.uint8)
+        cnt = C.c_int32()
+        dp = C.POINTER(C.c_double)
+        self.check(self.fn("identify_critical")(C.byref(gv.struct), _ptr(best), _ptr(mc, i64p), _ptr(sm, dp),
+                                                criterion, keep_q, _ptr(rnd, dp), _ptr(crit, u8p), C.byref(cnt)))
+        return crit, cnt.value
+
+    def aggressive_clone(self, s, critical):
+        n = s.n
+        cap = 2 * n
+        arr = [np.zeros((cap, w), np.float32) for w in (3, 3, 4)] + [np.zeros(cap, np.float32),
+                                                                     np.zeros((cap, 48), np.float32)]
+        for a, src in zip(arr, (s.centers, s.log_scales, s.rotations, s.opacity_logits, s.sh)):
+            a[:n] = src
+        ms = np.zeros(cap, np.int32)
+        n_out = C.c_int32()
+        crit = np.ascontiguousarray(critical, np.uint8)
+        if self.kind == "oracle":
+            self.check(self.fn("aggressive_clone")(*[_ptr(a) for a in arr], n, cap, _ptr(crit, u8p), _ptr(ms, ip),
+                                                   C.byref(n_out)))
+        else:
+            gv = GaussiansView(s)
+            self.check(self.fn("aggressive_clone_apply")(C.byref(gv.struct), _ptr(crit, u8p), *[_ptr(a) for a in arr],
+                                                         cap, _ptr(ms, ip), C.byref(n_out)))
+        m = n_out.value
+        return [a[:m] for a in arr], ms[:m]
+
+    def importance_prune(self, importance, keep_q, s=None):
+        imp = np.ascontiguousarray(importance, np.float64)
+        kept = np.zeros(max(imp.size, 1), np.int32)
+        nk = C.c_int32()
+        dp = C.POINTER(C.c_double)
+        if self.kind == "oracle":
+            self.check(self.fn("importance_prune")(_ptr(imp, dp), imp.size, keep_q, _ptr(kept, ip), C.byref(nk)))
+        else:
+            gv = GaussiansView(s)
+            self.check(self.fn("importance_prune_set")(C.byref(gv.struct), _ptr(imp, dp), keep_q, _ptr(kept, ip),
+                                                       C.byref(nk)))
+        return kept[: nk.value]
+
+    # reference-only entry points
+    def random_scores(self, seed, n):
+        out = np.zeros(n, np.float64)
+        self.check(self.fn("random_scores")(seed, n, _ptr(out, C.POINTER(C.c_double))))
+        return out
+
+    def identify_critical_views(self, s, cams, criterion, keep_q, seed=0, cfg=None, masks=None):
+        gv = GaussiansView(s)
+        cam_arr = (Camera * len(cams))(*cams)
+        m = None if masks is None else np.ascontiguousarray(masks, np.uint8)
+        crit = np.zeros(s.n, np.uint8)
+        cnt = C.c_int32()
+        self.check(self.fn("identify_critical_views")(C.byref(gv.struct), cam_arr, len(cams), C.byref(cfg or RasterConfig()),
+                                                      criterion, keep_q, seed, _ptr(m, u8p), _ptr(crit, u8p),
+                                                      C.byref(cnt)))
+        return crit, cnt.value
+
+    def build_masks(self, s, cams, keep_q, cfg=None):
+        gv = GaussiansView(s)
+        cam_arr = (Camera * len(cams))(*cams)
+        masks = np.zeros((len(cams), s.n), np.uint8)
+        self.check(self.fn("build_masks")(C.byref(gv.struct), cam_arr, len(cams), C.byref(cfg or RasterConfig()), keep_q,
+                                          _ptr(masks, u8p)))
+        return masks
+

@@ -55,3 +55,39 @@ def test_oracle_exp_modes():
     gb = np.array([b.exp(float(x)) for x in xs], np.float32)
     ga = np.array([a.exp(float(x)) for x in xs], np.float32)
     assert np.all(np.abs(gb.view(np.int32) - ga.view(np.int32)) <= 1)
+
+
+LOG_SRC = r'''
+#include "splat_expf.h"
+#include <stdio.h>
+#include <stdlib.h>
+int main(void) {
+    long n = 0, over1 = 0; double worst = 0;
+    for (uint32_t u = 1; u < 0x7f800000u; u += 97) {   /* every 97th positive finite float */
+        float x; memcpy(&x, &u, 4);
+        ++n;
+        const float a = splat_logf(x);
+        const double r = log((double)x);
+        const float rf = (float)r;
+        const double ulp = fabs((double)nextafterf(rf, INFINITY) - (double)rf);
+        const double e = fabs((double)a - r) / ulp;
+        if (e > worst) worst = e;
+        if (e > 1.0) ++over1;
+    }
+    printf("%ld %ld %.4f %a %a %a\n", n, over1, worst, splat_logf(1.0f), splat_logf(0.0f), splat_logf(-1.0f));
+    return 0;
+}
+'''
+
+
+def test_splat_logf_accuracy(tmp_path):
+    """splat_logf (the log shared by densify.cu and the mode-B oracle): < 1 ulp everywhere."""
+    c = tmp_path / "l.c"
+    c.write_text(LOG_SRC)
+    exe = tmp_path / "l"
+    subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off", f"-I{ROOT / 'include'}", str(c), "-o", str(exe), "-lm"],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    n, over, worst = int(out[0]), int(out[1]), float(out[2])
+    assert n > 20_000_000 and over == 0 and worst < 1.0, out
+    assert out[3] == "0x0p+0" and out[4] == "-inf" and out[5] in ("nan", "-nan"), out
