@@ -252,6 +252,25 @@ int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* 
                                 float threshold, uint32_t* bitmask_dev, double* accum_dev,
                                 int64_t* counts_dev, float* max_all_dev);
 
+/* ---- SSIM and the photometric loss (loss.cpp:78-153) -------------- */
+/* ssim<float>: value_dev (device float) = mean SSIM of H x W x ch images a, b with the 11-tap
+ * sigma-1.5 window; grad_dev (nullable) = d mean SSIM / d a.  Per-pixel values are the
+ * reference's bit for bit; the image mean is summed in fp64 (the reference: one float sum). */
+int splat_ssim(splat_ctx* ctx, const float* a_dev, const float* b_dev, int32_t width, int32_t height,
+               int32_t channels, float* grad_dev, float* value_dev);
+/* photometric_loss<float> (loss.cpp:136-147): (1 - lambda) l1 + lambda (1 - ssim) and its
+ * gradient (nullable) with respect to `rendered`. */
+int splat_photometric_loss(splat_ctx* ctx, const float* rendered_dev, const float* target_dev, int32_t width,
+                           int32_t height, int32_t channels, float lambda, float* grad_dev, float* value_dev);
+/* The training step's loss + backward with lambda_dssim (trainer.cpp:226-239): after splat_render
+ * on the same inputs, photometric_loss(colour, target, lambda) -> dL/dC -> render_backward.
+ * loss_dev (nullable) receives the loss. */
+int splat_render_backward_photometric(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam,
+                                      const splat_raster_config* cfg, const float* target_dev,
+                                      const uint8_t* mask_dev, const float background[3],
+                                      const splat_param_grads* grads, int accumulate, float lambda,
+                                      float* loss_dev);
+
 /* ---- densification and simplification on device ---------- */
 /* These run every few hundred iterations; each synchronises the context stream once or twice
  * to read back the scalars the reference's control flow branches on. */

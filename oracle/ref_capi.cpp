@@ -509,4 +509,24 @@ int ref_importance_prune_set(const splat_gaussians* g, const double* importance,
     REF_CATCH
 }
 
+// ssim / photometric_loss (loss.cpp:78-147) on H x W x ch images.
+float ref_ssim(const float* a, const float* b, int w, int h, int ch, float* grad_a) {
+    Imagef ia(w, h, ch), ib(w, h, ch), ig;
+    std::memcpy(ia.data.data(), a, sizeof(float) * ia.size());
+    std::memcpy(ib.data.data(), b, sizeof(float) * ib.size());
+    const float s = ssim<float>(ia, ib, grad_a ? &ig : nullptr);
+    if (grad_a) std::memcpy(grad_a, ig.data.data(), sizeof(float) * ig.size());
+    return s;
+}
+
+float ref_photometric_loss(const float* rendered, const float* target, int w, int h, int ch, float lambda,
+                           float* grad) {
+    Imagef ia(w, h, ch), ib(w, h, ch), ig;
+    std::memcpy(ia.data.data(), rendered, sizeof(float) * ia.size());
+    std::memcpy(ib.data.data(), target, sizeof(float) * ib.size());
+    const float l = photometric_loss<float>(ia, ib, lambda, grad ? &ig : nullptr);
+    if (grad) std::memcpy(grad, ig.data.data(), sizeof(float) * ig.size());
+    return l;
+}
+
 }  // extern "C"

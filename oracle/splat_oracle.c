@@ -1065,3 +1065,115 @@ int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep
     return 0;
 }
 
+/* ---- SSIM and the photometric loss (loss.cpp:10-153) ------------- */
+#define SSIM_W 11
+/* gaussian_kernel (loss.cpp:13-22) */
+static void ssim_kernel(float k[SSIM_W]) {
+    float sum = 0.0f;
+    for (int i = 0; i < SSIM_W; ++i) {
+        const float d = (float)(i - SSIM_W / 2);
+        k[i] = EXP(-d * d / (float)(2 * 1.5 * 1.5));
+        sum += k[i];
+    }
+    for (int i = 0; i < SSIM_W; ++i) k[i] /= sum;
+}
+
+void ORACLE_FN(ssim_window)(float* out11) { ssim_kernel(out11); }
+
+/* blur (loss.cpp:26-53): separable "same" convolution, zero padding by skipping. */
+static void ssim_blur(const float* img, int w, int h, int ch, const float k[SSIM_W], float* out, float* tmp) {
+    const int half = SSIM_W / 2;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < ch; ++c) {
+                float acc = 0.0f;
+                for (int q = -half; q <= half; ++q) {
+                    const int xx = x + q;
+                    if (xx < 0 || xx >= w) continue;
+                    acc += k[q + half] * img[((size_t)y * w + xx) * ch + c];
+                }
+                tmp[((size_t)y * w + x) * ch + c] = acc;
+            }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < ch; ++c) {
+                float acc = 0.0f;
+                for (int q = -half; q <= half; ++q) {
+                    const int yy = y + q;
+                    if (yy < 0 || yy >= h) continue;
+                    acc += k[q + half] * tmp[((size_t)yy * w + x) * ch + c];
+                }
+                out[((size_t)y * w + x) * ch + c] = acc;
+            }
+}
+
+/* ssim<float> (loss.cpp:78-134): mean SSIM; grad_a (nullable) = d mean SSIM / d a. */
+float ORACLE_FN(ssim)(const float* a, const float* b, int w, int h, int ch, float* grad_a) {
+    const float c1 = (float)(0.01 * 0.01), c2 = (float)(0.03 * 0.03);
+    float k[SSIM_W];
+    ssim_kernel(k);
+    const size_t n = (size_t)w * h * ch;
+    float* buf = (float*)malloc(sizeof(float) * n * 12);
+    float *aa = buf, *bb = buf + n, *ab = buf + 2 * n, *mu_a = buf + 3 * n, *mu_b = buf + 4 * n,
+          *m_aa = buf + 5 * n, *m_bb = buf + 6 * n, *m_ab = buf + 7 * n, *tmp = buf + 8 * n, *t1 = buf + 9 * n,
+          *t2 = buf + 10 * n, *t3 = buf + 11 * n;
+    for (size_t i = 0; i < n; ++i) {
+        aa[i] = a[i] * a[i];
+        bb[i] = b[i] * b[i];
+        ab[i] = a[i] * b[i];
+    }
+    ssim_blur(a, w, h, ch, k, mu_a, tmp);
+    ssim_blur(b, w, h, ch, k, mu_b, tmp);
+    ssim_blur(aa, w, h, ch, k, m_aa, tmp);
+    ssim_blur(bb, w, h, ch, k, m_bb, tmp);
+    ssim_blur(ab, w, h, ch, k, m_ab, tmp);
+    const float inv_n = 1.0f / (float)n;
+    float total = 0.0f;
+    for (size_t i = 0; i < n; ++i) {
+        const float ma = mu_a[i], mb = mu_b[i];
+        const float va = m_aa[i] - ma * ma;
+        const float vb = m_bb[i] - mb * mb;
+        const float cov = m_ab[i] - ma * mb;
+        const float a1 = 2.0f * ma * mb + c1;
+        const float a2 = 2.0f * cov + c2;
+        const float b1 = ma * ma + mb * mb + c1;
+        const float b2 = va + vb + c2;
+        const float sv = (a1 * a2) / (b1 * b2);
+        total += sv;
+        if (grad_a) {
+            const float ds_dmu = 2.0f * (mb * a2 * b1 - ma * a1 * a2) / (b1 * b1 * b2);
+            const float ds_dva = -a1 * a2 / (b1 * b2 * b2);
+            const float ds_dcov = 2.0f * a1 / (b1 * b2);
+            t1[i] = inv_n * (ds_dmu - 2.0f * ma * ds_dva - mb * ds_dcov);
+            t2[i] = inv_n * ds_dva;
+            t3[i] = inv_n * ds_dcov;
+        }
+    }
+    if (grad_a) {
+        float* g1 = aa; /* reuse */
+        float* g2 = bb;
+        float* g3 = ab;
+        ssim_blur(t1, w, h, ch, k, g1, tmp);
+        ssim_blur(t2, w, h, ch, k, g2, tmp);
+        ssim_blur(t3, w, h, ch, k, g3, tmp);
+        for (size_t i = 0; i < n; ++i) grad_a[i] = g1[i] + 2.0f * a[i] * g2[i] + b[i] * g3[i];
+    }
+    free(buf);
+    return total * inv_n;
+}
+
+/* photometric_loss<float> (loss.cpp:136-147). grad nullable. */
+float ORACLE_FN(photometric_loss)(const float* rendered, const float* target, int w, int h, int ch, float lambda,
+                                  float* grad) {
+    const size_t n = (size_t)w * h * ch;
+    float* g_l1 = grad ? (float*)malloc(sizeof(float) * n) : NULL;
+    float* g_s = grad ? (float*)malloc(sizeof(float) * n) : NULL;
+    const float l1 = ORACLE_FN(l1_loss)(rendered, target, (int64_t)n, g_l1);
+    const float sv = ORACLE_FN(ssim)(rendered, target, w, h, ch, g_s);
+    if (grad)
+        for (size_t i = 0; i < n; ++i) grad[i] = (1.0f - lambda) * g_l1[i] - lambda * g_s[i];
+    free(g_l1);
+    free(g_s);
+    return (1.0f - lambda) * l1 + lambda * (1.0f - sv);
+}
+

@@ -101,6 +101,14 @@ int ORACLE_FN(aggressive_clone)(float* centers, float* log_scales, float* rotati
                                 int32_t* n_out);
 int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep_q, int32_t* kept, int32_t* n_kept);
 
+/* ssim<float> (loss.cpp:78-134) on H x W x ch images: mean SSIM, grad_a nullable. */
+float ORACLE_FN(ssim)(const float* a, const float* b, int w, int h, int ch, float* grad_a);
+/* photometric_loss<float> (loss.cpp:136-147). */
+float ORACLE_FN(photometric_loss)(const float* rendered, const float* target, int w, int h, int ch, float lambda,
+                                  float* grad);
+/* the normalised 11-tap window gaussian_kernel builds (loss.cpp:13-22) */
+void ORACLE_FN(ssim_window)(float* out11);
+
 /* The exp the library was built with (splat_expf or glibc expf). */
 float ORACLE_FN(exp)(float x);
 

@@ -28,6 +28,7 @@ SOURCES = {
     "binning.cu": [],
     "importance.cu": [],
     "densify.cu": ["--fmad=false"],
+    "ssim.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

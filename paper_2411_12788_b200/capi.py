@@ -239,6 +239,13 @@ _EXPORTS = {
     "splat_importance_prune": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
                                          C.POINTER(C.c_int32)]),
     "splat_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "splat_ssim": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                             C.c_void_p]),
+    "splat_photometric_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_float, C.c_void_p, C.c_void_p]),
+    "splat_render_backward_photometric": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera),
+                                                    C.POINTER(RasterConfig), fp, u8p, C.POINTER(C.c_float),
+                                                    C.POINTER(ParamGrads), C.c_int, C.c_float, fp]),
     "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

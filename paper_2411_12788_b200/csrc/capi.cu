@@ -129,6 +129,8 @@ struct splat_ctx {
     DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
     // densify / simplify scratch (separate from the forward's buffers)
     DevBuf dkey[2], dval[2], dhi, dflags, doffsets, dscalar;
+    // SSIM scratch: t1..t3 maps, per-CTA partial sums, dL/dC of the photometric backward
+    DevBuf ssim_tmp, ssim_partials, d_color_buf;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
@@ -1123,6 +1125,44 @@ int splat_gather_rows(splat_ctx* ctx, const float* src, int32_t width, const int
         return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "gather_rows: bad args");
     CK(launch_gather_rows(ctx->lc, src, width, source, n_rows, dst), "gather rows");
     return SPLAT_OK;
+}
+
+int splat_photometric_loss(splat_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                           int32_t height, int32_t channels, float lambda, float* grad, float* value) {
+    if (!ctx || !rendered || !target || width <= 0 || height <= 0 || channels <= 0)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "ssim: shape mismatch");
+    const size_t n = (size_t)width * height * channels;
+    if (grad) CK(ctx->ssim_tmp.ensure(3 * n * 4), "alloc ssim");
+    CK(ctx->ssim_partials.ensure(2 * ssim_partials_count(width, height, channels) * 8), "alloc ssim");
+    CK(launch_ssim(ctx->lc, rendered, target, width, height, channels, lambda, grad, value,
+                   grad ? ctx->ssim_tmp.as<float>() : nullptr, ctx->ssim_partials.as<double>()),
+       "ssim");
+    return SPLAT_OK;
+}
+
+int splat_ssim(splat_ctx* ctx, const float* a, const float* b, int32_t width, int32_t height, int32_t channels,
+               float* grad, float* value) {
+    return splat_photometric_loss(ctx, a, b, width, height, channels, -1.0f, grad, value);
+}
+
+int splat_render_backward_photometric(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam,
+                                      const splat_raster_config* cfg, const float* target, const uint8_t* mask,
+                                      const float background[3], const splat_param_grads* grads, int accumulate,
+                                      float lambda, float* loss) {
+    if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    if (!target) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward_photometric: target missing");
+    const float zero[3] = {0, 0, 0};
+    const float* bg = background ? background : zero;
+    if (!state_matches(ctx, g, cam, mask, bg))
+        return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE,
+                       "render_backward_photometric: needs a preceding splat_render on the same inputs");
+    const int w = ctx->st.cp.width, h = ctx->st.cp.height;
+    CK(ctx->d_color_buf.ensure((size_t)w * h * 3 * 4), "alloc d_color");
+    float* dc = ctx->d_color_buf.as<float>();
+    if ((rc = splat_photometric_loss(ctx, ctx->st.color, target, w, h, 3, lambda, dc, loss))) return rc;
+    return run_backward(ctx, g, cam, cfg, dc, nullptr, mask, bg, grads, accumulate, nullptr);
 }
 
 }  // extern "C"

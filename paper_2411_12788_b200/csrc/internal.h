@@ -202,4 +202,10 @@ cudaError_t launch_compact_index(LaunchCtx& lc, const uint32_t* flags, const uin
 cudaError_t launch_gather_rows(LaunchCtx& lc, const float* src, int width, const int32_t* source, int n_rows,
                                float* dst);
 
+// ssim.cu: mean SSIM (lambda < 0) or the photometric loss into value_dev,
+// optional gradient; tmp = 3 w h ch floats when grad != null, partials = 2 ssim_partials_count.
+size_t ssim_partials_count(int w, int h, int ch);
+cudaError_t launch_ssim(LaunchCtx& lc, const float* a, const float* b, int w, int h, int ch, float lambda,
+                        float* grad, float* value_dev, float* tmp, double* partials);
+
 }  // namespace splat_b200

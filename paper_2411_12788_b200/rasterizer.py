@@ -343,6 +343,40 @@ def l1_loss(a, b, want_grad: bool = True, ctx: Optional[Context] = None):
     return loss, grad
 
 
+def _img_pair(a, b, ctx, what):
+    torch = _torch()
+    dev = f"cuda:{ctx.device}"
+    host = isinstance(a, np.ndarray)
+    ta = torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev) if host else a.contiguous()
+    tb = torch.from_numpy(np.ascontiguousarray(b, np.float32)).to(dev) if isinstance(b, np.ndarray) else b.contiguous()
+    if tuple(ta.shape) != tuple(tb.shape) or ta.dim() != 3:
+        raise ValueError(f"{what}: shape mismatch")
+    return ta, tb, host
+
+
+def ssim(a, b, want_grad: bool = True, ctx: Optional[Context] = None):
+    """ssim<float> (loss.cpp:78-134) of H x W x C images: returns (mean SSIM, d/da)."""
+    return photometric_loss(a, b, -1.0, want_grad, ctx, _what="ssim")
+
+
+def photometric_loss(rendered, target, lam: float, want_grad: bool = True, ctx: Optional[Context] = None,
+                     _what: str = "photometric_loss"):
+    """photometric_loss<float> (loss.cpp:136-147): (1 - lam) L1 + lam (1 - SSIM), and its gradient.
+    (lam < 0 gives plain SSIM: see ssim.)"""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    ta, tb, host = _img_pair(rendered, target, ctx, _what)
+    h, w, ch = ta.shape
+    grad = torch.empty_like(ta) if want_grad else None
+    val = torch.zeros(1, dtype=torch.float32, device=ta.device)
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_photometric_loss(ctx.h, ta.data_ptr(), tb.data_ptr(), w, h, ch, lam,
+                                             grad.data_ptr() if grad is not None else None, val.data_ptr()))
+    if host:
+        return float(val.item()), (grad.cpu().numpy() if grad is not None else None)
+    return val, grad
+
+
 class OptimState:
     """OptimState (optimizer.hpp:37-76): Adam moments in HBM with the packed parameter layout."""
 

@@ -4,6 +4,7 @@ One step (trainer.cpp:226-240 with lambda_dssim = 0, batched as BASELINE config 
   for each view of this rank's batch:
       render<float>                                   (splat_render)
       l1_loss + render_backward<float>, grads summed  (splat_render_backward_l1, ParamGrads::add)
+        or, with lambda_dssim > 0, photometric_loss   (splat_render_backward_photometric)
   all-reduce of the packed gradient (torch.distributed / NCCL), only when world_size > 1:
       the 3N mean gradients when only means are optimised (config 1), all 59N floats otherwise
   OptimState::step on the selected parameter groups (splat_adam_step)
@@ -46,7 +47,7 @@ class ViewTrainer:
     def __init__(self, params: DeviceGaussians, adam: Optional[capi.AdamConfig] = None,
                  group_mask: int = capi.GROUP_ALL, cfg: Optional[RasterConfig] = None,
                  background=(0.0, 0.0, 0.0), ctx: Optional[Context] = None, max_views: int = 64,
-                 process_group=None):
+                 process_group=None, lambda_dssim: float = 0.0):
         torch = _torch()
         self.torch = torch
         self.ctx = ctx or Context.default()
@@ -58,6 +59,8 @@ class ViewTrainer:
         self.opt = OptimState(adam or capi.AdamConfig(), params.n, self.ctx.device)
         self.loss = torch.zeros(max_views, dtype=torch.float32, device=f"cuda:{self.ctx.device}")
         self.pg = process_group
+        # photometric loss weight (trainer.hpp:46; 0 = the L1-only BASELINE configs)
+        self.lambda_dssim = float(lambda_dssim)
         self.pairs_last_step: list[int] = []
         self.survivors_last_step: list[int] = []
         self._empty_out = RenderOutputs()
@@ -92,9 +95,14 @@ class ViewTrainer:
             self.survivors_last_step.append(ns_.value)
             if ready is not None:
                 self.torch.cuda.current_stream().wait_event(ready[j])
-            self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
-                                                        as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
-                                                        1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
+            if self.lambda_dssim > 0.0:  # photometric_loss -> render_backward (trainer.cpp:226-239)
+                self.ctx.check(lib.splat_render_backward_photometric(
+                    h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), as_fp(tgt.data_ptr()), None, self.bg,
+                    C.byref(self._gr), 1 if j > 0 else 0, self.lambda_dssim, as_fp(self.loss.data_ptr() + 4 * j)))
+            else:
+                self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
+                                                            as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
+                                                            1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
 
     def _finish(self) -> None:
         if self.world_size > 1:

@@ -79,6 +79,10 @@ class OracleLib:
         getattr(L, p + "exp").restype = C.c_float
         for fn in ("project", "tiles", "render", "render_backward"):
             getattr(L, p + fn).restype = C.c_int
+        getattr(L, p + "ssim").argtypes = [fp, fp, C.c_int, C.c_int, C.c_int, fp]
+        getattr(L, p + "ssim").restype = C.c_float
+        getattr(L, p + "photometric_loss").argtypes = [fp, fp, C.c_int, C.c_int, C.c_int, C.c_float, fp]
+        getattr(L, p + "photometric_loss").restype = C.c_float
         if kind == "oracle":
             getattr(L, p + "adam_step").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp, fp, fp,
                                           C.POINTER(AdamConfig), ip, C.c_uint32]
@@ -382,4 +386,21 @@ class OracleLib:
         self.check(self.fn("build_masks")(C.byref(gv.struct), cam_arr, len(cams), C.byref(cfg or RasterConfig()), keep_q,
                                           _ptr(masks, u8p)))
         return masks
+
+    # ---- SSIM / photometric loss (loss.cpp:78-147) ------------------------------------------
+    def ssim(self, a, b, want_grad=True):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        h, w, ch = a.shape
+        g = np.zeros_like(a) if want_grad else None
+        v = self.fn("ssim")(_ptr(a), _ptr(b), w, h, ch, _ptr(g))
+        return float(v), g
+
+    def photometric_loss(self, rendered, target, lam, want_grad=True):
+        a = np.ascontiguousarray(rendered, np.float32)
+        b = np.ascontiguousarray(target, np.float32)
+        h, w, ch = a.shape
+        g = np.zeros_like(a) if want_grad else None
+        v = self.fn("photometric_loss")(_ptr(a), _ptr(b), w, h, ch, lam, _ptr(g))
+        return float(v), g
 
