@@ -252,6 +252,19 @@ int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* 
                                 float threshold, uint32_t* bitmask_dev, double* accum_dev,
                                 int64_t* counts_dev, float* max_all_dev);
 
+/* ---- depth re-initialisation tail (densify.cpp:227-251, spatial.cpp:9-121; §8f rank 2) ---- */
+/* third_neighbor_distances: out_dev[i] = max(distance from point i to its k-th nearest other
+ * point, min_dist), k = min(3, m - 1) (all min_dist when m < 2); points_dev [m][3].  Exact (the
+ * k-th smallest of all pairwise float distances, computed in the reference's order). */
+int splat_third_neighbor_distances(splat_ctx* ctx, const float* points_dev, int32_t m, float min_dist,
+                                   float* out_dev);
+/* The fresh set depth_reinitialize builds from sampled points (densify.cpp:237-251): centers =
+ * points, log-scales = log(third-neighbour distance) (isotropic), rotation (1,0,0,0), opacity
+ * logit(0.1), SH DC = (rgb - 0.5) / C0 from colors_dev [m][3] (NULL: 0), higher bands 0.  out
+ * holds m rows (out->n is ignored). */
+int splat_reinit_gaussians(splat_ctx* ctx, const float* points_dev, const float* colors_dev, int32_t m,
+                           float min_dist, const splat_params_mut* out);
+
 /* ---- SSIM and the photometric loss (loss.cpp:78-153) -------------- */
 /* ssim<float>: value_dev (device float) = mean SSIM of H x W x ch images a, b with the 11-tap
  * sigma-1.5 window; grad_dev (nullable) = d mean SSIM / d a.  Per-pixel values are the

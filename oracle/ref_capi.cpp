@@ -23,6 +23,7 @@
 #include "splat/optimizer.hpp"
 #include "splat/rasterizer.hpp"
 #include "splat/simplify.hpp"
+#include "splat/spatial.hpp"
 #include "splat/visibility.hpp"
 
 using namespace splat;
@@ -527,6 +528,65 @@ float ref_photometric_loss(const float* rendered, const float* target, int w, in
     const float l = photometric_loss<float>(ia, ib, lambda, grad ? &ig : nullptr);
     if (grad) std::memcpy(grad, ig.data.data(), sizeof(float) * ig.size());
     return l;
+}
+
+// ---- depth re-initialisation tail (densify.cpp:227-251, spatial.cpp:101-121) -------------
+int ref_third_neighbor_distances(const float* points, int32_t m, float min_dist, float* out) {
+    REF_TRY
+    std::vector<Vec3f> p(m);
+    for (int i = 0; i < m; ++i) p[i] = Vec3f(points[3 * i], points[3 * i + 1], points[3 * i + 2]);
+    const std::vector<float> d = third_neighbor_distances(p, min_dist);
+    for (int i = 0; i < m; ++i) out[i] = d[i];
+    return 0;
+    REF_CATCH
+}
+
+// The pool indices depth_reinitialize's partial Fisher-Yates draws (densify.cpp:227-235) from a
+// fresh std::mt19937(seed) — the reference's sampling, exported so the device path can be fed it.
+int ref_fisher_yates(uint32_t seed, int32_t pool, int32_t take, int32_t* idx_out) {
+    std::mt19937 rng(seed);
+    std::vector<int> idx(pool);
+    for (int i = 0; i < pool; ++i) idx[i] = i;
+    for (int r = 0; r < take; ++r) {
+        std::uniform_int_distribution<int> pick(r, pool - 1);
+        std::swap(idx[r], idx[pick(rng)]);
+    }
+    for (int r = 0; r < take; ++r) idx_out[r] = idx[r];
+    return 0;
+}
+
+// depth_reinitialize over several views with their images: the fresh set, rows = min(sample_count, pool).
+int ref_depth_reinitialize_views(const splat_gaussians* g, const splat_camera* cams, int32_t n_cams,
+                                 const splat_raster_config* cf, const float* images, int32_t sample_count,
+                                 uint32_t seed, float* centers, float* log_scales, float* rotations,
+                                 float* opacity_logits, float* sh, int32_t* count_out) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<Camera> cv;
+    std::vector<Imagef> imgs;
+    size_t off = 0;
+    for (int k = 0; k < n_cams; ++k) {
+        cv.push_back(to_cam(&cams[k]));
+        Imagef img(cv.back().width, cv.back().height, 3);
+        std::memcpy(img.data.data(), images + off, sizeof(float) * img.data.size());
+        off += img.data.size();
+        imgs.push_back(std::move(img));
+    }
+    std::mt19937 rng(seed);
+    const GaussianSet fresh = depth_reinitialize(set, cv, imgs, sample_count, to_cfg(cf), rng);
+    const int m = fresh.size();
+    *count_out = m;
+    for (int i = 0; i < m; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            centers[3 * i + c] = fresh.centers[i][c];
+            log_scales[3 * i + c] = fresh.log_scales[i][c];
+        }
+        for (int c = 0; c < 4; ++c) rotations[4 * i + c] = fresh.rotations[i][c];
+        opacity_logits[i] = fresh.opacity_logits[i];
+    }
+    if (m > 0) std::memcpy(sh, fresh.sh.data(), sizeof(float) * 48 * static_cast<size_t>(m));
+    return 0;
+    REF_CATCH
 }
 
 }  // extern "C"

@@ -1177,3 +1177,60 @@ float ORACLE_FN(photometric_loss)(const float* rendered, const float* target, in
     return (1.0f - lambda) * l1 + lambda * (1.0f - sv);
 }
 
+/* ---- depth re-initialisation tail (spatial.cpp:101-121, densify.cpp:237-251) ------------ */
+/* third_neighbor_distances: the k-th smallest distance to the other points, by brute force
+ * (spatial.cpp:107-117 restated for every n; the reference's grid gives the same values). */
+int ORACLE_FN(third_neighbor_distances)(const float* p, int32_t m, float min_dist, float* out) {
+    if (m < 2) {
+        for (int32_t i = 0; i < m; ++i) out[i] = min_dist;
+        return 0;
+    }
+    const int k = m - 1 < 3 ? m - 1 : 3;
+    for (int32_t i = 0; i < m; ++i) {
+        float d[3] = {INFINITY, INFINITY, INFINITY};
+        for (int32_t j = 0; j < m; ++j) {
+            if (j == i) continue;
+            const float e[3] = {p[3 * j] - p[3 * i], p[3 * j + 1] - p[3 * i + 1], p[3 * j + 2] - p[3 * i + 2]};
+            const float dist = sqrtf(sq3(e));
+            if (dist < d[2]) {
+                if (dist < d[1]) {
+                    d[2] = d[1];
+                    if (dist < d[0]) {
+                        d[1] = d[0];
+                        d[0] = dist;
+                    } else {
+                        d[1] = dist;
+                    }
+                } else {
+                    d[2] = dist;
+                }
+            }
+        }
+        out[i] = fmax_std(d[k - 1], min_dist);
+    }
+    return 0;
+}
+
+/* The fresh set of depth_reinitialize (densify.cpp:237-251) from sampled points / colours. */
+int ORACLE_FN(reinit_gaussians)(const float* points, const float* colors, int32_t m, float min_dist, float* centers,
+                                float* log_scales, float* rotations, float* opacity_logits, float* sh) {
+    float* nn3 = (float*)malloc(sizeof(float) * (size_t)(m > 0 ? m : 1));
+    ORACLE_FN(third_neighbor_distances)(points, m, min_dist, nn3);
+    const float logit01 = LOG(0.1f / (1.f - 0.1f));
+    const float c0 = (float)0.28209479177387814;
+    for (int32_t r = 0; r < m; ++r) {
+        const float ls = LOG(nn3[r]);
+        for (int c = 0; c < 3; ++c) {
+            centers[3 * r + c] = points[3 * r + c];
+            log_scales[3 * r + c] = ls;
+        }
+        rotations[4 * r] = 1.f;
+        rotations[4 * r + 1] = rotations[4 * r + 2] = rotations[4 * r + 3] = 0.f;
+        opacity_logits[r] = logit01;
+        for (int c = 0; c < 48; ++c) sh[48 * (size_t)r + c] = 0.f;
+        for (int c = 0; c < 3; ++c) sh[48 * (size_t)r + c] = colors ? (colors[3 * r + c] - 0.5f) / c0 : 0.f;
+    }
+    free(nn3);
+    return 0;
+}
+

@@ -109,6 +109,12 @@ float ORACLE_FN(photometric_loss)(const float* rendered, const float* target, in
 /* the normalised 11-tap window gaussian_kernel builds (loss.cpp:13-22) */
 void ORACLE_FN(ssim_window)(float* out11);
 
+/* third_neighbor_distances (spatial.cpp:101-121) and depth_reinitialize's fresh set
+ * (densify.cpp:237-251); contracts as splat_third_neighbor_distances / splat_reinit_gaussians. */
+int ORACLE_FN(third_neighbor_distances)(const float* points, int32_t m, float min_dist, float* out);
+int ORACLE_FN(reinit_gaussians)(const float* points, const float* colors, int32_t m, float min_dist, float* centers,
+                                float* log_scales, float* rotations, float* opacity_logits, float* sh);
+
 /* The exp the library was built with (splat_expf or glibc expf). */
 float ORACLE_FN(exp)(float x);
 

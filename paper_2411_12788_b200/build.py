@@ -29,6 +29,7 @@ SOURCES = {
     "importance.cu": [],
     "densify.cu": ["--fmad=false"],
     "ssim.cu": ["--fmad=false"],
+    "spatial.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

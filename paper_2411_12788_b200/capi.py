@@ -246,6 +246,9 @@ _EXPORTS = {
     "splat_render_backward_photometric": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera),
                                                     C.POINTER(RasterConfig), fp, u8p, C.POINTER(C.c_float),
                                                     C.POINTER(ParamGrads), C.c_int, C.c_float, fp]),
+    "splat_third_neighbor_distances": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_float, C.c_void_p]),
+    "splat_reinit_gaussians": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_float,
+                                         C.POINTER(ParamsMut)]),
     "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

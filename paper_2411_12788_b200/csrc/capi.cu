@@ -131,6 +131,8 @@ struct splat_ctx {
     DevBuf dkey[2], dval[2], dhi, dflags, doffsets, dscalar;
     // SSIM scratch: t1..t3 maps, per-CTA partial sums, dL/dC of the photometric backward
     DevBuf ssim_tmp, ssim_partials, d_color_buf;
+    // k-NN grid: bounds, per-point cell, cell starts / cursors, cell-sorted points, distances
+    DevBuf knn_bounds, knn_cell, knn_start, knn_cursor, knn_sorted, knn_dist;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
@@ -1163,6 +1165,74 @@ int splat_render_backward_photometric(splat_ctx* ctx, const splat_gaussians* g, 
     float* dc = ctx->d_color_buf.as<float>();
     if ((rc = splat_photometric_loss(ctx, ctx->st.color, target, w, h, 3, lambda, dc, loss))) return rc;
     return run_backward(ctx, g, cam, cfg, dc, nullptr, mask, bg, grads, accumulate, nullptr);
+}
+
+int splat_third_neighbor_distances(splat_ctx* ctx, const float* points, int32_t m, float min_dist, float* out) {
+    if (!ctx || m < 0 || (m > 0 && (!points || !out)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "third_neighbor_distances: bad args");
+    LaunchCtx& lc = ctx->lc;
+    if (m < 2) {  // spatial.cpp:103-105
+        CK(launch_fill(lc, out, m, min_dist), "fill");
+        return SPLAT_OK;
+    }
+    const int k = std::min(3, m - 1);
+    if (m <= 256) {
+        CK(launch_knn_brute(lc, points, m, k, min_dist, out), "knn brute");
+        return SPLAT_OK;
+    }
+    CK(ctx->knn_bounds.ensure(64), "alloc");
+    CK(launch_point_bounds(lc, points, m, ctx->knn_bounds.as<uint32_t>()), "bounds");
+    uint32_t keys[6];
+    CK(cudaMemcpyAsync(keys, ctx->knn_bounds.p, sizeof(keys), cudaMemcpyDeviceToHost, ctx->stream), "read bounds");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    float lo[3], hi[3];
+    decode_bounds(keys, lo, hi);
+    // a dense grid of ~8 cells per point, at most 2^26 cells
+    double e[3], vol = 1.0, emax = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        e[c] = std::max((double)hi[c] - (double)lo[c], 1e-6);
+        vol *= e[c];
+        emax = std::max(emax, e[c]);
+    }
+    const double target = std::min(8.0 * m, (double)(1 << 26));
+    double hh = std::max({std::cbrt(vol / target), emax / 2048.0, 1e-6});
+    KnnGrid g{};
+    for (;;) {
+        g.nx = (int)(e[0] / hh) + 1;
+        g.ny = (int)(e[1] / hh) + 1;
+        g.nz = (int)(e[2] / hh) + 1;
+        if ((double)g.nx * g.ny * g.nz <= (double)(1 << 26)) break;
+        hh *= 1.25;
+    }
+    g.ox = lo[0];
+    g.oy = lo[1];
+    g.oz = lo[2];
+    g.h = (float)hh;
+    g.inv_h = (float)(1.0 / hh);
+    const size_t ncells = (size_t)g.nx * g.ny * g.nz;
+    CK(ctx->knn_cell.ensure((size_t)m * 4), "alloc");
+    CK(ctx->knn_sorted.ensure((size_t)m * 4), "alloc");
+    CK(ctx->knn_start.ensure((ncells + 1) * 4), "alloc");
+    CK(ctx->knn_cursor.ensure(ncells * 4), "alloc");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(ncells) + 64) * 4), "alloc");
+    CK(launch_grid_build(lc, points, m, g, ctx->knn_cell.as<uint32_t>(), ctx->knn_start.as<uint32_t>(),
+                         ctx->knn_cursor.as<uint32_t>(), ctx->knn_sorted.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>()),
+       "grid");
+    CK(launch_knn(lc, points, m, g, ctx->knn_start.as<uint32_t>(), ctx->knn_sorted.as<uint32_t>(), k, min_dist, out),
+       "knn");
+    return SPLAT_OK;
+}
+
+int splat_reinit_gaussians(splat_ctx* ctx, const float* points, const float* colors, int32_t m, float min_dist,
+                           const splat_params_mut* out) {
+    if (!ctx || !out || m < 0 || (m > 0 && (!points || !out->centers || !out->log_scales || !out->rotations ||
+                                             !out->opacity_logits || !out->sh)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "reinit_gaussians: bad args");
+    CK(ctx->knn_dist.ensure((size_t)(m > 0 ? m : 1) * 4), "alloc");
+    int rc = splat_third_neighbor_distances(ctx, points, m, min_dist, ctx->knn_dist.as<float>());
+    if (rc) return rc;
+    CK(launch_reinit_set(ctx->lc, points, colors, ctx->knn_dist.as<float>(), m, *out), "reinit set");
+    return SPLAT_OK;
 }
 
 }  // extern "C"

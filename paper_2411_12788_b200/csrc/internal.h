@@ -208,4 +208,20 @@ size_t ssim_partials_count(int w, int h, int ch);
 cudaError_t launch_ssim(LaunchCtx& lc, const float* a, const float* b, int w, int h, int ch, float lambda,
                         float* grad, float* value_dev, float* tmp, double* partials);
 
+// spatial.cu: uniform-grid k-NN and the depth-reinit fresh set.
+struct KnnGrid {
+    float ox, oy, oz, h, inv_h;
+    int nx, ny, nz;
+};
+cudaError_t launch_point_bounds(LaunchCtx& lc, const float* p, int m, uint32_t* bounds6);
+void decode_bounds(const uint32_t* keys6, float lo[3], float hi[3]);
+cudaError_t launch_grid_build(LaunchCtx& lc, const float* p, int m, const KnnGrid& g, uint32_t* cell_of,
+                              uint32_t* start, uint32_t* cursor, uint32_t* sorted, uint32_t* scan_tmp);
+cudaError_t launch_knn(LaunchCtx& lc, const float* p, int m, const KnnGrid& g, const uint32_t* start,
+                       const uint32_t* sorted, int k, float min_dist, float* out);
+cudaError_t launch_knn_brute(LaunchCtx& lc, const float* p, int m, int k, float min_dist, float* out);
+cudaError_t launch_fill(LaunchCtx& lc, float* out, int m, float v);
+cudaError_t launch_reinit_set(LaunchCtx& lc, const float* points, const float* colors, const float* nn3, int m,
+                              const splat_params_mut& out);
+
 }  // namespace splat_b200

@@ -8,6 +8,7 @@ reference's API over the C-ABI (include/splat_b200.h):
   importance_prune     simplify.cpp:94-107       select_above_quantile on global importance
   select / remap       gaussian_set.hpp:96-110, OptimState::remap optimizer.cpp:73-108
   quantile_threshold   quantile.hpp:16-28
+  third_neighbor_distances / depth_reinitialize   spatial.cpp:101-121, densify.cpp:198-252
 
 Everything per Gaussian runs in CUDA (csrc/densify.cu + the radix sort); the host reads back
 only the scalars the reference's control flow branches on.  No CPU fallback.
@@ -212,3 +213,63 @@ def importance_prune(params: DeviceGaussians, importance, keep_q: float, ctx: Op
     ctx.check(ctx.lib.splat_importance_prune(ctx.h, importance.data_ptr(), n, keep_q, kept.data_ptr(), C.byref(nk)))
     kept = kept[: nk.value]
     return select(params, kept, ctx=ctx), kept
+
+
+def third_neighbor_distances(points, min_dist: float = 1e-7, ctx: Optional[Context] = None):
+    """third_neighbor_distances over a CUDA float32 tensor [m, 3] (grid k-NN on device)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    m = int(points.shape[0])
+    out = torch.empty(max(m, 1), dtype=torch.float32, device=points.device)
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_third_neighbor_distances(ctx.h, points.contiguous().data_ptr(), m, min_dist,
+                                                     out.data_ptr()))
+    return out[:m]
+
+
+def depth_reinitialize(set_, cams: Sequence[capi.Camera], images, sample_count: int, sample=None,
+                       cfg: Optional[RasterConfig] = None, min_dist: float = 1e-7, ctx: Optional[Context] = None,
+                       generator=None) -> DeviceGaussians:
+    """depth_reinitialize (densify.cpp:198-252) on device: render each view, unproject every pixel
+    with a max contributor (view-major, raster order = the reference's pool order), draw
+    min(sample_count, pool) of them, and build the fresh set (3rd-NN isotropic scales, identity
+    rotation, opacity 0.1, SH DC from the image colour).
+
+    images: CUDA float32 [views, H, W, 3].  sample: optional CUDA int32 pool indices in draw
+    order (the reference draws them with a partial Fisher-Yates over its std::mt19937; its exact
+    sequence is libstdc++'s); default: a seeded uniform draw without replacement on device
+    (torch.randperm with `generator`).  Raises RuntimeError when no pixel has a valid depth
+    (densify.cpp:223-225)."""
+    torch = _torch()
+    from .rasterizer import depth_points
+    ctx = ctx or Context.default()
+    if len(cams) == 0:
+        raise ValueError("depth_reinitialize: no cameras")
+    if images.shape[0] != len(cams):
+        raise ValueError("depth_reinitialize: camera/image count mismatch")
+    if sample_count < 1:
+        raise ValueError("depth_reinitialize: sample_count < 1")
+    ds, _ = _device_set(set_, ctx.device)
+    pts, views, pix = depth_points(ds, cams, cfg, rule=capi.DEPTH_RULE_ARGMAX, stride=1, seed=0, ctx=ctx)
+    pool = int(pts.shape[0])
+    if pool == 0:
+        raise RuntimeError("depth_reinitialize: no valid depth pixels (model renders nothing)")
+    take = min(sample_count, pool)
+    if sample is None:
+        sample = torch.randperm(pool, device=pts.device, generator=generator)[:take].to(torch.int32)
+    sample = sample[:take].contiguous()
+    hw = images.shape[1] * images.shape[2]
+    # colour of each pooled point: row (view * HW + pixel) of the [views * HW, 3] image rows
+    src = (views.to(torch.int64) * hw + pix.to(torch.int64)).to(torch.int32)[sample.to(torch.int64)].contiguous()
+    sampled = torch.empty((take, 3), dtype=torch.float32, device=pts.device)
+    colors = torch.empty((take, 3), dtype=torch.float32, device=pts.device)
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_gather_rows(ctx.h, pts.contiguous().data_ptr(), 3, sample.data_ptr(), take,
+                                        sampled.data_ptr()))
+    ctx.check(ctx.lib.splat_gather_rows(ctx.h, images.contiguous().data_ptr(), 3, src.data_ptr(), take,
+                                        colors.data_ptr()))
+    fresh = DeviceGaussians(take, ds.active_sh_degree, ctx.device)
+    ctx.check(ctx.lib.splat_reinit_gaussians(ctx.h, sampled.data_ptr(), colors.data_ptr(), take, min_dist,
+                                             C.byref(fresh.mut())))
+    return fresh
+

@@ -79,6 +79,7 @@ class OracleLib:
         getattr(L, p + "exp").restype = C.c_float
         for fn in ("project", "tiles", "render", "render_backward"):
             getattr(L, p + fn).restype = C.c_int
+        getattr(L, p + "third_neighbor_distances").argtypes = [fp, C.c_int32, C.c_float, fp]
         getattr(L, p + "ssim").argtypes = [fp, fp, C.c_int, C.c_int, C.c_int, fp]
         getattr(L, p + "ssim").restype = C.c_float
         getattr(L, p + "photometric_loss").argtypes = [fp, fp, C.c_int, C.c_int, C.c_int, C.c_float, fp]
@@ -95,6 +96,7 @@ class OracleLib:
             getattr(L, p + "identify_critical").argtypes = [G, fp, i64p, dp, C.c_int, C.c_double, dp, u8p, ip]
             getattr(L, p + "aggressive_clone").argtypes = [fp, fp, fp, fp, fp, C.c_int32, C.c_int64, u8p, ip, ip]
             getattr(L, p + "importance_prune").argtypes = [dp, C.c_int32, C.c_double, ip, ip]
+            getattr(L, p + "reinit_gaussians").argtypes = [fp, fp, C.c_int32, C.c_float, fp, fp, fp, fp, fp]
         else:
             getattr(L, p + "adam_steps").argtypes = [fp, fp, fp, fp, fp, C.c_int32, fp, fp, fp, fp, fp,
                                            C.POINTER(AdamConfig), C.c_int32]
@@ -103,6 +105,9 @@ class OracleLib:
             getattr(L, p + "render_backward_f64").argtypes = [G, CAM, CFG, fp, u8p, fp, dp, dp, dp, dp, dp]
             getattr(L, p + "global_importance").argtypes = [G, CAM, C.c_int32, CFG, C.POINTER(C.c_double), ip]
             getattr(L, p + "random_scores").argtypes = [C.c_uint32, C.c_int32, dp]
+            getattr(L, p + "fisher_yates").argtypes = [C.c_uint32, C.c_int32, C.c_int32, ip]
+            getattr(L, p + "depth_reinitialize_views").argtypes = [G, CAM, C.c_int32, CFG, fp, C.c_int32, C.c_uint32,
+                                                                   fp, fp, fp, fp, fp, ip]
             getattr(L, p + "identify_critical_views").argtypes = [G, CAM, C.c_int32, CFG, C.c_int, C.c_double,
                                                                   C.c_uint32, u8p, u8p, ip]
             getattr(L, p + "aggressive_clone_apply").argtypes = [G, u8p, fp, fp, fp, fp, fp, C.c_int64, ip, ip]
@@ -403,4 +408,38 @@ class OracleLib:
         g = np.zeros_like(a) if want_grad else None
         v = self.fn("photometric_loss")(_ptr(a), _ptr(b), w, h, ch, lam, _ptr(g))
         return float(v), g
+
+    # ---- depth re-initialisation tail (spatial.cpp, densify.cpp:227-251) ----------------------
+    def third_neighbor_distances(self, points, min_dist=1e-7):
+        p = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+        out = np.zeros(max(p.shape[0], 1), np.float32)
+        self.check(self.fn("third_neighbor_distances")(_ptr(p), p.shape[0], min_dist, _ptr(out)))
+        return out[: p.shape[0]]
+
+    def reinit_gaussians(self, points, colors, min_dist=1e-7):
+        p = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+        col = None if colors is None else np.ascontiguousarray(colors, np.float32).reshape(-1, 3)
+        m = p.shape[0]
+        out = [np.zeros((m, 3), np.float32), np.zeros((m, 3), np.float32), np.zeros((m, 4), np.float32),
+               np.zeros(m, np.float32), np.zeros((m, 48), np.float32)]
+        self.check(self.fn("reinit_gaussians")(_ptr(p), _ptr(col), m, min_dist, *[_ptr(a) for a in out]))
+        return out
+
+    def fisher_yates(self, seed, pool, take):
+        out = np.zeros(max(take, 1), np.int32)
+        self.check(self.fn("fisher_yates")(seed, pool, take, _ptr(out, ip)))
+        return out[:take]
+
+    def depth_reinitialize_views(self, s, cams, images, sample_count, seed=0, cfg=None):
+        gv = GaussiansView(s)
+        cam_arr = (Camera * len(cams))(*cams)
+        imgs = np.ascontiguousarray(np.concatenate([np.asarray(i, np.float32).reshape(-1) for i in images]))
+        cap = sample_count
+        out = [np.zeros((cap, 3), np.float32), np.zeros((cap, 3), np.float32), np.zeros((cap, 4), np.float32),
+               np.zeros(cap, np.float32), np.zeros((cap, 48), np.float32)]
+        cnt = C.c_int32()
+        self.check(self.fn("depth_reinitialize_views")(C.byref(gv.struct), cam_arr, len(cams), C.byref(cfg or RasterConfig()),
+                                                       _ptr(imgs), sample_count, seed, *[_ptr(a) for a in out],
+                                                       C.byref(cnt)))
+        return [a[: cnt.value] for a in out]
 
