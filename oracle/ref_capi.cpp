@@ -21,6 +21,7 @@
 #include "splat/gradients.hpp"
 #include "splat/loss.hpp"
 #include "splat/optimizer.hpp"
+#include "splat/ply_io.hpp"
 #include "splat/rasterizer.hpp"
 #include "splat/simplify.hpp"
 #include "splat/spatial.hpp"
@@ -585,6 +586,34 @@ int ref_depth_reinitialize_views(const splat_gaussians* g, const splat_camera* c
         opacity_logits[i] = fresh.opacity_logits[i];
     }
     if (m > 0) std::memcpy(sh, fresh.sh.data(), sizeof(float) * 48 * static_cast<size_t>(m));
+    return 0;
+    REF_CATCH
+}
+
+// ---- PLY checkpoints (ply_io.cpp) ------------------------------------------------------
+int ref_write_ply(const char* path, const splat_gaussians* g) {
+    REF_TRY
+    write_ply(path, to_set(g));
+    return 0;
+    REF_CATCH
+}
+
+// read_ply into caller arrays with room for `capacity` rows; *n_out = rows in the file.
+int ref_read_ply(const char* path, float* centers, float* log_scales, float* rotations, float* opacity_logits,
+                 float* sh, int32_t capacity, int32_t* n_out) {
+    REF_TRY
+    const GaussianSet s = read_ply(path);
+    *n_out = s.size();
+    if (s.size() > capacity) throw std::invalid_argument("ref_read_ply: capacity");
+    for (int i = 0; i < s.size(); ++i) {
+        for (int c = 0; c < 3; ++c) {
+            centers[3 * i + c] = s.centers[i][c];
+            log_scales[3 * i + c] = s.log_scales[i][c];
+        }
+        for (int c = 0; c < 4; ++c) rotations[4 * i + c] = s.rotations[i][c];
+        opacity_logits[i] = s.opacity_logits[i];
+    }
+    if (s.size() > 0) std::memcpy(sh, s.sh.data(), sizeof(float) * 48 * static_cast<size_t>(s.size()));
     return 0;
     REF_CATCH
 }

@@ -442,4 +442,3 @@ class OracleLib:
                                                        _ptr(imgs), sample_count, seed, *[_ptr(a) for a in out],
                                                        C.byref(cnt)))
         return [a[: cnt.value] for a in out]
-
