@@ -108,6 +108,7 @@ struct FwdState {
     float bg[3] = {0, 0, 0};
     const float* g_centers = nullptr;  // identity of the inputs (reuse check)
     const uint8_t* mask = nullptr;
+    const uint32_t* order = nullptr;  // survivors in (depth, index) order (device)
     float* color = nullptr;
     float* alpha = nullptr;
     float* depth = nullptr;
@@ -133,6 +134,9 @@ struct splat_ctx {
     DevBuf ssim_tmp, ssim_partials, d_color_buf;
     // k-NN grid: bounds, per-point cell, cell starts / cursors, cell-sorted points, distances
     DevBuf knn_bounds, knn_cell, knn_start, knn_cursor, knn_sorted, knn_dist;
+    // cooperative depth sort: third key/value buffer + histogram/count scratch
+    DevBuf ktmp, vtmp, coop_work;
+    bool coop_sort = true;
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
@@ -250,6 +254,28 @@ int ceil_log2(uint32_t v) {
     return b;
 }
 
+// Stable sort of the N depth keys (with Gaussian ids): one cooperative kernel when the tiles fit
+// a resident wave (result in buffer 1), else the Onesweep passes.
+cudaError_t depth_sort(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint64_t n, bool* alt) {
+    LaunchCtx& lc = ctx->lc;
+    if (ctx->coop_sort) {
+        cudaError_t e = ctx->ktmp.ensure(n * 4);
+        if (e == cudaSuccess) e = ctx->vtmp.ensure(n * 4);
+        if (e == cudaSuccess) e = ctx->coop_work.ensure(radix_coop_count_words(n) * 4);
+        if (e != cudaSuccess) return e;
+        e = radix_sort_coop(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(),
+                            ctx->ktmp.as<uint32_t>(), ctx->vtmp.as<uint32_t>(), n, ctx->coop_work.as<uint32_t>());
+        if (e == cudaSuccess) {
+            *alt = true;
+            return cudaSuccess;
+        }
+        if (e != cudaErrorCooperativeLaunchTooLarge) return e;
+        cudaGetLastError();
+    }
+    return radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), n, 0, 32,
+                            ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), alt);
+}
+
 // The full forward of one view.  `out` fields may be null; the backward state (t_final,
 // last_index, colour) always lands in ctx buffers or the caller's colour buffer.
 int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
@@ -312,10 +338,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
         CK(cudaEventRecord(ctx->ev_counts, s), "record counts");
         bool alt = false;
-        CK(radix_sort_pairs(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(), (uint64_t)n, 0,
-                            32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
-           "depth sort");
+        CK(depth_sort(ctx, keys, vals, (uint64_t)n, &alt), "depth sort");
         const uint32_t* order = alt ? ctx->vals[1].as<uint32_t>() : vals;
+        ctx->st.order = order;
         const int sts = supertile_side();
         const int st_x = (cp.tiles_x + sts - 1) / sts, st_y = (cp.tiles_y + sts - 1) / sts;
         const int n_st = st_x * st_y;
@@ -623,6 +648,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
         c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
         const char* e2 = std::getenv("SPLAT_BWD_PX2");
         c->lc.bwd_px2 = !(e2 && std::strcmp(e2, "0") == 0);
+        const char* e3 = std::getenv("SPLAT_COOP_SORT");
+        c->coop_sort = !(e3 && std::strcmp(e3, "0") == 0);
     }
     *out = c;
     return SPLAT_OK;
@@ -857,6 +884,19 @@ int splat_sort_pairs(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* k
     CK(ctx->hist.ensure(hw * 4), "alloc hist");
     CK(ctx->scan_tmp.ensure((scan_temp_words(hw) + 64) * 4), "alloc scan");
     bool alt = false;
+    if (ctx->coop_sort && begin_bit == 0 && end_bit == 32 && n > 0) {  // the depth sort's path
+        CK(ctx->ktmp.ensure((size_t)n * 4), "alloc");
+        CK(ctx->vtmp.ensure((size_t)n * 4), "alloc");
+        CK(ctx->coop_work.ensure(radix_coop_count_words((uint64_t)n) * 4), "alloc");
+        const cudaError_t e = radix_sort_coop(ctx->lc, keys, vals, keys_alt, vals_alt, ctx->ktmp.as<uint32_t>(),
+                                              ctx->vtmp.as<uint32_t>(), (uint64_t)n, ctx->coop_work.as<uint32_t>());
+        if (e == cudaSuccess) {
+            *result_in_alt = 1;
+            return SPLAT_OK;
+        }
+        if (e != cudaErrorCooperativeLaunchTooLarge) return cuda_err(ctx, e, "sort_pairs");
+        cudaGetLastError();
+    }
     CK(radix_sort_pairs(ctx->lc, keys, vals, keys_alt, vals_alt, (uint64_t)n, begin_bit, end_bit,
                         ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(), &alt),
        "sort_pairs");
@@ -958,8 +998,7 @@ int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int3
         if (p >= st.n_pairs) p = st.n_pairs;
     }
     if (depth_order && st.n_surv) {
-        // depth sort of N keys: 4 passes of 8 bits -> result back in buffer 0
-        CK(cudaMemcpy(depth_order, ctx->vals[0].p, 4 * (size_t)st.n_surv, cudaMemcpyDeviceToHost), "copy");
+        CK(cudaMemcpy(depth_order, st.order, 4 * (size_t)st.n_surv, cudaMemcpyDeviceToHost), "copy");
     }
     return SPLAT_OK;
 }

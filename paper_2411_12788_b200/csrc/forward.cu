@@ -12,7 +12,7 @@ namespace splat_b200 {
 #ifdef SPLAT_STATS
 // Instrumented builds only (tools/stats_build.sh): forward traversal counters, read with
 // splat_debug_stats.
-__device__ unsigned long long g_stats[8];
+__device__ unsigned long long g_stats[12];
 #endif
 
 namespace {
@@ -430,6 +430,16 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
             const int cnt = pipe.stage(b, !done, bx0, bx1, by0, by1, sm);
             if (cnt < 0) break;
 #ifdef SPLAT_STATS
+            {
+                const unsigned wa = __ballot_sync(0xffffffffu, !done);
+                const int act = __syncthreads_count(!done);
+                if ((tid & 31) == 0 && wa) atomicAdd(&g_stats[7], 1ull);          // warps with work
+                if (tid == 0) {
+                    atomicAdd(&g_stats[8], (unsigned long long)((act + 31) / 32));  // warps needed
+                    atomicAdd(&g_stats[9], (unsigned long long)act);                  // active pixels
+                    atomicAdd(&g_stats[10], 1ull);                                    // CTA batches
+                }
+            }
             if (tid == 0) {
                 atomicAdd(&g_stats[4], (unsigned long long)cnt);
                 atomicAdd(&g_stats[6], (unsigned long long)min((uint32_t)nthreads, end - start - (uint32_t)b * nthreads));
@@ -815,9 +825,9 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
 extern "C" int splat_debug_stats(unsigned long long* out, int reset) {
 #ifdef SPLAT_STATS
     cudaDeviceSynchronize();
-    if (cudaMemcpyFromSymbol(out, splat_b200::g_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return 3;
+    if (cudaMemcpyFromSymbol(out, splat_b200::g_stats, sizeof(unsigned long long) * 12) != cudaSuccess) return 3;
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(splat_b200::g_stats, z, sizeof(z));
     }
     return 0;

@@ -18,6 +18,8 @@
 // tile's global digit offsets, and scatter.  2 + passes launches per sort instead of 5 per pass.
 #include <algorithm>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "common.cuh"
@@ -417,6 +419,163 @@ void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint
     lc.count += 2;
 }
 
+// ---- cooperative whole-sort kernel ---------------------------------------------------------
+// For N up to (resident CTAs) x 2048 keys the whole LSD sort runs as ONE cooperative kernel: each
+// CTA owns one 2048-key tile for the whole sort, so a pass is rank -> publish per-digit tile
+// counts -> grid barrier -> 256 CTAs scan one digit row each -> grid barrier -> scatter -> grid
+// barrier, with no look-back chain (the Onesweep look-back serialises ~tiles/16 round trips when
+// every tile runs in the same wave).  The first phase histograms all four byte digits; passes
+// whose digit is the same for every key are skipped, and the buffer chain is routed through a
+// third buffer so the result always lands in (keys1, vals1).
+namespace cg = cooperative_groups;
+constexpr int kCoopItems = 8;
+constexpr int kCoopTile = kThreads * kCoopItems;  // 2048
+
+__global__ void __launch_bounds__(kThreads, 4) radix_coop_kernel(uint32_t* __restrict__ k0, uint32_t* __restrict__ v0,
+                                                                 uint32_t* __restrict__ k1, uint32_t* __restrict__ v1,
+                                                                 uint32_t* __restrict__ k2, uint32_t* __restrict__ v2,
+                                                                 uint32_t n, uint32_t* __restrict__ hist,
+                                                                 uint32_t* __restrict__ counts) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t s_cnt[kWarps][256];
+    __shared__ uint32_t s_gh[4][256];
+    __shared__ uint32_t s_warp[kWarps];
+    const uint32_t tile = blockIdx.x, ntiles = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
+    uint32_t k[kCoopItems], v[kCoopItems];
+#pragma unroll
+    for (int r = 0; r < kCoopItems; ++r) {
+        const uint32_t i = wbase + r * 32 + lane;
+        k[r] = i < n ? k0[i] : 0u;
+        v[r] = i < n ? v0[i] : 0u;
+    }
+    // phase 0: digit histograms of all four bytes
+    for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kCoopItems; ++r)
+        if (wbase + r * 32 + lane < n)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) atomicAdd(&s_gh[p][(k[r] >> (8 * p)) & 255u], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += kThreads)
+        if ((&s_gh[0][0])[i]) atomicAdd(&hist[i], (&s_gh[0][0])[i]);
+    grid.sync();
+    for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = hist[i];
+    __syncthreads();
+    // executed passes (uniform over the grid) and the buffer chain 0 -> ... -> 1 (alternating
+    // 1 / 2 backwards from the last pass)
+    int passes[4], m = 0;
+    for (int p = 0; p < 4; ++p) {
+        bool trivial = false;
+        for (int d = threadIdx.x; d < 256; d += kThreads) trivial |= s_gh[p][d] == n;
+        if (!__syncthreads_or(trivial)) passes[m++] = p;
+    }
+    uint32_t* kb[3] = {k0, k1, k2};
+    uint32_t* vb[3] = {v0, v1, v2};
+    if (m == 0) {  // nothing to reorder: copy to the result buffers
+#pragma unroll
+        for (int r = 0; r < kCoopItems; ++r) {
+            const uint32_t i = wbase + r * 32 + lane;
+            if (i < n) {
+                k1[i] = k[r];
+                v1[i] = v[r];
+            }
+        }
+        return;
+    }
+    int src = 0;
+    const unsigned lt = lanemask_lt();
+    for (int j = 0; j < m; ++j) {
+        const int dst = ((m - 1 - j) & 1) ? 2 : 1;
+        const int shift = 8 * passes[j];
+        if (j > 0) {
+#pragma unroll
+            for (int r = 0; r < kCoopItems; ++r) {
+                const uint32_t i = wbase + r * 32 + lane;
+                k[r] = i < n ? kb[src][i] : 0u;
+                v[r] = i < n ? vb[src][i] : 0u;
+            }
+        }
+        for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_cnt[0][0])[i] = 0u;
+        __syncthreads();
+        uint32_t rank[kCoopItems];
+#pragma unroll
+        for (int r = 0; r < kCoopItems; ++r) {
+            const bool valid = wbase + r * 32 + lane < n;
+            const uint32_t d = (k[r] >> shift) & 255u;
+            const uint32_t label = valid ? d : (0x80000000u | (uint32_t)lane);
+            const unsigned peers = __match_any_sync(0xffffffffu, label);
+            const uint32_t old = valid ? s_cnt[warp][d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0u) s_cnt[warp][d] = old + __popc(peers);
+            __syncwarp();
+            rank[r] = old + __popc(peers & lt);
+        }
+        __syncthreads();
+        {  // tile totals per digit (thread d), published digit-major
+            const int d = threadIdx.x;
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) c += s_cnt[w][d];
+            counts[(size_t)d * ntiles + tile] = c;
+        }
+        grid.sync();
+        // phase B: digit rows, exclusive over tiles, plus the digit's global base
+        for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) {
+            uint32_t base = 0;  // exclusive scan of the pass histogram up to d (cheap: <= 256 adds)
+            for (uint32_t e = lane; e < d; e += 32) base += s_gh[passes[j]][e];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+            uint32_t* row = counts + (size_t)d * ntiles;
+            uint32_t carry = base;
+            for (uint32_t t0 = 0; t0 < ntiles; t0 += kThreads * 3) {
+                uint32_t x[3], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const uint32_t t = t0 + threadIdx.x * 3 + q;
+                    x[q] = t < ntiles ? row[t] : 0u;
+                    sum += x[q];
+                }
+                uint32_t tot;
+                const uint32_t ex = block_exclusive_scan(sum, &tot, s_warp);
+                uint32_t acc = carry + ex;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const uint32_t t = t0 + threadIdx.x * 3 + q;
+                    if (t < ntiles) row[t] = acc;
+                    acc += x[q];
+                }
+                carry += tot;
+            }
+        }
+        grid.sync();
+        {  // phase C: tile offsets per digit, per-warp runs, scatter
+            const int d = threadIdx.x;
+            uint32_t run = counts[(size_t)d * ntiles + tile];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t cw = s_cnt[w][d];
+                s_cnt[w][d] = run;
+                run += cw;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kCoopItems; ++r) {
+            const uint32_t i = wbase + r * 32 + lane;
+            if (i < n) {
+                const uint32_t pos = s_cnt[warp][(k[r] >> shift) & 255u] + rank[r];
+                kb[dst][pos] = k[r];
+                vb[dst][pos] = v[r];
+            }
+        }
+        src = dst;
+        grid.sync();
+    }
+}
+
 }  // namespace
 
 size_t scan_temp_words(uint64_t n) {
@@ -497,6 +656,37 @@ cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint
         *result_in_alt = !*result_in_alt;
     }
     return cudaGetLastError();
+}
+
+size_t radix_coop_count_words(uint64_t n) {
+    const uint64_t nt = (n + kCoopTile - 1) / kCoopTile;
+    return (size_t)(4 * 256 + 256 * nt + 16);
+}
+
+// Whole 32-bit LSD sort of (keys, vals) as one cooperative kernel; the result always lands in
+// (keys_alt, vals_alt).  Returns cudaErrorCooperativeLaunchTooLarge (nothing launched) when the
+// tiles do not fit in one resident wave; the caller falls back to radix_sort_pairs.
+cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                            uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work) {
+    if (n == 0) return cudaSuccess;
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, radix_coop_kernel, kThreads, 0) != cudaSuccess)
+            per_sm = 0;
+    }
+    const uint64_t nt = (n + kCoopTile - 1) / kCoopTile;
+    if (nt > (uint64_t)lc.num_sms * per_sm || n >= (1ull << 31)) return cudaErrorCooperativeLaunchTooLarge;
+    cudaError_t e = cudaMemsetAsync(work, 0, 4 * 256 * 4, lc.stream);
+    if (e != cudaSuccess) return e;
+    uint32_t* hist = work;
+    uint32_t* counts = work + 4 * 256;
+    uint32_t nn = (uint32_t)n;
+    void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts};
+    LaunchScope s(lc, "radix_sort");
+    e = cudaLaunchCooperativeKernel((const void*)radix_coop_kernel, dim3((unsigned)nt), dim3(kThreads), args, 0,
+                                    lc.stream);
+    lc.count++;
+    return e;
 }
 
 }  // namespace splat_b200

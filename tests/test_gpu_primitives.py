@@ -26,10 +26,16 @@ def _sort(keys, vals, begin, end):
 
 
 @pytest.mark.parametrize("n,bits,spread", [(1000, 32, 1), (1_000_000, 32, 1), (1_000_000, 32, 0),
-                                          (3_500_000, 9, 1), (5000, 9, 1), (777_777, 13, 1)])
+                                          (3_500_000, 9, 1), (5000, 9, 1), (777_777, 13, 1),
+                                          # 32-bit sorts run as one cooperative kernel when the
+                                          # 2048-key tiles fit one wave; 3 M keys fall back
+                                          (1, 32, 1), (2048, 32, 1), (2049, 32, 0), (3_000_000, 32, 1),
+                                          (100_000, 32, 2)])
 def test_radix_sort_is_stable(n, bits, spread):
     rng = np.random.default_rng(n + bits)
-    if spread:
+    if spread == 2:  # all keys equal: every pass trivial
+        keys = np.full(n, 0x40123456, np.uint32)
+    elif spread:
         keys = rng.integers(0, 1 << bits, size=n, dtype=np.uint64).astype(np.uint32)
     else:  # depth-like keys: float bits of values in one binade (top byte constant) with ties
         keys = np.round(rng.uniform(2.1, 3.9, size=n), 3).astype(np.float32).view(np.uint32)

@@ -20,14 +20,14 @@ s = scenes.make_gaussians(1_000_000, seed=0)
 ds = DeviceGaussians.from_host(s, 0)
 cam = scenes.ring_camera(0, 64)
 render(ds, cam, want_depth=False, ctx=ctx)
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 12)()
 lib = ctx.lib
 lib.splat_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 assert lib.splat_debug_stats(buf, 1) == 0, "not an instrumented build"
 from paper_2411_12788_b200 import capi  # noqa: E402
 from paper_2411_12788_b200.rasterizer import render_backward  # noqa: E402
 lib.splat_debug_bstats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-bbuf = (C.c_ulonglong * 8)()
+bbuf = (C.c_ulonglong * 12)()
 render(ds, cam, want_depth=False, ctx=ctx)
 torch.cuda.synchronize()
 lib.splat_debug_stats(buf, 1)
@@ -45,7 +45,8 @@ print(f"bwd eligible lanes per evaluation {bv[2] / max(bv[0], 1):.1f}, committin
 v = list(buf)
 names = ["warp-entries evaluated", "  of which exact 8x4 patch test fails", "  of which >=1 lane gate passes",
          "  exact patch passes but no lane passes", "entries staged (block cull kept)", "lanes active at eval (sum)",
-         "entries offered to staging"]
+         "entries offered to staging", "warp-batches with active lanes", "warp-batches needed (packed)",
+         "active pixel-batches", "CTA batches"]
 for n, x in zip(names, v):
     print(f"{n:45s} {x:,}")
 print(f"mean active lanes per evaluation {v[5] / max(v[0], 1):.1f}")
