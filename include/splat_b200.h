@@ -265,6 +265,21 @@ int splat_third_neighbor_distances(splat_ctx* ctx, const float* points_dev, int3
 int splat_reinit_gaussians(splat_ctx* ctx, const float* points_dev, const float* colors_dev, int32_t m,
                            float min_dist, const splat_params_mut* out);
 
+/* ---- native training step (trainer.cpp:208-240, one process) ------------------------------ */
+/* One optimisation step over n_views views, the body of the reference's training iteration run
+ * natively: for each view, render (splat_render), the loss (L1, or photometric_loss with
+ * lambda_dssim > 0) and render_backward with gradients summed over the views
+ * (ParamGrads::add), then OptimState::step on group_mask.  targets[k] is view k's H x W x 3
+ * target: device memory, or, with targets_on_host != 0, host memory (pinned for an asynchronous
+ * copy) that is copied on a side stream while the view's forward runs.  loss_host (nullable,
+ * n_views floats) receives each view's loss and makes the call synchronous; otherwise nothing
+ * is synchronised (loss_dev, nullable, gets the losses on the device). */
+int splat_train_step(splat_ctx* ctx, const splat_params_mut* params, const splat_param_grads* grads,
+                     const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
+                     uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
+                     int targets_on_host, const splat_raster_config* cfg, const float background[3],
+                     float lambda_dssim, float* loss_dev, float* loss_host);
+
 /* ---- SSIM and the photometric loss (loss.cpp:78-153) -------------- */
 /* ssim<float>: value_dev (device float) = mean SSIM of H x W x ch images a, b with the 11-tap
  * sigma-1.5 window; grad_dev (nullable) = d mean SSIM / d a.  Per-pixel values are the

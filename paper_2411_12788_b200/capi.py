@@ -249,6 +249,10 @@ _EXPORTS = {
     "splat_third_neighbor_distances": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_float, C.c_void_p]),
     "splat_reinit_gaussians": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_float,
                                          C.POINTER(ParamsMut)]),
+    "splat_train_step": (C.c_int, [C.c_void_p, C.POINTER(ParamsMut), C.POINTER(ParamGrads), C.POINTER(AdamMoments),
+                                   C.POINTER(AdamConfig), C.POINTER(C.c_int32), C.c_uint32, C.c_void_p, C.c_int32,
+                                   C.c_void_p, C.c_int, C.POINTER(RasterConfig), C.POINTER(C.c_float), C.c_float,
+                                   C.c_void_p, C.c_void_p]),
     "splat_sort_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),

@@ -137,6 +137,10 @@ struct splat_ctx {
     // cooperative depth sort: third key/value buffer + histogram/count scratch
     DevBuf ktmp, vtmp, coop_work;
     bool coop_sort = true;
+    // native train step: device staging of host targets, per-view losses, copy stream + events
+    DevBuf tgt_stage, step_loss;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_free = nullptr, ev_copied[8] = {};
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
@@ -637,6 +641,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
         return SPLAT_ERR_OUT_OF_MEMORY;
     }
     if (cudaStreamCreateWithFlags(&c->zstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_free, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd_start, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_zero, cudaEventDisableTiming) != cudaSuccess) {
         cudaFree(c->lc.work_counters);
@@ -667,6 +673,13 @@ int splat_ctx_destroy(splat_ctx* ctx) {
         cudaStreamSynchronize(ctx->zstream);
         cudaStreamDestroy(ctx->zstream);
     }
+    if (ctx->cstream) {
+        cudaStreamSynchronize(ctx->cstream);
+        cudaStreamDestroy(ctx->cstream);
+    }
+    if (ctx->ev_free) cudaEventDestroy(ctx->ev_free);
+    for (cudaEvent_t ev : ctx->ev_copied)
+        if (ev) cudaEventDestroy(ev);
     delete ctx->lc.prof;
     delete ctx;
     return SPLAT_OK;
@@ -1271,6 +1284,83 @@ int splat_reinit_gaussians(splat_ctx* ctx, const float* points, const float* col
     int rc = splat_third_neighbor_distances(ctx, points, m, min_dist, ctx->knn_dist.as<float>());
     if (rc) return rc;
     CK(launch_reinit_set(ctx->lc, points, colors, ctx->knn_dist.as<float>(), m, *out), "reinit set");
+    return SPLAT_OK;
+}
+
+int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param_grads* grads,
+                     const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
+                     uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
+                     int targets_on_host, const splat_raster_config* cfg, const float background[3],
+                     float lambda_dssim, float* loss_dev, float* loss_host) {
+    if (!ctx || !p || !grads || !moments || !adam || !step_count || !cams || !targets || n_views < 1)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "train_step: bad args");
+    const splat_gaussians g{p->centers, p->log_scales, p->rotations, p->opacity_logits, p->sh, p->n,
+                            p->active_sh_degree};
+    const float zero[3] = {0, 0, 0};
+    const float* bg = background ? background : zero;
+    cudaStream_t s = ctx->stream;
+    float* losses = loss_dev;
+    if (!losses) {
+        CK(ctx->step_loss.ensure((size_t)n_views * 4), "alloc loss");
+        losses = ctx->step_loss.as<float>();
+    }
+    // host targets: staged in device memory by a side stream, up to 8 views in flight; view k's
+    // backward waits only for its own copy, so the transfer overlaps the view's forward
+    const int slots = 8;
+    size_t view_floats = 0;
+    if (targets_on_host) {
+        for (int k = 0; k < n_views && k < slots; ++k) view_floats = std::max(view_floats, (size_t)cams[k].width * cams[k].height * 3);
+        for (int k = 0; k < n_views; ++k)
+            if ((size_t)cams[k].width * cams[k].height * 3 > view_floats) view_floats = (size_t)cams[k].width * cams[k].height * 3;
+        CK(ctx->tgt_stage.ensure(view_floats * 4 * (size_t)std::min(n_views, slots)), "alloc target staging");
+        for (int k = 0; k < slots; ++k)
+            if (!ctx->ev_copied[k]) CK(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming), "event");
+    }
+    auto issue_copy = [&](int k) -> int {
+        const int slot = k % slots;
+        float* dst = ctx->tgt_stage.as<float>() + (size_t)slot * view_floats;
+        const size_t bytes = (size_t)cams[k].width * cams[k].height * 3 * 4;
+        CK(cudaMemcpyAsync(dst, targets[k], bytes, cudaMemcpyHostToDevice, ctx->cstream), "target copy");
+        CK(cudaEventRecord(ctx->ev_copied[slot], ctx->cstream), "copy event");
+        return SPLAT_OK;
+    };
+    int rc;
+    if (targets_on_host) {
+        // the staging slots are free once everything already queued on the compute stream ran
+        CK(cudaEventRecord(ctx->ev_free, s), "record");
+        CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_free, 0), "wait");
+        for (int k = 0; k < std::min(n_views, slots); ++k)
+            if ((rc = issue_copy(k))) return rc;
+    }
+    for (int k = 0; k < n_views; ++k) {
+        if ((rc = run_forward(ctx, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr))) return rc;
+        const float* tgt = targets[k];
+        if (targets_on_host) {
+            const int slot = k % slots;
+            CK(cudaStreamWaitEvent(s, ctx->ev_copied[slot], 0), "wait target");
+            tgt = ctx->tgt_stage.as<float>() + (size_t)slot * view_floats;
+        }
+        const int acc = k > 0 ? 1 : 0;
+        if (lambda_dssim > 0.0f) {
+            const int w = cams[k].width, h = cams[k].height;
+            CK(ctx->d_color_buf.ensure((size_t)w * h * 3 * 4), "alloc d_color");
+            float* dc = ctx->d_color_buf.as<float>();
+            if ((rc = splat_photometric_loss(ctx, ctx->st.color, tgt, w, h, 3, lambda_dssim, dc, losses + k))) return rc;
+            if ((rc = run_backward(ctx, &g, &cams[k], cfg, dc, nullptr, nullptr, bg, grads, acc, nullptr))) return rc;
+        } else {
+            if ((rc = run_backward(ctx, &g, &cams[k], cfg, nullptr, tgt, nullptr, bg, grads, acc, losses + k))) return rc;
+        }
+        if (targets_on_host && k + slots < n_views) {  // refill the slot once this view's backward ran
+            CK(cudaEventRecord(ctx->ev_free, s), "record");
+            CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_free, 0), "wait");
+            if ((rc = issue_copy(k + slots))) return rc;
+        }
+    }
+    if ((rc = splat_adam_step(ctx, p, grads, moments, adam, step_count, group_mask))) return rc;
+    if (loss_host) {
+        CK(cudaMemcpyAsync(loss_host, losses, (size_t)n_views * 4, cudaMemcpyDeviceToHost, s), "read loss");
+        CK(cudaStreamSynchronize(s), "sync");
+    }
     return SPLAT_OK;
 }
 

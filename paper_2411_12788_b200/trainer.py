@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import capi
-from .capi import Camera, RasterConfig, RenderOutputs, as_fp
+from .capi import Camera, RasterConfig
 from .rasterizer import Context, DeviceGaussians, DeviceGrads, OptimState, _torch
 
 
@@ -63,10 +63,7 @@ class ViewTrainer:
         self.lambda_dssim = float(lambda_dssim)
         self.pairs_last_step: list[int] = []
         self.survivors_last_step: list[int] = []
-        self._empty_out = RenderOutputs()
-        self._gs = params.struct()
         self._gr = self.grads.struct()
-        self._staging = None
 
     @property
     def world_size(self) -> int:
@@ -80,63 +77,59 @@ class ViewTrainer:
             return self.grads.flat[: 3 * n]
         return self.grads.flat[: 59 * n]
 
-    def _views(self, cams: Sequence[Camera], targets, ready=None) -> None:
-        """`ready[j]` (optional): an event the backward of view j waits for (its target's H2D
-        copy), so the copy overlaps that view's forward."""
+    def _native(self, cams: Sequence[Camera], ptrs, on_host: bool, group_mask: int, loss_host=None) -> None:
+        """splat_train_step: the whole per-step loop (render, loss, backward summed over views,
+        Adam on group_mask; group_mask 0 = no optimiser step) in one native call."""
         lib, h = self.ctx.lib, self.ctx.h
-        self.pairs_last_step = []
-        self.survivors_last_step = []
-        for j, (cam, tgt) in enumerate(zip(cams, targets)):
-            self.ctx.check(lib.splat_render(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), None, self.bg,
-                                            C.byref(self._empty_out), None))
-            ns_, np_ = C.c_int64(), C.c_int64()
-            lib.splat_forward_counts(h, C.byref(ns_), C.byref(np_), None, None)
-            self.pairs_last_step.append(np_.value)
-            self.survivors_last_step.append(ns_.value)
-            if ready is not None:
-                self.torch.cuda.current_stream().wait_event(ready[j])
-            if self.lambda_dssim > 0.0:  # photometric_loss -> render_backward (trainer.cpp:226-239)
-                self.ctx.check(lib.splat_render_backward_photometric(
-                    h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg), as_fp(tgt.data_ptr()), None, self.bg,
-                    C.byref(self._gr), 1 if j > 0 else 0, self.lambda_dssim, as_fp(self.loss.data_ptr() + 4 * j)))
-            else:
-                self.ctx.check(lib.splat_render_backward_l1(h, C.byref(self._gs), C.byref(cam), C.byref(self.cfg),
-                                                            as_fp(tgt.data_ptr()), None, self.bg, C.byref(self._gr),
-                                                            1 if j > 0 else 0, as_fp(self.loss.data_ptr() + 4 * j)))
+        v = len(cams)
+        if v > self.loss.numel():
+            raise ValueError("more views than max_views")
+        cam_arr = (Camera * v)(*cams)
+        tp = (C.c_void_p * v)(*ptrs)
+        t = C.c_int32(self.opt.t)
+        self.ctx.check(lib.splat_train_step(
+            h, C.byref(self.params.mut()), C.byref(self._gr), C.byref(self.opt._moments()), C.byref(self.opt.config),
+            C.byref(t), group_mask, cam_arr, v, tp, 1 if on_host else 0, C.byref(self.cfg), self.bg,
+            self.lambda_dssim, self.loss.data_ptr(), loss_host))
+        if group_mask:
+            self.opt.t = t.value
+        ns_, np_ = C.c_int64(), C.c_int64()
+        lib.splat_forward_counts(h, C.byref(ns_), C.byref(np_), None, None)  # the last view's
+        self.pairs_last_step = [np_.value] * v
+        self.survivors_last_step = [ns_.value] * v
 
-    def _finish(self) -> None:
-        if self.world_size > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
+    def _views(self, cams: Sequence[Camera], targets) -> None:
+        """Render + loss + backward of the views (gradients summed), no optimiser step."""
+        self._native(cams, [t.data_ptr() for t in targets], False, 0)
+
+    def _finish_distributed(self) -> None:
+        import torch.distributed as dist
+        dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
         self.opt.step(self.params, self.grads, self.group_mask, self.ctx)
 
-    def step(self, cams: Sequence[Camera], targets, ready=None) -> "object":
+    def step(self, cams: Sequence[Camera], targets) -> "object":
         """Device-resident step: targets are CUDA tensors [H, W, 3]. Returns the per-view loss
-        tensor (device); nothing is synchronised."""
+        tensor (device); nothing is synchronised.  One process: a single splat_train_step call;
+        several ranks: views + backward natively, NCCL all-reduce, then Adam."""
         self.ctx.bind_stream()
-        self._views(cams, targets, ready)
-        self._finish()
+        ptrs = [t.data_ptr() for t in targets]
+        if self.world_size > 1:
+            self._native(cams, ptrs, False, 0)
+            self._finish_distributed()
+        else:
+            self._native(cams, ptrs, False, self.group_mask)
         return self.loss[: len(cams)]
 
     def step_host(self, cams: Sequence[Camera], targets_host) -> np.ndarray:
         """End-to-end step through the public API: each view's target is copied host->device
-        (pinned, async) inside the step and the per-view losses are read back to the host.
-
-        The copies run on a side stream and each view's backward waits only for its own target,
-        so the H2D transfer overlaps that view's forward (preprocess, sort, binning, blend)."""
-        torch = self.torch
-        k = len(cams)
-        shape = tuple(targets_host[0].shape)
-        if self._staging is None or self._staging.shape[0] < k or tuple(self._staging.shape[1:]) != shape:
-            self._staging = torch.empty((k, *shape), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
-            self._copy_stream = torch.cuda.Stream(device=self.ctx.device)
-            self._copy_events = [torch.cuda.Event() for _ in range(k)]
-        compute = torch.cuda.current_stream(self.ctx.device)
-        cs = self._copy_stream
-        cs.wait_stream(compute)  # the staging buffer is free once the previous step's backward ran
-        with torch.cuda.stream(cs):
-            for j in range(k):
-                self._staging[j].copy_(targets_host[j], non_blocking=True)
-                self._copy_events[j].record(cs)
-        self.step(cams, [self._staging[j] for j in range(k)], ready=self._copy_events[:k])
-        return self.loss[:k].cpu().numpy()
+        (pinned, async, on the library's copy stream, overlapping that view's forward) inside the
+        step and the per-view losses are read back to the host (the call returns after the step)."""
+        self.ctx.bind_stream()
+        ptrs = [t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data for t in targets_host]
+        out = np.zeros(len(cams), np.float32)
+        if self.world_size > 1:
+            self._native(cams, ptrs, True, 0)
+            self._finish_distributed()
+            return self.loss[: len(cams)].cpu().numpy()
+        self._native(cams, ptrs, True, self.group_mask, out.ctypes.data)
+        return out
