@@ -279,7 +279,7 @@ struct PixBwd {
     uint32_t bits;
 };
 
-template <bool THR>
+template <bool THR, bool COMPACT>
 __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
                                                          const uint32_t* __restrict__ pair_gauss,
                                                          const ProjRec* __restrict__ rec,
@@ -289,7 +289,8 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                                                          const float* __restrict__ color,
                                                          const float* __restrict__ target, float inv_n,
                                                          float* __restrict__ loss_partials,
-                                                         float4* __restrict__ grad2d) {
+                                                         float4* __restrict__ grad2d,
+                                                         const uint32_t* __restrict__ bidx, int bcnt) {
     constexpr int BW = 8, BH = 8;
     __shared__ StageSmem<32> sm;
     __shared__ StageRaw<32> raw;
@@ -339,11 +340,31 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
         const float ws = warp_sum(l);
         if (lane == 0) loss_partials[bid] = ws;
     }
+    if (COMPACT) {  // tile-list positions -> positions in the block's staged list (bidx increases)
+        __shared__ uint32_t s_bidx[kBlockList];
+        for (int i = lane; i < bcnt; i += 32) s_bidx[i] = bidx[i];
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (P[h].last < 0) continue;
+            int lo = 0, hi = bcnt - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int)s_bidx[mid] <= P[h].last) lo = mid;
+                else hi = mid - 1;
+            }
+            P[h].last = lo;
+        }
+        __syncwarp();
+    }
     const int wlA = (int)__reduce_max_sync(0xffffffffu, (unsigned)(P[0].last + 1)) - 1;
     const int wlB = (int)__reduce_max_sync(0xffffffffu, (unsigned)(P[1].last + 1)) - 1;
     const int block_last = max(wlA, wlB);
-    const uint32_t start = ranges[2 * tile];
+    // COMPACT: the forward's staged (block-culled) list of this block, positions 0.. (last_index
+    // holds positions in it); else the tile list from ranges, culled again while staging
+    const uint32_t start = COMPACT ? 0u : ranges[2 * tile];
     if (block_last < (int)start) return;  // nothing committed in this block
+    const uint32_t* list = COMPACT ? pair_gauss + (size_t)bid * kBlockList : pair_gauss;
 
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
     constexpr uint32_t kRowsA = 0xfu << 16, kRowsB = 0xf0u << 16;
@@ -354,7 +375,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
         const int i = block_last - b * 32 - t;
         return i >= (int)start ? i : -1;
     };
-    StagePipe<32, decltype(pos)> pipe(pos, pair_gauss, rec, &raw);
+    StagePipe<32, decltype(pos), !COMPACT> pipe(pos, list, rec, &raw);
     pipe.start();
     const int nb = (block_last + 1 - (int)start + 31) / 32;
     for (int b = 0; b < nb; ++b) {
@@ -439,14 +460,21 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
     const ProjRec* __restrict__ rec, const float* __restrict__ t_final, const int32_t* __restrict__ last_index,
     float bg0, float bg1, float bg2, const float* __restrict__ d_color, const float* __restrict__ color,
     const float* __restrict__ target, float inv_n, float* __restrict__ loss_partials, float4* __restrict__ grad2d,
-    int nblocks, int* __restrict__ counter) {
+    int nblocks, int* __restrict__ counter, const uint32_t* __restrict__ blist, const uint32_t* __restrict__ bidx,
+    const int32_t* __restrict__ bcount) {
     for (;;) {
         int b = 0;
         if (threadIdx.x == 0) b = atomicAdd(counter, 1);
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b >= nblocks) break;
-        blend_backward_block_px2<THR>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color,
-                                      color, target, inv_n, loss_partials, grad2d);
+        const int bc = blist ? bcount[b] : kBlockList + 1;
+        if (bc <= kBlockList)
+            blend_backward_block_px2<THR, true>(b, cp, ranges, blist, rec, t_final, last_index, bg0, bg1, bg2,
+                                                d_color, color, target, inv_n, loss_partials, grad2d,
+                                                bidx + (size_t)b * kBlockList, bc);
+        else
+            blend_backward_block_px2<THR, false>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2,
+                                                 d_color, color, target, inv_n, loss_partials, grad2d, nullptr, 0);
         __syncwarp();
     }
 }
@@ -589,7 +617,8 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
                                   const uint32_t* pair_gauss, const ProjRec* rec, const float* t_final,
                                   const int32_t* last_index, const float bg[3], const float* d_color,
-                                  const float* color, const float* target, float* loss_partials, float* grad2d) {
+                                  const float* color, const float* target, float* loss_partials, float* grad2d,
+                                  const uint32_t* blist, const uint32_t* bidx, const int32_t* bcount) {
     const int ts = cp.tile_size;
     const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
@@ -631,11 +660,13 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
             if (k)
                 blend_backward_px2_persistent<true><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
-                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);
+                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
+                    bidx, bcount);
             else
                 blend_backward_px2_persistent<false><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
-                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);
+                    inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
+                    bidx, bcount);
         } else if (cp.apply_thresholds) BLEND_BWD(true);
         else BLEND_BWD(false);
 #undef BLEND_BWD

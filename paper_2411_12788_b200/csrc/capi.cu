@@ -109,6 +109,9 @@ struct FwdState {
     const float* g_centers = nullptr;  // identity of the inputs (reuse check)
     const uint8_t* mask = nullptr;
     const uint32_t* order = nullptr;  // survivors in (depth, index) order (device)
+    const uint32_t* blist = nullptr;  // per-block staged lists of the forward (or null)
+    const uint32_t* bidx = nullptr;
+    const int32_t* bcount = nullptr;
     float* color = nullptr;
     float* alpha = nullptr;
     float* depth = nullptr;
@@ -139,6 +142,8 @@ struct splat_ctx {
     bool coop_sort = true;
     // native train step: device staging of host targets, per-view losses, copy stream + events
     DevBuf tgt_stage, step_loss;
+    // per 8 x 8 block: the staged list entries the forward walked (replayed by the backward)
+    DevBuf blist, bidx, bcount;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_free = nullptr, ev_copied[8] = {};
     uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
@@ -420,6 +425,21 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     fo.max_pixel_count = report ? rep->max_pixel_count : nullptr;
     fo.t_final = ctx->t_final.as<float>();
     fo.last_index = ctx->last_index.as<int32_t>();
+    // the backward's one-warp 8 x 8 kernel replays the forward's per-block staged lists
+    const bool block_lists = lc.bwd_px2 && lc.persistent_blend && lc.work_counters && cp.block_w == 8 &&
+                             cp.block_h == 8 && cp.tile_size >= 16 && !rep;
+    fo.blist = nullptr;
+    fo.bidx = nullptr;
+    fo.bcount = nullptr;
+    if (block_lists && n > 0) {
+        const size_t n_blocks = (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8);
+        CK(ctx->blist.ensure(n_blocks * kBlockList * 4), "alloc block lists");
+        CK(ctx->bidx.ensure(n_blocks * kBlockList * 4), "alloc block lists");
+        fo.bidx = ctx->bidx.as<uint32_t>();
+        CK(ctx->bcount.ensure(n_blocks * 4), "alloc block counts");
+        fo.blist = ctx->blist.as<uint32_t>();
+        fo.bcount = ctx->bcount.as<int32_t>();
+    }
     // the gradient zero-fill of a following backward may start here: it then overlaps the blend
     // kernels (issue-bound) rather than the latency-bound sort and binning
     CK(cudaEventRecord(ctx->ev_fwd_start, s), "record forward start");
@@ -440,6 +460,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     st.alpha = fo.alpha;
     st.depth = fo.depth;
     st.max_contributor = fo.max_contributor;
+    st.blist = fo.blist;
+    st.bidx = fo.bidx;
+    st.bcount = fo.bcount;
     st.valid = true;
     return SPLAT_OK;
 }
@@ -602,7 +625,7 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
         const uint32_t* sorted_gauss = ctx->pair_gauss[st.pairs_in_alt ? 1 : 0].as<uint32_t>();
         CK(launch_blend_backward(lc, st.cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
                                  ctx->t_final.as<float>(), ctx->last_index.as<int32_t>(), bg, d_color, st.color, target,
-                                 partials, ctx->grad2d.as<float>()),
+                                 partials, ctx->grad2d.as<float>(), st.blist, st.bidx, st.bcount),
            "blend backward");
     }
     if (n > 0) {

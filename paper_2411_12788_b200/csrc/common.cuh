@@ -276,7 +276,8 @@ struct StageRaw {
 };
 
 // PosFn pos(b, t): list position of thread t's entry in batch b, or -1 when batch b has no entry t.
-template <int CAP, typename PosFn>
+// CULL = false: the list is already block-culled (the forward's per-block list): keep every entry.
+template <int CAP, typename PosFn, bool CULL = true>
 struct StagePipe {
     PosFn pos;
     const uint32_t* __restrict__ pair_gauss;
@@ -325,7 +326,7 @@ struct StagePipe {
             rr.r0 = raw->r[tid][0];
             rr.r1 = raw->r[tid][1];
             rr.r2 = raw->r[tid][2];
-            keep = may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1);
+            keep = CULL ? may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1) : true;
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) sm.wcnt[warp] = __popc(m);

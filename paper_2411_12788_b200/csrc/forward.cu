@@ -413,6 +413,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
     const uint32_t a_gid = smem_base(sm.gid), a_idx = smem_base(sm.idx);
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, wmax = 0.0f;
     int32_t amax_gid = -1, last = -1;
+    int run = 0;  // entries staged so far (position in the block list)
     bool done = !inside;
     if (REPORT) {
         s_imp[tid] = 0.0f;
@@ -429,6 +430,10 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
         for (int b = 0; b < nb; ++b) {
             const int cnt = pipe.stage(b, !done, bx0, bx1, by0, by1, sm);
             if (cnt < 0) break;
+            if (!REPORT && out.blist && run + cnt <= kBlockList && tid < cnt) {
+                out.blist[(size_t)bid * kBlockList + run + tid] = sm.gid[tid];
+                out.bidx[(size_t)bid * kBlockList + run + tid] = (uint32_t)sm.idx[tid];
+            }
 #ifdef SPLAT_STATS
             {
                 const unsigned wa = __ballot_sync(0xffffffffu, !done);
@@ -571,9 +576,11 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                 }
             }
             // the next stage() starts with a barrier: staged entries stay until every warp is done
+            run += cnt;
         }
         pipe.finish();
     }
+    if (!REPORT && out.bcount && tid == 0) out.bcount[bid] = run;
     if (!inside) return;
     const size_t pix = (size_t)py * cp.width + px;
     if (REPORT && amax_gid >= 0) atomicAdd(&out.max_pixel_count[amax_gid], 1);

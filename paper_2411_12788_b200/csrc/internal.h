@@ -127,7 +127,15 @@ struct FwdOutputs {
     int32_t* max_pixel_count;// [n] or null
     float* t_final;          // [H][W] backward state or null
     int32_t* last_index;     // [H][W] backward state or null
+    // Per 8 x 8 block, the staged (block-culled) list entries the forward walked, for the
+    // backward to replay without re-culling: blist[block][kBlockList] Gaussian ids, bidx the same
+    // entries' tile-list positions (increasing), bcount[block] = entries walked (> kBlockList:
+    // not stored, the backward re-culls the tile list).
+    uint32_t* blist;         // or null
+    uint32_t* bidx;
+    int32_t* bcount;
 };
+constexpr int kBlockList = 512;
 
 // K6 (+K7 depth epilogue): per-tile front-to-back blend.
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
@@ -156,7 +164,9 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const uint32_t* pair_gauss, const ProjRec* rec,
                                   const float* t_final, const int32_t* last_index, const float bg[3],
                                   const float* d_color, const float* color, const float* target,
-                                  float* loss_partials, float* grad2d);
+                                  float* loss_partials, float* grad2d,
+                                  const uint32_t* blist = nullptr, const uint32_t* bidx = nullptr,
+                                  const int32_t* bcount = nullptr);
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
 // K10 chain.  list: scratch of n_surv + 1 words (touched-Gaussian list; touched <= survivors).
 // prezeroed: a fresh (accumulate = 0) gradient whose rows were already zero-filled (side stream);
