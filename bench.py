@@ -42,15 +42,34 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=20,
                     help="extra steps after the timed region, with per-kernel CUDA events (breakdown/roofline)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--views", type=int, default=1, help="ring views per rank per step")
-    ap.add_argument("--gaussians", type=int, default=1_000_000)
+    ap.add_argument("--config", type=int, choices=(1, 4), default=1,
+                    help="1: the metric's workload (default); 4: BASELINE config 4, 3 M Gaussians, 8 views per rank "
+                         "from 256 ring views, all 59 gradients all-reduced, Adam on every group")
+    ap.add_argument("--views", type=int, default=None, help="ring views per rank per step (default 1, config 4: 8)")
+    ap.add_argument("--gaussians", type=int, default=None, help="default 1 M (config 4: 3 M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.views is None:
+        a.views = 8 if a.config == 4 else 1
+    if a.gaussians is None:
+        a.gaussians = 3_000_000 if a.config == 4 else 1_000_000
+    return a
+
+
+METRIC4 = "fwd+bwd views/s (3M Gaussians, 1237x822, SH3, 8 views/GPU, all-param Adam) at 1/2/4/8 B200"
 
 
 def workload_config(args, world):
+    if args.config == 4:
+        return {"workload": "cfg4: 3M Gaussians SH3, 8 ring views per rank per step from 256, 1237x822, L1 vs "
+                            "perturbed-means target, fwd+bwd summed over views, 59N-float gradient all-reduce, "
+                            "Adam on all parameter groups",
+                "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
+                "ring_views": 256, "n_ranks": world,
+                "allreduce": "59N gradient floats (fp32, NCCL sum) when N > 1",
+                "l2": "inputs larger than L2; views rotate each step", "scene_seed": 0}
     return {"workload": "cfg1: 1M Gaussians SH3, 1237x822 ring views, L1 vs perturbed-means target, "
                         "fwd+bwd (59 grads) + Adam(means, lr 1.6e-4)",
             "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
@@ -307,16 +326,18 @@ def run_ours(args):
     s = scenes.make_gaussians(args.gaussians, seed=0)
     ds = DeviceGaussians.from_host(s, device)
     dt = DeviceGaussians.from_host(scenes.perturbed(s), device)
-    cams = [scenes.ring_camera(k, RING) for k in range(RING)]
+    ring = 256 if args.config == 4 else RING
+    cams = [scenes.ring_camera(k, ring) for k in range(ring)]
     targets = [render(dt, cam, want_depth=False, ctx=ctx).color.clone() for cam in cams]
     del dt
-    trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=capi.GROUP_CENTERS, ctx=ctx, max_views=max(args.views, 1))
+    gmask = capi.GROUP_ALL if args.config == 4 else capi.GROUP_CENTERS
+    trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=gmask, ctx=ctx, max_views=max(args.views, 1))
     V = args.views
 
     from paper_2411_12788_b200.trainer import views_for as _views_for
 
     def views_for(step):
-        idx = _views_for(step, rank, world, V, RING)
+        idx = _views_for(step, rank, world, V, ring)
         return [cams[i] for i in idx], [targets[i] for i in idx], idx
 
     stream = torch.cuda.current_stream()
@@ -354,6 +375,7 @@ def run_ours(args):
     # ---- per-kernel breakdown: a separate profiled pass (CUDA events around every launch) ------
     lib.splat_profile_enable(ctx.h, 1)
     p_steps = max(1, args.profile_steps)
+    trainer.ar_events = [] if world > 1 else None
     for st in range(args.warmup + args.steps, args.warmup + args.steps + p_steps):
         c, t, _ = views_for(st)
         trainer.step(c, t)
@@ -365,6 +387,15 @@ def run_ours(args):
     ctx.check(lib.splat_profile_read(ctx.h, names, 4096, tot, cnt, 64, C.byref(nk)))
     lib.splat_profile_enable(ctx.h, 0)
     kern = {nm: (tot[i], cnt[i]) for i, nm in enumerate(names.value.decode().split("\n")[: nk.value])}
+    allreduce = None
+    if world > 1 and trainer.ar_events:
+        ar_ms = float(np.mean([a.elapsed_time(b) for a, b in trainer.ar_events]))
+        nbytes = trainer.reduce_slice().numel() * 4
+        allreduce = {"bytes": nbytes, "ms": ar_ms, "algbw_gbs": nbytes / (ar_ms * 1e6),
+                     "busbw_gbs": 2 * (world - 1) / world * nbytes / (ar_ms * 1e6),
+                     "note": "NCCL all_reduce of the optimised gradient slice, CUDA events on the compute stream "
+                             "(profiled pass)"}
+    trainer.ar_events = None
     if world > 1:
         t_ms = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
@@ -375,7 +406,7 @@ def run_ours(args):
     # ---- e2e through the public API with host buffers -------------------------------------------
     e2e = None
     if not args.no_e2e:
-        host_t = [targets[i].cpu().pin_memory() for i in range(min(RING, 8 * V))]
+        host_t = [targets[i].cpu().pin_memory() for i in range(min(ring, 8 * V))]
         for st in range(2):
             c, _, idx = views_for(st)
             trainer.step_host(c, [host_t[i % len(host_t)] for i in idx])
@@ -432,7 +463,7 @@ def run_ours(args):
                      "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 1:
         threads = cpu_threads_default(args, 16)
         try:
             cpu = cpu_views_per_s(args.gaussians, threads, 1)
@@ -442,12 +473,16 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC4 if args.config == 4 else METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE cfg1 shapes)",
+                "vs_baseline": None, "dtype": "f32",
+                "data": f"synthetic (seeded, BASELINE cfg{args.config} shapes)",
                 "config": workload_config(args, world), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
                 "pairs_per_view": avg_pairs, "survivors_per_view": n_surv, "kernel_breakdown": breakdown}
+        if allreduce:
+            line["allreduce"] = allreduce
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -104,7 +104,14 @@ class ViewTrainer:
 
     def _finish_distributed(self) -> None:
         import torch.distributed as dist
+        ev = None
+        if getattr(self, "ar_events", None) is not None:  # bench: time the exchange
+            ev = (self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
+        if ev is not None:
+            ev[1].record()
+            self.ar_events.append(ev)
         self.opt.step(self.params, self.grads, self.group_mask, self.ctx)
 
     def step(self, cams: Sequence[Camera], targets) -> "object":
