@@ -30,6 +30,7 @@ NAME_MAP = [  # (regex on the demangled ncu kernel name, bench launch name)
     (r"bin_count_kernel", "bin_count"),
     (r"bin_emit_kernel", "bin_emit"),
     (r"bin_map_kernel", "bin_map"),
+    (r"radix_coop_kernel", "radix_sort"),
     (r"radix_onesweep_kernel", "radix_onesweep"),
     (r"radix_histogram_kernel", "radix_histogram"),
     (r"scan_lookback_kernel", "scan"),
