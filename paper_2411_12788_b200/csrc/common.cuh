@@ -277,39 +277,51 @@ struct StageRaw {
 
 // PosFn pos(b, t): list position of thread t's entry in batch b, or -1 when batch b has no entry t.
 // CULL = false: the list is already block-culled (the forward's per-block list): keep every entry.
-template <int CAP, typename PosFn, bool CULL = true>
+template <int CAP, typename PosFn, bool CULL = true, int ITEMS = 1>
 struct StagePipe {
+    // ITEMS entries per thread and batch: slot s = q * blockDim.x + tid holds list position
+    // pos(b, s); batches are CAP = ITEMS * blockDim.x entries, compacted in slot order.
     PosFn pos;
     const uint32_t* __restrict__ pair_gauss;
     const ProjRec* __restrict__ rec;
     StageRaw<CAP>* raw;
-    int idx_f;       // entry whose record is in flight to raw (batch b)
-    uint32_t gid_f;
-    int idx_n;       // entry of batch b + 1, id loaded into gid_n
-    uint32_t gid_n;
+    int idx_f[ITEMS];       // entries whose records are in flight to raw (batch b)
+    uint32_t gid_f[ITEMS];
+    int idx_n[ITEMS];       // entries of batch b + 1, ids loaded into gid_n
+    uint32_t gid_n[ITEMS];
 
     __device__ __forceinline__ StagePipe(PosFn p, const uint32_t* pg, const ProjRec* rc, StageRaw<CAP>* rw)
         : pos(p), pair_gauss(pg), rec(rc), raw(rw) {}
 
     __device__ __forceinline__ void launch_copy() {
-        if (idx_f >= 0) {
-            const float4* src = reinterpret_cast<const float4*>(rec + gid_f);
-            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&raw->r[threadIdx.x][0]);
-            cp_async16(dst, src);
-            cp_async16(dst + 16u, src + 1);
-            cp_async16(dst + 32u, src + 2);
-        }
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q)
+            if (idx_f[q] >= 0) {
+                const float4* src = reinterpret_cast<const float4*>(rec + gid_f[q]);
+                const uint32_t dst =
+                    (uint32_t)__cvta_generic_to_shared(&raw->r[q * blockDim.x + threadIdx.x][0]);
+                cp_async16(dst, src);
+                cp_async16(dst + 16u, src + 1);
+                cp_async16(dst + 32u, src + 2);
+            }
         cp_async_commit();
     }
 
     // Batch 0 in flight, batch 1's ids loading.
     __device__ __forceinline__ void start() {
-        const int t = threadIdx.x;
-        idx_f = pos(0, t);
-        gid_f = idx_f >= 0 ? pair_gauss[idx_f] : 0u;
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            const int sl = q * blockDim.x + threadIdx.x;
+            idx_f[q] = pos(0, sl);
+            gid_f[q] = idx_f[q] >= 0 ? pair_gauss[idx_f[q]] : 0u;
+        }
         launch_copy();
-        idx_n = pos(1, t);
-        gid_n = idx_n >= 0 ? __ldg(pair_gauss + idx_n) : 0u;
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            const int sl = q * blockDim.x + threadIdx.x;
+            idx_n[q] = pos(1, sl);
+            gid_n[q] = idx_n[q] >= 0 ? __ldg(pair_gauss + idx_n[q]) : 0u;
+        }
     }
 
     // Stage batch b (whose records are in flight): cull + compact into sm, then launch batch
@@ -320,41 +332,57 @@ struct StagePipe {
         cp_async_wait_all();
         // raw is complete and visible; every thread is done reading the previous staging area
         if (__syncthreads_count(active) == 0) return -1;
-        bool keep = false;
-        ProjRec rr;
-        if (idx_f >= 0) {
-            rr.r0 = raw->r[tid][0];
-            rr.r1 = raw->r[tid][1];
-            rr.r2 = raw->r[tid][2];
-            keep = CULL ? may_contribute(rr.r0, rr.r1, rr.r2.w, bx0, bx1, by0, by1) : true;
+        bool keep[ITEMS];
+        unsigned m[ITEMS];
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            keep[q] = false;
+            if (idx_f[q] >= 0) {
+                const int sl = q * blockDim.x + tid;
+                keep[q] = CULL ? may_contribute(raw->r[sl][0], raw->r[sl][1], raw->r[sl][2].w, bx0, bx1, by0, by1)
+                               : true;
+            }
+            m[q] = __ballot_sync(0xffffffffu, keep[q]);
+            if (lane == 0) sm.wcnt[q * nwarps + warp] = __popc(m[q]);
         }
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) sm.wcnt[warp] = __popc(m);
         __syncthreads();
-        int off = 0, total = 0;
-        for (int w = 0; w < nwarps; ++w) {
-            const int c = sm.wcnt[w];
-            off += w < warp ? c : 0;
-            total += c;
-        }
-        if (keep) {
-            const int p = off + __popc(m & lanemask_lt());
-            const int X0 = max(range_lo(rr.r1.z), bx0) - bx0, X1 = min(range_hi(rr.r1.z), bx1) - bx0;
-            const int Y0 = max(range_lo(rr.r1.w), by0) - by0, Y1 = min(range_hi(rr.r1.w), by1) - by0;
+        int total = 0;
+        for (int w = 0; w < ITEMS * nwarps; ++w) total += sm.wcnt[w];
+        const unsigned lt = lanemask_lt();
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            if (!keep[q]) continue;
+            int off = 0;
+            for (int w = 0; w < q * nwarps + warp; ++w) off += sm.wcnt[w];
+            const int p = off + __popc(m[q] & lt);
+            const int sl = q * blockDim.x + tid;  // re-read from shared memory: no records held across the barrier
+            ProjRec r;
+            r.r0 = raw->r[sl][0];
+            r.r1 = raw->r[sl][1];
+            r.r2 = raw->r[sl][2];
+            const int X0 = max(range_lo(r.r1.z), bx0) - bx0, X1 = min(range_hi(r.r1.z), bx1) - bx0;
+            const int Y0 = max(range_lo(r.r1.w), by0) - by0, Y1 = min(range_hi(r.r1.w), by1) - by0;
             const uint32_t cols = ((1u << X1) - 1u) & ~((1u << X0) - 1u);
             const uint32_t rows = ((1u << Y1) - 1u) & ~((1u << Y0) - 1u);
-            sm.r0[p] = rr.r0;
-            sm.r1[p] = make_float4(rr.r1.x, rr.r1.y, __uint_as_float(cols | (rows << 16)), rr.r2.w);
-            sm.r2[p] = rr.r2;
-            sm.gid[p] = gid_f;
-            sm.idx[p] = idx_f;
+            sm.r0[p] = r.r0;
+            sm.r1[p] = make_float4(r.r1.x, r.r1.y, __uint_as_float(cols | (rows << 16)), r.r2.w);
+            sm.r2[p] = r.r2;
+            sm.gid[p] = gid_f[q];
+            sm.idx[p] = idx_f[q];
         }
         __syncthreads();  // staged batch visible; raw reads done
-        idx_f = idx_n;
-        gid_f = gid_n;
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            idx_f[q] = idx_n[q];
+            gid_f[q] = gid_n[q];
+        }
         launch_copy();
-        idx_n = pos(b + 2, tid);
-        gid_n = idx_n >= 0 ? __ldg(pair_gauss + idx_n) : 0u;
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            const int sl = q * blockDim.x + tid;
+            idx_n[q] = pos(b + 2, sl);
+            gid_n[q] = idx_n[q] >= 0 ? __ldg(pair_gauss + idx_n[q]) : 0u;
+        }
         return total;
     }
 
