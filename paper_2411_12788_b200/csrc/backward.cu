@@ -25,32 +25,9 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// Transpose-reduce of 12 per-lane values (four groups of 3) across the warp in 18 shuffles
-// (a butterfly would take 60): the first two levels exchange the half a lane does not keep, the
-// last three reduce the 3 remaining values.  On return, lanes 0, 8, 16, 24 hold the warp totals of
-// groups 0, 1, 2, 3 (values 3g .. 3g+2) in out[0..2].
-__device__ __forceinline__ void warp_reduce12(const float v[12], int lane, float out[3]) {
-    const bool a = lane & 16, b = lane & 8;
-    float u[6];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-        const float send = a ? v[i] : v[6 + i];
-        const float keep = a ? v[6 + i] : v[i];
-        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const float send = b ? u[i] : u[3 + i];
-        const float keep = b ? u[3 + i] : u[i];
-        out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
-}
-
-// The same transpose reduction for 24 values (two entries x four groups of 3) in 27 shuffles: on
+// Transpose reduction of 24 per-lane values (two entries x four groups of 3) across the warp in
+// 27 shuffles (a butterfly would take 120): the first three levels exchange the half a lane does
+// not keep, the last two reduce the 3 remaining values.  On
 // return lanes 4g (g = 0..7) hold the warp totals of values 3g .. 3g+2 in out[0..2].
 __device__ __forceinline__ void warp_reduce24(const float v[24], int lane, float out[3]) {
     const bool a = lane & 16, b = lane & 8, c = lane & 4;

@@ -310,58 +310,6 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
     }
 }
 
-__global__ void gather_counts_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
-                                     uint32_t* __restrict__ out, int n) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) out[r] = counts[order[r]];
-}
-
-// One warp per Gaussian (in depth order): lanes stride over its tile rect.
-__global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restrict__ order,
-                                                        const uint32_t* __restrict__ offsets,
-                                                        const ProjRec* __restrict__ rec, int tile_size,
-                                                        int tiles_x, int n_surv, uint32_t* __restrict__ pair_tile,
-                                                        uint32_t* __restrict__ pair_gauss) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n_surv) return;
-    const uint32_t gid = order[warp];
-    const uint32_t off = offsets[warp];
-    const float4 r1 = rec[gid].r1;
-    const int x0 = range_lo(r1.z), x1 = range_hi(r1.z), y0 = range_lo(r1.w), y1 = range_hi(r1.w);
-    const int tx0 = x0 / tile_size, tx1 = (x1 - 1) / tile_size;
-    const int ty0 = y0 / tile_size, ty1 = (y1 - 1) / tile_size;
-    const int nx = tx1 - tx0 + 1;
-    const int total = nx * (ty1 - ty0 + 1);
-    for (int k = lane; k < total; k += 32) {
-        const int ty = ty0 + k / nx, tx = tx0 + k % nx;
-        pair_tile[off + k] = (uint32_t)(ty * tiles_x + tx);
-        pair_gauss[off + k] = gid;
-    }
-}
-
-// CSR ranges over the tile-sorted pairs: ranges[2t] = lower_bound(t), ranges[2t+1] =
-// lower_bound(t + 1).  Empty tiles get [p, p] exactly like detail::bin_tiles' empty lists.
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ tiles, uint32_t n, uint32_t* __restrict__ ranges,
-                                   int n_tiles) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tiles) return;
-    uint32_t bounds[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t key = (uint32_t)t + k;
-        uint32_t lo = 0, hi = n;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (tiles[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        bounds[k] = lo;
-    }
-    ranges[2 * t] = bounds[0];
-    ranges[2 * t + 1] = bounds[1];
-}
-
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -727,40 +675,6 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
             preprocess_kernel<false><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
                                                                               tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
-    lc.count++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
-                                 uint32_t* counts_sorted, int n) {
-    if (n == 0) return cudaSuccess;
-    {
-        LaunchScope ls_(lc, "gather_counts");
-        gather_counts_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(order, tile_counts, counts_sorted, n);
-    }
-    lc.count++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32_t* offsets, const ProjRec* rec,
-                              const CamParams& cp, int n_survivors, uint32_t* pair_tile, uint32_t* pair_gauss) {
-    if (n_survivors == 0) return cudaSuccess;
-    {
-        LaunchScope ls_(lc, "emit_pairs");
-        emit_pairs_kernel<<<blocks_for((int64_t)n_survivors * 32, 256), 256, 0, lc.stream>>>(
-        order, offsets, rec, cp.tile_size, cp.tiles_x, n_survivors, pair_tile, pair_gauss);
-    }
-    lc.count++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs, uint32_t* ranges,
-                               int n_tiles) {
-    {
-        LaunchScope ls_(lc, "tile_ranges");
-        tile_ranges_kernel<<<blocks_for(n_tiles, 256), 256, 0, lc.stream>>>(sorted_tiles, (uint32_t)n_pairs, ranges,
-                                                                        n_tiles);
-    }
     lc.count++;
     return cudaGetLastError();
 }

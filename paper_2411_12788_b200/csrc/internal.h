@@ -74,16 +74,6 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
                               float* depth_out, uint2* rect_ref);
-// counts_sorted[r] = tile_counts[order[r]]
-cudaError_t launch_gather_counts(LaunchCtx& lc, const uint32_t* order, const uint32_t* tile_counts,
-                                 uint32_t* counts_sorted, int n);
-// K3: pairs (tile id, Gaussian id) in depth order.
-cudaError_t launch_emit_pairs(LaunchCtx& lc, const uint32_t* order, const uint32_t* offsets,
-                              const ProjRec* rec, const CamParams& cp, int n_survivors,
-                              uint32_t* pair_tile, uint32_t* pair_gauss);
-// K5: ranges[2t], ranges[2t+1] = [start, end) of tile t in the sorted pairs.
-cudaError_t launch_tile_ranges(LaunchCtx& lc, const uint32_t* sorted_tiles, uint64_t n_pairs,
-                               uint32_t* ranges, int n_tiles);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 struct BinningArgs {

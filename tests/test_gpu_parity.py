@@ -112,7 +112,7 @@ def test_fused_l1_backward_matches_split(oracle):
     assert abs(loss.item() - want_loss) <= 1e-5 * abs(want_loss)
 
 
-@pytest.mark.parametrize("tile", [8, 16, 32, 64])
+@pytest.mark.parametrize("tile", [8, 16, 32, 48, 64])  # 48: non-power-of-two tile division path
 def test_tile_sizes(oracle, tile):
     s, cam = small_scene(n=400, w=50, h=38)  # not tile-aligned
     cfg = RasterConfig(tile_size=tile)
