@@ -48,7 +48,7 @@ cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const u
 // Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result lands in keys/vals
 // or, when *result_in_alt, in keys_alt/vals_alt.
 // Whole sort as one cooperative kernel (result in keys_alt / vals_alt); returns
-// cudaErrorCooperativeLaunchTooLarge when N does not fit one resident wave of 2048-key tiles.
+// cudaErrorCooperativeLaunchTooLarge when N does not fit one resident wave of 4096-key tiles.
 size_t radix_coop_count_words(uint64_t n);
 cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                             uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work);

@@ -420,18 +420,18 @@ void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint
 }
 
 // ---- cooperative whole-sort kernel ---------------------------------------------------------
-// For N up to (resident CTAs) x 2048 keys the whole LSD sort runs as ONE cooperative kernel: each
-// CTA owns one 2048-key tile for the whole sort, so a pass is rank -> publish per-digit tile
+// For N up to (resident CTAs) x 4096 keys the whole LSD sort runs as ONE cooperative kernel: each
+// CTA owns one 4096-key tile for the whole sort, so a pass is rank -> publish per-digit tile
 // counts -> grid barrier -> 256 CTAs scan one digit row each -> grid barrier -> scatter -> grid
 // barrier, with no look-back chain (the Onesweep look-back serialises ~tiles/16 round trips when
 // every tile runs in the same wave).  The first phase histograms all four byte digits; passes
 // whose digit is the same for every key are skipped, and the buffer chain is routed through a
 // third buffer so the result always lands in (keys1, vals1).
 namespace cg = cooperative_groups;
-constexpr int kCoopItems = 8;
-constexpr int kCoopTile = kThreads * kCoopItems;  // 2048
+constexpr int kCoopItems = 16;
+constexpr int kCoopTile = kThreads * kCoopItems;  // 4096 (245 CTAs at N = 1 M: fewer to barrier)
 
-__global__ void __launch_bounds__(kThreads, 4) radix_coop_kernel(uint32_t* __restrict__ k0, uint32_t* __restrict__ v0,
+__global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __restrict__ k0, uint32_t* __restrict__ v0,
                                                                  uint32_t* __restrict__ k1, uint32_t* __restrict__ v1,
                                                                  uint32_t* __restrict__ k2, uint32_t* __restrict__ v2,
                                                                  uint32_t n, uint32_t* __restrict__ hist,
