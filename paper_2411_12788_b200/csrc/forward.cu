@@ -84,12 +84,18 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
     __shared__ float4 s_sh[VEC_SH ? kPreThreads * kShRow : 1];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (VEC_SH) {
+        // the block's SH rows stream into shared memory (cp.async, coalesced) while the geometry
+        // below runs; the colour waits for them after the projection
         const int base = blockIdx.x * kPreThreads;
         const int cnt = min(kPreThreads, g.n - base);
         const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)base);
-        for (int q = threadIdx.x; q < cnt * 12; q += kPreThreads) s_sh[(q / 12) * kShRow + q % 12] = __ldg(src + q);
-        __syncthreads();
+        const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(s_sh);
+        for (int q = threadIdx.x; q < cnt * 12; q += kPreThreads)
+            cp_async16(dst0 + 16u * (uint32_t)((q / 12) * kShRow + q % 12), src + q);
+        cp_async_commit();
     }
+    bool want_rgb = false;
+    float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     bool alive = i < g.n;
     if (alive && mask && !mask[i]) alive = false;
     float px = 0.f, py = 0.f, pz = 0.f, zc = 0.f;
@@ -191,29 +197,16 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
             }
             if (alive) {
                 const float opacity = 1.0f / (1.0f + splat_expf(-__ldg(&g.opacity_logits[i])));
-                // view_dir = (p - cam_center).normalized()
-                float u0 = px - cp.center[0], u1 = py - cp.center[1], u2 = pz - cp.center[2];
+                // view_dir = (p - cam_center).normalized(); the SH colour follows after the barrier
+                u0 = px - cp.center[0];
+                u1 = py - cp.center[1];
+                u2 = pz - cp.center[2];
                 const float zz = dot3(u0, u1, u2, u0, u1, u2);
                 if (zz > 0.0f) {
                     const float nn = sqrtf(zz);
                     u0 = u0 / nn; u1 = u1 / nn; u2 = u2 / nn;
                 }
-                float rgb[3];
-                if (VEC_SH) {
-                    float shv[48];
-                    const float4* s4 = &s_sh[threadIdx.x * kShRow];
-#pragma unroll
-                    for (int k = 0; k < 12; ++k) {
-                        const float4 v = s4[k];
-                        shv[4 * k] = v.x; shv[4 * k + 1] = v.y; shv[4 * k + 2] = v.z; shv[4 * k + 3] = v.w;
-                    }
-                    sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
-                } else {
-                    float shv[48];
-#pragma unroll
-                    for (int k = 0; k < 48; ++k) shv[k] = __ldg(&g.sh[48 * (size_t)i + k]);
-                    sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
-                }
+                want_rgb = true;
                 const int ts = cp.tile_size;
                 const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts, ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
                 tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
@@ -246,7 +239,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                 r.r0 = make_float4(m0, m1, k0, k1);
                 r.r1 = make_float4(k2, opacity, __uint_as_float(pack_range(ex0, ex1)),
                                    __uint_as_float(pack_range(ey0, ey1)));
-                r.r2 = make_float4(rgb[0], rgb[1], rgb[2], cut);
+                r.r2 = make_float4(0.f, 0.f, 0.f, cut);  // colour filled in after the SH barrier
                 ref_rect = make_uint2(pack_range(x0, x1), pack_range(y0, y1));
                 if (aux) {
                     const float smax = std_max(std_max(ls0, ls1), ls2);
@@ -274,6 +267,29 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                 }
             }
         }
+    }
+    if (VEC_SH) {
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    if (want_rgb && alive) {  // sh_to_color (rasterizer.cpp:75)
+        float rgb[3];
+        float shv[48];
+        if (VEC_SH) {
+            const float4* s4 = &s_sh[threadIdx.x * kShRow];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) {
+                const float4 v = s4[k];
+                shv[4 * k] = v.x; shv[4 * k + 1] = v.y; shv[4 * k + 2] = v.z; shv[4 * k + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 48; ++k) shv[k] = __ldg(&g.sh[48 * (size_t)i + k]);
+        }
+        sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
+        r.r2.x = rgb[0];
+        r.r2.y = rgb[1];
+        r.r2.z = rgb[2];
     }
     if (i < g.n) {
         keys[i] = alive ? __float_as_uint(zc) : 0xffffffffu;
