@@ -100,10 +100,27 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
     if (alive && mask && !mask[i]) alive = false;
     float px = 0.f, py = 0.f, pz = 0.f, zc = 0.f;
     float pc0 = 0.f, pc1 = 0.f;
-    if (alive) {
+    // every parameter load issued up front (independent of the culls) so their latencies overlap
+    float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, qw = 0.f, qx = 0.f, qy = 0.f, qz = 0.f, ologit = 0.f;
+    if (i < g.n) {
         px = __ldg(&g.centers[3 * i]);
         py = __ldg(&g.centers[3 * i + 1]);
         pz = __ldg(&g.centers[3 * i + 2]);
+        ls0 = __ldg(&g.log_scales[3 * i]);
+        ls1 = __ldg(&g.log_scales[3 * i + 1]);
+        ls2 = __ldg(&g.log_scales[3 * i + 2]);
+        if ((reinterpret_cast<uintptr_t>(g.rotations) & 15u) == 0) {
+            const float4 q4 = __ldg(reinterpret_cast<const float4*>(g.rotations) + i);
+            qw = q4.x; qx = q4.y; qy = q4.z; qz = q4.w;
+        } else {
+            qw = __ldg(&g.rotations[4 * i]);
+            qx = __ldg(&g.rotations[4 * i + 1]);
+            qy = __ldg(&g.rotations[4 * i + 2]);
+            qz = __ldg(&g.rotations[4 * i + 3]);
+        }
+        ologit = __ldg(&g.opacity_logits[i]);
+    }
+    if (alive) {
         pc0 = dot3(cp.R[0], cp.R[1], cp.R[2], px, py, pz) + cp.t[0];
         pc1 = dot3(cp.R[3], cp.R[4], cp.R[5], px, py, pz) + cp.t[1];
         zc = dot3(cp.R[6], cp.R[7], cp.R[8], px, py, pz) + cp.t[2];
@@ -118,10 +135,6 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
         const float m0 = cp.fx * pc0 / z + cp.cx;
         const float m1 = cp.fy * pc1 / z + cp.cy;
         // covariance_from_params (gaussian_set.hpp:41-55)
-        const float ls0 = __ldg(&g.log_scales[3 * i]), ls1 = __ldg(&g.log_scales[3 * i + 1]),
-                    ls2 = __ldg(&g.log_scales[3 * i + 2]);
-        float qw = __ldg(&g.rotations[4 * i]), qx = __ldg(&g.rotations[4 * i + 1]),
-              qy = __ldg(&g.rotations[4 * i + 2]), qz = __ldg(&g.rotations[4 * i + 3]);
         const float qn = sqrtf((qw * qw + qx * qx) + (qy * qy + qz * qz));
         if (!(qn > 0.0f)) {
             qw = 1.0f; qx = qy = qz = 0.0f;
@@ -196,7 +209,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                 if (x0 >= x1 || y0 >= y1) alive = false;
             }
             if (alive) {
-                const float opacity = 1.0f / (1.0f + splat_expf(-__ldg(&g.opacity_logits[i])));
+                const float opacity = 1.0f / (1.0f + splat_expf(-ologit));
                 // view_dir = (p - cam_center).normalized(); the SH colour follows after the barrier
                 u0 = px - cp.center[0];
                 u1 = py - cp.center[1];
