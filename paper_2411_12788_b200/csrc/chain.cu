@@ -112,8 +112,13 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     // dopacity), g2 = d colour, g3.x = number of committed (warp, pixel) samples
     const float4 g0 = grad2d[4 * (size_t)i], g1 = grad2d[4 * (size_t)i + 1], g2 = grad2d[4 * (size_t)i + 2],
                  g3 = grad2d[4 * (size_t)i + 3];
-    const bool touched = g3.x > 0.0f;
     const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i, i48 = 48 * (size_t)i;
+    // the per-Gaussian inputs, loaded before the touched test so every load is in flight at once
+    const ProjRec pr = rec[i];
+    const float p0 = g.centers[i3], p1 = g.centers[i3 + 1], p2 = g.centers[i3 + 2];
+    const float qraw[4] = {g.rotations[i4], g.rotations[i4 + 1], g.rotations[i4 + 2], g.rotations[i4 + 3]};
+    const float ls[3] = {g.log_scales[i3], g.log_scales[i3 + 1], g.log_scales[i3 + 2]};
+    const bool touched = g3.x > 0.0f;
     if (!touched) {
         if (!accumulate) {
 #pragma unroll
@@ -143,7 +148,6 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     const float dQ[4] = {g0.z, g1.x, g1.x, g1.y};  // row-major (00, 01, 10, 11); 01 == 10
     const float dopac = g1.z;
     const float dcol[3] = {g2.x, g2.y, g2.z};
-    const ProjRec pr = rec[i];
     const float k0 = pr.r0.z, k1 = pr.r0.w, k2 = pr.r1.x, opacity = pr.r1.y;
 
     const float gaccum = sqrtf(dm0 * dm0 + dm1 * dm1);
@@ -160,7 +164,6 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
 #pragma unroll
         for (int c = 0; c < 2; ++c) dV[r * 2 + c] = N[r * 2] * Q[c] + N[r * 2 + 1] * Q[2 + c];
 
-    const float p0 = g.centers[i3], p1 = g.centers[i3 + 1], p2 = g.centers[i3 + 2];
     const float* Rc = cp.R;
     const float fx = cp.fx, fy = cp.fy;
     const float pc0 = dot3(Rc[0], Rc[1], Rc[2], p0, p1, p2) + cp.t[0];
@@ -173,8 +176,6 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
 #pragma unroll
         for (int c = 0; c < 3; ++c) Mm[r * 3 + c] = dot3(J[r * 3], J[r * 3 + 1], J[r * 3 + 2], Rc[c], Rc[3 + c], Rc[6 + c]);
     // covariance_from_params
-    const float qraw[4] = {g.rotations[i4], g.rotations[i4 + 1], g.rotations[i4 + 2], g.rotations[i4 + 3]};
-    const float ls[3] = {g.log_scales[i3], g.log_scales[i3 + 1], g.log_scales[i3 + 2]};
     float Rq0[9];
     rotation_from_quat(qraw, Rq0);
     const float sc[3] = {splat_expf(ls[0]), splat_expf(ls[1]), splat_expf(ls[2])};
