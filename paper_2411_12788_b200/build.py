@@ -8,6 +8,7 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -46,16 +47,20 @@ def _stale(target: Path, deps) -> bool:
 def build(verbose: bool = False, force: bool = False, extra_flags=()) -> Path:
     OBJ.mkdir(exist_ok=True)
     LIB.parent.mkdir(exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src, flags in SOURCES.items():
         s = CSRC / src
         o = OBJ / (src + ".o")
         objs.append(o)
         if force or _stale(o, [s, *HEADERS]):
-            cmd = [NVCC, *COMMON, *flags, *extra_flags, "-c", str(s), "-o", str(o)]
+            cmds.append([NVCC, *COMMON, *flags, *extra_flags, "-c", str(s), "-o", str(o)])
+    # independent translation units: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for cmd in cmds:
             if verbose:
                 print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
+        for f in [pool.submit(subprocess.run, cmd, check=True) for cmd in cmds]:
+            f.result()
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
         if verbose:

@@ -232,10 +232,13 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
                 float r[3];
                 warp_reduce24(v, lane, r);
                 const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
-                const bool mine = (lane & 3) == 0 && (grp < 4 ? any_a : any_b);
+                // the commit count (value 9, group 3) rides in the 4th slot of group 2's record
+                const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
+                const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
                 if (mine) {
                     const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
-                    red_add_v4(grad2d + 4 * (size_t)gid + (grp & 3), r[0], r[1], r[2], 0.0f);
+                    red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2],
+                               (grp & 3) == 2 ? cnt : 0.0f);
                 }
             }
         }
@@ -420,10 +423,13 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 float r[3];
                 warp_reduce24(v, lane, r);
                 const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
-                const bool mine = (lane & 3) == 0 && (grp < 4 ? any_a : any_b);
+                // the commit count (value 9, group 3) rides in the 4th slot of group 2's record
+                const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
+                const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
                 if (mine) {
                     const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
-                    red_add_v4(grad2d + 4 * (size_t)gid + (grp & 3), r[0], r[1], r[2], 0.0f);
+                    red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2],
+                               (grp & 3) == 2 ? cnt : 0.0f);
                 }
             }
         }
@@ -480,7 +486,8 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_persistent(CamParams c
                                                             const float* __restrict__ color,
                                                             const float* __restrict__ target, float inv_n,
                                                             float* __restrict__ loss_partials,
-                                                            float4* __restrict__ grad2d, int nblocks, int* __restrict__ counter) {
+                                                            float4* __restrict__ grad2d,
+                                                            int nblocks, int* __restrict__ counter) {
     __shared__ int s_bid;
     for (;;) {
         __syncthreads();
@@ -554,22 +561,60 @@ __global__ void __launch_bounds__(kLossThreads) loss_reduce_kernel(const float* 
 }
 
 // adam_delta (optimizer.cpp:29-36) with every fp64 operation explicitly rounded (no DFMA), so
-// the update is bit-identical to the reference's.
-__global__ void adam_kernel(float* __restrict__ param, const float* __restrict__ grad, float* __restrict__ m,
-                            float* __restrict__ v, int64_t count, double lr, double lr_alt, int sh_layout,
-                            double b1, double omb1, double b2, double omb2, double eps, double bias1, double bias2) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    const double g = (double)grad[i];
-    const float mf = (float)__dadd_rn(__dmul_rn(b1, (double)m[i]), __dmul_rn(omb1, g));
-    const float vf = (float)__dadd_rn(__dmul_rn(b2, (double)v[i]), __dmul_rn(__dmul_rn(omb2, g), g));
-    m[i] = mf;
-    v[i] = vf;
-    const double m_hat = __ddiv_rn((double)mf, bias1);
-    const double v_hat = __ddiv_rn((double)vf, bias2);
-    const double l = (sh_layout && (i % 48) >= 3) ? lr_alt : lr;
-    const float delta = (float)__ddiv_rn(__dmul_rn(l, m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
-    param[i] = __fsub_rn(param[i], delta);
+// the update is bit-identical to the reference's.  One element: returns the new parameter and
+// writes the new moments.  mf == 0 (eps > 0) gives delta = +-0 exactly (0 / positive), so the three fp64
+// divisions and the square root (whose zero operands take the slow library paths) are skipped.
+__device__ __forceinline__ float adam_one(float p, float gr, float& m, float& v, double l, double b1, double omb1,
+                                          double b2, double omb2, double eps, double bias1, double bias2) {
+    const double g = (double)gr;
+    const float mf = (float)__dadd_rn(__dmul_rn(b1, (double)m), __dmul_rn(omb1, g));
+    const float vf = (float)__dadd_rn(__dmul_rn(b2, (double)v), __dmul_rn(__dmul_rn(omb2, g), g));
+    m = mf;
+    v = vf;
+    float delta;
+    if (mf == 0.0f && vf >= 0.0f && vf < INFINITY && eps > 0.0) {
+        delta = copysignf(0.0f, mf);  // l * (+-0 / bias1) / (sqrt(v_hat) + eps), all factors positive
+    } else {
+        const double m_hat = __ddiv_rn((double)mf, bias1);
+        const double v_hat = __ddiv_rn((double)vf, bias2);
+        delta = (float)__ddiv_rn(__dmul_rn(l, m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
+    }
+    return __fsub_rn(p, delta);
+}
+
+// Four consecutive elements per thread (float4 traffic when the group is 16-byte aligned), so four
+// independent fp64 chains are in flight per thread.  SH: per-48 rows, coefficients k >= 3 use
+// lr_alt (rows start at multiples of 48, so a 4-element group never straddles a row).
+template <bool SH, bool VEC>
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ param, const float* __restrict__ grad,
+                                                   float* __restrict__ m, float* __restrict__ v, int64_t count,
+                                                   double lr, double lr_alt, double b1, double omb1, double b2,
+                                                   double omb2, double eps, double bias1, double bias2) {
+    const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= count) return;
+    const int r0 = SH ? (int)(i0 % 48) : 0;
+    if (VEC && i0 + 4 <= count) {
+        float4 p4 = *reinterpret_cast<const float4*>(param + i0);
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(grad + i0));
+        float4 m4 = *reinterpret_cast<const float4*>(m + i0);
+        float4 v4 = *reinterpret_cast<const float4*>(v + i0);
+        p4.x = adam_one(p4.x, g4.x, m4.x, v4.x, SH && r0 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.y = adam_one(p4.y, g4.y, m4.y, v4.y, SH && r0 + 1 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.z = adam_one(p4.z, g4.z, m4.z, v4.z, SH && r0 + 2 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.w = adam_one(p4.w, g4.w, m4.w, v4.w, SH && r0 + 3 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        *reinterpret_cast<float4*>(param + i0) = p4;
+        *reinterpret_cast<float4*>(m + i0) = m4;
+        *reinterpret_cast<float4*>(v + i0) = v4;
+        return;
+    }
+    for (int k = 0; k < 4 && i0 + k < count; ++k) {
+        const int64_t i = i0 + k;
+        float mm = m[i], vv = v[i];
+        param[i] = adam_one(param[i], grad[i], mm, vv, SH && r0 + k >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps,
+                            bias1, bias2);
+        m[i] = mm;
+        v[i] = vv;
+    }
 }
 
 // normalized_quat (gaussian_set.hpp:15-20) in place, optimizer.cpp:69
@@ -677,9 +722,20 @@ cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, dou
     if (a.count == 0) return cudaSuccess;
     {
         LaunchScope ls_(lc, "adam");
-        adam_kernel<<<blocks_for(a.count, 256), 256, 0, lc.stream>>>(a.param, a.grad, a.m, a.v, a.count, a.lr, a.lr_alt,
-                                                                a.sh_layout, beta1, 1.0 - beta1, beta2, 1.0 - beta2,
-                                                                eps, bias1, bias2);
+        const bool vec = ((reinterpret_cast<uintptr_t>(a.param) | reinterpret_cast<uintptr_t>(a.grad) |
+                           reinterpret_cast<uintptr_t>(a.m) | reinterpret_cast<uintptr_t>(a.v)) & 15u) == 0;
+        const unsigned grid = blocks_for((a.count + 3) / 4, 256);
+#define ADAM_LAUNCH(SH, VEC)                                                                                      \
+    adam_kernel<SH, VEC><<<grid, 256, 0, lc.stream>>>(a.param, a.grad, a.m, a.v, a.count, a.lr, a.lr_alt, beta1,  \
+                                                     1.0 - beta1, beta2, 1.0 - beta2, eps, bias1, bias2)
+        if (a.sh_layout) {
+            if (vec) ADAM_LAUNCH(true, true);
+            else ADAM_LAUNCH(true, false);
+        } else {
+            if (vec) ADAM_LAUNCH(false, true);
+            else ADAM_LAUNCH(false, false);
+        }
+#undef ADAM_LAUNCH
     }
     lc.count++;
     return cudaGetLastError();

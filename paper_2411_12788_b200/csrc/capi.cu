@@ -599,7 +599,7 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     const FwdState& st = ctx->st;
     LaunchCtx& lc = ctx->lc;
     const int n = g->n;
-    CK(ctx->grad2d.ensure((size_t)(n > 0 ? n : 1) * 64, true, ctx->stream), "alloc grad2d");
+    CK(ctx->grad2d.ensure(grad2d_bytes((size_t)(n > 0 ? n : 1)), true, ctx->stream), "alloc grad2d");
     const bool zero_async = !accumulate && n > 0 && ctx->fwd_start_recorded;
     if (zero_async) {
         cudaStream_t z = ctx->zstream;

@@ -109,16 +109,16 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
                                           int i, float4* s_sh, int row) {
     if (i >= g.n) return;
     // accumulator (blend_backward): g0 = (dmean.x, dmean.y, dconic00), g1 = (dconic01, dconic11,
-    // dopacity), g2 = d colour, g3.x = number of committed (warp, pixel) samples
-    const float4 g0 = grad2d[4 * (size_t)i], g1 = grad2d[4 * (size_t)i + 1], g2 = grad2d[4 * (size_t)i + 2],
-                 g3 = grad2d[4 * (size_t)i + 3];
+    // dopacity), g2 = (d colour, number of committed (warp, pixel) samples)
+    const float4 g0 = grad2d[kG2Stride * (size_t)i], g1 = grad2d[kG2Stride * (size_t)i + 1], g2 = grad2d[kG2Stride * (size_t)i + 2];
+    const float cnt = g2.w;
     const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i, i48 = 48 * (size_t)i;
     // the per-Gaussian inputs, loaded before the touched test so every load is in flight at once
     const ProjRec pr = rec[i];
     const float p0 = g.centers[i3], p1 = g.centers[i3 + 1], p2 = g.centers[i3 + 2];
     const float qraw[4] = {g.rotations[i4], g.rotations[i4 + 1], g.rotations[i4 + 2], g.rotations[i4 + 3]};
     const float ls[3] = {g.log_scales[i3], g.log_scales[i3 + 1], g.log_scales[i3 + 2]};
-    const bool touched = g3.x > 0.0f;
+    const bool touched = cnt > 0.0f;
     if (!touched) {
         if (!accumulate) {
 #pragma unroll
@@ -142,7 +142,7 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     }
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) grad2d[4 * (size_t)i + k] = zero4;
+    for (int k = 0; k < 3; ++k) grad2d[kG2Stride * (size_t)i + k] = zero4;
 
     const float dm0 = g0.x, dm1 = g0.y;
     const float dQ[4] = {g0.z, g1.x, g1.x, g1.y};  // row-major (00, 01, 10, 11); 01 == 10
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __rest
     __shared__ uint32_t s_base;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool touched = i < n && grad2d[4 * (size_t)i + 3].x > 0.0f;
+    const bool touched = i < n && grad2d[kG2Stride * (size_t)i + 2].w > 0.0f;
     const unsigned m = __ballot_sync(0xffffffffu, touched);
     if (lane == 0) s_wc[warp] = __popc(m);
     __syncthreads();

@@ -17,6 +17,11 @@ namespace splat_b200 {
 
 constexpr int kBlock = 256;  // threads per tile CTA (16 x 16 pixels)
 
+// 2D gradient accumulator of blend_backward: 3 float4 per Gaussian, (dmean.x, dmean.y, dconic00,
+// 0), (dconic01, dconic11, dopacity, 0), (dcolour rgb, number of committed (warp, pixel) samples).
+constexpr int kG2Stride = 3;
+constexpr size_t grad2d_bytes(size_t n) { return n * 16 * kG2Stride; }
+
 // Projected Gaussian record, 48 B (3 x float4), indexed by Gaussian id:
 //   r0 = (mean2d.x, mean2d.y, conic0, conic1)
 //   r1 = (conic2, opacity, eff x0 | x1 << 16, eff y0 | y1 << 16)

@@ -440,9 +440,15 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     __shared__ uint32_t s_cnt[kWarps][256];
     __shared__ uint32_t s_gh[4][256];
     __shared__ uint32_t s_warp[kWarps];
+    __shared__ uint32_t s_delta[256];
+    // the tile's keys in local (digit, original position) order: the scatter then writes each
+    // digit's run of the tile to consecutive global positions (coalesced)
+    __shared__ uint32_t s_k[kCoopTile], s_v[kCoopTile];
     const uint32_t tile = blockIdx.x, ntiles = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
+    const uint32_t tbase = tile * kCoopTile;
+    const uint32_t tcount = n > tbase ? min(n - tbase, (uint32_t)kCoopTile) : 0u;
     uint32_t k[kCoopItems], v[kCoopItems];
 #pragma unroll
     for (int r = 0; r < kCoopItems; ++r) {
@@ -514,13 +520,33 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             rank[r] = old + __popc(peers & lt);
         }
         __syncthreads();
-        {  // tile totals per digit (thread d), published digit-major
+        // thread d: tile total of digit d (published digit-major), its local start L (exclusive
+        // over digits) and the local start of every warp's run of d
+        uint32_t local_start;
+        {
             const int d = threadIdx.x;
             uint32_t c = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) c += s_cnt[w][d];
             counts[(size_t)d * ntiles + tile] = c;
+            uint32_t tot;
+            local_start = block_exclusive_scan(c, &tot, s_warp);
+            uint32_t run = local_start;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t cw = s_cnt[w][d];
+                s_cnt[w][d] = run;
+                run += cw;
+            }
         }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kCoopItems; ++r)
+            if (wbase + r * 32 + lane < n) {
+                const uint32_t lp = s_cnt[warp][(k[r] >> shift) & 255u] + rank[r];
+                s_k[lp] = k[r];
+                s_v[lp] = v[r];
+            }
         grid.sync();
         // phase B: digit rows, exclusive over tiles, plus the digit's global base
         for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) {
@@ -551,25 +577,17 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             }
         }
         grid.sync();
-        {  // phase C: tile offsets per digit, per-warp runs, scatter
-            const int d = threadIdx.x;
-            uint32_t run = counts[(size_t)d * ntiles + tile];
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const uint32_t cw = s_cnt[w][d];
-                s_cnt[w][d] = run;
-                run += cw;
-            }
-        }
+        // phase C: global position = tile's global offset of the digit + (local position - L)
+        s_delta[threadIdx.x] = counts[(size_t)threadIdx.x * ntiles + tile] - local_start;
         __syncthreads();
-#pragma unroll
-        for (int r = 0; r < kCoopItems; ++r) {
-            const uint32_t i = wbase + r * 32 + lane;
-            if (i < n) {
-                const uint32_t pos = s_cnt[warp][(k[r] >> shift) & 255u] + rank[r];
-                kb[dst][pos] = k[r];
-                vb[dst][pos] = v[r];
-            }
+        uint32_t* kd = kb[dst];
+        uint32_t* vd = vb[dst];
+#pragma unroll 4
+        for (uint32_t i = threadIdx.x; i < tcount; i += kThreads) {
+            const uint32_t key = s_k[i];
+            const uint32_t pos = s_delta[(key >> shift) & 255u] + i;
+            kd[pos] = key;
+            vd[pos] = s_v[i];
         }
         src = dst;
         grid.sync();

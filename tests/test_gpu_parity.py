@@ -205,6 +205,37 @@ def test_adam_bit_exact(oracle):
     assert opt.step_count() == t == 3
 
 
+def test_adam_zero_gradients_and_tail(oracle):
+    """Zero / negative-zero gradients (the mf == 0 shortcut) and a count that is not a multiple of
+    4 (the scalar tail of the 4-wide kernel), over steps with and without gradients."""
+    n = 1003
+    rng = np.random.default_rng(6)
+    s = scenes.make_gaussians(n, seed=6)
+    shapes = dict(d_centers=(n, 3), d_log_scales=(n, 3), d_rotations=(n, 4), d_opacity_logits=(n,), d_sh=(n, 48))
+    import torch
+    ds = R.DeviceGaussians.from_host(s)
+    dg = R.DeviceGrads(n)
+    opt = R.OptimState(AdamConfig(scene_extent=2.0), n)
+    hs, m, v, t = s, np.zeros(59 * n, np.float32), np.zeros(59 * n, np.float32), 0
+    for step in range(4):
+        grads = {}
+        for k, shp in shapes.items():
+            g = rng.normal(size=shp).astype(np.float32)
+            g[rng.random(shp) < 0.5] = 0.0
+            g[rng.random(shp) < 0.1] = -0.0
+            if step == 2:
+                g[:] = 0.0
+            grads[k] = g
+            getattr(dg, k).copy_(torch.from_numpy(g))
+        opt.step(ds, dg)
+        hs, m, v, t = oracle.adam_step(hs, grads, m, v, AdamConfig(scene_extent=2.0), t)
+    got = ds.to_host()
+    for k in ("centers", "log_scales", "rotations", "opacity_logits", "sh"):
+        assert_bitwise(getattr(got, k), getattr(hs, k), f"adam {k}")
+    assert_bitwise(opt.m.cpu().numpy(), m, "adam m")
+    assert_bitwise(opt.v.cpu().numpy(), v, "adam v")
+
+
 def test_adam_means_only(oracle):
     rng = np.random.default_rng(5)
     s = scenes.make_gaussians(200, seed=5)
