@@ -33,7 +33,9 @@ namespace {
 constexpr int kST = 4;              // supertile side in tiles
 constexpr int kSTT = kST * kST;     // tiles per supertile
 constexpr int kL2Threads = 512;     // level-2 CTA: one per piece of a supertile list
-constexpr int kStChunk = 128;       // depth-ordered survivors per chunk of the supertile pass
+constexpr int kStChunk = 128;       // depth-ordered survivors per warp of the supertile pass
+constexpr int kStWarps = 4;         // warps per supertile-pass CTA
+constexpr int kStChunkCta = kStChunk * kStWarps;  // survivors per CTA chunk (one count column)
 constexpr int kStMaxSmem = 6144;    // supertiles the chunked pass keeps in shared memory
 
 struct TileRect {
@@ -103,26 +105,46 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
-// Supertile pass over one chunk of depth-ordered survivors, one warp per chunk.  The chunk's
-// Gaussians are flattened, 32 at a time, into (Gaussian, supertile) entries in (depth, raster)
-// order; every window of 32 entries is ranked per supertile with __match_any_sync, and a
-// per-supertile running count in shared memory carries the rank across windows.
-//   EMIT = false: cnt[st * nchunks + c] = entries of chunk c in supertile st.
-//   EMIT = true:  cnt holds the exclusive scan of those counts; writes st_gauss[offset + rank].
+// Supertile pass over one chunk of depth-ordered survivors: kStWarps warps per CTA, each owning
+// kStChunk consecutive survivors of the CTA's chunk.  A warp flattens its Gaussians, 32 at a
+// time, into (Gaussian, supertile) entries in (depth, raster) order; every window of 32 entries is
+// ranked per supertile with __match_any_sync, and a per-(warp, supertile) running count in shared
+// memory carries the rank across windows.
+//   EMIT = false: each warp counts its entries per supertile; wcnt[(c kStWarps + warp) n_st + st]
+//                 gets the warp's counts (coalesced rows) and cnt[st nchunks + c] the CTA's.
+//   EMIT = true:  cnt holds the exclusive scan of the CTA counts (supertile-major); launched with
+//                 one warp per CTA (1-warp CTAs: 32 resident per SM, measured faster than
+//                 kStWarps-warp CTAs), whose base for st is cnt[st nchunks + c] plus the earlier
+//                 warps' wcnt rows; it writes st_gauss[base + rank].
 template <bool EMIT>
-__global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict__ order,
-                                                      const uint2* __restrict__ rect_ref, int n_surv, int ts,
-                                                      int ts_shift, int st_x, int n_st, int nchunks,
-                                                      uint32_t* __restrict__ cnt, uint32_t* __restrict__ st_gauss,
-                                                      uint16_t* __restrict__ st_cover) {
-    extern __shared__ uint32_t s_run[];  // [n_st]
-    const int c = blockIdx.x, lane = threadIdx.x;
-    for (int st = lane; st < n_st; st += 32) s_run[st] = EMIT ? cnt[(size_t)st * nchunks + c] : 0u;
-    if (!EMIT && c == 0 && lane == 0) cnt[(size_t)n_st * nchunks] = 0u;  // scan slot of the total
-    __syncwarp();
-    const int g0 = c * kStChunk, g1 = min(g0 + kStChunk, n_surv);
+__global__ void __launch_bounds__(EMIT ? 32 : 32 * kStWarps) st_chunk_kernel(const uint32_t* __restrict__ order,
+                                                                 const uint2* __restrict__ rect_ref, int n_surv,
+                                                                 int ts, int ts_shift, int st_x, int n_st, int nchunks,
+                                                                 uint32_t* __restrict__ cnt,
+                                                                 uint32_t* __restrict__ st_gauss,
+                                                                 uint16_t* __restrict__ st_cover) {
+    // count: kStWarps warps per CTA chunk, s_mem = [kStWarps][n_st] per-warp counts;
+    // emit: one warp per CTA (warp `warp` of chunk c), s_mem = [n_st] running offsets
+    extern __shared__ uint32_t s_mem[];
+    const int lane = threadIdx.x & 31;
+    const int c = EMIT ? blockIdx.x / kStWarps : blockIdx.x;
+    const int warp = EMIT ? blockIdx.x % kStWarps : threadIdx.x >> 5;
+    uint32_t* s_run = EMIT ? s_mem : s_mem + (size_t)warp * n_st;
+    uint32_t* wcnt = cnt + (size_t)n_st * nchunks + 1;
+    if (EMIT) {
+        const uint32_t* wrow = wcnt + (size_t)c * kStWarps * n_st;
+        for (int st = lane; st < n_st; st += 32) {
+            uint32_t b = cnt[(size_t)st * nchunks + c];
+            for (int ww = 0; ww < warp; ++ww) b += wrow[(size_t)ww * n_st + st];
+            s_run[st] = b;
+        }
+    } else {
+        for (int st = lane; st < n_st; st += 32) s_run[st] = 0u;
+        if (c == 0 && threadIdx.x == 0) cnt[(size_t)n_st * nchunks] = 0u;  // scan slot of the total
+    }
+    const int g0 = c * kStChunkCta + warp * kStChunk, g1 = min(g0 + kStChunk, n_surv);
     const unsigned lt = lanemask_lt();
-    // the whole chunk's ids and rects are loaded up front (two dependent round trips per chunk)
+    // the warp's ids and rects are loaded up front (two dependent round trips)
     constexpr int kPer = kStChunk / 32;
     uint32_t gids[kPer];
     uint2 rects[kPer];
@@ -136,10 +158,10 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
         const int r = g0 + k * 32 + lane;
         rects[k] = r < g1 ? rect_ref[gids[k]] : make_uint2(0u, 0u);
     }
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const int r = g0 + k * 32 + lane;
-        const uint32_t gid = gids[k];
         int sx0 = 0, sy0 = 0, w = 1, m = 0;
         uint32_t ptx = 0, pty = 0;  // (tx0 | tx1 << 16), (ty0 | ty1 << 16)
         if (r < g1) {
@@ -152,10 +174,19 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
             pty = (uint32_t)t.ty0 | ((uint32_t)t.ty1 << 16);
         }
         if (!EMIT) {  // counts are order-free: shared-memory atomics per entry
-            for (int q = 0; q < m; ++q) atomicAdd(&s_run[(sy0 + q / w) * st_x + sx0 + q % w], 1u);
+            int x = 0, row = sy0 * st_x + sx0;
+            for (int q = 0; q < m; ++q) {
+                atomicAdd(&s_run[row + x], 1u);
+                if (++x == w) {
+                    x = 0;
+                    row += st_x;
+                }
+            }
             continue;
         }
         if (!__any_sync(0xffffffffu, m > 0)) continue;
+        const uint32_t gid = gids[k];
+        const float rcp_w = __frcp_rn((float)w);
         const int inc = (int)warp_incl_scan((uint32_t)m, lane);
         const int off = inc - m;
         const int total = __shfl_sync(0xffffffffu, inc, 31);
@@ -168,8 +199,13 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
                 if (__shfl_sync(0xffffffffu, off, owner + step) <= e) owner += step;
             const int q = e - __shfl_sync(0xffffffffu, off, owner);
             const int ow = __shfl_sync(0xffffffffu, w, owner);
-            const int esx = __shfl_sync(0xffffffffu, sx0, owner) + q % ow;
-            const int esy = __shfl_sync(0xffffffffu, sy0, owner) + q / ow;
+            const float orcp = __shfl_sync(0xffffffffu, rcp_w, owner);
+            // q / ow without an integer division: (q + 0.5) / ow is >= 0.5 / ow away from an
+            // integer and its float error is below (q + 0.5) 2^-23 / ow, so truncation is exact
+            // for q < 2^22 (q < n_st here)
+            const int qy = __float2int_rz(((float)q + 0.5f) * orcp);
+            const int esx = __shfl_sync(0xffffffffu, sx0, owner) + (q - qy * ow);
+            const int esy = __shfl_sync(0xffffffffu, sy0, owner) + qy;
             const int st = esy * st_x + esx;
             const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
             const uint32_t optx = __shfl_sync(0xffffffffu, ptx, owner), opty = __shfl_sync(0xffffffffu, pty, owner);
@@ -192,7 +228,15 @@ __global__ void __launch_bounds__(32) st_chunk_kernel(const uint32_t* __restrict
     }
     if (!EMIT) {
         __syncwarp();
-        for (int st = lane; st < n_st; st += 32) cnt[(size_t)st * nchunks + c] = s_run[st];
+        uint32_t* wrow = wcnt + ((size_t)c * kStWarps + warp) * n_st;
+        for (int st = lane; st < n_st; st += 32) wrow[st] = s_run[st];
+        __syncthreads();
+        for (int st = threadIdx.x; st < n_st; st += blockDim.x) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int ww = 0; ww < kStWarps; ++ww) t += s_mem[(size_t)ww * n_st + st];
+            cnt[(size_t)st * nchunks + c] = t;
+        }
     }
 }
 
@@ -242,6 +286,15 @@ __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
     }
 }
 
+// The 16 cover bits of a lane as four words of byte counters (byte j of word i = bit 4 i + j):
+// each nibble is spread to bytes by one multiply (copies at bit offsets 0, 7, 14, 21 never
+// overlap), so per-tile counts over a warp are four __reduce_add_sync instead of 16 ballots.
+__device__ __forceinline__ void spread16(uint32_t c, uint32_t out[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = (((c >> (4 * i)) & 0xfu) * 0x00204081u) & 0x01010101u;
+}
+__device__ __forceinline__ uint32_t byte_of(const uint32_t w[4], int f) { return (w[f >> 2] >> (8 * (f & 3))) & 0xffu; }
+
 struct PieceInfo {
     int st;
     uint32_t p, lo_s, hi_s, lo, hi;
@@ -277,14 +330,19 @@ __global__ void __launch_bounds__(kL2Threads) bin_count_kernel(const uint32_t* _
         const uint32_t e = pi.lo + k * kL2Threads + tid;
         cv[k] = e < pi.hi ? (uint32_t)st_cover[e] : 0u;
     }
-    uint32_t mine = 0;  // lane f: this warp's entries covering tile f
+    // lane f: this warp's entries covering tile f (byte counters: <= 32 kPieceK = 128 per byte)
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int f = 0; f < kSTT; ++f) {
-        uint32_t c = 0;
+    for (int k = 0; k < kPieceK; ++k) {
+        uint32_t sp[4];
+        spread16(cv[k], sp);
 #pragma unroll
-        for (int k = 0; k < kPieceK; ++k) c += __popc(__ballot_sync(0xffffffffu, (cv[k] >> f) & 1u));
-        if (lane == f) mine = c;
+        for (int i = 0; i < 4; ++i) acc[i] += sp[i];
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = __reduce_add_sync(0xffffffffu, acc[i]);
+    static_assert(32 * kPieceK < 256, "byte counters");
+    const uint32_t mine = byte_of(acc, lane & 15);
     __syncthreads();
     if (lane < kSTT && mine) atomicAdd(&s_cnt[lane], mine);
     __syncthreads();
@@ -318,12 +376,13 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
         cv[k] = ok ? (uint32_t)st_cover[e] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < kPieceK; ++k)
+    for (int k = 0; k < kPieceK; ++k) {
+        uint32_t sp[4];
+        spread16(cv[k], sp);
 #pragma unroll
-        for (int f = 0; f < kSTT; ++f) {
-            const unsigned m = __ballot_sync(0xffffffffu, (cv[k] >> f) & 1u);
-            if (lane == f) s_c[k][warp][f] = __popc(m);
-        }
+        for (int i = 0; i < 4; ++i) sp[i] = __reduce_add_sync(0xffffffffu, sp[i]);
+        if (lane < kSTT) s_c[k][warp][lane] = byte_of(sp, lane);
+    }
     __syncthreads();
     {   // warp f: exclusive scan of tile f's counts over the 64 (slice, warp) positions in entry order
         static_assert(kPieceK * kW == 64 && kW == kSTT, "scan layout assumes 16 warps x 4 slices");
@@ -395,8 +454,9 @@ size_t bin_l2_pieces(uint64_t st_pairs, int n_st) { return (size_t)(st_pairs / k
 size_t bin_l2_words(uint64_t st_pairs, int n_st) { return bin_l2_pieces(st_pairs, n_st) * (1 + kSTT) + 1; }
 
 bool st_chunked(int n_st) { return n_st <= kStMaxSmem; }
-int st_chunks(int n_surv) { return n_surv > kStChunk ? (n_surv + kStChunk - 1) / kStChunk : 1; }
-size_t st_chunk_words(int n_surv, int n_st) { return (size_t)n_st * st_chunks(n_surv) + 1; }
+int st_chunks(int n_surv) { return n_surv > kStChunkCta ? (n_surv + kStChunkCta - 1) / kStChunkCta : 1; }
+// CTA counts (scanned in place) + the total slot, then the per-warp count rows
+size_t st_chunk_words(int n_surv, int n_st) { return (size_t)n_st * st_chunks(n_surv) * (1 + kStWarps) + 1; }
 
 cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     const int n_st = a.st_x * a.st_y;
@@ -411,24 +471,24 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     }
     if (st_chunked(n_st)) {
         const int nchunks = st_chunks(a.n_surv);
-        const size_t smem = (size_t)n_st * 4;
-        if (smem > 48 * 1024) {
-            cudaFuncSetAttribute(st_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaFuncSetAttribute(st_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        }
+        const size_t smem_count = (size_t)n_st * 4 * kStWarps, smem_emit = (size_t)n_st * 4;
+        if (smem_count > 48 * 1024)
+            cudaFuncSetAttribute(st_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count);
+        if (smem_emit > 48 * 1024)
+            cudaFuncSetAttribute(st_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_emit);
         {
             LaunchScope s(lc, "st_count");
-            st_chunk_kernel<false><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, ts, ts_shift,
-                                                                     a.st_x, n_st, nchunks, a.st_cnt, nullptr, nullptr);
+            st_chunk_kernel<false><<<nchunks, 32 * kStWarps, smem_count, lc.stream>>>(
+                a.order, a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, nullptr, nullptr);
             lc.count++;
         }
         e = exclusive_scan_u32(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.scan_tmp, nullptr);
         if (e != cudaSuccess) return e;
         {
             LaunchScope s(lc, "st_emit");
-            st_chunk_kernel<true><<<nchunks, 32, smem, lc.stream>>>(a.order, a.rect_ref, a.n_surv, ts, ts_shift,
-                                                                    a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
-                                                                    a.st_cover);
+            st_chunk_kernel<true><<<nchunks * kStWarps, 32, smem_emit, lc.stream>>>(
+                a.order, a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
+                a.st_cover);
             lc.count++;
         }
         gauss = a.st_gauss[0];

@@ -17,6 +17,7 @@
 // (stable), publish per-digit tile counts, look back per digit (one thread per digit) for the
 // tile's global digit offsets, and scatter.  2 + passes launches per sort instead of 5 per pass.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -428,6 +429,17 @@ void launch_onesweep(LaunchCtx& lc, const uint32_t* ki, const uint32_t* vi, uint
 // whose digit is the same for every key are skipped, and the buffer chain is routed through a
 // third buffer so the result always lands in (keys1, vals1).
 namespace cg = cooperative_groups;
+#ifdef SPLAT_SORT_STAMPS  // phase timestamps of CTA 0 printed at exit (tools/variant_build.py experiments)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define STAMP(i) \
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamps[i] = gtimer()
+#else
+#define STAMP(i)
+#endif
 constexpr int kCoopItems = 16;
 constexpr int kCoopTile = kThreads * kCoopItems;  // 4096 (245 CTAs at N = 1 M: fewer to barrier)
 
@@ -437,7 +449,13 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                                                                  uint32_t n, uint32_t* __restrict__ hist,
                                                                  uint32_t* __restrict__ counts) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t s_cnt[kWarps][256];
+#ifdef SPLAT_SORT_STAMPS
+    unsigned long long stamps[32];
+    int ns = 0;
+#endif
+    STAMP(0);
+    constexpr int kVW = 2 * kWarps;  // virtual warps (two per warp)
+    __shared__ __align__(16) uint16_t s_cnt[kVW][256];
     __shared__ uint32_t s_gh[4][256];
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint32_t s_delta[256];
@@ -467,7 +485,9 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     __syncthreads();
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads)
         if ((&s_gh[0][0])[i]) atomicAdd(&hist[i], (&s_gh[0][0])[i]);
+    STAMP(1);
     grid.sync();
+    STAMP(2);
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = hist[i];
     __syncthreads();
     // executed passes (uniform over the grid) and the buffer chain 0 -> ... -> 1 (alternating
@@ -504,38 +524,57 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                 v[r] = i < n ? vb[src][i] : 0u;
             }
         }
-        for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&s_cnt[0][0])[i] = 0u;
+        for (int i = threadIdx.x; i < kVW * 256 / 2; i += kThreads) reinterpret_cast<uint32_t*>(&s_cnt[0][0])[i] = 0u;
         __syncthreads();
+        // Stable ranks per virtual warp: warp w's rows 0-7 are virtual warp 2w, rows 8-15 virtual
+        // warp 2w + 1 (key order), so each warp runs two independent counter chains.  Lanes with
+        // equal digits are found with 8 ballots (faster than __match_any_sync).
         uint32_t rank[kCoopItems];
 #pragma unroll
-        for (int r = 0; r < kCoopItems; ++r) {
-            const bool valid = wbase + r * 32 + lane < n;
-            const uint32_t d = (k[r] >> shift) & 255u;
-            const uint32_t label = valid ? d : (0x80000000u | (uint32_t)lane);
-            const unsigned peers = __match_any_sync(0xffffffffu, label);
-            const uint32_t old = valid ? s_cnt[warp][d] : 0u;
+        for (int r = 0; r < kCoopItems / 2; ++r) {
+            unsigned peers[2];
+            uint32_t dd[2], old[2];
+            bool valid[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = r + h * (kCoopItems / 2);
+                valid[h] = wbase + rr * 32 + lane < n;
+                dd[h] = (k[rr] >> shift) & 255u;
+                unsigned pm = __ballot_sync(0xffffffffu, valid[h]);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const bool bit = (dd[h] >> b) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                    pm &= bit ? bal : ~bal;
+                }
+                peers[h] = pm;
+                old[h] = valid[h] ? s_cnt[2 * warp + h][dd[h]] : 0u;
+            }
             __syncwarp();
-            if (valid && (peers & lt) == 0u) s_cnt[warp][d] = old + __popc(peers);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (valid[h] && (peers[h] & lt) == 0u) s_cnt[2 * warp + h][dd[h]] = (uint16_t)(old[h] + __popc(peers[h]));
             __syncwarp();
-            rank[r] = old + __popc(peers & lt);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) rank[r + h * (kCoopItems / 2)] = old[h] + __popc(peers[h] & lt);
         }
         __syncthreads();
         // thread d: tile total of digit d (published digit-major), its local start L (exclusive
-        // over digits) and the local start of every warp's run of d
+        // over digits) and the local start of every virtual warp's run of d (< 4096: fits 16 bits)
         uint32_t local_start;
         {
             const int d = threadIdx.x;
             uint32_t c = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) c += s_cnt[w][d];
+            for (int w = 0; w < kVW; ++w) c += s_cnt[w][d];
             counts[(size_t)d * ntiles + tile] = c;
             uint32_t tot;
             local_start = block_exclusive_scan(c, &tot, s_warp);
             uint32_t run = local_start;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
+            for (int w = 0; w < kVW; ++w) {
                 const uint32_t cw = s_cnt[w][d];
-                s_cnt[w][d] = run;
+                s_cnt[w][d] = (uint16_t)run;
                 run += cw;
             }
         }
@@ -543,11 +582,13 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
 #pragma unroll
         for (int r = 0; r < kCoopItems; ++r)
             if (wbase + r * 32 + lane < n) {
-                const uint32_t lp = s_cnt[warp][(k[r] >> shift) & 255u] + rank[r];
+                const uint32_t lp = s_cnt[2 * warp + r / (kCoopItems / 2)][(k[r] >> shift) & 255u] + rank[r];
                 s_k[lp] = k[r];
                 s_v[lp] = v[r];
             }
+        STAMP(3 + 6 * j);
         grid.sync();
+        STAMP(4 + 6 * j);
         // phase B: digit rows, exclusive over tiles, plus the digit's global base
         for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) {
             uint32_t base = 0;  // exclusive scan of the pass histogram up to d (cheap: <= 256 adds)
@@ -576,7 +617,9 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                 carry += tot;
             }
         }
+        STAMP(5 + 6 * j);
         grid.sync();
+        STAMP(6 + 6 * j);
         // phase C: global position = tile's global offset of the digit + (local position - L)
         s_delta[threadIdx.x] = counts[(size_t)threadIdx.x * ntiles + tile] - local_start;
         __syncthreads();
@@ -590,8 +633,18 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             vd[pos] = s_v[i];
         }
         src = dst;
+        STAMP(7 + 6 * j);
         grid.sync();
+        STAMP(8 + 6 * j);
     }
+#ifdef SPLAT_SORT_STAMPS
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ns = 3 + 6 * m;
+        printf("SORTSTAMPS m=%d", m);
+        for (int i = 1; i < ns; ++i) printf(" %llu", stamps[i] - stamps[i - 1]);
+        printf("\n");
+    }
+#endif
 }
 
 }  // namespace

@@ -2,7 +2,7 @@
 """Build a variant of the product library from a patched copy of one source file, into
 paper_2411_12788_b200/lib_<name>/ (for A/B timing with SPLAT_B200_LIB; not used by the product).
 
-    python tools/variant_build.py <name> <source.cu> <sed-expression>
+    python tools/variant_build.py <name> <source.cu> <sed-expression | file:<path>>
 """
 import shutil
 import subprocess
@@ -17,7 +17,10 @@ work = Path("/tmp") / f"variant_{name}"
 if work.exists():
     shutil.rmtree(work)
 shutil.copytree(b.CSRC, work)
-subprocess.run(["sed", "-i", expr, str(work / src)], check=True)
+if expr.startswith("file:"):  # replace the source by another file (e.g. a copy from git history)
+    shutil.copy(expr[5:], work / src)
+else:
+    subprocess.run(["sed", "-i", expr, str(work / src)], check=True)
 b.CSRC = work
 b.HEADERS = [work / "common.cuh", work / "internal.h"] + b.HEADERS[2:]
 b.OBJ = b.PKG / f"build_{name}"
