@@ -61,6 +61,57 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
                  : "memory");
 }
 
+// One committed sample of the per-pixel back-to-front recursion (gradients.cpp:73-123) in moment
+// form: with s = dL/dalpha * g (the opacity gradient of the sample), the pixel adds s, s dx, s dy,
+// s dx^2, s dx dy, s dy^2 to vv[0..5]; the per-Gaussian factors (opacity, conic) are applied once
+// per Gaussian by the chain (chain.cu), after the sums over all pixels:
+//   d mean.x = -o (c0 Sx + c1 Sy), d mean.y = -o (c2 Sy + c1 Sx), d conic = -o/2 (Sxx, Sxy, Syy),
+// which is sum(dpower * (-(c0 dx + c1 dy))), ... of the reference with dpower = o s.  vv[6..8] get
+// the colour gradient w dL, vv[9] counts the commit.  T_before = T_after / (1 - alpha).
+__device__ __forceinline__ void commit_sample(float* vv, float& T, float& b0, float& b1, float& b2, float dL0,
+                                              float dL1, float dL2, const float4& r2, float alpha, float g2d,
+                                              bool clamped, float dx, float dy) {
+    const float one_m_a = 1.0f - alpha;
+    const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
+    const float w = t_before * alpha;
+    vv[6] += w * dL0;
+    vv[7] += w * dL1;
+    vv[8] += w * dL2;
+    const float da = t_before * (dL0 * (r2.x - b0) + dL1 * (r2.y - b1) + dL2 * (r2.z - b2));
+    if (!clamped) {
+        const float sv = da * g2d;
+        const float sx = sv * dx, sy = sv * dy;
+        vv[0] += sv;
+        vv[1] += sx;
+        vv[2] += sy;
+        vv[3] += sx * dx;
+        vv[4] += sx * dy;
+        vv[5] += sy * dy;
+    }
+    vv[9] += 1.0f;
+    b0 = alpha * r2.x + one_m_a * b0;
+    b1 = alpha * r2.y + one_m_a * b1;
+    b2 = alpha * r2.z + one_m_a * b2;
+    T = t_before;
+}
+
+// Warp-reduce the 24 values of staged entries ja (v[0..11]) and jb (v[12..23]) and add them to
+// the per-Gaussian accumulator (common.cuh kG2Stride records): lanes 4g hold group g's totals;
+// groups 0-2 are added as they are (moments, colour), the commit count (group 3) rides in the
+// 4th slot of group 2's record.
+__device__ __forceinline__ void emit_entry_grads(const float v[24], int lane, bool any_a, bool any_b, uint32_t ja,
+                                                 uint32_t jb, uint32_t a_gid, float4* __restrict__ grad2d) {
+    float r[3];
+    warp_reduce24(v, lane, r);
+    const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
+    const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
+    const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
+    if (mine) {
+        const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? ja : jb));
+        red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2], (grp & 3) == 2 ? cnt : 0.0f);
+    }
+}
+
 // Blend backward (gradients.cpp:73-123): per pixel, walk the tile list back to front from the
 // pixel's last committed sample, re-evaluating the forward gates; b = colour behind the sample
 // (normalised), exactly the reference recursion; T_before = T_after / (1 - alpha).
@@ -186,33 +237,10 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
             float v[24];
 #pragma unroll
             for (int k = 0; k < 24; ++k) v[k] = 0.0f;
-            auto commit = [&](float* vv, const float4& r0, const float4& r1, const float4& r2, float alpha, float g2d,
-                              bool clamped, float dx, float dy) {
-                const float one_m_a = 1.0f - alpha;
-                const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
-                const float w = t_before * alpha;
-                vv[6] = w * dL0;
-                vv[7] = w * dL1;
-                vv[8] = w * dL2;
-                const float da = t_before * (dL0 * (r2.x - b0) + dL1 * (r2.y - b1) + dL2 * (r2.z - b2));
-                if (!clamped) {
-                    vv[5] = da * g2d;
-                    const float dpower = da * r1.y * g2d;
-                    vv[0] = dpower * (-(r0.z * dx + r0.w * dy));
-                    vv[1] = dpower * (-(r1.x * dy + r0.w * dx));
-                    const float hp = -0.5f * dpower;
-                    vv[2] = hp * dx * dx;
-                    vv[3] = hp * dx * dy;
-                    vv[4] = hp * dy * dy;
-                }
-                vv[9] = 1.0f;
-                b0 = alpha * r2.x + one_m_a * b0;
-                b1 = alpha * r2.y + one_m_a * b1;
-                b2 = alpha * r2.z + one_m_a * b2;
-                T = t_before;
-            };
-            if (ga) commit(v, r0a, r1a, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
-            if (gb) commit(v + 12, r0b, r1b, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+            if (ga) commit_sample(v, T, b0, b1, b2, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
+            if (gb)
+                commit_sample(v + 12, T, b0, b1, b2, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb,
+                              dyb);
             const bool any_a = __any_sync(0xffffffffu, ga), any_b = __any_sync(0xffffffffu, gb);
 #ifdef SPLAT_STATS
             {
@@ -228,19 +256,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
                 }
             }
 #endif
-            if (any_a || any_b) {
-                float r[3];
-                warp_reduce24(v, lane, r);
-                const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
-                // the commit count (value 9, group 3) rides in the 4th slot of group 2's record
-                const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
-                const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
-                if (mine) {
-                    const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
-                    red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2],
-                               (grp & 3) == 2 ? cnt : 0.0f);
-                }
-            }
+            if (any_a || any_b) emit_entry_grads(v, lane, any_a, any_b, (uint32_t)j, jb, a_gid, grad2d);
         }
         // the next stage() starts with a barrier before it overwrites the staging area
     }
@@ -377,31 +393,6 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
 #pragma unroll
             for (int k = 0; k < 24; ++k) v[k] = 0.0f;
             bool anyc_a = false, anyc_b = false;
-            auto commit = [&](float* vv, PixBwd& q, const float4& r0, const float4& r1, const float4& r2, float alpha,
-                              float g2d, bool clamped, float dx, float dy) {
-                const float one_m_a = 1.0f - alpha;
-                const float t_before = __fdividef(q.T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
-                const float w = t_before * alpha;
-                vv[6] += w * q.dL0;
-                vv[7] += w * q.dL1;
-                vv[8] += w * q.dL2;
-                const float da = t_before * (q.dL0 * (r2.x - q.b0) + q.dL1 * (r2.y - q.b1) + q.dL2 * (r2.z - q.b2));
-                if (!clamped) {
-                    vv[5] += da * g2d;
-                    const float dpower = da * r1.y * g2d;
-                    vv[0] += dpower * (-(r0.z * dx + r0.w * dy));
-                    vv[1] += dpower * (-(r1.x * dy + r0.w * dx));
-                    const float hp = -0.5f * dpower;
-                    vv[2] += hp * dx * dx;
-                    vv[3] += hp * dx * dy;
-                    vv[4] += hp * dy * dy;
-                }
-                vv[9] += 1.0f;
-                q.b0 = alpha * r2.x + one_m_a * q.b0;
-                q.b1 = alpha * r2.y + one_m_a * q.b1;
-                q.b2 = alpha * r2.z + one_m_a * q.b2;
-                q.T = t_before;
-            };
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const bool wa = h == 0 ? waA : waB, wb = h == 0 ? wbA : wbB;
@@ -413,25 +404,17 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 bool gb = gate_sample_nb<THR>(r0b, r1b, q.bits, q.x, q.y, amax_c, cmin, alpha_b, g_b, cl_b, dxb, dyb);
                 ga = ga && wa && idx_a <= q.last;
                 gb = gb && wb && idx_b <= q.last;
-                if (ga) commit(v, q, r0a, r1a, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
-                if (gb) commit(v + 12, q, r0b, r1b, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+                if (ga)
+                    commit_sample(v, q.T, q.b0, q.b1, q.b2, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
+                                  cl_a, dxa, dya);
+                if (gb)
+                    commit_sample(v + 12, q.T, q.b0, q.b1, q.b2, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
+                                  g_b, cl_b, dxb, dyb);
                 anyc_a |= ga;
                 anyc_b |= gb;
             }
             const bool any_a = __any_sync(0xffffffffu, anyc_a), any_b = __any_sync(0xffffffffu, anyc_b);
-            if (any_a || any_b) {
-                float r[3];
-                warp_reduce24(v, lane, r);
-                const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
-                // the commit count (value 9, group 3) rides in the 4th slot of group 2's record
-                const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
-                const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
-                if (mine) {
-                    const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? (uint32_t)j : jb));
-                    red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2],
-                               (grp & 3) == 2 ? cnt : 0.0f);
-                }
-            }
+            if (any_a || any_b) emit_entry_grads(v, lane, any_a, any_b, (uint32_t)j, jb, a_gid, grad2d);
         }
     }
     pipe.finish();

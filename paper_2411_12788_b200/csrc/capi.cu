@@ -153,6 +153,8 @@ struct splat_ctx {
     // view's blend forward (ev_fwd_start) and joined before the chain (ev_zero).
     cudaStream_t zstream = nullptr;
     cudaEvent_t ev_fwd_start = nullptr, ev_zero = nullptr;
+    // the L1 partial sums are reduced on zstream (ev_bwd -> loss_reduce -> ev_loss), beside the chain
+    cudaEvent_t ev_bwd = nullptr, ev_loss = nullptr;
     bool fwd_start_recorded = false;
     FwdState st;
 };
@@ -628,6 +630,18 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
                                  partials, ctx->grad2d.as<float>(), st.blist, st.bidx, st.bcount),
            "blend backward");
     }
+    const float inv_n = 1.0f / (float)(3 * (int64_t)st.cp.width * st.cp.height);
+    // with the side stream in use, the loss reduction (one small CTA) runs there beside the chain
+    const bool loss_side = partials && zero_async;
+    if (loss_side) {
+        CK(cudaEventRecord(ctx->ev_bwd, ctx->stream), "record backward");
+        CK(cudaStreamWaitEvent(ctx->zstream, ctx->ev_bwd, 0), "loss wait");
+        lc.stream = ctx->zstream;
+        const cudaError_t e = launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev);
+        lc.stream = ctx->stream;
+        CK(e, "loss reduce");
+        CK(cudaEventRecord(ctx->ev_loss, ctx->zstream), "record loss");
+    }
     if (n > 0) {
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
         CK(ctx->chain_list.ensure(((size_t)st.n_surv + 2) * 4), "alloc chain list");
@@ -636,10 +650,8 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
                         ctx->chain_list.as<uint32_t>(), zero_async),
            "chain");
     }
-    if (partials) {
-        const float inv_n = 1.0f / (float)(3 * (int64_t)st.cp.width * st.cp.height);
-        CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
-    }
+    if (loss_side) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_loss, 0), "loss join");
+    else if (partials) CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
     (void)cfg;
     (void)mask;
     return SPLAT_OK;
@@ -667,7 +679,9 @@ int splat_ctx_create(int device, splat_ctx** out) {
         cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_free, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd_start, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_zero, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_zero, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_bwd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_loss, cudaEventDisableTiming) != cudaSuccess) {
         cudaFree(c->lc.work_counters);
         delete c;
         return SPLAT_ERR_CUDA;
@@ -692,6 +706,8 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (ctx->lc.work_counters) cudaFree(ctx->lc.work_counters);
     if (ctx->ev_fwd_start) cudaEventDestroy(ctx->ev_fwd_start);
     if (ctx->ev_zero) cudaEventDestroy(ctx->ev_zero);
+    if (ctx->ev_bwd) cudaEventDestroy(ctx->ev_bwd);
+    if (ctx->ev_loss) cudaEventDestroy(ctx->ev_loss);
     if (ctx->zstream) {
         cudaStreamSynchronize(ctx->zstream);
         cudaStreamDestroy(ctx->zstream);

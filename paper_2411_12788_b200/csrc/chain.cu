@@ -108,8 +108,8 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
                                           const ProjRec* __restrict__ rec, splat_param_grads out, int accumulate,
                                           int i, float4* s_sh, int row) {
     if (i >= g.n) return;
-    // accumulator (blend_backward): g0 = (dmean.x, dmean.y, dconic00), g1 = (dconic01, dconic11,
-    // dopacity), g2 = (d colour, number of committed (warp, pixel) samples)
+    // accumulator (blend_backward, moment form): g0 = (S0, Sx, Sy), g1 = (Sxx, Sxy, Syy) with
+    // s = dL/dalpha g per sample, g2 = (d colour, number of committed (warp, pixel) samples)
     const float4 g0 = grad2d[kG2Stride * (size_t)i], g1 = grad2d[kG2Stride * (size_t)i + 1], g2 = grad2d[kG2Stride * (size_t)i + 2];
     const float cnt = g2.w;
     const size_t i3 = 3 * (size_t)i, i4 = 4 * (size_t)i, i48 = 48 * (size_t)i;
@@ -144,11 +144,15 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
 #pragma unroll
     for (int k = 0; k < 3; ++k) grad2d[kG2Stride * (size_t)i + k] = zero4;
 
-    const float dm0 = g0.x, dm1 = g0.y;
-    const float dQ[4] = {g0.z, g1.x, g1.x, g1.y};  // row-major (00, 01, 10, 11); 01 == 10
-    const float dopac = g1.z;
-    const float dcol[3] = {g2.x, g2.y, g2.z};
     const float k0 = pr.r0.z, k1 = pr.r0.w, k2 = pr.r1.x, opacity = pr.r1.y;
+    // moments -> 2D gradients (backward.cu commit_sample): dmean = -o (conic (Sx, Sy)),
+    // dconic = -o/2 (Sxx, Sxy, Syy), dopacity = S0
+    const float dm0 = -opacity * (k0 * g0.y + k1 * g0.z);
+    const float dm1 = -opacity * (k2 * g0.z + k1 * g0.y);
+    const float hq = -0.5f * opacity;
+    const float dQ[4] = {hq * g1.x, hq * g1.y, hq * g1.y, hq * g1.z};  // row-major (00, 01, 10, 11); 01 == 10
+    const float dopac = g0.x;
+    const float dcol[3] = {g2.x, g2.y, g2.z};
 
     const float gaccum = sqrtf(dm0 * dm0 + dm1 * dm1);
     // dV = (-Q) dQ Q

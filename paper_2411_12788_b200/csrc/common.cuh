@@ -17,8 +17,8 @@ namespace splat_b200 {
 
 constexpr int kBlock = 256;  // threads per tile CTA (16 x 16 pixels)
 
-// 2D gradient accumulator of blend_backward: 3 float4 per Gaussian, (dmean.x, dmean.y, dconic00,
-// 0), (dconic01, dconic11, dopacity, 0), (dcolour rgb, number of committed (warp, pixel) samples).
+// 2D gradient accumulator of blend_backward: 3 float4 per Gaussian in moment form (backward.cu
+// commit_sample), (S0, Sx, Sy, 0), (Sxx, Sxy, Syy, 0), (dcolour rgb, committed (warp, pixel) samples).
 constexpr int kG2Stride = 3;
 constexpr size_t grad2d_bytes(size_t n) { return n * 16 * kG2Stride; }
 
