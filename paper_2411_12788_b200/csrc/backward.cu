@@ -68,16 +68,19 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
 //   d mean.x = -o (c0 Sx + c1 Sy), d mean.y = -o (c2 Sy + c1 Sx), d conic = -o/2 (Sxx, Sxy, Syy),
 // which is sum(dpower * (-(c0 dx + c1 dy))), ... of the reference with dpower = o s.  vv[6..8] get
 // the colour gradient w dL, vv[9] counts the commit.  T_before = T_after / (1 - alpha).
-__device__ __forceinline__ void commit_sample(float* vv, float& T, float& b0, float& b1, float& b2, float dL0,
-                                              float dL1, float dL2, const float4& r2, float alpha, float g2d,
-                                              bool clamped, float dx, float dy) {
+__device__ __forceinline__ void commit_sample(float* vv, float& T, float& B, float dL0, float dL1, float dL2,
+                                              const float4& r2, float alpha, float g2d, bool clamped, float dx,
+                                              float dy) {
     const float one_m_a = 1.0f - alpha;
     const float t_before = __fdividef(T, one_m_a);  // 2 ulp; T_before is not bit-exact anyway
     const float w = t_before * alpha;
     vv[6] += w * dL0;
     vv[7] += w * dL1;
     vv[8] += w * dL2;
-    const float da = t_before * (dL0 * (r2.x - b0) + dL1 * (r2.y - b1) + dL2 * (r2.z - b2));
+    // B = dL . b, b the colour behind the sample (gradients.cpp: b = alpha c + (1 - alpha) b): the
+    // recursion is linear in b, so the pixel carries the scalar dL . b instead of three channels
+    const float diff = (dL0 * r2.x + dL1 * r2.y + dL2 * r2.z) - B;
+    const float da = t_before * diff;
     if (!clamped) {
         const float sv = da * g2d;
         const float sx = sv * dx, sy = sv * dy;
@@ -89,9 +92,7 @@ __device__ __forceinline__ void commit_sample(float* vv, float& T, float& b0, fl
         vv[5] += sy * dy;
     }
     vv[9] += 1.0f;
-    b0 = alpha * r2.x + one_m_a * b0;
-    b1 = alpha * r2.y + one_m_a * b1;
-    b2 = alpha * r2.z + one_m_a * b2;
+    B = B + alpha * diff;
     T = t_before;
 }
 
@@ -199,7 +200,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
     const uint32_t a_r0 = smem_base(sm.r0), a_r1 = smem_base(sm.r1), a_r2 = smem_base(sm.r2);
     const uint32_t a_idx = smem_base(sm.idx), a_gid = smem_base(sm.gid);
     float T = inside ? t_final[pix] : 1.0f;
-    float b0 = bg0, b1 = bg1, b2 = bg2;
+    float B = dL0 * bg0 + dL1 * bg1 + dL2 * bg2;
 
     auto pos = [&](int b, int t) -> int {
         const int i = block_last - b * nthreads - t;
@@ -237,9 +238,9 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
             float v[24];
 #pragma unroll
             for (int k = 0; k < 24; ++k) v[k] = 0.0f;
-            if (ga) commit_sample(v, T, b0, b1, b2, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
+            if (ga) commit_sample(v, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
             if (gb)
-                commit_sample(v + 12, T, b0, b1, b2, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb,
+                commit_sample(v + 12, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb,
                               dyb);
             const bool any_a = __any_sync(0xffffffffu, ga), any_b = __any_sync(0xffffffffu, gb);
 #ifdef SPLAT_STATS
@@ -270,7 +271,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
 // work per pixel), and the two pixel chains are independent instruction streams.  Entries whose
 // effective rect misses a half skip that half's gates (warp-uniform).
 struct PixBwd {
-    float T, b0, b1, b2, dL0, dL1, dL2, x, y;
+    float T, B, dL0, dL1, dL2, x, y;
     int last;
     uint32_t bits;
 };
@@ -325,9 +326,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
         }
         q.last = inside ? last_index[pix] : -1;
         q.T = inside ? t_final[pix] : 1.0f;
-        q.b0 = bg0;
-        q.b1 = bg1;
-        q.b2 = bg2;
+        q.B = q.dL0 * bg0 + q.dL1 * bg1 + q.dL2 * bg2;
         q.x = (float)px + 0.5f;
         q.y = (float)py + 0.5f;
         q.bits = (1u << lx) | (1u << (16 + ly + 4 * h));
@@ -405,10 +404,10 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 ga = ga && wa && idx_a <= q.last;
                 gb = gb && wb && idx_b <= q.last;
                 if (ga)
-                    commit_sample(v, q.T, q.b0, q.b1, q.b2, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
+                    commit_sample(v, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
                                   cl_a, dxa, dya);
                 if (gb)
-                    commit_sample(v + 12, q.T, q.b0, q.b1, q.b2, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
+                    commit_sample(v + 12, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
                                   g_b, cl_b, dxb, dyb);
                 anyc_a |= ga;
                 anyc_b |= gb;

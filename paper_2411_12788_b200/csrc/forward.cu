@@ -350,7 +350,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 // CTAs sharing its list (blockIdx.y).  The tile list is walked in batches of blockDim.x entries;
 // each batch is culled to the Gaussians that can reach the alpha floor inside the block and
 // staged in shared memory, and all threads walk it in the same order (broadcast reads).
-template <bool REPORT, bool THR, int BW, int BH>
+// ARG: track each pixel's max-weight sample (max_contributor, depth, importance counts); off in
+// training, where only colour, T and the last committed position are consumed.
+template <bool REPORT, bool THR, int BW, int BH, bool ARG = true>
 __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
@@ -483,7 +485,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                         acc0 = acc0 + w * r2.x;
                         acc1 = acc1 + w * r2.y;
                         acc2 = acc2 + w * r2.z;
-                        if (w > wmax) {
+                        if (ARG && w > wmax) {
                             wmax = w;
                             amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
                         }
@@ -501,7 +503,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                         acc0 = acc0 + w * r2.x;
                         acc1 = acc1 + w * r2.y;
                         acc2 = acc2 + w * r2.z;
-                        if (w > wmax) {
+                        if (ARG && w > wmax) {
                             wmax = w;
                             amax_gid = (int32_t)lds_u32(a_gid + 4u * jb);
                         }
@@ -530,7 +532,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                                 acc0 = acc0 + w * r2.x;
                                 acc1 = acc1 + w * r2.y;
                                 acc2 = acc2 + w * r2.z;
-                                if (w > wmax) {
+                                if (ARG && w > wmax) {
                                     wmax = w;
                                     amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
                                 }
@@ -611,18 +613,18 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
     }
 }
 
-template <bool REPORT, bool THR, int BW, int BH>
+template <bool REPORT, bool THR, int BW, int BH, bool ARG>
 __global__ void __launch_bounds__(BW * BH) blend_forward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
                                                            float bg2, FwdOutputs out) {
-    blend_forward_block<REPORT, THR, BW, BH>((int)blockIdx.x, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
+    blend_forward_block<REPORT, THR, BW, BH, ARG>((int)blockIdx.x, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
 }
 
 // Persistent variant: one wave of CTAs pulls pixel blocks from a work counter (no CTA launch /
 // retire gaps between blocks, occupancy stays at the register limit through the whole kernel).
-template <bool REPORT, bool THR, int BW, int BH>
+template <bool REPORT, bool THR, int BW, int BH, bool ARG>
 __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp, const uint32_t* __restrict__ ranges,
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp
         __syncthreads();
         const int b = s_bid;
         if (b >= nblocks) break;
-        blend_forward_block<REPORT, THR, BW, BH>(b, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
+        blend_forward_block<REPORT, THR, BW, BH, ARG>(b, cp, ranges, pair_gauss, rec, aux, bg0, bg1, bg2, out);
     }
 }
 
@@ -714,33 +716,37 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
     const int ts = cp.tile_size;
     const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     LaunchScope ls_(lc, "blend_forward");
-#define BLEND_FWD_SHAPE(R, T, W, H)                                                                              \
+#define BLEND_FWD_SHAPE(R, T, W, H, A)                                                                           \
     do {                                                                                                         \
         if (lc.persistent_blend && lc.work_counters) {                                                           \
             static int per_sm = 0;                                                                               \
-            if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_forward_persistent<R, T, W, H>, \
+            if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_forward_persistent<R, T, W, H, A>, \
                                                                       W * H, 0);                                 \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                             \
             cudaMemsetAsync(lc.work_counters, 0, 4, lc.stream);                                                  \
-            blend_forward_persistent<R, T, W, H><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(               \
+            blend_forward_persistent<R, T, W, H, A><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(            \
                 cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters);       \
         } else {                                                                                                 \
-            blend_forward_kernel<R, T, W, H><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, bg[0], \
-                                                                           bg[1], bg[2], out);                   \
+            blend_forward_kernel<R, T, W, H, A><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, \
+                                                                              bg[0], bg[1], bg[2], out);         \
         }                                                                                                        \
     } while (0)
-#define BLEND_FWD(R, T)                                                        \
+#define BLEND_FWD(R, T, A)                                                     \
     do {                                                                       \
-        if (cp.block_w == 16) BLEND_FWD_SHAPE(R, T, 16, 16);                   \
-        else if (cp.block_h == 8) BLEND_FWD_SHAPE(R, T, 8, 8);                 \
-        else BLEND_FWD_SHAPE(R, T, 8, 4);                                      \
+        if (cp.block_w == 16) BLEND_FWD_SHAPE(R, T, 16, 16, A);                \
+        else if (cp.block_h == 8) BLEND_FWD_SHAPE(R, T, 8, 8, A);              \
+        else BLEND_FWD_SHAPE(R, T, 8, 4, A);                                   \
     } while (0)
+    const bool arg = out.max_contributor || out.depth;
     if (out.importance) {
-        if (cp.apply_thresholds) BLEND_FWD(true, true);
-        else BLEND_FWD(true, false);
+        if (cp.apply_thresholds) BLEND_FWD(true, true, true);
+        else BLEND_FWD(true, false, true);
+    } else if (arg) {
+        if (cp.apply_thresholds) BLEND_FWD(false, true, true);
+        else BLEND_FWD(false, false, true);
     } else {
-        if (cp.apply_thresholds) BLEND_FWD(false, true);
-        else BLEND_FWD(false, false);
+        if (cp.apply_thresholds) BLEND_FWD(false, true, false);
+        else BLEND_FWD(false, false, false);
     }
 #undef BLEND_FWD_SHAPE
 #undef BLEND_FWD
