@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
     const int32_t* __restrict__ bcount) {
     for (;;) {
         int b = 0;
-        if (threadIdx.x == 0) b = atomicAdd(counter, 1);
+        if (threadIdx.x == 0) b = pull_work(counter, nblocks);
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b >= nblocks) break;
         const int bc = blist ? bcount[b] : kBlockList + 1;
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_persistent(CamParams c
     __shared__ int s_bid;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_bid = atomicAdd(counter, 1);
+        if (threadIdx.x == 0) s_bid = pull_work(counter, nblocks);
         __syncthreads();
         const int b = s_bid;
         if (b >= nblocks) break;
@@ -635,7 +635,6 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
             if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_backward_persistent<T, W, H>, \
                                                                       W * H, 0);                                  \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                              \
-            cudaMemsetAsync(lc.work_counters + 1, 0, 4, lc.stream);                                               \
             blend_backward_persistent<T, W, H><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(                  \
                 cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
                 loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);              \
@@ -660,7 +659,6 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
             }
             unsigned pg = (unsigned)(lc.num_sms * (per_sm[k] > 0 ? per_sm[k] : 1));
             if (pg > grid) pg = grid;
-            cudaMemsetAsync(lc.work_counters + 1, 0, 4, lc.stream);
             if (k)
                 blend_backward_px2_persistent<true><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,

@@ -482,7 +482,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
                 a.order, a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, nullptr, nullptr);
             lc.count++;
         }
-        e = exclusive_scan_u32(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.scan_tmp, nullptr);
+        e = exclusive_scan_u32_zeroed(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.st_scan_tmp);
         if (e != cudaSuccess) return e;
         {
             LaunchScope s(lc, "st_emit");

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <map>
 #include <vector>
@@ -124,11 +125,15 @@ struct splat_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     LaunchCtx lc;
+    // run once by the next run_forward right after it queued the blend forward: splat_train_step
+    // issues its host->device target copies there, so the bulk transfer overlaps the (long,
+    // launch-free) forward kernel instead of slowing the launches of the sort and binning kernels
+    std::function<int()> post_forward_hook;
     std::string err;
     // per-Gaussian
     DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
     // per-pair
-    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_ranges, l2_tmp, st_cover;
+    DevBuf pair_gauss[2], st_key[2], st_gauss[2], st_cnt, st_scan_tmp, st_ranges, l2_tmp, st_cover;
     // misc
     DevBuf chain_list, ranges, hist, scan_tmp, t_final, last_index, color, loss_partials, flags, flag_offsets;
     // densify / simplify scratch (separate from the forward's buffers)
@@ -146,7 +151,8 @@ struct splat_ctx {
     DevBuf blist, bidx, bcount;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_free = nullptr, ev_copied[8] = {};
-    uint32_t* host_counters = nullptr;  // pinned [n_surv, Ps, P]
+    uint32_t* host_counters = nullptr;  // mapped pinned [n_surv, Ps, P], written by preprocess's last block
+    uint32_t* host_counters_dev = nullptr;  // its device alias
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
     // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
@@ -272,7 +278,7 @@ cudaError_t depth_sort(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint64_t 
     if (ctx->coop_sort) {
         cudaError_t e = ctx->ktmp.ensure(n * 4);
         if (e == cudaSuccess) e = ctx->vtmp.ensure(n * 4);
-        if (e == cudaSuccess) e = ctx->coop_work.ensure(radix_coop_count_words(n) * 4);
+        if (e == cudaSuccess) e = ctx->coop_work.ensure(radix_coop_count_words(n) * 4, true, ctx->stream);
         if (e != cudaSuccess) return e;
         e = radix_sort_coop(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(),
                             ctx->ktmp.as<uint32_t>(), ctx->vtmp.as<uint32_t>(), n, ctx->coop_work.as<uint32_t>());
@@ -317,7 +323,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     CK(ctx->rect_ref.ensure(nn * 8), "alloc rects");
     CK(ctx->counts_sorted.ensure(nn * 4), "alloc counts");
     CK(ctx->offsets.ensure((nn + 1) * 4), "alloc offsets");
-    CK(ctx->counters.ensure(64), "alloc counters");
+    CK(ctx->counters.ensure(64, true, s), "alloc counters");  // zero at rest (preprocess re-zeroes them)
     CK(ctx->hist.ensure(radix_hist_words(nn, 8) * 4), "alloc hist");
     CK(ctx->scan_tmp.ensure((scan_temp_words(radix_hist_words(nn, 8)) + scan_temp_words(nn) + 64) * 4), "alloc scan");
     CK(ctx->ranges.ensure((size_t)n_tiles * 8), "alloc ranges");
@@ -328,11 +334,14 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         CK(ctx->color.ensure(hw * 12), "alloc color");
         color_out = ctx->color.as<float>();
     }
-    if (!ctx->host_counters) CK(cudaMallocHost(&ctx->host_counters, 64), "alloc pinned");
+    if (!ctx->host_counters) {
+        CK(cudaHostAlloc(&ctx->host_counters, 64, cudaHostAllocMapped), "alloc pinned");
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_counters_dev), ctx->host_counters, 0),
+           "map pinned");
+    }
     if (!ctx->ev_counts) CK(cudaEventCreateWithFlags(&ctx->ev_counts, cudaEventDisableTiming), "event");
 
-    uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] = n_surv, [1] = P
-    CK(cudaMemsetAsync(d_counters, 0, 16, s), "memset counters");  // [0] survivors [1] Ps [2] P
+    uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] survivors [1] Ps [2] P [3] done blocks
     int n_surv = 0;
     uint64_t n_pairs = 0;
     const bool pairs_alt = false;
@@ -341,12 +350,12 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* keys = ctx->keys[0].as<uint32_t>();
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
-                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>()),
+                             keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
+                             ctx->host_counters_dev),
            "preprocess");
-        // The host needs [n_surv, Ps, P] (sizes and allocations below); they are final after
-        // preprocess, so the copy is queued before the depth sort and the host waits only for
-        // it: the sort runs while the rest of the view is enqueued.
-        CK(cudaMemcpyAsync(ctx->host_counters, d_counters, 12, cudaMemcpyDeviceToHost, s), "read counts");
+        // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
+        // writes them to mapped pinned memory, so the host waits only for preprocess (event) while
+        // the depth sort runs and the rest of the view is enqueued.
         CK(cudaEventRecord(ctx->ev_counts, s), "record counts");
         bool alt = false;
         CK(depth_sort(ctx, keys, vals, (uint64_t)n, &alt), "depth sort");
@@ -361,15 +370,20 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
                                          (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), nullptr),
                "scan supertile counts");
         CK(cudaEventSynchronize(ctx->ev_counts), "sync counts");
-        n_surv = (int)ctx->host_counters[0];
-        const uint64_t st_pairs = ctx->host_counters[1];
-        n_pairs = ctx->host_counters[2];
+        const volatile uint32_t* hc = ctx->host_counters;
+        n_surv = (int)hc[0];
+        const uint64_t st_pairs = hc[1];
+        n_pairs = hc[2];
         for (int k = 0; k < (chunked ? 1 : 2); ++k) {
             if (!chunked) CK(ctx->st_key[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
             CK(ctx->st_gauss[k].ensure(st_pairs * 4 + 4), "alloc st pairs");
         }
         const size_t st_words = chunked ? st_chunk_words(n_surv, n_st) : 1;
-        if (chunked) CK(ctx->st_cnt.ensure(st_words * 4), "alloc st counts");
+        if (chunked) {
+            CK(ctx->st_cnt.ensure(st_words * 4), "alloc st counts");
+            CK(ctx->st_scan_tmp.ensure(scan_temp_words((uint64_t)n_st * st_chunks(n_surv) + 1) * 4, true, s),
+               "alloc st scan");
+        }
         if (tile_list_capacity(st_pairs) >= (size_t)UINT32_MAX)
             return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "too many tile-Gaussian pairs for 32-bit list offsets");
         CK(ctx->pair_gauss[0].ensure(tile_list_capacity(st_pairs) * 4 + 4), "alloc pairs");
@@ -397,6 +411,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
             ba.st_gauss[k] = ctx->st_gauss[k].as<uint32_t>();
         }
         ba.st_cnt = ctx->st_cnt.as<uint32_t>();
+        ba.st_scan_tmp = ctx->st_scan_tmp.as<uint32_t>();
         ba.st_ranges = ctx->st_ranges.as<uint32_t>();
         ba.l2_tmp = ctx->l2_tmp.as<uint32_t>();
         ba.st_cover = ctx->st_cover.as<uint16_t>();
@@ -449,6 +464,11 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     CK(launch_blend_forward(lc, cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
                             want_depth ? ctx->aux.as<AuxRec>() : nullptr, bg, fo),
        "blend forward");
+    if (ctx->post_forward_hook) {
+        std::function<int()> hook;
+        hook.swap(ctx->post_forward_hook);
+        if ((rc = hook())) return rc;
+    }
     FwdState& st = ctx->st;
     st.cp = cp;
     st.n = n;
@@ -671,7 +691,9 @@ int splat_ctx_create(int device, splat_ctx** out) {
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         c->lc.num_sms = sms;
-    if (cudaMalloc(&c->lc.work_counters, 16 * sizeof(int)) != cudaSuccess) {
+    // persistent-kernel work queues: zero at rest (pull_work re-zeroes them)
+    if (cudaMalloc(&c->lc.work_counters, 16 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(c->lc.work_counters, 0, 16 * sizeof(int)) != cudaSuccess) {
         delete c;
         return SPLAT_ERR_OUT_OF_MEMORY;
     }
@@ -939,7 +961,7 @@ int splat_sort_pairs(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* k
     if (ctx->coop_sort && begin_bit == 0 && end_bit == 32 && n > 0) {  // the depth sort's path
         CK(ctx->ktmp.ensure((size_t)n * 4), "alloc");
         CK(ctx->vtmp.ensure((size_t)n * 4), "alloc");
-        CK(ctx->coop_work.ensure(radix_coop_count_words((uint64_t)n) * 4), "alloc");
+        CK(ctx->coop_work.ensure(radix_coop_count_words((uint64_t)n) * 4, true, ctx->stream), "alloc");
         const cudaError_t e = radix_sort_coop(ctx->lc, keys, vals, keys_alt, vals_alt, ctx->ktmp.as<uint32_t>(),
                                               ctx->vtmp.as<uint32_t>(), (uint64_t)n, ctx->coop_work.as<uint32_t>());
         if (e == cudaSuccess) {
@@ -1368,11 +1390,20 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         // the staging slots are free once everything already queued on the compute stream ran
         CK(cudaEventRecord(ctx->ev_free, s), "record");
         CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_free, 0), "wait");
-        for (int k = 0; k < std::min(n_views, slots); ++k)
-            if ((rc = issue_copy(k))) return rc;
+        // the first copies are issued from inside the first view's forward, once its blend
+        // forward is queued (a bulk H2D in flight delays the launches of the kernels before it)
+        ctx->post_forward_hook = [&, n_views]() -> int {
+            int r;
+            for (int k = 0; k < std::min(n_views, slots); ++k)
+                if ((r = issue_copy(k))) return r;
+            return SPLAT_OK;
+        };
     }
     for (int k = 0; k < n_views; ++k) {
-        if ((rc = run_forward(ctx, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr))) return rc;
+        rc = run_forward(ctx, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr);
+        if (rc == SPLAT_OK && ctx->post_forward_hook) rc = ctx->post_forward_hook();  // not run by run_forward
+        ctx->post_forward_hook = nullptr;
+        if (rc) return rc;
         const float* tgt = targets[k];
         if (targets_on_host) {
             const int slot = k % slots;

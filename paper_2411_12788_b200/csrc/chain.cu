@@ -393,7 +393,8 @@ __device__ __forceinline__ void zero_span_warp(float* p, int count, int lane) {
 // the same way.
 __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __restrict__ grad2d, int n,
                                                             splat_param_grads out, int zero_untouched,
-                                                            uint32_t* __restrict__ list) {
+                                                            uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                                                            uint32_t* __restrict__ count_next) {
     // one list append (atomic) per CTA: a single counter takes ~1 ns per atomic, so per-warp
     // appends would serialise ~n/32 of them
     __shared__ uint32_t s_wc[8];
@@ -411,10 +412,13 @@ __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __rest
             s_wc[w] = tot;
             tot += c;
         }
-        s_base = tot ? atomicAdd(list, tot) : 0u;
+        s_base = tot ? atomicAdd(count, tot) : 0u;
+        // the other slot was consumed by the previous view's chain (stream order): zero it for the
+        // next view, so no memset precedes this kernel
+        if (blockIdx.x == 0) *count_next = 0u;
     }
     __syncthreads();
-    if (touched) list[1 + s_base + s_wc[warp] + __popc(m & lanemask_lt())] = (uint32_t)i;
+    if (touched) list[s_base + s_wc[warp] + __popc(m & lanemask_lt())] = (uint32_t)i;
     if (!zero_untouched) return;  // accumulating, or the rows are already zero
     // Every gradient of the warp's 32 Gaussians is zeroed here (touched ones are overwritten by
     // pass 2): each array's span for the warp is contiguous, so the warp writes it with float4
@@ -435,11 +439,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_touched_kernel(GaussianPt
                                                                      float4* __restrict__ grad2d,
                                                                      const ProjRec* __restrict__ rec,
                                                                      splat_param_grads out, int accumulate,
-                                                                     const uint32_t* __restrict__ list) {
+                                                                     const uint32_t* __restrict__ list,
+                                                                     const uint32_t* __restrict__ count) {
     __shared__ float4 s_sh[kChainThreads * kShRow];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int)list[0]) return;
-    const int i = (int)list[1 + t];
+    if (t >= (int)*count) return;
+    const int i = (int)list[t];
     const int row = threadIdx.x;
     const float4* src = reinterpret_cast<const float4*>(g.sh + 48 * (size_t)i);
 #pragma unroll
@@ -475,18 +480,21 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
         lc.count++;
         return cudaGetLastError();
     }
-    cudaError_t e = cudaMemsetAsync(list, 0, 4, lc.stream);
-    if (e != cudaSuccess) return e;
+    // touched-list length: two slots (work_counters[4 + parity]) used alternately, each zeroed by the
+    // compact kernel of the call before its next use (zero at rest initially)
+    uint32_t* count = reinterpret_cast<uint32_t*>(lc.work_counters + 4 + lc.chain_parity);
+    uint32_t* count_next = reinterpret_cast<uint32_t*>(lc.work_counters + 5 - lc.chain_parity);
+    lc.chain_parity ^= 1;
     {
         LaunchScope ls(lc, "chain_compact");
-        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out,
-                                                                          !accumulate && !prezeroed, list);
+        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out, !accumulate && !prezeroed,
+                                                                          list, count, count_next);
         lc.count++;
     }
     if (n_surv > 0) {
         LaunchScope ls(lc, "chain");
         chain_touched_kernel<<<blocks_for(n_surv, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, g2, rec, out,
-                                                                                               accumulate, list);
+                                                                                               accumulate, list, count);
         lc.count++;
     }
     return cudaGetLastError();

@@ -339,6 +339,18 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
     }
 }
 
+// [survivors, Ps, P] straight to the host's mapped pinned memory, and the device counters back to
+// zero for the next view: a one-warp kernel instead of a memset + a copy-engine transfer (a bulk
+// H2D in flight queues copy-engine work behind it).
+__global__ void publish_counts_kernel(uint32_t* __restrict__ n_surv, uint32_t* host_counts) {
+    if (threadIdx.x < 3) {
+        const uint32_t c = n_surv[threadIdx.x];
+        n_surv[threadIdx.x] = 0u;
+        reinterpret_cast<volatile uint32_t*>(host_counts)[threadIdx.x] = c;
+    }
+    __threadfence_system();
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -633,7 +645,7 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp
     __shared__ int s_bid;
     for (;;) {
         __syncthreads();  // the previous block's shared-memory reads are done
-        if (threadIdx.x == 0) s_bid = atomicAdd(counter, 1);
+        if (threadIdx.x == 0) s_bid = pull_work(counter, nblocks);
         __syncthreads();
         const int b = s_bid;
         if (b >= nblocks) break;
@@ -691,7 +703,8 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
-                              uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref) {
+                              uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref,
+                              uint32_t* host_counts) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
@@ -707,6 +720,10 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                                                                               tile_counts, n_survivors_dev, depth_out, rect_ref);
         }
     lc.count++;
+    if (host_counts) {
+        publish_counts_kernel<<<1, 32, 0, lc.stream>>>(n_survivors_dev, host_counts);
+        lc.count++;
+    }
     return cudaGetLastError();
 }
 
@@ -723,7 +740,6 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
             if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_forward_persistent<R, T, W, H, A>, \
                                                                       W * H, 0);                                 \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                             \
-            cudaMemsetAsync(lc.work_counters, 0, 4, lc.stream);                                                  \
             blend_forward_persistent<R, T, W, H, A><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(            \
                 cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters);       \
         } else {                                                                                                 \

@@ -21,7 +21,9 @@ struct LaunchCtx {
     cudaStream_t stream = nullptr;
     int64_t count = 0;  // kernels launched (bench accounting)
     int num_sms = 148;
-    int* work_counters = nullptr;  // device ints for persistent-CTA work queues ([0] fwd, [1] bwd)
+    int* work_counters = nullptr;  // device ints, zero at rest: [0] fwd / [1] bwd work queues (+8: exit
+                                   // counts), [4 + p] chain touched-list lengths
+    int chain_parity = 0;
     bool persistent_blend = true;  // blend kernels as persistent CTAs pulling pixel blocks
     bool bwd_px2 = true;           // 8 x 8 backward: one warp, two pixels per thread
     ProfileState* prof = nullptr;  // non-null while per-kernel CUDA-event timing is on
@@ -42,6 +44,9 @@ size_t scan_temp_words(uint64_t n);
 size_t radix_hist_words(uint64_t n, int bits);
 cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n,
                                uint32_t* tmp, uint32_t* total_dev);
+// Same, with a dedicated tmp that is zero at rest (allocated zeroed; the kernel re-zeroes it):
+// no memset launch before the scan.
+cudaError_t exclusive_scan_u32_zeroed(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tmp);
 // out[i] = sum_{r < i} in[idx[r]] (gather fused into the single-pass scan)
 cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const uint32_t* idx, uint32_t* out,
                                       uint64_t n, uint32_t* tmp, uint32_t* total_dev);
@@ -73,7 +78,7 @@ struct GaussianPtrs {
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
-                              float* depth_out, uint2* rect_ref);
+                              float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 struct BinningArgs {
@@ -86,6 +91,7 @@ struct BinningArgs {
     uint32_t* st_key[2];    // fallback path only
     uint32_t* st_gauss[2];  // [0]: supertile lists (chunked path); both: sort ping-pong (fallback)
     uint32_t* st_cnt;       // [st_chunk_words] chunked path: (supertile, chunk) counts / offsets
+    uint32_t* st_scan_tmp;  // [scan_temp_words] zero at rest, for the st_cnt scan only
     uint32_t* st_ranges;   // [2 * n_st]
     uint16_t* st_cover;     // [st_pairs] tile cover (16 bits) of each supertile list entry
     uint32_t* l2_tmp;      // [bin_l2_words] level-2 piece map and per-piece tile counts

@@ -92,8 +92,10 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
 }
 
 // ---- single-pass scan -------------------------------------------------------------------------
-// tmp layout (u64 words): [0] tile counter, [1 + t] look-back word of tile t.
-template <bool GATHER>
+// tmp layout (u64 words): [0] tile counter, [1 + t] look-back word of tile t, [1 + ntiles] done
+// count.  RESET: tmp is zero at rest (no memset before the launch): the last tile to finish its
+// look-back re-zeroes the counter, the look-back words and the done count.
+template <bool GATHER, bool RESET = false>
 __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t* __restrict__ in,
                                                                 const uint32_t* __restrict__ idx,
                                                                 uint32_t* __restrict__ out, uint64_t n,
@@ -146,10 +148,21 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
             }
             if (lane == 0) st_relaxed64(&status[tile], kFlagInc | (prefix + agg));
         }
+        const uint64_t ntiles = (n + kTile - 1) / kTile;
         if (lane == 0) {
             s_prefix = prefix;
-            const uint64_t ntiles = (n + kTile - 1) / kTile;
             if (total_out && tile == ntiles - 1) *total_out = (uint32_t)(prefix + agg);
+        }
+        if (RESET) {
+            unsigned long long last = 0;
+            if (lane == 0) {
+                __threadfence();
+                last = atomicAdd(reinterpret_cast<unsigned long long*>(status + ntiles), 1ull) == ntiles - 1;
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {  // every tile is past its look-back
+                __threadfence();
+                for (uint64_t q = lane; q < ntiles + 2; q += 32) tmp[q] = 0ull;
+            }
         }
     }
     __syncthreads();
@@ -509,6 +522,9 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                 v1[i] = v[r];
             }
         }
+        grid.sync();  // every CTA has read hist
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i < 4 * 256; i += kThreads) hist[i] = 0u;  // zero at rest
         return;
     }
     int src = 0;
@@ -637,6 +653,10 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
         grid.sync();
         STAMP(8 + 6 * j);
     }
+    // hist was last read before the first pass's first grid barrier: re-zero it for the next sort
+    // (the caller allocates it zeroed; no memset launch per sort)
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 4 * 256; i += kThreads) hist[i] = 0u;
 #ifdef SPLAT_SORT_STAMPS
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ns = 3 + 6 * m;
@@ -663,6 +683,16 @@ size_t radix_hist_words(uint64_t n, int bits) {
 cudaError_t exclusive_scan_u32(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tmp,
                                uint32_t* total_dev) {
     return exclusive_scan_gather_u32(lc, in, nullptr, out, n, tmp, total_dev);
+}
+
+cudaError_t exclusive_scan_u32_zeroed(LaunchCtx& lc, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tmp) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t nt = (n + kTile - 1) / kTile;
+    LaunchScope s(lc, "scan");
+    scan_lookback_kernel<false, true><<<(unsigned)nt, kThreads, 0, lc.stream>>>(
+        in, nullptr, out, n, reinterpret_cast<uint64_t*>(tmp), nullptr);
+    lc.count++;
+    return cudaGetLastError();
 }
 
 cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const uint32_t* idx, uint32_t* out,
@@ -747,9 +777,8 @@ cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint3
     }
     const uint64_t nt = (n + kCoopTile - 1) / kCoopTile;
     if (nt > (uint64_t)lc.num_sms * per_sm || n >= (1ull << 31)) return cudaErrorCooperativeLaunchTooLarge;
-    cudaError_t e = cudaMemsetAsync(work, 0, 4 * 256 * 4, lc.stream);
-    if (e != cudaSuccess) return e;
-    uint32_t* hist = work;
+    cudaError_t e;
+    uint32_t* hist = work;  // zero at rest: allocated zeroed, re-zeroed by the kernel
     uint32_t* counts = work + 4 * 256;
     uint32_t nn = (uint32_t)n;
     void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts};

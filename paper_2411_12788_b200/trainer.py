@@ -87,8 +87,12 @@ class ViewTrainer:
         cam_arr = (Camera * v)(*cams)
         tp = (C.c_void_p * v)(*ptrs)
         t = C.c_int32(self.opt.t)
+        key = (self.params.centers.data_ptr(), self.params.sh.data_ptr(), self.params.n, self.params.active_sh_degree,
+               self.opt.m.data_ptr())
+        if key != getattr(self, "_ckey", None):  # ctypes views of the parameter / moment buffers
+            self._ckey, self._pm, self._mo = key, self.params.mut(), self.opt._moments()
         self.ctx.check(lib.splat_train_step(
-            h, C.byref(self.params.mut()), C.byref(self._gr), C.byref(self.opt._moments()), C.byref(self.opt.config),
+            h, C.byref(self._pm), C.byref(self._gr), C.byref(self._mo), C.byref(self.opt.config),
             C.byref(t), group_mask, cam_arr, v, tp, 1 if on_host else 0, C.byref(self.cfg), self.bg,
             self.lambda_dssim, self.loss.data_ptr(), loss_host))
         if group_mask:

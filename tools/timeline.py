@@ -43,6 +43,13 @@ def main(steps: int = 3, warmup: int = 5, host: bool = False):
     prof.export_chrome_trace(str(path))
     ev = json.load(open(path))["traceEvents"]
     ks = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda e: e["ts"])
+    if "--api" in sys.argv:  # host-side runtime calls between the last two preprocess launches
+        api = sorted([e for e in ev if e.get("cat") == "cuda_runtime"], key=lambda e: e["ts"])
+        pre = [e for e in api if "Launch" in e["name"] or "Memcpy" in e["name"] or "Memset" in e["name"]
+               or "Synchronize" in e["name"] or "Event" in e["name"]]
+        t0 = pre[len(pre) // 2]["ts"] if pre else 0
+        for e in pre[len(pre) // 2: len(pre) // 2 + 60]:
+            print(f"API {e['ts'] - t0:9.1f} {e['dur']:8.1f}  {e['name']}")
     # split into steps at the preprocess kernel
     cur, all_steps = [], []
     for e in ks:
@@ -58,7 +65,8 @@ def main(steps: int = 3, warmup: int = 5, host: bool = False):
         print(f"--- step {si}: {len(st)} records")
         for e in st:
             gap = e["ts"] - end
-            nm = e["name"].split("(")[0].replace("void ", "")[-40:]
+            nm = e["name"].replace("void ", "").replace("splat_b200::", "").replace("(anonymous namespace)::", "")
+            nm = nm.split("(")[0][:40]
             print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} gap {gap:7.1f}  s{e.get('args', {}).get('stream', '?')}  {nm}")
             end = max(end, e["ts"] + e["dur"])
             busy += e["dur"]
