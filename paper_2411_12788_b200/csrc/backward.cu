@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ param, co
                                                    float* __restrict__ m, float* __restrict__ v, int64_t count,
                                                    double lr, double lr_alt, double b1, double omb1, double b2,
                                                    double omb2, double eps, double bias1, double bias2) {
+    pdl_wait();
     const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i0 >= count) return;
     const int r0 = SH ? (int)(i0 % 48) : 0;
@@ -706,8 +707,8 @@ cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, dou
                            reinterpret_cast<uintptr_t>(a.m) | reinterpret_cast<uintptr_t>(a.v)) & 15u) == 0;
         const unsigned grid = blocks_for((a.count + 3) / 4, 256);
 #define ADAM_LAUNCH(SH, VEC)                                                                                      \
-    adam_kernel<SH, VEC><<<grid, 256, 0, lc.stream>>>(a.param, a.grad, a.m, a.v, a.count, a.lr, a.lr_alt, beta1,  \
-                                                     1.0 - beta1, beta2, 1.0 - beta2, eps, bias1, bias2)
+    launch_pdl(lc.stream, adam_kernel<SH, VEC>, dim3(grid), dim3(256), 0, a.param, a.grad, a.m, a.v, a.count, a.lr,  \
+               a.lr_alt, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps, bias1, bias2)
         if (a.sh_layout) {
             if (vec) ADAM_LAUNCH(true, true);
             else ADAM_LAUNCH(true, false);

@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(EMIT ? 32 : 32 * kStWarps) st_chunk_kernel(con
     // count: kStWarps warps per CTA chunk, s_mem = [kStWarps][n_st] per-warp counts;
     // emit: one warp per CTA (warp `warp` of chunk c), s_mem = [n_st] running offsets
     extern __shared__ uint32_t s_mem[];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int c = EMIT ? blockIdx.x / kStWarps : blockIdx.x;
     const int warp = EMIT ? blockIdx.x % kStWarps : threadIdx.x >> 5;
@@ -267,6 +269,8 @@ __device__ __forceinline__ uint32_t st_lo(const uint32_t* __restrict__ st_cnt, i
 __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges,
                                int n_st, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ piece_st,
                                uint32_t* __restrict__ ranges) {
+    pdl_wait();
+    pdl_trigger();
     const int st = blockIdx.x * blockDim.x + threadIdx.x;
     if (st >= n_st) return;
     const uint32_t lo = st_lo(st_cnt, nchunks, st_ranges, n_st, st);
@@ -320,6 +324,8 @@ __global__ void __launch_bounds__(kL2Threads) bin_count_kernel(const uint32_t* _
                                                               const uint16_t* __restrict__ st_cover,
                                                               uint32_t* __restrict__ piece_cnt) {
     __shared__ uint32_t s_cnt[kSTT];
+    pdl_wait();
+    pdl_trigger();
     PieceInfo pi;
     if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -357,6 +363,8 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     constexpr int kW = kL2Threads / 32;
     __shared__ uint32_t s_c[kPieceK][kW][kSTT];    // (slice k, warp) entries covering tile f, then their list position
     __shared__ uint32_t s_prefix[kSTT];
+    pdl_wait();
+    pdl_trigger();
     PieceInfo pi;
     if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -478,17 +486,20 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
             cudaFuncSetAttribute(st_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_emit);
         {
             LaunchScope s(lc, "st_count");
-            st_chunk_kernel<false><<<nchunks, 32 * kStWarps, smem_count, lc.stream>>>(
-                a.order, a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, nullptr, nullptr);
+            e = launch_pdl(lc.stream, st_chunk_kernel<false>, dim3(nchunks), dim3(32 * kStWarps), smem_count, a.order,
+                           a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, (uint32_t*)nullptr,
+                           (uint16_t*)nullptr);
+            if (e != cudaSuccess) return e;
             lc.count++;
         }
         e = exclusive_scan_u32_zeroed(lc, a.st_cnt, a.st_cnt, (uint64_t)n_st * nchunks + 1, a.st_scan_tmp);
         if (e != cudaSuccess) return e;
         {
             LaunchScope s(lc, "st_emit");
-            st_chunk_kernel<true><<<nchunks * kStWarps, 32, smem_emit, lc.stream>>>(
-                a.order, a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
-                a.st_cover);
+            e = launch_pdl(lc.stream, st_chunk_kernel<true>, dim3(nchunks * kStWarps), dim3(32), smem_emit, a.order,
+                           a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
+                           a.st_cover);
+            if (e != cudaSuccess) return e;
             lc.count++;
         }
         gauss = a.st_gauss[0];
@@ -526,21 +537,25 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
         uint32_t* piece_cnt = a.l2_tmp + np;
         {
             LaunchScope s(lc, "bin_map");
-            bin_map_kernel<<<blocks_for(n_st, 128), 128, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, a.tiles_x,
-                                                                         a.tiles_y, a.st_x, piece_st, a.ranges);
+            e = launch_pdl(lc.stream, bin_map_kernel, dim3(blocks_for(n_st, 128)), dim3(128), 0, cnt, nch,
+                           (const uint32_t*)a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, piece_st, a.ranges);
+            if (e != cudaSuccess) return e;
             lc.count++;
         }
         if (np > 0) {
             {
                 LaunchScope s(lc, "bin_count");
-                bin_count_kernel<<<np, kL2Threads, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, piece_st, a.st_cover,
-                                                                   piece_cnt);
+                e = launch_pdl(lc.stream, bin_count_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
+                               (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)piece_st,
+                               (const uint16_t*)a.st_cover, piece_cnt);
+                if (e != cudaSuccess) return e;
                 lc.count++;
             }
             LaunchScope s(lc, "bin_emit");
-            bin_emit_kernel<<<np, kL2Threads, 0, lc.stream>>>(cnt, nch, a.st_ranges, n_st, piece_st, piece_cnt, gauss,
-                                                              a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss,
-                                                              a.ranges);
+            e = launch_pdl(lc.stream, bin_emit_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
+                           (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)piece_st, (const uint32_t*)piece_cnt,
+                           gauss, (const uint16_t*)a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss, a.ranges);
+            if (e != cudaSuccess) return e;
             lc.count++;
         }
     }

@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __rest
     // appends would serialise ~n/32 of them
     __shared__ uint32_t s_wc[8];
     __shared__ uint32_t s_base;
+    pdl_trigger();  // chain_touched (PDL) may be scheduled
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool touched = i < n && grad2d[kG2Stride * (size_t)i + 2].w > 0.0f;
@@ -442,6 +443,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_touched_kernel(GaussianPt
                                                                      const uint32_t* __restrict__ list,
                                                                      const uint32_t* __restrict__ count) {
     __shared__ float4 s_sh[kChainThreads * kShRow];
+    pdl_wait();
+    pdl_trigger();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int)*count) return;
     const int i = (int)list[t];
@@ -493,8 +496,10 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
     }
     if (n_surv > 0) {
         LaunchScope ls(lc, "chain");
-        chain_touched_kernel<<<blocks_for(n_surv, kChainThreads), kChainThreads, 0, lc.stream>>>(g, cp, g2, rec, out,
-                                                                                               accumulate, list, count);
+        const cudaError_t e = launch_pdl(lc.stream, chain_touched_kernel, dim3(blocks_for(n_surv, kChainThreads)),
+                                         dim3(kChainThreads), 0, g, cp, g2, rec, out, accumulate,
+                                         (const uint32_t*)list, (const uint32_t*)count);
+        if (e != cudaSuccess) return e;
         lc.count++;
     }
     return cudaGetLastError();

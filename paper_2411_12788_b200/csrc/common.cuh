@@ -56,6 +56,14 @@ struct CamParams {
     float log_cond_limit;  // float(log(1e12))
 };
 
+// Programmatic dependent launch (PDL): kernels launched with launch_pdl (internal.h) may start
+// while their predecessor in the stream finishes; pdl_wait() blocks until the predecessor grid has
+// completed and its memory is visible (a no-op for a normal launch), and pdl_trigger() lets the
+// successor's CTAs be scheduled once every CTA of this grid has issued it.  Every PDL-launched
+// kernel waits before touching global memory.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Work queue of the persistent blend kernels (one thread per CTA calls it): returns the next pixel
 // block.  The last CTA to run dry re-zeroes the queue and its exit count (counter[8]), so the
 // counter is zero at rest and no memset precedes a launch.

@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                                                         uint32_t* __restrict__ n_surv, float* __restrict__ depth_out,
                                                         uint2* __restrict__ rect_ref) {
     __shared__ float4 s_sh[VEC_SH ? kPreThreads * kShRow : 1];
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (VEC_SH) {
         // the block's SH rows stream into shared memory (cp.async, coalesced) while the geometry
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
 // zero for the next view: a one-warp kernel instead of a memset + a copy-engine transfer (a bulk
 // H2D in flight queues copy-engine work behind it).
 __global__ void publish_counts_kernel(uint32_t* __restrict__ n_surv, uint32_t* host_counts) {
+    pdl_wait();
     if (threadIdx.x < 3) {
         const uint32_t c = n_surv[threadIdx.x];
         n_surv[threadIdx.x] = 0u;
@@ -643,6 +646,7 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
                                                            float bg2, FwdOutputs out, int nblocks, int* __restrict__ counter) {
     __shared__ int s_bid;
+    pdl_wait();
     for (;;) {
         __syncthreads();  // the previous block's shared-memory reads are done
         if (threadIdx.x == 0) s_bid = pull_work(counter, nblocks);
@@ -721,7 +725,9 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
         }
     lc.count++;
     if (host_counts) {
-        publish_counts_kernel<<<1, 32, 0, lc.stream>>>(n_survivors_dev, host_counts);
+        const cudaError_t e = launch_pdl(lc.stream, publish_counts_kernel, dim3(1), dim3(32), 0, n_survivors_dev,
+                                         host_counts);
+        if (e != cudaSuccess) return e;
         lc.count++;
     }
     return cudaGetLastError();
@@ -740,8 +746,8 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
             if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_forward_persistent<R, T, W, H, A>, \
                                                                       W * H, 0);                                 \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                             \
-            blend_forward_persistent<R, T, W, H, A><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(            \
-                cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters);       \
+            launch_pdl(lc.stream, blend_forward_persistent<R, T, W, H, A>, dim3(pg < grid ? pg : grid), dim3(W * H), \
+                       0, cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters); \
         } else {                                                                                                 \
             blend_forward_kernel<R, T, W, H, A><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, \
                                                                               bg[0], bg[1], bg[2], out);         \

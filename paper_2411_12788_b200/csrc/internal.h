@@ -32,6 +32,22 @@ struct LaunchCtx {
     void prof_end();
 };
 
+// Launch with programmatic stream serialisation (the kernel must call pdl_wait() first).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(cudaStream_t s, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // RAII bracket: LaunchScope s(lc, "name"); kernel<<<...>>>;
 struct LaunchScope {
     LaunchCtx& lc;

@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
     __shared__ uint32_t s_data[kTile];
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint64_t s_tile, s_prefix;
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned long long*>(tmp), 1ull);
     __syncthreads();
     const uint64_t tile = s_tile;
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                                                                  uint32_t n, uint32_t* __restrict__ hist,
                                                                  uint32_t* __restrict__ counts) {
     cg::grid_group grid = cg::this_grid();
+    pdl_trigger();  // st_count (PDL) may be scheduled on the SM slots left free
 #ifdef SPLAT_SORT_STAMPS
     unsigned long long stamps[32];
     int ns = 0;
@@ -689,10 +692,11 @@ cudaError_t exclusive_scan_u32_zeroed(LaunchCtx& lc, const uint32_t* in, uint32_
     if (n == 0) return cudaSuccess;
     const uint64_t nt = (n + kTile - 1) / kTile;
     LaunchScope s(lc, "scan");
-    scan_lookback_kernel<false, true><<<(unsigned)nt, kThreads, 0, lc.stream>>>(
-        in, nullptr, out, n, reinterpret_cast<uint64_t*>(tmp), nullptr);
+    const cudaError_t e = launch_pdl(lc.stream, scan_lookback_kernel<false, true>, dim3((unsigned)nt), dim3(kThreads), 0,
+                                     in, (const uint32_t*)nullptr, out, n, reinterpret_cast<uint64_t*>(tmp),
+                                     (uint32_t*)nullptr);
     lc.count++;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const uint32_t* idx, uint32_t* out,
