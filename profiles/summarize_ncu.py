@@ -36,6 +36,7 @@ NAME_MAP = [  # (regex on the demangled ncu kernel name, bench launch name)
     (r"scan_lookback_kernel", "scan"),
     (r"seg_setup_kernel", "seg_setup"),
     (r"loss_reduce_kernel", "loss_reduce"),
+    (r"publish_counts_kernel", "publish_counts"),
     (r"st_ranges_from_chunks_kernel", "st_ranges"),
     (r"ranges_from_slots_kernel", "tile_ranges"),
     (r"quat_normalize_kernel", "quat_normalize"),
