@@ -411,8 +411,27 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                                   g_b, cl_b, dxb, dyb);
                 anyc_a |= ga;
                 anyc_b |= gb;
+#ifdef SPLAT_STATS
+                {  // [0] half-entries evaluated, [1] of which with a commit, [2] eligible lanes, [3] commits
+                    const unsigned ca = __ballot_sync(0xffffffffu, ga), cb = __ballot_sync(0xffffffffu, gb);
+                    const unsigned ea = __ballot_sync(0xffffffffu, wa && idx_a <= q.last);
+                    const unsigned eb = __ballot_sync(0xffffffffu, wb && idx_b <= q.last);
+                    if (lane == 0) {
+                        atomicAdd(&g_bstats[0], (unsigned long long)(wa + wb));
+                        atomicAdd(&g_bstats[1], (unsigned long long)((ca != 0) + (cb != 0)));
+                        atomicAdd(&g_bstats[2], (unsigned long long)(__popc(ea) + __popc(eb)));
+                        atomicAdd(&g_bstats[3], (unsigned long long)(__popc(ca) + __popc(cb)));
+                    }
+                }
+#endif
             }
             const bool any_a = __any_sync(0xffffffffu, anyc_a), any_b = __any_sync(0xffffffffu, anyc_b);
+#ifdef SPLAT_STATS
+            if (lane == 0) {
+                atomicAdd(&g_bstats[4], 1ull);
+                atomicAdd(&g_bstats[5], (unsigned long long)(any_a + any_b));
+            }
+#endif
             if (any_a || any_b) emit_entry_grads(v, lane, any_a, any_b, (uint32_t)j, jb, a_gid, grad2d);
         }
     }

@@ -175,11 +175,15 @@ __device__ __forceinline__ bool quad_box_reaches(const float4& r0, float c, floa
         // q minus a rounding bound proportional to the magnitudes of its terms: the per-pixel
         // gate evaluates the same quadratic in another order, and for elongated Gaussians the
         // terms cancel (|terms| >> q), so the cull must not trust q beyond ~1e-5 of sum |terms|.
+        // Explicit FMAs and approximate reciprocals (forward.cu is compiled --fmad=false for the
+        // gates): the cull only needs q to ~1e-6 relative, far inside its 1e-5 bound and the
+        // 1e-3 margin in cut, and an approximate vertex moves q by O(error^2) at the minimum.
         auto q_lo = [&](float dx, float dy) {
-            const float t0 = a * dx * dx, t1 = 2.0f * b * dx * dy, t2 = c * dy * dy;
-            return (t0 + t1 + t2) - 1e-5f * (t0 + fabsf(t1) + t2);
+            const float t0 = __fmul_rn(__fmul_rn(a, dx), dx), t1 = __fmul_rn(__fmul_rn(2.0f * b, dx), dy);
+            const float t2 = __fmul_rn(__fmul_rn(c, dy), dy);
+            return __fmaf_rn(-1e-5f, t0 + fabsf(t1) + t2, t0 + t1 + t2);
         };
-        const float ia = 1.0f / a, ic = 1.0f / c;
+        const float ia = __fdividef(1.0f, a), ic = __fdividef(1.0f, c);
         const float y_at_xl = fminf(fmaxf(-b * dxl * ic, dyl), dyh);
         const float y_at_xh = fminf(fmaxf(-b * dxh * ic, dyl), dyh);
         const float x_at_yl = fminf(fmaxf(-b * dyl * ia, dxl), dxh);

@@ -809,8 +809,9 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
 // Instrumented builds: copy (and with reset != 0, zero) the forward traversal counters.
 extern "C" int splat_debug_stats(unsigned long long* out, int reset) {
 #ifdef SPLAT_STATS
-    cudaDeviceSynchronize();
-    if (cudaMemcpyFromSymbol(out, splat_b200::g_stats, sizeof(unsigned long long) * 12) != cudaSuccess) return 3;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out, splat_b200::g_stats, sizeof(unsigned long long) * 12);
+    if (e != cudaSuccess) return 100 + (int)e;
     if (reset) {
         unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(splat_b200::g_stats, z, sizeof(z));

@@ -23,7 +23,8 @@ render(ds, cam, want_depth=False, ctx=ctx)
 buf = (C.c_ulonglong * 12)()
 lib = ctx.lib
 lib.splat_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-assert lib.splat_debug_stats(buf, 1) == 0, "not an instrumented build"
+rc0 = lib.splat_debug_stats(buf, 1)
+assert rc0 == 0, f"not an instrumented build (rc {rc0})"
 from paper_2411_12788_b200 import capi  # noqa: E402
 from paper_2411_12788_b200.rasterizer import render_backward  # noqa: E402
 lib.splat_debug_bstats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
@@ -37,8 +38,8 @@ render_backward(ds, cam, capi.RasterConfig(), d_color, ctx=ctx)
 torch.cuda.synchronize()
 lib.splat_debug_bstats(bbuf, 1)
 bv = list(bbuf)
-bnames = ["bwd warp-entries evaluated", "  with >=1 commit (reductions)", "  eligible lanes (idx <= last)",
-          "  committing lanes", "  pair iterations"]
+bnames = ["bwd half-entries evaluated", "  with >=1 commit", "  eligible lanes (idx <= last)",
+          "  committing lanes", "  pair iterations (past the skip test)", "  entries reduced"]
 for n, x in zip(bnames, bv):
     print(f"{n:45s} {x:,}")
 print(f"bwd eligible lanes per evaluation {bv[2] / max(bv[0], 1):.1f}, committing {bv[3] / max(bv[1], 1):.1f} per reduction")
