@@ -34,9 +34,10 @@ constexpr int kST = 4;              // supertile side in tiles
 constexpr int kSTT = kST * kST;     // tiles per supertile
 constexpr int kL2Threads = 512;     // level-2 CTA: one per piece of a supertile list
 constexpr int kStChunk = 128;       // depth-ordered survivors per warp of the supertile pass
-constexpr int kStWarps = 4;         // warps per supertile-pass CTA
+constexpr int kStWarps = 16;        // warps per supertile-count CTA (one count column per 2048 survivors)
+constexpr int kEmitWarps = 1;       // warps per supertile-emit CTA (1: 60 us, 4 independent warps: 67 us)
 constexpr int kStChunkCta = kStChunk * kStWarps;  // survivors per CTA chunk (one count column)
-constexpr int kStMaxSmem = 6144;    // supertiles the chunked pass keeps in shared memory
+constexpr int kStMaxSmem = 3328;    // supertiles the chunked pass keeps in shared memory (x kStWarps rows)
 
 struct TileRect {
     int tx0, tx1, ty0, ty1;  // inclusive tile range of a Gaussian's pixel rect
@@ -110,36 +111,36 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 // time, into (Gaussian, supertile) entries in (depth, raster) order; every window of 32 entries is
 // ranked per supertile with __match_any_sync, and a per-(warp, supertile) running count in shared
 // memory carries the rank across windows.
-//   EMIT = false: each warp counts its entries per supertile; wcnt[(c kStWarps + warp) n_st + st]
-//                 gets the warp's counts (coalesced rows) and cnt[st nchunks + c] the CTA's.
+//   EMIT = false: each warp counts its entries per supertile; wpre[(c kStWarps + warp) n_st + st]
+//                 gets the warp's exclusive prefix within the chunk (coalesced rows) and
+//                 cnt[st nchunks + c] the CTA's total.
 //   EMIT = true:  cnt holds the exclusive scan of the CTA counts (supertile-major); launched with
-//                 one warp per CTA (1-warp CTAs: 32 resident per SM, measured faster than
-//                 kStWarps-warp CTAs), whose base for st is cnt[st nchunks + c] plus the earlier
-//                 warps' wcnt rows; it writes st_gauss[base + rank].
+//                 kEmitWarps independent warps per CTA (one: more resident warps per SM were
+//                 measured slower — the shuffle / shared-memory pipe, not latency, bounds it),
+//                 each with base cnt[st nchunks + c] plus its wpre row; it writes
+//                 st_gauss[base + rank].
 template <bool EMIT>
-__global__ void __launch_bounds__(EMIT ? 32 : 32 * kStWarps) st_chunk_kernel(const uint32_t* __restrict__ order,
+__global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chunk_kernel(const uint32_t* __restrict__ order,
                                                                  const uint2* __restrict__ rect_ref, int n_surv,
                                                                  int ts, int ts_shift, int st_x, int n_st, int nchunks,
                                                                  uint32_t* __restrict__ cnt,
                                                                  uint32_t* __restrict__ st_gauss,
                                                                  uint16_t* __restrict__ st_cover) {
     // count: kStWarps warps per CTA chunk, s_mem = [kStWarps][n_st] per-warp counts;
-    // emit: one warp per CTA (warp `warp` of chunk c), s_mem = [n_st] running offsets
+    // emit: kEmitWarps independent warps per CTA (global warp gw = warp `warp` of chunk c), each
+    // with its own [n_st] running offsets in s_mem; no CTA barrier
     extern __shared__ uint32_t s_mem[];
     pdl_wait();
     pdl_trigger();
     const int lane = threadIdx.x & 31;
-    const int c = EMIT ? blockIdx.x / kStWarps : blockIdx.x;
-    const int warp = EMIT ? blockIdx.x % kStWarps : threadIdx.x >> 5;
-    uint32_t* s_run = EMIT ? s_mem : s_mem + (size_t)warp * n_st;
-    uint32_t* wcnt = cnt + (size_t)n_st * nchunks + 1;
+    const int gw = blockIdx.x * kEmitWarps + (threadIdx.x >> 5);
+    const int c = EMIT ? gw / kStWarps : blockIdx.x;
+    const int warp = EMIT ? gw % kStWarps : threadIdx.x >> 5;
+    uint32_t* s_run = s_mem + (size_t)(threadIdx.x >> 5) * n_st;
+    uint32_t* wcnt = cnt + (size_t)n_st * nchunks + 1;  // per-warp prefix rows
     if (EMIT) {
-        const uint32_t* wrow = wcnt + (size_t)c * kStWarps * n_st;
-        for (int st = lane; st < n_st; st += 32) {
-            uint32_t b = cnt[(size_t)st * nchunks + c];
-            for (int ww = 0; ww < warp; ++ww) b += wrow[(size_t)ww * n_st + st];
-            s_run[st] = b;
-        }
+        const uint32_t* wpre = wcnt + ((size_t)c * kStWarps + warp) * n_st;
+        for (int st = lane; st < n_st; st += 32) s_run[st] = cnt[(size_t)st * nchunks + c] + wpre[st];
     } else {
         for (int st = lane; st < n_st; st += 32) s_run[st] = 0u;
         if (c == 0 && threadIdx.x == 0) cnt[(size_t)n_st * nchunks] = 0u;  // scan slot of the total
@@ -229,14 +230,18 @@ __global__ void __launch_bounds__(EMIT ? 32 : 32 * kStWarps) st_chunk_kernel(con
         }
     }
     if (!EMIT) {
-        __syncwarp();
-        uint32_t* wrow = wcnt + ((size_t)c * kStWarps + warp) * n_st;
-        for (int st = lane; st < n_st; st += 32) wrow[st] = s_run[st];
+        // per supertile: the CTA total (scanned later) and each warp's exclusive prefix within the
+        // chunk (coalesced rows: the emit warp then reads one row)
         __syncthreads();
+        uint32_t* wpre = wcnt + (size_t)c * kStWarps * n_st;
         for (int st = threadIdx.x; st < n_st; st += blockDim.x) {
             uint32_t t = 0;
 #pragma unroll
-            for (int ww = 0; ww < kStWarps; ++ww) t += s_mem[(size_t)ww * n_st + st];
+            for (int ww = 0; ww < kStWarps; ++ww) {
+                const uint32_t x = s_mem[(size_t)ww * n_st + st];
+                wpre[(size_t)ww * n_st + st] = t;
+                t += x;
+            }
             cnt[(size_t)st * nchunks + c] = t;
         }
     }
@@ -479,7 +484,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     }
     if (st_chunked(n_st)) {
         const int nchunks = st_chunks(a.n_surv);
-        const size_t smem_count = (size_t)n_st * 4 * kStWarps, smem_emit = (size_t)n_st * 4;
+        const size_t smem_count = (size_t)n_st * 4 * kStWarps, smem_emit = (size_t)n_st * 4 * kEmitWarps;
         if (smem_count > 48 * 1024)
             cudaFuncSetAttribute(st_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count);
         if (smem_emit > 48 * 1024)
@@ -496,7 +501,8 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
         if (e != cudaSuccess) return e;
         {
             LaunchScope s(lc, "st_emit");
-            e = launch_pdl(lc.stream, st_chunk_kernel<true>, dim3(nchunks * kStWarps), dim3(32), smem_emit, a.order,
+            e = launch_pdl(lc.stream, st_chunk_kernel<true>, dim3(nchunks * (kStWarps / kEmitWarps)), dim3(32 * kEmitWarps),
+                           smem_emit, a.order,
                            a.rect_ref, a.n_surv, ts, ts_shift, a.st_x, n_st, nchunks, a.st_cnt, a.st_gauss[0],
                            a.st_cover);
             if (e != cudaSuccess) return e;

@@ -456,13 +456,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define STAMP(i)
 #endif
 constexpr int kCoopItems = 16;
-constexpr int kCoopTile = kThreads * kCoopItems;  // 4096 (245 CTAs at N = 1 M: fewer to barrier)
+constexpr int kCoopTile = kThreads * kCoopItems;
+constexpr int kCoopMaxTpc = 6;  // tiles per CTA (up to 148 x 6 x 4096 = 3.6 M keys in one wave)
+constexpr size_t coop_dyn_smem(int tpc) { return (size_t)tpc * (2 * kCoopTile + 256) * 4; }  // 4096 (245 CTAs at N = 1 M: fewer to barrier)
 
+// Multi-tile form: CTA b owns tiles b, b + grid, ... (tpc of them); each tile's keys are held in
+// its own dynamic shared-memory slot between the rank phase and the scatter, so the three grid
+// barriers per pass are shared by all of the CTA's tiles.
+// TPC = 1: one tile per CTA, its slot in static shared memory; TPC = 0: `tpc` tiles per CTA in
+// dynamic shared memory.
+template <int TPC>
 __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __restrict__ k0, uint32_t* __restrict__ v0,
-                                                                 uint32_t* __restrict__ k1, uint32_t* __restrict__ v1,
-                                                                 uint32_t* __restrict__ k2, uint32_t* __restrict__ v2,
-                                                                 uint32_t n, uint32_t* __restrict__ hist,
-                                                                 uint32_t* __restrict__ counts) {
+                                                              uint32_t* __restrict__ k1, uint32_t* __restrict__ v1,
+                                                              uint32_t* __restrict__ k2, uint32_t* __restrict__ v2,
+                                                              uint32_t n, uint32_t* __restrict__ hist,
+                                                              uint32_t* __restrict__ counts, int tpc_rt) {
+    const int tpc = TPC > 0 ? TPC : tpc_rt;
     cg::grid_group grid = cg::this_grid();
     pdl_trigger();  // st_count (PDL) may be scheduled on the SM slots left free
 #ifdef SPLAT_SORT_STAMPS
@@ -475,29 +484,35 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     __shared__ uint32_t s_gh[4][256];
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint32_t s_delta[256];
-    // the tile's keys in local (digit, original position) order: the scatter then writes each
-    // digit's run of the tile to consecutive global positions (coalesced)
-    __shared__ uint32_t s_k[kCoopTile], s_v[kCoopTile];
-    const uint32_t tile = blockIdx.x, ntiles = gridDim.x;
+    // per owned tile: its keys / values in local (digit, original position) order (the scatter then
+    // writes each digit's run of the tile to consecutive global positions) and the local start of
+    // each digit
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    __shared__ __align__(16) uint32_t s_static[TPC == 1 ? 2 * kCoopTile + 256 : 1];
+    uint32_t* const s_slots = TPC == 1 ? s_static : s_dyn;
+    const uint32_t ntiles = (n + kCoopTile - 1) / kCoopTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
-    const uint32_t tbase = tile * kCoopTile;
-    const uint32_t tcount = n > tbase ? min(n - tbase, (uint32_t)kCoopTile) : 0u;
+    auto slot_k = [&](int q) { return s_slots + (size_t)q * (2 * kCoopTile + 256); };
+    auto slot_v = [&](int q) { return s_slots + (size_t)q * (2 * kCoopTile + 256) + kCoopTile; };
+    auto slot_ls = [&](int q) { return s_slots + (size_t)q * (2 * kCoopTile + 256) + 2 * kCoopTile; };
+    auto tile_of = [&](int q) { return blockIdx.x + (uint32_t)q * gridDim.x; };
     uint32_t k[kCoopItems], v[kCoopItems];
-#pragma unroll
-    for (int r = 0; r < kCoopItems; ++r) {
-        const uint32_t i = wbase + r * 32 + lane;
-        k[r] = i < n ? k0[i] : 0u;
-        v[r] = i < n ? v0[i] : 0u;
-    }
     // phase 0: digit histograms of all four bytes
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = 0u;
     __syncthreads();
+    // (owned tiles in reverse, so tile 0's keys stay in registers for the first pass)
+    for (int q = tpc - 1; q >= 0; --q) {
+        const uint32_t wbase = tile_of(q) * kCoopTile + warp * (kCoopTile / kWarps);
 #pragma unroll
-    for (int r = 0; r < kCoopItems; ++r)
-        if (wbase + r * 32 + lane < n)
+        for (int r = 0; r < kCoopItems; ++r) {
+            const uint32_t i = wbase + r * 32 + lane;
+            k[r] = i < n ? k0[i] : 0u;
+            if (q == 0) v[r] = i < n ? v0[i] : 0u;
+            if (i < n)
 #pragma unroll
-            for (int p = 0; p < 4; ++p) atomicAdd(&s_gh[p][(k[r] >> (8 * p)) & 255u], 1u);
+                for (int p = 0; p < 4; ++p) atomicAdd(&s_gh[p][(k[r] >> (8 * p)) & 255u], 1u);
+        }
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads)
         if ((&s_gh[0][0])[i]) atomicAdd(&hist[i], (&s_gh[0][0])[i]);
@@ -517,14 +532,12 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     uint32_t* kb[3] = {k0, k1, k2};
     uint32_t* vb[3] = {v0, v1, v2};
     if (m == 0) {  // nothing to reorder: copy to the result buffers
-#pragma unroll
-        for (int r = 0; r < kCoopItems; ++r) {
-            const uint32_t i = wbase + r * 32 + lane;
-            if (i < n) {
-                k1[i] = k[r];
-                v1[i] = v[r];
+        for (int q = 0; q < tpc; ++q)
+            for (uint32_t i = tile_of(q) * kCoopTile + threadIdx.x; i < min(n, (tile_of(q) + 1) * kCoopTile);
+                 i += kThreads) {
+                k1[i] = k0[i];
+                v1[i] = v0[i];
             }
-        }
         grid.sync();  // every CTA has read hist
         if (blockIdx.x == 0)
             for (int i = threadIdx.x; i < 4 * 256; i += kThreads) hist[i] = 0u;  // zero at rest
@@ -535,76 +548,85 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     for (int j = 0; j < m; ++j) {
         const int dst = ((m - 1 - j) & 1) ? 2 : 1;
         const int shift = 8 * passes[j];
-        if (j > 0) {
+        for (int q = 0; q < tpc; ++q) {
+            const uint32_t tile = tile_of(q);
+            if (tile >= ntiles) break;  // the last CTAs own one tile fewer (CTA-uniform)
+            const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
+            if (j > 0 || q > 0) {  // tile 0 of the first pass is still in registers
 #pragma unroll
-            for (int r = 0; r < kCoopItems; ++r) {
-                const uint32_t i = wbase + r * 32 + lane;
-                k[r] = i < n ? kb[src][i] : 0u;
-                v[r] = i < n ? vb[src][i] : 0u;
-            }
-        }
-        for (int i = threadIdx.x; i < kVW * 256 / 2; i += kThreads) reinterpret_cast<uint32_t*>(&s_cnt[0][0])[i] = 0u;
-        __syncthreads();
-        // Stable ranks per virtual warp: warp w's rows 0-7 are virtual warp 2w, rows 8-15 virtual
-        // warp 2w + 1 (key order), so each warp runs two independent counter chains.  Lanes with
-        // equal digits are found with 8 ballots (faster than __match_any_sync).
-        uint32_t rank[kCoopItems];
-#pragma unroll
-        for (int r = 0; r < kCoopItems / 2; ++r) {
-            unsigned peers[2];
-            uint32_t dd[2], old[2];
-            bool valid[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = r + h * (kCoopItems / 2);
-                valid[h] = wbase + rr * 32 + lane < n;
-                dd[h] = (k[rr] >> shift) & 255u;
-                unsigned pm = __ballot_sync(0xffffffffu, valid[h]);
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const bool bit = (dd[h] >> b) & 1u;
-                    const unsigned bal = __ballot_sync(0xffffffffu, bit);
-                    pm &= bit ? bal : ~bal;
+                for (int r = 0; r < kCoopItems; ++r) {
+                    const uint32_t i = wbase + r * 32 + lane;
+                    k[r] = i < n ? kb[src][i] : 0u;
+                    v[r] = i < n ? vb[src][i] : 0u;
                 }
-                peers[h] = pm;
-                old[h] = valid[h] ? s_cnt[2 * warp + h][dd[h]] : 0u;
             }
-            __syncwarp();
+            for (int i = threadIdx.x; i < kVW * 256 / 2; i += kThreads) reinterpret_cast<uint32_t*>(&s_cnt[0][0])[i] = 0u;
+            __syncthreads();
+            // Stable ranks per virtual warp: warp w's rows 0-7 are virtual warp 2w, rows 8-15
+            // virtual warp 2w + 1 (key order), so each warp runs two independent counter chains.
+            // Lanes with equal digits are found with 8 ballots (faster than __match_any_sync).
+            uint32_t rank[kCoopItems];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-                if (valid[h] && (peers[h] & lt) == 0u) s_cnt[2 * warp + h][dd[h]] = (uint16_t)(old[h] + __popc(peers[h]));
-            __syncwarp();
+            for (int r = 0; r < kCoopItems / 2; ++r) {
+                unsigned peers[2];
+                uint32_t dd[2], old[2];
+                bool valid[2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) rank[r + h * (kCoopItems / 2)] = old[h] + __popc(peers[h] & lt);
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = r + h * (kCoopItems / 2);
+                    valid[h] = wbase + rr * 32 + lane < n;
+                    dd[h] = (k[rr] >> shift) & 255u;
+                    unsigned pm = __ballot_sync(0xffffffffu, valid[h]);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const bool bit = (dd[h] >> b) & 1u;
+                        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                        pm &= bit ? bal : ~bal;
+                    }
+                    peers[h] = pm;
+                    old[h] = valid[h] ? s_cnt[2 * warp + h][dd[h]] : 0u;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (valid[h] && (peers[h] & lt) == 0u)
+                        s_cnt[2 * warp + h][dd[h]] = (uint16_t)(old[h] + __popc(peers[h]));
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < 2; ++h) rank[r + h * (kCoopItems / 2)] = old[h] + __popc(peers[h] & lt);
+            }
+            __syncthreads();
+            // thread d: tile total of digit d (published digit-major), its local start L (exclusive
+            // over digits) and the local start of every virtual warp's run of d (< 4096: 16 bits)
+            {
+                const int d = threadIdx.x;
+                uint32_t c = 0;
+#pragma unroll
+                for (int w = 0; w < kVW; ++w) c += s_cnt[w][d];
+                counts[(size_t)d * ntiles + tile] = c;
+                uint32_t tot;
+                const uint32_t ls = block_exclusive_scan(c, &tot, s_warp);
+                slot_ls(q)[d] = ls;
+                uint32_t run = ls;
+#pragma unroll
+                for (int w = 0; w < kVW; ++w) {
+                    const uint32_t cw = s_cnt[w][d];
+                    s_cnt[w][d] = (uint16_t)run;
+                    run += cw;
+                }
+            }
+            __syncthreads();
+            uint32_t* sk = slot_k(q);
+            uint32_t* sv = slot_v(q);
+#pragma unroll
+            for (int r = 0; r < kCoopItems; ++r)
+                if (wbase + r * 32 + lane < n) {
+                    const uint32_t lp = s_cnt[2 * warp + r / (kCoopItems / 2)][(k[r] >> shift) & 255u] + rank[r];
+                    sk[lp] = k[r];
+                    sv[lp] = v[r];
+                }
+            __syncthreads();  // s_cnt is reused by the next owned tile
         }
-        __syncthreads();
-        // thread d: tile total of digit d (published digit-major), its local start L (exclusive
-        // over digits) and the local start of every virtual warp's run of d (< 4096: fits 16 bits)
-        uint32_t local_start;
-        {
-            const int d = threadIdx.x;
-            uint32_t c = 0;
-#pragma unroll
-            for (int w = 0; w < kVW; ++w) c += s_cnt[w][d];
-            counts[(size_t)d * ntiles + tile] = c;
-            uint32_t tot;
-            local_start = block_exclusive_scan(c, &tot, s_warp);
-            uint32_t run = local_start;
-#pragma unroll
-            for (int w = 0; w < kVW; ++w) {
-                const uint32_t cw = s_cnt[w][d];
-                s_cnt[w][d] = (uint16_t)run;
-                run += cw;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < kCoopItems; ++r)
-            if (wbase + r * 32 + lane < n) {
-                const uint32_t lp = s_cnt[2 * warp + r / (kCoopItems / 2)][(k[r] >> shift) & 255u] + rank[r];
-                s_k[lp] = k[r];
-                s_v[lp] = v[r];
-            }
         STAMP(3 + 6 * j);
         grid.sync();
         STAMP(4 + 6 * j);
@@ -619,19 +641,19 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             for (uint32_t t0 = 0; t0 < ntiles; t0 += kThreads * 3) {
                 uint32_t x[3], sum = 0;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const uint32_t t = t0 + threadIdx.x * 3 + q;
-                    x[q] = t < ntiles ? row[t] : 0u;
-                    sum += x[q];
+                for (int qq = 0; qq < 3; ++qq) {
+                    const uint32_t t = t0 + threadIdx.x * 3 + qq;
+                    x[qq] = t < ntiles ? row[t] : 0u;
+                    sum += x[qq];
                 }
                 uint32_t tot;
                 const uint32_t ex = block_exclusive_scan(sum, &tot, s_warp);
                 uint32_t acc = carry + ex;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const uint32_t t = t0 + threadIdx.x * 3 + q;
+                for (int qq = 0; qq < 3; ++qq) {
+                    const uint32_t t = t0 + threadIdx.x * 3 + qq;
                     if (t < ntiles) row[t] = acc;
-                    acc += x[q];
+                    acc += x[qq];
                 }
                 carry += tot;
             }
@@ -640,16 +662,25 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
         grid.sync();
         STAMP(6 + 6 * j);
         // phase C: global position = tile's global offset of the digit + (local position - L)
-        s_delta[threadIdx.x] = counts[(size_t)threadIdx.x * ntiles + tile] - local_start;
-        __syncthreads();
         uint32_t* kd = kb[dst];
         uint32_t* vd = vb[dst];
+        for (int q = 0; q < tpc; ++q) {
+            const uint32_t tile = tile_of(q);
+            if (tile >= ntiles) break;
+            const uint32_t tbase = tile * kCoopTile;
+            const uint32_t tcount = min(n - tbase, (uint32_t)kCoopTile);
+            s_delta[threadIdx.x] = counts[(size_t)threadIdx.x * ntiles + tile] - slot_ls(q)[threadIdx.x];
+            __syncthreads();
+            const uint32_t* sk = slot_k(q);
+            const uint32_t* sv = slot_v(q);
 #pragma unroll 4
-        for (uint32_t i = threadIdx.x; i < tcount; i += kThreads) {
-            const uint32_t key = s_k[i];
-            const uint32_t pos = s_delta[(key >> shift) & 255u] + i;
-            kd[pos] = key;
-            vd[pos] = s_v[i];
+            for (uint32_t i = threadIdx.x; i < tcount; i += kThreads) {
+                const uint32_t key = sk[i];
+                const uint32_t pos = s_delta[(key >> shift) & 255u] + i;
+                kd[pos] = key;
+                vd[pos] = sv[i];
+            }
+            __syncthreads();  // s_delta is reused by the next owned tile
         }
         src = dst;
         STAMP(7 + 6 * j);
@@ -774,21 +805,47 @@ size_t radix_coop_count_words(uint64_t n) {
 cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                             uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work) {
     if (n == 0) return cudaSuccess;
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, radix_coop_kernel, kThreads, 0) != cudaSuccess)
-            per_sm = 0;
-    }
+    if (n >= (1ull << 31)) return cudaErrorCooperativeLaunchTooLarge;
     const uint64_t nt = (n + kCoopTile - 1) / kCoopTile;
-    if (nt > (uint64_t)lc.num_sms * per_sm || n >= (1ull << 31)) return cudaErrorCooperativeLaunchTooLarge;
-    cudaError_t e;
+    // tiles per CTA: the fewest that fit the tiles into one resident wave (each owned tile keeps
+    // 33 KB of shared memory between its rank phase and its scatter; one tile: static memory)
+    static int per_sm_of[kCoopMaxTpc + 1] = {};
+    int tpc = 0, grid = 0;
+    for (int t = 1; t <= kCoopMaxTpc; ++t) {
+        const size_t smem = t == 1 ? 0 : coop_dyn_smem(t);
+        if (!per_sm_of[t]) {
+            cudaError_t e = cudaSuccess;
+            if (t == 1) {
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_of[t], radix_coop_kernel<1>, kThreads, 0);
+            } else {
+                if (smem > 48 * 1024)
+                    e = cudaFuncSetAttribute(radix_coop_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_of[t], radix_coop_kernel<0>, kThreads, smem);
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                per_sm_of[t] = -1;
+            }
+        }
+        if (per_sm_of[t] <= 0) continue;
+        const uint64_t cap = (uint64_t)lc.num_sms * per_sm_of[t];
+        if (cap * t >= nt) {
+            tpc = t;
+            grid = (int)((nt + t - 1) / t);
+            break;
+        }
+    }
+    if (!tpc) return cudaErrorCooperativeLaunchTooLarge;
+    const size_t smem = tpc == 1 ? 0 : coop_dyn_smem(tpc);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(radix_coop_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t* hist = work;  // zero at rest: allocated zeroed, re-zeroed by the kernel
     uint32_t* counts = work + 4 * 256;
     uint32_t nn = (uint32_t)n;
-    void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts};
+    void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts, &tpc};
     LaunchScope s(lc, "radix_sort");
-    e = cudaLaunchCooperativeKernel((const void*)radix_coop_kernel, dim3((unsigned)nt), dim3(kThreads), args, 0,
-                                    lc.stream);
+    const void* fn = tpc == 1 ? (const void*)radix_coop_kernel<1> : (const void*)radix_coop_kernel<0>;
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, smem, lc.stream);
     lc.count++;
     return e;
 }

@@ -27,10 +27,12 @@ def _sort(keys, vals, begin, end):
 
 @pytest.mark.parametrize("n,bits,spread", [(1000, 32, 1), (1_000_000, 32, 1), (1_000_000, 32, 0),
                                           (3_500_000, 9, 1), (5000, 9, 1), (777_777, 13, 1),
-                                          # 32-bit sorts run as one cooperative kernel when the
-                                          # 2048-key tiles fit one wave; 3 M keys fall back
+                                          # 32-bit sorts run as one cooperative kernel while the
+                                          # 4096-key tiles fit one wave at <= 6 tiles per CTA
+                                          # (multi-tile CTAs from ~1.2 M keys); 4 M keys fall back
                                           (1, 32, 1), (2048, 32, 1), (2049, 32, 0), (3_000_000, 32, 1),
-                                          (100_000, 32, 2)])
+                                          (100_000, 32, 2), (2_000_003, 32, 0), (2_500_000, 32, 2),
+                                          (4_000_000, 32, 1)])
 def test_radix_sort_is_stable(n, bits, spread):
     rng = np.random.default_rng(n + bits)
     if spread == 2:  # all keys equal: every pass trivial
