@@ -490,41 +490,44 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                         }
                     }
 #endif
-                    if (ga) {
-                        const float next = T * (1.0f - alpha_a);
-                        if (THR && next < tmin) {
-                            done = true;
-                            break;
-                        }
-                        const float w = T * alpha_a;
-                        const float4 r2 = lds_f4(a_r2 + 16u * j);
-                        acc0 = acc0 + w * r2.x;
-                        acc1 = acc1 + w * r2.y;
-                        acc2 = acc2 + w * r2.z;
-                        if (ARG && w > wmax) {
-                            wmax = w;
+                    {  // branch-free commits of a then b (b only when a did not end the pixel)
+                        const float na = T * (1.0f - alpha_a);
+                        const bool sa = THR && ga && na < tmin;
+                        const bool ca = ga && !sa;
+                        const float wa_ = T * alpha_a;
+                        const float4 r2a = lds_f4(a_r2 + 16u * j);
+                        const float a0 = acc0 + wa_ * r2a.x, a1 = acc1 + wa_ * r2a.y, a2 = acc2 + wa_ * r2a.z;
+                        acc0 = ca ? a0 : acc0;
+                        acc1 = ca ? a1 : acc1;
+                        acc2 = ca ? a2 : acc2;
+                        if (ARG && ca && wa_ > wmax) {
+                            wmax = wa_;
                             amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
                         }
-                        last = (int32_t)lds_u32(a_idx + 4u * j);
-                        T = next;
-                    }
-                    if (gb) {
-                        const float next = T * (1.0f - alpha_b);
-                        if (THR && next < tmin) {
+                        const int32_t ia = (int32_t)lds_u32(a_idx + 4u * j);
+                        last = ca ? ia : last;
+                        T = ca ? na : T;
+                        const bool gb2 = gb && !sa;
+                        const float nb = T * (1.0f - alpha_b);
+                        const bool sb = THR && gb2 && nb < tmin;
+                        const bool cb = gb2 && !sb;
+                        const float wb_ = T * alpha_b;
+                        const float4 r2b = lds_f4(a_r2 + 16u * jb);
+                        const float b0 = acc0 + wb_ * r2b.x, b1 = acc1 + wb_ * r2b.y, b2 = acc2 + wb_ * r2b.z;
+                        acc0 = cb ? b0 : acc0;
+                        acc1 = cb ? b1 : acc1;
+                        acc2 = cb ? b2 : acc2;
+                        if (ARG && cb && wb_ > wmax) {
+                            wmax = wb_;
+                            amax_gid = (int32_t)lds_u32(a_gid + 4u * jb);
+                        }
+                        const int32_t ib = (int32_t)lds_u32(a_idx + 4u * jb);
+                        last = cb ? ib : last;
+                        T = cb ? nb : T;
+                        if (sa || sb) {
                             done = true;
                             break;
                         }
-                        const float w = T * alpha_b;
-                        const float4 r2 = lds_f4(a_r2 + 16u * jb);
-                        acc0 = acc0 + w * r2.x;
-                        acc1 = acc1 + w * r2.y;
-                        acc2 = acc2 + w * r2.z;
-                        if (ARG && w > wmax) {
-                            wmax = w;
-                            amax_gid = (int32_t)lds_u32(a_gid + 4u * jb);
-                        }
-                        last = (int32_t)lds_u32(a_idx + 4u * jb);
-                        T = next;
                     }
                 }
             } else {
