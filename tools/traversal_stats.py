@@ -24,7 +24,7 @@ buf = (C.c_ulonglong * 12)()
 lib = ctx.lib
 lib.splat_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 rc0 = lib.splat_debug_stats(buf, 1)
-assert rc0 == 0, f"not an instrumented build (rc {rc0})"
+print("forward stats:", "on" if rc0 == 0 else f"off (rc {rc0})")
 from paper_2411_12788_b200 import capi  # noqa: E402
 from paper_2411_12788_b200.rasterizer import render_backward  # noqa: E402
 lib.splat_debug_bstats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
