@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
         }
         if (!__any_sync(0xffffffffu, m > 0)) continue;
         const uint32_t gid = gids[k];
-        const float rcp_w = __frcp_rn((float)w);
         const int inc = (int)warp_incl_scan((uint32_t)m, lane);
         const int off = inc - m;
         const int total = __shfl_sync(0xffffffffu, inc, 31);
@@ -201,17 +200,19 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
             for (int step = 16; step > 0; step >>= 1)
                 if (__shfl_sync(0xffffffffu, off, owner + step) <= e) owner += step;
             const int q = e - __shfl_sync(0xffffffffu, off, owner);
-            const int ow = __shfl_sync(0xffffffffu, w, owner);
-            const float orcp = __shfl_sync(0xffffffffu, rcp_w, owner);
-            // q / ow without an integer division: (q + 0.5) / ow is >= 0.5 / ow away from an
-            // integer and its float error is below (q + 0.5) 2^-23 / ow, so truncation is exact
-            // for q < 2^22 (q < n_st here)
-            const int qy = __float2int_rz(((float)q + 0.5f) * orcp);
-            const int esx = __shfl_sync(0xffffffffu, sx0, owner) + (q - qy * ow);
-            const int esy = __shfl_sync(0xffffffffu, sy0, owner) + qy;
-            const int st = esy * st_x + esx;
-            const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
+            // the owner's tile rect is all the entry needs (its supertile rect follows from it):
+            // four shuffles per window, the shuffle pipe being what bounds this kernel
             const uint32_t optx = __shfl_sync(0xffffffffu, ptx, owner), opty = __shfl_sync(0xffffffffu, pty, owner);
+            const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
+            const int osx0 = (int)(optx & 0xffffu) / kST, osy0 = (int)(opty & 0xffffu) / kST;
+            const int ow = (int)(optx >> 16) / kST - osx0 + 1;
+            // q / ow without an integer division: (q + 0.5) / ow is >= 0.5 / ow away from an
+            // integer and the float error of (q + 0.5) * rcp(ow) is below (q + 0.5) 2^-21 / ow,
+            // so truncation is exact for q < 2^20 (q < n_st here)
+            const int qy = __float2int_rz(((float)q + 0.5f) * __fdividef(1.0f, (float)ow));
+            const int esx = osx0 + (q - qy * ow);
+            const int esy = osy0 + qy;
+            const int st = esy * st_x + esx;
             const unsigned grp = __match_any_sync(0xffffffffu, valid ? st : -1);
             const int leader = __ffs(grp) - 1;
             uint32_t base = 0;
