@@ -1,0 +1,64 @@
+"""Device state that persists between calls (SURVEY.md §8b boundary, capi.cu): the survivor /
+pair counters, the persistent kernels' work queues, the depth sort's histogram, the binning scan's
+look-back words and the alternating touched-list counters are all re-zeroed by the kernels that
+consume them instead of by memsets.  Interleave every entry point over changing set sizes, image
+shapes and tile sizes (buffers regrow, the sort changes tiles per CTA) and check each result
+against the oracle, so a counter left dirty by one call shows up in the next."""
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise, assert_grads_close
+from paper_2411_12788_b200 import capi, scenes
+from paper_2411_12788_b200 import rasterizer as R
+from paper_2411_12788_b200.capi import AdamConfig, RasterConfig
+from paper_2411_12788_b200.trainer import ViewTrainer
+
+pytestmark = pytest.mark.gpu
+
+
+def _forward_matches(oracle, s, cam, cfg, what):
+    out = R.render(s, cam, cfg)
+    want = oracle.render(s, cam, cfg)
+    for k in ("color", "alpha", "transmittance", "max_contributor"):
+        assert_bitwise(getattr(out, k), want[k], f"{what} {k}")
+    return want
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_interleaved_calls_over_changing_sizes(oracle, seed):
+    rng = np.random.default_rng(seed)
+    plan = [(12_000, 160, 120, 16), (40_000, 256, 192, 16), (3_000, 96, 64, 8), (25_000, 200, 150, 32),
+            (0, 64, 64, 16), (30_000, 256, 256, 16)]
+    for i, (n, w, h, ts) in enumerate(plan):
+        cfg = RasterConfig(tile_size=ts)
+        cam = scenes.fov_camera(w, h, 60.0, (0.3 * float(rng.normal()), 0.2, -3.0))
+        if n == 0:  # an empty set between populated ones
+            out = R.render(scenes.GaussianSet.empty(0), cam, cfg)
+            assert np.all(out.alpha == 0)
+            continue
+        s = scenes.make_gaussians(n, seed=seed * 10 + i)
+        want = _forward_matches(oracle, s, cam, cfg, f"step {i} render")
+        target = oracle.render(scenes.perturbed(s), cam, cfg)["color"]
+        _, d_color = oracle.l1_loss(want["color"], target)
+        got = R.render_backward(s, cam, cfg, d_color)
+        ref = oracle.render_backward(s, cam, d_color, cfg)
+        assert_grads_close(got, ref, what=f"step {i} backward")
+        # the same forward again right after a backward: queues and counters are back at zero
+        _forward_matches(oracle, s, cam, cfg, f"step {i} render again")
+
+
+def test_training_steps_then_render(oracle):
+    """Native training steps (host and device targets), then a plain render of the updated set:
+    equal to the oracle's render of the same parameters."""
+    import torch
+    s = scenes.make_gaussians(15_000, seed=3)
+    cams = [scenes.fov_camera(192, 128, 60.0, (0.2 * k, 0.1, -3.0)) for k in range(3)]
+    targets = [oracle.render(scenes.perturbed(s), c)["color"] for c in cams]
+    ds = R.DeviceGaussians.from_host(s)
+    tr = ViewTrainer(ds, AdamConfig(), group_mask=capi.GROUP_ALL)
+    for k in range(3):
+        tr.step_host([cams[k]], [np.ascontiguousarray(targets[k])])
+        tr.step([cams[(k + 1) % 3]], [torch.from_numpy(targets[(k + 1) % 3]).cuda()])
+    torch.cuda.synchronize()
+    updated = ds.to_host()
+    _forward_matches(oracle, updated, cams[0], RasterConfig(), "after training")
