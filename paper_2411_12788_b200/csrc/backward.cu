@@ -694,6 +694,20 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
     return cudaGetLastError();
 }
 
+// Device floats straight into mapped pinned host memory (the per-view losses of a training step):
+// a kernel instead of a copy-engine transfer, which would queue behind bulk host copies.
+__global__ void copy_to_host_kernel(const float* __restrict__ src, float* dst_mapped, int n) {
+    pdl_wait();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<volatile float*>(dst_mapped)[i] = src[i];
+}
+
+cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n) {
+    if (n <= 0) return cudaSuccess;
+    const cudaError_t e = launch_pdl(lc.stream, copy_to_host_kernel, dim3(1), dim3(128), 0, src, dst_mapped, n);
+    lc.count++;
+    return e;
+}
+
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss) {
     {
         LaunchScope ls_(lc, "loss_reduce");

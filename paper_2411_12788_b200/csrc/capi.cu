@@ -153,6 +153,9 @@ struct splat_ctx {
     cudaEvent_t ev_free = nullptr, ev_copied[8] = {};
     uint32_t* host_counters = nullptr;  // mapped pinned [n_surv, Ps, P], written by preprocess's last block
     uint32_t* host_counters_dev = nullptr;  // its device alias
+    float* host_loss = nullptr;             // mapped pinned per-view losses of splat_train_step
+    float* host_loss_dev = nullptr;
+    int host_loss_cap = 0;
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
     // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
@@ -724,6 +727,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (!ctx) return SPLAT_OK;
     cudaSetDevice(ctx->device);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
+    if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
     if (ctx->lc.work_counters) cudaFree(ctx->lc.work_counters);
     if (ctx->ev_fwd_start) cudaEventDestroy(ctx->ev_fwd_start);
@@ -1428,8 +1432,18 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
     }
     if ((rc = splat_adam_step(ctx, p, grads, moments, adam, step_count, group_mask))) return rc;
     if (loss_host) {
-        CK(cudaMemcpyAsync(loss_host, losses, (size_t)n_views * 4, cudaMemcpyDeviceToHost, s), "read loss");
+        if (ctx->host_loss_cap < n_views) {
+            if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
+            ctx->host_loss = nullptr;
+            ctx->host_loss_cap = 0;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_loss), (size_t)n_views * 4, cudaHostAllocMapped),
+               "alloc pinned loss");
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_loss_dev), ctx->host_loss, 0), "map loss");
+            ctx->host_loss_cap = n_views;
+        }
+        CK(launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views), "read loss");
         CK(cudaStreamSynchronize(s), "sync");
+        std::memcpy(loss_host, ctx->host_loss, (size_t)n_views * 4);
     }
     return SPLAT_OK;
 }

@@ -66,8 +66,10 @@ class Context:
 
     def bind_stream(self):
         torch = _torch()
-        s = torch.cuda.current_stream(self.device)
-        self.lib.splat_ctx_set_stream(self.h, C.c_void_p(s.cuda_stream))
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != getattr(self, "_bound_stream", None):  # one C call per stream change, not per step
+            self.lib.splat_ctx_set_stream(self.h, C.c_void_p(s))
+            self._bound_stream = s
 
     def check(self, rc: int):
         if rc == 0:
