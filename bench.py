@@ -459,6 +459,14 @@ def run_ours(args):
             if ncu:
                 roof["traffic"] = ncu.get("dram_bytes_per_launch")
                 roof["ncu"] = ncu
+    # whole-step roofline (SURVEY.md §8d compulsory traffic: 1020 N + 12 P + 60 HW bytes per view at
+    # config 1, Adam on means), against the measured HBM peak
+    step_roof = None
+    if args.config == 1 and n_views:
+        bpv = 1020.0 * n + 12.0 * avg_pairs + 60.0 * hw
+        ach = bpv * value / world / 1e9  # per GPU
+        step_roof = {"bytes_per_view": bpv, "achieved_gbs_per_gpu": ach, "peak": peak, "frac": ach / peak,
+                     "note": "SURVEY.md 8d algorithmic bytes of the whole view (fwd + bwd + Adam on means)"}
     breakdown = {k: {"ms_per_step": v[0] / p_steps, "launches_per_step": v[1] / p_steps,
                      "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
 
@@ -479,7 +487,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32",
                 "data": f"synthetic (seeded, BASELINE cfg{args.config} shapes)",
                 "config": workload_config(args, world), "e2e": e2e, "gpu_launches": int(launches),
-                "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
                 "pairs_per_view": avg_pairs, "survivors_per_view": n_surv, "kernel_breakdown": breakdown}
         if allreduce:
             line["allreduce"] = allreduce
