@@ -129,6 +129,16 @@ struct splat_ctx {
     // issues its host->device target copies there, so the bulk transfer overlaps the (long,
     // launch-free) forward kernel instead of slowing the launches of the sort and binning kernels
     std::function<int()> post_forward_hook;
+    // Multi-view training steps alternate views between this context and a twin (own stream and
+    // buffers), so one view's latency-bound preprocess / sort / binning overlaps the other's
+    // issue-bound blend kernels; the chains (which accumulate into the shared gradients) are
+    // serialised across the two by events.
+    splat_ctx* twin = nullptr;
+    cudaStream_t own_stream = nullptr;  // the twin's compute stream
+    bool view_overlap = true;
+    bool twin_member = false;  // part of an overlapped multi-view step (record ev_chain_done)
+    cudaEvent_t chain_wait = nullptr;  // run_backward: wait for this before the chain
+    cudaEvent_t ev_chain_done = nullptr, ev_step = nullptr;
     std::string err;
     // per-Gaussian
     DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
@@ -669,12 +679,14 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
         CK(ctx->chain_list.ensure(((size_t)st.n_surv + 2) * 4), "alloc chain list");
         if (zero_async) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_zero, 0), "zero join");
+        if (ctx->chain_wait) CK(cudaStreamWaitEvent(ctx->stream, ctx->chain_wait, 0), "chain order");
         CK(launch_chain(lc, gp, st.cp, ctx->grad2d.as<float>(), ctx->rec.as<ProjRec>(), *grads, accumulate, st.n_surv,
                         ctx->chain_list.as<uint32_t>(), zero_async),
            "chain");
     }
     if (loss_side) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_loss, 0), "loss join");
     else if (partials) CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
+    if (ctx->chain_wait || ctx->twin_member) CK(cudaEventRecord(ctx->ev_chain_done, ctx->stream), "chain done");
     (void)cfg;
     (void)mask;
     return SPLAT_OK;
@@ -706,7 +718,9 @@ int splat_ctx_create(int device, splat_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_fwd_start, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_zero, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_bwd, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_loss, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_chain_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming) != cudaSuccess) {
         cudaFree(c->lc.work_counters);
         delete c;
         return SPLAT_ERR_CUDA;
@@ -718,6 +732,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
         c->lc.bwd_px2 = !(e2 && std::strcmp(e2, "0") == 0);
         const char* e3 = std::getenv("SPLAT_COOP_SORT");
         c->coop_sort = !(e3 && std::strcmp(e3, "0") == 0);
+        const char* e4 = std::getenv("SPLAT_VIEW_OVERLAP");
+        c->view_overlap = !(e4 && std::strcmp(e4, "0") == 0);
     }
     *out = c;
     return SPLAT_OK;
@@ -726,6 +742,16 @@ int splat_ctx_create(int device, splat_ctx** out) {
 int splat_ctx_destroy(splat_ctx* ctx) {
     if (!ctx) return SPLAT_OK;
     cudaSetDevice(ctx->device);
+    if (ctx->twin) {
+        ctx->twin->lc.prof = nullptr;  // shared with this context
+        splat_ctx_destroy(ctx->twin);
+    }
+    if (ctx->own_stream) {
+        cudaStreamSynchronize(ctx->own_stream);
+        cudaStreamDestroy(ctx->own_stream);
+    }
+    if (ctx->ev_chain_done) cudaEventDestroy(ctx->ev_chain_done);
+    if (ctx->ev_step) cudaEventDestroy(ctx->ev_step);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
     if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
@@ -765,7 +791,9 @@ int splat_sync(splat_ctx* ctx) {
 
 const char* splat_last_error(const splat_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-int64_t splat_kernel_launches(const splat_ctx* ctx) { return ctx ? ctx->lc.count : 0; }
+int64_t splat_kernel_launches(const splat_ctx* ctx) {
+    return ctx ? ctx->lc.count + (ctx->twin ? ctx->twin->lc.count : 0) : 0;
+}
 
 int splat_profile_enable(splat_ctx* ctx, int on) {
     if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
@@ -1403,32 +1431,71 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
             return SPLAT_OK;
         };
     }
+    // views alternate between this context and its twin (own stream and buffers) so that one
+    // view's latency-bound preprocess / sort / binning overlaps the other's blend kernels; the
+    // chains accumulate into the shared gradients one after the other (chain_wait events)
+    const bool overlap = n_views > 1 && ctx->view_overlap;
+    if (overlap && !ctx->twin) {
+        splat_ctx* tw = nullptr;
+        if ((rc = splat_ctx_create(ctx->device, &tw))) return set_err(ctx, rc, "train_step: twin context");
+        ctx->twin = tw;
+        CK(cudaStreamCreateWithFlags(&tw->own_stream, cudaStreamNonBlocking), "twin stream");
+        tw->stream = tw->lc.stream = tw->own_stream;
+    }
+    if (overlap) {
+        splat_ctx* tw = ctx->twin;
+        tw->lc.prof = ctx->lc.prof;  // one per-kernel profile for both
+        CK(cudaEventRecord(ctx->ev_step, s), "record step");
+        CK(cudaStreamWaitEvent(tw->stream, ctx->ev_step, 0), "twin start");
+        ctx->twin_member = tw->twin_member = true;
+    }
+    cudaEvent_t prev_chain = nullptr;
+    auto fail = [&](splat_ctx* c, int r) {
+        if (c != ctx) ctx->err = c->err;
+        ctx->chain_wait = nullptr;
+        ctx->twin_member = false;
+        if (ctx->twin) ctx->twin->chain_wait = nullptr;
+        return r;
+    };
     for (int k = 0; k < n_views; ++k) {
-        rc = run_forward(ctx, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr);
-        if (rc == SPLAT_OK && ctx->post_forward_hook) rc = ctx->post_forward_hook();  // not run by run_forward
+        splat_ctx* c = overlap && (k & 1) ? ctx->twin : ctx;
+        rc = run_forward(c, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr);
+        if (rc == SPLAT_OK && ctx->post_forward_hook) {  // the host copies, once view 0's forward is queued
+            std::function<int()> hook;
+            hook.swap(ctx->post_forward_hook);
+            rc = hook();
+        }
         ctx->post_forward_hook = nullptr;
-        if (rc) return rc;
+        if (rc) return fail(c, rc);
         const float* tgt = targets[k];
         if (targets_on_host) {
             const int slot = k % slots;
-            CK(cudaStreamWaitEvent(s, ctx->ev_copied[slot], 0), "wait target");
+            CK(cudaStreamWaitEvent(c->stream, ctx->ev_copied[slot], 0), "wait target");
             tgt = ctx->tgt_stage.as<float>() + (size_t)slot * view_floats;
         }
         const int acc = k > 0 ? 1 : 0;
+        c->chain_wait = overlap ? prev_chain : nullptr;
         if (lambda_dssim > 0.0f) {
             const int w = cams[k].width, h = cams[k].height;
-            CK(ctx->d_color_buf.ensure((size_t)w * h * 3 * 4), "alloc d_color");
-            float* dc = ctx->d_color_buf.as<float>();
-            if ((rc = splat_photometric_loss(ctx, ctx->st.color, tgt, w, h, 3, lambda_dssim, dc, losses + k))) return rc;
-            if ((rc = run_backward(ctx, &g, &cams[k], cfg, dc, nullptr, nullptr, bg, grads, acc, nullptr))) return rc;
+            CK(c->d_color_buf.ensure((size_t)w * h * 3 * 4), "alloc d_color");
+            float* dc = c->d_color_buf.as<float>();
+            if ((rc = splat_photometric_loss(c, c->st.color, tgt, w, h, 3, lambda_dssim, dc, losses + k))) return fail(c, rc);
+            if ((rc = run_backward(c, &g, &cams[k], cfg, dc, nullptr, nullptr, bg, grads, acc, nullptr))) return fail(c, rc);
         } else {
-            if ((rc = run_backward(ctx, &g, &cams[k], cfg, nullptr, tgt, nullptr, bg, grads, acc, losses + k))) return rc;
+            if ((rc = run_backward(c, &g, &cams[k], cfg, nullptr, tgt, nullptr, bg, grads, acc, losses + k)))
+                return fail(c, rc);
         }
+        c->chain_wait = nullptr;
+        prev_chain = c->ev_chain_done;
         if (targets_on_host && k + slots < n_views) {  // refill the slot once this view's backward ran
-            CK(cudaEventRecord(ctx->ev_free, s), "record");
+            CK(cudaEventRecord(ctx->ev_free, c->stream), "record");
             CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_free, 0), "wait");
             if ((rc = issue_copy(k + slots))) return rc;
         }
+    }
+    if (overlap) {  // everything of every view is ordered before the last chain
+        CK(cudaStreamWaitEvent(s, prev_chain, 0), "join twin");
+        ctx->twin_member = ctx->twin->twin_member = false;
     }
     if ((rc = splat_adam_step(ctx, p, grads, moments, adam, step_count, group_mask))) return rc;
     if (loss_host) {
