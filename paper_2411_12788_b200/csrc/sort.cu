@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     int ns = 0;
 #endif
     STAMP(0);
-    constexpr int kVW = 2 * kWarps;  // virtual warps (two per warp)
+    constexpr int kChains = 2;  // independent rank-counter chains per warp
+    constexpr int kVW = kChains * kWarps;  // virtual warps
     __shared__ __align__(16) uint16_t s_cnt[kVW][256];
     __shared__ uint32_t s_gh[4][256];
     __shared__ uint32_t s_warp[kWarps];
@@ -562,18 +563,20 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             }
             for (int i = threadIdx.x; i < kVW * 256 / 2; i += kThreads) reinterpret_cast<uint32_t*>(&s_cnt[0][0])[i] = 0u;
             __syncthreads();
-            // Stable ranks per virtual warp: warp w's rows 0-7 are virtual warp 2w, rows 8-15
-            // virtual warp 2w + 1 (key order), so each warp runs two independent counter chains.
-            // Lanes with equal digits are found with 8 ballots (faster than __match_any_sync).
+            // Stable ranks per virtual warp: warp w's rows are cut into kChains consecutive groups,
+            // group h being virtual warp kChains w + h (key order), so each warp runs kChains
+            // independent counter chains.  Lanes with equal digits are found with 8 ballots
+            // (faster than __match_any_sync).
+            constexpr int kRows = kCoopItems / kChains;
             uint32_t rank[kCoopItems];
 #pragma unroll
-            for (int r = 0; r < kCoopItems / 2; ++r) {
-                unsigned peers[2];
-                uint32_t dd[2], old[2];
-                bool valid[2];
+            for (int r = 0; r < kRows; ++r) {
+                unsigned peers[kChains];
+                uint32_t dd[kChains], old[kChains];
+                bool valid[kChains];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int rr = r + h * (kCoopItems / 2);
+                for (int h = 0; h < kChains; ++h) {
+                    const int rr = r + h * kRows;
                     valid[h] = wbase + rr * 32 + lane < n;
                     dd[h] = (k[rr] >> shift) & 255u;
                     unsigned pm = __ballot_sync(0xffffffffu, valid[h]);
@@ -584,16 +587,16 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                         pm &= bit ? bal : ~bal;
                     }
                     peers[h] = pm;
-                    old[h] = valid[h] ? s_cnt[2 * warp + h][dd[h]] : 0u;
+                    old[h] = valid[h] ? s_cnt[kChains * warp + h][dd[h]] : 0u;
                 }
                 __syncwarp();
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                for (int h = 0; h < kChains; ++h)
                     if (valid[h] && (peers[h] & lt) == 0u)
-                        s_cnt[2 * warp + h][dd[h]] = (uint16_t)(old[h] + __popc(peers[h]));
+                        s_cnt[kChains * warp + h][dd[h]] = (uint16_t)(old[h] + __popc(peers[h]));
                 __syncwarp();
 #pragma unroll
-                for (int h = 0; h < 2; ++h) rank[r + h * (kCoopItems / 2)] = old[h] + __popc(peers[h] & lt);
+                for (int h = 0; h < kChains; ++h) rank[r + h * kRows] = old[h] + __popc(peers[h] & lt);
             }
             __syncthreads();
             // thread d: tile total of digit d (published digit-major), its local start L (exclusive
@@ -621,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
 #pragma unroll
             for (int r = 0; r < kCoopItems; ++r)
                 if (wbase + r * 32 + lane < n) {
-                    const uint32_t lp = s_cnt[2 * warp + r / (kCoopItems / 2)][(k[r] >> shift) & 255u] + rank[r];
+                    const uint32_t lp = s_cnt[kChains * warp + r / (kCoopItems / kChains)][(k[r] >> shift) & 255u] + rank[r];
                     sk[lp] = k[r];
                     sv[lp] = v[r];
                 }
