@@ -183,12 +183,15 @@ __device__ __forceinline__ bool quad_box_reaches(const float4& r0, float c, floa
             const float t2 = __fmul_rn(__fmul_rn(c, dy), dy);
             return __fmaf_rn(-1e-5f, t0 + fabsf(t1) + t2, t0 + t1 + t2);
         };
+        // Only edges facing the centre (the origin of (dx, dy)) can hold the minimum: at a
+        // boundary minimiser p, -grad q(p) lies in the box's outward normal cone, and convexity
+        // (q(0) <= q(p)) puts the centre on the outer side of that edge's line.  At most one
+        // x-edge and one y-edge face it; the edge picked when none faces only adds a box point.
         const float ia = __fdividef(1.0f, a), ic = __fdividef(1.0f, c);
-        const float y_at_xl = fminf(fmaxf(-b * dxl * ic, dyl), dyh);
-        const float y_at_xh = fminf(fmaxf(-b * dxh * ic, dyl), dyh);
-        const float x_at_yl = fminf(fmaxf(-b * dyl * ia, dxl), dxh);
-        const float x_at_yh = fminf(fmaxf(-b * dyh * ia, dxl), dxh);
-        qmin = fminf(fminf(q_lo(dxl, y_at_xl), q_lo(dxh, y_at_xh)), fminf(q_lo(x_at_yl, dyl), q_lo(x_at_yh, dyh)));
+        const float ex = dxl > 0.0f ? dxl : dxh, ey = dyl > 0.0f ? dyl : dyh;
+        const float y_at_x = fminf(fmaxf(-b * ex * ic, dyl), dyh);
+        const float x_at_y = fminf(fmaxf(-b * ey * ia, dxl), dxh);
+        qmin = fminf(q_lo(ex, y_at_x), q_lo(x_at_y, ey));
     }
     return -0.5f * qmin >= cut;
 }
