@@ -77,7 +77,11 @@ __device__ __forceinline__ void commit_sample(bool p, float* vv, float& T, float
                                               float dy) {
     const float a = p ? alpha : 0.0f, g = p ? g2d : 0.0f;
     const float one_m_a = 1.0f - a;
-    const float t_before = p ? __fdividef(T, one_m_a) : T;
+    // 1 - alpha is in [0.01, 1] (alpha <= alpha_max) and T is normal: one rcp.approx.ftz (~1 ulp)
+    // instead of __fdividef's denormal-range handling; T_before is not bit-exact anyway
+    float rcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(one_m_a));
+    const float t_before = p ? T * rcp : T;
     const float w = t_before * a;
     vv[6] += w * dL0;
     vv[7] += w * dL1;
