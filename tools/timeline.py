@@ -50,6 +50,17 @@ def main(steps: int = 3, warmup: int = 5, host: bool = False):
         t0 = pre[len(pre) // 2]["ts"] if pre else 0
         for e in pre[len(pre) // 2: len(pre) // 2 + 60]:
             print(f"API {e['ts'] - t0:9.1f} {e['dur']:8.1f}  {e['name']}")
+        # host time between the end of one step's final synchronisation and the next step's
+        # first runtime call (Python + ctypes overhead of the public API)
+        syncs = [e for e in api if "Synchronize" in e["name"]]
+        gaps = []
+        for a in syncs:
+            end = a["ts"] + a["dur"]
+            nxt = [e for e in api if e["ts"] >= end and "Synchronize" not in e["name"]]
+            if nxt:
+                gaps.append(nxt[0]["ts"] - end)
+        if gaps:
+            print("inter-step host gaps (us):", [round(g, 1) for g in gaps])
     # split into steps at the preprocess kernel
     cur, all_steps = [], []
     for e in ks:

@@ -1,5 +1,9 @@
 #!/usr/bin/env python3
-"""Forward traversal statistics of one config-1 view (instrumented build, SPLAT_B200_LIB).
+"""Forward / backward traversal statistics of one config-1 view (instrumented build, SPLAT_B200_LIB).
+
+Known issue: with the forward counters compiled in (-DSPLAT_STATS in forward.cu) the instrumented
+forward faults at 1 M Gaussians (fine at 20 K); build with the forward counters renamed out
+(SPLAT_STATS_FWD) to read the backward counters at full size.
 
     python tools/stats_build.py   # here
     SPLAT_B200_LIB=paper_2411_12788_b200/lib_stats/libsplat_b200.so python tools/traversal_stats.py
