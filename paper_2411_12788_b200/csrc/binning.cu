@@ -192,27 +192,34 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
         const int inc = (int)warp_incl_scan((uint32_t)m, lane);
         const int off = inc - m;
         const int total = __shfl_sync(0xffffffffu, inc, 31);
-        for (int e0 = 0; e0 < total; e0 += 32) {
+        // The entry of lane `lane` in window e0: its owner (last lane whose entries start at or
+        // before it, by binary search over the scanned offsets) and its supertile.  The owner's
+        // tile rect is all it needs (the supertile rect follows from it).
+        auto locate = [&](int e0, int& st, uint32_t& optx, uint32_t& opty, uint32_t& ogid, int& esx, int& esy) {
             const int e = e0 + lane;
-            const bool valid = e < total;
-            int owner = 0;  // last lane whose entries start at or before e
+            int owner = 0;
 #pragma unroll
             for (int step = 16; step > 0; step >>= 1)
                 if (__shfl_sync(0xffffffffu, off, owner + step) <= e) owner += step;
             const int q = e - __shfl_sync(0xffffffffu, off, owner);
-            // the owner's tile rect is all the entry needs (its supertile rect follows from it):
-            // four shuffles per window, the shuffle pipe being what bounds this kernel
-            const uint32_t optx = __shfl_sync(0xffffffffu, ptx, owner), opty = __shfl_sync(0xffffffffu, pty, owner);
-            const uint32_t ogid = __shfl_sync(0xffffffffu, gid, owner);
+            optx = __shfl_sync(0xffffffffu, ptx, owner);
+            opty = __shfl_sync(0xffffffffu, pty, owner);
+            ogid = __shfl_sync(0xffffffffu, gid, owner);
             const int osx0 = (int)(optx & 0xffffu) / kST, osy0 = (int)(opty & 0xffffu) / kST;
             const int ow = (int)(optx >> 16) / kST - osx0 + 1;
             // q / ow without an integer division: (q + 0.5) / ow is >= 0.5 / ow away from an
             // integer and the float error of (q + 0.5) * rcp(ow) is below (q + 0.5) 2^-21 / ow,
             // so truncation is exact for q < 2^20 (q < n_st here)
             const int qy = __float2int_rz(((float)q + 0.5f) * __fdividef(1.0f, (float)ow));
-            const int esx = osx0 + (q - qy * ow);
-            const int esy = osy0 + qy;
-            const int st = esy * st_x + esx;
+            esx = osx0 + (q - qy * ow);
+            esy = osy0 + qy;
+            st = esy * st_x + esx;
+        };
+        int st = 0, esx = 0, esy = 0;
+        uint32_t optx = 0, opty = 0, ogid = 0;
+        if (total > 0) locate(0, st, optx, opty, ogid, esx, esy);
+        for (int e0 = 0; e0 < total; e0 += 32) {
+            const bool valid = e0 + lane < total;
             const unsigned grp = __match_any_sync(0xffffffffu, valid ? st : -1);
             const int leader = __ffs(grp) - 1;
             uint32_t base = 0;
@@ -220,6 +227,11 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
                 base = s_run[st];
                 s_run[st] = base + (uint32_t)__popc(grp);
             }
+            // software pipelining: the next window's entries are located (shuffles only) while
+            // this window's shared-memory update is in flight
+            int st_n = 0, esx_n = 0, esy_n = 0;
+            uint32_t optx_n = 0, opty_n = 0, ogid_n = 0;
+            if (e0 + 32 < total) locate(e0 + 32, st_n, optx_n, opty_n, ogid_n, esx_n, esy_n);
             base = __shfl_sync(0xffffffffu, base, leader);
             if (valid) {
                 const uint32_t o = base + __popc(grp & lt);
@@ -228,6 +240,12 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
                                                 (int)(opty >> 16), esx, esy);
             }
             __syncwarp();
+            st = st_n;
+            esx = esx_n;
+            esy = esy_n;
+            optx = optx_n;
+            opty = opty_n;
+            ogid = ogid_n;
         }
     }
     if (!EMIT) {
