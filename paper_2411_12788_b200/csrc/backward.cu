@@ -338,16 +338,20 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
         if (lane == 0) loss_partials[bid] = ws;
     }
     if (COMPACT) {  // tile-list positions -> positions in the block's staged list (bidx increases)
-        __shared__ uint32_t s_bidx[kBlockList];
-        for (int i = lane; i < bcnt; i += 32) s_bidx[i] = bidx[i];
-        __syncwarp();
+        // (the few blocks with more than kBlockListSmem staged entries search bidx in global memory)
+        __shared__ uint32_t s_bidx[kBlockListSmem];
+        const bool in_smem = bcnt <= kBlockListSmem;
+        if (in_smem) {
+            for (int i = lane; i < bcnt; i += 32) s_bidx[i] = bidx[i];
+            __syncwarp();
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (P[h].last < 0) continue;
             int lo = 0, hi = bcnt - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if ((int)s_bidx[mid] <= P[h].last) lo = mid;
+                if ((int)(in_smem ? s_bidx[mid] : __ldg(bidx + mid)) <= P[h].last) lo = mid;
                 else hi = mid - 1;
             }
             P[h].last = lo;

@@ -147,7 +147,8 @@ struct FwdOutputs {
     uint32_t* bidx;
     int32_t* bcount;
 };
-constexpr int kBlockList = 512;
+constexpr int kBlockList = 2048;      // replay-list capacity per 8 x 8 block
+constexpr int kBlockListSmem = 512;   // entries the backward maps through shared memory
 
 // K6 (+K7 depth epilogue): per-tile front-to-back blend.
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
