@@ -930,7 +930,8 @@ int ORACLE_FN(visibility_mask)(const float* importance, int32_t n, double keep_q
     }
     if (any_pos) {
         float tau;
-        int rc = ORACLE_FN(quantile_threshold)(importance, pos, n, keep_q, &tau, NULL);
+        /* visibility.cpp:23: quantile_threshold(positive, float(keep_q)) */
+        int rc = ORACLE_FN(quantile_threshold)(importance, pos, n, (double)(float)keep_q, &tau, NULL);
         if (rc) {
             free(pos);
             return rc;
@@ -977,7 +978,8 @@ int ORACLE_FN(identify_critical)(const splat_gaussians* g, const float* best, co
         return 0;
     }
     float tau;
-    int rc = ORACLE_FN(quantile_threshold)(best, ever, n, keep_q, &tau, NULL);
+    /* densify.cpp:63: quantile_threshold(candidate_weights, float(keep_q)) */
+    int rc = ORACLE_FN(quantile_threshold)(best, ever, n, (double)(float)keep_q, &tau, NULL);
     if (rc) {
         free(ever);
         return rc;

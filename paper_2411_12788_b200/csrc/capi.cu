@@ -107,7 +107,7 @@ struct FwdState {
     uint64_t n_pairs = 0;
     bool pairs_in_alt = false;
     float bg[3] = {0, 0, 0};
-    const float* g_centers = nullptr;  // identity of the inputs (reuse check)
+    splat_gaussians g{};               // identity of the inputs (reuse check: every pointer, n, SH degree)
     const uint8_t* mask = nullptr;
     const uint32_t* order = nullptr;  // survivors in (depth, index) order (device)
     const uint32_t* blist = nullptr;  // per-block staged lists of the forward (or null)
@@ -463,12 +463,20 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     fo.bcount = nullptr;
     if (block_lists && n > 0) {
         const size_t n_blocks = (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8);
-        CK(ctx->blist.ensure(n_blocks * kBlockList * 4), "alloc block lists");
-        CK(ctx->bidx.ensure(n_blocks * kBlockList * 4), "alloc block lists");
-        fo.bidx = ctx->bidx.as<uint32_t>();
-        CK(ctx->bcount.ensure(n_blocks * 4), "alloc block counts");
-        fo.blist = ctx->blist.as<uint32_t>();
-        fo.bcount = ctx->bcount.as<int32_t>();
+        // the replay lists are an optimisation (8 B per staged entry, up to kBlockList per block):
+        // when they do not fit in HBM the backward re-culls the tile lists instead of failing
+        cudaError_t e = ctx->blist.ensure(n_blocks * kBlockList * 4);
+        if (e == cudaSuccess) e = ctx->bidx.ensure(n_blocks * kBlockList * 4);
+        if (e == cudaSuccess) e = ctx->bcount.ensure(n_blocks * 4);
+        if (e == cudaSuccess) {
+            fo.blist = ctx->blist.as<uint32_t>();
+            fo.bidx = ctx->bidx.as<uint32_t>();
+            fo.bcount = ctx->bcount.as<int32_t>();
+        } else if (e == cudaErrorMemoryAllocation) {
+            (void)cudaGetLastError();  // not sticky: clear it and take the re-cull path
+        } else {
+            CK(e, "alloc block lists");
+        }
     }
     // the gradient zero-fill of a following backward may start here: it then overlaps the blend
     // kernels (issue-bound) rather than the latency-bound sort and binning
@@ -489,7 +497,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     st.n_pairs = n_pairs;
     st.pairs_in_alt = pairs_alt;
     std::memcpy(st.bg, bg, sizeof(st.bg));
-    st.g_centers = g->centers;
+    st.g = *g;
     st.mask = mask;
     st.color = color_out;
     st.alpha = fo.alpha;
@@ -615,13 +623,21 @@ uint32_t read_u32(splat_ctx* ctx, const uint32_t* dev, int* rc) {
     return v;
 }
 
-bool state_matches(const splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const uint8_t* mask,
-                   const float bg[3]) {
+bool state_matches(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                   const uint8_t* mask, const float bg[3]) {
     const FwdState& st = ctx->st;
-    if (!st.valid || st.n != g->n || st.g_centers != g->centers || st.mask != mask) return false;
-    if (st.cp.width != cam->width || st.cp.height != cam->height) return false;
-    if (std::memcmp(st.cp.R, cam->rotation, sizeof(st.cp.R)) || std::memcmp(st.cp.t, cam->translation, sizeof(st.cp.t)))
+    if (!st.valid || st.mask != mask || !cam || !cfg) return false;
+    const splat_gaussians& a = st.g;
+    if (a.n != g->n || a.active_sh_degree != g->active_sh_degree || a.centers != g->centers ||
+        a.log_scales != g->log_scales || a.rotations != g->rotations || a.opacity_logits != g->opacity_logits ||
+        a.sh != g->sh)
         return false;
+    // the full camera and raster config, through the same derived parameters the forward used
+    CamParams cp;
+    const std::string saved_err = ctx->err;
+    const bool ok = make_params(ctx, cam, cfg, &cp) == SPLAT_OK;
+    ctx->err = saved_err;
+    if (!ok || std::memcmp(&cp, &st.cp, sizeof(cp))) return false;
     return st.bg[0] == bg[0] && st.bg[1] == bg[1] && st.bg[2] == bg[2];
 }
 
@@ -865,7 +881,7 @@ int splat_render_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_
     if (!d_color) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward: dLoss/dColor shape mismatch");
     const float zero[3] = {0, 0, 0};
     const float* bg = background ? background : zero;
-    if (!(reuse_forward && state_matches(ctx, g, cam, mask, bg))) {
+    if (!(reuse_forward && state_matches(ctx, g, cam, cfg, mask, bg))) {
         if ((rc = run_forward(ctx, g, cam, cfg, mask, bg, nullptr, nullptr))) return rc;
     }
     return run_backward(ctx, g, cam, cfg, d_color, nullptr, mask, bg, grads, accumulate, nullptr);
@@ -893,7 +909,7 @@ int splat_render_backward_l1(splat_ctx* ctx, const splat_gaussians* g, const spl
     if (!target) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward_l1: target missing");
     const float zero[3] = {0, 0, 0};
     const float* bg = background ? background : zero;
-    if (!state_matches(ctx, g, cam, mask, bg))
+    if (!state_matches(ctx, g, cam, cfg, mask, bg))
         return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "render_backward_l1: needs a preceding splat_render on the same inputs");
     return run_backward(ctx, g, cam, cfg, nullptr, target, mask, bg, grads, accumulate, loss);
 }
@@ -1122,6 +1138,7 @@ int splat_quantile_threshold_f64(splat_ctx* ctx, const double* values, const uin
 }
 
 int splat_visibility_mask(splat_ctx* ctx, const float* importance, int32_t n, double keep_q, uint8_t* mask) {
+    keep_q = (double)(float)keep_q;  // visibility.cpp:23 passes float(keep_q) to quantile_threshold
     if (!ctx || n < 0 || (n > 0 && (!importance || !mask)))
         return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "visibility_mask: bad args");
     if (n == 0) return SPLAT_OK;
@@ -1152,6 +1169,7 @@ int splat_visibility_mask(splat_ctx* ctx, const float* importance, int32_t n, do
 int splat_identify_critical(splat_ctx* ctx, const splat_gaussians* g, const float* best, const int64_t* max_count,
                             const double* summed, int criterion, double keep_q, const double* random,
                             uint8_t* critical, int32_t* count_out) {
+    keep_q = (double)(float)keep_q;  // densify.cpp:63 passes float(keep_q) to quantile_threshold
     if (!ctx || !g || !critical || !count_out || !best || !max_count)
         return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "identify_critical: bad args");
     if (criterion < SPLAT_CRITERION_RANDOM || criterion > SPLAT_CRITERION_MAX_WEIGHT)
@@ -1302,7 +1320,7 @@ int splat_render_backward_photometric(splat_ctx* ctx, const splat_gaussians* g, 
     if (!target) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "render_backward_photometric: target missing");
     const float zero[3] = {0, 0, 0};
     const float* bg = background ? background : zero;
-    if (!state_matches(ctx, g, cam, mask, bg))
+    if (!state_matches(ctx, g, cam, cfg, mask, bg))
         return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE,
                        "render_backward_photometric: needs a preceding splat_render on the same inputs");
     const int w = ctx->st.cp.width, h = ctx->st.cp.height;
@@ -1422,14 +1440,6 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         // the staging slots are free once everything already queued on the compute stream ran
         CK(cudaEventRecord(ctx->ev_free, s), "record");
         CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_free, 0), "wait");
-        // the first copies are issued from inside the first view's forward, once its blend
-        // forward is queued (a bulk H2D in flight delays the launches of the kernels before it)
-        ctx->post_forward_hook = [&, n_views]() -> int {
-            int r;
-            for (int k = 0; k < std::min(n_views, slots); ++k)
-                if ((r = issue_copy(k))) return r;
-            return SPLAT_OK;
-        };
     }
     // views alternate between this context and its twin (own stream and buffers) so that one
     // view's latency-bound preprocess / sort / binning overlaps the other's blend kernels; the
@@ -1448,6 +1458,21 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         CK(cudaEventRecord(ctx->ev_step, s), "record step");
         CK(cudaStreamWaitEvent(tw->stream, ctx->ev_step, 0), "twin start");
         ctx->twin_member = tw->twin_member = true;
+    }
+    // the hook captures this frame's locals by reference: it must never outlive the call
+    struct HookGuard {
+        splat_ctx* c;
+        ~HookGuard() { c->post_forward_hook = nullptr; }
+    } hook_guard{ctx};
+    if (targets_on_host) {
+        // the first copies are issued from inside the first view's forward, once its blend
+        // forward is queued (a bulk H2D in flight delays the launches of the kernels before it)
+        ctx->post_forward_hook = [&, n_views]() -> int {
+            int r;
+            for (int k = 0; k < std::min(n_views, slots); ++k)
+                if ((r = issue_copy(k))) return r;
+            return SPLAT_OK;
+        };
     }
     cudaEvent_t prev_chain = nullptr;
     auto fail = [&](splat_ctx* c, int r) {

@@ -190,3 +190,19 @@ CONFIGS = {
 
 def default_raster_config(**kw) -> RasterConfig:
     return RasterConfig(**kw)
+
+
+def grid_gaussians(count: int, seed: int = 0, extent: float = 1.5, log_scale: float = math.log(0.01)) -> GaussianSet:
+    """`count` small, non-overlapping Gaussians on a square grid in the z = 0 plane (test scenes whose
+    visible / max-contributor count is exactly `count` from `fov_camera(..., (0, 0, -3))`)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    side = int(math.ceil(math.sqrt(count)))
+    u = np.linspace(-extent, extent, side)
+    gx, gy = np.meshgrid(u, u)
+    s = GaussianSet.empty(count)
+    s.centers[:, 0] = gx.ravel()[:count]
+    s.centers[:, 1] = gy.ravel()[:count]
+    s.log_scales[:] = np.float32(log_scale)
+    s.opacity_logits[:] = rng.uniform(-2.0, 3.0, count).astype(np.float32)
+    s.sh[:, :3] = rng.normal(0.0, 0.5, (count, 3)).astype(np.float32)
+    return s

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import capi
 from .capi import Camera, RasterConfig
-from .rasterizer import Context, DeviceGaussians, DeviceGrads, OptimState, _torch
+from .rasterizer import Context, DeviceGaussians, DeviceGrads, LogicError, OptimState, _torch
 
 
 def views_for(step: int, rank: int, world: int, views_per_rank: int, ring: int) -> list[int]:
@@ -87,6 +87,12 @@ class ViewTrainer:
         cam_arr = (Camera * v)(*cams)
         tp = (C.c_void_p * v)(*ptrs)
         t = C.c_int32(self.opt.t)
+        n = self.params.n
+        if self.opt.n != n:  # optimizer.cpp:42-43
+            raise LogicError("ViewTrainer: optimizer rows out of sync with the parameter set (remap the moments)")
+        if self.grads.n != n:  # the set was densified / pruned: the gradient buffer follows its size
+            self.grads = DeviceGrads(n, self.ctx.device)
+            self._gr = self.grads.struct()
         key = (self.params.centers.data_ptr(), self.params.sh.data_ptr(), self.params.n, self.params.active_sh_degree,
                self.opt.m.data_ptr())
         if key != getattr(self, "_ckey", None):  # ctypes views of the parameter / moment buffers

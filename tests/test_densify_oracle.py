@@ -81,6 +81,30 @@ def test_identify_critical_with_visibility_masks(oracle, ref, scene):
     assert got_n == want_n and np.array_equal(got, want)
 
 
+def test_float_keep_q_1001_candidates(oracle, ref):
+    """visibility.cpp:23 / densify.cpp:63 narrow keep_q to float before the quantile: with 1001
+    positives and keep_q = 0.99 the lower order statistic is 9 (float) rather than 10 (double)."""
+    s = scenes.grid_gaussians(1001, seed=5)
+    # eleven faint Gaussians ~25 % apart at the bottom of the order, so the two candidate order
+    # statistics (9 vs 10) interpolate to visibly different thresholds
+    s.opacity_logits[:11] = np.linspace(-5.0, -2.5, 11, dtype=np.float32)
+    s.opacity_logits[11:] = np.abs(s.opacity_logits[11:]) + 0.5
+    cam = scenes.fov_camera(256, 256, 60.0, (0.0, 0.0, -3.0))
+    imp = oracle.render(s, cam)["importance"]
+    assert int((imp > 0).sum()) == 1001
+    want = ref.build_masks(s, [cam], 0.99)[0]
+    got = oracle.visibility_mask(imp, 0.99)
+    assert np.array_equal(got, want)
+    v = np.sort(imp[imp > 0])
+    assert want.sum() == int((imp > _np_quantile(v, float(np.float32(0.99)))).sum())
+    assert want.sum() != int((imp > _np_quantile(v, 0.99)).sum())  # the narrowing matters here
+    wc, wn = ref.identify_critical_views(s, [cam], CRITERIA["max-weight"], 0.99)
+    best, cnt, summed = oracle.view_statistics(s, [cam])
+    assert int((cnt > 0).sum()) == 1001
+    gc, gn = oracle.identify_critical(s, best, cnt, summed, CRITERIA["max-weight"], 0.99)
+    assert gn == wn and np.array_equal(gc, wc)
+
+
 def test_aggressive_clone_pinned(oracle, ref, scene):
     s, _ = scene
     rng = np.random.default_rng(3)

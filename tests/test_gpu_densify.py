@@ -43,6 +43,21 @@ def test_quantile_threshold_matches_oracle(oracle):
         D.quantile_threshold(_cuda(np.ones(4, np.float32)), 0.0)
 
 
+def test_float_keep_q_1001_candidates(oracle, ref):
+    """keep_q is narrowed to float before the quantile (visibility.cpp:23, densify.cpp:63): 1001
+    positives / candidates at keep_q = 0.99 take order statistic 9, not 10."""
+    s = scenes.grid_gaussians(1001, seed=5)
+    s.opacity_logits[:11] = np.linspace(-5.0, -2.5, 11, dtype=np.float32)
+    s.opacity_logits[11:] = np.abs(s.opacity_logits[11:]) + 0.5
+    cam = scenes.fov_camera(256, 256, 60.0, (0.0, 0.0, -3.0))
+    want = ref.build_masks(s, [cam], 0.99)[0]
+    assert_bitwise(D.build_masks(s, [cam], 0.99)[0].cpu().numpy(), want, "mask, 1001 positives")
+    wc, wn = ref.identify_critical_views(s, [cam], CRITERIA["max-weight"], 0.99)
+    gc, gn = D.identify_critical(s, [cam], "max-weight", 0.99)
+    assert gn == wn
+    assert_bitwise(gc.cpu().numpy(), wc, "critical, 1001 candidates")
+
+
 def test_build_masks(oracle, ref, scene):
     s, cams = scene
     # the mask kernel on identical importances is bit-exact

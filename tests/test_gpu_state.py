@@ -90,3 +90,52 @@ def test_overlapped_multi_view_step_host_targets(oracle, lam):
     # values agree to the oracle's own summation error, the gradients are the strict check
     assert np.allclose(loss, want, rtol=1e-4 if lam == 0 else 1e-3, atol=1e-7)
     assert_grads_close(tr.grads.to_host(), unpack_grads(flat, s.n), what=f"10-view summed grads (lambda {lam})")
+
+
+def test_reuse_forward_requires_identical_inputs(oracle):
+    """render_backward(reuse_forward = 1) / the fused L1 backward reuse the preceding forward only
+    when every input matches: the full camera, the raster config, every parameter pointer and the
+    SH degree.  Otherwise the fused call reports SPLAT_ERR_NO_FORWARD_STATE and the
+    reuse call re-renders (its gradients equal a fresh backward)."""
+    import ctypes as C
+    import torch
+    s = scenes.make_gaussians(3000, seed=4)
+    cam = scenes.fov_camera(96, 80, 60.0, (0.0, 0.0, -3.0))
+    ctx = R.Context.default()
+    ds = R.DeviceGaussians.from_host(s)
+    tgt = torch.zeros(cam.height, cam.width, 3, device="cuda")
+    g = R.DeviceGrads(s.n)
+    loss = torch.zeros(1, device="cuda")
+
+    def fused(cam_, cfg_, ds_):
+        ctx.bind_stream()
+        return ctx.lib.splat_render_backward_l1(ctx.h, C.byref(ds_.struct()), C.byref(cam_), C.byref(cfg_), tgt.data_ptr(),
+                                                None, R._bg((0, 0, 0)), C.byref(g.struct()), 0, loss.data_ptr())
+
+    base = RasterConfig()
+    R.render(ds, cam, base)
+    assert fused(cam, base, ds) == 0
+    variants = []
+    c2 = scenes.fov_camera(96, 80, 60.0, (0.0, 0.0, -3.0))
+    c2.fx *= 1.01
+    variants.append((c2, base, ds))
+    c3 = scenes.fov_camera(96, 80, 60.0, (0.0, 0.0, -3.0))
+    c3.cx += 0.5
+    variants.append((c3, base, ds))
+    cfg2 = RasterConfig()
+    cfg2.contribution_min = 2.0 / 255.0
+    variants.append((cam, cfg2, ds))
+    cfg3 = RasterConfig()
+    cfg3.tile_size = 32
+    variants.append((cam, cfg3, ds))
+    ds2 = R.DeviceGaussians.from_host(s)
+    ds2.active_sh_degree = 1
+    variants.append((cam, base, ds2))
+    for k, (c_, f_, d_) in enumerate(variants):
+        R.render(ds, cam, base)
+        assert fused(c_, f_, d_) == capi.SPLAT_ERR_NO_FORWARD_STATE, k
+    # reuse_forward with a changed camera re-renders: equal to a fresh backward on that camera
+    want = oracle.render_backward(s, c2, np.ones((80, 96, 3), np.float32), base)
+    R.render(ds, cam, base)
+    got = R.render_backward(ds, c2, base, torch.ones(80, 96, 3, device="cuda"), reuse_forward=True).to_host()
+    assert_grads_close(got, want, what="reuse after a camera change")
