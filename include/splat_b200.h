@@ -354,6 +354,46 @@ int splat_aggressive_clone(splat_ctx* ctx, const splat_params_mut* p, int64_t ca
 int splat_importance_prune(splat_ctx* ctx, const double* importance_dev, int32_t n, double keep_q, int32_t* kept_dev,
                            int32_t* n_kept);
 
+/* ---- the reference's random draws (include/splat_rng.h; host side, no device work) ---------
+ * splat_rng is a std::mt19937 (densify.cpp:35, 134, 198: the trainer's engine passed by
+ * reference): create it from a seed, or move a caller's engine in and out with the state words
+ * libstdc++ streams (operator<< / >>: x[0..623] then the index _M_p), so a C++ caller's
+ * std::mt19937& advances exactly as the reference's call would advance it. */
+typedef struct splat_rng splat_rng;
+int splat_rng_create(uint32_t seed, splat_rng** out);
+void splat_rng_destroy(splat_rng* rng);
+int splat_rng_get_state(const splat_rng* rng, uint32_t words_out[625]);
+int splat_rng_set_state(splat_rng* rng, const uint32_t words[625]);
+/* identify_critical's Random scores (densify.cpp:78-80): n uniform doubles in [0, 1) from rng,
+ * written to out (host or device pointer: out_on_device selects). */
+int splat_random_scores(splat_ctx* ctx, splat_rng* rng, int32_t n, double* out, int out_on_device);
+/* depth_reinitialize's sample draw (densify.cpp:227-235): the first `take` entries of a partial
+ * Fisher-Yates over [0, pool) with uniform_int_distribution<int> on rng -> idx_dev[take]. */
+int splat_pool_sample(splat_ctx* ctx, splat_rng* rng, int32_t pool, int32_t take, int32_t* idx_dev);
+
+/* importance_sample (simplify.cpp:36-92): target_count rows drawn without replacement with
+ * probability proportional to importance_dev (fp64) by Efraimidis-Spirakis keys log(u)/w from
+ * std::mt19937_64(seed) (u drawn on the host, keys + the 64-bit stable sort on the device, ties by
+ * index); non-positive weights only fill a deficit (uniform partial Fisher-Yates over them, in
+ * index order); no positive weight: a uniform draw.  kept_dev = ascending indices, *n_kept =
+ * target_count.  SPLAT_ERR_INVALID_ARGUMENT when target_count is outside [1, n]. */
+int splat_importance_sample(splat_ctx* ctx, const double* importance_dev, int32_t n, int32_t target_count,
+                            uint64_t seed, int32_t* kept_dev, int32_t* n_kept);
+
+/* vanilla_clone_split + apply_densify_plan, Progressive mode (densify.cpp:132-163, 182-191).
+ * Rows of `in` with grad2d_count > 0 and grad2d_accum / count > grad_threshold are cloned when
+ * max(exp(log_scale)) <= scale_threshold * scene_extent, else split: two children at centre +
+ * R(q) (exp(log_scale) .* n), n ~ N(0, I3) from rng (normal_distribution<float>, drawn on the host
+ * in the reference's order), log-scales - log(1.6).  `out` (capacity rows, must not alias `in`)
+ * receives the kept rows (split rows removed) in index order, then the new rows in index order;
+ * moment_source_dev[*n_out]: old row for kept rows, -1 for new rows.  *n_clone / *n_split may be
+ * NULL.  SPLAT_ERR_INVALID_ARGUMENT when capacity is too small (*n_out = rows needed, rng and
+ * out untouched). */
+int splat_vanilla_clone_split(splat_ctx* ctx, const splat_gaussians* in, const float* grad2d_accum_dev,
+                              const int32_t* grad2d_count_dev, float grad_threshold, float scale_threshold,
+                              float scene_extent, splat_rng* rng, const splat_params_mut* out, int64_t capacity,
+                              int32_t* moment_source_dev, int32_t* n_out, int32_t* n_clone, int32_t* n_split);
+
 /* Row gather: dst[r][c] = src[source[r]][c] for r < n_rows, c < width; source[r] < 0 gives a zero
  * row (OptimState::remap, optimizer.cpp:73-108; GaussianSet::select, gaussian_set.hpp:96-110).
  * src and dst must not overlap. */

@@ -590,6 +590,83 @@ int ref_depth_reinitialize_views(const splat_gaussians* g, const splat_camera* c
     REF_CATCH
 }
 
+// ---- the reference's random draws and the draw-consuming §8f functions ---------------------
+// std::normal_distribution<float>(0, 1) on a fresh std::mt19937(seed), one distribution object
+// (the draws vanilla_clone_split makes, densify.cpp:141, 154).
+int ref_rng_normal_f32(uint32_t seed, int32_t n, float* out) {
+    std::mt19937 rng(seed);
+    std::normal_distribution<float> gauss(0.f, 1.f);
+    for (int i = 0; i < n; ++i) out[i] = gauss(rng);
+    return 0;
+}
+
+// uniform_real_distribution<double> / uniform_int_distribution<int>(lo[i], hi[i]) interleaved on a
+// fresh std::mt19937_64(seed): kinds[i] = 0 real, 1 int (the engine importance_sample uses).
+int ref_rng_mixed_64(uint64_t seed, int32_t n, const int32_t* kinds, const int32_t* lo, const int32_t* hi,
+                     double* out) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    for (int i = 0; i < n; ++i) {
+        if (kinds[i] == 0) {
+            out[i] = u(rng);
+        } else {
+            std::uniform_int_distribution<int> pick(lo[i], hi[i]);
+            out[i] = pick(rng);
+        }
+    }
+    return 0;
+}
+
+// importance_sample (simplify.cpp:36-92): kept indices (ascending), target_count of them.
+int ref_importance_sample_set(const splat_gaussians* g, const double* importance, int32_t target, uint64_t seed,
+                              int32_t* kept, int32_t* n_kept) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    std::vector<double> imp(importance, importance + g->n);
+    const SimplifyResult r = importance_sample(set, imp, target, seed);
+    for (size_t k = 0; k < r.kept.size(); ++k) kept[k] = r.kept[k];
+    *n_kept = static_cast<int32_t>(r.kept.size());
+    return 0;
+    REF_CATCH
+}
+
+// vanilla_clone_split + apply_densify_plan (densify.cpp:132-195, Progressive mode) with a fresh
+// std::mt19937(seed): the resulting set (capacity rows), moment sources, clone / split counts.
+int ref_vanilla_clone_split_apply(const splat_gaussians* g, const float* grad2d_accum, const int32_t* grad2d_count,
+                                  float grad_threshold, float scale_threshold, float scene_extent, uint32_t seed,
+                                  float* centers, float* log_scales, float* rotations, float* opacity_logits, float* sh,
+                                  int64_t capacity, int32_t* moment_source, int32_t* n_out, int32_t* n_clone,
+                                  int32_t* n_split) {
+    REF_TRY
+    const GaussianSet set = to_set(g);
+    ParamGrads<float> grads;
+    grads.resize_zero(g->n);
+    for (int i = 0; i < g->n; ++i) {
+        grads.grad2d_accum[i] = grad2d_accum[i];
+        grads.grad2d_count[i] = grad2d_count[i];
+    }
+    std::mt19937 rng(seed);
+    const DensifyPlan plan = vanilla_clone_split(set, grads, grad_threshold, scale_threshold, scene_extent, rng);
+    const DensifyApplied out = apply_densify_plan(set, plan);
+    const int m = out.set.size();
+    *n_out = m;
+    *n_clone = static_cast<int32_t>(plan.clone_indices.size());
+    *n_split = static_cast<int32_t>(plan.split_indices.size());
+    if (m > capacity) throw std::invalid_argument("vanilla_clone_split: capacity too small");
+    for (int i = 0; i < m; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            centers[3 * i + c] = out.set.centers[i][c];
+            log_scales[3 * i + c] = out.set.log_scales[i][c];
+        }
+        for (int c = 0; c < 4; ++c) rotations[4 * i + c] = out.set.rotations[i][c];
+        opacity_logits[i] = out.set.opacity_logits[i];
+        moment_source[i] = out.moment_source[i];
+    }
+    if (m > 0) std::memcpy(sh, out.set.sh.data(), sizeof(float) * 48 * static_cast<size_t>(m));
+    return 0;
+    REF_CATCH
+}
+
 // ---- PLY checkpoints (ply_io.cpp) ------------------------------------------------------
 int ref_write_ply(const char* path, const splat_gaussians* g) {
     REF_TRY

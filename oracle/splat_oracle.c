@@ -25,6 +25,9 @@
 #define LOG splat_logf
 #endif
 
+#define SPLAT_RNG_LOGF LOG
+#include "splat_rng.h"
+
 static char g_err[256];
 static int fail(int code, const char* msg) {
     snprintf(g_err, sizeof g_err, "%s", msg);
@@ -1064,6 +1067,201 @@ int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep
     for (int32_t i = 0; i < n; ++i)
         if (!any || importance[i] > tau) kept[k++] = i;
     *n_kept = k;
+    return 0;
+}
+
+/* ---- the reference's random draws (include/splat_rng.h) and their consumers -------------- */
+/* std::normal_distribution<float>(0, 1) on std::mt19937(seed), one distribution object. */
+int ORACLE_FN(rng_normal_f32)(uint32_t seed, int32_t n, float* out) {
+    splat_mt19937 g;
+    splat_normal_f32 d = {0.0f, 0};
+    splat_mt19937_seed(&g, seed);
+    for (int32_t i = 0; i < n; ++i) out[i] = splat_normal_f32_next(&d, &g, 0.0f, 1.0f);
+    return 0;
+}
+
+/* kinds[i] = 0: uniform_real_distribution<double>(0, 1), 1: uniform_int_distribution<int>(lo, hi),
+ * interleaved on one std::mt19937_64(seed). */
+int ORACLE_FN(rng_mixed_64)(uint64_t seed, int32_t n, const int32_t* kinds, const int32_t* lo, const int32_t* hi,
+                            double* out) {
+    splat_mt19937_64 g;
+    splat_mt19937_64_seed(&g, seed);
+    for (int32_t i = 0; i < n; ++i)
+        out[i] = kinds[i] == 0 ? splat_canonical_f64_64(&g) : (double)splat_uniform_int_64(&g, lo[i], hi[i]);
+    return 0;
+}
+
+/* std::uniform_real_distribution<double>(0, 1) on std::mt19937(seed) (densify.cpp:78-80). */
+int ORACLE_FN(rng_uniform_f64_32)(uint32_t seed, int32_t n, double* out) {
+    splat_mt19937 g;
+    splat_mt19937_seed(&g, seed);
+    for (int32_t i = 0; i < n; ++i) out[i] = splat_canonical_f64_32(&g);
+    return 0;
+}
+
+/* depth_reinitialize's pool draw (densify.cpp:227-235) from std::mt19937(seed). */
+int ORACLE_FN(rng_fisher_yates)(uint32_t seed, int32_t pool, int32_t take, int32_t* idx_out) {
+    splat_mt19937 g;
+    splat_mt19937_seed(&g, seed);
+    int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(pool > 0 ? pool : 1));
+    splat_partial_fisher_yates(&g, idx, pool, take);
+    memcpy(idx_out, idx, sizeof(int32_t) * (size_t)take);
+    free(idx);
+    return 0;
+}
+
+typedef struct {
+    double key;
+    int32_t idx;
+} keyed_t;
+static int cmp_keyed(const void* a, const void* b) { /* simplify.cpp:72-75: key desc, index asc */
+    const keyed_t* x = (const keyed_t*)a;
+    const keyed_t* y = (const keyed_t*)b;
+    if (x->key != y->key) return x->key > y->key ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+static int cmp_i32(const void* a, const void* b) {
+    const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* importance_sample (simplify.cpp:36-92): Efraimidis-Spirakis keys log(u)/w on std::mt19937_64(seed),
+ * the target_count largest (ties by index), a uniform filler from the zero-weight rows, or a
+ * uniform draw when no weight is positive; kept ascending. */
+int ORACLE_FN(importance_sample)(const double* importance, int32_t n, int32_t target, uint64_t seed, int32_t* kept,
+                                 int32_t* n_kept) {
+    if (target < 1 || target > n) return fail(SPLAT_ERR_INVALID_ARGUMENT, "importance_sample: target_count out of range");
+    splat_mt19937_64 g;
+    splat_mt19937_64_seed(&g, seed);
+    keyed_t* keyed = (keyed_t*)malloc(sizeof(keyed_t) * (size_t)n);
+    int32_t* zero = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t nk = 0, nz = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        double u = splat_canonical_f64_64(&g);
+        if (u < 1e-300) u = 1e-300; /* std::max(u, 1e-300) */
+        if (importance[i] > 0.0) {
+            keyed[nk].key = log(u) / importance[i];
+            keyed[nk].idx = i;
+            ++nk;
+        } else {
+            zero[nz++] = i;
+        }
+    }
+    int32_t k = 0;
+    if (nk == 0) {
+        int32_t* idx = zero; /* every row has zero weight: idx = 0..n-1 */
+        for (int32_t i = 0; i < n; ++i) idx[i] = i;
+        for (int32_t r = 0; r < target; ++r) {
+            const int32_t j = splat_uniform_int_64(&g, r, n - 1);
+            const int32_t t = idx[r];
+            idx[r] = idx[j];
+            idx[j] = t;
+        }
+        for (int32_t r = 0; r < target; ++r) kept[k++] = idx[r];
+    } else {
+        const int32_t from_weighted = target < nk ? target : nk;
+        qsort(keyed, (size_t)nk, sizeof(keyed_t), cmp_keyed);
+        for (int32_t r = 0; r < from_weighted; ++r) kept[k++] = keyed[r].idx;
+        int32_t deficit = target - from_weighted;
+        for (int32_t r = 0; deficit > 0; --deficit, ++r) {
+            const int32_t j = splat_uniform_int_64(&g, r, nz - 1);
+            const int32_t t = zero[r];
+            zero[r] = zero[j];
+            zero[j] = t;
+            kept[k++] = zero[r];
+        }
+    }
+    qsort(kept, (size_t)k, sizeof(int32_t), cmp_i32);
+    *n_kept = k;
+    free(keyed);
+    free(zero);
+    return 0;
+}
+
+/* vanilla_clone_split + apply_densify_plan, Progressive mode (densify.cpp:132-163, 182-195): rows
+ * whose mean 2D gradient exceeds grad_threshold are cloned (max scale <= scale_threshold * extent)
+ * or split into two children at centre + R(q) (s .* n), n ~ N(0, I) from std::mt19937(seed),
+ * log-scales - log(1.6).  Output: the kept rows in index order, then the new rows in index order;
+ * moment_source = old row for kept rows, -1 for new rows. */
+int ORACLE_FN(vanilla_clone_split)(const splat_gaussians* g, const float* grad2d_accum, const int32_t* grad2d_count,
+                                   float grad_threshold, float scale_threshold, float scene_extent, uint32_t seed,
+                                   float* centers, float* log_scales, float* rotations, float* opacity_logits,
+                                   float* sh, int64_t capacity, int32_t* moment_source, int32_t* n_out,
+                                   int32_t* n_clone, int32_t* n_split) {
+    const int32_t n = g->n;
+    uint8_t* kind = (uint8_t*)malloc((size_t)(n > 0 ? n : 1));
+    int32_t nc = 0, ns = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        kind[i] = 0;
+        if (grad2d_count[i] <= 0) continue;
+        const float avg = grad2d_accum[i] / (float)grad2d_count[i];
+        if (avg <= grad_threshold) continue;
+        float sc[3];
+        for (int c = 0; c < 3; ++c) sc[c] = EXP(g->log_scales[3 * i + c]);
+        float mx = sc[0];
+        for (int c = 1; c < 3; ++c) mx = fmax_std(mx, sc[c]);
+        if (mx <= scale_threshold * scene_extent) {
+            kind[i] = 1;
+            ++nc;
+        } else {
+            kind[i] = 2;
+            ++ns;
+        }
+    }
+    const int64_t m = (int64_t)n - ns + nc + 2 * (int64_t)ns;
+    *n_out = (int32_t)m;
+    *n_clone = nc;
+    *n_split = ns;
+    if (m > capacity) {
+        free(kind);
+        return fail(SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: capacity too small");
+    }
+    int64_t r = 0;
+    for (int32_t i = 0; i < n; ++i) { /* kept rows (apply_densify_plan: select(keep)) */
+        if (kind[i] == 2) continue;
+        memcpy(centers + 3 * r, g->centers + 3 * (size_t)i, 12);
+        memcpy(log_scales + 3 * r, g->log_scales + 3 * (size_t)i, 12);
+        memcpy(rotations + 4 * r, g->rotations + 4 * (size_t)i, 16);
+        opacity_logits[r] = g->opacity_logits[i];
+        memcpy(sh + 48 * r, g->sh + 48 * (size_t)i, 192);
+        moment_source[r] = i;
+        ++r;
+    }
+    splat_mt19937 rng;
+    splat_normal_f32 gauss = {0.0f, 0};
+    splat_mt19937_seed(&rng, seed);
+    const float split_shift = LOG(1.6f);
+    for (int32_t i = 0; i < n; ++i) { /* plan.new_rows, appended in index order */
+        if (kind[i] == 0) continue;
+        const int children = kind[i] == 1 ? 1 : 2;
+        float rot[9], sc[3];
+        if (kind[i] == 2) {
+            rotation_from_quat(g->rotations + 4 * (size_t)i, rot);
+            for (int c = 0; c < 3; ++c) sc[c] = EXP(g->log_scales[3 * i + c]);
+        }
+        for (int child = 0; child < children; ++child) {
+            memcpy(centers + 3 * r, g->centers + 3 * (size_t)i, 12);
+            memcpy(log_scales + 3 * r, g->log_scales + 3 * (size_t)i, 12);
+            memcpy(rotations + 4 * r, g->rotations + 4 * (size_t)i, 16);
+            opacity_logits[r] = g->opacity_logits[i];
+            memcpy(sh + 48 * r, g->sh + 48 * (size_t)i, 192);
+            moment_source[r] = -1;
+            if (kind[i] == 2) {
+                float nv[3], v[3];
+                /* Vec3f n(gauss(rng), gauss(rng), gauss(rng)): GCC evaluates the three arguments
+                 * right to left (pinned against the reference build) */
+                nv[2] = splat_normal_f32_next(&gauss, &rng, 0.0f, 1.0f);
+                nv[1] = splat_normal_f32_next(&gauss, &rng, 0.0f, 1.0f);
+                nv[0] = splat_normal_f32_next(&gauss, &rng, 0.0f, 1.0f);
+                for (int c = 0; c < 3; ++c) v[c] = sc[c] * nv[c];
+                for (int c = 0; c < 3; ++c)
+                    centers[3 * r + c] = g->centers[3 * (size_t)i + c] + dot3(&rot[3 * c], v);
+                for (int c = 0; c < 3; ++c) log_scales[3 * r + c] = g->log_scales[3 * (size_t)i + c] - split_shift;
+            }
+            ++r;
+        }
+    }
+    free(kind);
     return 0;
 }
 

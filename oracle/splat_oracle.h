@@ -116,6 +116,20 @@ int ORACLE_FN(reinit_gaussians)(const float* points, const float* colors, int32_
                                 float* log_scales, float* rotations, float* opacity_logits, float* sh);
 
 /* The exp the library was built with (splat_expf or glibc expf). */
+/* The reference's random draws (include/splat_rng.h) and the §8f functions that consume them
+ * (oracle_ restatement; the ref_ build exports its own wrappers in ref_capi.cpp). */
+int ORACLE_FN(rng_normal_f32)(uint32_t seed, int32_t n, float* out);
+int ORACLE_FN(rng_mixed_64)(uint64_t seed, int32_t n, const int32_t* kinds, const int32_t* lo, const int32_t* hi,
+                            double* out);
+int ORACLE_FN(rng_uniform_f64_32)(uint32_t seed, int32_t n, double* out);
+int ORACLE_FN(rng_fisher_yates)(uint32_t seed, int32_t pool, int32_t take, int32_t* idx_out);
+int ORACLE_FN(importance_sample)(const double* importance, int32_t n, int32_t target, uint64_t seed, int32_t* kept,
+                                 int32_t* n_kept);
+int ORACLE_FN(vanilla_clone_split)(const splat_gaussians* g, const float* grad2d_accum, const int32_t* grad2d_count,
+                                   float grad_threshold, float scale_threshold, float scene_extent, uint32_t seed,
+                                   float* centers, float* log_scales, float* rotations, float* opacity_logits,
+                                   float* sh, int64_t capacity, int32_t* moment_source, int32_t* n_out,
+                                   int32_t* n_clone, int32_t* n_split);
 float ORACLE_FN(exp)(float x);
 
 #ifdef __cplusplus

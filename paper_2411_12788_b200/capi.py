@@ -239,6 +239,18 @@ _EXPORTS = {
     "splat_importance_prune": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
                                          C.POINTER(C.c_int32)]),
     "splat_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "splat_rng_create": (C.c_int, [C.c_uint32, C.POINTER(C.c_void_p)]),
+    "splat_rng_destroy": (None, [C.c_void_p]),
+    "splat_rng_get_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "splat_rng_set_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "splat_random_scores": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int]),
+    "splat_pool_sample": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "splat_importance_sample": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p,
+                                          C.POINTER(C.c_int32)]),
+    "splat_vanilla_clone_split": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.c_void_p, C.c_void_p, C.c_float,
+                                            C.c_float, C.c_float, C.c_void_p, C.POINTER(ParamsMut), C.c_int64,
+                                            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                            C.POINTER(C.c_int32)]),
     "splat_ssim": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                              C.c_void_p]),
     "splat_photometric_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "splat_b200.h"
+#include "splat_rng.h"
 
 using namespace splat_b200;
 
@@ -708,7 +709,70 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     return SPLAT_OK;
 }
 
+// Scratch for sort_u64_pairs over n entries: keys lo in dkey[0], hi in dhi, vals in dval[0].
+int ensure_u64_sort(splat_ctx* ctx, int n) {
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    for (int k = 0; k < 2; ++k) {
+        CK(ctx->dkey[k].ensure(nn * 4), "alloc keys");
+        CK(ctx->dval[k].ensure(nn * 4), "alloc vals");
+    }
+    CK(ctx->dhi.ensure(nn * 4), "alloc keys");
+    CK(ctx->dflags.ensure(nn * 4), "alloc flags");
+    CK(ctx->doffsets.ensure((nn + 1) * 4), "alloc offsets");
+    CK(ctx->dscalar.ensure(64), "alloc scalar");
+    CK(ctx->hist.ensure(radix_hist_words(nn, 8) * 4), "alloc hist");
+    CK(ctx->scan_tmp.ensure((scan_temp_words(std::max(nn, radix_hist_words(nn, 8))) + 64) * 4), "alloc scan");
+    return SPLAT_OK;
+}
+
+// Stable ascending sort of n (hi:lo, val) pairs by the 64-bit key: LSD over the low word, then the
+// high word gathered into the new order.  *sorted_vals = the values in key order.
+int sort_u64_pairs(splat_ctx* ctx, int n, const uint32_t** sorted_vals) {
+    LaunchCtx& lc = ctx->lc;
+    const size_t nn = (size_t)n;
+    uint32_t* hi = ctx->dhi.as<uint32_t>();
+    bool a1 = false;
+    CK(radix_sort_pairs(lc, ctx->dkey[0].as<uint32_t>(), ctx->dval[0].as<uint32_t>(), ctx->dkey[1].as<uint32_t>(),
+                        ctx->dval[1].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(),
+                        &a1),
+       "sort lo");
+    const int a = a1 ? 1 : 0;
+    CK(launch_gather_u32(lc, hi, ctx->dval[a].as<uint32_t>(), n, ctx->dkey[a].as<uint32_t>()), "gather hi");
+    bool a2 = false;
+    CK(radix_sort_pairs(lc, ctx->dkey[a].as<uint32_t>(), ctx->dval[a].as<uint32_t>(), ctx->dkey[1 - a].as<uint32_t>(),
+                        ctx->dval[1 - a].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(),
+                        ctx->scan_tmp.as<uint32_t>(), &a2),
+       "sort hi");
+    *sorted_vals = ctx->dval[a2 ? 1 - a : a].as<uint32_t>();
+    return SPLAT_OK;
+}
+
+// Exclusive scan of n flags into offsets; *total = the flag sum (read back: a host branch).
+int scan_count(splat_ctx* ctx, const uint32_t* flags, uint32_t* offsets, int n, uint32_t* total) {
+    CK(ctx->scan_tmp.ensure((scan_temp_words((uint64_t)(n > 0 ? n : 1)) + 64) * 4), "alloc scan");
+    CK(ctx->dscalar.ensure(64), "alloc scalar");
+    CK(exclusive_scan_u32(ctx->lc, flags, offsets, (uint64_t)n, ctx->scan_tmp.as<uint32_t>(),
+                          ctx->dscalar.as<uint32_t>()),
+       "scan");
+    int rc = 0;
+    *total = read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
+    return rc;
+}
+
+// Host -> device copy of a host vector, complete on return (the vector may then go away).
+template <typename T>
+int upload(splat_ctx* ctx, const std::vector<T>& v, T* dst) {
+    if (v.empty()) return SPLAT_OK;
+    CK(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "upload");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    return SPLAT_OK;
+}
+
 }  // namespace
+
+struct splat_rng {
+    splat_mt19937 g;
+};
 
 extern "C" {
 
@@ -1208,32 +1272,14 @@ int splat_identify_critical(splat_ctx* ctx, const splat_gaussians* g, const floa
     }
     // score order, descending, ties by index (densify.cpp:96-101): stable LSD over the 64-bit
     // inverted keys (low word, then high word)
-    LaunchCtx& lc = ctx->lc;
-    const size_t nn = (size_t)n;
-    for (int k = 0; k < 2; ++k) {
-        CK(ctx->dkey[k].ensure(nn * 4), "alloc");
-        CK(ctx->dval[k].ensure(nn * 4), "alloc");
-    }
-    CK(ctx->dhi.ensure(nn * 4), "alloc");
-    uint32_t* hi = ctx->dhi.as<uint32_t>();
-    CK(launch_score_keys(lc, criterion, g->opacity_logits, summed, random, n, ctx->dkey[0].as<uint32_t>(), hi,
-                         ctx->dval[0].as<uint32_t>()),
+    if ((rc = ensure_u64_sort(ctx, n))) return rc;
+    CK(launch_score_keys(ctx->lc, criterion, g->opacity_logits, summed, random, n, ctx->dkey[0].as<uint32_t>(),
+                         ctx->dhi.as<uint32_t>(), ctx->dval[0].as<uint32_t>()),
        "score keys");
-    bool a1 = false;
-    CK(radix_sort_pairs(lc, ctx->dkey[0].as<uint32_t>(), ctx->dval[0].as<uint32_t>(), ctx->dkey[1].as<uint32_t>(),
-                        ctx->dval[1].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(), ctx->scan_tmp.as<uint32_t>(),
-                        &a1),
-       "sort lo");
-    const int a = a1 ? 1 : 0;
-    CK(launch_gather_u32(lc, hi, ctx->dval[a].as<uint32_t>(), n, ctx->dkey[a].as<uint32_t>()), "gather hi");
-    bool a2 = false;
-    CK(radix_sort_pairs(lc, ctx->dkey[a].as<uint32_t>(), ctx->dval[a].as<uint32_t>(), ctx->dkey[1 - a].as<uint32_t>(),
-                        ctx->dval[1 - a].as<uint32_t>(), nn, 0, 32, ctx->hist.as<uint32_t>(),
-                        ctx->scan_tmp.as<uint32_t>(), &a2),
-       "sort hi");
-    const int fin = a2 ? 1 - a : a;
+    const uint32_t* order = nullptr;
+    if ((rc = sort_u64_pairs(ctx, n, &order))) return rc;
     CK(cudaMemsetAsync(critical, 0, (size_t)n, ctx->stream), "zero critical");
-    CK(launch_mark_first(lc, ctx->dval[fin].as<uint32_t>(), count, critical), "mark");
+    CK(launch_mark_first(ctx->lc, order, count, critical), "mark");
     return SPLAT_OK;
 }
 
@@ -1282,6 +1328,185 @@ int splat_importance_prune(splat_ctx* ctx, const double* importance, int32_t n, 
     CK(launch_compact_index(ctx->lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), n, kept), "compact");
     *n_kept = (int32_t)read_u32(ctx, ctx->dscalar.as<uint32_t>(), &rc);
     return rc;
+}
+
+// ---- the reference's random draws (host side) -------------------------------------------------
+int splat_rng_create(uint32_t seed, splat_rng** out) {
+    if (!out) return SPLAT_ERR_INVALID_ARGUMENT;
+    splat_rng* r = new (std::nothrow) splat_rng;
+    if (!r) return SPLAT_ERR_OUT_OF_MEMORY;
+    splat_mt19937_seed(&r->g, seed);
+    *out = r;
+    return SPLAT_OK;
+}
+
+void splat_rng_destroy(splat_rng* rng) { delete rng; }
+
+int splat_rng_get_state(const splat_rng* rng, uint32_t words_out[625]) {
+    if (!rng || !words_out) return SPLAT_ERR_INVALID_ARGUMENT;
+    std::memcpy(words_out, rng->g.x, sizeof(rng->g.x));
+    words_out[624] = rng->g.p;
+    return SPLAT_OK;
+}
+
+int splat_rng_set_state(splat_rng* rng, const uint32_t words[625]) {
+    if (!rng || !words || words[624] > 624) return SPLAT_ERR_INVALID_ARGUMENT;
+    std::memcpy(rng->g.x, words, sizeof(rng->g.x));
+    rng->g.p = words[624];
+    return SPLAT_OK;
+}
+
+int splat_random_scores(splat_ctx* ctx, splat_rng* rng, int32_t n, double* out, int out_on_device) {
+    if (!rng || n < 0 || (n > 0 && !out) || (out_on_device && !ctx))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "random_scores: bad args");
+    std::vector<double> v((size_t)n);
+    for (int32_t i = 0; i < n; ++i) v[i] = splat_canonical_f64_32(&rng->g);  // densify.cpp:78-80
+    if (!out_on_device) {
+        if (n) std::memcpy(out, v.data(), v.size() * sizeof(double));
+        return SPLAT_OK;
+    }
+    return upload(ctx, v, out);
+}
+
+int splat_pool_sample(splat_ctx* ctx, splat_rng* rng, int32_t pool, int32_t take, int32_t* idx_dev) {
+    if (!ctx || !rng || pool < 0 || take < 0 || take > pool || (take > 0 && !idx_dev))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "pool_sample: bad args");
+    std::vector<int32_t> idx((size_t)pool);
+    splat_partial_fisher_yates(&rng->g, idx.data(), pool, take);  // densify.cpp:227-235
+    idx.resize((size_t)take);
+    return upload(ctx, idx, idx_dev);
+}
+
+int splat_importance_sample(splat_ctx* ctx, const double* importance, int32_t n, int32_t target_count, uint64_t seed,
+                            int32_t* kept, int32_t* n_kept) {
+    if (!ctx || !n_kept || n < 0 || (n > 0 && (!importance || !kept)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "importance_sample: bad args");
+    *n_kept = 0;
+    if (target_count < 1 || target_count > n)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "importance_sample: target_count out of range");
+    // simplify.cpp:44-58: u_i from std::mt19937_64(seed) in index order, log(max(u, 1e-300)) on the
+    // host (the reference's libm log); the keys log(u)/w are formed on the device
+    splat_mt19937_64 g;
+    splat_mt19937_64_seed(&g, seed);
+    std::vector<double> logu((size_t)n);
+    for (int32_t i = 0; i < n; ++i) logu[i] = std::log(std::max(splat_canonical_f64_64(&g), 1e-300));
+    int rc = ensure_u64_sort(ctx, n);
+    if (rc) return rc;
+    CK(ctx->ssim_tmp.ensure((size_t)n * 8 + (size_t)n), "alloc sample scratch");
+    double* dlogu = ctx->ssim_tmp.as<double>();
+    uint8_t* sel = reinterpret_cast<uint8_t*>(dlogu + n);
+    if ((rc = upload(ctx, logu, dlogu))) return rc;
+    uint32_t* zero_flags = ctx->dflags.as<uint32_t>();
+    CK(launch_sample_keys(ctx->lc, importance, dlogu, n, ctx->dkey[0].as<uint32_t>(), ctx->dhi.as<uint32_t>(),
+                          ctx->dval[0].as<uint32_t>(), zero_flags),
+       "sample keys");
+    uint32_t nz = 0;
+    if ((rc = scan_count(ctx, zero_flags, ctx->doffsets.as<uint32_t>(), n, &nz))) return rc;
+    const int32_t nk = n - (int32_t)nz;
+    CK(cudaMemsetAsync(sel, 0, (size_t)n, ctx->stream), "zero selection");
+    std::vector<int32_t> picked;  // host-drawn rows (uniform fallback / zero-weight filler)
+    if (nk == 0) {
+        // simplify.cpp:63-70: no positive weight -> uniform partial Fisher-Yates over all rows
+        std::vector<int32_t> idx((size_t)n);
+        for (int32_t i = 0; i < n; ++i) idx[i] = i;
+        for (int32_t r = 0; r < target_count; ++r) std::swap(idx[r], idx[splat_uniform_int_64(&g, r, n - 1)]);
+        picked.assign(idx.begin(), idx.begin() + target_count);
+    } else {
+        // simplify.cpp:71-76: the from_weighted largest keys (descending, ties by index)
+        const int32_t from_weighted = std::min(target_count, nk);
+        const uint32_t* order = nullptr;
+        if ((rc = sort_u64_pairs(ctx, n, &order))) return rc;
+        CK(launch_mark_first(ctx->lc, order, from_weighted, sel), "mark weighted");
+        const int32_t deficit = target_count - from_weighted;
+        if (deficit > 0) {
+            // simplify.cpp:77-83: filler from the zero-weight rows (index order), partial Fisher-Yates
+            CK(ctx->dkey[1].ensure((size_t)nz * 4 + 4), "alloc zero rows");
+            int32_t* zrows = ctx->dkey[1].as<int32_t>();
+            CK(launch_compact_index(ctx->lc, zero_flags, ctx->doffsets.as<uint32_t>(), n, zrows), "zero rows");
+            std::vector<int32_t> zero((size_t)nz);
+            CK(cudaMemcpyAsync(zero.data(), zrows, (size_t)nz * 4, cudaMemcpyDeviceToHost, ctx->stream), "read zero rows");
+            CK(cudaStreamSynchronize(ctx->stream), "sync");
+            for (int32_t r = 0; r < deficit; ++r) {
+                std::swap(zero[r], zero[splat_uniform_int_64(&g, r, (int32_t)nz - 1)]);
+                picked.push_back(zero[r]);
+            }
+        }
+    }
+    if (!picked.empty()) {
+        CK(ctx->dhi.ensure(picked.size() * 4 + 4), "alloc picks");
+        if ((rc = upload(ctx, picked, ctx->dhi.as<int32_t>()))) return rc;
+        CK(launch_mark_list(ctx->lc, ctx->dhi.as<int32_t>(), (int)picked.size(), sel), "mark picks");
+    }
+    // kept = selected rows, ascending (simplify.cpp:86)
+    CK(launch_flags_from_bytes(ctx->lc, sel, n, ctx->dflags.as<uint32_t>()), "flags");
+    uint32_t total = 0;
+    if ((rc = scan_count(ctx, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), n, &total))) return rc;
+    CK(launch_compact_index(ctx->lc, ctx->dflags.as<uint32_t>(), ctx->doffsets.as<uint32_t>(), n, kept), "compact");
+    *n_kept = (int32_t)total;
+    if (total != (uint32_t)target_count) return set_err(ctx, SPLAT_ERR_LOGIC, "importance_sample: selection size");
+    return SPLAT_OK;
+}
+
+int splat_vanilla_clone_split(splat_ctx* ctx, const splat_gaussians* in, const float* grad2d_accum,
+                              const int32_t* grad2d_count, float grad_threshold, float scale_threshold,
+                              float scene_extent, splat_rng* rng, const splat_params_mut* out, int64_t capacity,
+                              int32_t* moment_source, int32_t* n_out, int32_t* n_clone, int32_t* n_split) {
+    if (!ctx || !in || !out || !rng || !n_out) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: bad args");
+    int rc = check_set(ctx, in);
+    if (rc) return rc;
+    const int n = in->n;
+    *n_out = n;
+    if (n_clone) *n_clone = 0;
+    if (n_split) *n_split = 0;
+    if (n > 0 && (!grad2d_accum || !grad2d_count))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: gradient rows mismatch");
+    if (n == 0) return SPLAT_OK;
+    if (!out->centers || !out->log_scales || !out->rotations || !out->opacity_logits || !out->sh)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: output arrays missing");
+    const size_t nn = (size_t)n;
+    // flag / offset arrays: keep, fresh (new rows per row), split rank
+    CK(ctx->ssim_tmp.ensure(nn * 4 * 6), "alloc split scratch");
+    uint32_t* keep = ctx->ssim_tmp.as<uint32_t>();
+    uint32_t* fresh = keep + nn;
+    uint32_t* split = fresh + nn;
+    uint32_t* keep_off = split + nn;
+    uint32_t* fresh_off = keep_off + nn;
+    uint32_t* split_off = fresh_off + nn;
+    // scale_threshold * scene_extent: one float product (densify.cpp:146)
+    volatile float limit = scale_threshold * scene_extent;
+    CK(launch_vcs_classify(ctx->lc, in->log_scales, grad2d_accum, grad2d_count, n, grad_threshold, limit, keep, fresh,
+                           split),
+       "classify");
+    uint32_t n_keep = 0, n_new = 0, ns = 0;
+    if ((rc = scan_count(ctx, keep, keep_off, n, &n_keep))) return rc;
+    if ((rc = scan_count(ctx, fresh, fresh_off, n, &n_new))) return rc;
+    if ((rc = scan_count(ctx, split, split_off, n, &ns))) return rc;
+    const int64_t m = (int64_t)n_keep + n_new;
+    *n_out = (int32_t)m;
+    if (n_clone) *n_clone = (int32_t)(n_new - 2 * ns);
+    if (n_split) *n_split = (int32_t)ns;
+    if (m > capacity) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: capacity too small");
+    // the split normals, in the reference's draw order (one normal_distribution per call)
+    std::vector<float> normals((size_t)ns * 6);
+    splat_normal_f32 gauss = {0.0f, 0};
+    for (auto& v : normals) v = splat_normal_f32_next(&gauss, &rng->g, 0.0f, 1.0f);
+    CK(ctx->d_color_buf.ensure(normals.size() * 4 + 4), "alloc normals");
+    if ((rc = upload(ctx, normals, ctx->d_color_buf.as<float>()))) return rc;
+    CK(ctx->dval[0].ensure((size_t)m * 4), "alloc sources");
+    int32_t* src = ctx->dval[0].as<int32_t>();
+    CK(launch_vcs_sources(ctx->lc, keep, keep_off, fresh, fresh_off, n, (int)n_keep, src, moment_source), "sources");
+    // GaussianSet::select(keep) + append(new_rows): one row gather per parameter group
+    const struct {
+        const float* s;
+        float* d;
+        int w;
+    } groups[5] = {{in->centers, out->centers, 3}, {in->log_scales, out->log_scales, 3}, {in->rotations, out->rotations, 4},
+                   {in->opacity_logits, out->opacity_logits, 1}, {in->sh, out->sh, 48}};
+    for (const auto& gr : groups) CK(launch_gather_rows(ctx->lc, gr.s, gr.w, src, (int)m, gr.d), "gather rows");
+    CK(launch_vcs_split(ctx->lc, *in, fresh, fresh_off, split_off, ctx->d_color_buf.as<float>(), (int)n_keep,
+                        splat_logf(1.6f), out->centers, out->log_scales),
+       "split children");
+    return SPLAT_OK;
 }
 
 int splat_gather_rows(splat_ctx* ctx, const float* src, int32_t width, const int32_t* source, int32_t n_rows,

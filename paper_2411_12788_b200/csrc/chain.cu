@@ -74,30 +74,6 @@ __device__ __forceinline__ void sh_basis_grad_all(float x, float y, float z, int
 #undef SET3
 }
 
-__device__ __forceinline__ void normalized_quat(float w, float x, float y, float z, float q[4]) {
-    const float n = sqrtf((w * w + x * x) + (y * y + z * z));
-    if (!(n > 0.0f)) {
-        q[0] = 1.0f; q[1] = q[2] = q[3] = 0.0f;
-        return;
-    }
-    q[0] = w / n; q[1] = x / n; q[2] = y / n; q[3] = z / n;
-}
-
-__device__ __forceinline__ void rotation_from_quat(const float qr[4], float r[9]) {
-    float q[4];
-    normalized_quat(qr[0], qr[1], qr[2], qr[3], q);
-    const float w = q[0], x = q[1], y = q[2], z = q[3];
-    r[0] = 1.0f - 2.0f * (y * y + z * z);
-    r[1] = 2.0f * (x * y - w * z);
-    r[2] = 2.0f * (x * z + w * y);
-    r[3] = 2.0f * (x * y + w * z);
-    r[4] = 1.0f - 2.0f * (x * x + z * z);
-    r[5] = 2.0f * (y * z - w * x);
-    r[6] = 2.0f * (x * z - w * y);
-    r[7] = 2.0f * (y * z + w * x);
-    r[8] = 1.0f - 2.0f * (x * x + y * y);
-}
-
 constexpr int kChainThreads = 128;
 constexpr int kShRow = 13;  // float4 per staged SH row (12 + 1 pad: conflict-free LDS/STS.128)
 

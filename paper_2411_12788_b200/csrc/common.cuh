@@ -41,6 +41,32 @@ struct __align__(16) AuxRec {
     float4 a0, a1, a2;
 };
 
+// normalized_quat / rotation_from_quat (gaussian_set.hpp:15-37) in the reference's operation
+// order; bit-exact only in translation units compiled with --fmad=false (chain.cu, densify.cu).
+__device__ __forceinline__ void normalized_quat(float w, float x, float y, float z, float q[4]) {
+    const float n = sqrtf((w * w + x * x) + (y * y + z * z));
+    if (!(n > 0.0f)) {
+        q[0] = 1.0f; q[1] = q[2] = q[3] = 0.0f;
+        return;
+    }
+    q[0] = w / n; q[1] = x / n; q[2] = y / n; q[3] = z / n;
+}
+
+__device__ __forceinline__ void rotation_from_quat(const float qr[4], float r[9]) {
+    float q[4];
+    normalized_quat(qr[0], qr[1], qr[2], qr[3], q);
+    const float w = q[0], x = q[1], y = q[2], z = q[3];
+    r[0] = 1.0f - 2.0f * (y * y + z * z);
+    r[1] = 2.0f * (x * y - w * z);
+    r[2] = 2.0f * (x * z + w * y);
+    r[3] = 2.0f * (x * y + w * z);
+    r[4] = 1.0f - 2.0f * (x * x + z * z);
+    r[5] = 2.0f * (y * z - w * x);
+    r[6] = 2.0f * (x * z - w * y);
+    r[7] = 2.0f * (y * z + w * x);
+    r[8] = 1.0f - 2.0f * (x * x + y * y);
+}
+
 // Camera + raster constants passed by value to kernels.
 struct CamParams {
     int width, height;

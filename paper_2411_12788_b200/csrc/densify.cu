@@ -193,6 +193,109 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, int width, con
     dst[t] = s >= 0 ? src[(int64_t)s * width + c] : 0.0f;
 }
 
+// importance_sample keys (simplify.cpp:51-58): key = log(u) / w for w > 0 (log(u) drawn on the
+// host), as a DESCENDING orderable 64-bit key; rows with w <= 0 (or NaN) get the all-ones key
+// (sorted after every keyed row) and a filler flag.
+__global__ void sample_keys_kernel(const double* __restrict__ imp, const double* __restrict__ logu, int n,
+                                   uint32_t* __restrict__ key_lo, uint32_t* __restrict__ key_hi,
+                                   uint32_t* __restrict__ vals, uint32_t* __restrict__ zero_flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double w = imp[i];
+    const bool keyed = w > 0.0;
+    const uint64_t k = keyed ? ~f64_key(__ddiv_rn(logu[i], w)) : ~0ull;
+    key_lo[i] = (uint32_t)k;
+    key_hi[i] = (uint32_t)(k >> 32);
+    vals[i] = (uint32_t)i;
+    zero_flags[i] = keyed ? 0u : 1u;
+}
+
+__global__ void mark_list_kernel(const int32_t* __restrict__ idx, int count, uint8_t* __restrict__ sel) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < count) sel[idx[r]] = 1;
+}
+
+// vanilla_clone_split classification (densify.cpp:142-149): 0 untouched, 1 clone, 2 split.
+// keep = not split; new rows = 1 (clone) / 2 (split); split rank flag.
+__global__ void vcs_classify_kernel(const float* __restrict__ log_scales, const float* __restrict__ accum,
+                                    const int32_t* __restrict__ count, int n, float grad_threshold,
+                                    float scale_limit, uint32_t* __restrict__ keep, uint32_t* __restrict__ fresh,
+                                    uint32_t* __restrict__ split) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int kind = 0;
+    const int c = count[i];
+    if (c > 0) {
+        const float avg = __fdiv_rn(accum[i], (float)c);
+        if (avg > grad_threshold) {
+            // Vec3f scale = exp(log_scales) (gaussian_set.hpp:84); maxCoeff as std::max in order
+            float m = splat_expf(log_scales[3 * i]);
+            const float s1 = splat_expf(log_scales[3 * i + 1]);
+            const float s2 = splat_expf(log_scales[3 * i + 2]);
+            m = m < s1 ? s1 : m;
+            m = m < s2 ? s2 : m;
+            kind = m <= scale_limit ? 1 : 2;
+        }
+    }
+    keep[i] = kind == 2 ? 0u : 1u;
+    fresh[i] = (uint32_t)kind;
+    split[i] = kind == 2 ? 1u : 0u;
+}
+
+// output row sources: kept rows in index order, then each clone's copy / split's two children
+__global__ void vcs_sources_kernel(const uint32_t* __restrict__ keep, const uint32_t* __restrict__ keep_off,
+                                   const uint32_t* __restrict__ fresh, const uint32_t* __restrict__ fresh_off,
+                                   int n, int n_keep, int32_t* __restrict__ src, int32_t* __restrict__ moment_source) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (keep[i]) {
+        src[keep_off[i]] = i;
+        if (moment_source) moment_source[keep_off[i]] = i;
+    }
+    const uint32_t f = fresh[i];
+    for (uint32_t c = 0; c < f; ++c) {
+        const size_t r = (size_t)n_keep + fresh_off[i] + c;
+        src[r] = i;
+        if (moment_source) moment_source[r] = -1;
+    }
+}
+
+// split children (densify.cpp:150-160): centre + R(q) (s .* n), log-scales - log(1.6); the
+// normals of split j arrive in draw order, three per child, and Vec3f n(g(), g(), g()) takes
+// them right to left (GCC's argument evaluation order, pinned against the reference build).
+__global__ void vcs_split_kernel(splat_gaussians in, const uint32_t* __restrict__ fresh,
+                                 const uint32_t* __restrict__ fresh_off, const uint32_t* __restrict__ split_rank,
+                                 const float* __restrict__ normals, int n_keep, float split_shift,
+                                 float* __restrict__ centers, float* __restrict__ log_scales) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= in.n || fresh[i] != 2) return;
+    float q[4], rot[9], sc[3], c0[3], ls[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = in.rotations[4 * (size_t)i + k];
+    rotation_from_quat(q, rot);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        ls[k] = in.log_scales[3 * (size_t)i + k];
+        sc[k] = splat_expf(ls[k]);
+        c0[k] = in.centers[3 * (size_t)i + k];
+    }
+    const float* nrm = normals + 6 * (size_t)split_rank[i];
+#pragma unroll
+    for (int child = 0; child < 2; ++child) {
+        const size_t r = (size_t)n_keep + fresh_off[i] + child;
+        float v[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = __fmul_rn(sc[k], nrm[3 * child + 2 - k]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float d = __fadd_rn(__fmul_rn(rot[3 * k], v[0]),
+                                      __fadd_rn(__fmul_rn(rot[3 * k + 1], v[1]), __fmul_rn(rot[3 * k + 2], v[2])));
+            centers[3 * r + k] = __fadd_rn(c0[k], d);
+            log_scales[3 * r + k] = __fsub_rn(ls[k], split_shift);
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_select_keys_f32(LaunchCtx& lc, const float* v, const uint8_t* sel, int n, const uint32_t* offsets,
@@ -319,6 +422,50 @@ cudaError_t launch_gather_rows(LaunchCtx& lc, const float* src, int width, const
     if (total == 0) return cudaSuccess;
     LaunchScope s(lc, "gather_rows");
     gather_rows_kernel<<<blocks_for(total, 256), 256, 0, lc.stream>>>(src, width, source, total, dst);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_keys(LaunchCtx& lc, const double* imp, const double* logu, int n, uint32_t* key_lo,
+                               uint32_t* key_hi, uint32_t* vals, uint32_t* zero_flags) {
+    if (n == 0) return cudaSuccess;
+    sample_keys_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(imp, logu, n, key_lo, key_hi, vals, zero_flags);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mark_list(LaunchCtx& lc, const int32_t* idx, int count, uint8_t* sel) {
+    if (count == 0) return cudaSuccess;
+    mark_list_kernel<<<blocks_for(count, 256), 256, 0, lc.stream>>>(idx, count, sel);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vcs_classify(LaunchCtx& lc, const float* log_scales, const float* accum, const int32_t* count,
+                                int n, float grad_threshold, float scale_limit, uint32_t* keep, uint32_t* fresh,
+                                uint32_t* split) {
+    if (n == 0) return cudaSuccess;
+    vcs_classify_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(log_scales, accum, count, n, grad_threshold,
+                                                                   scale_limit, keep, fresh, split);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vcs_sources(LaunchCtx& lc, const uint32_t* keep, const uint32_t* keep_off, const uint32_t* fresh,
+                               const uint32_t* fresh_off, int n, int n_keep, int32_t* src, int32_t* moment_source) {
+    if (n == 0) return cudaSuccess;
+    vcs_sources_kernel<<<blocks_for(n, 256), 256, 0, lc.stream>>>(keep, keep_off, fresh, fresh_off, n, n_keep, src,
+                                                                  moment_source);
+    lc.count++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vcs_split(LaunchCtx& lc, const splat_gaussians& in, const uint32_t* fresh, const uint32_t* fresh_off,
+                             const uint32_t* split_rank, const float* normals, int n_keep, float split_shift,
+                             float* centers, float* log_scales) {
+    if (in.n == 0) return cudaSuccess;
+    vcs_split_kernel<<<blocks_for(in.n, 256), 256, 0, lc.stream>>>(in, fresh, fresh_off, split_rank, normals, n_keep,
+                                                                    split_shift, centers, log_scales);
     lc.count++;
     return cudaGetLastError();
 }

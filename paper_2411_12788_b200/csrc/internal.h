@@ -230,6 +230,18 @@ cudaError_t launch_keep_flags(LaunchCtx& lc, const double* v, int n, double tau,
 cudaError_t launch_compact_index(LaunchCtx& lc, const uint32_t* flags, const uint32_t* offsets, int n, int32_t* out);
 cudaError_t launch_gather_rows(LaunchCtx& lc, const float* src, int width, const int32_t* source, int n_rows,
                                float* dst);
+// importance_sample (simplify.cpp:36-92) and vanilla_clone_split (densify.cpp:132-163)
+cudaError_t launch_sample_keys(LaunchCtx& lc, const double* imp, const double* logu, int n, uint32_t* key_lo,
+                               uint32_t* key_hi, uint32_t* vals, uint32_t* zero_flags);
+cudaError_t launch_mark_list(LaunchCtx& lc, const int32_t* idx, int count, uint8_t* sel);
+cudaError_t launch_vcs_classify(LaunchCtx& lc, const float* log_scales, const float* accum, const int32_t* count,
+                                int n, float grad_threshold, float scale_limit, uint32_t* keep, uint32_t* fresh,
+                                uint32_t* split);
+cudaError_t launch_vcs_sources(LaunchCtx& lc, const uint32_t* keep, const uint32_t* keep_off, const uint32_t* fresh,
+                               const uint32_t* fresh_off, int n, int n_keep, int32_t* src, int32_t* moment_source);
+cudaError_t launch_vcs_split(LaunchCtx& lc, const splat_gaussians& in, const uint32_t* fresh, const uint32_t* fresh_off,
+                             const uint32_t* split_rank, const float* normals, int n_keep, float split_shift,
+                             float* centers, float* log_scales);
 
 // ssim.cu: mean SSIM (lambda < 0) or the photometric loss into value_dev,
 // optional gradient; tmp = 3 w h ch floats when grad != null, partials = 2 ssim_partials_count.

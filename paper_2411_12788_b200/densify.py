@@ -130,6 +130,91 @@ def identify_critical(set_, cams: Sequence[capi.Camera], criterion="max-weight",
     return crit[:ds.n], count.value
 
 
+class Rng:
+    """The reference trainer's std::mt19937 (passed by reference to identify_critical,
+    vanilla_clone_split and depth_reinitialize), held by the library as a splat_rng: the draws
+    are the reference's own sequences (include/splat_rng.h)."""
+
+    def __init__(self, seed: int = 5489, ctx: Optional[Context] = None):
+        self.lib = (ctx or Context.default()).lib
+        h = C.c_void_p()
+        rc = self.lib.splat_rng_create(seed & 0xFFFFFFFF, C.byref(h))
+        if rc:
+            raise RuntimeError(f"splat_rng_create: status {rc}")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.splat_rng_destroy(self.h)
+            self.h = None
+
+    def state(self):
+        w = (C.c_uint32 * 625)()
+        self.lib.splat_rng_get_state(self.h, w)
+        return list(w)
+
+    def set_state(self, words) -> None:
+        w = (C.c_uint32 * 625)(*words)
+        if self.lib.splat_rng_set_state(self.h, w):
+            raise ValueError("splat_rng_set_state: bad state")
+
+
+def random_scores(rng: Rng, n: int, ctx: Optional[Context] = None):
+    """identify_critical's Random-criterion draws (densify.cpp:78-80) as a float64 CUDA tensor."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_random_scores(ctx.h, rng.h, n, out.data_ptr(), 1))
+    return out[:n]
+
+
+def importance_sample(params: DeviceGaussians, importance, target_count: int, seed: int,
+                      ctx: Optional[Context] = None):
+    """importance_sample (simplify.cpp:36-92) on a float64 CUDA importance tensor.  Returns
+    (kept DeviceGaussians, kept indices int32 CUDA tensor, ascending)."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    n = params.n
+    kept = torch.empty(max(n, 1), dtype=torch.int32, device=params.flat.device)
+    nk = C.c_int32()
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_importance_sample(ctx.h, importance.data_ptr(), n, int(target_count),
+                                              int(seed) & 0xFFFFFFFFFFFFFFFF, kept.data_ptr(), C.byref(nk)))
+    kept = kept[: nk.value]
+    return select(params, kept, ctx=ctx), kept
+
+
+def vanilla_clone_split(params: DeviceGaussians, grad2d_accum, grad2d_count, grad_threshold: float,
+                        scale_threshold: float, scene_extent: float, rng: Rng, ctx: Optional[Context] = None):
+    """vanilla_clone_split + apply_densify_plan (Progressive mode, densify.cpp:132-163, 182-191).
+    grad2d_accum / grad2d_count: the ParamGrads statistics (CUDA float32 / int32 [n]).  Returns
+    (new DeviceGaussians, moment_source int32 CUDA tensor, clones, splits); rng advances exactly
+    as the reference's std::mt19937 would."""
+    torch = _torch()
+    ctx = ctx or Context.default()
+    ctx.bind_stream()
+    ds, _ = _device_set(params, ctx.device)
+    g = ds.struct()
+    n_out, nc, ns = C.c_int32(), C.c_int32(), C.c_int32()
+    dev = f"cuda:{ctx.device}"
+    # sizing call: capacity 0 returns the row count without drawing or writing anything
+    probe = DeviceGaussians(0, ds.active_sh_degree, ctx.device)
+    rc = ctx.lib.splat_vanilla_clone_split(ctx.h, C.byref(g), grad2d_accum.data_ptr(), grad2d_count.data_ptr(),
+                                           grad_threshold, scale_threshold, scene_extent, rng.h, C.byref(probe.mut()),
+                                           0, None, C.byref(n_out), C.byref(nc), C.byref(ns))
+    if rc not in (0, capi.SPLAT_ERR_INVALID_ARGUMENT) or (rc and n_out.value == 0):
+        ctx.check(rc)
+    need = n_out.value
+    out = DeviceGaussians(need, ds.active_sh_degree, ctx.device)
+    ms = torch.empty(max(need, 1), dtype=torch.int32, device=dev)
+    ctx.check(ctx.lib.splat_vanilla_clone_split(ctx.h, C.byref(g), grad2d_accum.data_ptr(), grad2d_count.data_ptr(),
+                                                grad_threshold, scale_threshold, scene_extent, rng.h,
+                                                C.byref(out.mut()), need, ms.data_ptr(), C.byref(n_out),
+                                                C.byref(nc), C.byref(ns)))
+    return out, ms[:need], nc.value, ns.value
+
+
 def _grow(params: DeviceGaussians, capacity: int) -> DeviceGaussians:
     """Copy of params in a layout with room for `capacity` rows (first params.n rows filled)."""
     out = DeviceGaussians(capacity, params.active_sh_degree, params.flat.device.index or 0)
@@ -229,16 +314,16 @@ def third_neighbor_distances(points, min_dist: float = 1e-7, ctx: Optional[Conte
 
 def depth_reinitialize(set_, cams: Sequence[capi.Camera], images, sample_count: int, sample=None,
                        cfg: Optional[RasterConfig] = None, min_dist: float = 1e-7, ctx: Optional[Context] = None,
-                       generator=None) -> DeviceGaussians:
+                       rng: Optional[Rng] = None) -> DeviceGaussians:
     """depth_reinitialize (densify.cpp:198-252) on device: render each view, unproject every pixel
     with a max contributor (view-major, raster order = the reference's pool order), draw
     min(sample_count, pool) of them, and build the fresh set (3rd-NN isotropic scales, identity
     rotation, opacity 0.1, SH DC from the image colour).
 
     images: CUDA float32 [views, H, W, 3].  sample: optional CUDA int32 pool indices in draw
-    order (the reference draws them with a partial Fisher-Yates over its std::mt19937; its exact
-    sequence is libstdc++'s); default: a seeded uniform draw without replacement on device
-    (torch.randperm with `generator`).  Raises RuntimeError when no pixel has a valid depth
+    order; default: the reference's own draw, a partial Fisher-Yates with
+    uniform_int_distribution<int> over `rng` (a std::mt19937, default seed 5489), drawn by the
+    library (splat_pool_sample).  Raises RuntimeError when no pixel has a valid depth
     (densify.cpp:223-225)."""
     torch = _torch()
     from .rasterizer import depth_points
@@ -256,7 +341,9 @@ def depth_reinitialize(set_, cams: Sequence[capi.Camera], images, sample_count: 
         raise RuntimeError("depth_reinitialize: no valid depth pixels (model renders nothing)")
     take = min(sample_count, pool)
     if sample is None:
-        sample = torch.randperm(pool, device=pts.device, generator=generator)[:take].to(torch.int32)
+        sample = torch.empty(take, dtype=torch.int32, device=pts.device)
+        ctx.bind_stream()
+        ctx.check(ctx.lib.splat_pool_sample(ctx.h, (rng or Rng(ctx=ctx)).h, pool, take, sample.data_ptr()))
     sample = sample[:take].contiguous()
     hw = images.shape[1] * images.shape[2]
     # colour of each pooled point: row (view * HW + pixel) of the [views * HW, 3] image rows

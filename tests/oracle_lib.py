@@ -114,6 +114,21 @@ class OracleLib:
             getattr(L, p + "build_masks").argtypes = [G, CAM, C.c_int32, CFG, C.c_double, u8p]
             getattr(L, p + "importance_prune_set").argtypes = [G, dp, C.c_double, ip, ip]
 
+        dp = C.POINTER(C.c_double)
+        getattr(L, p + "rng_normal_f32").argtypes = [C.c_uint32, C.c_int32, fp]
+        getattr(L, p + "rng_mixed_64").argtypes = [C.c_uint64, C.c_int32, ip, ip, ip, dp]
+        if kind == "oracle":
+            getattr(L, p + "rng_uniform_f64_32").argtypes = [C.c_uint32, C.c_int32, dp]
+            getattr(L, p + "rng_fisher_yates").argtypes = [C.c_uint32, C.c_int32, C.c_int32, ip]
+            getattr(L, p + "importance_sample").argtypes = [dp, C.c_int32, C.c_int32, C.c_uint64, ip, ip]
+            getattr(L, p + "vanilla_clone_split").argtypes = [G, fp, ip, C.c_float, C.c_float, C.c_float, C.c_uint32,
+                                                              fp, fp, fp, fp, fp, C.c_int64, ip, ip, ip, ip]
+        else:
+            getattr(L, p + "importance_sample_set").argtypes = [G, dp, C.c_int32, C.c_uint64, ip, ip]
+            getattr(L, p + "vanilla_clone_split_apply").argtypes = [G, fp, ip, C.c_float, C.c_float, C.c_float,
+                                                                    C.c_uint32, fp, fp, fp, fp, fp, C.c_int64, ip, ip,
+                                                                    ip, ip]
+
     def fn(self, name):
         return getattr(self.lib, self.p + name)
 
@@ -442,3 +457,61 @@ class OracleLib:
                                                        _ptr(imgs), sample_count, seed, *[_ptr(a) for a in out],
                                                        C.byref(cnt)))
         return [a[: cnt.value] for a in out]
+
+    # ---- the reference's random draws and their §8f consumers ------------------------------
+    def rng_normal_f32(self, seed, n):
+        out = np.zeros(max(n, 1), np.float32)
+        self.check(self.fn("rng_normal_f32")(seed, n, _ptr(out)))
+        return out[:n]
+
+    def rng_mixed_64(self, seed, kinds, lo, hi):
+        k, l, h = (np.ascontiguousarray(a, np.int32) for a in (kinds, lo, hi))
+        out = np.zeros(max(k.size, 1), np.float64)
+        self.check(self.fn("rng_mixed_64")(seed, k.size, _ptr(k, ip), _ptr(l, ip), _ptr(h, ip),
+                                           _ptr(out, C.POINTER(C.c_double))))
+        return out[:k.size]
+
+    def rng_uniform_f64_32(self, seed, n):
+        if self.kind == "ref":
+            return self.random_scores(seed, n)
+        out = np.zeros(max(n, 1), np.float64)
+        self.check(self.fn("rng_uniform_f64_32")(seed, n, _ptr(out, C.POINTER(C.c_double))))
+        return out[:n]
+
+    def rng_fisher_yates(self, seed, pool, take):
+        out = np.zeros(max(take, 1), np.int32)
+        self.check(self.fn("rng_fisher_yates" if self.kind == "oracle" else "fisher_yates")(seed, pool, take,
+                                                                                              _ptr(out, ip)))
+        return out[:take]
+
+    def importance_sample(self, importance, target, seed, s=None):
+        imp = np.ascontiguousarray(importance, np.float64)
+        kept = np.zeros(max(imp.size, 1), np.int32)
+        nk = C.c_int32()
+        dp = C.POINTER(C.c_double)
+        if self.kind == "oracle":
+            self.check(self.fn("importance_sample")(_ptr(imp, dp), imp.size, target, seed, _ptr(kept, ip), C.byref(nk)))
+        else:
+            gv = GaussiansView(s)
+            self.check(self.fn("importance_sample_set")(C.byref(gv.struct), _ptr(imp, dp), target, seed, _ptr(kept, ip),
+                                                        C.byref(nk)))
+        return kept[:nk.value]
+
+    def vanilla_clone_split(self, s, grad2d_accum, grad2d_count, grad_threshold, scale_threshold, scene_extent, seed):
+        """Returns (GaussianSet after apply_densify_plan, moment_source, n_clone, n_split)."""
+        from paper_2411_12788_b200.scenes import GaussianSet
+        gv = GaussiansView(s)
+        acc = np.ascontiguousarray(grad2d_accum, np.float32)
+        cnt = np.ascontiguousarray(grad2d_count, np.int32)
+        cap = 3 * s.n + 1
+        out = GaussianSet.empty(cap, s.active_sh_degree)
+        ms = np.zeros(cap, np.int32)
+        no, nc, ns = C.c_int32(), C.c_int32(), C.c_int32()
+        name = "vanilla_clone_split" if self.kind == "oracle" else "vanilla_clone_split_apply"
+        self.check(self.fn(name)(C.byref(gv.struct), _ptr(acc), _ptr(cnt, ip), grad_threshold, scale_threshold,
+                                 scene_extent, seed, _ptr(out.centers), _ptr(out.log_scales), _ptr(out.rotations),
+                                 _ptr(out.opacity_logits), _ptr(out.sh), cap, _ptr(ms, ip), C.byref(no), C.byref(nc),
+                                 C.byref(ns)))
+        m = no.value
+        return out.select(np.arange(m)), ms[:m], nc.value, ns.value
+

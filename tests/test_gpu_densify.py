@@ -145,3 +145,84 @@ def test_importance_prune_select_and_remap(oracle, scene):
         assert_bitwise(new, exp.astype(np.float32), f"remapped moments width {w}")
         o_old += w * n_old
         o_new += w * n_new
+
+
+def test_rng_draws_match_reference(ref):
+    """splat_rng (std::mt19937 restated) draws the reference's Random scores and Fisher-Yates picks."""
+    for seed in (0, 17):
+        got = D.random_scores(D.Rng(seed), 5000).cpu().numpy()
+        assert np.array_equal(got, ref.random_scores(seed, 5000))
+    r = D.Rng(3)
+    a = D.random_scores(r, 700).cpu().numpy()
+    st = r.state()
+    b = D.random_scores(r, 900).cpu().numpy()
+    r2 = D.Rng(1)
+    r2.set_state(st)
+    assert np.array_equal(D.random_scores(r2, 900).cpu().numpy(), b)
+    assert np.array_equal(np.concatenate([a, b]), ref.random_scores(3, 1600))
+    from paper_2411_12788_b200.rasterizer import Context
+    ctx = Context.default()
+    out = torch.empty(2500, dtype=torch.int32, device="cuda")
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_pool_sample(ctx.h, D.Rng(9).h, 100_000, 2500, out.data_ptr()))
+    assert np.array_equal(out.cpu().numpy(), ref.fisher_yates(9, 100_000, 2500))
+
+
+def test_identify_critical_random_with_library_draws(ref, scene):
+    s, cams = scene
+    want, want_n = ref.identify_critical_views(s, cams, CRITERIA["random"], 0.6, seed=1234)
+    rnd = D.random_scores(D.Rng(1234), s.n)
+    got, got_n = D.identify_critical(s, cams, "random", 0.6, random_scores=rnd)
+    assert got_n == want_n
+    assert_bitwise(got.cpu().numpy(), want, "random-criterion selection")
+
+
+@pytest.mark.parametrize("case", ["mixed", "all_positive", "all_zero", "deficit", "ties"])
+def test_importance_sample_matches_reference(ref, case):
+    rng = np.random.default_rng(5)
+    n = 30_000
+    s = scenes.make_gaussians(n, seed=2)
+    imp = rng.gamma(0.5, 2.0, n)
+    targets = (1, 999, n)
+    if case == "mixed":
+        imp[rng.random(n) < 0.3] = 0.0
+        targets = (1, 17, 15_000, n)
+    elif case == "all_zero":
+        imp[:] = 0.0
+    elif case == "deficit":
+        imp[:] = 0.0
+        imp[rng.choice(n, 2000, replace=False)] = rng.random(2000) + 0.1
+        imp[5] = -1.0
+        targets = (1500, 2000, 2001, 20_000, n)
+    elif case == "ties":
+        imp = np.where(np.arange(n) % 3 == 0, 1.0, 2.0)
+        targets = (10, 10_000)
+    ds = DeviceGaussians.from_host(s)
+    for t in targets:
+        for seed in (0, 2**40 + 1):
+            kept_set, kept = D.importance_sample(ds, _cuda(imp), t, seed)
+            want = ref.importance_sample(imp, t, seed, s=s)
+            assert_bitwise(kept.cpu().numpy(), want, f"{case} target {t} seed {seed}")
+            assert kept_set.n == t
+    with pytest.raises(Exception):
+        D.importance_sample(ds, _cuda(imp), 0, 0)
+    with pytest.raises(Exception):
+        D.importance_sample(ds, _cuda(imp), n + 1, 0)
+
+
+@pytest.mark.parametrize("seed", [0, 7])
+def test_vanilla_clone_split_matches_reference(ref, seed):
+    rng = np.random.default_rng(seed)
+    n = 40_000
+    s = scenes.make_gaussians(n, seed=seed + 1)
+    cnt = rng.integers(0, 5, n).astype(np.int32)
+    acc = (rng.random(n) * 4e-4 * np.maximum(cnt, 1)).astype(np.float32)
+    ds = DeviceGaussians.from_host(s)
+    for thr, sthr, ext in ((2e-4, 0.01, 3.3), (0.0, 0.02, 1.0), (1.0, 0.01, 3.3)):
+        out, ms, nc, ns = D.vanilla_clone_split(ds, _cuda(acc), _cuda(cnt), thr, sthr, ext, D.Rng(seed))
+        want, wms, wc, ws = ref.vanilla_clone_split(s, acc, cnt, thr, sthr, ext, seed)
+        assert (nc, ns) == (wc, ws)
+        assert_bitwise(ms.cpu().numpy(), wms, "moment source")
+        got = out.to_host()
+        for k in ("centers", "log_scales", "rotations", "opacity_logits", "sh"):
+            assert_bitwise(getattr(got, k), getattr(want, k), f"{k} thr {thr}")

@@ -39,11 +39,14 @@ def test_depth_reinitialize_matches_reference(oracle, ref):
     want = ref.depth_reinitialize_views(s, cams, list(images), sample_count=900, seed=5)
     pool = sum(int((oracle.render(s, c)["max_contributor"] >= 0).sum()) for c in cams)
     idx = ref.fisher_yates(5, pool, min(900, pool))
-    fresh = D.depth_reinitialize(s, cams, torch.from_numpy(images).cuda(), 900,
-                                 sample=torch.from_numpy(idx).cuda()).to_host()
-    for a, b, name in zip((fresh.centers, fresh.log_scales, fresh.rotations, fresh.opacity_logits, fresh.sh), want,
-                          ("centers", "log_scales", "rotations", "opacity_logits", "sh")):
-        assert_bitwise(a, b, f"fresh {name}")
+    fed = D.depth_reinitialize(s, cams, torch.from_numpy(images).cuda(), 900,
+                               sample=torch.from_numpy(idx).cuda()).to_host()
+    # default draw: the library's own std::mt19937 partial Fisher-Yates (splat_pool_sample)
+    drawn = D.depth_reinitialize(s, cams, torch.from_numpy(images).cuda(), 900, rng=D.Rng(5)).to_host()
+    for fresh, how in ((fed, "fed the reference's draw"), (drawn, "library draw")):
+        for a, b, name in zip((fresh.centers, fresh.log_scales, fresh.rotations, fresh.opacity_logits, fresh.sh),
+                              want, ("centers", "log_scales", "rotations", "opacity_logits", "sh")):
+            assert_bitwise(a, b, f"fresh {name} ({how})")
     # a set that renders nothing: std::runtime_error in the reference (densify.cpp:223-225)
     empty = s.select(np.zeros(0, np.int64))
     with pytest.raises(RuntimeError):
