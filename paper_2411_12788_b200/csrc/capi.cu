@@ -1461,8 +1461,6 @@ int splat_vanilla_clone_split(splat_ctx* ctx, const splat_gaussians* in, const f
     if (n > 0 && (!grad2d_accum || !grad2d_count))
         return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: gradient rows mismatch");
     if (n == 0) return SPLAT_OK;
-    if (!out->centers || !out->log_scales || !out->rotations || !out->opacity_logits || !out->sh)
-        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: output arrays missing");
     const size_t nn = (size_t)n;
     // flag / offset arrays: keep, fresh (new rows per row), split rank
     CK(ctx->ssim_tmp.ensure(nn * 4 * 6), "alloc split scratch");
@@ -1486,6 +1484,8 @@ int splat_vanilla_clone_split(splat_ctx* ctx, const splat_gaussians* in, const f
     if (n_clone) *n_clone = (int32_t)(n_new - 2 * ns);
     if (n_split) *n_split = (int32_t)ns;
     if (m > capacity) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: capacity too small");
+    if (!out->centers || !out->log_scales || !out->rotations || !out->opacity_logits || !out->sh)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "vanilla_clone_split: output arrays missing");
     // the split normals, in the reference's draw order (one normal_distribution per call)
     std::vector<float> normals((size_t)ns * 6);
     splat_normal_f32 gauss = {0.0f, 0};

@@ -203,7 +203,8 @@ def vanilla_clone_split(params: DeviceGaussians, grad2d_accum, grad2d_count, gra
     rc = ctx.lib.splat_vanilla_clone_split(ctx.h, C.byref(g), grad2d_accum.data_ptr(), grad2d_count.data_ptr(),
                                            grad_threshold, scale_threshold, scene_extent, rng.h, C.byref(probe.mut()),
                                            0, None, C.byref(n_out), C.byref(nc), C.byref(ns))
-    if rc not in (0, capi.SPLAT_ERR_INVALID_ARGUMENT) or (rc and n_out.value == 0):
+    if rc not in (0, capi.SPLAT_ERR_INVALID_ARGUMENT) or (rc and "capacity" not in
+                                                            (ctx.lib.splat_last_error(ctx.h) or b"").decode()):
         ctx.check(rc)
     need = n_out.value
     out = DeviceGaussians(need, ds.active_sh_degree, ctx.device)
@@ -343,7 +344,8 @@ def depth_reinitialize(set_, cams: Sequence[capi.Camera], images, sample_count: 
     if sample is None:
         sample = torch.empty(take, dtype=torch.int32, device=pts.device)
         ctx.bind_stream()
-        ctx.check(ctx.lib.splat_pool_sample(ctx.h, (rng or Rng(ctx=ctx)).h, pool, take, sample.data_ptr()))
+        rng = rng or Rng(ctx=ctx)  # keep the engine alive across the call
+        ctx.check(ctx.lib.splat_pool_sample(ctx.h, rng.h, pool, take, sample.data_ptr()))
     sample = sample[:take].contiguous()
     hw = images.shape[1] * images.shape[2]
     # colour of each pooled point: row (view * HW + pixel) of the [views * HW, 3] image rows

@@ -164,7 +164,8 @@ def test_rng_draws_match_reference(ref):
     ctx = Context.default()
     out = torch.empty(2500, dtype=torch.int32, device="cuda")
     ctx.bind_stream()
-    ctx.check(ctx.lib.splat_pool_sample(ctx.h, D.Rng(9).h, 100_000, 2500, out.data_ptr()))
+    r9 = D.Rng(9)
+    ctx.check(ctx.lib.splat_pool_sample(ctx.h, r9.h, 100_000, 2500, out.data_ptr()))
     assert np.array_equal(out.cpu().numpy(), ref.fisher_yates(9, 100_000, 2500))
 
 

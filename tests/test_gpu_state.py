@@ -109,8 +109,9 @@ def test_reuse_forward_requires_identical_inputs(oracle):
 
     def fused(cam_, cfg_, ds_):
         ctx.bind_stream()
-        return ctx.lib.splat_render_backward_l1(ctx.h, C.byref(ds_.struct()), C.byref(cam_), C.byref(cfg_), tgt.data_ptr(),
-                                                None, R._bg((0, 0, 0)), C.byref(g.struct()), 0, loss.data_ptr())
+        return ctx.lib.splat_render_backward_l1(ctx.h, C.byref(ds_.struct()), C.byref(cam_), C.byref(cfg_),
+                                                capi.as_fp(tgt.data_ptr()), None, R._bg((0, 0, 0)),
+                                                C.byref(g.struct()), 0, capi.as_fp(loss.data_ptr()))
 
     base = RasterConfig()
     R.render(ds, cam, base)
