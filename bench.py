@@ -5,8 +5,9 @@ Workload (BASELINE.json configs[1], the config the metric is quoted on): 1,000,0
 (config-0 distributions, seed 0), SH degree 3, 1237x822 ring views (fov 70 deg, radius 3R,
 height 0.5R), L1 loss against targets rendered from the same set with means + N(0, 0.01^2).
 One step = per rank `--views` ring views of: preprocess -> (depth, tile) radix sorts -> blend
-forward -> fused L1 -> blend backward -> per-Gaussian chain (all 59 gradients), then (N > 1) an
-NCCL all-reduce of the optimised gradient slice, then Adam on means (lr 1.6e-4).
+forward -> fused L1 -> blend backward -> per-Gaussian chain (all 59 gradients), then Adam on means
+(lr 1.6e-4); with N > 1 ranks the full 59N-float gradient is exchanged (NCCL reduce-scatter ->
+Adam on this rank's shards -> all-gather of the parameters, exchange.py).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
@@ -68,13 +69,13 @@ def workload_config(args, world):
                             "Adam on all parameter groups",
                 "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
                 "ring_views": 256, "n_ranks": world,
-                "allreduce": "59N gradient floats (fp32, NCCL sum) when N > 1",
+                "allreduce": "59N gradient floats (fp32) when N > 1: NCCL reduce-scatter -> sharded Adam -> all-gather",
                 "l2": "inputs larger than L2; views rotate each step", "scene_seed": 0}
     return {"workload": "cfg1: 1M Gaussians SH3, 1237x822 ring views, L1 vs perturbed-means target, "
                         "fwd+bwd (59 grads) + Adam(means, lr 1.6e-4)",
             "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
             "ring_views": RING, "n_ranks": world,
-            "allreduce": "3N mean gradients (fp32, NCCL sum) when N > 1",
+            "allreduce": "59N gradient floats (fp32) when N > 1: NCCL reduce-scatter -> sharded Adam -> all-gather",
             "l2": "inputs larger than L2 (236 MB parameters + ~160 MB pair lists per view); views rotate each step",
             "scene_seed": 0}
 
@@ -375,7 +376,8 @@ def run_ours(args):
     # ---- per-kernel breakdown: a separate profiled pass (CUDA events around every launch) ------
     lib.splat_profile_enable(ctx.h, 1)
     p_steps = max(1, args.profile_steps)
-    trainer.ar_events = [] if world > 1 else None
+    if trainer.exchange is not None:
+        trainer.exchange.events = []
     for st in range(args.warmup + args.steps, args.warmup + args.steps + p_steps):
         c, t, _ = views_for(st)
         trainer.step(c, t)
@@ -388,14 +390,16 @@ def run_ours(args):
     lib.splat_profile_enable(ctx.h, 0)
     kern = {nm: (tot[i], cnt[i]) for i, nm in enumerate(names.value.decode().split("\n")[: nk.value])}
     allreduce = None
-    if world > 1 and trainer.ar_events:
-        ar_ms = float(np.mean([a.elapsed_time(b) for a, b in trainer.ar_events]))
-        nbytes = trainer.reduce_slice().numel() * 4
+    if trainer.exchange is not None and trainer.exchange.events:
+        ex = trainer.exchange
+        ar_ms = float(np.mean([a.elapsed_time(b) for a, b in ex.events]))
+        nbytes = 59 * trainer.params.n * 4
         allreduce = {"bytes": nbytes, "ms": ar_ms, "algbw_gbs": nbytes / (ar_ms * 1e6),
-                     "busbw_gbs": 2 * (world - 1) / world * nbytes / (ar_ms * 1e6),
-                     "note": "NCCL all_reduce of the optimised gradient slice, CUDA events on the compute stream "
-                             "(profiled pass)"}
-    trainer.ar_events = None
+                     "busbw_gbs": 2 * (world - 1) / world * nbytes / (ar_ms * 1e6), "buckets": ex.buckets,
+                     "note": "whole exchange of the 59N-float packed gradient: bucketed NCCL reduce-scatter -> "
+                             "Adam on this rank's shards -> all-gather of the parameters -> quaternion renorm "
+                             "(CUDA events on the compute stream, profiled pass)"}
+        ex.events = None
     if world > 1:
         t_ms = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)

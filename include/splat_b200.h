@@ -224,6 +224,20 @@ int splat_adam_step(splat_ctx* ctx, const splat_params_mut* params_dev,
                     const splat_param_grads* grads_dev, const splat_adam_moments* moments_dev,
                     const splat_adam_config* cfg, int32_t* step_count, uint32_t group_mask);
 
+/* OptimState::step on a shard of the packed parameter layout (the view-parallel step, SURVEY
+ * §8e: reduce-scatter -> sharded Adam -> all-gather).  params_flat / m_flat / v_flat are the
+ * packed [centers 3n | log_scales 3n | rotations 4n | opacity n | sh 48n] buffers (+ padding);
+ * elements [begin, begin + count) are updated from grad_shard[count] (the reduce-scattered
+ * gradient), each with its group's learning rate (position lr at step `step`, the count BEFORE
+ * this step, as OptimState::step uses it; bias corrections of step + 1).  Padding elements (>= 59n)
+ * and groups outside group_mask are skipped.  The quaternion renormalisation (optimizer.cpp:69)
+ * is NOT applied: call splat_quat_normalize on the gathered rotations. */
+int splat_adam_step_range(splat_ctx* ctx, float* params_flat, const float* grad_shard_dev, float* m_flat,
+                          float* v_flat, int32_t n, int64_t begin, int64_t count, const splat_adam_config* cfg,
+                          int32_t step, uint32_t group_mask);
+/* normalized_quat (gaussian_set.hpp:15-20) over n (w,x,y,z) rows in place (optimizer.cpp:69). */
+int splat_quat_normalize(splat_ctx* ctx, float* rotations_dev, int32_t n);
+
 /* ---- depth unprojection ------------------------------------------------------------- */
 /* For the preceding splat_render: every valid pixel (rule) whose raster index satisfies
  * (view_index*H*W + pixel + seed) % stride == 0 is unprojected to

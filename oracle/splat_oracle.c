@@ -1070,6 +1070,39 @@ int ORACLE_FN(importance_prune)(const double* importance, int32_t n, double keep
     return 0;
 }
 
+/* OptimState::step restricted to elements [begin, begin + count) of the packed layout (the
+ * sharded step of the view-parallel exchange, splat_adam_step_range): the per-element update of
+ * optimizer.cpp:53-68 with the element's group learning rate, no quaternion renormalisation. */
+int ORACLE_FN(adam_step_range)(float* params, const float* grad_shard, float* m, float* v, int32_t n, int64_t begin,
+                               int64_t count, const splat_adam_config* cfg, int32_t step, uint32_t group_mask) {
+    const double lr_pos = ORACLE_FN(lr_at)(cfg, step) * cfg->scene_extent;
+    const double bias1 = 1.0 - pow(cfg->beta1, step + 1);
+    const double bias2 = 1.0 - pow(cfg->beta2, step + 1);
+    const int64_t N = n;
+    for (int64_t e = begin; e < begin + count && e < 59 * N; ++e) {
+        uint32_t bit;
+        double lr;
+        if (e < 3 * N) { bit = SPLAT_GROUP_CENTERS; lr = lr_pos; }
+        else if (e < 6 * N) { bit = SPLAT_GROUP_SCALES; lr = cfg->lr_scale; }
+        else if (e < 10 * N) { bit = SPLAT_GROUP_ROTATIONS; lr = cfg->lr_rotation; }
+        else if (e < 11 * N) { bit = SPLAT_GROUP_OPACITY; lr = cfg->lr_opacity; }
+        else { bit = SPLAT_GROUP_SH; lr = (e - 11 * N) % 48 < 3 ? cfg->lr_sh_dc : cfg->lr_sh_rest; }
+        if (!(group_mask & bit)) continue;
+        params[e] -= adam_delta(&m[e], &v[e], grad_shard[e - begin], cfg->beta1, cfg->beta2, cfg->eps, bias1, bias2, lr);
+    }
+    return 0;
+}
+
+/* normalized_quat over n rows in place (optimizer.cpp:69). */
+int ORACLE_FN(quat_normalize)(float* rotations, int32_t n) {
+    for (int32_t i = 0; i < n; ++i) {
+        float q[4];
+        normalized_quat(&rotations[4 * (size_t)i], q);
+        for (int k = 0; k < 4; ++k) rotations[4 * (size_t)i + k] = q[k];
+    }
+    return 0;
+}
+
 /* ---- the reference's random draws (include/splat_rng.h) and their consumers -------------- */
 /* std::normal_distribution<float>(0, 1) on std::mt19937(seed), one distribution object. */
 int ORACLE_FN(rng_normal_f32)(uint32_t seed, int32_t n, float* out) {

@@ -130,6 +130,9 @@ int ORACLE_FN(vanilla_clone_split)(const splat_gaussians* g, const float* grad2d
                                    float* centers, float* log_scales, float* rotations, float* opacity_logits,
                                    float* sh, int64_t capacity, int32_t* moment_source, int32_t* n_out,
                                    int32_t* n_clone, int32_t* n_split);
+int ORACLE_FN(adam_step_range)(float* params, const float* grad_shard, float* m, float* v, int32_t n, int64_t begin,
+                               int64_t count, const splat_adam_config* cfg, int32_t step, uint32_t group_mask);
+int ORACLE_FN(quat_normalize)(float* rotations, int32_t n);
 float ORACLE_FN(exp)(float x);
 
 #ifdef __cplusplus

@@ -239,6 +239,9 @@ _EXPORTS = {
     "splat_importance_prune": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
                                          C.POINTER(C.c_int32)]),
     "splat_gather_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "splat_adam_step_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                        C.c_int64, C.c_int64, C.POINTER(AdamConfig), C.c_int32, C.c_uint32]),
+    "splat_quat_normalize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "splat_rng_create": (C.c_int, [C.c_uint32, C.POINTER(C.c_void_p)]),
     "splat_rng_destroy": (None, [C.c_void_p]),
     "splat_rng_get_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),

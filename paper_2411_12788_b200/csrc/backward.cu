@@ -594,20 +594,23 @@ template <bool SH, bool VEC>
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ param, const float* __restrict__ grad,
                                                    float* __restrict__ m, float* __restrict__ v, int64_t count,
                                                    double lr, double lr_alt, double b1, double omb1, double b2,
-                                                   double omb2, double eps, double bias1, double bias2) {
+                                                   double omb2, double eps, double bias1, double bias2,
+                                                   int sh_phase) {
     pdl_wait();
     const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i0 >= count) return;
-    const int r0 = SH ? (int)(i0 % 48) : 0;
+    // position of element i0 inside its 48-value SH row (sh_phase: the row position of element 0,
+    // nonzero when a shard of the packed buffer starts mid-row); a 4-group may straddle rows then
+    const int r0 = SH ? (int)((i0 + sh_phase) % 48) : 0;
     if (VEC && i0 + 4 <= count) {
         float4 p4 = *reinterpret_cast<const float4*>(param + i0);
         const float4 g4 = __ldg(reinterpret_cast<const float4*>(grad + i0));
         float4 m4 = *reinterpret_cast<const float4*>(m + i0);
         float4 v4 = *reinterpret_cast<const float4*>(v + i0);
-        p4.x = adam_one(p4.x, g4.x, m4.x, v4.x, SH && r0 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
-        p4.y = adam_one(p4.y, g4.y, m4.y, v4.y, SH && r0 + 1 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
-        p4.z = adam_one(p4.z, g4.z, m4.z, v4.z, SH && r0 + 2 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
-        p4.w = adam_one(p4.w, g4.w, m4.w, v4.w, SH && r0 + 3 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.x = adam_one(p4.x, g4.x, m4.x, v4.x, SH && r0 % 48 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.y = adam_one(p4.y, g4.y, m4.y, v4.y, SH && (r0 + 1) % 48 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.z = adam_one(p4.z, g4.z, m4.z, v4.z, SH && (r0 + 2) % 48 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
+        p4.w = adam_one(p4.w, g4.w, m4.w, v4.w, SH && (r0 + 3) % 48 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps, bias1, bias2);
         *reinterpret_cast<float4*>(param + i0) = p4;
         *reinterpret_cast<float4*>(m + i0) = m4;
         *reinterpret_cast<float4*>(v + i0) = v4;
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ param, co
     for (int k = 0; k < 4 && i0 + k < count; ++k) {
         const int64_t i = i0 + k;
         float mm = m[i], vv = v[i];
-        param[i] = adam_one(param[i], grad[i], mm, vv, SH && r0 + k >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps,
+        param[i] = adam_one(param[i], grad[i], mm, vv, SH && (r0 + k) % 48 >= 3 ? lr_alt : lr, b1, omb1, b2, omb2, eps,
                             bias1, bias2);
         m[i] = mm;
         v[i] = vv;
@@ -745,7 +748,7 @@ cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, dou
         const unsigned grid = blocks_for((a.count + 3) / 4, 256);
 #define ADAM_LAUNCH(SH, VEC)                                                                                      \
     launch_pdl(lc.stream, adam_kernel<SH, VEC>, dim3(grid), dim3(256), 0, a.param, a.grad, a.m, a.v, a.count, a.lr,  \
-               a.lr_alt, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps, bias1, bias2)
+               a.lr_alt, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps, bias1, bias2, a.sh_phase)
         if (a.sh_layout) {
             if (vec) ADAM_LAUNCH(true, true);
             else ADAM_LAUNCH(true, false);

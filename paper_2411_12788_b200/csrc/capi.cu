@@ -709,6 +709,23 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     return SPLAT_OK;
 }
 
+// LrSchedule::at (optimizer.cpp:8-12) at step t (before the increment) times the scene extent,
+// and the bias corrections of step t + 1 (optimizer.cpp:45-47), host fp64.
+struct AdamStepConsts {
+    double lr_pos, bias1, bias2;
+};
+AdamStepConsts adam_consts(const splat_adam_config* cfg, int t) {
+    double lr_sched;
+    if (t <= 0) {
+        lr_sched = cfg->lr_init;
+    } else {
+        double tt = (double)t / (double)cfg->max_steps;
+        if (tt > 1.0) tt = 1.0;
+        lr_sched = std::exp((1.0 - tt) * std::log(cfg->lr_init) + tt * std::log(cfg->lr_final));
+    }
+    return {lr_sched * cfg->scene_extent, 1.0 - std::pow(cfg->beta1, t + 1), 1.0 - std::pow(cfg->beta2, t + 1)};
+}
+
 // Scratch for sort_u64_pairs over n entries: keys lo in dkey[0], hi in dhi, vals in dval[0].
 int ensure_u64_sort(splat_ctx* ctx, int n) {
     const size_t nn = (size_t)(n > 0 ? n : 1);
@@ -982,20 +999,9 @@ int splat_adam_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param
                     const splat_adam_config* cfg, int32_t* step_count, uint32_t group_mask) {
     if (!ctx || !p || !gr || !m || !cfg || !step_count) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "adam: null args");
     if (p->n < 0) return set_err(ctx, SPLAT_ERR_LOGIC, "OptimState::step: moment/gradient rows out of sync with set");
-    // LrSchedule::at (optimizer.cpp:8-12) and bias corrections (optimizer.cpp:45-47), host fp64
     const int t = *step_count;
-    double lr_sched;
-    if (t <= 0) {
-        lr_sched = cfg->lr_init;
-    } else {
-        double tt = (double)t / (double)cfg->max_steps;
-        if (tt > 1.0) tt = 1.0;
-        lr_sched = std::exp((1.0 - tt) * std::log(cfg->lr_init) + tt * std::log(cfg->lr_final));
-    }
-    const double lr_pos = lr_sched * cfg->scene_extent;
+    const AdamStepConsts k = adam_consts(cfg, t);
     *step_count = t + 1;
-    const double bias1 = 1.0 - std::pow(cfg->beta1, *step_count);
-    const double bias2 = 1.0 - std::pow(cfg->beta2, *step_count);
     const int64_t n = p->n;
     LaunchCtx& lc = ctx->lc;
     auto run = [&](uint32_t bit, float* param, const float* grad, float* mm, float* vv, int64_t cnt, double lr,
@@ -1004,11 +1010,11 @@ int splat_adam_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param
         if (cnt > 0 && (!param || !grad || !mm || !vv))
             return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "adam: group pointers missing");
         AdamGroupArgs a{param, grad, mm, vv, cnt, lr, lr_alt, sh};
-        CK(launch_adam(lc, a, cfg->beta1, cfg->beta2, cfg->eps, bias1, bias2), "adam");
+        CK(launch_adam(lc, a, cfg->beta1, cfg->beta2, cfg->eps, k.bias1, k.bias2), "adam");
         return SPLAT_OK;
     };
     int rc;
-    if ((rc = run(SPLAT_GROUP_CENTERS, p->centers, gr->d_centers, m->m_centers, m->v_centers, 3 * n, lr_pos, lr_pos, 0))) return rc;
+    if ((rc = run(SPLAT_GROUP_CENTERS, p->centers, gr->d_centers, m->m_centers, m->v_centers, 3 * n, k.lr_pos, k.lr_pos, 0))) return rc;
     if ((rc = run(SPLAT_GROUP_SCALES, p->log_scales, gr->d_log_scales, m->m_log_scales, m->v_log_scales, 3 * n,
                   cfg->lr_scale, cfg->lr_scale, 0))) return rc;
     if ((rc = run(SPLAT_GROUP_ROTATIONS, p->rotations, gr->d_rotations, m->m_rotations, m->v_rotations, 4 * n,
@@ -1017,6 +1023,43 @@ int splat_adam_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param
                   cfg->lr_opacity, cfg->lr_opacity, 0))) return rc;
     if ((rc = run(SPLAT_GROUP_SH, p->sh, gr->d_sh, m->m_sh, m->v_sh, 48 * n, cfg->lr_sh_dc, cfg->lr_sh_rest, 1))) return rc;
     if (group_mask & SPLAT_GROUP_ROTATIONS) CK(launch_quat_normalize(lc, p->rotations, (int)n), "quat normalize");
+    return SPLAT_OK;
+}
+
+int splat_adam_step_range(splat_ctx* ctx, float* params_flat, const float* grad_shard, float* m_flat, float* v_flat,
+                          int32_t n, int64_t begin, int64_t count, const splat_adam_config* cfg, int32_t step,
+                          uint32_t group_mask) {
+    if (!ctx || !cfg || n < 0 || begin < 0 || count < 0 ||
+        (count > 0 && (!params_flat || !grad_shard || !m_flat || !v_flat)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "adam_step_range: bad args");
+    const AdamStepConsts k = adam_consts(cfg, step);
+    const int64_t nn = n;
+    // the packed groups [centers 3n | log_scales 3n | rotations 4n | opacity n | sh 48n]
+    const struct {
+        uint32_t bit;
+        int64_t lo, hi;
+        double lr, lr_alt;
+        int sh;
+    } groups[5] = {{SPLAT_GROUP_CENTERS, 0, 3 * nn, k.lr_pos, k.lr_pos, 0},
+                   {SPLAT_GROUP_SCALES, 3 * nn, 6 * nn, cfg->lr_scale, cfg->lr_scale, 0},
+                   {SPLAT_GROUP_ROTATIONS, 6 * nn, 10 * nn, cfg->lr_rotation, cfg->lr_rotation, 0},
+                   {SPLAT_GROUP_OPACITY, 10 * nn, 11 * nn, cfg->lr_opacity, cfg->lr_opacity, 0},
+                   {SPLAT_GROUP_SH, 11 * nn, 59 * nn, cfg->lr_sh_dc, cfg->lr_sh_rest, 1}};
+    const int64_t end = begin + count;
+    for (const auto& gr : groups) {
+        if (!(group_mask & gr.bit)) continue;
+        const int64_t lo = std::max(begin, gr.lo), hi = std::min(end, gr.hi);
+        if (hi <= lo) continue;
+        AdamGroupArgs a{params_flat + lo, grad_shard + (lo - begin), m_flat + lo, v_flat + lo, hi - lo, gr.lr, gr.lr_alt,
+                        gr.sh, gr.sh ? (int)((lo - gr.lo) % 48) : 0};
+        CK(launch_adam(ctx->lc, a, cfg->beta1, cfg->beta2, cfg->eps, k.bias1, k.bias2), "adam range");
+    }
+    return SPLAT_OK;
+}
+
+int splat_quat_normalize(splat_ctx* ctx, float* rotations, int32_t n) {
+    if (!ctx || n < 0 || (n > 0 && !rotations)) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "quat_normalize: bad args");
+    CK(launch_quat_normalize(ctx->lc, rotations, (int)n), "quat normalize");
     return SPLAT_OK;
 }
 

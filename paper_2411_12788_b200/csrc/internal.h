@@ -201,6 +201,7 @@ struct AdamGroupArgs {
     double lr;
     double lr_alt;   // for SH: lr of coefficients k >= 3 (rest)
     int sh_layout;   // 1: per-48 row, first 3 use lr, rest lr_alt
+    int sh_phase = 0;  // SH: row position (0..47) of element 0 (a shard starting mid-row)
 };
 cudaError_t launch_adam(LaunchCtx& lc, const AdamGroupArgs& a, double beta1, double beta2, double eps,
                         double bias1, double bias2);

@@ -101,11 +101,23 @@ class DeviceGaussians:
     Gaussian laid out [centers 3N | log_scales 3N | rotations 4N | opacity N | sh 48N], so the
     packed gradient / all-reduce buffer has the same layout."""
 
-    def __init__(self, n: int, active_sh_degree: int = 3, device: int = 0):
+    def __init__(self, n: int, active_sh_degree: int = 3, device: int = 0, flat_len: int = 0):
         torch = _torch()
         self.n = int(n)
         self.active_sh_degree = int(active_sh_degree)
-        self.flat = torch.zeros(max(59 * self.n, 1), dtype=torch.float32, device=f"cuda:{device}")
+        # flat_len > 59 n: zero padding after the packed groups (the sharded exchange splits the
+        # buffer into equal per-rank pieces)
+        self.flat = torch.zeros(max(59 * self.n, flat_len, 1), dtype=torch.float32, device=f"cuda:{device}")
+        self._views()
+
+    def ensure_flat_len(self, flat_len: int) -> None:
+        """Grow the padding after the packed groups to flat_len floats (re-points the views)."""
+        if self.flat.numel() >= flat_len:
+            return
+        torch = _torch()
+        f = torch.zeros(flat_len, dtype=torch.float32, device=self.flat.device)
+        f[: 59 * self.n].copy_(self.flat[: 59 * self.n])
+        self.flat = f
         self._views()
 
     def _views(self):
@@ -151,10 +163,10 @@ class DeviceGaussians:
 class DeviceGrads:
     """ParamGrads<float> in HBM with the DeviceGaussians packed layout (+ grad2d stats)."""
 
-    def __init__(self, n: int, device: int = 0):
+    def __init__(self, n: int, device: int = 0, flat_len: int = 0):
         torch = _torch()
         self.n = n
-        self.flat = torch.zeros(max(59 * n, 1), dtype=torch.float32, device=f"cuda:{device}")
+        self.flat = torch.zeros(max(59 * n, flat_len, 1), dtype=torch.float32, device=f"cuda:{device}")
         self.grad2d_accum = torch.zeros(max(n, 1), dtype=torch.float32, device=f"cuda:{device}")
         self.grad2d_count = torch.zeros(max(n, 1), dtype=torch.int32, device=f"cuda:{device}")
         f = self.flat
@@ -382,13 +394,13 @@ def photometric_loss(rendered, target, lam: float, want_grad: bool = True, ctx: 
 class OptimState:
     """OptimState (optimizer.hpp:37-76): Adam moments in HBM with the packed parameter layout."""
 
-    def __init__(self, config: Optional[AdamConfig] = None, n: int = 0, device: int = 0):
+    def __init__(self, config: Optional[AdamConfig] = None, n: int = 0, device: int = 0, flat_len: int = 0):
         torch = _torch()
         self.config = config or AdamConfig()
         self.n = n
         self.t = 0
-        self.m = torch.zeros(max(59 * n, 1), dtype=torch.float32, device=f"cuda:{device}")
-        self.v = torch.zeros(max(59 * n, 1), dtype=torch.float32, device=f"cuda:{device}")
+        self.m = torch.zeros(max(59 * n, flat_len, 1), dtype=torch.float32, device=f"cuda:{device}")
+        self.v = torch.zeros(max(59 * n, flat_len, 1), dtype=torch.float32, device=f"cuda:{device}")
 
     def size(self) -> int:
         return self.n

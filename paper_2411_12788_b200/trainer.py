@@ -5,9 +5,9 @@ One step (trainer.cpp:226-240 with lambda_dssim = 0, batched as BASELINE config 
       render<float>                                   (splat_render)
       l1_loss + render_backward<float>, grads summed  (splat_render_backward_l1, ParamGrads::add)
         or, with lambda_dssim > 0, photometric_loss   (splat_render_backward_photometric)
-  all-reduce of the packed gradient (torch.distributed / NCCL), only when world_size > 1:
-      the 3N mean gradients when only means are optimised (config 1), all 59N floats otherwise
-  OptimState::step on the selected parameter groups (splat_adam_step)
+  one process: OptimState::step on the selected parameter groups (splat_adam_step)
+  world_size > 1: the sharded exchange of the full 59N-float packed gradient (exchange.py:
+      bucketed reduce-scatter -> Adam on this rank's shards -> all-gather of the parameters)
 
 Views shard across ranks with no data-path collective other than that gradient exchange.
 """
@@ -20,6 +20,7 @@ import numpy as np
 
 from . import capi
 from .capi import Camera, RasterConfig
+from .exchange import ShardedExchange, padded_len
 from .rasterizer import Context, DeviceGaussians, DeviceGrads, LogicError, OptimState, _torch
 
 
@@ -47,7 +48,7 @@ class ViewTrainer:
     def __init__(self, params: DeviceGaussians, adam: Optional[capi.AdamConfig] = None,
                  group_mask: int = capi.GROUP_ALL, cfg: Optional[RasterConfig] = None,
                  background=(0.0, 0.0, 0.0), ctx: Optional[Context] = None, max_views: int = 64,
-                 process_group=None, lambda_dssim: float = 0.0):
+                 process_group=None, lambda_dssim: float = 0.0, buckets: int = 4):
         torch = _torch()
         self.torch = torch
         self.ctx = ctx or Context.default()
@@ -63,19 +64,33 @@ class ViewTrainer:
         self.lambda_dssim = float(lambda_dssim)
         self.pairs_last_step: list[int] = []
         self.survivors_last_step: list[int] = []
+        self.exchange: Optional[ShardedExchange] = None
+        self.buckets = buckets
+        if self.world_size > 1:
+            self._setup_exchange()
         self._gr = self.grads.struct()
+
+    def _setup_exchange(self) -> None:
+        """Packed buffers padded for the sharded exchange (params are re-pointed in place)."""
+        import torch.distributed as dist
+        n = self.params.n
+        L = padded_len(n, self.world_size, self.buckets)
+        self.params.ensure_flat_len(L)
+        if self.grads.flat.numel() < L:
+            self.grads = DeviceGrads(n, self.ctx.device, flat_len=L)
+        if self.opt.m.numel() < L:
+            torch = self.torch
+            for name in ("m", "v"):
+                old = getattr(self.opt, name)
+                new = torch.zeros(L, dtype=torch.float32, device=old.device)
+                new[: 59 * n].copy_(old[: 59 * n])
+                setattr(self.opt, name, new)
+        self.exchange = ShardedExchange(n, self.world_size, dist.get_rank(self.pg), self.pg, self.buckets)
 
     @property
     def world_size(self) -> int:
         import torch.distributed as dist
         return dist.get_world_size(self.pg) if dist.is_available() and dist.is_initialized() else 1
-
-    def reduce_slice(self):
-        """The part of the packed gradient that the optimiser consumes (the exchanged bytes)."""
-        n = self.params.n
-        if self.group_mask == capi.GROUP_CENTERS:
-            return self.grads.flat[: 3 * n]
-        return self.grads.flat[: 59 * n]
 
     def _native(self, cams: Sequence[Camera], ptrs, on_host: bool, group_mask: int, loss_host=None) -> None:
         """splat_train_step: the whole per-step loop (render, loss, backward summed over views,
@@ -92,6 +107,8 @@ class ViewTrainer:
             raise LogicError("ViewTrainer: optimizer rows out of sync with the parameter set (remap the moments)")
         if self.grads.n != n:  # the set was densified / pruned: the gradient buffer follows its size
             self.grads = DeviceGrads(n, self.ctx.device)
+            if self.world_size > 1:
+                self._setup_exchange()
             self._gr = self.grads.struct()
         key = (self.params.centers.data_ptr(), self.params.sh.data_ptr(), self.params.n, self.params.active_sh_degree,
                self.opt.m.data_ptr())
@@ -113,16 +130,13 @@ class ViewTrainer:
         self._native(cams, [t.data_ptr() for t in targets], False, 0)
 
     def _finish_distributed(self) -> None:
-        import torch.distributed as dist
-        ev = None
-        if getattr(self, "ar_events", None) is not None:  # bench: time the exchange
-            ev = (self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True))
-            ev[0].record()
-        dist.all_reduce(self.reduce_slice(), op=dist.ReduceOp.SUM, group=self.pg)
-        if ev is not None:
-            ev[1].record()
-            self.ar_events.append(ev)
-        self.opt.step(self.params, self.grads, self.group_mask, self.ctx)
+        """Sharded exchange + optimiser step of this rank's summed gradients (exchange.py)."""
+        if self.exchange is None or self.exchange.n != self.params.n:
+            self._setup_exchange()
+            self._gr = self.grads.struct()
+        self.exchange.step(self.params.flat, self.grads.flat, self.opt.m, self.opt.v, self.opt.config, self.opt.t,
+                           self.group_mask, self.ctx)
+        self.opt.t += 1
 
     def step(self, cams: Sequence[Camera], targets) -> "object":
         """Device-resident step: targets are CUDA tensors [H, W, 3]. Returns the per-view loss

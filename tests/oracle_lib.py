@@ -118,6 +118,9 @@ class OracleLib:
         getattr(L, p + "rng_normal_f32").argtypes = [C.c_uint32, C.c_int32, fp]
         getattr(L, p + "rng_mixed_64").argtypes = [C.c_uint64, C.c_int32, ip, ip, ip, dp]
         if kind == "oracle":
+            getattr(L, p + "adam_step_range").argtypes = [fp, fp, fp, fp, C.c_int32, C.c_int64, C.c_int64,
+                                                          C.POINTER(AdamConfig), C.c_int32, C.c_uint32]
+            getattr(L, p + "quat_normalize").argtypes = [fp, C.c_int32]
             getattr(L, p + "rng_uniform_f64_32").argtypes = [C.c_uint32, C.c_int32, dp]
             getattr(L, p + "rng_fisher_yates").argtypes = [C.c_uint32, C.c_int32, C.c_int32, ip]
             getattr(L, p + "importance_sample").argtypes = [dp, C.c_int32, C.c_int32, C.c_uint64, ip, ip]
@@ -514,4 +517,12 @@ class OracleLib:
                                  C.byref(ns)))
         m = no.value
         return out.select(np.arange(m)), ms[:m], nc.value, ns.value
+
+    def adam_step_range(self, params, grad_shard, m, v, n, begin, count, cfg, step, group_mask):
+        """In place on float32 numpy arrays (packed layout, + padding)."""
+        self.check(self.fn("adam_step_range")(_ptr(params), _ptr(grad_shard), _ptr(m), _ptr(v), n, begin, count,
+                                              C.byref(cfg), step, group_mask))
+
+    def quat_normalize(self, rotations, n):
+        self.check(self.fn("quat_normalize")(_ptr(rotations), n))
 

@@ -1,8 +1,11 @@
 """View-parallel training step across ranks with the gloo backend on CPU:
 each rank computes the gradients of its views (the CPU oracle stands in for the per-view CUDA
-work, which needs a GPU), the packed 59-float gradients are summed with all_reduce exactly as
-ViewTrainer does over NCCL, and Adam then runs on every rank.  The result must equal one process
-training all views, and stay identical across ranks."""
+work, which needs a GPU) into the padded packed 59N buffer, and the product's exchange
+(paper_2411_12788_b200/exchange.py: bucketed reduce-scatter -> Adam on this rank's shards ->
+all-gather -> quaternion renorm; the oracle's restatement of splat_adam_step_range stands in for
+the kernel) steps the replicas.  The result must equal an all-reduce followed by the full
+OptimState::step bit for bit, equal one process training all views within float-sum tolerance,
+and stay identical across ranks."""
 import os
 import sys
 from pathlib import Path
@@ -30,11 +33,13 @@ def _view_grads(oracle, s, cam, target):
     return oracle.render_backward(s, cam, dc)
 
 
-def _train(rank, world, out_q, port):
+def _train(rank, world, out_q, port, mode="exchange", buckets=3):
     sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
     from oracle_lib import OracleLib
     from paper_2411_12788_b200 import scenes
-    from paper_2411_12788_b200.capi import AdamConfig
+    from paper_2411_12788_b200.capi import AdamConfig, GROUP_ALL
+    from paper_2411_12788_b200.exchange import ShardedExchange
+    from paper_2411_12788_b200.scenes import GaussianSet
     from paper_2411_12788_b200.trainer import pack_grads, unpack_grads, views_for
     if world > 1:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -42,29 +47,51 @@ def _train(rank, world, out_q, port):
     oracle = OracleLib("oracle", "B")
     s, cams = _scene()
     targets = [oracle.render(scenes.perturbed(s), c)["color"] for c in cams]
-    m = np.zeros(59 * N_GAUSS, np.float32)
-    v = np.zeros(59 * N_GAUSS, np.float32)
+    n = N_GAUSS
+    cfg = AdamConfig()
+    ex = ShardedExchange(n, world, rank, buckets=buckets,
+                         adam_range=lambda p, g, m_, v_, n_, b, c, cf, st, mk: oracle.adam_step_range(
+                             p.numpy(), g.numpy(), m_.numpy(), v_.numpy(), n_, b, c, cf, st, mk),
+                         quat_normalize=lambda r, n_: oracle.quat_normalize(r.numpy(), n_))
+    L = ex.flat_len
+    params = torch.zeros(L)
+    params[:59 * n] = torch.from_numpy(pack_grads(dict(d_centers=s.centers, d_log_scales=s.log_scales,
+                                                       d_rotations=s.rotations, d_opacity_logits=s.opacity_logits,
+                                                       d_sh=s.sh)))
+    m, v = torch.zeros(L), torch.zeros(L)
     t = 0
     for step in range(STEPS):
+        cur = unpack_grads(params[:59 * n].numpy().copy(), n)
+        s = GaussianSet(cur["d_centers"], cur["d_log_scales"], cur["d_rotations"], cur["d_opacity_logits"],
+                        cur["d_sh"])
         idx = views_for(step, rank, world, V * 2 // world, RING)  # same global batch for any world
-        flat = np.zeros(59 * N_GAUSS, np.float32)
+        flat = np.zeros(59 * n, np.float32)
         for i in idx:
             flat += pack_grads(_view_grads(oracle, s, cams[i], targets[i]))
-        if world > 1:
-            buf = torch.from_numpy(flat)
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
-            flat = buf.numpy()
-        s, m, v, t = oracle.adam_step(s, unpack_grads(flat, N_GAUSS), m, v, AdamConfig(), t)
-    out_q.put((rank, s.centers.copy(), s.sh.copy()))
+        grads = torch.zeros(L)
+        grads[:59 * n] = torch.from_numpy(flat)
+        if mode == "exchange":
+            ex.step(params, grads, m, v, cfg, t, GROUP_ALL)
+            t += 1
+        else:  # all-reduce + the full OptimState::step on every rank
+            if world > 1:
+                dist.all_reduce(grads, op=dist.ReduceOp.SUM)
+            s2, m2, v2, t = oracle.adam_step(s, unpack_grads(grads[:59 * n].numpy(), n), m[:59 * n].numpy(),
+                                             v[:59 * n].numpy(), cfg, t)
+            params[:59 * n] = torch.from_numpy(pack_grads(dict(d_centers=s2.centers, d_log_scales=s2.log_scales,
+                                                               d_rotations=s2.rotations,
+                                                               d_opacity_logits=s2.opacity_logits, d_sh=s2.sh)))
+            m[:59 * n], v[:59 * n] = torch.from_numpy(m2), torch.from_numpy(v2)
+    out_q.put((rank, params[:59 * n].numpy().copy()))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def _run(world, port):
+def _run(world, port, mode="exchange", buckets=3):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_train, args=(r, world, q, port)) for r in range(world)]
+    procs = [ctx.Process(target=_train, args=(r, world, q, port, mode, buckets)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -82,12 +109,27 @@ def test_views_partition_covers_ring_once_per_epoch():
 
 
 @pytest.mark.timeout(600)
-def test_two_rank_gloo_step_matches_single_process():
-    single = _run(1, 29611)
-    two = _run(2, 29612)
-    # ranks agree bit for bit (identical reduced gradients, identical Adam)
-    assert np.array_equal(two[0][1], two[1][1]) and np.array_equal(two[0][2], two[1][2])
-    # and match one process summing all views; the float sum order differs (rank-local partial
-    # sums), so compare within tolerance
+def test_two_rank_gloo_exchange_matches_allreduce_and_single_process():
+    single = _run(1, 29611, mode="allreduce")
+    two = _run(2, 29612, mode="exchange", buckets=3)
+    two_ar = _run(2, 29613, mode="allreduce")
+    # ranks agree bit for bit (the gather hands every replica the same parameters)
+    assert np.array_equal(two[0][1], two[1][1])
+    # reduce-scatter + Adam on shards + all-gather + renorm == all-reduce + the full step, bitwise
+    assert np.array_equal(two[0][1], two_ar[0][1])
+    # and one process summing all views, within the float-sum order difference
     assert np.allclose(two[0][1], single[0][1], rtol=0, atol=1e-6)
-    assert np.allclose(two[0][2], single[0][2], rtol=0, atol=1e-6)
+
+
+def test_exchange_ranges_partition_the_padded_buffer():
+    from paper_2411_12788_b200.exchange import ShardedExchange, padded_len
+    for n, world, buckets in ((1, 2, 1), (600, 2, 3), (1001, 8, 4), (3_000_000, 8, 4), (7, 3, 5)):
+        L = padded_len(n, world, buckets)
+        assert L >= 59 * n and L % (world * buckets * 4) == 0
+        covered = np.zeros(L, np.int32)
+        for r in range(world):
+            ex = ShardedExchange(n, world, r, buckets=buckets)
+            for b0, s0 in ex.ranges():
+                assert b0 <= s0 and s0 + ex.shard_len <= b0 + ex.bucket_len and s0 % 4 == 0
+                covered[s0:s0 + ex.shard_len] += 1
+        assert (covered == 1).all()
