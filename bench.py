@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--comm", choices=("torch", "native"), default="torch",
+                    help="N > 1 exchange: torch.distributed NCCL collectives (exchange.py) or the library's own "
+                         "NCCL communicator inside splat_train_step")
+    ap.add_argument("--buckets", type=int, default=4, help="exchange buckets (reduce-scatter / Adam pipelining)")
     a = ap.parse_args()
     if a.views is None:
         a.views = 8 if a.config == 4 else 1
@@ -332,7 +336,8 @@ def run_ours(args):
     targets = [render(dt, cam, want_depth=False, ctx=ctx).color.clone() for cam in cams]
     del dt
     gmask = capi.GROUP_ALL if args.config == 4 else capi.GROUP_CENTERS
-    trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=gmask, ctx=ctx, max_views=max(args.views, 1))
+    trainer = ViewTrainer(ds, capi.AdamConfig(), group_mask=gmask, ctx=ctx, max_views=max(args.views, 1),
+                          buckets=args.buckets, native_comm=(world > 1 and args.comm == "native"))
     V = args.views
 
     from paper_2411_12788_b200.trainer import views_for as _views_for

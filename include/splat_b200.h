@@ -55,7 +55,8 @@ typedef enum splat_status {
     SPLAT_ERR_RUNTIME = 3,          /* std::runtime_error (e.g. no valid depth pixel) */
     SPLAT_ERR_CUDA = 4,
     SPLAT_ERR_OUT_OF_MEMORY = 5,
-    SPLAT_ERR_NO_FORWARD_STATE = 6  /* fused/reuse call without a matching forward */
+    SPLAT_ERR_NO_FORWARD_STATE = 6, /* fused/reuse call without a matching forward */
+    SPLAT_ERR_NCCL = 7              /* NCCL missing or a collective failed (view-parallel exchange) */
 } splat_status;
 
 /* Mirrors CameraT<float> (camera.hpp:12-22). rotation is row-major world->camera. */
@@ -293,6 +294,40 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* params, const splat
                      uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
                      int targets_on_host, const splat_raster_config* cfg, const float background[3],
                      float lambda_dssim, float* loss_dev, float* loss_host);
+/* With a communicator on ctx (splat_comm_init), splat_train_step is the view-parallel step of
+ * one rank: its views' gradients are summed locally, then splat_exchange_step replaces the plain
+ * OptimState::step.  This needs the packed layout for params, grads and moments (each group
+ * right after the previous one: centers, centers + 3n, + 6n, + 10n, + 11n) with at least
+ * splat_exchange_len(n, nranks, buckets) floats per buffer (zero padding after 59n). */
+
+/* ---- view-parallel exchange over the library's own NCCL communicator ---------
+ * One process per GPU, each holding a replica of the Gaussians and training its own views.
+ * splat_comm_unique_id on one rank, its 128 bytes broadcast by the caller (MPI, torch, a file),
+ * then splat_comm_init on every rank (libnccl is loaded at run time).  The exchange:
+ * reduce-scatter(sum) of the packed gradient in `buckets` pieces on a communication stream ->
+ * OptimState::step on this rank's shard of each bucket (splat_adam_step_range, overlapping the
+ * later buckets' reduce-scatter) -> in-place all-gather of the updated parameters ->
+ * rotation renormalisation.  Only this rank's shards of m and v are kept current. */
+#define SPLAT_UNIQUE_ID_BYTES 128
+int splat_comm_unique_id(void* id_out);
+int splat_comm_init(splat_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id, int32_t buckets);
+int splat_comm_destroy(splat_ctx* ctx);
+/* Padded packed length: 59 n rounded up to a multiple of nranks * buckets * 4 floats. */
+int64_t splat_exchange_len(int32_t n, int32_t nranks, int32_t buckets);
+/* The exchange + optimiser step on packed flats of flat_len floats (>= splat_exchange_len);
+ * *step_count is OptimState's count (incremented).  Without a communicator: the plain step. */
+int splat_exchange_step(splat_ctx* ctx, float* params_flat, const float* grads_flat, float* m_flat, float* v_flat,
+                        int32_t n, int64_t flat_len, const splat_adam_config* cfg, int32_t* step_count,
+                        uint32_t group_mask);
+/* In-place all-reduce over the communicator on ctx's stream (the config-3 importance sums / max
+ * weights / argmax counts across ranks).  dtype: SPLAT_DTYPE_*; op: SPLAT_OP_*. */
+#define SPLAT_DTYPE_INT32 2
+#define SPLAT_DTYPE_INT64 4
+#define SPLAT_DTYPE_FLOAT32 7
+#define SPLAT_DTYPE_FLOAT64 8
+#define SPLAT_OP_SUM 0
+#define SPLAT_OP_MAX 2
+int splat_allreduce(splat_ctx* ctx, void* buf_dev, int64_t count, int32_t dtype, int32_t op);
 
 /* ---- SSIM and the photometric loss (loss.cpp:78-153) -------------- */
 /* ssim<float>: value_dev (device float) = mean SSIM of H x W x ch images a, b with the 11-tap

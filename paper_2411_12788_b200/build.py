@@ -31,6 +31,7 @@ SOURCES = {
     "densify.cu": ["--fmad=false"],
     "ssim.cu": ["--fmad=false"],
     "spatial.cu": ["--fmad=false"],
+    "comm.cu": [],
     "capi.cu": [],
 }
 HEADERS = [CSRC / "common.cuh", CSRC / "internal.h", ROOT / "include" / "splat_b200.h",

@@ -24,6 +24,7 @@ SPLAT_ERR_RUNTIME = 3
 SPLAT_ERR_CUDA = 4
 SPLAT_ERR_OUT_OF_MEMORY = 5
 SPLAT_ERR_NO_FORWARD_STATE = 6
+SPLAT_ERR_NCCL = 7
 
 GROUP_CENTERS = 1
 GROUP_SCALES = 2
@@ -242,6 +243,13 @@ _EXPORTS = {
     "splat_adam_step_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                         C.c_int64, C.c_int64, C.POINTER(AdamConfig), C.c_int32, C.c_uint32]),
     "splat_quat_normalize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "splat_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "splat_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32]),
+    "splat_comm_destroy": (C.c_int, [C.c_void_p]),
+    "splat_exchange_len": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "splat_exchange_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                      C.c_int64, C.POINTER(AdamConfig), C.POINTER(C.c_int32), C.c_uint32]),
+    "splat_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32]),
     "splat_rng_create": (C.c_int, [C.c_uint32, C.POINTER(C.c_void_p)]),
     "splat_rng_destroy": (None, [C.c_void_p]),
     "splat_rng_get_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),

@@ -122,6 +122,8 @@ struct FwdState {
 
 }  // namespace
 
+constexpr int kMaxBuckets = 16;
+
 struct splat_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -177,6 +179,12 @@ struct splat_ctx {
     cudaEvent_t ev_bwd = nullptr, ev_loss = nullptr;
     bool fwd_start_recorded = false;
     FwdState st;
+    // view-parallel exchange (splat_comm_init): NCCL communicator, its stream, per-bucket events
+    Comm* comm = nullptr;
+    int comm_buckets = 4;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ex[2 * kMaxBuckets + 2] = {};
+    DevBuf ex_shard;
 };
 
 namespace {
@@ -839,6 +847,7 @@ int splat_ctx_create(int device, splat_ctx** out) {
 int splat_ctx_destroy(splat_ctx* ctx) {
     if (!ctx) return SPLAT_OK;
     cudaSetDevice(ctx->device);
+    splat_comm_destroy(ctx);
     if (ctx->twin) {
         ctx->twin->lc.prof = nullptr;  // shared with this context
         splat_ctx_destroy(ctx->twin);
@@ -1054,6 +1063,102 @@ int splat_adam_step_range(splat_ctx* ctx, float* params_flat, const float* grad_
                         gr.sh, gr.sh ? (int)((lo - gr.lo) % 48) : 0};
         CK(launch_adam(ctx->lc, a, cfg->beta1, cfg->beta2, cfg->eps, k.bias1, k.bias2), "adam range");
     }
+    return SPLAT_OK;
+}
+
+// ---- view-parallel exchange over the library's NCCL communicator ---------------
+int splat_comm_unique_id(void* id_out) {
+    if (!id_out) return SPLAT_ERR_INVALID_ARGUMENT;
+    std::string err;
+    if (comm_unique_id(id_out, &err)) {
+        std::fprintf(stderr, "splat_comm_unique_id: %s\n", err.c_str());
+        return SPLAT_ERR_NCCL;
+    }
+    return SPLAT_OK;
+}
+
+int splat_comm_init(splat_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id, int32_t buckets) {
+    if (!ctx || !unique_id || nranks < 1 || rank < 0 || rank >= nranks || buckets < 1 || buckets > kMaxBuckets)
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "comm_init: bad args");
+    splat_comm_destroy(ctx);
+    CK(cudaSetDevice(ctx->device), "set device");
+    std::string err;
+    Comm* c = comm_create(nranks, rank, unique_id, &err);
+    if (!c) return set_err(ctx, SPLAT_ERR_NCCL, "comm_init: " + err);
+    ctx->comm = c;
+    ctx->comm_buckets = buckets;
+    if (!ctx->comm_stream) CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking), "comm stream");
+    for (cudaEvent_t& ev : ctx->ev_ex)
+        if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "comm event");
+    return SPLAT_OK;
+}
+
+int splat_comm_destroy(splat_ctx* ctx) {
+    if (!ctx) return SPLAT_OK;
+    if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+    comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    return SPLAT_OK;
+}
+
+int64_t splat_exchange_len(int32_t n, int32_t nranks, int32_t buckets) {
+    if (n < 0 || nranks < 1 || buckets < 1) return -1;
+    const int64_t a = (int64_t)nranks * buckets * 4;
+    return std::max(a, (59 * (int64_t)n + a - 1) / a * a);
+}
+
+int splat_exchange_step(splat_ctx* ctx, float* params, const float* grads, float* m, float* v, int32_t n,
+                        int64_t flat_len, const splat_adam_config* cfg, int32_t* step_count, uint32_t group_mask) {
+    if (!ctx || !cfg || !step_count || n < 0 || (n > 0 && (!params || !grads || !m || !v)))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "exchange_step: bad args");
+    const int t = *step_count;
+    int rc;
+    if (!ctx->comm) {  // one process: the plain step over the packed buffers
+        if ((rc = splat_adam_step_range(ctx, params, grads, m, v, n, 0, 59 * (int64_t)n, cfg, t, group_mask))) return rc;
+    } else {
+        const int nr = comm_ranks(ctx->comm), r = comm_rank(ctx->comm), B = ctx->comm_buckets;
+        const int64_t L = splat_exchange_len(n, nr, B);
+        if (flat_len < L) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "exchange_step: buffers not padded to splat_exchange_len");
+        const int64_t bucket = L / B, shard = bucket / nr;
+        CK(ctx->ex_shard.ensure((size_t)(B * shard) * 4), "alloc exchange shard");
+        float* sh = ctx->ex_shard.as<float>();
+        cudaStream_t cs = ctx->comm_stream, s = ctx->stream;
+        cudaEvent_t* ev_rs = ctx->ev_ex;           // [B]: bucket b reduced
+        cudaEvent_t* ev_ad = ctx->ev_ex + kMaxBuckets;  // [B]: bucket b's shard stepped
+        cudaEvent_t ev_in = ctx->ev_ex[2 * kMaxBuckets], ev_out = ctx->ev_ex[2 * kMaxBuckets + 1];
+        std::string err;
+        CK(cudaEventRecord(ev_in, s), "record");  // the gradients are complete
+        CK(cudaStreamWaitEvent(cs, ev_in, 0), "wait");
+        for (int b = 0; b < B; ++b) {
+            if (comm_reduce_scatter(ctx->comm, grads + b * bucket, sh + b * shard, (size_t)shard, cs, &err))
+                return set_err(ctx, SPLAT_ERR_NCCL, "exchange_step: " + err);
+            CK(cudaEventRecord(ev_rs[b], cs), "record");
+        }
+        for (int b = 0; b < B; ++b) {
+            const int64_t s0 = b * bucket + r * shard;
+            CK(cudaStreamWaitEvent(s, ev_rs[b], 0), "wait");
+            if ((rc = splat_adam_step_range(ctx, params, sh + b * shard, m, v, n, s0, shard, cfg, t, group_mask)))
+                return rc;
+            CK(cudaEventRecord(ev_ad[b], s), "record");
+            CK(cudaStreamWaitEvent(cs, ev_ad[b], 0), "wait");
+            // in place: this rank's shard is already at recv + r * shard
+            if (comm_all_gather(ctx->comm, params + s0, params + b * bucket, (size_t)shard, cs, &err))
+                return set_err(ctx, SPLAT_ERR_NCCL, "exchange_step: " + err);
+        }
+        CK(cudaEventRecord(ev_out, cs), "record");
+        CK(cudaStreamWaitEvent(s, ev_out, 0), "wait");
+    }
+    if (group_mask & SPLAT_GROUP_ROTATIONS) CK(launch_quat_normalize(ctx->lc, params + 6 * (int64_t)n, (int)n), "quat normalize");
+    *step_count = t + 1;
+    return SPLAT_OK;
+}
+
+int splat_allreduce(splat_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t op) {
+    if (!ctx || count < 0 || (count > 0 && !buf)) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "allreduce: bad args");
+    if (!ctx->comm || count == 0) return SPLAT_OK;
+    std::string err;
+    if (comm_all_reduce(ctx->comm, buf, buf, (size_t)count, dtype, op, ctx->stream, &err))
+        return set_err(ctx, SPLAT_ERR_NCCL, "allreduce: " + err);
     return SPLAT_OK;
 }
 
@@ -1790,7 +1895,31 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         CK(cudaStreamWaitEvent(s, prev_chain, 0), "join twin");
         ctx->twin_member = ctx->twin->twin_member = false;
     }
-    if ((rc = splat_adam_step(ctx, p, grads, moments, adam, step_count, group_mask))) return rc;
+    if (ctx->comm && group_mask) {
+        // view-parallel: the sharded exchange on the packed buffers (layout checked here)
+        const int64_t nn = p->n;
+        const bool packed = p->log_scales == p->centers + 3 * nn && p->rotations == p->centers + 6 * nn &&
+                            p->opacity_logits == p->centers + 10 * nn && p->sh == p->centers + 11 * nn &&
+                            grads->d_log_scales == grads->d_centers + 3 * nn &&
+                            grads->d_rotations == grads->d_centers + 6 * nn &&
+                            grads->d_opacity_logits == grads->d_centers + 10 * nn &&
+                            grads->d_sh == grads->d_centers + 11 * nn &&
+                            moments->m_log_scales == moments->m_centers + 3 * nn &&
+                            moments->m_rotations == moments->m_centers + 6 * nn &&
+                            moments->m_opacity == moments->m_centers + 10 * nn &&
+                            moments->m_sh == moments->m_centers + 11 * nn &&
+                            moments->v_log_scales == moments->v_centers + 3 * nn &&
+                            moments->v_rotations == moments->v_centers + 6 * nn &&
+                            moments->v_opacity == moments->v_centers + 10 * nn &&
+                            moments->v_sh == moments->v_centers + 11 * nn;
+        if (!packed) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "train_step: the exchange needs the packed layout");
+        if ((rc = splat_exchange_step(ctx, p->centers, grads->d_centers, moments->m_centers, moments->v_centers, p->n,
+                                      splat_exchange_len(p->n, comm_ranks(ctx->comm), ctx->comm_buckets), adam,
+                                      step_count, group_mask)))
+            return rc;
+    } else if ((rc = splat_adam_step(ctx, p, grads, moments, adam, step_count, group_mask))) {
+        return rc;
+    }
     if (loss_host) {
         if (ctx->host_loss_cap < n_views) {
             if (ctx->host_loss) cudaFreeHost(ctx->host_loss);

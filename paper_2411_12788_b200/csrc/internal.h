@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <utility>
 
 #include <cuda_runtime.h>
@@ -265,5 +266,18 @@ cudaError_t launch_knn_brute(LaunchCtx& lc, const float* p, int m, int k, float 
 cudaError_t launch_fill(LaunchCtx& lc, float* out, int m, float v);
 cudaError_t launch_reinit_set(LaunchCtx& lc, const float* points, const float* colors, const float* nn3, int m,
                               const splat_params_mut& out);
+
+
+// ---- comm.cu: the library's NCCL communicator (libnccl bound at run time) -------------------
+struct Comm;
+int comm_unique_id(void* id_out, std::string* err);
+Comm* comm_create(int nranks, int rank, const void* id, std::string* err);
+void comm_destroy(Comm* c);
+int comm_ranks(const Comm* c);
+int comm_rank(const Comm* c);
+int comm_reduce_scatter(Comm* c, const float* send, float* recv, size_t recv_count, cudaStream_t s, std::string* err);
+int comm_all_gather(Comm* c, const float* send, float* recv, size_t send_count, cudaStream_t s, std::string* err);
+int comm_all_reduce(Comm* c, const void* send, void* recv, size_t count, int dtype, int op, cudaStream_t s,
+                    std::string* err);
 
 }  // namespace splat_b200

@@ -48,7 +48,10 @@ class ViewTrainer:
     def __init__(self, params: DeviceGaussians, adam: Optional[capi.AdamConfig] = None,
                  group_mask: int = capi.GROUP_ALL, cfg: Optional[RasterConfig] = None,
                  background=(0.0, 0.0, 0.0), ctx: Optional[Context] = None, max_views: int = 64,
-                 process_group=None, lambda_dssim: float = 0.0, buckets: int = 4):
+                 process_group=None, lambda_dssim: float = 0.0, buckets: int = 4, native_comm: bool = False):
+        """native_comm: the exchange runs inside splat_train_step over the library's own NCCL
+        communicator (splat_comm_init; its unique id is broadcast through torch.distributed when
+        world_size > 1) instead of through torch.distributed collectives (exchange.py)."""
         torch = _torch()
         self.torch = torch
         self.ctx = ctx or Context.default()
@@ -66,15 +69,15 @@ class ViewTrainer:
         self.survivors_last_step: list[int] = []
         self.exchange: Optional[ShardedExchange] = None
         self.buckets = buckets
-        if self.world_size > 1:
+        self.native_comm = bool(native_comm)
+        if self.native_comm:
+            self._setup_native_comm()
+        elif self.world_size > 1:
             self._setup_exchange()
         self._gr = self.grads.struct()
 
-    def _setup_exchange(self) -> None:
-        """Packed buffers padded for the sharded exchange (params are re-pointed in place)."""
-        import torch.distributed as dist
+    def _pad_buffers(self, L: int) -> None:
         n = self.params.n
-        L = padded_len(n, self.world_size, self.buckets)
         self.params.ensure_flat_len(L)
         if self.grads.flat.numel() < L:
             self.grads = DeviceGrads(n, self.ctx.device, flat_len=L)
@@ -85,6 +88,30 @@ class ViewTrainer:
                 new = torch.zeros(L, dtype=torch.float32, device=old.device)
                 new[: 59 * n].copy_(old[: 59 * n])
                 setattr(self.opt, name, new)
+
+    def _setup_native_comm(self) -> None:
+        """The library's NCCL communicator on this context (one rank per process and GPU)."""
+        world = self.world_size
+        rank = 0
+        uid = (C.c_char * 128)()
+        if world > 1:
+            import torch.distributed as dist
+            rank = dist.get_rank(self.pg)
+            if rank == 0:
+                self.ctx.check(self.ctx.lib.splat_comm_unique_id(uid))
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=self.pg)
+            uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        else:
+            self.ctx.check(self.ctx.lib.splat_comm_unique_id(uid))
+        self.ctx.check(self.ctx.lib.splat_comm_init(self.ctx.h, world, rank, uid, self.buckets))
+        self._pad_buffers(int(self.ctx.lib.splat_exchange_len(self.params.n, world, self.buckets)))
+
+    def _setup_exchange(self) -> None:
+        """Packed buffers padded for the sharded exchange (params are re-pointed in place)."""
+        import torch.distributed as dist
+        n = self.params.n
+        self._pad_buffers(padded_len(n, self.world_size, self.buckets))
         self.exchange = ShardedExchange(n, self.world_size, dist.get_rank(self.pg), self.pg, self.buckets)
 
     @property
@@ -107,7 +134,9 @@ class ViewTrainer:
             raise LogicError("ViewTrainer: optimizer rows out of sync with the parameter set (remap the moments)")
         if self.grads.n != n:  # the set was densified / pruned: the gradient buffer follows its size
             self.grads = DeviceGrads(n, self.ctx.device)
-            if self.world_size > 1:
+            if self.native_comm:
+                self._pad_buffers(int(lib.splat_exchange_len(n, self.world_size, self.buckets)))
+            elif self.world_size > 1:
                 self._setup_exchange()
             self._gr = self.grads.struct()
         key = (self.params.centers.data_ptr(), self.params.sh.data_ptr(), self.params.n, self.params.active_sh_degree,
@@ -144,7 +173,7 @@ class ViewTrainer:
         several ranks: views + backward natively, NCCL all-reduce, then Adam."""
         self.ctx.bind_stream()
         ptrs = [t.data_ptr() for t in targets]
-        if self.world_size > 1:
+        if self.world_size > 1 and not self.native_comm:
             self._native(cams, ptrs, False, 0)
             self._finish_distributed()
         else:
@@ -158,7 +187,7 @@ class ViewTrainer:
         self.ctx.bind_stream()
         ptrs = [t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data for t in targets_host]
         out = np.zeros(len(cams), np.float32)
-        if self.world_size > 1:
+        if self.world_size > 1 and not self.native_comm:
             self._native(cams, ptrs, True, 0)
             self._finish_distributed()
             return self.loss[: len(cams)].cpu().numpy()

@@ -52,3 +52,67 @@ def test_sharded_adam_equals_full_step(n, world, buckets, mask):
     assert torch.equal(shard.flat[: 59 * n], full.flat[: 59 * n])
     assert torch.equal(m[: 59 * n], opt_full.m[: 59 * n]) and torch.equal(v[: 59 * n], opt_full.v[: 59 * n])
     assert not shard.flat[59 * n:].any() and not m[59 * n:].any()
+
+
+@pytest.mark.parametrize("mask", [capi.GROUP_ALL, capi.GROUP_CENTERS])
+def test_native_nccl_exchange_single_rank_equals_plain_step(mask):
+    """splat_train_step with the library's own NCCL communicator (one rank here: reduce-scatter and
+    all-gather over a 1-rank communicator, sharded Adam over its one shard per bucket) equals the
+    plain step bit for bit — this runs the C-ABI's NCCL exchange path end to end."""
+    from paper_2411_12788_b200 import scenes
+    from paper_2411_12788_b200.rasterizer import render
+    from paper_2411_12788_b200.trainer import ViewTrainer
+    s = scenes.make_gaussians(30_001, seed=4)
+    cams = [scenes.ring_camera(k, 6, width=320, height=214) for k in range(6)]
+    ctx_plain, ctx_comm = Context(0), Context(0)
+    pert = DeviceGaussians.from_host(scenes.perturbed(s))
+    targets = [render(pert, c, want_depth=False, ctx=ctx_plain).color.clone() for c in cams]
+    out = []
+    for ctx, native in ((ctx_plain, False), (ctx_comm, True)):
+        tr = ViewTrainer(DeviceGaussians.from_host(s), capi.AdamConfig(), group_mask=mask, ctx=ctx, max_views=3,
+                         buckets=3, native_comm=native)
+        tr.step(cams[:3], targets[:3])
+        tr.step_host(cams[3:], [t.cpu().pin_memory() for t in targets[3:]])
+        torch.cuda.synchronize()
+        out.append((tr.params.flat[: 59 * s.n].clone(), tr.opt.t))
+    assert out[0][1] == out[1][1] == 2
+    # the blend backward's float atomics make the summed gradients run-to-run different in the last
+    # bits, so the two trainers agree to rounding (the exchange itself is checked bitwise below)
+    d = (out[0][0] - out[1][0]).abs()
+    assert float((d > 1e-6).float().mean()) <= 1e-4 and float(d.max()) <= 0.2
+    ctx_comm.check(ctx_comm.lib.splat_comm_destroy(ctx_comm.h))
+
+
+def test_native_nccl_exchange_step_bitwise():
+    """splat_exchange_step over a 1-rank NCCL communicator == splat_adam_step, bit for bit."""
+    from paper_2411_12788_b200 import scenes
+    n, buckets = 40_003, 5
+    ctx_plain, ctx_comm = Context(0), Context(0)
+    uid = (C.c_char * 128)()
+    ctx_comm.check(ctx_comm.lib.splat_comm_unique_id(uid))
+    ctx_comm.check(ctx_comm.lib.splat_comm_init(ctx_comm.h, 1, 0, uid, buckets))
+    L = int(ctx_comm.lib.splat_exchange_len(n, 1, buckets))
+    assert L == padded_len(n, 1, buckets)
+    s = scenes.make_gaussians(n, seed=9)
+    rng = np.random.default_rng(1)
+    a = DeviceGaussians.from_host(s)
+    b = DeviceGaussians.from_host(s)
+    b.ensure_flat_len(L)
+    grads = DeviceGrads(n, flat_len=L)
+    grads.flat[: 59 * n] = torch.from_numpy(rng.normal(0, 1e-3, 59 * n).astype(np.float32)).cuda()
+    opt = OptimState(capi.AdamConfig(), n)
+    m, v = torch.zeros(L, device="cuda"), torch.zeros(L, device="cuda")
+    cfg = capi.AdamConfig()
+    t = C.c_int32(0)
+    for _ in range(3):
+        ctx_plain.bind_stream()
+        opt.step(a, grads, capi.GROUP_ALL, ctx_plain)
+        ctx_comm.bind_stream()
+        ctx_comm.check(ctx_comm.lib.splat_exchange_step(ctx_comm.h, b.flat.data_ptr(), grads.flat.data_ptr(),
+                                                        m.data_ptr(), v.data_ptr(), n, L, C.byref(cfg), C.byref(t),
+                                                        capi.GROUP_ALL))
+    torch.cuda.synchronize()
+    assert t.value == 3
+    assert torch.equal(a.flat[: 59 * n], b.flat[: 59 * n])
+    assert torch.equal(opt.m[: 59 * n], m[: 59 * n]) and torch.equal(opt.v[: 59 * n], v[: 59 * n])
+    ctx_comm.check(ctx_comm.lib.splat_comm_destroy(ctx_comm.h))
