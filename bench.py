@@ -43,9 +43,11 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=20,
                     help="extra steps after the timed region, with per-kernel CUDA events (breakdown/roofline)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, choices=(1, 4), default=1,
-                    help="1: the metric's workload (default); 4: BASELINE config 4, 3 M Gaussians, 8 views per rank "
-                         "from 256 ring views, all 59 gradients all-reduced, Adam on every group")
+    ap.add_argument("--config", type=int, choices=(1, 2, 3, 4), default=1,
+                    help="1: the metric's workload (default); 2: the depth + unprojection pass (3 M Gaussians, "
+                         "64 views); 3: the importance / visibility pass (700 K Gaussians, 200 views); 4: BASELINE "
+                         "config 4, 3 M Gaussians, 8 views per rank from 256 ring views, the 59N gradient exchange, "
+                         "Adam on every group")
     ap.add_argument("--views", type=int, default=None, help="ring views per rank per step (default 1, config 4: 8)")
     ap.add_argument("--gaussians", type=int, default=None, help="default 1 M (config 4: 3 M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -57,9 +59,11 @@ def parse():
     ap.add_argument("--buckets", type=int, default=4, help="exchange buckets (reduce-scatter / Adam pipelining)")
     a = ap.parse_args()
     if a.views is None:
-        a.views = 8 if a.config == 4 else 1
+        a.views = {4: 8, 2: 64, 3: 200}.get(a.config, 1)
     if a.gaussians is None:
-        a.gaussians = 3_000_000 if a.config == 4 else 1_000_000
+        a.gaussians = {4: 3_000_000, 2: 3_000_000, 3: 700_000}.get(a.config, 1_000_000)
+    if a.config in (2, 3) and "--steps" not in sys.argv:
+        a.steps, a.warmup, a.profile_steps = 5, 3, 1
     return a
 
 
@@ -505,10 +509,241 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------------------------
+# configs 2 and 3: the two per-view passes (depth + unprojection, importance / visibility)
+# ---------------------------------------------------------------------------------------------
+PASS_METRIC = {2: "depth+unproject views/s (3M Gaussians, 1237x822, 64 ring views, alpha>0.5, stride 4)",
+               3: "importance+visibility views/s (700K Gaussians, 1237x822, 200 ring views)"}
+
+
+def pass_config(args, world):
+    if args.config == 2:
+        return {"workload": "cfg2: depth render + unprojection of every pixel with alpha > 0.5 and (view*HW + pixel) "
+                            "% 4 == 0 over 64 ring views (aggressive densification's depth pass)",
+                "gaussians": args.gaussians, "log_scale_mean": "ln 0.005", "width": 1237, "height": 822,
+                "views_per_step": args.views, "n_ranks": world, "scene_seed": 0,
+                "l2": "inputs larger than L2 (708 MB parameters); 64 distinct views per step"}
+    return {"workload": "cfg3: accumulate_importance per view -> per-view visibility bitmask (max blend weight > "
+                        "1e-3), fp64 global importance, argmax counts, over 200 ring views",
+            "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_step": args.views,
+            "n_ranks": world, "scene_seed": 0,
+            "l2": "inputs larger than L2 (165 MB parameters); 200 distinct views per step"}
+
+
+def cpu_pass_views_per_s(args, threads):
+    """The reference's own render<float> (cfg 2: colour, alpha, depth, argmax; the unprojection loop
+    over the pixels is not included) or accumulate_importance<float> (cfg 3), one ring view per host
+    thread, all threads in parallel."""
+    from paper_2411_12788_b200 import scenes
+    from paper_2411_12788_b200.capi import Camera, Gaussians, RasterConfig
+    lib = C.CDLL(str(ROOT / "oracle" / "_ref" / "libsplat_ref_libm.so"))
+    ls = np.log(0.005) if args.config == 2 else np.log(0.02)
+    s = scenes.make_gaussians(args.gaussians, seed=0, log_scale_mean=ls)
+    arrs = [np.ascontiguousarray(a, np.float32) for a in (s.centers, s.log_scales, s.rotations, s.opacity_logits, s.sh)]
+    fp = C.POINTER(C.c_float)
+    g = Gaussians(*[a.ctypes.data_as(fp) for a in arrs], s.n, 3)
+    cfg = RasterConfig()
+    cams = [scenes.ring_camera(k, args.views) for k in range(threads)]
+    hw = 1237 * 822
+    errors = []
+
+    def work(i):
+        if args.config == 2:
+            col = np.empty(hw * 3, np.float32)
+            a = np.empty(hw, np.float32)
+            d = np.empty(hw, np.float32)
+            t = np.empty(hw, np.float32)
+            mc = np.empty(hw, np.int32)
+            bg = (C.c_float * 3)(0, 0, 0)
+            rc = lib.ref_render(C.byref(g), C.byref(cams[i]), C.byref(cfg), None, bg, col.ctypes.data_as(fp),
+                                a.ctypes.data_as(fp), d.ctypes.data_as(fp), t.ctypes.data_as(fp),
+                                mc.ctypes.data_as(C.POINTER(C.c_int32)), None, None, None, None)
+        else:
+            imp = np.empty(s.n, np.float32)
+            mw = np.empty(s.n, np.float32)
+            mp = np.empty(s.n, np.int32)
+            rc = lib.ref_accumulate_importance(C.byref(g), C.byref(cams[i]), C.byref(cfg), None, imp.ctypes.data_as(fp),
+                                               mw.ctypes.data_as(fp), mp.ctypes.data_as(C.POINTER(C.c_int32)))
+        if rc:
+            errors.append(rc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    if errors:
+        raise RuntimeError(f"reference pass failed: {errors[:3]}")
+    what = "render<float>" if args.config == 2 else "accumulate_importance<float>"
+    return {"value": threads / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{threads} threads x 1 cfg{args.config} ring view each through the reference's own {what}, "
+                      f"{wall:.1f} s wall"}
+
+
+def run_pass(args):
+    """Configs 2 / 3: one step = the whole multi-view pass (views partitioned across ranks, results
+    gathered in view order)."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    device = torch.cuda.current_device()
+    from paper_2411_12788_b200 import capi, multiview as MV, scenes
+    from paper_2411_12788_b200.rasterizer import Context, DeviceGaussians
+    ctx = Context.default(device)
+    ls = np.log(0.005) if args.config == 2 else np.log(0.02)
+    s = scenes.make_gaussians(args.gaussians, seed=0, log_scale_mean=ls)
+    ds = DeviceGaussians.from_host(s, device)
+    cams = [scenes.ring_camera(k, args.views) for k in range(args.views)]
+
+    def one_pass(set_):
+        if args.config == 2:
+            return MV.depth_points_views(set_, cams, rule=capi.DEPTH_RULE_ALPHA, alpha_threshold=0.5, stride=4,
+                                         seed=0, ctx=ctx)
+        return MV.visibility_pass_views(set_, cams, threshold=1e-3, ctx=ctx)
+
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(device)
+    clocks.start()
+    for _ in range(args.warmup):
+        out = one_pass(ds)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.monotonic()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = one_pass(ds)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.monotonic()
+    launches = ctx.launches() - launches0
+    clk = clocks.stop(t_wall0, t_wall1)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t_ms = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        ms = float(t_ms.item())
+    value = args.views * args.steps / (ms / 1000.0)
+    n_points = int(out[0].shape[0]) if args.config == 2 else None
+
+    # per-kernel breakdown (a profiled pass) and the per-view pair counts
+    ctx.lib.splat_profile_enable(ctx.h, 1)
+    one_pass(ds)
+    torch.cuda.synchronize()
+    names = C.create_string_buffer(4096)
+    tot = (C.c_double * 64)()
+    cnt = (C.c_int64 * 64)()
+    nk = C.c_int()
+    ctx.check(ctx.lib.splat_profile_read(ctx.h, names, 4096, tot, cnt, 64, C.byref(nk)))
+    ctx.lib.splat_profile_enable(ctx.h, 0)
+    kern = {nm: (tot[i], cnt[i]) for i, nm in enumerate(names.value.decode().split("\n")[: nk.value])}
+    ns_, np_ = C.c_int64(), C.c_int64()
+    pairs = []
+    for cam in cams[:: max(1, args.views // 8)]:
+        if args.config == 2:
+            from paper_2411_12788_b200.rasterizer import render
+            render(ds, cam, ctx=ctx, want_depth=True)
+        else:
+            MV.visibility_pass_views(ds, [cam], ctx=ctx)
+        ctx.lib.splat_forward_counts(ctx.h, C.byref(ns_), C.byref(np_), None, None)
+        pairs.append(np_.value)
+    avg_pairs = float(np.mean(pairs))
+
+    # e2e: the Gaussian set from pinned host memory, the pass, the results read back to the host
+    host_flat = ds.flat.cpu().pin_memory()
+    ds2 = DeviceGaussians(s.n, 3, device)
+    h2d = host_flat.numel() * 4
+    d2h = 0
+
+    def e2e_pass():
+        ds2.flat.copy_(host_flat, non_blocking=True)
+        res = one_pass(ds2)
+        return [r.cpu() for r in res]
+
+    for _ in range(2):
+        res = e2e_pass()
+    d2h = sum(r.numel() * r.element_size() for r in res)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_pass()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        t_ms = torch.tensor([ems], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        ems = float(t_ms.item())
+    e2e = {"value": args.views * args.steps / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h),
+           "path": "Gaussian set from pinned host memory -> device, the multiview pass through the C-ABI, "
+                   + ("points / views / pixels" if args.config == 2 else "bitmasks / fp64 importance / counts")
+                   + " read back to the host"}
+
+    peak, peak_src = 6453.1, "fallback"
+    try:
+        peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    dom = max(kern.items(), key=lambda kv: kv[1][0])[0] if kern else None
+    roof = None
+    if dom:
+        avg_ms = kern[dom][0] / max(kern[dom][1], 1)
+        hw = 1237 * 822
+        n = args.gaussians
+        # ids 4 P + records 48 B per Gaussian + outputs: cfg 2 colour / alpha / depth / argmax per
+        # pixel (24 B); cfg 3 the importance report (sum, max weight, argmax count: 12 B per Gaussian)
+        out_b = 24 * hw if args.config == 2 else 12 * n
+        ab = {"blend_forward": 4 * avg_pairs + 48 * n + out_b, "preprocess": 236 * n + 48 * n + 12 * n}.get(dom)
+        if ab:
+            achieved = ab / (avg_ms / 1000.0) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": ab,
+                    "avg_launch_ms": avg_ms, "peak_source": peak_src}
+        else:
+            roof = {"kernel": dom, "avg_launch_ms": avg_ms, "note": "no algorithmic-bytes model for this kernel"}
+    breakdown = {k: {"ms_per_step": v[0], "launches_per_step": v[1],
+                     "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads_default(args, 16)
+        try:
+            cpu = cpu_pass_views_per_s(args, threads)
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
+    if rank == 0:
+        line = {"metric": PASS_METRIC[args.config], "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": f"synthetic (seeded, BASELINE cfg{args.config} shapes)", "config": pass_config(args, world),
+                "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+                "pairs_per_view": avg_pairs, "kernel_breakdown": breakdown}
+        if n_points is not None:
+            line["points_per_step"] = n_points
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config in (2, 3):
+        run_pass(args)
     else:
         run_ours(args)
 
