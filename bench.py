@@ -371,8 +371,6 @@ def run_ours(args):
     for st in range(args.warmup, args.warmup + args.steps):
         c, t, _ = views_for(st)
         trainer.step(c, t)
-        pairs += trainer.pairs_last_step
-        survivors += trainer.survivors_last_step
     ev1.record(stream)
     torch.cuda.synchronize()
     t_wall1 = time.monotonic()
@@ -390,6 +388,8 @@ def run_ours(args):
     for st in range(args.warmup + args.steps, args.warmup + args.steps + p_steps):
         c, t, _ = views_for(st)
         trainer.step(c, t)
+        pairs += trainer.pairs_last_step  # (host queries outside the timed region)
+        survivors += trainer.survivors_last_step
     torch.cuda.synchronize()
     names = C.create_string_buffer(4096)
     tot = (C.c_double * 64)()

@@ -65,8 +65,6 @@ class ViewTrainer:
         self.pg = process_group
         # photometric loss weight (trainer.hpp:46; 0 = the L1-only BASELINE configs)
         self.lambda_dssim = float(lambda_dssim)
-        self.pairs_last_step: list[int] = []
-        self.survivors_last_step: list[int] = []
         self.exchange: Optional[ShardedExchange] = None
         self.buckets = buckets
         self.native_comm = bool(native_comm)
@@ -139,20 +137,32 @@ class ViewTrainer:
             elif self.world_size > 1:
                 self._setup_exchange()
             self._gr = self.grads.struct()
-        key = (self.params.centers.data_ptr(), self.params.sh.data_ptr(), self.params.n, self.params.active_sh_degree,
-               self.opt.m.data_ptr())
-        if key != getattr(self, "_ckey", None):  # ctypes views of the parameter / moment buffers
+        # ctypes views of the parameter / moment buffers, rebuilt only when a buffer is replaced
+        key = (id(self.params.flat), n, self.params.active_sh_degree, id(self.opt.m), id(self.opt.v))
+        if key != getattr(self, "_ckey", None):
             self._ckey, self._pm, self._mo = key, self.params.mut(), self.opt._moments()
+            self._loss_ptr = self.loss.data_ptr()
         self.ctx.check(lib.splat_train_step(
             h, C.byref(self._pm), C.byref(self._gr), C.byref(self._mo), C.byref(self.opt.config),
             C.byref(t), group_mask, cam_arr, v, tp, 1 if on_host else 0, C.byref(self.cfg), self.bg,
-            self.lambda_dssim, self.loss.data_ptr(), loss_host))
+            self.lambda_dssim, self._loss_ptr, loss_host))
         if group_mask:
             self.opt.t = t.value
+        self._views_last_step = v
+
+    def _last_counts(self):
         ns_, np_ = C.c_int64(), C.c_int64()
-        lib.splat_forward_counts(h, C.byref(ns_), C.byref(np_), None, None)  # the last view's
-        self.pairs_last_step = [np_.value] * v
-        self.survivors_last_step = [ns_.value] * v
+        self.ctx.lib.splat_forward_counts(self.ctx.h, C.byref(ns_), C.byref(np_), None, None)  # the last view's
+        return ns_.value, np_.value
+
+    @property
+    def pairs_last_step(self) -> list[int]:
+        """Tile-Gaussian pairs of the last step's views (the last view's count, per view)."""
+        return [self._last_counts()[1]] * getattr(self, "_views_last_step", 0)
+
+    @property
+    def survivors_last_step(self) -> list[int]:
+        return [self._last_counts()[0]] * getattr(self, "_views_last_step", 0)
 
     def _views(self, cams: Sequence[Camera], targets) -> None:
         """Render + loss + backward of the views (gradients summed), no optimiser step."""
