@@ -416,6 +416,14 @@ def run_ours(args):
     total_views = world * V * args.steps
     value = total_views / (ms / 1000.0)
 
+    # ---- V / C of one ring view (traverse_pixel visits and commits; a measurement pass) -----------
+    vc = None
+    if rank == 0 and args.config in (1, 4):
+        from paper_2411_12788_b200.rasterizer import render, traversal_counts
+        render(trainer.params, cams[0], ctx=ctx, want_depth=False)
+        vc = traversal_counts(ctx)
+        torch.cuda.synchronize()
+
     # ---- e2e through the public API with host buffers -------------------------------------------
     e2e = None
     if not args.no_e2e:
@@ -472,14 +480,35 @@ def run_ours(args):
             if ncu:
                 roof["traffic"] = ncu.get("dram_bytes_per_launch")
                 roof["ncu"] = ncu
+    # FP32 peak: SMs x 128 lanes x 2 flop x the SM clock under load (nvidia-smi median in the timed
+    # region), and at the maximum clock
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    clk_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    fp32_peak = sms * 128 * 2 * clk_mhz * 1e6 / 1e12  # TFLOP/s
+    if roof and vc and dom in ("blend_backward", "blend_forward"):
+        V, Cc = vc
+        fl = (15.0 * V + 45.0 * Cc) if dom == "blend_backward" else (15.0 * V + 12.0 * Cc)
+        tf = fl / (roof["avg_launch_ms"] / 1000.0) / 1e12
+        roof.update({"flops_per_launch": fl, "achieved_tflops": tf, "fp32_peak_tflops": fp32_peak,
+                     "fp32_frac": tf / fp32_peak, "frac_max": max(roof["frac"], tf / fp32_peak),
+                     "flops_model": "SURVEY.md 8d: backward 15 V + 45 C, forward 15 V + 12 C (V, C measured)"})
     # whole-step roofline (SURVEY.md §8d compulsory traffic: 1020 N + 12 P + 60 HW bytes per view at
-    # config 1, Adam on means), against the measured HBM peak
+    # config 1, Adam on means; FP32 work 600 N + 15 V + 12 C (fwd) + 15 V + 45 C (bwd) + 900 N (chain)),
+    # max(bytes / HBM peak, flops / FP32 peak) / measured time
     step_roof = None
     if args.config == 1 and n_views:
         bpv = 1020.0 * n + 12.0 * avg_pairs + 60.0 * hw
         ach = bpv * value / world / 1e9  # per GPU
         step_roof = {"bytes_per_view": bpv, "achieved_gbs_per_gpu": ach, "peak": peak, "frac": ach / peak,
                      "note": "SURVEY.md 8d algorithmic bytes of the whole view (fwd + bwd + Adam on means)"}
+        if vc:
+            V, Cc = vc
+            fpv = 1500.0 * n + 30.0 * V + 57.0 * Cc
+            t_view = world / value  # s per view per GPU
+            step_roof.update({"visits_per_view": V, "commits_per_view": Cc, "flops_per_view": fpv,
+                              "achieved_tflops_per_gpu": fpv / t_view / 1e12, "fp32_peak_tflops": fp32_peak,
+                              "fp32_frac": fpv / t_view / 1e12 / fp32_peak,
+                              "frac_max": max(bpv / (peak * 1e9), fpv / (fp32_peak * 1e12)) / t_view})
     breakdown = {k: {"ms_per_step": v[0] / p_steps, "launches_per_step": v[1] / p_steps,
                      "share": v[0] / max(sum(x[0] for x in kern.values()), 1e-9)} for k, v in kern.items()}
 
@@ -501,7 +530,9 @@ def run_ours(args):
                 "data": f"synthetic (seeded, BASELINE cfg{args.config} shapes)",
                 "config": workload_config(args, world), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
-                "pairs_per_view": avg_pairs, "survivors_per_view": n_surv, "kernel_breakdown": breakdown}
+                "pairs_per_view": avg_pairs, "survivors_per_view": n_surv,
+                "visits_per_view": vc[0] if vc else None, "commits_per_view": vc[1] if vc else None,
+                "kernel_breakdown": breakdown}
         if allreduce:
             line["allreduce"] = allreduce
         print(json.dumps(line))

@@ -462,6 +462,10 @@ int splat_exclusive_scan(splat_ctx* ctx, const uint32_t* in_dev, uint32_t* out_d
 /* n_survivors / n_pairs of the last forward. */
 int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs,
                          int32_t* tiles_x, int32_t* tiles_y);
+/* traverse_pixel statistics of the last forward (rasterizer.hpp:116-147; SURVEY §8d's V and C):
+ * list entries visited (the breaking sample included) and samples committed, summed over the
+ * pixels.  A measurement pass (one plain thread per pixel over the per-tile lists), synchronous. */
+int splat_traversal_counts(splat_ctx* ctx, int64_t* visits, int64_t* commits);
 /* Per Gaussian (index order): rect[4] = x0,x1,y0,y1 (0,0,0,0 when culled), radius,
  * depth bits, survivor flag. Any pointer may be NULL. */
 int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* depth,

@@ -281,6 +281,7 @@ _EXPORTS = {
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "splat_forward_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "splat_traversal_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "splat_project_debug": (C.c_int, [C.c_void_p, ip, ip, fp, u8p, fp, fp, fp, fp]),
     "splat_tiles_debug": (C.c_int, [C.c_void_p, ip, ip, ip, ip]),
 }

@@ -1255,6 +1255,26 @@ int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs,
     return SPLAT_OK;
 }
 
+int splat_traversal_counts(splat_ctx* ctx, int64_t* visits, int64_t* commits) {
+    if (!ctx || !visits || !commits) return SPLAT_ERR_INVALID_ARGUMENT;
+    const FwdState& st = ctx->st;
+    if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
+    *visits = *commits = 0;
+    if (st.n == 0 || st.n_pairs == 0) return SPLAT_OK;
+    CK(ctx->dscalar.ensure(64), "alloc");
+    CK(cudaMemsetAsync(ctx->dscalar.p, 0, 16, ctx->stream), "zero counts");
+    unsigned long long* d = ctx->dscalar.as<unsigned long long>();
+    CK(launch_traversal_counts(ctx->lc, st.cp, ctx->ranges.as<uint32_t>(), ctx->pair_gauss[st.pairs_in_alt ? 1 : 0].as<uint32_t>(),
+                               ctx->rec.as<ProjRec>(), ctx->rect_ref.as<uint2>(), d),
+       "traversal counts");
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, ctx->stream), "read counts");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    *visits = (int64_t)h[0];
+    *commits = (int64_t)h[1];
+    return SPLAT_OK;
+}
+
 int splat_project_debug(splat_ctx* ctx, int32_t* rect, int32_t* radius, float* depth, uint8_t* survivor, float* mean2d,
                         float* conic, float* color, float* opacity) {
     if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;

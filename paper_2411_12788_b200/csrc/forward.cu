@@ -661,6 +661,54 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp
     }
 }
 
+// Traversal statistics of the reference's traverse_pixel (rasterizer.hpp:116-147) over the forward's
+// per-tile lists, per pixel and plain (one thread per pixel, no culls): V = list entries visited
+// (the breaking sample included), C = samples committed.  A measurement kernel (bench / tests),
+// not on the training path; gates in the reference's operation order (this file: --fmad=false).
+__global__ void traversal_counts_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
+                                        const uint32_t* __restrict__ pair_gauss, const ProjRec* __restrict__ rec,
+                                        const uint2* __restrict__ rect_ref, unsigned long long* __restrict__ out) {
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = 0, c = 0;
+    if (pix < (int64_t)cp.width * cp.height) {
+        const int px = (int)(pix % cp.width), py = (int)(pix / cp.width);
+        const int tile = (py / cp.tile_size) * cp.tiles_x + px / cp.tile_size;
+        const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+        const float x = (float)px + 0.5f, y = (float)py + 0.5f;
+        float T = 1.0f;
+        for (uint32_t k = start; k < end; ++k) {
+            const uint32_t gid = pair_gauss[k];
+            ++v;
+            const uint2 rr = rect_ref[gid];
+            if (px < (int)(rr.x & 0xffffu) || px >= (int)(rr.x >> 16) || py < (int)(rr.y & 0xffffu) ||
+                py >= (int)(rr.y >> 16))
+                continue;
+            const ProjRec r = rec[gid];
+            const float dx = r.r0.x - x, dy = r.r0.y - y;
+            const float power = -0.5f * (r.r0.z * dx * dx + r.r1.x * dy * dy) - r.r0.w * dx * dy;
+            if (power > 0.0f) continue;
+            float a = r.r1.y * splat_expf(power);
+            if (cp.apply_thresholds) {
+                if (a > cp.alpha_max) a = cp.alpha_max;
+                if (a < cp.contribution_min) continue;
+            }
+            const float next = T * (1.0f - a);
+            if (cp.apply_thresholds && next < cp.transmittance_min) break;
+            ++c;
+            T = next;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (v || c)) {
+        atomicAdd(out, v);
+        atomicAdd(out + 1, c);
+    }
+}
+
 __global__ void unproject_flags_kernel(int width, int height, const int32_t* __restrict__ max_contributor,
                                        const float* __restrict__ alpha, int rule, float thr, int64_t view_index,
                                        int32_t stride, int64_t seed, uint32_t* __restrict__ flags) {
@@ -804,6 +852,17 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
         count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev);
     }
     lc.count += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_traversal_counts(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+                                    const uint32_t* pair_gauss, const ProjRec* rec, const uint2* rect_ref,
+                                    unsigned long long* out) {
+    const int64_t hw = (int64_t)cp.width * cp.height;
+    if (hw == 0) return cudaSuccess;
+    traversal_counts_kernel<<<(unsigned)((hw + 255) / 256), 256, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, rect_ref,
+                                                                                 out);
+    lc.count++;
     return cudaGetLastError();
 }
 

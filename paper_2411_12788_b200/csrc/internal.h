@@ -151,6 +151,11 @@ struct FwdOutputs {
 constexpr int kBlockList = 2048;      // replay-list capacity per 8 x 8 block
 constexpr int kBlockListSmem = 512;   // entries the backward maps through shared memory
 
+// traverse_pixel statistics (V visits, C commits) of the last forward's lists: out[0..1] += (V, C).
+cudaError_t launch_traversal_counts(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+                                    const uint32_t* pair_gauss, const ProjRec* rec, const uint2* rect_ref,
+                                    unsigned long long* out);
+
 // K6 (+K7 depth epilogue): per-tile front-to-back blend.
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
                                  const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux,

@@ -467,6 +467,16 @@ def forward_debug(ctx: Optional[Context] = None) -> dict:
                 gaussian=gauss[:P], ranges=ranges, order=order[: ns.value])
 
 
+def traversal_counts(ctx: Optional[Context] = None) -> tuple[int, int]:
+    """(V, C) of the preceding forward: traverse_pixel list visits and committed samples summed over
+    the pixels (a measurement pass, synchronous)."""
+    ctx = ctx or Context.default()
+    v, c = C.c_int64(), C.c_int64()
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_traversal_counts(ctx.h, C.byref(v), C.byref(c)))
+    return v.value, c.value
+
+
 def project_debug(n: int, ctx: Optional[Context] = None) -> dict:
     ctx = ctx or Context.default()
     rect = np.zeros((max(n, 1), 4), np.int32)

@@ -52,6 +52,13 @@ RAW = {
     "registers": "launch__registers_per_thread",
     "l2_hit": "lts__t_sector_hit_rate.pct",
     "inst": "smsp__inst_executed.sum",
+    # pipe utilisation (% of peak, active cycles) and SIMT efficiency (threads per warp instruction)
+    "pipe_fma": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "pipe_alu": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "pipe_xu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "pipe_lsu": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "fma_cycles": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "simt": "smsp__thread_inst_executed_per_inst_executed.ratio",
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9,
               "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
@@ -96,7 +103,8 @@ def summarise(reps):
             e["launches"] += 1
             e["duration_us"] += (d["duration_ns"] or 0) / 1e3
             e["dram_bytes"] += (d["dram_read"] or 0) + (d["dram_write"] or 0)
-            for k in ("ipc", "issue_active", "occupancy", "registers", "l2_hit", "inst"):
+            for k in ("ipc", "issue_active", "occupancy", "registers", "l2_hit", "inst", "pipe_fma", "pipe_alu", "pipe_xu",
+                      "pipe_lsu", "fma_cycles", "simt"):
                 if d[k] is not None:
                     e[k] = d[k]
             e["top_stalls"] = {k: round(v / tot, 3) for k, v in top}
@@ -114,14 +122,16 @@ def main(reps):
     old["note"] = ("ncu --set full --clock-control none captures (cold caches, serialised replays): use shares and "
                    "per-launch DRAM bytes, not absolute times; regenerate with profiles/summarize_ncu.py")
     path.write_text(json.dumps(old, indent=1, sort_keys=True) + "\n")
-    lines = ["| kernel | launches | us/launch | DRAM MB/launch | DRAM GB/s | issue % | IPC | occ % | regs | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| kernel | launches | us/launch | DRAM MB/launch | DRAM GB/s | issue % | IPC | occ % | regs | FMA pipe % | "
+             "ALU % | XU % | LSU % | SIMT (thr/inst) | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for name, e in sorted(old["kernels"].items(), key=lambda kv: -kv[1]["duration_us"]):
         st = ", ".join(f"{k} {v:.0%}" for k, v in e.get("top_stalls", {}).items())
         lines.append(f"| {name} | {e['launches']} | {e['duration_us_per_launch']:.1f} | "
                      f"{e['dram_bytes_per_launch'] / 1e6:.1f} | {e['dram_gbs'] or 0:.0f} | "
                      f"{e.get('issue_active', 0):.1f} | {e.get('ipc', 0):.2f} | {e.get('occupancy', 0):.1f} | "
-                     f"{e.get('registers', 0):.0f} | {st} |")
+                     f"{e.get('registers', 0):.0f} | {e.get('pipe_fma') or 0:.1f} | {e.get('pipe_alu') or 0:.1f} | "
+                     f"{e.get('pipe_xu') or 0:.1f} | {e.get('pipe_lsu') or 0:.1f} | {e.get('simt') or 0:.1f} | {st} |")
     (HERE / "ncu_summary.md").write_text("# ncu --set full summary (per launch)\n\n" + "\n".join(lines) + "\n")
     print("\n".join(lines))
 

@@ -326,3 +326,17 @@ def test_invalid_arguments():
         R.render_backward(s, cam, RasterConfig(), np.zeros((3, 3, 3), np.float32))
     with pytest.raises(ValueError):
         R.render(s, cam, RasterConfig(tile_size=12))
+
+
+@pytest.mark.parametrize("tile", [16, 32])
+def test_traversal_counts_equal_oracle(oracle, tile):
+    """V (list visits) and C (commits) of traverse_pixel, counted on the GPU over the forward's
+    lists, equal the oracle's counts exactly (SURVEY.md §8d workload symbols)."""
+    s, cam = cfg0_scene()
+    cfg = RasterConfig()
+    cfg.tile_size = tile
+    R.render(s, cam, cfg)
+    v, c = R.traversal_counts()
+    want = oracle.render(s, cam, cfg, report=False)
+    assert (v, c) == (want["visits"], want["commits"])
+    assert 0 < c < v
