@@ -531,41 +531,74 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
                     }
                 }
             } else {
+                // accumulate_importance (rasterizer.cpp:184-193): the training loop's branch-free
+                // pair form; each entry's per-warp weight sum and maximum go to shared memory
+                // (combining the CTA's two warps), then one global atomic pair per entry and batch.
                 const int lane = tid & 31;
-                for (int j = 0; j < cnt; ++j) {
+                for (int j = 0; j < cnt; j += 2) {
                     if (__all_sync(0xffffffffu, done)) break;
-                    float w = 0.0f;
-                    const float4 r1 = lds_f4(a_r1 + 16u * j);
-                    if (!(__float_as_uint(r1.z) & wrows) || !(__float_as_uint(r1.z) & wcols)) continue;  // misses this warp
-                    if (!done) {
-                        float alpha, g2d, dx, dy;
-                        bool clamped;
-                        const float4 r0 = lds_f4(a_r0 + 16u * j);
-                        if (gate_sample<THR>(r0, r1, mybits, x, y, amax_c, cmin, alpha, g2d, clamped, dx, dy)) {
-                            const float next = T * (1.0f - alpha);
-                            if (THR && next < tmin) {
-                                done = true;
-                            } else {
-                                w = T * alpha;
-                                const float4 r2 = lds_f4(a_r2 + 16u * j);
-                                acc0 = acc0 + w * r2.x;
-                                acc1 = acc1 + w * r2.y;
-                                acc2 = acc2 + w * r2.z;
-                                if (ARG && w > wmax) {
-                                    wmax = w;
-                                    amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
-                                }
-                                last = (int32_t)lds_u32(a_idx + 4u * j);
-                                T = next;
-                            }
-                        }
+                    const bool has_b = j + 1 < cnt;
+                    const uint32_t jb = has_b ? (uint32_t)(j + 1) : (uint32_t)j;
+                    const float4 r1a = lds_f4(a_r1 + 16u * j);
+                    const float4 r1b = lds_f4(a_r1 + 16u * jb);
+                    const uint32_t ma = __float_as_uint(r1a.z), mb = __float_as_uint(r1b.z);
+                    const bool wa = (ma & wrows) && (ma & wcols);  // warp-uniform: rect meets the patch
+                    const bool wb = has_b && (mb & wrows) && (mb & wcols);
+                    if (!wa && !wb) continue;
+                    const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
+                    float alpha_a, alpha_b, g2d, dx, dy;
+                    bool clamped;
+                    const bool ga = gate_sample_nb<THR>(r0a, r1a, mybits, x, y, amax_c, cmin, alpha_a, g2d, clamped, dx,
+                                                        dy) && wa && !done;
+                    const bool gb = gate_sample_nb<THR>(r0b, r1b, mybits, x, y, amax_c, cmin, alpha_b, g2d, clamped, dx,
+                                                        dy) && wb && !done;
+                    const float na = T * (1.0f - alpha_a);
+                    const bool sa = THR && ga && na < tmin;
+                    const bool ca = ga && !sa;
+                    const float wa_ = ca ? T * alpha_a : 0.0f;
+                    {
+                        const float4 r2a = lds_f4(a_r2 + 16u * j);
+                        acc0 = ca ? acc0 + wa_ * r2a.x : acc0;
+                        acc1 = ca ? acc1 + wa_ * r2a.y : acc1;
+                        acc2 = ca ? acc2 + wa_ * r2a.z : acc2;
                     }
-                    if (__any_sync(0xffffffffu, w > 0.0f)) {
-                        const float sum = warp_sum(w);
-                        const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
+                    if (ARG && ca && wa_ > wmax) {
+                        wmax = wa_;
+                        amax_gid = (int32_t)lds_u32(a_gid + 4u * j);
+                    }
+                    T = ca ? na : T;
+                    const bool gb2 = gb && !sa;
+                    const float nb = T * (1.0f - alpha_b);
+                    const bool sb = THR && gb2 && nb < tmin;
+                    const bool cb = gb2 && !sb;
+                    const float wb_ = cb ? T * alpha_b : 0.0f;
+                    {
+                        const float4 r2b = lds_f4(a_r2 + 16u * jb);
+                        acc0 = cb ? acc0 + wb_ * r2b.x : acc0;
+                        acc1 = cb ? acc1 + wb_ * r2b.y : acc1;
+                        acc2 = cb ? acc2 + wb_ * r2b.z : acc2;
+                    }
+                    if (ARG && cb && wb_ > wmax) {
+                        wmax = wb_;
+                        amax_gid = (int32_t)lds_u32(a_gid + 4u * jb);
+                    }
+                    T = cb ? nb : T;
+                    done = done || sa || sb;
+                    // weights are >= 0: their float bits order like the values (max over the warp)
+                    if (__any_sync(0xffffffffu, ca)) {
+                        const float sum = warp_sum(wa_);
+                        const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(wa_));
                         if (lane == 0) {
                             atomicAdd(&s_imp[j], sum);
                             atomicMax(&s_maxw[j], mx);
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, cb)) {
+                        const float sum = warp_sum(wb_);
+                        const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(wb_));
+                        if (lane == 0) {
+                            atomicAdd(&s_imp[jb], sum);
+                            atomicMax(&s_maxw[jb], mx);
                         }
                     }
                 }
