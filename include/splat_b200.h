@@ -462,6 +462,27 @@ int splat_exclusive_scan(splat_ctx* ctx, const uint32_t* in_dev, uint32_t* out_d
 /* n_survivors / n_pairs of the last forward. */
 int splat_forward_counts(splat_ctx* ctx, int64_t* n_survivors, int64_t* n_pairs,
                          int32_t* tiles_x, int32_t* tiles_y);
+/* ProjectedGaussian<float> (rasterizer.hpp:27-41). */
+typedef struct splat_projected {
+    float mean2d[2];
+    float cov2d[3];          /* xx, xy, yy after the low-pass */
+    float conic[3];
+    float depth_mean;
+    int32_t radius;
+    int32_t index;
+    float opacity;
+    float color[3];
+    int32_t x0, x1, y0, y1;  /* pixel rect, half-open */
+    float center_world[3];
+    float cov_world_inv[9];  /* row-major (symmetric: the cofactor inverse is exactly symmetric) */
+    int32_t cov_degenerate;
+} splat_projected;
+/* project<float> (rasterizer.cpp:10-90): the survivors' records sorted by (depth, index), written
+ * to out_host[0 .. *count) (host memory, capacity records; SPLAT_ERR_INVALID_ARGUMENT with *count
+ * set when it is too small).  Runs the forward (also leaves its state for the debug getters). */
+int splat_project(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                  const uint8_t* mask, splat_projected* out_host, int64_t capacity, int32_t* count);
+
 /* traverse_pixel statistics of the last forward (rasterizer.hpp:116-147; SURVEY §8d's V and C):
  * list entries visited (the breaking sample included) and samples committed, summed over the
  * pixels.  A measurement pass (one plain thread per pixel over the per-tile lists), synchronous. */

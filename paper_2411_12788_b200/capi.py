@@ -115,6 +115,25 @@ class ImportanceOutputs(C.Structure):
     _fields_ = [("importance", fp), ("max_weight", fp), ("max_pixel_count", ip)]
 
 
+class Projected(C.Structure):
+    """splat_projected — ProjectedGaussian<float> (rasterizer.hpp:27-41)."""
+
+    _fields_ = [
+        ("mean2d", C.c_float * 2),
+        ("cov2d", C.c_float * 3),
+        ("conic", C.c_float * 3),
+        ("depth_mean", C.c_float),
+        ("radius", C.c_int32),
+        ("index", C.c_int32),
+        ("opacity", C.c_float),
+        ("color", C.c_float * 3),
+        ("x0", C.c_int32), ("x1", C.c_int32), ("y0", C.c_int32), ("y1", C.c_int32),
+        ("center_world", C.c_float * 3),
+        ("cov_world_inv", C.c_float * 9),
+        ("cov_degenerate", C.c_int32),
+    ]
+
+
 class ParamGrads(C.Structure):
     _fields_ = [
         ("d_centers", fp),
@@ -281,6 +300,8 @@ _EXPORTS = {
     "splat_exclusive_scan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "splat_forward_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "splat_project": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera), C.POINTER(RasterConfig), u8p,
+                                C.c_void_p, C.c_int64, C.POINTER(C.c_int32)]),
     "splat_traversal_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "splat_project_debug": (C.c_int, [C.c_void_p, ip, ip, fp, u8p, fp, fp, fp, fp]),
     "splat_tiles_debug": (C.c_int, [C.c_void_p, ip, ip, ip, ip]),

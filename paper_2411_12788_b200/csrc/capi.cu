@@ -162,6 +162,9 @@ struct splat_ctx {
     DevBuf tgt_stage, step_loss;
     // per 8 x 8 block: the staged list entries the forward walked (replayed by the backward)
     DevBuf blist, bidx, bcount;
+    // splat_project: the forward also records cov2d and the radius per Gaussian
+    bool want_proj = false;
+    DevBuf proj_dbg;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_free = nullptr, ev_copied[8] = {};
     uint32_t* host_counters = nullptr;  // mapped pinned [n_surv, Ps, P], written by preprocess's last block
@@ -343,6 +346,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     CK(ctx->tile_counts.ensure(nn * 4), "alloc counts");
     CK(ctx->depth.ensure(nn * 4), "alloc depth");
     CK(ctx->rect_ref.ensure(nn * 8), "alloc rects");
+    if (ctx->want_proj) CK(ctx->proj_dbg.ensure(nn * 16), "alloc projection records");
     CK(ctx->counts_sorted.ensure(nn * 4), "alloc counts");
     CK(ctx->offsets.ensure((nn + 1) * 4), "alloc offsets");
     CK(ctx->counters.ensure(64, true, s), "alloc counters");  // zero at rest (preprocess re-zeroes them)
@@ -373,7 +377,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev),
+                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr),
            "preprocess");
         // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
         // writes them to mapped pinned memory, so the host waits only for preprocess (event) while
@@ -1272,6 +1276,72 @@ int splat_traversal_counts(splat_ctx* ctx, int64_t* visits, int64_t* commits) {
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     *visits = (int64_t)h[0];
     *commits = (int64_t)h[1];
+    return SPLAT_OK;
+}
+
+int splat_project(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
+                  const uint8_t* mask, splat_projected* out, int64_t capacity, int32_t* count) {
+    if (!ctx || !count) return SPLAT_ERR_INVALID_ARGUMENT;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    *count = 0;
+    const size_t hw = (size_t)(cam ? cam->width : 0) * (cam ? cam->height : 0);
+    CK(ctx->d_color_buf.ensure(hw * 4 + 4), "alloc depth");
+    const splat_render_outputs ro{nullptr, nullptr, ctx->d_color_buf.as<float>(), nullptr, nullptr};
+    const float zero[3] = {0, 0, 0};
+    ctx->want_proj = true;
+    rc = run_forward(ctx, g, cam, cfg, mask, zero, &ro, nullptr);
+    ctx->want_proj = false;
+    if (rc) return rc;
+    const FwdState& st = ctx->st;
+    const int n = st.n, m = st.n_surv;
+    *count = m;
+    if (m == 0) return SPLAT_OK;
+    if (!out || capacity < m) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "project: output capacity too small");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    std::vector<ProjRec> rec(n);
+    std::vector<AuxRec> aux(n);
+    std::vector<float4> dbg(n);
+    std::vector<uint2> rect(n);
+    std::vector<float> depth(n);
+    std::vector<uint32_t> order(m);
+    CK(cudaMemcpy(rec.data(), ctx->rec.p, sizeof(ProjRec) * n, cudaMemcpyDeviceToHost), "copy records");
+    CK(cudaMemcpy(aux.data(), ctx->aux.p, sizeof(AuxRec) * n, cudaMemcpyDeviceToHost), "copy aux");
+    CK(cudaMemcpy(dbg.data(), ctx->proj_dbg.p, 16 * (size_t)n, cudaMemcpyDeviceToHost), "copy cov2d");
+    CK(cudaMemcpy(rect.data(), ctx->rect_ref.p, 8 * (size_t)n, cudaMemcpyDeviceToHost), "copy rects");
+    CK(cudaMemcpy(depth.data(), ctx->depth.p, 4 * (size_t)n, cudaMemcpyDeviceToHost), "copy depths");
+    CK(cudaMemcpy(order.data(), st.order, 4 * (size_t)m, cudaMemcpyDeviceToHost), "copy order");
+    for (int r = 0; r < m; ++r) {  // project's result, sorted by (depth, index) (rasterizer.cpp:85-88)
+        const uint32_t i = order[r];
+        splat_projected& o = out[r];
+        const ProjRec& q = rec[i];
+        const AuxRec& a = aux[i];
+        o.mean2d[0] = q.r0.x;
+        o.mean2d[1] = q.r0.y;
+        o.cov2d[0] = dbg[i].x;
+        o.cov2d[1] = dbg[i].y;
+        o.cov2d[2] = dbg[i].z;
+        o.conic[0] = q.r0.z;
+        o.conic[1] = q.r0.w;
+        o.conic[2] = q.r1.x;
+        o.depth_mean = depth[i];
+        std::memcpy(&o.radius, &dbg[i].w, 4);
+        o.index = (int32_t)i;
+        o.opacity = q.r1.y;
+        o.color[0] = q.r2.x;
+        o.color[1] = q.r2.y;
+        o.color[2] = q.r2.z;
+        o.x0 = (int32_t)(rect[i].x & 0xffffu);
+        o.x1 = (int32_t)(rect[i].x >> 16);
+        o.y0 = (int32_t)(rect[i].y & 0xffffu);
+        o.y1 = (int32_t)(rect[i].y >> 16);
+        o.center_world[0] = a.a0.x;
+        o.center_world[1] = a.a0.y;
+        o.center_world[2] = a.a0.z;
+        o.cov_degenerate = a.a0.w != 0.0f ? 1 : 0;
+        const float inv[9] = {a.a1.x, a.a1.y, a.a1.z, a.a1.y, a.a1.w, a.a2.x, a.a1.z, a.a2.x, a.a2.y};  // symmetric
+        std::memcpy(o.cov_world_inv, inv, sizeof(inv));
+    }
     return SPLAT_OK;
 }
 

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ tile_counts,
                                                         uint32_t* __restrict__ n_surv, float* __restrict__ depth_out,
-                                                        uint2* __restrict__ rect_ref) {
+                                                        uint2* __restrict__ rect_ref, float4* __restrict__ proj_dbg) {
     __shared__ float4 s_sh[VEC_SH ? kPreThreads * kShRow : 1];
     pdl_wait();
     pdl_trigger();
@@ -197,12 +197,13 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
             const float inv_det = 1.0f / det;
             const float k0 = c2 * inv_det, k1 = -c1 * inv_det, k2 = c0 * inv_det;
             int x0, x1, y0, y1;
+            int radius = max(cp.width, cp.height);  // exact mode (rasterizer.cpp:53-56)
             if (!cp.apply_thresholds) {
                 x0 = 0; x1 = cp.width; y0 = 0; y1 = cp.height;
             } else {
                 const float mid = 0.5f * (c0 + c2);
                 const float lmax = mid + sqrtf(std_max(mid * mid - det, 0.0f));
-                const int radius = (int)ceilf(cp.radius_sigmas * sqrtf(lmax));
+                radius = (int)ceilf(cp.radius_sigmas * sqrtf(lmax));
                 const float rf = (float)radius;
                 x0 = max(0, (int)ceilf(m0 - rf - 0.5f));
                 x1 = min(cp.width, (int)floorf(m0 + rf - 0.5f) + 1);
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                                    __uint_as_float(pack_range(ey0, ey1)));
                 r.r2 = make_float4(0.f, 0.f, 0.f, cut);  // colour filled in after the SH barrier
                 ref_rect = make_uint2(pack_range(x0, x1), pack_range(y0, y1));
+                if (proj_dbg) proj_dbg[i] = make_float4(c0, c1, c2, __int_as_float(radius));  // splat_project
                 if (aux) {
                     const float smax = std_max(std_max(ls0, ls1), ls2);
                     const float smin = std_min(std_min(ls0, ls1), ls2);
@@ -793,20 +795,20 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
                               uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref,
-                              uint32_t* host_counts) {
+                              uint32_t* host_counts, float4* proj_dbg) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<true><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                             tile_counts, n_survivors_dev, depth_out, rect_ref);
+                                                                             tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg);
         }
     else
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<false><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref);
+                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg);
         }
     lc.count++;
     if (host_counts) {

@@ -95,7 +95,8 @@ struct GaussianPtrs {
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp,
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
-                              float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr);
+                              float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
+                              float4* proj_dbg = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 struct BinningArgs {

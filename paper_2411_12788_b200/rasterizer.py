@@ -467,6 +467,23 @@ def forward_debug(ctx: Optional[Context] = None) -> dict:
                 gaussian=gauss[:P], ranges=ranges, order=order[: ns.value])
 
 
+def project(set_, cam: Camera, cfg: Optional[RasterConfig] = None, mask=None, ctx: Optional[Context] = None):
+    """project<float> (rasterizer.cpp:10-90): the survivors' ProjectedGaussian records sorted by
+    (depth, index), as a numpy structured array with capi.Projected's fields."""
+    ctx = ctx or Context.default()
+    cfg = cfg or RasterConfig()
+    ds, _ = _device_set(set_, ctx.device)
+    m = _device_mask(mask, ds.n, ctx.device)
+    out = (capi.Projected * max(ds.n, 1))()
+    cnt = C.c_int32()
+    ctx.bind_stream()
+    ctx.check(ctx.lib.splat_project(ctx.h, C.byref(ds.struct()), C.byref(cam), C.byref(cfg),
+                                    as_u8p(m.data_ptr()) if m is not None else capi.u8p(), C.cast(out, C.c_void_p),
+                                    max(ds.n, 1), C.byref(cnt)))
+    arr = np.ctypeslib.as_array(out)[: cnt.value].copy()
+    return arr
+
+
 def traversal_counts(ctx: Optional[Context] = None) -> tuple[int, int]:
     """(V, C) of the preceding forward: traverse_pixel list visits and committed samples summed over
     the pixels (a measurement pass, synchronous)."""

@@ -17,3 +17,16 @@ def test_cpp_adapter_matches_reference():
     r = subprocess.run([str(EXE)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASSED" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_adapter_timing_config1():
+    """The drop-in at BASELINE config 1 scale (1 M Gaussians, 1237 x 822) through the adapter, by
+    value and with a resident set: the measured cost of switching the reference's call sites."""
+    if not EXE.exists():
+        pytest.skip("adapter_check not built (needs /root/reference at build time)")
+    r = subprocess.run([str(EXE), "--time", "1000000"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("ADAPTER_TIME")]
+    print("\n".join(lines))
+    assert len(lines) == 2

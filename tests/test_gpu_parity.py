@@ -340,3 +340,29 @@ def test_traversal_counts_equal_oracle(oracle, tile):
     want = oracle.render(s, cam, cfg, report=False)
     assert (v, c) == (want["visits"], want["commits"])
     assert 0 < c < v
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_project_records_equal_oracle(oracle, exact):
+    """splat_project (project<float>): survivors in (depth, index) order with their rects, radii,
+    depths, 2D means, conics, colours and opacities bit-exact; cov2d is the matrix the conic was
+    inverted from (the reference's inv_det multiply reproduces the conic bit for bit)."""
+    s, cam = cfg0_scene()
+    cfg = exact_cfg() if exact else RasterConfig()
+    got = R.project(s, cam, cfg)
+    want = oracle.project(s, cam, cfg)
+    order = want["order"][: want["n_survivors"]]
+    assert_bitwise(got["index"], order, "survivor order")
+    rect = np.stack([got["x0"], got["x1"], got["y0"], got["y1"]], 1)
+    assert_bitwise(rect, want["rect"][order], "rects")
+    assert_bitwise(got["radius"], want["radius"][order], "radius")
+    assert_bitwise(got["depth_mean"], want["depth"][order], "depth")
+    assert_bitwise(got["mean2d"], want["mean2d"][order], "mean2d")
+    assert_bitwise(got["conic"], want["conic"][order], "conic")
+    assert_bitwise(got["color"], want["color"][order], "colour")
+    assert_bitwise(got["opacity"], want["opacity"][order], "opacity")
+    c = got["cov2d"].astype(np.float32)
+    det = c[:, 0] * c[:, 2] - c[:, 1] * c[:, 1]
+    inv = np.float32(1.0) / det
+    assert_bitwise(np.stack([c[:, 2] * inv, -c[:, 1] * inv, c[:, 0] * inv], 1), got["conic"], "conic from cov2d")
+    assert_bitwise(got["center_world"], s.centers[order], "centre")
