@@ -449,12 +449,35 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
     float bg0, float bg1, float bg2, const float* __restrict__ d_color, const float* __restrict__ color,
     const float* __restrict__ target, float inv_n, float* __restrict__ loss_partials, float4* __restrict__ grad2d,
     int nblocks, int* __restrict__ counter, const uint32_t* __restrict__ blist, const uint32_t* __restrict__ bidx,
-    const int32_t* __restrict__ bcount) {
+    const int32_t* __restrict__ bcount, const uint32_t* __restrict__ cls_cnt, const uint32_t* __restrict__ cls_list) {
+    // Work order: the forward filed every block under a cost class (heaviest first); lane l holds
+    // the exclusive starts of classes 2l and 2l + 1, so the k-th pull maps to (class, rank) with
+    // two ballots.  Without classes the blocks go in raster order.
+    const int lane = threadIdx.x;
+    uint32_t e0 = 0, e1 = 0;
+    if (cls_cnt) {
+        const uint32_t c0 = cls_cnt[2 * lane], c1 = cls_cnt[2 * lane + 1];
+        uint32_t incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        e0 = incl - c0 - c1;
+        e1 = e0 + c0;
+    }
     for (;;) {
         int b = 0;
         if (threadIdx.x == 0) b = pull_work(counter, nblocks);
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b >= nblocks) break;
+        if (cls_cnt) {
+            const unsigned m0 = __ballot_sync(0xffffffffu, e0 <= (uint32_t)b);
+            const unsigned m1 = __ballot_sync(0xffffffffu, e1 <= (uint32_t)b);
+            const int c = __popc(m0) + __popc(m1) - 1;
+            const uint32_t ex = __shfl_sync(0xffffffffu, (c & 1) ? e1 : e0, c >> 1);
+            b = (int)cls_list[(size_t)c * nblocks + ((uint32_t)b - ex)];
+        }
         const int bc = blist ? bcount[b] : kBlockList + 1;
         if (bc <= kBlockList)
             blend_backward_block_px2<THR, true>(b, cp, ranges, blist, rec, t_final, last_index, bg0, bg1, bg2,
@@ -649,7 +672,8 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const uint32_t* pair_gauss, const ProjRec* rec, const float* t_final,
                                   const int32_t* last_index, const float bg[3], const float* d_color,
                                   const float* color, const float* target, float* loss_partials, float* grad2d,
-                                  const uint32_t* blist, const uint32_t* bidx, const int32_t* bcount) {
+                                  const uint32_t* blist, const uint32_t* bidx, const int32_t* bcount,
+                                  const uint32_t* cls_cnt, const uint32_t* cls_list) {
     const int ts = cp.tile_size;
     const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     const float inv_n = 1.0f / (float)(3 * (int64_t)cp.width * cp.height);
@@ -690,12 +714,12 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                 blend_backward_px2_persistent<true><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
                     inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
-                    bidx, bcount);
+                    bidx, bcount, cls_cnt, cls_list);
             else
                 blend_backward_px2_persistent<false><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
                     inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
-                    bidx, bcount);
+                    bidx, bcount, cls_cnt, cls_list);
         } else if (cp.apply_thresholds) BLEND_BWD(true);
         else BLEND_BWD(false);
 #undef BLEND_BWD

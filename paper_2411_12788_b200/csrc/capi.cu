@@ -114,6 +114,8 @@ struct FwdState {
     const uint32_t* blist = nullptr;  // per-block staged lists of the forward (or null)
     const uint32_t* bidx = nullptr;
     const int32_t* bcount = nullptr;
+    const uint32_t* cls_cnt = nullptr;
+    const uint32_t* cls_list = nullptr;
     float* color = nullptr;
     float* alpha = nullptr;
     float* depth = nullptr;
@@ -162,6 +164,8 @@ struct splat_ctx {
     DevBuf tgt_stage, step_loss;
     // per 8 x 8 block: the staged list entries the forward walked (replayed by the backward)
     DevBuf blist, bidx, bcount;
+    DevBuf cls;  // the backward's work-order classes: [64 counters | 64 x n_blocks lists]
+    bool block_order_on = true;
     // splat_project: the forward also records cov2d and the radius per Gaussian
     bool want_proj = false;
     DevBuf proj_dbg;
@@ -368,6 +372,15 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     if (!ctx->ev_counts) CK(cudaEventCreateWithFlags(&ctx->ev_counts, cudaEventDisableTiming), "event");
 
     uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] survivors [1] Ps [2] P [3] done blocks
+    // the backward's work-order classes (FwdOutputs::cls_cnt), sized for 8 x 8 pixel blocks
+    uint32_t* cls_cnt = nullptr;
+    if (ctx->block_order_on && n > 0 && cp.tile_size >= 16 && !rep) {
+        const size_t nb = (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8);
+        if (ctx->cls.ensure((kCostClasses + (size_t)kCostClasses * nb) * 4) == cudaSuccess)
+            cls_cnt = ctx->cls.as<uint32_t>();
+        else
+            (void)cudaGetLastError();
+    }
     int n_surv = 0;
     uint64_t n_pairs = 0;
     const bool pairs_alt = false;
@@ -377,7 +390,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr),
+                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt),
            "preprocess");
         // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
         // writes them to mapped pinned memory, so the host waits only for preprocess (event) while
@@ -474,6 +487,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     fo.blist = nullptr;
     fo.bidx = nullptr;
     fo.bcount = nullptr;
+    fo.cls_cnt = nullptr;
+    fo.cls_list = nullptr;
+    fo.n_blocks = 0;
     if (block_lists && n > 0) {
         const size_t n_blocks = (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8);
         // the replay lists are an optimisation (8 B per staged entry, up to kBlockList per block):
@@ -485,6 +501,13 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
             fo.blist = ctx->blist.as<uint32_t>();
             fo.bidx = ctx->bidx.as<uint32_t>();
             fo.bcount = ctx->bcount.as<int32_t>();
+            // the backward's heaviest-first work order (SPLAT_BLOCK_ORDER=0: raster order); the
+            // counters were zeroed by publish_counts after preprocess
+            if (cls_cnt) {
+                fo.cls_cnt = cls_cnt;
+                fo.cls_list = cls_cnt + kCostClasses;
+                fo.n_blocks = (int)n_blocks;
+            }
         } else if (e == cudaErrorMemoryAllocation) {
             (void)cudaGetLastError();  // not sticky: clear it and take the re-cull path
         } else {
@@ -519,6 +542,8 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     st.blist = fo.blist;
     st.bidx = fo.bidx;
     st.bcount = fo.bcount;
+    st.cls_cnt = fo.cls_cnt;
+    st.cls_list = fo.cls_list;
     st.valid = true;
     return SPLAT_OK;
 }
@@ -689,7 +714,8 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
         const uint32_t* sorted_gauss = ctx->pair_gauss[st.pairs_in_alt ? 1 : 0].as<uint32_t>();
         CK(launch_blend_backward(lc, st.cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
                                  ctx->t_final.as<float>(), ctx->last_index.as<int32_t>(), bg, d_color, st.color, target,
-                                 partials, ctx->grad2d.as<float>(), st.blist, st.bidx, st.bcount),
+                                 partials, ctx->grad2d.as<float>(), st.blist, st.bidx, st.bcount, st.cls_cnt,
+                                 st.cls_list),
            "blend backward");
     }
     const float inv_n = 1.0f / (float)(3 * (int64_t)st.cp.width * st.cp.height);
@@ -839,6 +865,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
         c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
         const char* e2 = std::getenv("SPLAT_BWD_PX2");
         c->lc.bwd_px2 = !(e2 && std::strcmp(e2, "0") == 0);
+        const char* eo = std::getenv("SPLAT_BLOCK_ORDER");
+        c->block_order_on = !(eo && std::strcmp(eo, "0") == 0);
         const char* e3 = std::getenv("SPLAT_COOP_SORT");
         c->coop_sort = !(e3 && std::strcmp(e3, "0") == 0);
         const char* e4 = std::getenv("SPLAT_VIEW_OVERLAP");

@@ -346,13 +346,17 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
 // [survivors, Ps, P] straight to the host's mapped pinned memory, and the device counters back to
 // zero for the next view: a one-warp kernel instead of a memset + a copy-engine transfer (a bulk
 // H2D in flight queues copy-engine work behind it).
-__global__ void publish_counts_kernel(uint32_t* __restrict__ n_surv, uint32_t* host_counts) {
+__global__ void publish_counts_kernel(uint32_t* __restrict__ n_surv, uint32_t* host_counts,
+                                      uint32_t* __restrict__ cls_cnt) {
     pdl_wait();
     if (threadIdx.x < 3) {
         const uint32_t c = n_surv[threadIdx.x];
         n_surv[threadIdx.x] = 0u;
         reinterpret_cast<volatile uint32_t*>(host_counts)[threadIdx.x] = c;
     }
+    // the backward's work-order classes of the view about to be blended (FwdOutputs::cls_cnt)
+    if (cls_cnt)
+        for (int k = threadIdx.x; k < kCostClasses; k += 32) cls_cnt[k] = 0u;
     // no system fence: the host reads after synchronising with this kernel's completion, which
     // makes its writes to mapped memory visible (a fence here costs ~3 us on the critical path)
 }
@@ -620,6 +624,10 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
         pipe.finish();
     }
     if (!REPORT && out.bcount && tid == 0) out.bcount[bid] = run;
+    if (!REPORT && out.cls_cnt && tid == 0) {  // the backward's work order: heaviest blocks first
+        const int c = kCostClasses - 1 - min(kCostClasses - 1, run >> 4);
+        out.cls_list[(size_t)c * out.n_blocks + atomicAdd(&out.cls_cnt[c], 1u)] = (uint32_t)bid;
+    }
     if (!inside) return;
     const size_t pix = (size_t)py * cp.width + px;
     if (REPORT && amax_gid >= 0) atomicAdd(&out.max_pixel_count[amax_gid], 1);
@@ -795,7 +803,7 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
                               uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref,
-                              uint32_t* host_counts, float4* proj_dbg) {
+                              uint32_t* host_counts, float4* proj_dbg, uint32_t* cls_cnt) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
@@ -813,7 +821,7 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
     lc.count++;
     if (host_counts) {
         const cudaError_t e = launch_pdl(lc.stream, publish_counts_kernel, dim3(1), dim3(32), 0, n_survivors_dev,
-                                         host_counts);
+                                         host_counts, cls_cnt);
         if (e != cudaSuccess) return e;
         lc.count++;
     }

@@ -96,7 +96,7 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
                               float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
-                              float4* proj_dbg = nullptr);
+                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 struct BinningArgs {
@@ -148,7 +148,14 @@ struct FwdOutputs {
     uint32_t* blist;         // or null
     uint32_t* bidx;
     int32_t* bcount;
+    // Work order for the backward: block b appends itself to cost class c = 63 - min(63, entries
+    // walked / 16) (heaviest first): cls_list[c * n_blocks + rank], rank from cls_cnt[c] (64
+    // counters, zeroed by publish_counts before the forward).  Null: not recorded.
+    uint32_t* cls_cnt;
+    uint32_t* cls_list;
+    int n_blocks;
 };
+constexpr int kCostClasses = 64;
 constexpr int kBlockList = 2048;      // replay-list capacity per 8 x 8 block
 constexpr int kBlockListSmem = 512;   // entries the backward maps through shared memory
 
@@ -186,7 +193,8 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const float* d_color, const float* color, const float* target,
                                   float* loss_partials, float* grad2d,
                                   const uint32_t* blist = nullptr, const uint32_t* bidx = nullptr,
-                                  const int32_t* bcount = nullptr);
+                                  const int32_t* bcount = nullptr, const uint32_t* cls_cnt = nullptr,
+                                  const uint32_t* cls_list = nullptr);
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
 cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n);
 // K10 chain.  list: scratch of n_surv + 1 words (touched-Gaussian list; touched <= survivors).
