@@ -290,9 +290,16 @@ __device__ __forceinline__ uint32_t st_lo(const uint32_t* __restrict__ st_cnt, i
 }
 
 // One thread per supertile: piece_st[id] for its id range; empty ranges for empty supertiles.
+// The forward's work order: tile t filed under cost class 63 - min(63, list length / 512) (longest
+// lists first), tcls = [64 counters (zeroed by publish_counts) | 64 x n_tiles lists].
+__device__ __forceinline__ void file_tile(uint32_t* tcls, int n_tiles, int t, uint32_t len) {
+    const int c = kCostClasses - 1 - (int)min((uint32_t)kCostClasses - 1u, len >> 9);
+    tcls[kCostClasses + (size_t)c * n_tiles + atomicAdd(&tcls[c], 1u)] = (uint32_t)t;
+}
+
 __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges,
                                int n_st, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ piece_st,
-                               uint32_t* __restrict__ ranges) {
+                               uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls) {
     pdl_wait();
     pdl_trigger();
     const int st = blockIdx.x * blockDim.x + threadIdx.x;
@@ -309,6 +316,7 @@ __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
             if (tx < tiles_x && ty < tiles_y) {
                 ranges[2 * (ty * tiles_x + tx)] = kSTT * lo;
                 ranges[2 * (ty * tiles_x + tx) + 1] = kSTT * lo;
+                if (tcls) file_tile(tcls, tiles_x * tiles_y, ty * tiles_x + tx, 0u);
             }
         }
     }
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges, int n_st,
     const uint32_t* __restrict__ piece_st, const uint32_t* __restrict__ piece_cnt,
     const uint32_t* __restrict__ st_gauss, const uint16_t* __restrict__ st_cover, int tiles_x, int tiles_y, int st_x,
-    uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges) {
+    uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls) {
     constexpr int kW = kL2Threads / 32;
     __shared__ uint32_t s_c[kPieceK][kW][kSTT];    // (slice k, warp) entries covering tile f, then their list position
     __shared__ uint32_t s_prefix[kSTT];
@@ -433,6 +441,7 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
                 const int t = ty * tiles_x + tx;
                 ranges[2 * t] = list0;
                 ranges[2 * t + 1] = base + inc;
+                if (tcls) file_tile(tcls, tiles_x * tiles_y, t, base + inc - list0);
             }
         }
     }
@@ -563,7 +572,8 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
         {
             LaunchScope s(lc, "bin_map");
             e = launch_pdl(lc.stream, bin_map_kernel, dim3(blocks_for(n_st, 128)), dim3(128), 0, cnt, nch,
-                           (const uint32_t*)a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, piece_st, a.ranges);
+                           (const uint32_t*)a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, piece_st, a.ranges,
+                           cnt ? a.tcls : nullptr);
             if (e != cudaSuccess) return e;
             lc.count++;
         }
@@ -579,7 +589,8 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
             LaunchScope s(lc, "bin_emit");
             e = launch_pdl(lc.stream, bin_emit_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
                            (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)piece_st, (const uint32_t*)piece_cnt,
-                           gauss, (const uint16_t*)a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss, a.ranges);
+                           gauss, (const uint16_t*)a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss, a.ranges,
+                           cnt ? a.tcls : nullptr);
             if (e != cudaSuccess) return e;
             lc.count++;
         }

@@ -373,13 +373,18 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
 
     uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] survivors [1] Ps [2] P [3] done blocks
     // the backward's work-order classes (FwdOutputs::cls_cnt), sized for 8 x 8 pixel blocks
+    // and the forward's (BinningArgs::tcls, tiles by list length)
     uint32_t* cls_cnt = nullptr;
-    if (ctx->block_order_on && n > 0 && cp.tile_size >= 16 && !rep) {
-        const size_t nb = (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8);
-        if (ctx->cls.ensure((kCostClasses + (size_t)kCostClasses * nb) * 4) == cudaSuccess)
-            cls_cnt = ctx->cls.as<uint32_t>();
-        else
+    uint32_t* tcls = nullptr;
+    if (ctx->block_order_on && n > 0) {
+        const size_t nb = cp.tile_size >= 16 && !rep ? (size_t)n_tiles * (cp.tile_size / 8) * (cp.tile_size / 8) : 0;
+        const size_t words = kCostClasses + (size_t)kCostClasses * n_tiles + (nb ? kCostClasses + kCostClasses * nb : 0);
+        if (ctx->cls.ensure(words * 4) == cudaSuccess) {
+            tcls = ctx->cls.as<uint32_t>();
+            if (nb) cls_cnt = tcls + kCostClasses + (size_t)kCostClasses * n_tiles;
+        } else {
             (void)cudaGetLastError();
+        }
     }
     int n_surv = 0;
     uint64_t n_pairs = 0;
@@ -390,7 +395,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt),
+                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls),
            "preprocess");
         // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
         // writes them to mapped pinned memory, so the host waits only for preprocess (event) while
@@ -458,6 +463,8 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         ba.pair_gauss = ctx->pair_gauss[0].as<uint32_t>();
         ba.hist = ctx->hist.as<uint32_t>();
         ba.scan_tmp = ctx->scan_tmp.as<uint32_t>();
+        ba.tcls = chunked ? tcls : nullptr;
+        if (!chunked) tcls = nullptr;  // the fallback binning does not file tiles
         CK(launch_binning(lc, ba), "binning");
     } else {
         CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_tiles * 8, s), "memset ranges");
@@ -519,7 +526,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     CK(cudaEventRecord(ctx->ev_fwd_start, s), "record forward start");
     ctx->fwd_start_recorded = true;
     CK(launch_blend_forward(lc, cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
-                            want_depth ? ctx->aux.as<AuxRec>() : nullptr, bg, fo),
+                            want_depth ? ctx->aux.as<AuxRec>() : nullptr, bg, fo, n > 0 ? tcls : nullptr),
        "blend forward");
     if (ctx->post_forward_hook) {
         std::function<int()> hook;

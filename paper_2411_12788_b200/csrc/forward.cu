@@ -347,16 +347,19 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
 // zero for the next view: a one-warp kernel instead of a memset + a copy-engine transfer (a bulk
 // H2D in flight queues copy-engine work behind it).
 __global__ void publish_counts_kernel(uint32_t* __restrict__ n_surv, uint32_t* host_counts,
-                                      uint32_t* __restrict__ cls_cnt) {
+                                      uint32_t* __restrict__ cls_cnt, uint32_t* __restrict__ tcls_cnt) {
     pdl_wait();
     if (threadIdx.x < 3) {
         const uint32_t c = n_surv[threadIdx.x];
         n_surv[threadIdx.x] = 0u;
         reinterpret_cast<volatile uint32_t*>(host_counts)[threadIdx.x] = c;
     }
-    // the backward's work-order classes of the view about to be blended (FwdOutputs::cls_cnt)
-    if (cls_cnt)
-        for (int k = threadIdx.x; k < kCostClasses; k += 32) cls_cnt[k] = 0u;
+    // the work-order classes of the view about to be binned and blended (BinningArgs::tcls,
+    // FwdOutputs::cls_cnt)
+    for (int k = threadIdx.x; k < kCostClasses; k += 32) {
+        if (cls_cnt) cls_cnt[k] = 0u;
+        if (tcls_cnt) tcls_cnt[k] = 0u;
+    }
     // no system fence: the host reads after synchronising with this kernel's completion, which
     // makes its writes to mapped memory visible (a fence here costs ~3 us on the critical path)
 }
@@ -691,12 +694,46 @@ __global__ void __launch_bounds__(BW * BH) blend_forward_persistent(CamParams cp
                                                            const uint32_t* __restrict__ pair_gauss,
                                                            const ProjRec* __restrict__ rec,
                                                            const AuxRec* __restrict__ aux, float bg0, float bg1,
-                                                           float bg2, FwdOutputs out, int nblocks, int* __restrict__ counter) {
+                                                           float bg2, FwdOutputs out, int nblocks, int* __restrict__ counter,
+                                                           const uint32_t* __restrict__ tcls) {
     __shared__ int s_bid;
+    __shared__ uint32_t s_excl[kCostClasses + 1];
     pdl_wait();
+    // Work order: binning filed every tile under a list-length class (longest first); the k-th
+    // pull is sub-block k % nsub of the (k / nsub)-th tile in that order (a tile's sub-blocks stay
+    // adjacent, so their list reads hit L2).  Without classes: raster order.
+    const int nsub = (cp.tile_size / BW) * (cp.tile_size / BH);
+    const int ntiles = cp.tiles_x * cp.tiles_y;
+    if (tcls && threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const uint32_t c0 = tcls[2 * lane], c1 = tcls[2 * lane + 1];
+        uint32_t incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        s_excl[2 * lane] = incl - c0 - c1;
+        s_excl[2 * lane + 1] = incl - c1;
+        if (lane == 31) s_excl[kCostClasses] = incl;
+    }
     for (;;) {
         __syncthreads();  // the previous block's shared-memory reads are done
-        if (threadIdx.x == 0) s_bid = pull_work(counter, nblocks);
+        if (threadIdx.x == 0) {
+            int b = pull_work(counter, nblocks);
+            if (tcls && b < nblocks) {
+                const uint32_t ti = (uint32_t)(b / nsub);
+                int lo = 0, hi = kCostClasses - 1;  // last class whose start <= ti
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_excl[mid] <= ti) lo = mid;
+                    else hi = mid - 1;
+                }
+                const uint32_t t = tcls[kCostClasses + (size_t)lo * ntiles + (ti - s_excl[lo])];
+                b = (int)t * nsub + b % nsub;
+            }
+            s_bid = b;
+        }
         __syncthreads();
         const int b = s_bid;
         if (b >= nblocks) break;
@@ -803,7 +840,7 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
                               uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref,
-                              uint32_t* host_counts, float4* proj_dbg, uint32_t* cls_cnt) {
+                              uint32_t* host_counts, float4* proj_dbg, uint32_t* cls_cnt, uint32_t* tcls_cnt) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
@@ -821,7 +858,7 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
     lc.count++;
     if (host_counts) {
         const cudaError_t e = launch_pdl(lc.stream, publish_counts_kernel, dim3(1), dim3(32), 0, n_survivors_dev,
-                                         host_counts, cls_cnt);
+                                         host_counts, cls_cnt, tcls_cnt);
         if (e != cudaSuccess) return e;
         lc.count++;
     }
@@ -830,7 +867,7 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
 
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
                                  const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux, const float bg[3],
-                                 const FwdOutputs& out) {
+                                 const FwdOutputs& out, const uint32_t* tcls) {
     const int ts = cp.tile_size;
     const unsigned grid = (unsigned)(cp.tiles_x * cp.tiles_y * (ts / cp.block_w) * (ts / cp.block_h));
     LaunchScope ls_(lc, "blend_forward");
@@ -842,7 +879,8 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
                                                                       W * H, 0);                                 \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                             \
             launch_pdl(lc.stream, blend_forward_persistent<R, T, W, H, A>, dim3(pg < grid ? pg : grid), dim3(W * H), \
-                       0, cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters); \
+                       0, cp, ranges, pair_gauss, rec, aux, bg[0], bg[1], bg[2], out, (int)grid, lc.work_counters,   \
+                       tcls);                                                                                    \
         } else {                                                                                                 \
             blend_forward_kernel<R, T, W, H, A><<<grid, W * H, 0, lc.stream>>>(cp, ranges, pair_gauss, rec, aux, \
                                                                               bg[0], bg[1], bg[2], out);         \

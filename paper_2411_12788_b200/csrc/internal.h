@@ -96,9 +96,11 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
                               float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
-                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr);
+                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
+constexpr int kCostClasses = 64;  // work-order cost classes of the persistent blend kernels
+
 struct BinningArgs {
     const uint32_t* order;       // survivors in (depth, index) order
     const uint32_t* st_offsets;  // exclusive scan of supertile counts in depth order
@@ -117,6 +119,9 @@ struct BinningArgs {
     uint32_t* pair_gauss;  // [16 * st_pairs] out: per-tile lists of Gaussian ids (capacity layout)
     uint32_t* hist;
     uint32_t* scan_tmp;
+    // the forward's work order (chunked path only; nullable): [64 counters | 64 x n_tiles lists],
+    // every tile filed under its list-length class as its range is written
+    uint32_t* tcls;
 };
 int supertile_side();
 // Capacity (entries) of the per-tile list buffer: every tile of supertile s gets L_s slots.
@@ -155,7 +160,7 @@ struct FwdOutputs {
     uint32_t* cls_list;
     int n_blocks;
 };
-constexpr int kCostClasses = 64;
+
 constexpr int kBlockList = 2048;      // replay-list capacity per 8 x 8 block
 constexpr int kBlockListSmem = 512;   // entries the backward maps through shared memory
 
@@ -167,7 +172,7 @@ cudaError_t launch_traversal_counts(LaunchCtx& lc, const CamParams& cp, const ui
 // K6 (+K7 depth epilogue): per-tile front-to-back blend.
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
                                  const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux,
-                                 const float bg[3], const FwdOutputs& out);
+                                 const float bg[3], const FwdOutputs& out, const uint32_t* tcls = nullptr);
 
 // Depth unprojection + stride-rule compaction over one rendered view.
 cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* max_contributor,
