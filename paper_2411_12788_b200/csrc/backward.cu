@@ -731,14 +731,22 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
 
 // Device floats straight into mapped pinned host memory (the per-view losses of a training step):
 // a kernel instead of a copy-engine transfer, which would queue behind bulk host copies.
-__global__ void copy_to_host_kernel(const float* __restrict__ src, float* dst_mapped, int n) {
+// The per-view losses to mapped host memory, then (seq != 0) a sequence number in the slot after
+// them once the values are visible system-wide: the host polls that word instead of waiting for
+// the stream (a synchronisation's wake-up costs more than the polling).
+__global__ void copy_to_host_kernel(const float* __restrict__ src, float* dst_mapped, int n, uint32_t seq) {
     pdl_wait();
     for (int i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<volatile float*>(dst_mapped)[i] = src[i];
+    if (seq) {
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) reinterpret_cast<volatile uint32_t*>(dst_mapped)[n] = seq;
+    }
 }
 
-cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n) {
+cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n, uint32_t seq) {
     if (n <= 0) return cudaSuccess;
-    const cudaError_t e = launch_pdl(lc.stream, copy_to_host_kernel, dim3(1), dim3(128), 0, src, dst_mapped, n);
+    const cudaError_t e = launch_pdl(lc.stream, copy_to_host_kernel, dim3(1), dim3(128), 0, src, dst_mapped, n, seq);
     lc.count++;
     return e;
 }

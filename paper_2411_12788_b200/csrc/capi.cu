@@ -176,6 +176,7 @@ struct splat_ctx {
     float* host_loss = nullptr;             // mapped pinned per-view losses of splat_train_step
     float* host_loss_dev = nullptr;
     int host_loss_cap = 0;
+    uint32_t loss_seq = 0;  // sequence word of splat_train_step's loss read-back
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
     // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
@@ -2050,13 +2051,24 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
             if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
             ctx->host_loss = nullptr;
             ctx->host_loss_cap = 0;
-            CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_loss), (size_t)n_views * 4, cudaHostAllocMapped),
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_loss), (size_t)(n_views + 1) * 4, cudaHostAllocMapped),
                "alloc pinned loss");
             CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_loss_dev), ctx->host_loss, 0), "map loss");
             ctx->host_loss_cap = n_views;
         }
-        CK(launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views), "read loss");
-        CK(cudaStreamSynchronize(s), "sync");
+        // the losses (the step's last kernel, after the optimiser) are ready when the sequence
+        // word arrives; poll it, checking the stream now and then so an error still surfaces
+        const uint32_t seq = ++ctx->loss_seq ? ctx->loss_seq : ++ctx->loss_seq;
+        volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(ctx->host_loss) + n_views;
+        CK(launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views, seq), "read loss");
+        for (uint32_t spin = 1; *flag != seq; ++spin) {
+            if ((spin & 1023u) == 0u) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q == cudaSuccess) break;  // done: the flag is visible now (re-read below)
+                if (q != cudaErrorNotReady) CK(q, "sync");
+            }
+        }
+        if (*flag != seq) CK(cudaStreamSynchronize(s), "sync");
         std::memcpy(loss_host, ctx->host_loss, (size_t)n_views * 4);
     }
     return SPLAT_OK;

@@ -201,7 +201,7 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                   const int32_t* bcount = nullptr, const uint32_t* cls_cnt = nullptr,
                                   const uint32_t* cls_list = nullptr);
 cudaError_t launch_loss_reduce(LaunchCtx& lc, const float* partials, int n, float inv_n, float* loss);
-cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n);
+cudaError_t launch_copy_to_host(LaunchCtx& lc, const float* src, float* dst_mapped, int n, uint32_t seq = 0);
 // K10 chain.  list: scratch of n_surv + 1 words (touched-Gaussian list; touched <= survivors).
 // prezeroed: a fresh (accumulate = 0) gradient whose rows were already zero-filled (side stream);
 // only touched rows are written.
