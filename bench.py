@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--comm", choices=("torch", "native"), default="torch",
                     help="N > 1 exchange: torch.distributed NCCL collectives (exchange.py) or the library's own "
                          "NCCL communicator inside splat_train_step")
-    ap.add_argument("--buckets", type=int, default=4, help="exchange buckets (reduce-scatter / Adam pipelining)")
+    ap.add_argument("--buckets", type=int, default=8, help="exchange buckets (reduce-scatter / Adam pipelining)")
     a = ap.parse_args()
     if a.views is None:
         a.views = {4: 8, 2: 64, 3: 200}.get(a.config, 1)

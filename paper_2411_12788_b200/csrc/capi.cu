@@ -1174,11 +1174,23 @@ int splat_exchange_step(splat_ctx* ctx, float* params, const float* grads, float
                 return set_err(ctx, SPLAT_ERR_NCCL, "exchange_step: " + err);
             CK(cudaEventRecord(ev_rs[b], cs), "record");
         }
+        // packed ranges of the groups the optimiser steps: only buckets holding one change
+        const int64_t nn = n;
+        const struct {
+            uint32_t bit;
+            int64_t lo, hi;
+        } spans[5] = {{SPLAT_GROUP_CENTERS, 0, 3 * nn}, {SPLAT_GROUP_SCALES, 3 * nn, 6 * nn},
+                      {SPLAT_GROUP_ROTATIONS, 6 * nn, 10 * nn}, {SPLAT_GROUP_OPACITY, 10 * nn, 11 * nn},
+                      {SPLAT_GROUP_SH, 11 * nn, 59 * nn}};
         for (int b = 0; b < B; ++b) {
             const int64_t s0 = b * bucket + r * shard;
             CK(cudaStreamWaitEvent(s, ev_rs[b], 0), "wait");
             if ((rc = splat_adam_step_range(ctx, params, sh + b * shard, m, v, n, s0, shard, cfg, t, group_mask)))
                 return rc;
+            bool changed = false;
+            for (const auto& sp : spans)
+                changed = changed || ((group_mask & sp.bit) && sp.lo < (b + 1) * bucket && b * bucket < sp.hi);
+            if (!changed) continue;  // every replica already holds this bucket's parameters
             CK(cudaEventRecord(ev_ad[b], s), "record");
             CK(cudaStreamWaitEvent(cs, ev_ad[b], 0), "wait");
             // in place: this rank's shard is already at recv + r * shard

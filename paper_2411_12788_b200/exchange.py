@@ -12,7 +12,8 @@ padding to a multiple of `world * buckets * 4` floats):
       wait for its reduce-scatter; OptimState::step on the shard (splat_adam_step_range: the
       element's group learning rate, fp64 moments, optimizer.cpp:29-68) — runs while later
       buckets are still being reduced
-      all-gather of the updated parameter shard -> every replica's bucket b (in place)
+      all-gather of the updated parameter shard -> every replica's bucket b (only buckets holding
+      a group the optimiser steps: the others are unchanged on every replica)
   renormalise the rotations (optimizer.cpp:69; after the gather, since a shard may cut a row)
 
 Bytes on the wire per rank are those of an all-reduce (2 (G-1)/G x 4 x 59N); the optimiser
@@ -54,6 +55,14 @@ class ShardedExchange:
         self._quat_normalize = quat_normalize
         self._shard = None
         self.events = None  # bench: list of (start, end) CUDA event pairs around each exchange
+
+    def _stepped(self, group_mask: int):
+        """Packed ranges [lo, hi) of the groups the optimiser steps (only these change)."""
+        n = self.n
+        spans = ((capi.GROUP_CENTERS, 0, 3 * n), (capi.GROUP_SCALES, 3 * n, 6 * n),
+                 (capi.GROUP_ROTATIONS, 6 * n, 10 * n), (capi.GROUP_OPACITY, 10 * n, 11 * n),
+                 (capi.GROUP_SH, 11 * n, 59 * n))
+        return [(lo, hi) for bit, lo, hi in spans if group_mask & bit]
 
     def ranges(self):
         """(bucket begin, shard begin) in the packed buffer for every bucket; the shard is this
@@ -103,10 +112,13 @@ class ShardedExchange:
             else:
                 rs.append(dist.reduce_scatter_tensor(out, src, group=self.group, async_op=True))
         ag = []
+        stepped = self._stepped(group_mask)
         for b, (b0, s0) in enumerate(self.ranges()):
             if rs[b] is not None:
                 rs[b].wait()
             adam(params_flat, self._shard[b * s:(b + 1) * s], m_flat, v_flat, self.n, s0, S, cfg, step, group_mask)
+            if not any(lo < b0 + B and b0 < hi for lo, hi in stepped):
+                continue  # no stepped parameter in this bucket: every replica already holds it
             dst = params_flat[b0:b0 + B]
             mine = params_flat[s0:s0 + S]
             if stage:

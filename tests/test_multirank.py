@@ -33,7 +33,7 @@ def _view_grads(oracle, s, cam, target):
     return oracle.render_backward(s, cam, dc)
 
 
-def _train(rank, world, out_q, port, mode="exchange", buckets=3):
+def _train(rank, world, out_q, port, mode="exchange", buckets=3, mask=31):
     sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
     from oracle_lib import OracleLib
     from paper_2411_12788_b200 import scenes
@@ -71,13 +71,13 @@ def _train(rank, world, out_q, port, mode="exchange", buckets=3):
         grads = torch.zeros(L)
         grads[:59 * n] = torch.from_numpy(flat)
         if mode == "exchange":
-            ex.step(params, grads, m, v, cfg, t, GROUP_ALL)
+            ex.step(params, grads, m, v, cfg, t, mask)
             t += 1
         else:  # all-reduce + the full OptimState::step on every rank
             if world > 1:
                 dist.all_reduce(grads, op=dist.ReduceOp.SUM)
             s2, m2, v2, t = oracle.adam_step(s, unpack_grads(grads[:59 * n].numpy(), n), m[:59 * n].numpy(),
-                                             v[:59 * n].numpy(), cfg, t)
+                                             v[:59 * n].numpy(), cfg, t, mask)
             params[:59 * n] = torch.from_numpy(pack_grads(dict(d_centers=s2.centers, d_log_scales=s2.log_scales,
                                                                d_rotations=s2.rotations,
                                                                d_opacity_logits=s2.opacity_logits, d_sh=s2.sh)))
@@ -88,10 +88,10 @@ def _train(rank, world, out_q, port, mode="exchange", buckets=3):
         dist.destroy_process_group()
 
 
-def _run(world, port, mode="exchange", buckets=3):
+def _run(world, port, mode="exchange", buckets=3, mask=31):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_train, args=(r, world, q, port, mode, buckets)) for r in range(world)]
+    procs = [ctx.Process(target=_train, args=(r, world, q, port, mode, buckets, mask)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -119,6 +119,17 @@ def test_two_rank_gloo_exchange_matches_allreduce_and_single_process():
     assert np.array_equal(two[0][1], two_ar[0][1])
     # and one process summing all views, within the float-sum order difference
     assert np.allclose(two[0][1], single[0][1], rtol=0, atol=1e-6)
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_exchange_means_only_skips_unchanged_buckets():
+    """Adam on the means only (config 1): buckets without a stepped group are not all-gathered,
+    and the result still equals all-reduce + the masked full step bit for bit."""
+    from paper_2411_12788_b200.capi import GROUP_CENTERS
+    two = _run(2, 29614, mode="exchange", buckets=5, mask=GROUP_CENTERS)
+    two_ar = _run(2, 29615, mode="allreduce", mask=GROUP_CENTERS)
+    assert np.array_equal(two[0][1], two[1][1])
+    assert np.array_equal(two[0][1], two_ar[0][1])
 
 
 def test_exchange_ranges_partition_the_padded_buffer():
