@@ -633,32 +633,53 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
         STAMP(3 + 6 * j);
         grid.sync();
         STAMP(4 + 6 * j);
-        // phase B: digit rows, exclusive over tiles, plus the digit's global base
-        for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) {
-            uint32_t base = 0;  // exclusive scan of the pass histogram up to d (cheap: <= 256 adds)
-            for (uint32_t e = lane; e < d; e += 32) base += s_gh[passes[j]][e];
+        // phase B: digit rows, exclusive over tiles, plus the digit's global base (the exclusive
+        // scan of the pass histogram, in s_delta until phase C reuses it).  A warp per row (a
+        // CTA per row cost two barriers per row: 256 rows on one CTA took 0.4 ms at 2 K keys);
+        // with few tiles a thread per row.
+        {
+            uint32_t tot;
+            const uint32_t hb = block_exclusive_scan(s_gh[passes[j]][threadIdx.x], &tot, s_warp);
+            s_delta[threadIdx.x] = hb;
+            __syncthreads();
+        }
+        if (ntiles <= 32) {
+            if (blockIdx.x == 0) {
+                uint32_t* row = counts + (size_t)threadIdx.x * ntiles;
+                uint32_t acc = s_delta[threadIdx.x];
+                for (uint32_t t0 = 0; t0 < ntiles; t0 += 8) {
+                    uint32_t x[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
-            uint32_t* row = counts + (size_t)d * ntiles;
-            uint32_t carry = base;
-            for (uint32_t t0 = 0; t0 < ntiles; t0 += kThreads * 3) {
-                uint32_t x[3], sum = 0;
+                    for (int qq = 0; qq < 8; ++qq) x[qq] = t0 + qq < ntiles ? row[t0 + qq] : 0u;
 #pragma unroll
-                for (int qq = 0; qq < 3; ++qq) {
-                    const uint32_t t = t0 + threadIdx.x * 3 + qq;
-                    x[qq] = t < ntiles ? row[t] : 0u;
-                    sum += x[qq];
+                    for (int qq = 0; qq < 8; ++qq) {
+                        if (t0 + qq < ntiles) row[t0 + qq] = acc;
+                        acc += x[qq];
+                    }
                 }
-                uint32_t tot;
-                const uint32_t ex = block_exclusive_scan(sum, &tot, s_warp);
-                uint32_t acc = carry + ex;
+            }
+        } else {
+            for (uint32_t d = blockIdx.x * kWarps + warp; d < 256; d += gridDim.x * kWarps) {
+                uint32_t* row = counts + (size_t)d * ntiles;
+                uint32_t carry = s_delta[d];
+                for (uint32_t t0 = 0; t0 < ntiles; t0 += 32 * 8) {
+                    uint32_t x[8], sum = 0;
 #pragma unroll
-                for (int qq = 0; qq < 3; ++qq) {
-                    const uint32_t t = t0 + threadIdx.x * 3 + qq;
-                    if (t < ntiles) row[t] = acc;
-                    acc += x[qq];
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const uint32_t t = t0 + lane * 8 + qq;
+                        x[qq] = t < ntiles ? row[t] : 0u;
+                        sum += x[qq];
+                    }
+                    const uint32_t inc = warp_incl_scan(sum, lane);
+                    uint32_t acc = carry + inc - sum;
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const uint32_t t = t0 + lane * 8 + qq;
+                        if (t < ntiles) row[t] = acc;
+                        acc += x[qq];
+                    }
+                    carry += __shfl_sync(0xffffffffu, inc, 31);
                 }
-                carry += tot;
             }
         }
         STAMP(5 + 6 * j);
