@@ -128,7 +128,7 @@ __device__ __forceinline__ void emit_entry_grads(const float v[24], int lane, bo
 // the CTA's L1 partial sum is written to loss_partials[block].
 template <bool THR, int BW, int BH>
 __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
-                                                            const uint32_t* __restrict__ pair_gauss,
+                                                            TileTails tt, const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
                                                             const float* __restrict__ t_final,
                                                             const int32_t* __restrict__ last_index, float bg0,
@@ -196,6 +196,10 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
     for (int w = 0; w < nwarps; ++w) block_last = max(block_last, s_maxlast[w]);
     const uint32_t start = ranges[2 * tile];
     if (block_last < (int)start) return;  // nothing committed in this block
+    __shared__ ListTail s_tail;
+    uint32_t vend;
+    const int split = list_tail_setup(tt.tails, tt.st_list, tt.st_cover, tile, cp.tiles_x, ranges[2 * tile + 1], vend,
+                                      &s_tail, tid == 0, []() { __syncthreads(); });
 
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
@@ -210,7 +214,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
         const int i = block_last - b * nthreads - t;
         return i >= (int)start ? i : -1;
     };
-    StagePipe<BW * BH, decltype(pos)> pipe(pos, pair_gauss, rec, &raw);
+    StagePipe<BW * BH, decltype(pos)> pipe(pos, pair_gauss, rec, &raw, split, &s_tail);
     pipe.start();
     const int nb = (block_last + 1 - (int)start + nthreads - 1) / nthreads;
     for (int b = 0; b < nb; ++b) {
@@ -280,7 +284,7 @@ struct PixBwd {
 
 template <bool THR, bool COMPACT>
 __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, const uint32_t* __restrict__ ranges,
-                                                         const uint32_t* __restrict__ pair_gauss,
+                                                         TileTails tt, const uint32_t* __restrict__ pair_gauss,
                                                          const ProjRec* __restrict__ rec,
                                                          const float* __restrict__ t_final,
                                                          const int32_t* __restrict__ last_index, float bg0, float bg1,
@@ -366,6 +370,11 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
     const uint32_t start = COMPACT ? 0u : ranges[2 * tile];
     if (block_last < (int)start) return;  // nothing committed in this block
     const uint32_t* list = COMPACT ? pair_gauss + (size_t)bid * kBlockList : pair_gauss;
+    __shared__ ListTail s_tail;
+    uint32_t vend;
+    const int split = COMPACT ? INT_MAX
+                              : list_tail_setup(tt.tails, tt.st_list, tt.st_cover, tile, cp.tiles_x,
+                                                ranges[2 * tile + 1], vend, &s_tail, lane == 0, []() { __syncwarp(); });
 
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min;
     constexpr uint32_t kRowsA = 0xfu << 16, kRowsB = 0xf0u << 16;
@@ -376,7 +385,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
         const int i = block_last - b * 32 - t;
         return i >= (int)start ? i : -1;
     };
-    StagePipe<32, decltype(pos), !COMPACT> pipe(pos, list, rec, &raw);
+    StagePipe<32, decltype(pos), !COMPACT> pipe(pos, list, rec, &raw, split, &s_tail);
     pipe.start();
     const int nb = (block_last + 1 - (int)start + 31) / 32;
     for (int b = 0; b < nb; ++b) {
@@ -449,7 +458,8 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
     float bg0, float bg1, float bg2, const float* __restrict__ d_color, const float* __restrict__ color,
     const float* __restrict__ target, float inv_n, float* __restrict__ loss_partials, float4* __restrict__ grad2d,
     int nblocks, int* __restrict__ counter, const uint32_t* __restrict__ blist, const uint32_t* __restrict__ bidx,
-    const int32_t* __restrict__ bcount, const uint32_t* __restrict__ cls_cnt, const uint32_t* __restrict__ cls_list) {
+    const int32_t* __restrict__ bcount, const uint32_t* __restrict__ cls_cnt, const uint32_t* __restrict__ cls_list,
+    TileTails tt) {
     // Work order: the forward filed every block under a cost class (heaviest first); lane l holds
     // the exclusive starts of classes 2l and 2l + 1, so the k-th pull maps to (class, rank) with
     // two ballots.  Without classes the blocks go in raster order.
@@ -480,11 +490,11 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
         }
         const int bc = blist ? bcount[b] : kBlockList + 1;
         if (bc <= kBlockList)
-            blend_backward_block_px2<THR, true>(b, cp, ranges, blist, rec, t_final, last_index, bg0, bg1, bg2,
+            blend_backward_block_px2<THR, true>(b, cp, ranges, tt, blist, rec, t_final, last_index, bg0, bg1, bg2,
                                                 d_color, color, target, inv_n, loss_partials, grad2d,
                                                 bidx + (size_t)b * kBlockList, bc);
         else
-            blend_backward_block_px2<THR, false>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2,
+            blend_backward_block_px2<THR, false>(b, cp, ranges, tt, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2,
                                                  d_color, color, target, inv_n, loss_partials, grad2d, nullptr, 0);
         __syncwarp();
     }
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(32) blend_backward_px2_persistent(
 
 template <bool THR, int BW, int BH>
 __global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, const uint32_t* __restrict__ ranges,
-                                                            const uint32_t* __restrict__ pair_gauss,
+                                                            TileTails tt, const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
                                                             const float* __restrict__ t_final,
                                                             const int32_t* __restrict__ last_index, float bg0,
@@ -501,12 +511,12 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_kernel(CamParams cp, c
                                                             const float* __restrict__ target, float inv_n,
                                                             float* __restrict__ loss_partials,
                                                             float4* __restrict__ grad2d) {
-    blend_backward_block<THR, BW, BH>((int)blockIdx.x, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
+    blend_backward_block<THR, BW, BH>((int)blockIdx.x, cp, ranges, tt, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
 }
 
 template <bool THR, int BW, int BH>
 __global__ void __launch_bounds__(BW * BH) blend_backward_persistent(CamParams cp, const uint32_t* __restrict__ ranges,
-                                                            const uint32_t* __restrict__ pair_gauss,
+                                                            TileTails tt, const uint32_t* __restrict__ pair_gauss,
                                                             const ProjRec* __restrict__ rec,
                                                             const float* __restrict__ t_final,
                                                             const int32_t* __restrict__ last_index, float bg0,
@@ -523,7 +533,7 @@ __global__ void __launch_bounds__(BW * BH) blend_backward_persistent(CamParams c
         __syncthreads();
         const int b = s_bid;
         if (b >= nblocks) break;
-        blend_backward_block<THR, BW, BH>(b, cp, ranges, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
+        blend_backward_block<THR, BW, BH>(b, cp, ranges, tt, pair_gauss, rec, t_final, last_index, bg0, bg1, bg2, d_color, color, target, inv_n, loss_partials, grad2d);
     }
 }
 
@@ -668,7 +678,7 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 }  // namespace
 
-cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges, TileTails tt,
                                   const uint32_t* pair_gauss, const ProjRec* rec, const float* t_final,
                                   const int32_t* last_index, const float bg[3], const float* d_color,
                                   const float* color, const float* target, float* loss_partials, float* grad2d,
@@ -687,12 +697,12 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                                                                       W * H, 0);                                  \
             const unsigned pg = (unsigned)(lc.num_sms * (per_sm > 0 ? per_sm : 1));                              \
             blend_backward_persistent<T, W, H><<<pg < grid ? pg : grid, W * H, 0, lc.stream>>>(                  \
-                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
-                loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);              \
+                cp, ranges, tt, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,  \
+                inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1);       \
         } else {                                                                                                  \
             blend_backward_kernel<T, W, H><<<grid, W * H, 0, lc.stream>>>(                                       \
-                cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target, inv_n, \
-                loss_partials, reinterpret_cast<float4*>(grad2d));                                                \
+                cp, ranges, tt, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,  \
+                inv_n, loss_partials, reinterpret_cast<float4*>(grad2d));                                         \
         }                                                                                                         \
     } while (0)
 #define BLEND_BWD(T)                                             \
@@ -714,12 +724,12 @@ cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint
                 blend_backward_px2_persistent<true><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
                     inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
-                    bidx, bcount, cls_cnt, cls_list);
+                    bidx, bcount, cls_cnt, cls_list, tt);
             else
                 blend_backward_px2_persistent<false><<<pg, 32, 0, lc.stream>>>(
                     cp, ranges, pair_gauss, rec, t_final, last_index, bg[0], bg[1], bg[2], d_color, color, target,
                     inv_n, loss_partials, reinterpret_cast<float4*>(grad2d), (int)grid, lc.work_counters + 1, blist,
-                    bidx, bcount, cls_cnt, cls_list);
+                    bidx, bcount, cls_cnt, cls_list, tt);
         } else if (cp.apply_thresholds) BLEND_BWD(true);
         else BLEND_BWD(false);
 #undef BLEND_BWD

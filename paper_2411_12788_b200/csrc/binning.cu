@@ -299,7 +299,7 @@ __device__ __forceinline__ void file_tile(uint32_t* tcls, int n_tiles, int t, ui
 
 __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges,
                                int n_st, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ piece_st,
-                               uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls) {
+                               uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls, uint32_t* __restrict__ tails) {
     pdl_wait();
     pdl_trigger();
     const int st = blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,6 +316,10 @@ __global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
             if (tx < tiles_x && ty < tiles_y) {
                 ranges[2 * (ty * tiles_x + tx)] = kSTT * lo;
                 ranges[2 * (ty * tiles_x + tx) + 1] = kSTT * lo;
+                if (tails) {
+                    tails[2 * (ty * tiles_x + tx)] = 0u;
+                    tails[2 * (ty * tiles_x + tx) + 1] = 0u;
+                }
                 if (tcls) file_tile(tcls, tiles_x * tiles_y, ty * tiles_x + tx, 0u);
             }
         }
@@ -391,22 +395,43 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges, int n_st,
     const uint32_t* __restrict__ piece_st, const uint32_t* __restrict__ piece_cnt,
     const uint32_t* __restrict__ st_gauss, const uint16_t* __restrict__ st_cover, int tiles_x, int tiles_y, int st_x,
-    uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls) {
+    uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls,
+    uint32_t* __restrict__ tails, uint32_t kpre) {
     constexpr int kW = kL2Threads / 32;
     __shared__ uint32_t s_c[kPieceK][kW][kSTT];    // (slice k, warp) entries covering tile f, then their list position
     __shared__ uint32_t s_prefix[kSTT];
+    __shared__ int s_open;  // tiles of the supertile whose list prefix is not complete yet
     pdl_wait();
     pdl_trigger();
     PieceInfo pi;
     if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t cap = pi.hi_s - pi.lo_s;  // capacity of every tile list of this supertile
-    if (tid < kSTT) {  // counts of this supertile's earlier pieces
+    const bool last_piece = pi.hi == pi.hi_s;
+    if (warp == 0) {  // counts of this supertile's earlier pieces
         const uint32_t id0 = pi.lo_s / kPiece + (uint32_t)pi.st;
         uint32_t pre = 0;
-        for (uint32_t q = 0; q < pi.p; ++q) pre += piece_cnt[(size_t)(id0 + q) * kSTT + tid];
-        s_prefix[tid] = pre;
+        if (lane < kSTT)
+            for (uint32_t q = 0; q < pi.p; ++q) pre += piece_cnt[(size_t)(id0 + q) * kSTT + lane];
+        if (lane < kSTT) s_prefix[lane] = pre;
+        const unsigned open = __ballot_sync(0xffffffffu, lane < kSTT && pre < kpre);
+        if (lane == 0) s_open = (int)open;
+        // every tile's prefix already complete: only the last piece has work (the tiles' ranges)
+        if (!open && last_piece && lane < kSTT) {
+            const int tx = (pi.st % st_x) * kST + (lane % kST), ty = (pi.st / st_x) * kST + (lane / kST);
+            if (tx < tiles_x && ty < tiles_y) {
+                const int t = ty * tiles_x + tx;
+                const uint32_t list0 = (uint32_t)kSTT * pi.lo_s + (uint32_t)lane * cap;
+                const uint32_t len = pre + piece_cnt[(size_t)blockIdx.x * kSTT + lane];
+                ranges[2 * t] = list0;
+                ranges[2 * t + 1] = list0 + kpre;
+                if (tcls) file_tile(tcls, tiles_x * tiles_y, t, len);
+            }
+        }
     }
+    __syncthreads();
+    const unsigned open = (unsigned)s_open;
+    if (!open) return;  // (pieces past every tile's prefix: no loads, no ballots)
     uint32_t gid[kPieceK], cv[kPieceK];
 #pragma unroll
     for (int k = 0; k < kPieceK; ++k) {
@@ -435,26 +460,46 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
         const uint32_t base = list0 + s_prefix[f];
         col[q0 * kSTT + f] = base + inc - v0 - v1;
         col[q1 * kSTT + f] = base + inc - v1;
-        if (lane == 31 && pi.hi == pi.hi_s) {  // last piece: the tile's range
+        if (lane == 31 && last_piece) {  // last piece: the tile's range (materialised part)
             const int tx = (pi.st % st_x) * kST + (f % kST), ty = (pi.st / st_x) * kST + (f / kST);
             if (tx < tiles_x && ty < tiles_y) {
                 const int t = ty * tiles_x + tx;
+                const uint32_t len = base + inc - list0;
                 ranges[2 * t] = list0;
-                ranges[2 * t + 1] = base + inc;
-                if (tcls) file_tile(tcls, tiles_x * tiles_y, t, base + inc - list0);
+                ranges[2 * t + 1] = list0 + min(len, kpre);
+                if (tcls) file_tile(tcls, tiles_x * tiles_y, t, len);
+                if (tails && len <= kpre) {  // complete list: no tail
+                    tails[2 * t] = 0u;
+                    tails[2 * t + 1] = 0u;
+                }
             }
         }
     }
     __syncthreads();
+    // Each tile's entries up to its prefix length kpre are written; the entry at rank kpre - 1
+    // records where the tile's tail starts in the supertile list (StagePipe reads it from there).
     const unsigned lt = lanemask_lt();
+    const int tx0 = (pi.st % st_x) * kST, ty0 = (pi.st / st_x) * kST;
 #pragma unroll
-    for (int k = 0; k < kPieceK; ++k)
+    for (int f = 0; f < kSTT; ++f) {
+        if (!((open >> f) & 1u)) continue;  // warp-uniform: this tile's prefix is complete
+        const uint32_t list0 = (uint32_t)kSTT * pi.lo_s + (uint32_t)f * cap;
 #pragma unroll
-        for (int f = 0; f < kSTT; ++f) {
+        for (int k = 0; k < kPieceK; ++k) {
             const bool on = (cv[k] >> f) & 1u;
             const unsigned m = __ballot_sync(0xffffffffu, on);
-            if (on) pair_gauss[s_c[k][warp][f] + __popc(m & lt)] = gid[k];
+            const uint32_t rank = s_c[k][warp][f] + __popc(m & lt) - list0;
+            if (on && rank < kpre) pair_gauss[list0 + rank] = gid[k];
+            if (on && rank + 1u == kpre && tails) {
+                const int tx = tx0 + (f % kST), ty = ty0 + (f / kST);
+                if (tx < tiles_x && ty < tiles_y) {
+                    const int t = ty * tiles_x + tx;
+                    tails[2 * t] = pi.lo + k * kL2Threads + tid + 1u;
+                    tails[2 * t + 1] = pi.hi_s;
+                }
+            }
         }
+    }
 }
 
 // Fallback path (supertile lists from the pair sort): covers from the rects.
@@ -498,6 +543,26 @@ bool st_chunked(int n_st) { return n_st <= kStMaxSmem; }
 int st_chunks(int n_surv) { return n_surv > kStChunkCta ? (n_surv + kStChunkCta - 1) / kStChunkCta : 1; }
 // CTA counts (scanned in place) + the total slot, then the per-warp count rows
 size_t st_chunk_words(int n_surv, int n_st) { return (size_t)n_st * st_chunks(n_surv) * (1 + kStWarps) + 1; }
+
+namespace {
+// Level 2's emit: every tile's list up to kpre entries (0xffffffff: the whole list) and the
+// supertile-list position of the rest (tails).
+cudaError_t launch_bin_emit(LaunchCtx& lc, const BinningArgs& a, const uint32_t* gauss, uint32_t kpre,
+                            uint32_t* tcls) {
+    const int n_st = a.st_x * a.st_y;
+    const uint32_t* cnt = st_chunked(n_st) ? a.st_cnt : nullptr;
+    const int nch = st_chunks(a.n_surv);
+    const uint32_t np = (uint32_t)bin_l2_pieces(a.st_pairs, n_st);
+    if (np == 0) return cudaSuccess;
+    LaunchScope s(lc, "bin_emit");
+    const cudaError_t e = launch_pdl(lc.stream, bin_emit_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
+                                     (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)a.l2_tmp,
+                                     (const uint32_t*)(a.l2_tmp + np), gauss, (const uint16_t*)a.st_cover, a.tiles_x,
+                                     a.tiles_y, a.st_x, a.pair_gauss, a.ranges, tcls, a.tails, kpre);
+    lc.count++;
+    return e;
+}
+}  // namespace
 
 cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
     const int n_st = a.st_x * a.st_y;
@@ -573,7 +638,7 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
             LaunchScope s(lc, "bin_map");
             e = launch_pdl(lc.stream, bin_map_kernel, dim3(blocks_for(n_st, 128)), dim3(128), 0, cnt, nch,
                            (const uint32_t*)a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, piece_st, a.ranges,
-                           cnt ? a.tcls : nullptr);
+                           cnt ? a.tcls : nullptr, a.tails);
             if (e != cudaSuccess) return e;
             lc.count++;
         }
@@ -586,17 +651,17 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
                 if (e != cudaSuccess) return e;
                 lc.count++;
             }
-            LaunchScope s(lc, "bin_emit");
-            e = launch_pdl(lc.stream, bin_emit_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
-                           (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)piece_st, (const uint32_t*)piece_cnt,
-                           gauss, (const uint16_t*)a.st_cover, a.tiles_x, a.tiles_y, a.st_x, a.pair_gauss, a.ranges,
-                           cnt ? a.tcls : nullptr);
+            e = launch_bin_emit(lc, a, gauss, a.list_prefix, cnt ? a.tcls : nullptr);
             if (e != cudaSuccess) return e;
-            lc.count++;
         }
     }
+    if (a.st_list) *a.st_list = gauss;
     (void)n_tiles;
     return cudaGetLastError();
+}
+
+cudaError_t complete_tile_lists(LaunchCtx& lc, const BinningArgs& a, const uint32_t* st_list) {
+    return launch_bin_emit(lc, a, st_list, 0xffffffffu, nullptr);
 }
 
 }  // namespace splat_b200

@@ -116,6 +116,9 @@ struct FwdState {
     const int32_t* bcount = nullptr;
     const uint32_t* cls_cnt = nullptr;
     const uint32_t* cls_list = nullptr;
+    TileTails tails{};                 // tile lists materialised only up to a prefix (or null)
+    BinningArgs ba{};                  // the binning of this forward (complete_tile_lists)
+    bool binned = false;
     float* color = nullptr;
     float* alpha = nullptr;
     float* depth = nullptr;
@@ -165,6 +168,10 @@ struct splat_ctx {
     // per 8 x 8 block: the staged list entries the forward walked (replayed by the backward)
     DevBuf blist, bidx, bcount;
     DevBuf cls;  // the backward's work-order classes: [64 counters | 64 x n_blocks lists]
+    DevBuf tails;  // per tile [first, end) of its list's rest in the supertile list
+    const uint32_t* st_list_used = nullptr;
+    uint32_t list_prefix = 4096;  // tile-list entries materialised per tile (SPLAT_LIST_PREFIX, 0: all)
+    bool list_prefix_adaptive = true;  // doubled after a forward walked past it
     bool block_order_on = true;
     // splat_project: the forward also records cov2d and the radius per Gaussian
     bool want_proj = false;
@@ -367,6 +374,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     }
     if (!ctx->host_counters) {
         CK(cudaHostAlloc(&ctx->host_counters, 64, cudaHostAllocMapped), "alloc pinned");
+        std::memset(ctx->host_counters, 0, 64);
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_counters_dev), ctx->host_counters, 0),
            "map pinned");
     }
@@ -390,6 +398,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     int n_surv = 0;
     uint64_t n_pairs = 0;
     const bool pairs_alt = false;
+    TileTails tt{};
+    BinningArgs saved_ba{};
+    bool binned = false;
     if (n > 0) {
         GaussianPtrs gp{g->centers, g->log_scales, g->rotations, g->opacity_logits, g->sh, n, g->active_sh_degree};
         uint32_t* keys = ctx->keys[0].as<uint32_t>();
@@ -466,7 +477,26 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         ba.scan_tmp = ctx->scan_tmp.as<uint32_t>();
         ba.tcls = chunked ? tcls : nullptr;
         if (!chunked) tcls = nullptr;  // the fallback binning does not file tiles
+        // tile lists past the prefix stay in the supertile lists (read through the tails): the
+        // blend kernels stop at saturation long before (config 1: deepest walk 3.4 K entries)
+        volatile uint32_t* note = ctx->host_counters + kTailNoteWord;
+        if (*note && ctx->list_prefix_adaptive) {  // a forward walked past its prefix: double it
+            *note = 0u;
+            ctx->list_prefix = ctx->list_prefix >= 0x40000000u ? 0xffffffffu : 2u * ctx->list_prefix;
+        }
+        ba.list_prefix = ctx->list_prefix;
+        ba.tails = nullptr;
+        if (ctx->list_prefix != 0xffffffffu) {
+            CK(ctx->tails.ensure((size_t)n_tiles * 8), "alloc tails");
+            ba.tails = ctx->tails.as<uint32_t>();
+        }
+        ba.st_list = &ctx->st_list_used;
         CK(launch_binning(lc, ba), "binning");
+        tt.tails = ba.tails;
+        tt.st_list = ctx->st_list_used;
+        tt.st_cover = ba.st_cover;
+        binned = true;
+        saved_ba = ba;
     } else {
         CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_tiles * 8, s), "memset ranges");
         CK(ctx->pair_gauss[0].ensure(4), "alloc pairs");
@@ -489,6 +519,10 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     fo.max_pixel_count = report ? rep->max_pixel_count : nullptr;
     fo.t_final = ctx->t_final.as<float>();
     fo.last_index = ctx->last_index.as<int32_t>();
+    fo.tails = tt.tails;
+    fo.st_list = tt.st_list;
+    fo.st_cover = tt.st_cover;
+    fo.tail_note = tt.tails ? ctx->host_counters_dev + kTailNoteWord : nullptr;
     // the backward's one-warp 8 x 8 kernel replays the forward's per-block staged lists
     const bool block_lists = lc.bwd_px2 && lc.persistent_blend && lc.work_counters && cp.block_w == 8 &&
                              cp.block_h == 8 && cp.tile_size >= 16 && !rep;
@@ -552,6 +586,9 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
     st.bcount = fo.bcount;
     st.cls_cnt = fo.cls_cnt;
     st.cls_list = fo.cls_list;
+    st.tails = tt;
+    st.ba = saved_ba;
+    st.binned = binned;
     st.valid = true;
     return SPLAT_OK;
 }
@@ -669,6 +706,16 @@ uint32_t read_u32(splat_ctx* ctx, const uint32_t* dev, int* rc) {
     return v;
 }
 
+// The last forward's tile lists in full (the bit-exact getters): materialise the parts past the
+// prefix; the blend kernels then find no tails.
+int complete_lists(splat_ctx* ctx) {
+    FwdState& st = ctx->st;
+    if (!st.tails.tails) return SPLAT_OK;
+    CK(complete_tile_lists(ctx->lc, st.ba, st.tails.st_list), "complete tile lists");
+    st.tails = TileTails{};
+    return SPLAT_OK;
+}
+
 bool state_matches(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cam, const splat_raster_config* cfg,
                    const uint8_t* mask, const float bg[3]) {
     const FwdState& st = ctx->st;
@@ -720,7 +767,7 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
     }
     if (n > 0 || (target && loss_dev)) {
         const uint32_t* sorted_gauss = ctx->pair_gauss[st.pairs_in_alt ? 1 : 0].as<uint32_t>();
-        CK(launch_blend_backward(lc, st.cp, ctx->ranges.as<uint32_t>(), sorted_gauss, ctx->rec.as<ProjRec>(),
+        CK(launch_blend_backward(lc, st.cp, ctx->ranges.as<uint32_t>(), st.tails, sorted_gauss, ctx->rec.as<ProjRec>(),
                                  ctx->t_final.as<float>(), ctx->last_index.as<int32_t>(), bg, d_color, st.color, target,
                                  partials, ctx->grad2d.as<float>(), st.blist, st.bidx, st.bcount, st.cls_cnt,
                                  st.cls_list),
@@ -873,6 +920,11 @@ int splat_ctx_create(int device, splat_ctx** out) {
         c->lc.persistent_blend = !(e && std::strcmp(e, "0") == 0);
         const char* e2 = std::getenv("SPLAT_BWD_PX2");
         c->lc.bwd_px2 = !(e2 && std::strcmp(e2, "0") == 0);
+        const char* ep = std::getenv("SPLAT_LIST_PREFIX");
+        if (ep) {  // a fixed prefix (A/B, tests)
+            c->list_prefix = std::atoi(ep) > 0 ? (uint32_t)std::atoi(ep) : 0xffffffffu;
+            c->list_prefix_adaptive = false;
+        }
         const char* eo = std::getenv("SPLAT_BLOCK_ORDER");
         c->block_order_on = !(eo && std::strcmp(eo, "0") == 0);
         const char* e3 = std::getenv("SPLAT_COOP_SORT");
@@ -1313,6 +1365,7 @@ int splat_traversal_counts(splat_ctx* ctx, int64_t* visits, int64_t* commits) {
     if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
     *visits = *commits = 0;
     if (st.n == 0 || st.n_pairs == 0) return SPLAT_OK;
+    if (int rc = complete_lists(ctx)) return rc;
     CK(ctx->dscalar.ensure(64), "alloc");
     CK(cudaMemsetAsync(ctx->dscalar.p, 0, 16, ctx->stream), "zero counts");
     unsigned long long* d = ctx->dscalar.as<unsigned long long>();
@@ -1442,6 +1495,7 @@ int splat_tiles_debug(splat_ctx* ctx, int32_t* key_tile, int32_t* gaussian, int3
     if (!ctx) return SPLAT_ERR_INVALID_ARGUMENT;
     const FwdState& st = ctx->st;
     if (!st.valid) return set_err(ctx, SPLAT_ERR_NO_FORWARD_STATE, "no forward state");
+    if (int rc = complete_lists(ctx)) return rc;
     CK(cudaStreamSynchronize(ctx->stream), "sync");
     const int k = st.pairs_in_alt ? 1 : 0;
     const int n_tiles = st.cp.tiles_x * st.cp.tiles_y;

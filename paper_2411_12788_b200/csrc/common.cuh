@@ -8,6 +8,7 @@
 // backward (compiled with FMA contraction on) replays the forward's alphas bit for bit.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -335,6 +336,42 @@ struct StageRaw {
     float4 r[CAP][3];  // one raw ProjRec per thread slot
 };
 
+// A tile list whose materialised part stops at a prefix (binning.cu, kListPrefix): positions from
+// `split` on are read from the tile's supertile list instead, from entry `first` on, skipping the
+// entries whose cover misses the tile (bit `bit`) — the same entries in the same (depth) order as
+// the full tile list.  Kept in shared memory (the staging loops read it only past the prefix).
+struct ListTail {
+    const uint32_t* gauss;  // supertile list (Gaussian ids)
+    const uint16_t* cover;  // their 16-bit tile covers
+    uint32_t first;         // supertile-list index of virtual position `split`
+    uint32_t bit;           // the tile's bit in the covers
+};
+
+// Tile t's list: positions [start, mend) in pair_gauss, then (tails[2 t] < tails[2 t + 1]) the
+// supertile-list entries [tails[2 t], tails[2 t + 1]) as virtual positions [mend, end).  Sets up
+// *tail (call with the CTA / warp converged; `sync` orders the write against earlier readers and
+// the pipe's first loads) and returns the split position (INT_MAX when the list is complete).
+template <typename Sync>
+__device__ __forceinline__ int list_tail_setup(const uint32_t* __restrict__ tails, const uint32_t* __restrict__ st_gauss,
+                                               const uint16_t* __restrict__ st_cover, int tile, int tiles_x,
+                                               uint32_t mend, uint32_t& end, ListTail* tail, bool leader, Sync sync) {
+    end = mend;
+    if (!tails) return INT_MAX;
+    const uint32_t t0 = tails[2 * tile], t1 = tails[2 * tile + 1];
+    if (t0 >= t1) return INT_MAX;
+    end = mend + (t1 - t0);
+    sync();  // every reader of the previous block's tail is past it
+    if (leader) {
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        tail->gauss = st_gauss;
+        tail->cover = st_cover;
+        tail->first = t0;
+        tail->bit = (uint32_t)((ty & 3) * 4 + (tx & 3));
+    }
+    sync();
+    return (int)mend;
+}
+
 // PosFn pos(b, t): list position of thread t's entry in batch b, or -1 when batch b has no entry t.
 // CULL = false: the list is already block-culled (the forward's per-block list): keep every entry.
 template <int CAP, typename PosFn, bool CULL = true, int ITEMS = 1>
@@ -345,13 +382,30 @@ struct StagePipe {
     const uint32_t* __restrict__ pair_gauss;
     const ProjRec* __restrict__ rec;
     StageRaw<CAP>* raw;
+    int split;              // positions >= split come from *tail (list_tail_setup)
+    const ListTail* tail;
     int idx_f[ITEMS];       // entries whose records are in flight to raw (batch b)
     uint32_t gid_f[ITEMS];
     int idx_n[ITEMS];       // entries of batch b + 1, ids loaded into gid_n
     uint32_t gid_n[ITEMS];
 
-    __device__ __forceinline__ StagePipe(PosFn p, const uint32_t* pg, const ProjRec* rc, StageRaw<CAP>* rw)
-        : pos(p), pair_gauss(pg), rec(rc), raw(rw) {}
+    __device__ __forceinline__ StagePipe(PosFn p, const uint32_t* pg, const ProjRec* rc, StageRaw<CAP>* rw,
+                                         int split_ = INT_MAX, const ListTail* tail_ = nullptr)
+        : pos(p), pair_gauss(pg), rec(rc), raw(rw), split(split_), tail(tail_) {}
+
+    // Gaussian id at list position idx (idx < 0: none); a tail entry whose cover misses the tile
+    // becomes an empty slot (idx = -1).
+    __device__ __forceinline__ uint32_t fetch(int& idx) const {
+        if (idx < 0) return 0u;
+        if (idx < split) return __ldg(pair_gauss + idx);
+        const uint32_t e = tail->first + (uint32_t)(idx - split);
+        const uint32_t cv = __ldg(tail->cover + e), gid = __ldg(tail->gauss + e);
+        if (!((cv >> tail->bit) & 1u)) {
+            idx = -1;
+            return 0u;
+        }
+        return gid;
+    }
 
     __device__ __forceinline__ void launch_copy() {
 #pragma unroll
@@ -373,14 +427,14 @@ struct StagePipe {
         for (int q = 0; q < ITEMS; ++q) {
             const int sl = q * blockDim.x + threadIdx.x;
             idx_f[q] = pos(0, sl);
-            gid_f[q] = idx_f[q] >= 0 ? pair_gauss[idx_f[q]] : 0u;
+            gid_f[q] = fetch(idx_f[q]);
         }
         launch_copy();
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
             const int sl = q * blockDim.x + threadIdx.x;
             idx_n[q] = pos(1, sl);
-            gid_n[q] = idx_n[q] >= 0 ? __ldg(pair_gauss + idx_n[q]) : 0u;
+            gid_n[q] = fetch(idx_n[q]);
         }
     }
 
@@ -441,7 +495,7 @@ struct StagePipe {
         for (int q = 0; q < ITEMS; ++q) {
             const int sl = q * blockDim.x + tid;
             idx_n[q] = pos(b + 2, sl);
-            gid_n[q] = idx_n[q] >= 0 ? __ldg(pair_gauss + idx_n[q]) : 0u;
+            gid_n[q] = fetch(idx_n[q]);
         }
         return total;
     }

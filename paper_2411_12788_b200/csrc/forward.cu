@@ -408,7 +408,11 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
     const int px = bx0 + lx;
     const int py = by0 + ly;
     const bool inside = px < cp.width && py < cp.height;
-    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const uint32_t start = ranges[2 * tile];
+    __shared__ ListTail s_tail;
+    uint32_t end;
+    const int split = list_tail_setup(out.tails, out.st_list, out.st_cover, tile, cp.tiles_x, ranges[2 * tile + 1], end,
+                                      &s_tail, tid == 0, []() { __syncthreads(); });
     const float amax_c = cp.alpha_max, cmin = cp.contribution_min, tmin = cp.transmittance_min;
     const float x = (float)px + 0.5f, y = (float)py + 0.5f;
     // this pixel's bits in the staged masks, and this warp's rows (32 / bw rows per warp)
@@ -432,7 +436,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
             const uint32_t i = start + (uint32_t)b * (uint32_t)CAP + (uint32_t)t;
             return i < end ? (int)i : -1;
         };
-        StagePipe<CAP, decltype(pos), true, ITEMS> pipe(pos, pair_gauss, rec, &raw);
+        StagePipe<CAP, decltype(pos), true, ITEMS> pipe(pos, pair_gauss, rec, &raw, split, &s_tail);
         pipe.start();
         const int nb = (int)((end - start + (uint32_t)CAP - 1u) / (uint32_t)CAP);
         for (int b = 0; b < nb; ++b) {
@@ -623,6 +627,10 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
             }
             // the next stage() starts with a barrier: staged entries stay until every warp is done
             run += cnt;
+            // the walk reached the list's tail (past the materialised prefix): tell the host,
+            // which materialises longer prefixes from the next view on
+            if (tid == 0 && out.tail_note && start + (uint32_t)(b + 1) * (uint32_t)CAP > (uint32_t)split)
+                *reinterpret_cast<volatile uint32_t*>(out.tail_note) = 1u;
         }
         pipe.finish();
     }

@@ -99,6 +99,7 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
+constexpr int kTailNoteWord = 9;  // host_counters[9]: a forward walked past a tile-list prefix
 constexpr int kCostClasses = 64;  // work-order cost classes of the persistent blend kernels
 
 struct BinningArgs {
@@ -122,7 +123,16 @@ struct BinningArgs {
     // the forward's work order (chunked path only; nullable): [64 counters | 64 x n_tiles lists],
     // every tile filed under its list-length class as its range is written
     uint32_t* tcls;
+    // List prefixes: each tile's list is materialised up to list_prefix entries (0xffffffff: all);
+    // tails[2 t .. 2 t + 1] = [first, end) of the rest in the supertile list (empty: complete), read
+    // through StagePipe / ListTail.  *st_list receives the supertile list the tails index.
+    uint32_t list_prefix;
+    uint32_t* tails;
+    const uint32_t** st_list;
 };
+// Materialise the rest of every tile list of the last launch_binning(a) (the bit-exact getters);
+// tails become empty.
+cudaError_t complete_tile_lists(LaunchCtx& lc, const BinningArgs& a, const uint32_t* st_list);
 int supertile_side();
 // Capacity (entries) of the per-tile list buffer: every tile of supertile s gets L_s slots.
 size_t bin_l2_pieces(uint64_t st_pairs, int n_st);
@@ -159,6 +169,12 @@ struct FwdOutputs {
     uint32_t* cls_cnt;
     uint32_t* cls_list;
     int n_blocks;
+    // tile-list tails (BinningArgs::tails; null: lists complete); *tail_note (mapped host memory)
+    // is set when a block walks into a tail
+    const uint32_t* tails;
+    const uint32_t* st_list;
+    const uint16_t* st_cover;
+    uint32_t* tail_note;
 };
 
 constexpr int kBlockList = 2048;      // replay-list capacity per 8 x 8 block
@@ -192,7 +208,13 @@ cudaError_t launch_visibility_update(LaunchCtx& lc, const float* importance, con
 //   g2 = d_colour, g3.x = committed samples (touched flag)
 struct Grad2D;
 
-cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
+// The tile lists' tails (BinningArgs::tails, StagePipe) for the kernels that walk tile lists.
+struct TileTails {
+    const uint32_t* tails;  // null: lists complete
+    const uint32_t* st_list;
+    const uint16_t* st_cover;
+};
+cudaError_t launch_blend_backward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges, TileTails tt,
                                   const uint32_t* pair_gauss, const ProjRec* rec,
                                   const float* t_final, const int32_t* last_index, const float bg[3],
                                   const float* d_color, const float* color, const float* target,
