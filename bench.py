@@ -84,7 +84,7 @@ def workload_config(args, world):
             "gaussians": args.gaussians, "width": 1237, "height": 822, "views_per_rank_per_step": args.views,
             "ring_views": RING, "n_ranks": world,
             "allreduce": "59N gradient floats (fp32) when N > 1: NCCL reduce-scatter -> sharded Adam -> all-gather",
-            "l2": "inputs larger than L2 (236 MB parameters + ~160 MB pair lists per view); views rotate each step",
+            "l2": "inputs larger than L2 (236 MB parameters + 59N-float gradients and Adam moments, ~100 MB of per-view records and lists); views rotate each step",
             "scene_seed": 0}
 
 
