@@ -106,6 +106,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
+// st_cnt layout (chunked path): [cnt: n_st x nchunks (supertile-major), exclusive-scanned in
+// place][total][per-warp prefix rows: nchunks x kStWarps x n_st]; cnt[st][0] is the start of
+// supertile st's list.
 // Supertile pass over one chunk of depth-ordered survivors: kStWarps warps per CTA, each owning
 // kStChunk consecutive survivors of the CTA's chunk.  A warp flattens its Gaussians, 32 at a
 // time, into (Gaussian, supertile) entries in (depth, raster) order; every window of 32 entries is
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
 // ---- level 2 -----------------------------------------------------------------------------------
 // Every supertile list is cut into pieces of kPiece entries.  Piece ids need no scan: supertile s
 // owns ids [g(s), g(s+1)) with g(s) = floor(lo_s / kPiece) + s (strictly increasing, and its
-// ceil(L_s / kPiece) pieces fit), so a tiny map kernel writes the id -> supertile table.  Each
+// ceil(L_s / kPiece) pieces fit), so each piece CTA finds its supertile by a ballot search.  Each
 // list entry carries its 16-bit tile cover (written by the level-1 emit), so level 2 reads only
 // coalesced (id, cover) pairs:
 //   bin_count: per piece, entries covering each of the 16 tiles (ballots);
@@ -280,7 +283,6 @@ __global__ void __launch_bounds__(EMIT ? 32 * kEmitWarps : 32 * kStWarps) st_chu
 //              run of the tile's list.
 constexpr int kPiece = 2048;
 constexpr int kPieceK = kPiece / kL2Threads;  // entries per thread
-constexpr uint32_t kNoPiece = 0xffffffffu;
 
 // lo_s: start of supertile s's list (s in [0, n_st]) in the concatenated supertile lists.
 __device__ __forceinline__ uint32_t st_lo(const uint32_t* __restrict__ st_cnt, int nchunks,
@@ -289,7 +291,6 @@ __device__ __forceinline__ uint32_t st_lo(const uint32_t* __restrict__ st_cnt, i
     return s < n_st ? st_ranges[2 * s] : st_ranges[2 * n_st - 1];
 }
 
-// One thread per supertile: piece_st[id] for its id range; empty ranges for empty supertiles.
 // The forward's work order: tile t filed under cost class 63 - min(63, list length / 512) (longest
 // lists first), tcls = [64 counters (zeroed by publish_counts) | 64 x n_tiles lists].
 __device__ __forceinline__ void file_tile(uint32_t* tcls, int n_tiles, int t, uint32_t len) {
@@ -297,34 +298,6 @@ __device__ __forceinline__ void file_tile(uint32_t* tcls, int n_tiles, int t, ui
     tcls[kCostClasses + (size_t)c * n_tiles + atomicAdd(&tcls[c], 1u)] = (uint32_t)t;
 }
 
-__global__ void bin_map_kernel(const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges,
-                               int n_st, int tiles_x, int tiles_y, int st_x, uint32_t* __restrict__ piece_st,
-                               uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls, uint32_t* __restrict__ tails) {
-    pdl_wait();
-    pdl_trigger();
-    const int st = blockIdx.x * blockDim.x + threadIdx.x;
-    if (st >= n_st) return;
-    const uint32_t lo = st_lo(st_cnt, nchunks, st_ranges, n_st, st);
-    const uint32_t hi = st_lo(st_cnt, nchunks, st_ranges, n_st, st + 1);
-    const uint32_t g0 = lo / kPiece + (uint32_t)st, g1 = hi / kPiece + (uint32_t)st + 1u;
-    const uint32_t np = (hi - lo + kPiece - 1) / kPiece;
-    for (uint32_t id = g0; id < g1; ++id) piece_st[id] = id - g0 < np ? (uint32_t)st : kNoPiece;
-    if (hi == lo) {
-        const int tx_base = (st % st_x) * kST, ty_base = (st / st_x) * kST;
-        for (int f = 0; f < kSTT; ++f) {
-            const int tx = tx_base + (f % kST), ty = ty_base + (f / kST);
-            if (tx < tiles_x && ty < tiles_y) {
-                ranges[2 * (ty * tiles_x + tx)] = kSTT * lo;
-                ranges[2 * (ty * tiles_x + tx) + 1] = kSTT * lo;
-                if (tails) {
-                    tails[2 * (ty * tiles_x + tx)] = 0u;
-                    tails[2 * (ty * tiles_x + tx) + 1] = 0u;
-                }
-                if (tcls) file_tile(tcls, tiles_x * tiles_y, ty * tiles_x + tx, 0u);
-            }
-        }
-    }
-}
 
 // The 16 cover bits of a lane as four words of byte counters (byte j of word i = bit 4 i + j):
 // each nibble is spread to bytes by one multiply (copies at bit offsets 0, 7, 14, 21 never
@@ -340,30 +313,72 @@ struct PieceInfo {
     uint32_t p, lo_s, hi_s, lo, hi;
 };
 
-__device__ __forceinline__ bool piece_info(uint32_t id, const uint32_t* __restrict__ piece_st,
-                                           const uint32_t* __restrict__ st_cnt, int nchunks,
-                                           const uint32_t* __restrict__ st_ranges, int n_st, PieceInfo& pi) {
-    const uint32_t st = piece_st[id];
-    if (st == kNoPiece) return false;
-    pi.st = (int)st;
-    pi.lo_s = st_lo(st_cnt, nchunks, st_ranges, n_st, pi.st);
-    pi.hi_s = st_lo(st_cnt, nchunks, st_ranges, n_st, pi.st + 1);
-    pi.p = id - (pi.lo_s / kPiece + st);
+// Piece id -> supertile without a map kernel: g(s) = floor(lo_s / kPiece) + s is strictly
+// increasing, so the owner is the last s with g(s) <= id — found by warp 0 with ballots over 32
+// candidates per round (two rounds up to 1024 supertiles) and shared with the CTA.  Returns false
+// for the ids past a supertile's last piece; *empty_st gets the supertile when the id is the one
+// id of an empty supertile (its tiles' ranges are written by bin_emit).
+__device__ __forceinline__ bool piece_info(uint32_t id, const uint32_t* __restrict__ st_cnt, int nchunks,
+                                           const uint32_t* __restrict__ st_ranges, int n_st, PieceInfo& pi,
+                                           int* empty_st) {
+    __shared__ int s_st;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int base = 0, span = n_st;
+        while (true) {
+            const int stride = span > 32 ? (span + 31) / 32 : 1;
+            const int cand = base + lane * stride;
+            const bool ok = lane * stride < span &&
+                            st_lo(st_cnt, nchunks, st_ranges, n_st, cand) / kPiece + (uint32_t)cand <= id;
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            base += (31 - __clz(m)) * stride;  // g(base) <= id always (g(0) = 0)
+            if (stride == 1) break;
+            span = min(stride, n_st - base);
+        }
+        if (lane == 0) s_st = base;
+    }
+    __syncthreads();
+    const int st = s_st;
+    pi.st = st;
+    pi.lo_s = st_lo(st_cnt, nchunks, st_ranges, n_st, st);
+    pi.hi_s = st_lo(st_cnt, nchunks, st_ranges, n_st, st + 1);
+    pi.p = id - (pi.lo_s / kPiece + (uint32_t)st);
+    const uint32_t np = (pi.hi_s - pi.lo_s + kPiece - 1) / kPiece;
+    if (empty_st) *empty_st = (np == 0) ? st : -1;
+    if (pi.p >= np) return false;
     pi.lo = pi.lo_s + pi.p * kPiece;
     pi.hi = min(pi.lo + (uint32_t)kPiece, pi.hi_s);
     return true;
 }
 
+// The ranges (empty) of an empty supertile's tiles, by its one bin_emit CTA.
+__device__ __forceinline__ void empty_supertile(int st, uint32_t lo, int tiles_x, int tiles_y, int st_x,
+                                                uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls,
+                                                uint32_t* __restrict__ tails) {
+    const int f = threadIdx.x;
+    if (f >= kSTT) return;
+    const int tx = (st % st_x) * kST + (f % kST), ty = (st / st_x) * kST + (f / kST);
+    if (tx < tiles_x && ty < tiles_y) {
+        const int t = ty * tiles_x + tx;
+        ranges[2 * t] = kSTT * lo;
+        ranges[2 * t + 1] = kSTT * lo;
+        if (tails) {
+            tails[2 * t] = 0u;
+            tails[2 * t + 1] = 0u;
+        }
+        if (tcls) file_tile(tcls, tiles_x * tiles_y, t, 0u);
+    }
+}
+
 __global__ void __launch_bounds__(kL2Threads) bin_count_kernel(const uint32_t* __restrict__ st_cnt, int nchunks,
                                                               const uint32_t* __restrict__ st_ranges, int n_st,
-                                                              const uint32_t* __restrict__ piece_st,
                                                               const uint16_t* __restrict__ st_cover,
                                                               uint32_t* __restrict__ piece_cnt) {
     __shared__ uint32_t s_cnt[kSTT];
     pdl_wait();
     pdl_trigger();
     PieceInfo pi;
-    if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
+    if (!piece_info(blockIdx.x, st_cnt, nchunks, st_ranges, n_st, pi, nullptr)) return;
     const int tid = threadIdx.x, lane = tid & 31;
     if (tid < kSTT) s_cnt[tid] = 0u;
     uint32_t cv[kPieceK];
@@ -393,8 +408,7 @@ __global__ void __launch_bounds__(kL2Threads) bin_count_kernel(const uint32_t* _
 
 __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     const uint32_t* __restrict__ st_cnt, int nchunks, const uint32_t* __restrict__ st_ranges, int n_st,
-    const uint32_t* __restrict__ piece_st, const uint32_t* __restrict__ piece_cnt,
-    const uint32_t* __restrict__ st_gauss, const uint16_t* __restrict__ st_cover, int tiles_x, int tiles_y, int st_x,
+    const uint32_t* __restrict__ piece_cnt, const uint32_t* __restrict__ st_gauss, const uint16_t* __restrict__ st_cover, int tiles_x, int tiles_y, int st_x,
     uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls,
     uint32_t* __restrict__ tails, uint32_t kpre) {
     constexpr int kW = kL2Threads / 32;
@@ -404,7 +418,11 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     pdl_wait();
     pdl_trigger();
     PieceInfo pi;
-    if (!piece_info(blockIdx.x, piece_st, st_cnt, nchunks, st_ranges, n_st, pi)) return;
+    int empty = -1;
+    if (!piece_info(blockIdx.x, st_cnt, nchunks, st_ranges, n_st, pi, &empty)) {
+        if (empty >= 0) empty_supertile(empty, pi.lo_s, tiles_x, tiles_y, st_x, ranges, tcls, tails);
+        return;
+    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t cap = pi.hi_s - pi.lo_s;  // capacity of every tile list of this supertile
     const bool last_piece = pi.hi == pi.hi_s;
@@ -556,8 +574,7 @@ cudaError_t launch_bin_emit(LaunchCtx& lc, const BinningArgs& a, const uint32_t*
     if (np == 0) return cudaSuccess;
     LaunchScope s(lc, "bin_emit");
     const cudaError_t e = launch_pdl(lc.stream, bin_emit_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
-                                     (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)a.l2_tmp,
-                                     (const uint32_t*)(a.l2_tmp + np), gauss, (const uint16_t*)a.st_cover, a.tiles_x,
+                                     (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)(a.l2_tmp + np), gauss, (const uint16_t*)a.st_cover, a.tiles_x,
                                      a.tiles_y, a.st_x, a.pair_gauss, a.ranges, tcls, a.tails, kpre);
     lc.count++;
     return e;
@@ -632,21 +649,12 @@ cudaError_t launch_binning(LaunchCtx& lc, const BinningArgs& a) {
         const uint32_t* cnt = st_chunked(n_st) ? a.st_cnt : nullptr;
         const int nch = st_chunks(a.n_surv);
         const uint32_t np = (uint32_t)bin_l2_pieces(a.st_pairs, n_st);
-        uint32_t* piece_st = a.l2_tmp;
-        uint32_t* piece_cnt = a.l2_tmp + np;
-        {
-            LaunchScope s(lc, "bin_map");
-            e = launch_pdl(lc.stream, bin_map_kernel, dim3(blocks_for(n_st, 128)), dim3(128), 0, cnt, nch,
-                           (const uint32_t*)a.st_ranges, n_st, a.tiles_x, a.tiles_y, a.st_x, piece_st, a.ranges,
-                           cnt ? a.tcls : nullptr, a.tails);
-            if (e != cudaSuccess) return e;
-            lc.count++;
-        }
+        uint32_t* piece_cnt = a.l2_tmp + np;  // (the first np words: unused)
         if (np > 0) {
             {
                 LaunchScope s(lc, "bin_count");
                 e = launch_pdl(lc.stream, bin_count_kernel, dim3(np), dim3(kL2Threads), 0, cnt, nch,
-                               (const uint32_t*)a.st_ranges, n_st, (const uint32_t*)piece_st,
+                               (const uint32_t*)a.st_ranges, n_st,
                                (const uint16_t*)a.st_cover, piece_cnt);
                 if (e != cudaSuccess) return e;
                 lc.count++;
