@@ -287,8 +287,11 @@ int splat_reinit_gaussians(splat_ctx* ctx, const float* points_dev, const float*
  * (ParamGrads::add), then OptimState::step on group_mask.  targets[k] is view k's H x W x 3
  * target: device memory, or, with targets_on_host != 0, host memory (pinned for an asynchronous
  * copy) that is copied on a side stream while the view's forward runs.  loss_host (nullable,
- * n_views floats) receives each view's loss and makes the call synchronous; otherwise nothing
- * is synchronised (loss_dev, nullable, gets the losses on the device). */
+ * n_views floats) receives each view's loss: the call returns once the losses are on the host
+ * (with the L1 loss that is before the chain and the optimiser step have finished: they complete
+ * on the context's stream, ahead of anything queued there later, so the next call needs no
+ * synchronisation; read parameters on another stream only after synchronising with it).
+ * Without loss_host nothing is synchronised (loss_dev, nullable, gets the losses on the device). */
 int splat_train_step(splat_ctx* ctx, const splat_params_mut* params, const splat_param_grads* grads,
                      const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
                      uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,

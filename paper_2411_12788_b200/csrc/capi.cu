@@ -184,6 +184,8 @@ struct splat_ctx {
     float* host_loss_dev = nullptr;
     int host_loss_cap = 0;
     uint32_t loss_seq = 0;  // sequence word of splat_train_step's loss read-back
+    bool loss_recorded = false;  // ev_loss marks the last backward's L1 loss (run_backward)
+    cudaStream_t lstream = nullptr;  // the loss read-back of splat_train_step (ahead of the optimiser)
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
     // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
@@ -794,8 +796,13 @@ int run_backward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* c
                         ctx->chain_list.as<uint32_t>(), zero_async),
            "chain");
     }
-    if (loss_side) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_loss, 0), "loss join");
-    else if (partials) CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
+    if (loss_side) {
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_loss, 0), "loss join");
+    } else if (partials) {
+        CK(launch_loss_reduce(lc, partials, n_blocks, inv_n, loss_dev), "loss reduce");
+        CK(cudaEventRecord(ctx->ev_loss, ctx->stream), "record loss");
+    }
+    ctx->loss_recorded = partials != nullptr;
     if (ctx->chain_wait || ctx->twin_member) CK(cudaEventRecord(ctx->ev_chain_done, ctx->stream), "chain done");
     (void)cfg;
     (void)mask;
@@ -958,6 +965,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (ctx->ev_zero) cudaEventDestroy(ctx->ev_zero);
     if (ctx->ev_bwd) cudaEventDestroy(ctx->ev_bwd);
     if (ctx->ev_loss) cudaEventDestroy(ctx->ev_loss);
+    if (ctx->lstream) cudaStreamDestroy(ctx->lstream);
     if (ctx->zstream) {
         cudaStreamSynchronize(ctx->zstream);
         cudaStreamDestroy(ctx->zstream);
@@ -2087,6 +2095,35 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         CK(cudaStreamWaitEvent(s, prev_chain, 0), "join twin");
         ctx->twin_member = ctx->twin->twin_member = false;
     }
+    // The losses are final once every view's L1 reduction ran (each context's last ev_loss covers
+    // its earlier views): read them back on a stream of their own, so the call returns while the
+    // chain and the optimiser still run (the next call's work queues behind them on `s`).
+    bool loss_early = false;
+    uint32_t seq = 0;
+    if (loss_host) {
+        if (ctx->host_loss_cap < n_views) {
+            if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
+            ctx->host_loss = nullptr;
+            ctx->host_loss_cap = 0;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_loss), (size_t)(n_views + 1) * 4, cudaHostAllocMapped),
+               "alloc pinned loss");
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_loss_dev), ctx->host_loss, 0), "map loss");
+            ctx->host_loss_cap = n_views;
+        }
+        seq = ++ctx->loss_seq ? ctx->loss_seq : ++ctx->loss_seq;
+        const bool twin_ok = !overlap || ctx->twin->loss_recorded;
+        if (lambda_dssim <= 0.0f && ctx->loss_recorded && twin_ok) {
+            if (!ctx->lstream) CK(cudaStreamCreateWithFlags(&ctx->lstream, cudaStreamNonBlocking), "loss stream");
+            CK(cudaStreamWaitEvent(ctx->lstream, ctx->ev_loss, 0), "loss ready");
+            if (overlap) CK(cudaStreamWaitEvent(ctx->lstream, ctx->twin->ev_loss, 0), "twin loss ready");
+            cudaStream_t keep = ctx->lc.stream;
+            ctx->lc.stream = ctx->lstream;
+            const cudaError_t e = launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views, seq);
+            ctx->lc.stream = keep;
+            CK(e, "read loss");
+            loss_early = true;
+        }
+    }
     if (ctx->comm && group_mask) {
         // view-parallel: the sharded exchange on the packed buffers (layout checked here)
         const int64_t nn = p->n;
@@ -2113,28 +2150,19 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         return rc;
     }
     if (loss_host) {
-        if (ctx->host_loss_cap < n_views) {
-            if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
-            ctx->host_loss = nullptr;
-            ctx->host_loss_cap = 0;
-            CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_loss), (size_t)(n_views + 1) * 4, cudaHostAllocMapped),
-               "alloc pinned loss");
-            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_loss_dev), ctx->host_loss, 0), "map loss");
-            ctx->host_loss_cap = n_views;
-        }
-        // the losses (the step's last kernel, after the optimiser) are ready when the sequence
-        // word arrives; poll it, checking the stream now and then so an error still surfaces
-        const uint32_t seq = ++ctx->loss_seq ? ctx->loss_seq : ++ctx->loss_seq;
+        // the losses are ready when the sequence word arrives; poll it, checking the stream now
+        // and then so an error still surfaces
         volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(ctx->host_loss) + n_views;
-        CK(launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views, seq), "read loss");
+        if (!loss_early) CK(launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views, seq), "read loss");
+        cudaStream_t ls = loss_early ? ctx->lstream : s;
         for (uint32_t spin = 1; *flag != seq; ++spin) {
             if ((spin & 1023u) == 0u) {
-                const cudaError_t q = cudaStreamQuery(s);
+                const cudaError_t q = cudaStreamQuery(ls);
                 if (q == cudaSuccess) break;  // done: the flag is visible now (re-read below)
                 if (q != cudaErrorNotReady) CK(q, "sync");
             }
         }
-        if (*flag != seq) CK(cudaStreamSynchronize(s), "sync");
+        if (*flag != seq) CK(cudaStreamSynchronize(ls), "sync");
         std::memcpy(loss_host, ctx->host_loss, (size_t)n_views * 4);
     }
     return SPLAT_OK;
