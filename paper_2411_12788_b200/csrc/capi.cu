@@ -320,7 +320,8 @@ cudaError_t depth_sort(splat_ctx* ctx, uint32_t* keys, uint32_t* vals, uint64_t 
         if (e == cudaSuccess) e = ctx->coop_work.ensure(radix_coop_count_words(n) * 4, true, ctx->stream);
         if (e != cudaSuccess) return e;
         e = radix_sort_coop(lc, keys, vals, ctx->keys[1].as<uint32_t>(), ctx->vals[1].as<uint32_t>(),
-                            ctx->ktmp.as<uint32_t>(), ctx->vtmp.as<uint32_t>(), n, ctx->coop_work.as<uint32_t>());
+                            ctx->ktmp.as<uint32_t>(), ctx->vtmp.as<uint32_t>(), n, ctx->coop_work.as<uint32_t>(),
+                            ctx->counters.as<uint32_t>() + kKeyRangeWord);
         if (e == cudaSuccess) {
             *alt = true;
             return cudaSuccess;
@@ -409,7 +410,8 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls),
+                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls,
+                             ctx->coop_sort ? d_counters + kKeyRangeWord : nullptr),
            "preprocess");
         // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
         // writes them to mapped pinned memory, so the host waits only for preprocess (event) while

@@ -69,11 +69,15 @@ cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const u
                                       uint64_t n, uint32_t* tmp, uint32_t* total_dev);
 // Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result lands in keys/vals
 // or, when *result_in_alt, in keys_alt/vals_alt.
+// key_range (nullable, zero at rest, re-zeroed by the sort): [max(~key), max(key)] over the keys
+// other than 0xFFFFFFFF (preprocess's survivors); the sort then derives its passes from the range
+// and needs no histogram pass, and the 0xFFFFFFFF keys come out last in no particular order.
 // Whole sort as one cooperative kernel (result in keys_alt / vals_alt); returns
 // cudaErrorCooperativeLaunchTooLarge when N does not fit one resident wave of 4096-key tiles.
 size_t radix_coop_count_words(uint64_t n);
 cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                            uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work);
+                            uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work,
+                            uint32_t* key_range = nullptr);
 cudaError_t radix_sort_pairs(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt,
                              uint32_t* vals_alt, uint64_t n, int begin_bit, int end_bit,
                              uint32_t* hist, uint32_t* scan_tmp, bool* result_in_alt);
@@ -96,10 +100,12 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
                               float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
-                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr);
+                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr,
+                              uint32_t* key_range = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 constexpr int kTailNoteWord = 9;  // host_counters[9]: a forward walked past a tile-list prefix
+constexpr int kKeyRangeWord = 8;  // counters[8] = max(~key), counters[9] = max(key) over survivors
 constexpr int kCostClasses = 64;  // work-order cost classes of the persistent blend kernels
 
 struct BinningArgs {

@@ -470,7 +470,8 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                                                               uint32_t* __restrict__ k1, uint32_t* __restrict__ v1,
                                                               uint32_t* __restrict__ k2, uint32_t* __restrict__ v2,
                                                               uint32_t n, uint32_t* __restrict__ hist,
-                                                              uint32_t* __restrict__ counts, int tpc_rt) {
+                                                              uint32_t* __restrict__ counts, int tpc_rt,
+                                                              uint32_t* key_range) {
     const int tpc = TPC > 0 ? TPC : tpc_rt;
     cg::grid_group grid = cg::this_grid();
     pdl_trigger();  // st_count (PDL) may be scheduled on the SM slots left free
@@ -498,6 +499,25 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     auto slot_ls = [&](int q) { return s_slots + (size_t)q * (2 * kCoopTile + 256) + 2 * kCoopTile; };
     auto tile_of = [&](int q) { return blockIdx.x + (uint32_t)q * gridDim.x; };
     uint32_t k[kCoopItems], v[kCoopItems];
+    // With the survivors' key range (the depth sort: [max(~key), max(key)] accumulated by
+    // preprocess) the executed passes follow from the range and each pass's histogram is summed
+    // from the tiles' digit counts in its rank phase: no phase 0 (one read of every key and one
+    // grid barrier less).  Culled keys (0xFFFFFFFF) become kmax + 1, so they still sort after
+    // every survivor when the passes above the range's common prefix are skipped.
+    const bool ranged = key_range != nullptr;
+    uint32_t kmax1 = 0;
+    int passes[4], m = 0;
+    if (ranged) {
+        const uint32_t r0 = *reinterpret_cast<volatile uint32_t*>(key_range);
+        const uint32_t r1 = *reinterpret_cast<volatile uint32_t*>(key_range + 1);
+        if (r0 | r1) {  // (no survivors: nothing to order)
+            const uint32_t kmin = ~r0;
+            kmax1 = r1 + 1u;
+            for (int p = 0; p < 4; ++p)
+                if ((kmin >> (8 * p)) != (kmax1 >> (8 * p))) passes[m++] = p;
+        }
+    }
+    if (!ranged) {
     // phase 0: digit histograms of all four bytes
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = 0u;
     __syncthreads();
@@ -524,11 +544,11 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     __syncthreads();
     // executed passes (uniform over the grid) and the buffer chain 0 -> ... -> 1 (alternating
     // 1 / 2 backwards from the last pass)
-    int passes[4], m = 0;
     for (int p = 0; p < 4; ++p) {
         bool trivial = false;
         for (int d = threadIdx.x; d < 256; d += kThreads) trivial |= s_gh[p][d] == n;
         if (!__syncthreads_or(trivial)) passes[m++] = p;
+    }
     }
     uint32_t* kb[3] = {k0, k1, k2};
     uint32_t* vb[3] = {v0, v1, v2};
@@ -539,9 +559,10 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
                 k1[i] = k0[i];
                 v1[i] = v0[i];
             }
-        grid.sync();  // every CTA has read hist
+        grid.sync();  // every CTA has read hist / the key range
         if (blockIdx.x == 0)
             for (int i = threadIdx.x; i < 4 * 256; i += kThreads) hist[i] = 0u;  // zero at rest
+        if (ranged && blockIdx.x == 0 && threadIdx.x < 2) key_range[threadIdx.x] = 0u;  // zero at rest
         return;
     }
     int src = 0;
@@ -553,12 +574,13 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             const uint32_t tile = tile_of(q);
             if (tile >= ntiles) break;  // the last CTAs own one tile fewer (CTA-uniform)
             const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
-            if (j > 0 || q > 0) {  // tile 0 of the first pass is still in registers
+            if (j > 0 || q > 0 || ranged) {  // (phase 0 left tile 0 of the first pass in registers)
 #pragma unroll
                 for (int r = 0; r < kCoopItems; ++r) {
                     const uint32_t i = wbase + r * 32 + lane;
                     k[r] = i < n ? kb[src][i] : 0u;
                     v[r] = i < n ? vb[src][i] : 0u;
+                    if (ranged && j == 0 && k[r] == 0xffffffffu) k[r] = kmax1;
                 }
             }
             for (int i = threadIdx.x; i < kVW * 256 / 2; i += kThreads) reinterpret_cast<uint32_t*>(&s_cnt[0][0])[i] = 0u;
@@ -607,6 +629,7 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
 #pragma unroll
                 for (int w = 0; w < kVW; ++w) c += s_cnt[w][d];
                 counts[(size_t)d * ntiles + tile] = c;
+                if (ranged && c) atomicAdd(&hist[256 * passes[j] + d], c);  // the pass histogram
                 uint32_t tot;
                 const uint32_t ls = block_exclusive_scan(c, &tot, s_warp);
                 slot_ls(q)[d] = ls;
@@ -637,6 +660,10 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
         // scan of the pass histogram, in s_delta until phase C reuses it).  A warp per row (a
         // CTA per row cost two barriers per row: 256 rows on one CTA took 0.4 ms at 2 K keys);
         // with few tiles a thread per row.
+        if (ranged) {
+            s_gh[passes[j]][threadIdx.x] = hist[256 * passes[j] + threadIdx.x];
+            __syncthreads();
+        }
         {
             uint32_t tot;
             const uint32_t hb = block_exclusive_scan(s_gh[passes[j]][threadIdx.x], &tot, s_warp);
@@ -715,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     // (the caller allocates it zeroed; no memset launch per sort)
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < 4 * 256; i += kThreads) hist[i] = 0u;
+    if (ranged && blockIdx.x == 0 && threadIdx.x < 2) key_range[threadIdx.x] = 0u;  // zero at rest
 #ifdef SPLAT_SORT_STAMPS
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ns = 3 + 6 * m;
@@ -827,7 +855,7 @@ size_t radix_coop_count_words(uint64_t n) {
 // (keys_alt, vals_alt).  Returns cudaErrorCooperativeLaunchTooLarge (nothing launched) when the
 // tiles do not fit in one resident wave; the caller falls back to radix_sort_pairs.
 cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                            uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work) {
+                            uint32_t* keys_tmp, uint32_t* vals_tmp, uint64_t n, uint32_t* work, uint32_t* key_range) {
     if (n == 0) return cudaSuccess;
     if (n >= (1ull << 31)) return cudaErrorCooperativeLaunchTooLarge;
     const uint64_t nt = (n + kCoopTile - 1) / kCoopTile;
@@ -866,7 +894,7 @@ cudaError_t radix_sort_coop(LaunchCtx& lc, uint32_t* keys, uint32_t* vals, uint3
     uint32_t* hist = work;  // zero at rest: allocated zeroed, re-zeroed by the kernel
     uint32_t* counts = work + 4 * 256;
     uint32_t nn = (uint32_t)n;
-    void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts, &tpc};
+    void* args[] = {&keys, &vals, &keys_alt, &vals_alt, &keys_tmp, &vals_tmp, &nn, &hist, &counts, &tpc, &key_range};
     LaunchScope s(lc, "radix_sort");
     const void* fn = tpc == 1 ? (const void*)radix_coop_kernel<1> : (const void*)radix_coop_kernel<0>;
     const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, smem, lc.stream);
