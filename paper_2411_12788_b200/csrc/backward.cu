@@ -407,15 +407,21 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
 #pragma unroll
             for (int k = 0; k < 24; ++k) v[k] = 0.0f;
             bool anyc_a = false, anyc_b = false;
+            // the lane's two pixels share their column: dx and the dx-only products once per entry
+            const float dxa = __fsub_rn(r0a.x, P[0].x), dxb = __fsub_rn(r0b.x, P[0].x);
+            const float adxa = __fmul_rn(__fmul_rn(r0a.z, dxa), dxa), adxb = __fmul_rn(__fmul_rn(r0b.z, dxb), dxb);
+            const float wdxa = __fmul_rn(r0a.w, dxa), wdxb = __fmul_rn(r0b.w, dxb);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const bool wa = h == 0 ? waA : waB, wb = h == 0 ? wbA : wbB;
                 if (!(wa || wb)) continue;
                 PixBwd& q = P[h];
-                float alpha_a, g_a, dxa, dya, alpha_b, g_b, dxb, dyb;
+                float alpha_a, g_a, dya, alpha_b, g_b, dyb;
                 bool cl_a, cl_b;
-                bool ga = gate_sample_nb<THR>(r0a, r1a, q.bits, q.x, q.y, amax_c, cmin, alpha_a, g_a, cl_a, dxa, dya);
-                bool gb = gate_sample_nb<THR>(r0b, r1b, q.bits, q.x, q.y, amax_c, cmin, alpha_b, g_b, cl_b, dxb, dyb);
+                bool ga = gate_sample_col<THR>(r0a, r1a, q.bits, dxa, adxa, wdxa, q.y, amax_c, cmin, alpha_a, g_a, cl_a,
+                                               dya);
+                bool gb = gate_sample_col<THR>(r0b, r1b, q.bits, dxb, adxb, wdxb, q.y, amax_c, cmin, alpha_b, g_b, cl_b,
+                                               dyb);
                 ga = ga && wa && idx_a <= q.last;
                 gb = gb && wb && idx_b <= q.last;
                 commit_sample(ga, v, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,

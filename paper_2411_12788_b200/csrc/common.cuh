@@ -178,6 +178,34 @@ __device__ __forceinline__ bool gate_sample_nb(const float4& r0, const float4& r
     return ok;
 }
 
+// gate_sample_nb with the column terms precomputed (the two pixels of a backward lane share x):
+// dx = mean.x - x, adx = (conic0 dx) dx, wdx = conic1 dx — the same rounded operations, so the
+// same alpha bits.
+template <bool THR>
+__device__ __forceinline__ bool gate_sample_col(const float4& r0, const float4& r1, uint32_t mybits, float dx,
+                                                float adx, float wdx, float y, float alpha_max, float contribution_min,
+                                                float& alpha, float& g2d, bool& clamped, float& dy) {
+    const bool inrect = (__float_as_uint(r1.z) & mybits) == mybits;
+    dy = __fsub_rn(r0.y, y);
+    const float b = __fmul_rn(__fmul_rn(r1.x, dy), dy);
+    const float m = __fmul_rn(-0.5f, __fadd_rn(adx, b));
+    const float power = __fsub_rn(m, __fmul_rn(wdx, dy));
+    bool ok = inrect && !(power > 0.0f);
+    if (THR) {
+        ok = ok && !(power < r1.w);
+        g2d = splat_expf_core(power);  // meaningless (never used) outside [cut, 0]
+        alpha = __fmul_rn(r1.y, g2d);
+        clamped = alpha > alpha_max;
+        alpha = clamped ? alpha_max : alpha;
+        ok = ok && !(alpha < contribution_min);
+    } else {
+        g2d = splat_expf(power);
+        alpha = __fmul_rn(r1.y, g2d);
+        clamped = false;
+    }
+    return ok;
+}
+
 // Exactness-preserving block cull.  The Gaussian can pass the alpha gate somewhere in the pixel
 // block [bx0, bx1) x [by0, by1) only if (a) its pixel rect meets the block and (b) the maximum of
 // power = -q(dx, dy) / 2 over the block's pixel centres reaches cut = ln(cmin / opacity) - 1e-3
