@@ -427,10 +427,21 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     const uint32_t cap = pi.hi_s - pi.lo_s;  // capacity of every tile list of this supertile
     const bool last_piece = pi.hi == pi.hi_s;
     if (warp == 0) {  // counts of this supertile's earlier pieces
+        // lane f + 16 h sums tile f's counts over the pieces q = h (mod 2), eight loads in flight
         const uint32_t id0 = pi.lo_s / kPiece + (uint32_t)pi.st;
+        const int f = lane & (kSTT - 1), h = lane >> 4;
         uint32_t pre = 0;
-        if (lane < kSTT)
-            for (uint32_t q = 0; q < pi.p; ++q) pre += piece_cnt[(size_t)(id0 + q) * kSTT + lane];
+        for (uint32_t q0 = (uint32_t)h; q0 < pi.p; q0 += 16) {
+            uint32_t x[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t q = q0 + 2u * r;
+                x[r] = q < pi.p ? piece_cnt[(size_t)(id0 + q) * kSTT + f] : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) pre += x[r];
+        }
+        pre += __shfl_xor_sync(0xffffffffu, pre, 16);
         if (lane < kSTT) s_prefix[lane] = pre;
         const unsigned open = __ballot_sync(0xffffffffu, lane < kSTT && pre < kpre);
         if (lane == 0) s_open = (int)open;
