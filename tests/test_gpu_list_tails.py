@@ -48,3 +48,56 @@ def test_default_prefix_on_deep_walks(oracle):
     fw = R.forward_debug()
     lens = fw["ranges"][:, 1] - fw["ranges"][:, 0]
     assert lens.max() > 4096, lens.max()
+
+
+def test_fallback_supertile_pass_with_prefix_lists(oracle):
+    """More supertiles than the chunked level-1 pass keeps in shared memory (2560 x 1600 at tile
+    size 8: 4000 supertiles) take the fallback supertile pass (pair sort + cover kernel); with the
+    prefix cut to 64 entries its tile lists are read through the tails too."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import sys
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+from helpers import assert_bitwise, assert_grads_close
+from oracle_lib import OracleLib
+from paper_2411_12788_b200 import scenes
+from paper_2411_12788_b200 import rasterizer as R
+from paper_2411_12788_b200.capi import RasterConfig
+oracle = OracleLib()
+s = scenes.make_gaussians(40_000, seed=11)
+cam = scenes.fov_camera(2560, 1600, 60.0, (0.0, 0.3, -3.0))
+cfg = RasterConfig()
+cfg.tile_size = 8
+out = R.render(s, cam, cfg)
+want = oracle.render(s, cam, cfg, report=False)
+for key in ("color", "alpha", "depth", "transmittance", "max_contributor"):
+    assert_bitwise(getattr(out, key), want[key], key)
+target = oracle.render(scenes.perturbed(s), cam, cfg, report=False)["color"]
+_, d_color = oracle.l1_loss(want["color"], target)
+# 4 M pixels: the float sums of the GPU (atomics) and of the reference (pixel order) drift apart by
+# ~1e-4 of a block's scale, so the GPU is held to the fp64 reference instead (as close as the
+# reference's own float path, like test_gpu_fullsize.py at config 1)
+import numpy as np
+got = R.render_backward(s, cam, cfg, d_color)
+want = oracle.render_backward(s, cam, d_color, cfg=cfg)
+g64 = OracleLib("ref", "B").render_backward_f64(s, cam, d_color, cfg=cfg)
+assert_grads_close(got, want, rtol=5e-4, what="fallback supertile pass", norm_tol=1e-4)
+for k in g64:
+    truth = np.asarray(g64[k], np.float64)
+    e_gpu = np.linalg.norm(np.asarray(got[k], np.float64) - truth)
+    e_ref = np.linalg.norm(np.asarray(want[k], np.float64) - truth)
+    assert e_gpu <= 1.05 * e_ref + 1e-6 * np.linalg.norm(truth), (k, e_gpu, e_ref)
+fw = R.forward_debug()
+to = oracle.tiles(s, cam, cfg)
+assert_bitwise(fw["ranges"], to["ranges"], "ranges")
+assert_bitwise(fw["gaussian"], to["gaussian"], "lists")
+print("fallback ok")
+'''
+    for env in ({}, {"SPLAT_LIST_PREFIX": "64"}):
+        r = subprocess.run([sys.executable, "-c", code, str(root)], capture_output=True, text=True, timeout=550,
+                           env=dict(os.environ, **env), cwd=str(root))
+        assert r.returncode == 0 and "fallback ok" in r.stdout, (env, (r.stdout + r.stderr)[-4000:])
