@@ -181,10 +181,15 @@ def cpu_views_per_s(n_gaussians, threads, rounds=1):
     return {"value": threads * rounds / wall, "unit": UNIT, "cores": threads, "kind": ref.kind,
             "sample": f"{threads} threads x {rounds} config-1 ring view(s) each through the reference's own "
                       f"render<float> -> l1_loss -> render_backward<float> -> OptimState::step (means), "
-                      f"{wall:.1f} s wall", "seconds": wall}
+                      f"{wall:.1f} s wall", "seconds": wall, "asymmetry": REF_ASYMMETRY}
 
 
 REF_BUDGET_S = 150.0  # whole reference arm: warm-up + timed rounds
+# stated in both arms' cpu_baseline: what the reference does differently per view
+REF_ASYMMETRY = ("targets are seeded uniform noise (the perturbed-set render is not part of the step; the L1 "
+                 "gradient has the same cost); OptimState::step runs over every group with the non-means "
+                 "gradients zero (the reference has no group mask: about 0.4 s of its ~5.8 s per view, measured "
+                 "with ref_adam_steps at 1 M), while the GPU arm steps the means group only")
 
 
 def run_reference_arm(args):
@@ -220,7 +225,8 @@ def run_reference_arm(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{threads} threads x 1 config-1 view per step, {steps} timed step(s) "
                                        f"(capped to a {REF_BUDGET_S:.0f} s arm); the reference's own C++ "
-                                       f"compiled in place, glibc expf"},
+                                       f"compiled in place, glibc expf",
+                             "asymmetry": REF_ASYMMETRY},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
