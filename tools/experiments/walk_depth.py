@@ -20,7 +20,7 @@ ds = DeviceGaussians.from_host(s, 0)
 buf = np.zeros(2 * 65536, np.uint32)
 ctx.lib.splat_debug_walk.argtypes = [C.c_void_p, C.c_int]
 ctx.lib.splat_debug_walk(buf.ctypes.data, 0)
-for k in (0, 16, 32, 48):
+for k in ([int(a) for a in sys.argv[1:]] or (0, 16, 32, 48)):
     cam = scenes.ring_camera(k, 64)
     render(ds, cam, want_depth=False, ctx=ctx)
     torch.cuda.synchronize()
@@ -28,6 +28,9 @@ for k in (0, 16, 32, 48):
     tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
     walked = buf[:65536][: 4 * tiles].reshape(tiles, 4).max(1).astype(np.int64)
     length = buf[65536:][: 4 * tiles].reshape(tiles, 4).max(1).astype(np.int64)
+    if len(sys.argv) > 5:
+        print(f"view {k}: walked max {walked.max()}, list max {length.max()}")
+        continue
     print(f"view {k}: tiles {tiles}, list entries {length.sum():,}, walked (deepest block per tile) {walked.sum():,} "
           f"({100 * walked.sum() / length.sum():.1f} %); list length p50/p90/max {np.percentile(length, 50):.0f}/"
           f"{np.percentile(length, 90):.0f}/{length.max()}, walked p50/p90/p99/max {np.percentile(walked, 50):.0f}/"
