@@ -410,8 +410,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls,
-                             ctx->coop_sort ? d_counters + kKeyRangeWord : nullptr),
+                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls),
            "preprocess");
         // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
         // writes them to mapped pinned memory, so the host waits only for preprocess (event) while

@@ -80,8 +80,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ tile_counts,
                                                         uint32_t* __restrict__ n_surv, float* __restrict__ depth_out,
-                                                        uint2* __restrict__ rect_ref, float4* __restrict__ proj_dbg,
-                                                        uint32_t* __restrict__ key_range) {
+                                                        uint2* __restrict__ rect_ref, float4* __restrict__ proj_dbg) {
     __shared__ float4 s_sh[VEC_SH ? kPreThreads * kShRow : 1];
     pdl_wait();
     pdl_trigger();
@@ -320,39 +319,27 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
             if (aux) aux[i] = a;
         }
     }
-    __shared__ uint32_t s_pairs[8], s_st[8], s_kmax[8], s_knmin[8];
+    __shared__ uint32_t s_pairs[8], s_st[8];
     uint32_t wp = tiles, ws = alive ? count : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         wp += __shfl_xor_sync(0xffffffffu, wp, o);
         ws += __shfl_xor_sync(0xffffffffu, ws, o);
     }
-    // the survivors' key range for the depth sort (radix_sort_coop key_range): max(key), max(~key)
-    const uint32_t key = __float_as_uint(zc);
-    const uint32_t wkmax = __reduce_max_sync(0xffffffffu, alive ? key : 0u);
-    const uint32_t wknmin = __reduce_max_sync(0xffffffffu, alive ? ~key : 0u);
     if ((threadIdx.x & 31) == 0) {
         s_pairs[threadIdx.x >> 5] = wp;
         s_st[threadIdx.x >> 5] = ws;
-        s_kmax[threadIdx.x >> 5] = wkmax;
-        s_knmin[threadIdx.x >> 5] = wknmin;
     }
     const int block_alive = __syncthreads_count(alive);
     if (threadIdx.x == 0 && block_alive) {
-        uint32_t bp = 0, bs = 0, kmx = 0, knm = 0;
+        uint32_t bp = 0, bs = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
             bp += s_pairs[w];
             bs += s_st[w];
-            kmx = max(kmx, s_kmax[w]);
-            knm = max(knm, s_knmin[w]);
         }
         atomicAdd(n_surv, (uint32_t)block_alive);
         atomicAdd(n_surv + 1, bs);
         atomicAdd(n_surv + 2, bp);
-        if (key_range) {
-            atomicMax(key_range, knm);
-            atomicMax(key_range + 1, kmx);
-        }
     }
 }
 
@@ -861,21 +848,20 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& cp, const uint8_t* mask,
                               ProjRec* rec, AuxRec* aux, uint32_t* keys, uint32_t* vals, uint32_t* tile_counts,
                               uint32_t* n_survivors_dev, float* depth_out, uint2* rect_ref,
-                              uint32_t* host_counts, float4* proj_dbg, uint32_t* cls_cnt, uint32_t* tcls_cnt,
-                              uint32_t* key_range) {
+                              uint32_t* host_counts, float4* proj_dbg, uint32_t* cls_cnt, uint32_t* tcls_cnt) {
     if (g.n == 0) return cudaSuccess;
     const bool vec = (reinterpret_cast<uintptr_t>(g.sh) & 15u) == 0;
     if (vec)
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<true><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                             tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg, key_range);
+                                                                             tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg);
         }
     else
         {
             LaunchScope ls_(lc, "preprocess");
             preprocess_kernel<false><<<blocks_for(g.n, kPreThreads), kPreThreads, 0, lc.stream>>>(g, cp, mask, rec, aux, keys, vals,
-                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg, key_range);
+                                                                              tile_counts, n_survivors_dev, depth_out, rect_ref, proj_dbg);
         }
     lc.count++;
     if (host_counts) {

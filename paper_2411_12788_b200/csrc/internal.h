@@ -69,9 +69,10 @@ cudaError_t exclusive_scan_gather_u32(LaunchCtx& lc, const uint32_t* in, const u
                                       uint64_t n, uint32_t* tmp, uint32_t* total_dev);
 // Stable LSD sort of (keys, vals) on key bits [begin_bit, end_bit). Result lands in keys/vals
 // or, when *result_in_alt, in keys_alt/vals_alt.
-// key_range (nullable, zero at rest, re-zeroed by the sort): [max(~key), max(key)] over the keys
-// other than 0xFFFFFFFF (preprocess's survivors); the sort then derives its passes from the range
-// and needs no histogram pass, and the 0xFFFFFFFF keys come out last in no particular order.
+// key_range (nullable; 2 words, zero at rest, re-zeroed by the sort): the sort first reduces
+// [max(~key), max(key)] over the keys other than 0xFFFFFFFF (the survivors), derives its passes from
+// that range and sums each pass's histogram in its rank phase; the 0xFFFFFFFF keys come out last in
+// no particular order.  Without it a phase 0 histograms all 4 byte digits (stable for every key).
 // Whole sort as one cooperative kernel (result in keys_alt / vals_alt); returns
 // cudaErrorCooperativeLaunchTooLarge when N does not fit one resident wave of 4096-key tiles.
 size_t radix_coop_count_words(uint64_t n);
@@ -100,12 +101,11 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               const uint8_t* mask, ProjRec* rec, AuxRec* aux, uint32_t* keys,
                               uint32_t* vals, uint32_t* tile_counts, uint32_t* n_survivors_dev,
                               float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
-                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr,
-                              uint32_t* key_range = nullptr);
+                              float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr);
 
 // ---- binning.cu ---------------------------------------------------------------------------
 constexpr int kTailNoteWord = 9;  // host_counters[9]: a forward walked past a tile-list prefix
-constexpr int kKeyRangeWord = 8;  // counters[8] = max(~key), counters[9] = max(key) over survivors
+constexpr int kKeyRangeWord = 8;  // counters[8..9]: the depth sort's key-range scratch (zero at rest)
 constexpr int kCostClasses = 64;  // work-order cost classes of the persistent blend kernels
 
 struct BinningArgs {

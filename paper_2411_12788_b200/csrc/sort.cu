@@ -499,15 +499,50 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
     auto slot_ls = [&](int q) { return s_slots + (size_t)q * (2 * kCoopTile + 256) + 2 * kCoopTile; };
     auto tile_of = [&](int q) { return blockIdx.x + (uint32_t)q * gridDim.x; };
     uint32_t k[kCoopItems], v[kCoopItems];
-    // With the survivors' key range (the depth sort: [max(~key), max(key)] accumulated by
-    // preprocess) the executed passes follow from the range and each pass's histogram is summed
-    // from the tiles' digit counts in its rank phase: no phase 0 (one read of every key and one
-    // grid barrier less).  Culled keys (0xFFFFFFFF) become kmax + 1, so they still sort after
-    // every survivor when the passes above the range's common prefix are skipped.
+    // The depth sort (key_range given): phase 0 only reduces the survivors' key range
+    // [max(~key), max(key)] (keys other than 0xFFFFFFFF); the executed passes follow from it and
+    // each pass's histogram is summed from the tiles' digit counts in its rank phase — no
+    // histogram atomics per key.  Culled keys (0xFFFFFFFF) become kmax + 1, so they still sort
+    // after every survivor when the passes above the range's common prefix are skipped.
     const bool ranged = key_range != nullptr;
     uint32_t kmax1 = 0;
     int passes[4], m = 0;
     if (ranged) {
+        uint32_t kmx = 0, knm = 0;
+        // (owned tiles in reverse, so tile 0's keys stay in registers for the first pass)
+        for (int q = tpc - 1; q >= 0; --q) {
+            const uint32_t wbase = tile_of(q) * kCoopTile + warp * (kCoopTile / kWarps);
+#pragma unroll
+            for (int r = 0; r < kCoopItems; ++r) {
+                const uint32_t i = wbase + r * 32 + lane;
+                k[r] = i < n ? k0[i] : 0xffffffffu;
+                if (q == 0) v[r] = i < n ? v0[i] : 0u;
+                if (k[r] != 0xffffffffu) {
+                    kmx = max(kmx, k[r]);
+                    knm = max(knm, ~k[r]);
+                }
+            }
+        }
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        knm = __reduce_max_sync(0xffffffffu, knm);
+        if (lane == 0) {
+            s_warp[warp] = kmx;
+            s_delta[warp] = knm;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kWarps; ++w) {
+                kmx = max(kmx, s_warp[w]);
+                knm = max(knm, s_delta[w]);
+            }
+            if (kmx | knm) {
+                atomicMax(key_range, knm);
+                atomicMax(key_range + 1, kmx);
+            }
+        }
+        STAMP(1);
+        grid.sync();
+        STAMP(2);
         const uint32_t r0 = *reinterpret_cast<volatile uint32_t*>(key_range);
         const uint32_t r1 = *reinterpret_cast<volatile uint32_t*>(key_range + 1);
         if (r0 | r1) {  // (no survivors: nothing to order)
@@ -515,9 +550,11 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             kmax1 = r1 + 1u;
             for (int p = 0; p < 4; ++p)
                 if ((kmin >> (8 * p)) != (kmax1 >> (8 * p))) passes[m++] = p;
+#pragma unroll
+            for (int r = 0; r < kCoopItems; ++r)  // tile 0, in registers
+                if (k[r] == 0xffffffffu) k[r] = kmax1;
         }
-    }
-    if (!ranged) {
+    } else {
     // phase 0: digit histograms of all four bytes
     for (int i = threadIdx.x; i < 4 * 256; i += kThreads) (&s_gh[0][0])[i] = 0u;
     __syncthreads();
@@ -574,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
             const uint32_t tile = tile_of(q);
             if (tile >= ntiles) break;  // the last CTAs own one tile fewer (CTA-uniform)
             const uint32_t wbase = tile * kCoopTile + warp * (kCoopTile / kWarps);
-            if (j > 0 || q > 0 || ranged) {  // (phase 0 left tile 0 of the first pass in registers)
+            if (j > 0 || q > 0) {  // tile 0 of the first pass is still in registers
 #pragma unroll
                 for (int r = 0; r < kCoopItems; ++r) {
                     const uint32_t i = wbase + r * 32 + lane;
