@@ -443,8 +443,10 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
             CK(ctx->st_scan_tmp.ensure(scan_temp_words((uint64_t)n_st * st_chunks(n_surv) + 1) * 4, true, s),
                "alloc st scan");
         }
-        if (tile_list_capacity(st_pairs) >= (size_t)UINT32_MAX)
-            return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "too many tile-Gaussian pairs for 32-bit list offsets");
+        // list positions are 31-bit ints in the blend kernels (tails continue past the capacity
+        // layout by at most one supertile list)
+        if (tile_list_capacity(st_pairs) + st_pairs >= (size_t)INT32_MAX)
+            return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "too many tile-Gaussian pairs for 31-bit list positions");
         CK(ctx->pair_gauss[0].ensure(tile_list_capacity(st_pairs) * 4 + 4), "alloc pairs");
         CK(ctx->st_ranges.ensure((size_t)n_st * 8), "alloc st ranges");
         CK(ctx->l2_tmp.ensure(bin_l2_words(st_pairs, n_st) * 4), "alloc binning scratch");

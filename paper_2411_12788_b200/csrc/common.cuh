@@ -394,7 +394,7 @@ __device__ __forceinline__ int list_tail_setup(const uint32_t* __restrict__ tail
         tail->gauss = st_gauss;
         tail->cover = st_cover;
         tail->first = t0;
-        tail->bit = (uint32_t)((ty & 3) * 4 + (tx & 3));
+        tail->bit = (uint32_t)((ty & 3) * 4 + (tx & 3));  // binning.cu's cover bit (4 x 4 tiles per supertile)
     }
     sync();
     return (int)mend;
