@@ -267,6 +267,26 @@ int splat_visibility_update_max(splat_ctx* ctx, const splat_importance_outputs* 
                                 float threshold, uint32_t* bitmask_dev, double* accum_dev,
                                 int64_t* counts_dev, float* max_all_dev);
 
+/* ---- whole multi-view passes (BASELINE configs 3 and 2) ------------------------------ */
+/* build_masks / global_importance over n_views views (visibility.cpp:9-37, simplify.cpp:13-34):
+ * for each view k, splat_accumulate_importance then splat_visibility_update_max into
+ * masks_dev[k * mask_words ..] (mask_words >= (n+31)/32), accum_dev, counts_dev and max_all_dev
+ * (nullable) — the same results as that loop (updates applied in view order), with consecutive
+ * views' rasterisation overlapped on an internal twin context. */
+int splat_visibility_pass(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cams, int32_t n_views,
+                          const splat_raster_config* cfg, float threshold, uint32_t* masks_dev, int64_t mask_words,
+                          double* accum_dev, int64_t* counts_dev, float* max_all_dev);
+/* depth_reinitialize's unprojection over n_views views (densify.cpp:207-222): for view k, a
+ * depth render and splat_depth_unproject with view_index first_view + k; the points of all views
+ * are appended in view order (raster order within a view) to points_dev [capacity][3],
+ * pixel_dev [capacity] and view_dev [capacity] (nullable: the view index of each point);
+ * *count_dev = the total (may exceed capacity: nothing is written past it).  Views overlap on an
+ * internal twin context as in splat_visibility_pass. */
+int splat_depth_points(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cams, int32_t n_views,
+                       const splat_raster_config* cfg, int rule, float alpha_threshold, int64_t first_view,
+                       int32_t stride, int64_t seed, float* points_dev, int32_t* view_dev, int32_t* pixel_dev,
+                       int64_t capacity, int32_t* count_dev);
+
 /* ---- depth re-initialisation tail (densify.cpp:227-251, spatial.cpp:9-121; §8f rank 2) ---- */
 /* third_neighbor_distances: out_dev[i] = max(distance from point i to its k-th nearest other
  * point, min_dist), k = min(3, m - 1) (all min_dist when m < 2); points_dev [m][3].  Exact (the

@@ -247,6 +247,12 @@ _EXPORTS = {
                                           C.c_void_p, C.c_void_p, C.c_void_p]),
     "splat_visibility_update_max": (C.c_int, [C.c_void_p, C.POINTER(ImportanceOutputs), C.c_int32, C.c_float,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "splat_visibility_pass": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera), C.c_int32,
+                                        C.POINTER(RasterConfig), C.c_float, C.c_void_p, C.c_int64, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]),
+    "splat_depth_points": (C.c_int, [C.c_void_p, C.POINTER(Gaussians), C.POINTER(Camera), C.c_int32,
+                                     C.POINTER(RasterConfig), C.c_int, C.c_float, C.c_int64, C.c_int32, C.c_int64,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "splat_quantile_threshold": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
                                            C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "splat_quantile_threshold_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,

@@ -147,6 +147,8 @@ struct splat_ctx {
     bool twin_member = false;  // part of an overlapped multi-view step (record ev_chain_done)
     cudaEvent_t chain_wait = nullptr;  // run_backward: wait for this before the chain
     cudaEvent_t ev_chain_done = nullptr, ev_step = nullptr;
+    cudaEvent_t ev_pass = nullptr;  // multi-view passes: this context's last per-view update
+    DevBuf pass_img, pass_rep;      // multi-view passes: this context's per-view images / report
     std::string err;
     // per-Gaussian
     DevBuf rec, aux, depth, rect_ref, keys[2], vals[2], tile_counts, counts_sorted, offsets, counters, grad2d;
@@ -920,7 +922,8 @@ int splat_ctx_create(int device, splat_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_bwd, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_chain_done, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_pass, cudaEventDisableTiming) != cudaSuccess) {
         cudaFree(c->lc.work_counters);
         delete c;
         return SPLAT_ERR_CUDA;
@@ -960,6 +963,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     }
     if (ctx->ev_chain_done) cudaEventDestroy(ctx->ev_chain_done);
     if (ctx->ev_step) cudaEventDestroy(ctx->ev_step);
+    if (ctx->ev_pass) cudaEventDestroy(ctx->ev_pass);
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
     if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
@@ -1974,6 +1978,24 @@ int splat_reinit_gaussians(splat_ctx* ctx, const float* points, const float* col
     return SPLAT_OK;
 }
 
+// The twin context of multi-view calls (own stream and buffers; created on first use), ordered
+// after everything queued on `s` so far.
+static int twin_begin(splat_ctx* ctx, cudaStream_t s) {
+    int rc;
+    if (!ctx->twin) {
+        splat_ctx* tw = nullptr;
+        if ((rc = splat_ctx_create(ctx->device, &tw))) return set_err(ctx, rc, "twin context");
+        ctx->twin = tw;
+        CK(cudaStreamCreateWithFlags(&tw->own_stream, cudaStreamNonBlocking), "twin stream");
+        tw->stream = tw->lc.stream = tw->own_stream;
+    }
+    splat_ctx* tw = ctx->twin;
+    tw->lc.prof = ctx->lc.prof;  // one per-kernel profile for both
+    CK(cudaEventRecord(ctx->ev_step, s), "record step");
+    CK(cudaStreamWaitEvent(tw->stream, ctx->ev_step, 0), "twin start");
+    return SPLAT_OK;
+}
+
 int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param_grads* grads,
                      const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
                      uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
@@ -2021,19 +2043,9 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
     // view's latency-bound preprocess / sort / binning overlaps the other's blend kernels; the
     // chains accumulate into the shared gradients one after the other (chain_wait events)
     const bool overlap = n_views > 1 && ctx->view_overlap;
-    if (overlap && !ctx->twin) {
-        splat_ctx* tw = nullptr;
-        if ((rc = splat_ctx_create(ctx->device, &tw))) return set_err(ctx, rc, "train_step: twin context");
-        ctx->twin = tw;
-        CK(cudaStreamCreateWithFlags(&tw->own_stream, cudaStreamNonBlocking), "twin stream");
-        tw->stream = tw->lc.stream = tw->own_stream;
-    }
     if (overlap) {
-        splat_ctx* tw = ctx->twin;
-        tw->lc.prof = ctx->lc.prof;  // one per-kernel profile for both
-        CK(cudaEventRecord(ctx->ev_step, s), "record step");
-        CK(cudaStreamWaitEvent(tw->stream, ctx->ev_step, 0), "twin start");
-        ctx->twin_member = tw->twin_member = true;
+        if ((rc = twin_begin(ctx, s))) return rc;
+        ctx->twin_member = ctx->twin->twin_member = true;
     }
     // the hook captures this frame's locals by reference: it must never outlive the call
     struct HookGuard {
@@ -2168,6 +2180,94 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
         if (*flag != seq) CK(cudaStreamSynchronize(ls), "sync");
         std::memcpy(loss_host, ctx->host_loss, (size_t)n_views * 4);
     }
+    return SPLAT_OK;
+}
+
+
+// ---- multi-view passes (BASELINE configs 2 and 3) -----------------------------------------------
+// Views alternate between the context and its twin (own stream and buffers), so one view's
+// latency-bound preprocess / sort / binning overlaps the other's forward; the per-view updates
+// (visibility accumulation, point appends) are chained by events in view order, so the results
+// equal the sequential loop's.
+
+int splat_visibility_pass(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cams, int32_t n_views,
+                          const splat_raster_config* cfg, float threshold, uint32_t* masks, int64_t mask_words,
+                          double* accum, int64_t* counts, float* max_all) {
+    if (!ctx || !g || n_views < 0 || (n_views > 0 && !cams)) return SPLAT_ERR_INVALID_ARGUMENT;
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    const int64_t n = g->n;
+    if (mask_words < (n + 31) / 32 || (n > 0 && (!accum || !counts || (n_views > 0 && !masks))))
+        return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "visibility_pass: outputs missing or too small");
+    cudaStream_t s = ctx->stream;
+    const bool overlap = n_views > 1 && ctx->view_overlap;
+    if (overlap && (rc = twin_begin(ctx, s))) return rc;
+    const float zero[3] = {0, 0, 0};
+    splat_ctx* prev = nullptr;
+    for (int k = 0; k < n_views; ++k) {
+        splat_ctx* c = overlap && (k & 1) ? ctx->twin : ctx;
+        CK(c->pass_rep.ensure((size_t)(n > 0 ? n : 1) * 12), "alloc report");
+        float* base = c->pass_rep.as<float>();
+        const splat_importance_outputs rep{base, base + n, reinterpret_cast<int32_t*>(base + 2 * n)};
+        if ((rc = run_forward(c, g, &cams[k], cfg, nullptr, zero, nullptr, &rep))) {
+            if (c != ctx) ctx->err = c->err;
+            return rc;
+        }
+        if (prev && prev != c) CK(cudaStreamWaitEvent(c->stream, prev->ev_pass, 0), "view order");
+        CK(launch_visibility_update(c->lc, rep.importance, rep.max_weight, rep.max_pixel_count, (int32_t)n, threshold,
+                                    masks + (size_t)k * mask_words, accum, counts, max_all),
+           "visibility update");
+        CK(cudaEventRecord(c->ev_pass, c->stream), "record update");
+        prev = c;
+    }
+    if (prev && prev != ctx) CK(cudaStreamWaitEvent(s, prev->ev_pass, 0), "join twin");
+    return SPLAT_OK;
+}
+
+int splat_depth_points(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cams, int32_t n_views,
+                       const splat_raster_config* cfg, int rule, float alpha_threshold, int64_t first_view,
+                       int32_t stride, int64_t seed, float* points, int32_t* views, int32_t* pixels,
+                       int64_t capacity, int32_t* count_dev) {
+    if (!ctx || !g || n_views < 0 || (n_views > 0 && !cams) || !count_dev) return SPLAT_ERR_INVALID_ARGUMENT;
+    if (stride < 1) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "depth_points: stride < 1");
+    if (capacity > 0 && (!points || !pixels)) return set_err(ctx, SPLAT_ERR_INVALID_ARGUMENT, "depth_points: outputs missing");
+    int rc = check_set(ctx, g);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(count_dev, 0, 4, s), "zero count");
+    const bool overlap = n_views > 1 && ctx->view_overlap;
+    if (overlap && (rc = twin_begin(ctx, s))) return rc;
+    const float zero[3] = {0, 0, 0};
+    splat_ctx* prev = nullptr;
+    for (int k = 0; k < n_views; ++k) {
+        splat_ctx* c = overlap && (k & 1) ? ctx->twin : ctx;
+        if ((rc = validate_camera(c, &cams[k]))) {
+            if (c != ctx) ctx->err = c->err;
+            return rc;
+        }
+        const size_t hw = (size_t)cams[k].width * cams[k].height;
+        CK(c->pass_img.ensure(hw * 12), "alloc images");
+        float* img = c->pass_img.as<float>();
+        splat_render_outputs outs{};
+        outs.depth = img;
+        outs.alpha = img + hw;
+        outs.max_contributor = reinterpret_cast<int32_t*>(img + 2 * hw);
+        if ((rc = run_forward(c, g, &cams[k], cfg, nullptr, zero, &outs, nullptr))) {
+            if (c != ctx) ctx->err = c->err;
+            return rc;
+        }
+        CK(c->flags.ensure(hw * 4), "alloc flags");
+        CK(c->flag_offsets.ensure(hw * 4), "alloc offsets");
+        CK(c->scan_tmp.ensure((scan_temp_words(hw) + 64) * 4), "alloc scan");
+        if (prev && prev != c) CK(cudaStreamWaitEvent(c->stream, prev->ev_pass, 0), "view order");
+        CK(launch_unproject(c->lc, c->st.cp, outs.max_contributor, outs.alpha, outs.depth, rule, alpha_threshold,
+                            first_view + k, stride, seed, points, pixels, capacity, count_dev, c->flags.as<uint32_t>(),
+                            c->flag_offsets.as<uint32_t>(), c->scan_tmp.as<uint32_t>(), true, views),
+           "unproject");
+        CK(cudaEventRecord(c->ev_pass, c->stream), "record unproject");
+        prev = c;
+    }
+    if (prev && prev != ctx) CK(cudaStreamWaitEvent(s, prev->ev_pass, 0), "join twin");
     return SPLAT_OK;
 }
 

@@ -809,13 +809,17 @@ __global__ void unproject_flags_kernel(int width, int height, const int32_t* __r
     flags[pix] = (valid && m == 0) ? 1u : 0u;
 }
 
+// append: the view's points go after the *count points already written (the multi-view pass),
+// and view_out (nullable) gets the view index of each point.
 __global__ void unproject_write_kernel(CamParams cp, const uint32_t* __restrict__ flags,
                                        const uint32_t* __restrict__ offsets, const float* __restrict__ depth,
-                                       float* __restrict__ points, int32_t* __restrict__ pixel, int64_t capacity) {
+                                       float* __restrict__ points, int32_t* __restrict__ pixel, int64_t capacity,
+                                       const int32_t* __restrict__ base, int32_t* __restrict__ view_out,
+                                       int32_t view_index) {
     const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t hw = (int64_t)cp.width * cp.height;
     if (pix >= hw || !flags[pix]) return;
-    const int64_t o = offsets[pix];
+    const int64_t o = offsets[pix] + (base ? (int64_t)*base : 0);
     if (o >= capacity) return;
     const int px = (int)(pix % cp.width), py = (int)(pix / cp.width);
     float d0 = ((float)px + 0.5f - cp.cx) / cp.fx;
@@ -834,11 +838,12 @@ __global__ void unproject_write_kernel(CamParams cp, const uint32_t* __restrict_
     points[3 * o + 1] = cp.center[1] + d * w1;
     points[3 * o + 2] = cp.center[2] + d * w2;
     pixel[o] = (int32_t)pix;
+    if (view_out) view_out[o] = view_index;
 }
 
 __global__ void count_from_scan_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ flags,
-                                       int64_t hw, int32_t* __restrict__ count) {
-    *count = (int32_t)(offsets[hw - 1] + flags[hw - 1]);
+                                       int64_t hw, int32_t* __restrict__ count, bool append) {
+    *count = (append ? *count : 0) + (int32_t)(offsets[hw - 1] + flags[hw - 1]);
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -920,7 +925,8 @@ cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint3
 cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* max_contributor, const float* alpha,
                              const float* depth, int rule, float alpha_threshold, int64_t view_index, int32_t stride,
                              int64_t seed, float* points, int32_t* pixel, int64_t capacity, int32_t* count_dev,
-                             uint32_t* flags, uint32_t* offsets, uint32_t* scan_tmp) {
+                             uint32_t* flags, uint32_t* offsets, uint32_t* scan_tmp, bool append,
+                             int32_t* view_out) {
     const int64_t hw = (int64_t)cp.width * cp.height;
     {
         LaunchScope ls_(lc, "unproject_flags");
@@ -934,11 +940,12 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
     {
         LaunchScope ls_(lc, "unproject_write");
         unproject_write_kernel<<<blocks_for(hw, 256), 256, 0, lc.stream>>>(cp, flags, offsets, depth, points, pixel,
-                                                                       capacity);
+                                                                       capacity, append ? count_dev : nullptr,
+                                                                       view_out, (int32_t)view_index);
     }
     {
         LaunchScope ls_(lc, "count_from_scan");
-        count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev);
+        count_from_scan_kernel<<<1, 1, 0, lc.stream>>>(offsets, flags, hw, count_dev, append);
     }
     lc.count += 2;
     return cudaGetLastError();

@@ -201,7 +201,8 @@ cudaError_t launch_unproject(LaunchCtx& lc, const CamParams& cp, const int32_t* 
                              const float* alpha, const float* depth, int rule, float alpha_threshold,
                              int64_t view_index, int32_t stride, int64_t seed, float* points,
                              int32_t* pixel, int64_t capacity, int32_t* count_dev, uint32_t* flags,
-                             uint32_t* offsets, uint32_t* scan_tmp);
+                             uint32_t* offsets, uint32_t* scan_tmp, bool append = false,
+                             int32_t* view_out = nullptr);
 
 // ---- importance.cu ------------------------------------------------------------------------
 cudaError_t launch_visibility_update(LaunchCtx& lc, const float* importance, const float* max_weight,

@@ -67,11 +67,12 @@ def _gather_rows(local, n_views: int, world: int, pg=None):
     return torch.cat(rows, 0)
 
 
-def importance_views(view_fn: Callable, n_views: int, n: int, device, pg=None):
+def importance_views(view_fn: Callable, n_views: int, n: int, device, pg=None, block_fn: Optional[Callable] = None):
     """Config-3 pass.  view_fn(k, mask_row, accum, counts, max_all) adds view k's importance into
     the running fp64 accum / int64 counts / fp32 max_all (in place) and writes its bitmask words
-    into mask_row.  Returns (masks [n_views, ceil(n/32)] int32, accum f64 [n], counts i64 [n],
-    max_all f32 [n]) on every rank."""
+    into mask_row; or block_fn(block, masks, accum, counts, max_all) does the rank's whole block of
+    views at once (the native pass).  Returns (masks [n_views, ceil(n/32)] int32, accum f64 [n],
+    counts i64 [n], max_all f32 [n]) on every rank."""
     torch = _torch_any()
     rank, world = rank_world(pg)
     block = view_block(n_views, rank, world)
@@ -80,8 +81,11 @@ def importance_views(view_fn: Callable, n_views: int, n: int, device, pg=None):
     accum = torch.zeros(max(n, 1), dtype=torch.float64, device=device)
     counts = torch.zeros(max(n, 1), dtype=torch.int64, device=device)
     max_all = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
-    for j, k in enumerate(block):
-        view_fn(k, masks[j], accum, counts, max_all)
+    if block_fn is not None:
+        block_fn(block, masks, accum, counts, max_all)
+    else:
+        for j, k in enumerate(block):
+            view_fn(k, masks[j], accum, counts, max_all)
     d = _dist()
     if d is not None and world > 1:
         d.all_reduce(accum, op=d.ReduceOp.SUM, group=pg)
@@ -91,21 +95,26 @@ def importance_views(view_fn: Callable, n_views: int, n: int, device, pg=None):
     return masks, accum[:n], counts[:n], max_all[:n]
 
 
-def points_views(view_fn: Callable, n_views: int, device, pg=None):
-    """Config-2 pass.  view_fn(k) returns (points [m, 3] f32, pixels [m] i32) of view k.  Returns
-    (points [M, 3], views [M] i32, pixels [M] i32) in view order on every rank."""
+def points_views(view_fn: Callable, n_views: int, device, pg=None, block_fn: Optional[Callable] = None):
+    """Config-2 pass.  view_fn(k) returns (points [m, 3] f32, pixels [m] i32) of view k; or
+    block_fn(block) returns (points, views, pixels) of the rank's whole block of views in view order
+    (the native pass).  Returns (points [M, 3], views [M] i32, pixels [M] i32) in view order on every
+    rank."""
     torch = _torch_any()
     rank, world = rank_world(pg)
-    pts, pix, vws = [], [], []
-    for k in view_block(n_views, rank, world):
-        p, x = view_fn(k)
-        pts.append(p)
-        pix.append(x)
-        vws.append(torch.full((x.shape[0],), k, dtype=torch.int32, device=device))
-    cat = lambda xs, shape, dt: torch.cat(xs) if xs else torch.zeros(shape, dtype=dt, device=device)  # noqa: E731
-    pts = cat(pts, (0, 3), torch.float32)
-    pix = cat(pix, (0,), torch.int32)
-    vws = cat(vws, (0,), torch.int32)
+    if block_fn is not None:
+        pts, vws, pix = block_fn(view_block(n_views, rank, world))
+    else:
+        pts, pix, vws = [], [], []
+        for k in view_block(n_views, rank, world):
+            p, x = view_fn(k)
+            pts.append(p)
+            pix.append(x)
+            vws.append(torch.full((x.shape[0],), k, dtype=torch.int32, device=device))
+        cat = lambda xs, shape, dt: torch.cat(xs) if xs else torch.zeros(shape, dtype=dt, device=device)  # noqa: E731
+        pts = cat(pts, (0, 3), torch.float32)
+        pix = cat(pix, (0,), torch.int32)
+        vws = cat(vws, (0,), torch.int32)
     d = _dist()
     if d is None or world == 1:
         return pts, vws, pix
@@ -127,9 +136,11 @@ def points_views(view_fn: Callable, n_views: int, device, pg=None):
 
 # ---- the CUDA per-view work ------------------------------------------------------------------
 def visibility_pass_views(set_, cams: Sequence[capi.Camera], cfg: Optional[RasterConfig] = None,
-                          threshold: float = 1e-3, ctx: Optional[Context] = None, pg=None):
+                          threshold: float = 1e-3, ctx: Optional[Context] = None, pg=None, per_view: bool = False):
     """Config 3 over `cams`, view-parallel across the ranks of `pg` (single process without one):
-    accumulate_importance + splat_visibility_update_max per local view, then the reductions above."""
+    the rank's views through splat_visibility_pass (accumulate_importance + visibility_update_max
+    per view, consecutive views overlapped on a twin context; per_view: one C-ABI call per view),
+    then the reductions above."""
     torch = _torch()
     ctx = ctx or Context.default()
     cfg = cfg or RasterConfig()
@@ -150,14 +161,24 @@ def visibility_pass_views(set_, cams: Sequence[capi.Camera], cfg: Optional[Raste
         ctx.check(ctx.lib.splat_visibility_update_max(ctx.h, C.byref(out), n, threshold, mask_row.data_ptr(),
                                                       accum.data_ptr(), counts.data_ptr(), max_all.data_ptr()))
 
-    return importance_views(view_fn, len(cams), n, dev, pg)
+    def block_fn(block, masks, accum, counts, max_all):  # the native pass over the block (twin overlap)
+        if len(block) == 0:
+            return
+        cam_arr = (capi.Camera * len(block))(*[cams[k] for k in block])
+        ctx.check(ctx.lib.splat_visibility_pass(ctx.h, C.byref(g), cam_arr, len(block), C.byref(cfg), threshold,
+                                                masks.data_ptr(), masks.shape[1], accum.data_ptr(), counts.data_ptr(),
+                                                max_all.data_ptr()))
+
+    return importance_views(view_fn, len(cams), n, dev, pg, block_fn=None if per_view else block_fn)
 
 
 def depth_points_views(set_, cams: Sequence[capi.Camera], cfg: Optional[RasterConfig] = None,
                        rule: int = capi.DEPTH_RULE_ALPHA, alpha_threshold: float = 0.5, stride: int = 4,
-                       seed: int = 0, ctx: Optional[Context] = None, pg=None):
-    """Config 2 over `cams`, view-parallel across the ranks of `pg`: render depth per local view,
-    unproject the selected pixels (rasterizer.unproject_depth), gather in view order."""
+                       seed: int = 0, ctx: Optional[Context] = None, pg=None, per_view: bool = False):
+    """Config 2 over `cams`, view-parallel across the ranks of `pg`: the rank's views through
+    splat_depth_points (depth render + unprojection per view, points appended in view order,
+    consecutive views overlapped on a twin context; per_view: render + rasterizer.unproject_depth per
+    view), gathered in view order."""
     ctx = ctx or Context.default()
     cfg = cfg or RasterConfig()
     ds, _ = _device_set(set_, ctx.device)
@@ -168,4 +189,25 @@ def depth_points_views(set_, cams: Sequence[capi.Camera], cfg: Optional[RasterCo
                                    stride=stride, seed=seed, ctx=ctx)
         return p.clone(), px.clone()
 
-    return points_views(view_fn, len(cams), f"cuda:{ctx.device}", pg)
+    def block_fn(block):  # the native pass over the block (twin overlap, points appended in view order)
+        torch = _torch()
+        dev = f"cuda:{ctx.device}"
+        if len(block) == 0:
+            return (torch.zeros((0, 3), dtype=torch.float32, device=dev),
+                    torch.zeros(0, dtype=torch.int32, device=dev), torch.zeros(0, dtype=torch.int32, device=dev))
+        cam_arr = (capi.Camera * len(block))(*[cams[k] for k in block])
+        cap = max(sum(cams[k].width * cams[k].height for k in block) // stride + len(block), 1)
+        pts = torch.empty((cap, 3), dtype=torch.float32, device=dev)
+        vws = torch.empty(cap, dtype=torch.int32, device=dev)
+        pix = torch.empty(cap, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        ctx.bind_stream()
+        ctx.check(ctx.lib.splat_depth_points(ctx.h, C.byref(ds.struct()), cam_arr, len(block), C.byref(cfg), rule,
+                                             alpha_threshold, block[0], stride, seed, pts.data_ptr(), vws.data_ptr(),
+                                             pix.data_ptr(), cap, cnt.data_ptr()))
+        m = int(cnt.item())
+        if m > cap:  # (cannot happen: at most one pixel in `stride` per view is selected)
+            raise RuntimeError(f"depth_points: {m} points exceed the capacity {cap}")
+        return pts[:m], vws[:m], pix[:m]
+
+    return points_views(view_fn, len(cams), f"cuda:{ctx.device}", pg, block_fn=None if per_view else block_fn)

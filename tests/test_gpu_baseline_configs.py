@@ -24,6 +24,7 @@ import pytest
 
 from helpers import assert_bitwise, assert_grads_close, rel_err
 from paper_2411_12788_b200 import capi, scenes
+from paper_2411_12788_b200 import multiview as MV
 from paper_2411_12788_b200 import rasterizer as R
 from paper_2411_12788_b200.capi import AdamConfig, RasterConfig
 
@@ -40,7 +41,10 @@ def _pmap(fn, items):
 def test_config2_full_size_unprojection(oracle):
     s = scenes.make_gaussians(3_000_000, seed=0, log_scale_mean=np.log(0.005))
     cams = [scenes.ring_camera(k, 64) for k in range(64)]
-    pts, views, pix = R.depth_points(s, cams, rule=capi.DEPTH_RULE_ALPHA, alpha_threshold=0.5, stride=4, seed=0)
+    # the native pass (splat_depth_points: views overlapped on the twin context, points appended in
+    # view order) — the bench's config-2 path
+    pts, views, pix = MV.depth_points_views(s, cams, rule=capi.DEPTH_RULE_ALPHA, alpha_threshold=0.5, stride=4,
+                                            seed=0)
     pts, views, pix = pts.cpu().numpy(), views.cpu().numpy(), pix.cpu().numpy()
 
     def view(k):
@@ -61,7 +65,8 @@ def test_config2_full_size_unprojection(oracle):
 def test_config3_full_size_visibility_importance_and_culled_step(oracle):
     s = scenes.make_gaussians(700_000, seed=0)
     cams = [scenes.ring_camera(k, 200) for k in range(200)]
-    masks, accum, counts = R.visibility_pass(s, cams, threshold=1e-3)
+    # the native pass (splat_visibility_pass) — the bench's config-3 path
+    masks, accum, counts, _ = MV.visibility_pass_views(s, cams, threshold=1e-3)
     masks = masks.cpu().numpy()
 
     def view(k):
