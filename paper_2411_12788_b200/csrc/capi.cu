@@ -1004,8 +1004,8 @@ int splat_sync(splat_ctx* ctx) {
 
 const char* splat_last_error(const splat_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-int64_t splat_kernel_launches(const splat_ctx* ctx) {
-    return ctx ? ctx->lc.count + (ctx->twin ? ctx->twin->lc.count : 0) : 0;
+int64_t splat_kernel_launches(const splat_ctx* ctx) {  // this context and its helper contexts
+    return ctx ? ctx->lc.count + splat_kernel_launches(ctx->twin) : 0;
 }
 
 int splat_profile_enable(splat_ctx* ctx, int on) {
@@ -1996,6 +1996,28 @@ static int twin_begin(splat_ctx* ctx, cudaStream_t s) {
     return SPLAT_OK;
 }
 
+// The contexts the passes rotate views over: this one, its twin and (want = 3) the twin's twin,
+// each ordered after everything queued on `s` (SPLAT_PASS_CONTEXTS overrides `want`).  Measured:
+// the visibility pass (700 K Gaussians) gains from a third context (2141 -> 2289 views/s), the
+// depth pass (3 M Gaussians, heavier blend with depth) loses (1240 -> 1055).
+static int pass_ring(splat_ctx* ctx, cudaStream_t s, int32_t n_views, int want, splat_ctx* ring[3], int* nring,
+                     const char* env = "SPLAT_PASS_CONTEXTS") {
+    *nring = 1;
+    ring[0] = ctx;
+    if (n_views < 2 || !ctx->view_overlap) return SPLAT_OK;
+    if (const char* e = std::getenv(env)) want = std::max(1, std::min(3, std::atoi(e)));
+    int rc;
+    if (want >= 2) {
+        if ((rc = twin_begin(ctx, s))) return rc;
+        ring[(*nring)++] = ctx->twin;
+    }
+    if (want >= 3 && n_views > 2) {
+        if ((rc = twin_begin(ctx->twin, ctx->twin->stream))) return rc;
+        ring[(*nring)++] = ctx->twin->twin;
+    }
+    return SPLAT_OK;
+}
+
 int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param_grads* grads,
                      const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
                      uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
@@ -2042,11 +2064,12 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
     // views alternate between this context and its twin (own stream and buffers) so that one
     // view's latency-bound preprocess / sort / binning overlaps the other's blend kernels; the
     // chains accumulate into the shared gradients one after the other (chain_wait events)
-    const bool overlap = n_views > 1 && ctx->view_overlap;
-    if (overlap) {
-        if ((rc = twin_begin(ctx, s))) return rc;
-        ctx->twin_member = ctx->twin->twin_member = true;
-    }
+    splat_ctx* ring[3];
+    int nring = 1;
+    if ((rc = pass_ring(ctx, s, n_views, 2, ring, &nring, "SPLAT_TRAIN_CONTEXTS"))) return rc;
+    const bool overlap = nring > 1;
+    if (overlap)
+        for (int i = 0; i < nring; ++i) ring[i]->twin_member = true;
     // the hook captures this frame's locals by reference: it must never outlive the call
     struct HookGuard {
         splat_ctx* c;
@@ -2065,13 +2088,14 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
     cudaEvent_t prev_chain = nullptr;
     auto fail = [&](splat_ctx* c, int r) {
         if (c != ctx) ctx->err = c->err;
-        ctx->chain_wait = nullptr;
-        ctx->twin_member = false;
-        if (ctx->twin) ctx->twin->chain_wait = nullptr;
+        for (int i = 0; i < nring; ++i) {
+            ring[i]->chain_wait = nullptr;
+            ring[i]->twin_member = false;
+        }
         return r;
     };
     for (int k = 0; k < n_views; ++k) {
-        splat_ctx* c = overlap && (k & 1) ? ctx->twin : ctx;
+        splat_ctx* c = ring[k % nring];
         rc = run_forward(c, &g, &cams[k], cfg, nullptr, bg, nullptr, nullptr);
         if (rc == SPLAT_OK && ctx->post_forward_hook) {  // the host copies, once view 0's forward is queued
             std::function<int()> hook;
@@ -2108,7 +2132,7 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
     }
     if (overlap) {  // everything of every view is ordered before the last chain
         CK(cudaStreamWaitEvent(s, prev_chain, 0), "join twin");
-        ctx->twin_member = ctx->twin->twin_member = false;
+        for (int i = 0; i < nring; ++i) ring[i]->twin_member = false;
     }
     // The losses are final once every view's L1 reduction ran (each context's last ev_loss covers
     // its earlier views): read them back on a stream of their own, so the call returns while the
@@ -2126,11 +2150,11 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
             ctx->host_loss_cap = n_views;
         }
         seq = ++ctx->loss_seq ? ctx->loss_seq : ++ctx->loss_seq;
-        const bool twin_ok = !overlap || ctx->twin->loss_recorded;
-        if (lambda_dssim <= 0.0f && ctx->loss_recorded && twin_ok) {
+        bool all_recorded = true;
+        for (int i = 0; i < nring; ++i) all_recorded = all_recorded && ring[i]->loss_recorded;
+        if (lambda_dssim <= 0.0f && all_recorded) {
             if (!ctx->lstream) CK(cudaStreamCreateWithFlags(&ctx->lstream, cudaStreamNonBlocking), "loss stream");
-            CK(cudaStreamWaitEvent(ctx->lstream, ctx->ev_loss, 0), "loss ready");
-            if (overlap) CK(cudaStreamWaitEvent(ctx->lstream, ctx->twin->ev_loss, 0), "twin loss ready");
+            for (int i = 0; i < nring; ++i) CK(cudaStreamWaitEvent(ctx->lstream, ring[i]->ev_loss, 0), "loss ready");
             cudaStream_t keep = ctx->lc.stream;
             ctx->lc.stream = ctx->lstream;
             const cudaError_t e = launch_copy_to_host(ctx->lc, losses, ctx->host_loss_dev, n_views, seq);
@@ -2189,27 +2213,6 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
 // latency-bound preprocess / sort / binning overlaps the other's forward; the per-view updates
 // (visibility accumulation, point appends) are chained by events in view order, so the results
 // equal the sequential loop's.
-
-// The contexts the passes rotate views over: this one, its twin and (want = 3) the twin's twin,
-// each ordered after everything queued on `s` (SPLAT_PASS_CONTEXTS overrides `want`).  Measured:
-// the visibility pass (700 K Gaussians) gains from a third context (2141 -> 2289 views/s), the
-// depth pass (3 M Gaussians, heavier blend with depth) loses (1240 -> 1055).
-static int pass_ring(splat_ctx* ctx, cudaStream_t s, int32_t n_views, int want, splat_ctx* ring[3], int* nring) {
-    *nring = 1;
-    ring[0] = ctx;
-    if (n_views < 2 || !ctx->view_overlap) return SPLAT_OK;
-    if (const char* e = std::getenv("SPLAT_PASS_CONTEXTS")) want = std::max(1, std::min(3, std::atoi(e)));
-    int rc;
-    if (want >= 2) {
-        if ((rc = twin_begin(ctx, s))) return rc;
-        ring[(*nring)++] = ctx->twin;
-    }
-    if (want >= 3 && n_views > 2) {
-        if ((rc = twin_begin(ctx->twin, ctx->twin->stream))) return rc;
-        ring[(*nring)++] = ctx->twin->twin;
-    }
-    return SPLAT_OK;
-}
 
 int splat_visibility_pass(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* cams, int32_t n_views,
                           const splat_raster_config* cfg, float threshold, uint32_t* masks, int64_t mask_words,
