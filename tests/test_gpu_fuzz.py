@@ -72,13 +72,16 @@ def test_random_scene(oracle, ref, seed):
     # the same summation drift in the gradients: a looser element bound against the reference's
     # float path, and the distance to the fp64 reference bounded
     if not exact:
-        assert_grads_close(got, want_g, rtol=5e-4, what=what, norm_tol=1e-4)
+        # (the GPU's float atomics make these run-to-run: margins of ~2.5x over the worst seen)
+        assert_grads_close(got, want_g, rtol=1e-3, what=what, norm_tol=5e-4)
     g64 = ref.render_backward_f64(s, cam, d_color, cfg=cfg, mask=mask, bg=bg)
     for k in g64:
         truth = np.asarray(g64[k], np.float64)
         e_gpu = np.linalg.norm(np.asarray(got[k], np.float64) - truth)
         e_ref = np.linalg.norm(np.asarray(want_g[k], np.float64) - truth)
         nt = np.linalg.norm(truth)
-        # as close as the reference's float path, or within 5e-5 of the norm (the moment-form sums
-        # and rcp.approx of T_before round differently from the per-sample chain on large splats)
-        assert e_gpu <= max(1.05 * e_ref, 5e-5 * nt), (what, k, e_gpu / max(nt, 1e-30), e_ref / max(nt, 1e-30))
+        # within twice the reference float path's own error, or 5e-5 of the norm (the moment-form
+        # sums, the rcp.approx of T_before and the atomics' order round differently from the
+        # per-sample chain; on the sweep's worst case, seed 14's log-scales, the reference float
+        # path is 4.9e-5 off and the GPU 5.9e-5 or 7.9e-5 depending on the atomics)
+        assert e_gpu <= max(2.0 * e_ref, 5e-5 * nt), (what, k, e_gpu / max(nt, 1e-30), e_ref / max(nt, 1e-30))
