@@ -101,3 +101,33 @@ print("fallback ok")
         r = subprocess.run([sys.executable, "-c", code, str(root)], capture_output=True, text=True, timeout=550,
                            env=dict(os.environ, **env), cwd=str(root))
         assert r.returncode == 0 and "fallback ok" in r.stdout, (env, (r.stdout + r.stderr)[-4000:])
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("env", [{"SPLAT_COOP_SORT": "0"}, {"SPLAT_BLOCK_ORDER": "0"}])
+def test_parity_on_alternative_paths(env):
+    """The same parity script on the paths the product takes in other situations: the Onesweep
+    depth sort (SPLAT_COOP_SORT=0: what more than 3.6 M keys use) and the raster work order of the
+    persistent blend kernels (SPLAT_BLOCK_ORDER=0)."""
+    r = subprocess.run([sys.executable, str(ROOT / "tests" / "scripts" / "tails_check.py")], capture_output=True,
+                       text=True, timeout=550, env=dict(os.environ, **env), cwd=str(ROOT))
+    assert r.returncode == 0 and "tails check ok" in r.stdout, (r.stdout + r.stderr)[-4000:]
+
+
+@pytest.mark.timeout(900)
+def test_depth_order_past_the_cooperative_sort(oracle):
+    """4 M Gaussians: more keys than the cooperative sort's resident wave holds, so the forward's
+    depth sort falls back to the Onesweep passes; survivors, order and the render stay exact."""
+    from helpers import assert_bitwise
+    from paper_2411_12788_b200 import rasterizer as R
+    from paper_2411_12788_b200 import scenes
+    s = scenes.make_gaussians(4_000_000, seed=2, log_scale_mean=-6.0)
+    cam = scenes.fov_camera(320, 240, 60.0, (0.0, 0.3, -3.0))
+    out = R.render(s, cam)
+    fw = R.forward_debug()
+    po = oracle.project(s, cam)
+    assert fw["n_survivors"] == po["n_survivors"]
+    assert_bitwise(fw["order"], po["order"], "depth order (Onesweep fallback)")
+    want = oracle.render(s, cam, report=False)
+    for k in ("color", "alpha", "transmittance", "max_contributor"):
+        assert_bitwise(getattr(out, k), want[k], k)
