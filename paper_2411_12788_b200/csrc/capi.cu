@@ -2018,6 +2018,14 @@ static int pass_ring(splat_ctx* ctx, cudaStream_t s, int32_t n_views, int want, 
     return SPLAT_OK;
 }
 
+// On an early return: whatever the helper contexts still have queued is ordered before anything
+// the caller queues next on `s` (they may still write the caller's outputs).
+static void join_ring(cudaStream_t s, splat_ctx* const ring[3], int nring) {
+    for (int i = 1; i < nring; ++i)
+        if (cudaEventRecord(ring[i]->ev_step, ring[i]->stream) == cudaSuccess)
+            cudaStreamWaitEvent(s, ring[i]->ev_step, 0);
+}
+
 int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_param_grads* grads,
                      const splat_adam_moments* moments, const splat_adam_config* adam, int32_t* step_count,
                      uint32_t group_mask, const splat_camera* cams, int32_t n_views, const float* const* targets,
@@ -2092,6 +2100,7 @@ int splat_train_step(splat_ctx* ctx, const splat_params_mut* p, const splat_para
             ring[i]->chain_wait = nullptr;
             ring[i]->twin_member = false;
         }
+        join_ring(s, ring, nring);
         return r;
     };
     for (int k = 0; k < n_views; ++k) {
@@ -2236,6 +2245,7 @@ int splat_visibility_pass(splat_ctx* ctx, const splat_gaussians* g, const splat_
         const splat_importance_outputs rep{base, base + n, reinterpret_cast<int32_t*>(base + 2 * n)};
         if ((rc = run_forward(c, g, &cams[k], cfg, nullptr, zero, nullptr, &rep))) {
             if (c != ctx) ctx->err = c->err;
+            join_ring(s, ring, nring);
             return rc;
         }
         if (prev && prev != c) CK(cudaStreamWaitEvent(c->stream, prev->ev_pass, 0), "view order");
@@ -2269,6 +2279,7 @@ int splat_depth_points(splat_ctx* ctx, const splat_gaussians* g, const splat_cam
         splat_ctx* c = ring[k % nring];
         if ((rc = validate_camera(c, &cams[k]))) {
             if (c != ctx) ctx->err = c->err;
+            join_ring(s, ring, nring);
             return rc;
         }
         const size_t hw = (size_t)cams[k].width * cams[k].height;
@@ -2280,6 +2291,7 @@ int splat_depth_points(splat_ctx* ctx, const splat_gaussians* g, const splat_cam
         outs.max_contributor = reinterpret_cast<int32_t*>(img + 2 * hw);
         if ((rc = run_forward(c, g, &cams[k], cfg, nullptr, zero, &outs, nullptr))) {
             if (c != ctx) ctx->err = c->err;
+            join_ring(s, ring, nring);
             return rc;
         }
         CK(c->flags.ensure(hw * 4), "alloc flags");
