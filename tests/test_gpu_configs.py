@@ -133,3 +133,26 @@ def test_view_parallel_passes_single_rank_match(oracle):
     p0, v0, x0 = R.depth_points(s, cams, stride=3, seed=1)
     for a, b, what in ((p, p0, "points"), (v, v0, "views"), (x, x0, "pixels")):
         assert_bitwise(a.cpu().numpy(), b.cpu().numpy(), f"view-parallel {what}")
+
+
+def test_native_passes_reject_a_bad_view_and_recover(oracle):
+    """A camera the validation rejects in the middle of a multi-view call: the call raises with the
+    reference's exception type, the helper contexts' queued work is joined, and the next call on
+    the same context returns the per-view loop's results."""
+    from paper_2411_12788_b200 import multiview as MV
+    s = scenes.make_gaussians(20_000, seed=9)
+    cams = [_ring(k, 4) for k in range(4)]
+    bad = list(cams)
+    bad[2] = scenes.fov_camera(0, 16, 60.0, (0.0, 0.0, -3.0))  # zero width
+    with pytest.raises(ValueError):  # std::invalid_argument
+        MV.depth_points_views(s, bad, stride=3, seed=1)
+    with pytest.raises(ValueError):
+        MV.visibility_pass_views(s, bad)
+    p, v, x = MV.depth_points_views(s, cams, stride=3, seed=1)
+    p0, v0, x0 = R.depth_points(s, cams, stride=3, seed=1)
+    for a, b, what in ((p, p0, "points"), (v, v0, "views"), (x, x0, "pixels")):
+        assert_bitwise(a.cpu().numpy(), b.cpu().numpy(), f"after an error: {what}")
+    masks, _, counts, _ = MV.visibility_pass_views(s, cams)
+    m0, _, c0 = R.visibility_pass(s, cams)
+    assert_bitwise(masks.cpu().numpy(), m0.cpu().numpy(), "after an error: masks")
+    assert_bitwise(counts.cpu().numpy(), c0.cpu().numpy(), "after an error: counts")
