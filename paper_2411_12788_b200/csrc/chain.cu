@@ -264,51 +264,47 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
     const int nco = (deg + 1) * (deg + 1);
     float basis[16];
     sh_basis_all(dir0, dir1, dir2, deg, basis);
-    float shv[48];
-    if (VEC) {
-        const float4* s4 = &s_sh[row * kShRow];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            const float4 vv = s4[k];
-            shv[4 * k] = vv.x; shv[4 * k + 1] = vv.y; shv[4 * k + 2] = vv.z; shv[4 * k + 3] = vv.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < 48; ++k) shv[k] = g.sh[i48 + k];
-    }
+    // SH coefficient j = 3 k + c, streamed from the staged shared-memory row a float4 at a time
+    // (conflict-free LDS.128 on the padded rows) in j order — the per-channel summation order of
+    // the reference — instead of 48 registers held across the SH section
+    const float4* s4 = VEC ? &s_sh[row * kShRow] : nullptr;
+    auto sh_quad = [&](int q) -> float4 {
+        if (VEC) return s4[q];
+        return make_float4(g.sh[i48 + 4 * q], g.sh[i48 + 4 * q + 1], g.sh[i48 + 4 * q + 2], g.sh[i48 + 4 * q + 3]);
+    };
     float rgb[3] = {0.5f, 0.5f, 0.5f};
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if (k < nco) {
-            rgb[0] = rgb[0] + basis[k] * shv[3 * k];
-            rgb[1] = rgb[1] + basis[k] * shv[3 * k + 1];
-            rgb[2] = rgb[2] + basis[k] * shv[3 * k + 2];
+    for (int q = 0; q < 12; ++q) {
+        const float4 v4 = sh_quad(q);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * q + e, k = j / 3, c = j % 3;
+            if (k < nco) rgb[c] = rgb[c] + basis[k] * vv[e];
         }
+    }
     float dc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) dc[c] = rgb[c] < 0.0f ? 0.0f : dcol[c];
-    float dsh[48];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const bool on = k < nco;
-        dsh[3 * k] = on ? basis[k] * dc[0] : 0.0f;
-        dsh[3 * k + 1] = on ? basis[k] * dc[1] : 0.0f;
-        dsh[3 * k + 2] = on ? basis[k] * dc[2] : 0.0f;
-    }
     if (deg > 0) {
         float gb[16][3];
         sh_basis_grad_all(dir0, dir1, dir2, deg, gb);
         float dd[3] = {0.0f, 0.0f, 0.0f};
+        float coef = 0.0f;
 #pragma unroll
-        for (int k = 1; k < 16; ++k) {
-            if (k < nco) {
-                float coef = 0.0f;
-                coef = coef + dc[0] * shv[3 * k];
-                coef = coef + dc[1] * shv[3 * k + 1];
-                coef = coef + dc[2] * shv[3 * k + 2];
-                dd[0] = dd[0] + gb[k][0] * coef;
-                dd[1] = dd[1] + gb[k][1] * coef;
-                dd[2] = dd[2] + gb[k][2] * coef;
+        for (int q = 0; q < 12; ++q) {
+            const float4 v4 = sh_quad(q);
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int j = 4 * q + e, k = j / 3, c = j % 3;
+                if (k < 1 || k >= nco) continue;
+                coef = (c == 0 ? 0.0f : coef) + dc[c] * vv[e];
+                if (c == 2) {
+                    dd[0] = dd[0] + gb[k][0] * coef;
+                    dd[1] = dd[1] + gb[k][1] * coef;
+                    dd[2] = dd[2] + gb[k][2] * coef;
+                }
             }
         }
         const float ddot = dot3(dir0, dir1, dir2, dd[0], dd[1], dd[2]);
@@ -330,12 +326,22 @@ __device__ __forceinline__ void chain_one(GaussianPtrs g, CamParams cp, float4* 
         out.d_rotations[i4 + k] = br + drot[k];
     }
     out.d_opacity_logits[i] = (accumulate ? out.d_opacity_logits[i] : 0.0f) + dlogit;
-    if (VEC) {  // the fresh gradient row; the caller writes (or adds) it coalesced
-        float4* d4 = &s_sh[row * kShRow];
+    // d_sh = basis_k * dc (zero past the active degree), after the SH row's last read
 #pragma unroll
-        for (int k = 0; k < 12; ++k) d4[k] = make_float4(dsh[4 * k], dsh[4 * k + 1], dsh[4 * k + 2], dsh[4 * k + 3]);
-    } else {
-        for (int k = 0; k < 48; ++k) out.d_sh[i48 + k] = (accumulate ? out.d_sh[i48 + k] : 0.0f) + dsh[k];
+    for (int q = 0; q < 12; ++q) {
+        float d[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * q + e, k = j / 3, c = j % 3;
+            d[e] = k < nco ? basis[k] * dc[c] : 0.0f;
+        }
+        if (VEC) {  // the fresh gradient row, over the staged SH row; the caller writes (or adds) it coalesced
+            s_sh[row * kShRow + q] = make_float4(d[0], d[1], d[2], d[3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                out.d_sh[i48 + 4 * q + e] = (accumulate ? out.d_sh[i48 + 4 * q + e] : 0.0f) + d[e];
+        }
     }
     if (out.grad2d_accum) out.grad2d_accum[i] = (accumulate ? out.grad2d_accum[i] : 0.0f) + gaccum;
     if (out.grad2d_count) out.grad2d_count[i] = (accumulate ? out.grad2d_count[i] : 0) + 1;
