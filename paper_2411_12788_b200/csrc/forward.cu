@@ -21,10 +21,33 @@ __device__ __forceinline__ float dot3(float a0, float a1, float a2, float b0, fl
     return a0 * b0 + (a1 * b1 + a2 * b2);  // Eigen 3.4 unrolled redux: x0 + (x1 + x2)
 }
 
-// sh_basis + sh_to_color (sh.hpp:27-51, 84-100)
-__device__ __forceinline__ void sh_color(const float* __restrict__ sh, float x, float y, float z, int degree,
-                                         float rgb[3]) {
+// sh_basis (sh.hpp:27-51)
+__device__ __forceinline__ void sh_basis16(float x, float y, float z, int degree, float b[16]);
+
+// sh_to_color (sh.hpp:84-100) with the 48 coefficients fetched a float4 at a time by quad(q)
+// (coefficient j = 3 k + c), accumulated in j order — per channel, the reference's k order.
+template <typename Quad>
+__device__ __forceinline__ void sh_color_stream(Quad quad, float x, float y, float z, int degree, float rgb[3]) {
     float b[16];
+    sh_basis16(x, y, z, degree, b);
+    rgb[0] = rgb[1] = rgb[2] = 0.5f;
+    const int n = (degree + 1) * (degree + 1);
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const float4 v4 = quad(q);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * q + e, k = j / 3, c = j % 3;
+            if (k < n) rgb[c] = rgb[c] + b[k] * vv[e];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (rgb[c] < 0.0f) rgb[c] = 0.0f;
+}
+
+__device__ __forceinline__ void sh_basis16(float x, float y, float z, int degree, float b[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) b[i] = 0.0f;
     b[0] = (float)(0.28209479177387814);
@@ -51,19 +74,6 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, float x, 
         b[14] = (float)(1.445305721320277) * z * (xx - yy);
         b[15] = (float)(-0.5900435899266435) * x * (xx - 3.0f * yy);
     }
-    rgb[0] = rgb[1] = rgb[2] = 0.5f;
-    const int n = (degree + 1) * (degree + 1);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        if (k < n) {
-            rgb[0] = rgb[0] + b[k] * sh[k * 3 + 0];
-            rgb[1] = rgb[1] + b[k] * sh[k * 3 + 1];
-            rgb[2] = rgb[2] + b[k] * sh[k * 3 + 2];
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        if (rgb[c] < 0.0f) rgb[c] = 0.0f;
 }
 
 __device__ __forceinline__ float std_max(float a, float b) { return (a < b) ? b : a; }
@@ -291,19 +301,15 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(GaussianPtrs g,
     }
     if (want_rgb && alive) {  // sh_to_color (rasterizer.cpp:75)
         float rgb[3];
-        float shv[48];
-        if (VEC_SH) {
-            const float4* s4 = &s_sh[threadIdx.x * kShRow];
-#pragma unroll
-            for (int k = 0; k < 12; ++k) {
-                const float4 v = s4[k];
-                shv[4 * k] = v.x; shv[4 * k + 1] = v.y; shv[4 * k + 2] = v.z; shv[4 * k + 3] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 48; ++k) shv[k] = __ldg(&g.sh[48 * (size_t)i + k]);
-        }
-        sh_color(shv, u0, u1, u2, g.sh_degree, rgb);
+        const float4* s4 = &s_sh[threadIdx.x * kShRow];
+        const float* shg = g.sh + 48 * (size_t)i;
+        sh_color_stream(
+            [&](int q) -> float4 {
+                if (VEC_SH) return s4[q];
+                return make_float4(__ldg(shg + 4 * q), __ldg(shg + 4 * q + 1), __ldg(shg + 4 * q + 2),
+                                   __ldg(shg + 4 * q + 3));
+            },
+            u0, u1, u2, g.sh_degree, rgb);
         r.r2.x = rgb[0];
         r.r2.y = rgb[1];
         r.r2.z = rgb[2];
