@@ -1,3 +1,5 @@
+"""Host-side cost of one ViewTrainer.step_host call on the B200 box: the end-to-end step time and
+the Python wrapper alone (the C-ABI call stubbed), config 1."""
 import time, sys
 sys.path.insert(0, '.')
 import torch, numpy as np
