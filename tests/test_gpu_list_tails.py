@@ -131,3 +131,17 @@ def test_depth_order_past_the_cooperative_sort(oracle):
     want = oracle.render(s, cam, report=False)
     for k in ("color", "alpha", "transmittance", "max_contributor"):
         assert_bitwise(getattr(out, k), want[k], k)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("env", [{"SPLAT_TRAIN_CONTEXTS": "3", "SPLAT_PASS_CONTEXTS": "3"},
+                                 {"SPLAT_TRAIN_CONTEXTS": "1", "SPLAT_PASS_CONTEXTS": "1"}])
+def test_multi_view_calls_with_other_context_counts(env):
+    """The multi-view step and passes with three contexts (and with one: no overlap) against the
+    oracle / the per-view loops: tests/test_gpu_configs.py's config-4 step and native-pass tests
+    in a process with the context counts set."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        str(ROOT / "tests" / "test_gpu_configs.py"), "-k",
+                        "config4_batched or view_parallel or bad_view"],
+                       capture_output=True, text=True, timeout=850, env=dict(os.environ, **env), cwd=str(ROOT))
+    assert r.returncode == 0 and " passed" in r.stdout, (r.stdout + r.stderr)[-4000:]
