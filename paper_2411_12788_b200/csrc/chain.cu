@@ -373,24 +373,35 @@ __device__ __forceinline__ void zero_span_warp(float* p, int count, int lane) {
 // coalesced stores.  Pass 2 runs the chain on the list with every lane busy; each thread stages
 // its own 192-byte SH row in shared memory with float4 loads and writes its gradient row back
 // the same way.
+constexpr int kCompactItems = 4;  // Gaussians per thread in chain_compact (four commit-count loads in flight)
+
 __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __restrict__ grad2d, int n,
                                                             splat_param_grads out, int zero_untouched,
                                                             uint32_t* __restrict__ list, uint32_t* __restrict__ count,
                                                             uint32_t* __restrict__ count_next) {
     // one list append (atomic) per CTA: a single counter takes ~1 ns per atomic, so per-warp
-    // appends would serialise ~n/32 of them
-    __shared__ uint32_t s_wc[8];
+    // appends would serialise ~n/32 of them.  The CTA's 1024 rows are listed in index order.
+    __shared__ uint32_t s_wc[kCompactItems * 8];
     __shared__ uint32_t s_base;
     pdl_trigger();  // chain_touched (PDL) may be scheduled
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool touched = i < n && grad2d[kG2Stride * (size_t)i + 2].w > 0.0f;
-    const unsigned m = __ballot_sync(0xffffffffu, touched);
-    if (lane == 0) s_wc[warp] = __popc(m);
+    const int base = blockIdx.x * (256 * kCompactItems);
+    bool touched[kCompactItems];
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        const int i = base + k * 256 + threadIdx.x;
+        touched[k] = i < n && grad2d[kG2Stride * (size_t)i + 2].w > 0.0f;
+    }
+    unsigned m[kCompactItems];
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        m[k] = __ballot_sync(0xffffffffu, touched[k]);
+        if (lane == 0) s_wc[k * 8 + warp] = __popc(m[k]);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t tot = 0;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kCompactItems * 8; ++w) {
             const uint32_t c = s_wc[w];
             s_wc[w] = tot;
             tot += c;
@@ -401,21 +412,27 @@ __global__ void __launch_bounds__(256) chain_compact_kernel(const float4* __rest
         if (blockIdx.x == 0) *count_next = 0u;
     }
     __syncthreads();
-    if (touched) list[s_base + s_wc[warp] + __popc(m & lanemask_lt())] = (uint32_t)i;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k)
+        if (touched[k]) list[s_base + s_wc[k * 8 + warp] + __popc(m[k] & lt)] = (uint32_t)(base + k * 256 + threadIdx.x);
     if (!zero_untouched) return;  // accumulating, or the rows are already zero
-    // Every gradient of the warp's 32 Gaussians is zeroed here (touched ones are overwritten by
-    // pass 2): each array's span for the warp is contiguous, so the warp writes it with float4
+    // Every gradient of the warp's rows is zeroed here (touched ones are overwritten by pass 2):
+    // each array's span for the warp's 32 rows is contiguous, so the warp writes it with float4
     // stores (full sectors only).
-    const int w0 = i - lane;
-    const int rows = min(32, n - w0);
-    if (rows <= 0) return;
-    zero_span_warp(out.d_centers + 3 * (size_t)w0, 3 * rows, lane);
-    zero_span_warp(out.d_log_scales + 3 * (size_t)w0, 3 * rows, lane);
-    zero_span_warp(out.d_rotations + 4 * (size_t)w0, 4 * rows, lane);
-    zero_span_warp(out.d_opacity_logits + (size_t)w0, rows, lane);
-    zero_span_warp(out.d_sh + 48 * (size_t)w0, 48 * rows, lane);
-    if (out.grad2d_accum) zero_span_warp(out.grad2d_accum + (size_t)w0, rows, lane);
-    if (out.grad2d_count && lane < rows) out.grad2d_count[w0 + lane] = 0;
+#pragma unroll 1
+    for (int k = 0; k < kCompactItems; ++k) {
+        const int w0 = base + k * 256 + warp * 32;
+        const int rows = min(32, n - w0);
+        if (rows <= 0) return;
+        zero_span_warp(out.d_centers + 3 * (size_t)w0, 3 * rows, lane);
+        zero_span_warp(out.d_log_scales + 3 * (size_t)w0, 3 * rows, lane);
+        zero_span_warp(out.d_rotations + 4 * (size_t)w0, 4 * rows, lane);
+        zero_span_warp(out.d_opacity_logits + (size_t)w0, rows, lane);
+        zero_span_warp(out.d_sh + 48 * (size_t)w0, 48 * rows, lane);
+        if (out.grad2d_accum) zero_span_warp(out.grad2d_accum + (size_t)w0, rows, lane);
+        if (out.grad2d_count && lane < rows) out.grad2d_count[w0 + lane] = 0;
+    }
 }
 
 __global__ void __launch_bounds__(kChainThreads) chain_touched_kernel(GaussianPtrs g, CamParams cp,
@@ -472,7 +489,7 @@ cudaError_t launch_chain(LaunchCtx& lc, const GaussianPtrs& g, const CamParams& 
     lc.chain_parity ^= 1;
     {
         LaunchScope ls(lc, "chain_compact");
-        chain_compact_kernel<<<blocks_for(g.n, 256), 256, 0, lc.stream>>>(g2, g.n, out, !accumulate && !prezeroed,
+        chain_compact_kernel<<<blocks_for(g.n, 256 * kCompactItems), 256, 0, lc.stream>>>(g2, g.n, out, !accumulate && !prezeroed,
                                                                           list, count, count_next);
         lc.count++;
     }
