@@ -25,29 +25,32 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// Transpose reduction of 24 per-lane values (two entries x four groups of 3) across the warp in
-// 27 shuffles (a butterfly would take 120): the first three levels exchange the half a lane does
-// not keep, the last two reduce the 3 remaining values.  On
-// return lanes 4g (g = 0..7) hold the warp totals of values 3g .. 3g+2 in out[0..2].
-__device__ __forceinline__ void warp_reduce24(const float v[24], int lane, float out[3]) {
+// Transpose reduction of 18 per-lane values (two entries x three groups of 3) across the warp
+// in 24 shuffles (a butterfly would take 90).  Level 16: lanes keep their entry (bit 16 clear:
+// a), send the other.  Level 8: lanes with bit 8 clear keep groups 0-1 and send group 2, their
+// partners keep group 2 (6 shuffles: one direction carries 6 values, the other 3).  Level 4: the
+// group-0/1 lanes split them, the group-2 lanes reduce theirs; levels 2 and 1 reduce the quad.  On
+// return lanes 4q hold, in out[0..2], the warp totals of entry (lane >> 4), group
+// (lane & 8 ? 2 : (lane >> 2) & 1) (lanes 12 and 28 duplicate 8 and 24).
+__device__ __forceinline__ void warp_reduce18(const float v[18], int lane, float out[3]) {
     const bool a = lane & 16, b = lane & 8, c = lane & 4;
-    float u[12], w[6];
+    float u[9], w[6];
 #pragma unroll
-    for (int i = 0; i < 12; ++i) {
-        const float send = a ? v[i] : v[12 + i];
-        const float keep = a ? v[12 + i] : v[i];
+    for (int i = 0; i < 9; ++i) {
+        const float send = a ? v[i] : v[9 + i];
+        const float keep = a ? v[9 + i] : v[i];
         u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
-        const float send = b ? u[i] : u[6 + i];
-        const float keep = b ? u[6 + i] : u[i];
+        const float send = b ? u[i] : u[6 + i % 3];
+        const float keep = b ? u[6 + i % 3] : u[i];
         w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float send = c ? w[i] : w[3 + i];
-        const float keep = c ? w[3 + i] : w[i];
+        const float send = (b || c) ? w[i] : w[3 + i];
+        const float keep = (!b && c) ? w[3 + i] : w[i];
         out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
 #pragma unroll
@@ -67,7 +70,7 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
 // Gaussian by the chain (chain.cu), after the sums over all pixels:
 //   d mean.x = -o (c0 Sx + c1 Sy), d mean.y = -o (c2 Sy + c1 Sx), d conic = -o/2 (Sxx, Sxy, Syy),
 // which is sum(dpower * (-(c0 dx + c1 dy))), ... of the reference with dpower = o s.  vv[6..8] get
-// the colour gradient w dL, vv[9] counts the commit.  T_before = T_after / (1 - alpha).  The pixel
+// the colour gradient w dL (commits are counted by the caller's ballots).  T_before = T_after / (1 - alpha).  The pixel
 // carries B = dL . b, b the colour behind the sample (b = alpha c + (1 - alpha) b is linear in b),
 // instead of three channels.  Branch-free: the kernels call it for every lane, and a sample the
 // pixel does not commit (p false) contributes exactly nothing (alpha = G = 0: T unchanged, w = 0,
@@ -95,25 +98,25 @@ __device__ __forceinline__ void commit_sample(bool p, float* vv, float& T, float
     vv[3] += sx * dx;
     vv[4] += sx * dy;
     vv[5] += sy * dy;
-    vv[9] += p ? 1.0f : 0.0f;
     B = B + a * diff;
     T = t_before;
 }
 
-// Warp-reduce the 24 values of staged entries ja (v[0..11]) and jb (v[12..23]) and add them to
-// the per-Gaussian accumulator (common.cuh kG2Stride records): lanes 4g hold group g's totals;
-// groups 0-2 are added as they are (moments, colour), the commit count (group 3) rides in the
-// 4th slot of group 2's record.
-__device__ __forceinline__ void emit_entry_grads(const float v[24], int lane, bool any_a, bool any_b, uint32_t ja,
+// Warp-reduce the 18 values of staged entries ja (v[0..8]) and jb (v[9..17]) and add them to
+// the per-Gaussian accumulator (common.cuh kG2Stride records): groups 0-2 (moments, colour) as
+// they are, the commit counts (popcounts of the callers' commit ballots) in the 4th slot of
+// group 2's record.
+__device__ __forceinline__ void emit_entry_grads(const float v[18], int lane, int cnt_a, int cnt_b, uint32_t ja,
                                                  uint32_t jb, uint32_t a_gid, float4* __restrict__ grad2d) {
     float r[3];
-    warp_reduce24(v, lane, r);
-    const int grp = lane >> 2;  // 0-3: entry a, float4 grp; 4-7: entry b, float4 grp - 4
-    const float cnt = __shfl_down_sync(0xffffffffu, r[0], 4);
-    const bool mine = (lane & 3) == 0 && (grp & 3) < 3 && (grp < 4 ? any_a : any_b);
+    warp_reduce18(v, lane, r);
+    const bool eb = lane & 16;
+    const int grp = (lane & 8) ? 2 : (lane >> 2) & 1;
+    const int cnt = eb ? cnt_b : cnt_a;
+    const bool mine = (lane & 3) == 0 && (lane & 12) != 12 && cnt > 0;
     if (mine) {
-        const uint32_t gid = lds_u32(a_gid + 4u * (grp < 4 ? ja : jb));
-        red_add_v4(grad2d + kG2Stride * (size_t)gid + (grp & 3), r[0], r[1], r[2], (grp & 3) == 2 ? cnt : 0.0f);
+        const uint32_t gid = lds_u32(a_gid + 4u * (eb ? jb : ja));
+        red_add_v4(grad2d + kG2Stride * (size_t)gid + grp, r[0], r[1], r[2], grp == 2 ? (float)cnt : 0.0f);
     }
 }
 
@@ -221,7 +224,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
         const int cnt = pipe.stage(b, true, bx0, bx1, by0, by1, sm);
         // Two staged entries per iteration: their gates are independent instruction streams (the
         // branch-free gate), the per-pixel recursion then commits them in list order (j first: the
-        // batch is staged back to front), and one 24-value transpose reduction serves both.
+        // batch is staged back to front), and one 18-value transpose reduction serves both.
         for (int j = 0; j < cnt; j += 2) {
             const bool has_b = j + 1 < cnt;
             const uint32_t jb = has_b ? (uint32_t)(j + 1) : (uint32_t)j;
@@ -243,12 +246,13 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
             gb = gb && wb && idx_b <= my_last;
             // v: (dmean.x, dmean.y, dconic00 | dconic01, dconic11, dopacity | dcolour rgb | commits)
             // for entry a in v[0..11], entry b in v[12..23]
-            float v[24];
+            float v[18];
 #pragma unroll
-            for (int k = 0; k < 24; ++k) v[k] = 0.0f;
+            for (int k = 0; k < 18; ++k) v[k] = 0.0f;
             commit_sample(ga, v, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
-            commit_sample(gb, v + 12, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
-            const bool any_a = __any_sync(0xffffffffu, ga), any_b = __any_sync(0xffffffffu, gb);
+            commit_sample(gb, v + 9, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+            const int cnt_a = __popc(__ballot_sync(0xffffffffu, ga)), cnt_b = __popc(__ballot_sync(0xffffffffu, gb));
+            const bool any_a = cnt_a > 0, any_b = cnt_b > 0;
 #ifdef SPLAT_STATS
             {
                 const unsigned el_a = __ballot_sync(0xffffffffu, wa && idx_a <= my_last);
@@ -263,7 +267,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
                 }
             }
 #endif
-            if (any_a || any_b) emit_entry_grads(v, lane, any_a, any_b, (uint32_t)j, jb, a_gid, grad2d);
+            if (any_a || any_b) emit_entry_grads(v, lane, cnt_a, cnt_b, (uint32_t)j, jb, a_gid, grad2d);
         }
         // the next stage() starts with a barrier before it overwrites the staging area
     }
@@ -273,7 +277,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
 // Two pixels per thread: one warp per 8 x 8 block, lane (lx, ly) owns pixels (lx, ly) ["A", top
 // half] and (lx, ly + 4) ["B", bottom half].  The per-pixel recursion and gates are those of
 // blend_backward_block; per staged pair of entries the two pixels' contributions are added in
-// registers before ONE 24-value warp reduction, which now covers 64 pixels (half the reduction
+// registers before ONE 18-value warp reduction, which now covers 64 pixels (half the reduction
 // work per pixel), and the two pixel chains are independent instruction streams.  Entries whose
 // effective rect misses a half skip that half's gates (warp-uniform).
 struct PixBwd {
@@ -403,10 +407,10 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
             const bool wbA = idx_b <= wlA && (mb & kRowsA), wbB = idx_b <= wlB && (mb & kRowsB);
             if (!(waA || waB || wbA || wbB)) continue;
             const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
-            float v[24];
+            float v[18];
 #pragma unroll
-            for (int k = 0; k < 24; ++k) v[k] = 0.0f;
-            bool anyc_a = false, anyc_b = false;
+            for (int k = 0; k < 18; ++k) v[k] = 0.0f;
+            int cnt_a = 0, cnt_b = 0;
             // the lane's two pixels share their column: dx and the dx-only products once per entry
             const float dxa = __fsub_rn(r0a.x, P[0].x), dxb = __fsub_rn(r0b.x, P[0].x);
             const float adxa = __fmul_rn(__fmul_rn(r0a.z, dxa), dxa), adxb = __fmul_rn(__fmul_rn(r0b.z, dxb), dxb);
@@ -426,10 +430,10 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 gb = gb && wb && idx_b <= q.last;
                 commit_sample(ga, v, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
                                 cl_a, dxa, dya);
-                commit_sample(gb, v + 12, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
+                commit_sample(gb, v + 9, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
                                 g_b, cl_b, dxb, dyb);
-                anyc_a |= ga;
-                anyc_b |= gb;
+                cnt_a += __popc(__ballot_sync(0xffffffffu, ga));
+                cnt_b += __popc(__ballot_sync(0xffffffffu, gb));
 #ifdef SPLAT_STATS
                 {  // [0] half-entries evaluated, [1] of which with a commit, [2] eligible lanes, [3] commits
                     const unsigned ca = __ballot_sync(0xffffffffu, ga), cb = __ballot_sync(0xffffffffu, gb);
@@ -444,14 +448,14 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 }
 #endif
             }
-            const bool any_a = __any_sync(0xffffffffu, anyc_a), any_b = __any_sync(0xffffffffu, anyc_b);
+            const bool any_a = cnt_a > 0, any_b = cnt_b > 0;
 #ifdef SPLAT_STATS
             if (lane == 0) {
                 atomicAdd(&g_bstats[4], 1ull);
                 atomicAdd(&g_bstats[5], (unsigned long long)(any_a + any_b));
             }
 #endif
-            if (any_a || any_b) emit_entry_grads(v, lane, any_a, any_b, (uint32_t)j, jb, a_gid, grad2d);
+            if (any_a || any_b) emit_entry_grads(v, lane, cnt_a, cnt_b, (uint32_t)j, jb, a_gid, grad2d);
         }
     }
     pipe.finish();
