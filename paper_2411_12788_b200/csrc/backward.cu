@@ -444,6 +444,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                         atomicAdd(&g_bstats[1], (unsigned long long)((ca != 0) + (cb != 0)));
                         atomicAdd(&g_bstats[2], (unsigned long long)(__popc(ea) + __popc(eb)));
                         atomicAdd(&g_bstats[3], (unsigned long long)(__popc(ca) + __popc(cb)));
+                        atomicAdd(&g_bstats[7], (unsigned long long)(wa != wb));  // half with one eligible entry
                     }
                 }
 #endif
@@ -453,6 +454,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
             if (lane == 0) {
                 atomicAdd(&g_bstats[4], 1ull);
                 atomicAdd(&g_bstats[5], (unsigned long long)(any_a + any_b));
+                atomicAdd(&g_bstats[6], (unsigned long long)(any_a != any_b));  // single-entry reductions
             }
 #endif
             if (any_a || any_b) emit_entry_grads(v, lane, cnt_a, cnt_b, (uint32_t)j, jb, a_gid, grad2d);

@@ -43,7 +43,8 @@ torch.cuda.synchronize()
 lib.splat_debug_bstats(bbuf, 1)
 bv = list(bbuf)
 bnames = ["bwd half-entries evaluated", "  with >=1 commit", "  eligible lanes (idx <= last)",
-          "  committing lanes", "  pair iterations (past the skip test)", "  entries reduced"]
+          "  committing lanes", "  pair iterations (past the skip test)", "  entries reduced",
+          "  reductions with one entry committing", "  half evaluations with one eligible entry"]
 for n, x in zip(bnames, bv):
     print(f"{n:45s} {x:,}")
 print(f"bwd eligible lanes per evaluation {bv[2] / max(bv[0], 1):.1f}, committing {bv[3] / max(bv[1], 1):.1f} per reduction")
