@@ -104,7 +104,7 @@ __device__ __forceinline__ void commit_sample(bool p, float* vv, float& T, float
 
 // Warp-reduce the 18 values of staged entries ja (v[0..8]) and jb (v[9..17]) and add them to
 // the per-Gaussian accumulator (common.cuh kG2Stride records): groups 0-2 (moments, colour) as
-// they are, the commit counts (popcounts of the callers' commit ballots) in the 4th slot of
+// they are, the warp's commit counts (from the callers: ballots or one add-reduction) in the 4th slot of
 // group 2's record.
 __device__ __forceinline__ void emit_entry_grads(const float v[18], int lane, int cnt_a, int cnt_b, uint32_t ja,
                                                  uint32_t jb, uint32_t a_gid, float4* __restrict__ grad2d) {
@@ -410,7 +410,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
             float v[18];
 #pragma unroll
             for (int k = 0; k < 18; ++k) v[k] = 0.0f;
-            int cnt_a = 0, cnt_b = 0;
+            uint32_t ncommit = 0;  // this lane's commits: entry a in the low half-word, b in the high
             // the lane's two pixels share their column: dx and the dx-only products once per entry
             const float dxa = __fsub_rn(r0a.x, P[0].x), dxb = __fsub_rn(r0b.x, P[0].x);
             const float adxa = __fmul_rn(__fmul_rn(r0a.z, dxa), dxa), adxb = __fmul_rn(__fmul_rn(r0b.z, dxb), dxb);
@@ -432,8 +432,7 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                                 cl_a, dxa, dya);
                 commit_sample(gb, v + 9, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
                                 g_b, cl_b, dxb, dyb);
-                cnt_a += __popc(__ballot_sync(0xffffffffu, ga));
-                cnt_b += __popc(__ballot_sync(0xffffffffu, gb));
+                ncommit += (ga ? 1u : 0u) + (gb ? 0x10000u : 0u);
 #ifdef SPLAT_STATS
                 {  // [0] half-entries evaluated, [1] of which with a commit, [2] eligible lanes, [3] commits
                     const unsigned ca = __ballot_sync(0xffffffffu, ga), cb = __ballot_sync(0xffffffffu, gb);
@@ -449,6 +448,9 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                 }
 #endif
             }
+            // the warp's commit counts of both entries in one reduction (<= 64 each)
+            const uint32_t nc = __reduce_add_sync(0xffffffffu, ncommit);
+            const int cnt_a = (int)(nc & 0xffffu), cnt_b = (int)(nc >> 16);
             const bool any_a = cnt_a > 0, any_b = cnt_b > 0;
 #ifdef SPLAT_STATS
             if (lane == 0) {
