@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
                                                                 uint32_t* __restrict__ out, uint64_t n,
                                                                 uint64_t* __restrict__ tmp,
                                                                 uint32_t* __restrict__ total_out) {
-    __shared__ uint32_t s_data[kTile];
+    // padded by one word per 32 (spad): a thread's kItems consecutive elements, read and written
+    // across the warp, would otherwise fall 16 lanes to a bank
+    __shared__ uint32_t s_data[kTile + kTile / 32];
+    auto spad = [](int li) { return li + (li >> 5); };
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint64_t s_tile, s_prefix;
     pdl_wait();
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
     for (int k = 0; k < kItems; ++k) {
         const int li = k * kThreads + threadIdx.x;
         const uint64_t i = base + li;
-        s_data[li] = i < n ? (GATHER ? in[idx[i]] : in[i]) : 0u;
+        s_data[spad(li)] = i < n ? (GATHER ? in[idx[i]] : in[i]) : 0u;
     }
     __syncthreads();
     uint32_t local[kItems];
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         local[k] = s;
-        s += s_data[threadIdx.x * kItems + k];
+        s += s_data[spad(threadIdx.x * kItems + k)];
     }
     uint32_t agg;
     const uint32_t ex = block_exclusive_scan(s, &agg, s_warp);
@@ -170,13 +173,13 @@ __global__ void __launch_bounds__(kThreads) scan_lookback_kernel(const uint32_t*
     __syncthreads();
     const uint32_t off = (uint32_t)s_prefix + ex;
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) s_data[threadIdx.x * kItems + k] = off + local[k];
+    for (int k = 0; k < kItems; ++k) s_data[spad(threadIdx.x * kItems + k)] = off + local[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         const int li = k * kThreads + threadIdx.x;
         const uint64_t i = base + li;
-        if (i < n) out[i] = s_data[li];
+        if (i < n) out[i] = s_data[spad(li)];
     }
 }
 
