@@ -412,7 +412,10 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
     uint32_t* __restrict__ pair_gauss, uint32_t* __restrict__ ranges, uint32_t* __restrict__ tcls,
     uint32_t* __restrict__ tails, uint32_t kpre) {
     constexpr int kW = kL2Threads / 32;
-    __shared__ uint32_t s_c[kPieceK][kW][kSTT];    // (slice k, warp) entries covering tile f, then their list position
+    // (slice k, warp) entries covering tile f, then their list position; rows padded to 17 words so
+    // the column scan below (lane reads rows 2 lane, 2 lane + 1) is 2-way instead of 32-way conflicted
+    constexpr int kRow = kSTT + 1;
+    __shared__ uint32_t s_c[kPieceK][kW][kRow];
     __shared__ uint32_t s_prefix[kSTT];
     __shared__ int s_open;  // tiles of the supertile whose list prefix is not complete yet
     pdl_wait();
@@ -483,12 +486,12 @@ __global__ void __launch_bounds__(kL2Threads, 2) bin_emit_kernel(
         const int f = warp;
         uint32_t* col = &s_c[0][0][0];
         const int q0 = 2 * lane, q1 = 2 * lane + 1;
-        const uint32_t v0 = col[q0 * kSTT + f], v1 = col[q1 * kSTT + f];
+        const uint32_t v0 = col[q0 * kRow + f], v1 = col[q1 * kRow + f];
         const uint32_t inc = warp_incl_scan(v0 + v1, lane);
         const uint32_t list0 = (uint32_t)kSTT * pi.lo_s + (uint32_t)f * cap;
         const uint32_t base = list0 + s_prefix[f];
-        col[q0 * kSTT + f] = base + inc - v0 - v1;
-        col[q1 * kSTT + f] = base + inc - v1;
+        col[q0 * kRow + f] = base + inc - v0 - v1;
+        col[q1 * kRow + f] = base + inc - v1;
         if (lane == 31 && last_piece) {  // last piece: the tile's range (materialised part)
             const int tx = (pi.st % st_x) * kST + (f % kST), ty = (pi.st / st_x) * kST + (f / kST);
             if (tx < tiles_x && ty < tiles_y) {
