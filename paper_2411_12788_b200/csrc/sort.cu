@@ -775,7 +775,9 @@ __global__ void __launch_bounds__(kThreads, 2) radix_coop_kernel(uint32_t* __res
         }
         src = dst;
         STAMP(7 + 6 * j);
-        grid.sync();
+        // the next pass reads what every CTA scattered; after the last pass nothing in this kernel
+        // does (hist / key_range were last read before this pass's phase-C barrier)
+        if (j + 1 < m) grid.sync();
         STAMP(8 + 6 * j);
     }
     // hist was last read before the first pass's first grid barrier: re-zero it for the next sort
