@@ -189,6 +189,7 @@ struct splat_ctx {
     bool loss_recorded = false;  // ev_loss marks the last backward's L1 loss (run_backward)
     cudaStream_t lstream = nullptr;  // the loss read-back of splat_train_step (ahead of the optimiser)
     cudaEvent_t ev_counts = nullptr;    // recorded after the counters' device-to-host copy
+    cudaEvent_t ev_pre = nullptr;       // preprocess done (the counters' publish forks on zstream)
     // A fresh ParamGrads is zero-filled on a side stream concurrently with the blend kernels
     // (HBM-bound fill under issue-bound kernels), ordered after everything enqueued before the
     // view's blend forward (ev_fwd_start) and joined before the chain (ev_zero).
@@ -384,6 +385,7 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
            "map pinned");
     }
     if (!ctx->ev_counts) CK(cudaEventCreateWithFlags(&ctx->ev_counts, cudaEventDisableTiming), "event");
+    if (!ctx->ev_pre) CK(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming), "event");
 
     uint32_t* d_counters = ctx->counters.as<uint32_t>();  // [0] survivors [1] Ps [2] P [3] done blocks
     // the backward's work-order classes (FwdOutputs::cls_cnt), sized for 8 x 8 pixel blocks
@@ -412,12 +414,17 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
         uint32_t* vals = ctx->vals[0].as<uint32_t>();
         CK(launch_preprocess(lc, gp, cp, mask, ctx->rec.as<ProjRec>(), want_depth ? ctx->aux.as<AuxRec>() : nullptr,
                              keys, vals, ctx->tile_counts.as<uint32_t>(), d_counters, ctx->depth.as<float>(), ctx->rect_ref.as<uint2>(),
-                             ctx->host_counters_dev, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr, cls_cnt, tcls),
+                             nullptr, ctx->want_proj ? ctx->proj_dbg.as<float4>() : nullptr),
            "preprocess");
-        // The host needs [n_surv, Ps, P] (sizes and allocations below); preprocess's last block
-        // writes them to mapped pinned memory, so the host waits only for preprocess (event) while
-        // the depth sort runs and the rest of the view is enqueued.
-        CK(cudaEventRecord(ctx->ev_counts, s), "record counts");
+        // The host needs [n_surv, Ps, P] (sizes and allocations below): a one-warp kernel on the
+        // side stream publishes them to mapped pinned memory (and re-zeroes the counters) while
+        // the depth sort starts right behind preprocess; the host waits only for the publish
+        // (event) and the rest of the view is enqueued while the sort runs.
+        CK(cudaEventRecord(ctx->ev_pre, s), "record preprocess");
+        CK(cudaStreamWaitEvent(ctx->zstream, ctx->ev_pre, 0), "publish wait");
+        CK(launch_publish_counts(ctx->zstream, d_counters, ctx->host_counters_dev, cls_cnt, tcls), "publish counts");
+        lc.count++;
+        CK(cudaEventRecord(ctx->ev_counts, ctx->zstream), "record counts");
         bool alt = false;
         CK(depth_sort(ctx, keys, vals, (uint64_t)n, &alt), "depth sort");
         const uint32_t* order = alt ? ctx->vals[1].as<uint32_t>() : vals;
@@ -431,6 +438,8 @@ int run_forward(splat_ctx* ctx, const splat_gaussians* g, const splat_camera* ca
                                          (uint64_t)n, ctx->scan_tmp.as<uint32_t>(), nullptr),
                "scan supertile counts");
         CK(cudaEventSynchronize(ctx->ev_counts), "sync counts");
+        // binning / the forward use the work-order counters the publish re-zeroed
+        CK(cudaStreamWaitEvent(s, ctx->ev_counts, 0), "join counts");
         const volatile uint32_t* hc = ctx->host_counters;
         n_surv = (int)hc[0];
         const uint64_t st_pairs = hc[1];
@@ -967,6 +976,7 @@ int splat_ctx_destroy(splat_ctx* ctx) {
     if (ctx->host_counters) cudaFreeHost(ctx->host_counters);
     if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     if (ctx->ev_counts) cudaEventDestroy(ctx->ev_counts);
+    if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
     if (ctx->lc.work_counters) cudaFree(ctx->lc.work_counters);
     if (ctx->ev_fwd_start) cudaEventDestroy(ctx->ev_fwd_start);
     if (ctx->ev_zero) cudaEventDestroy(ctx->ev_zero);

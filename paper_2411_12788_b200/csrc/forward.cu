@@ -884,6 +884,12 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
     return cudaGetLastError();
 }
 
+cudaError_t launch_publish_counts(cudaStream_t s, uint32_t* n_survivors_dev, uint32_t* host_counts, uint32_t* cls_cnt,
+                                  uint32_t* tcls_cnt) {
+    publish_counts_kernel<<<1, 32, 0, s>>>(n_survivors_dev, host_counts, cls_cnt, tcls_cnt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_blend_forward(LaunchCtx& lc, const CamParams& cp, const uint32_t* ranges,
                                  const uint32_t* pair_gauss, const ProjRec* rec, const AuxRec* aux, const float bg[3],
                                  const FwdOutputs& out, const uint32_t* tcls) {

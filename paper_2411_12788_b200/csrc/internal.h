@@ -103,6 +103,11 @@ cudaError_t launch_preprocess(LaunchCtx& lc, const GaussianPtrs& g, const CamPar
                               float* depth_out, uint2* rect_ref, uint32_t* host_counts = nullptr,
                               float4* proj_dbg = nullptr, uint32_t* cls_cnt = nullptr, uint32_t* tcls_cnt = nullptr);
 
+// [survivors, Ps, P] to the host's mapped memory + the counters re-zeroed (one warp), on a side
+// stream so the depth sort does not queue behind it.
+cudaError_t launch_publish_counts(cudaStream_t s, uint32_t* n_survivors_dev, uint32_t* host_counts, uint32_t* cls_cnt,
+                                  uint32_t* tcls_cnt);
+
 // ---- binning.cu ---------------------------------------------------------------------------
 constexpr int kTailNoteWord = 9;  // host_counters[9]: a forward walked past a tile-list prefix
 constexpr int kKeyRangeWord = 8;  // counters[8..9]: the depth sort's key-range scratch (zero at rest)
