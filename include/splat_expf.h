@@ -86,7 +86,20 @@ SPLAT_HD float splat_expf(float x) {
  * tests/test_expf.py).  The blend kernels use it after the `power >= cut` test, which confines
  * the argument to [ln(cmin) - 1e-3, 0]. */
 SPLAT_HD float splat_expf_core(float x) {
-    const float kf = rintf(splat_mul(x, 1.44269502162933349609375f));
+    /* rint(x / ln2) by the 1.5 * 2^23 shifter: in the core's domain |x / ln2| < 2^22, so the
+     * sum lands in [2^23, 2^24) (ulp 1) and rounds x / ln2 to the nearest integer, ties to even,
+     * exactly as rintf; the shifter's low mantissa bits are that integer k.  Two adds and an
+     * integer subtract instead of a round and a float-to-int conversion (the XU pipe). */
+    const float t = splat_mul(x, 1.44269502162933349609375f);
+    const float sh = splat_fma(1.0f, t, 12582912.0f);   /* t + 1.5 * 2^23, rounded once */
+    const float kf = splat_fma(1.0f, sh, -12582912.0f); /* exact */
+    uint32_t shb;
+#if defined(__CUDA_ARCH__)
+    shb = __float_as_uint(sh);
+#else
+    memcpy(&shb, &sh, 4);
+#endif
+    const int k = (int)(shb - 0x4B400000u);
     float r = splat_fma(kf, -0.693145751953125f, x);
     r = splat_fma(kf, -1.428606765330187045037746429443359375e-06f, r);
     float p = 1.98412698412698412698e-4f;
@@ -97,7 +110,7 @@ SPLAT_HD float splat_expf_core(float x) {
     p = splat_fma(p, r, 0.5f);
     p = splat_fma(p, r, 1.0f);
     p = splat_fma(p, r, 1.0f);
-    return splat_mul(p, splat_bits_to_float((uint32_t)((int)kf + 127) << 23));
+    return splat_mul(p, splat_bits_to_float((uint32_t)(k + 127) << 23));
 }
 
 SPLAT_HD float splat_add(float a, float b) {
