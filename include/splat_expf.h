@@ -113,6 +113,35 @@ SPLAT_HD float splat_expf_core(float x) {
     return splat_mul(p, splat_bits_to_float((uint32_t)(k + 127) << 23));
 }
 
+/* splat_expf_core with the final scaling as an exponent add: for k >= -125 (x >= -86.6) p * 2^k
+ * is a normal float, so the product is exact and equals p's bits plus k << 23 — one integer
+ * multiply-add instead of building 2^k and a multiply.  Bit-identical to splat_expf on
+ * [-86.6, 0] (tests/test_expf.py); the gates use it on [ln(cmin) - 1e-3, 0]. */
+SPLAT_HD float splat_expf_gate(float x) {
+    const float t = splat_mul(x, 1.44269502162933349609375f);
+    const float sh = splat_fma(1.0f, t, 12582912.0f);
+    const float kf = splat_fma(1.0f, sh, -12582912.0f);
+    float r = splat_fma(kf, -0.693145751953125f, x);
+    r = splat_fma(kf, -1.428606765330187045037746429443359375e-06f, r);
+    float p = 1.98412698412698412698e-4f;
+    p = splat_fma(p, r, 1.38888888888888888889e-3f);
+    p = splat_fma(p, r, 8.33333333333333333333e-3f);
+    p = splat_fma(p, r, 4.16666666666666666667e-2f);
+    p = splat_fma(p, r, 1.66666666666666666667e-1f);
+    p = splat_fma(p, r, 0.5f);
+    p = splat_fma(p, r, 1.0f);
+    p = splat_fma(p, r, 1.0f);
+    uint32_t shb, pb;
+#if defined(__CUDA_ARCH__)
+    shb = __float_as_uint(sh);
+    pb = __float_as_uint(p);
+#else
+    memcpy(&shb, &sh, 4);
+    memcpy(&pb, &p, 4);
+#endif
+    return splat_bits_to_float(pb + ((shb - 0x4B400000u) << 23));
+}
+
 SPLAT_HD float splat_add(float a, float b) {
 #if defined(__CUDA_ARCH__)
     return __fadd_rn(a, b);

@@ -165,7 +165,7 @@ __device__ __forceinline__ bool gate_sample_nb(const float4& r0, const float4& r
         ok = ok && !(power < r1.w);
         // unconditional: measured faster than a branch around it for the lanes that need it
         // (forward 301 -> 311 us, backward 491 -> 538 us)
-        g2d = splat_expf_core(power);  // meaningless (never used) outside [cut, 0]
+        g2d = splat_expf_gate(power);  // meaningless (never used) outside [cut, 0]
         alpha = __fmul_rn(r1.y, g2d);
         clamped = alpha > alpha_max;
         alpha = clamped ? alpha_max : alpha;
@@ -193,7 +193,7 @@ __device__ __forceinline__ bool gate_sample_col(const float4& r0, const float4& 
     bool ok = inrect && !(power > 0.0f);
     if (THR) {
         ok = ok && !(power < r1.w);
-        g2d = splat_expf_core(power);  // meaningless (never used) outside [cut, 0]
+        g2d = splat_expf_gate(power);  // meaningless (never used) outside [cut, 0]
         alpha = __fmul_rn(r1.y, g2d);
         clamped = alpha > alpha_max;
         alpha = clamped ? alpha_max : alpha;

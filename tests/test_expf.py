@@ -1,5 +1,5 @@
-"""The shared exponential (include/splat_expf.h): accuracy, and splat_expf_core == splat_expf on
-the range the blend kernels use it for."""
+"""The shared exponential (include/splat_expf.h): accuracy, and splat_expf_core / splat_expf_gate ==
+splat_expf on the ranges the blend kernels use them for."""
 import subprocess
 from pathlib import Path
 
@@ -11,7 +11,7 @@ SRC = r'''
 #include <stdio.h>
 #include <stdlib.h>
 int main(void) {
-    long n = 0, over1ulp = 0, core_diff = 0;
+    long n = 0, over1ulp = 0, core_diff = 0, gate_diff = 0;
     /* every 61st float in [-103.9, 88.7]; exhaustive for core on every 7th float in [-87.3, 0] */
     for (uint32_t u = 0; u < 0xFFFFFFFFu - 61; u += 61) {
         float x; memcpy(&x, &u, 4);
@@ -27,8 +27,12 @@ int main(void) {
         if (!(x >= -87.3f)) continue;
         float a = splat_expf(x), b = splat_expf_core(x);
         if (memcmp(&a, &b, 4)) ++core_diff;
+        if (x >= -86.6f) {
+            float c = splat_expf_gate(x);
+            if (memcmp(&a, &c, 4)) ++gate_diff;
+        }
     }
-    printf("%ld %ld %ld\n", n, over1ulp, core_diff);
+    printf("%ld %ld %ld %ld\n", n, over1ulp, core_diff, gate_diff);
     return 0;
 }
 '''
@@ -40,10 +44,12 @@ def test_splat_expf_accuracy_and_core(tmp_path):
     exe = tmp_path / "t"
     subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off", f"-I{ROOT / 'include'}", str(c), "-o", str(exe), "-lm"],
                    check=True)
-    n, over, core = (int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split())
+    n, over, core, gate = (int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                          check=True).stdout.split())
     assert n > 10_000_000
     assert over == 0, f"{over} samples off by more than 1 ulp"
     assert core == 0, f"splat_expf_core differs from splat_expf on {core} samples"
+    assert gate == 0, f"splat_expf_gate differs from splat_expf on {gate} samples"
 
 
 def test_oracle_exp_modes():
