@@ -7,6 +7,7 @@
 // the set of committed samples is identical to the forward's.  FMA contraction is allowed here.
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -75,6 +76,7 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float x, float y, float
 // instead of three channels.  Branch-free: the kernels call it for every lane, and a sample the
 // pixel does not commit (p false) contributes exactly nothing (alpha = G = 0: T unchanged, w = 0,
 // B += 0) and is not counted — measured faster than a divergent branch (backward 484 -> 450 us).
+template <bool ACC = true>  // false: the first sample into vv assigns (no zero-init, no 0 + x)
 __device__ __forceinline__ void commit_sample(bool p, float* vv, float& T, float& B, float dL0, float dL1, float dL2,
                                               const float4& r2, float alpha, float g2d, bool clamped, float dx,
                                               float dy) {
@@ -86,18 +88,19 @@ __device__ __forceinline__ void commit_sample(bool p, float* vv, float& T, float
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(one_m_a));
     const float t_before = p ? T * rcp : T;
     const float w = t_before * a;
-    vv[6] += w * dL0;
-    vv[7] += w * dL1;
-    vv[8] += w * dL2;
+    auto put = [&](int k, float x) { vv[k] = ACC ? vv[k] + x : x; };
+    put(6, w * dL0);
+    put(7, w * dL1);
+    put(8, w * dL2);
     const float diff = (dL0 * r2.x + dL1 * r2.y + dL2 * r2.z) - B;
     const float sv = clamped ? 0.0f : t_before * diff * g;
     const float sx = sv * dx, sy = sv * dy;
-    vv[0] += sv;
-    vv[1] += sx;
-    vv[2] += sy;
-    vv[3] += sx * dx;
-    vv[4] += sx * dy;
-    vv[5] += sy * dy;
+    put(0, sv);
+    put(1, sx);
+    put(2, sy);
+    put(3, sx * dx);
+    put(4, sx * dy);
+    put(5, sy * dy);
     B = B + a * diff;
     T = t_before;
 }
@@ -246,11 +249,10 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
             gb = gb && wb && idx_b <= my_last;
             // v: (dmean.x, dmean.y, dconic00 | dconic01, dconic11, dopacity | dcolour rgb | commits)
             // for entry a in v[0..11], entry b in v[12..23]
-            float v[18];
-#pragma unroll
-            for (int k = 0; k < 18; ++k) v[k] = 0.0f;
-            commit_sample(ga, v, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
-            commit_sample(gb, v + 9, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb, dyb);
+            float v[18];  // assigned by the two commits (entry a: v[0..8], b: v[9..17])
+            commit_sample<false>(ga, v, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a, cl_a, dxa, dya);
+            commit_sample<false>(gb, v + 9, T, B, dL0, dL1, dL2, lds_f4(a_r2 + 16u * jb), alpha_b, g_b, cl_b, dxb,
+                                 dyb);
             const int cnt_a = __popc(__ballot_sync(0xffffffffu, ga)), cnt_b = __popc(__ballot_sync(0xffffffffu, gb));
             const bool any_a = cnt_a > 0, any_b = cnt_b > 0;
 #ifdef SPLAT_STATS
@@ -408,17 +410,15 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
             if (!(waA || waB || wbA || wbB)) continue;
             const float4 r0a = lds_f4(a_r0 + 16u * j), r0b = lds_f4(a_r0 + 16u * jb);
             float v[18];
-#pragma unroll
-            for (int k = 0; k < 18; ++k) v[k] = 0.0f;
-            uint32_t ncommit = 0;  // this lane's commits: entry a in the low half-word, b in the high
+            uint32_t ncommit;  // this lane's commits: entry a in the low half-word, b in the high
             // the lane's two pixels share their column: dx and the dx-only products once per entry
             const float dxa = __fsub_rn(r0a.x, P[0].x), dxb = __fsub_rn(r0b.x, P[0].x);
             const float adxa = __fmul_rn(__fmul_rn(r0a.z, dxa), dxa), adxb = __fmul_rn(__fmul_rn(r0b.z, dxb), dxb);
             const float wdxa = __fmul_rn(r0a.w, dxa), wdxb = __fmul_rn(r0b.w, dxb);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            // one half's gates and commits; the first half evaluated assigns v (ACC false)
+            auto run_half = [&](auto acc, const int h) {
+                constexpr bool ACC = decltype(acc)::value;
                 const bool wa = h == 0 ? waA : waB, wb = h == 0 ? wbA : wbB;
-                if (!(wa || wb)) continue;
                 PixBwd& q = P[h];
                 float alpha_a, g_a, dya, alpha_b, g_b, dyb;
                 bool cl_a, cl_b;
@@ -428,11 +428,12 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                                                dyb);
                 ga = ga && wa && idx_a <= q.last;
                 gb = gb && wb && idx_b <= q.last;
-                commit_sample(ga, v, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
-                                cl_a, dxa, dya);
-                commit_sample(gb, v + 9, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
-                                g_b, cl_b, dxb, dyb);
-                ncommit += (ga ? 1u : 0u) + (gb ? 0x10000u : 0u);
+                commit_sample<ACC>(ga, v, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * j), alpha_a, g_a,
+                                   cl_a, dxa, dya);
+                commit_sample<ACC>(gb, v + 9, q.T, q.B, q.dL0, q.dL1, q.dL2, lds_f4(a_r2 + 16u * jb), alpha_b,
+                                   g_b, cl_b, dxb, dyb);
+                const uint32_t nh = (ga ? 1u : 0u) + (gb ? 0x10000u : 0u);
+                ncommit = ACC ? ncommit + nh : nh;
 #ifdef SPLAT_STATS
                 {  // [0] half-entries evaluated, [1] of which with a commit, [2] eligible lanes, [3] commits
                     const unsigned ca = __ballot_sync(0xffffffffu, ga), cb = __ballot_sync(0xffffffffu, gb);
@@ -447,6 +448,13 @@ __device__ __forceinline__ void blend_backward_block_px2(int bid, CamParams cp, 
                     }
                 }
 #endif
+            };
+            // (the skip test above guarantees at least one half)
+            if (waA || wbA) {
+                run_half(std::false_type{}, 0);
+                if (waB || wbB) run_half(std::true_type{}, 1);
+            } else {
+                run_half(std::false_type{}, 1);
             }
             // the warp's commit counts of both entries in one reduction (<= 64 each)
             const uint32_t nc = __reduce_add_sync(0xffffffffu, ncommit);
