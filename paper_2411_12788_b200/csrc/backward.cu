@@ -147,7 +147,7 @@ __device__ __forceinline__ void blend_backward_block(int bid, CamParams cp, cons
     __shared__ StageRaw<BW * BH> raw;
     __shared__ float s_red[BW * BH / 32];
     __shared__ int s_maxlast[BW * BH / 32];
-    const int nthreads = blockDim.x;
+    constexpr int nthreads = BW * BH;  // (every launch uses BW * BH threads)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = nthreads >> 5;
     const int ts = cp.tile_size;

@@ -404,6 +404,9 @@ __device__ __forceinline__ int list_tail_setup(const uint32_t* __restrict__ tail
 // CULL = false: the list is already block-culled (the forward's per-block list): keep every entry.
 template <int CAP, typename PosFn, bool CULL = true, int ITEMS = 1>
 struct StagePipe {
+    // every user launches CAP / ITEMS threads: compile-time counts let the per-batch warp-count
+    // loops unroll (they ran as runtime loops over blockDim)
+    static constexpr int kThreads = CAP / ITEMS, kWarps = kThreads / 32;
     // ITEMS entries per thread and batch: slot s = q * blockDim.x + tid holds list position
     // pos(b, s); batches are CAP = ITEMS * blockDim.x entries, compacted in slot order.
     PosFn pos;
@@ -441,7 +444,7 @@ struct StagePipe {
             if (idx_f[q] >= 0) {
                 const float4* src = reinterpret_cast<const float4*>(rec + gid_f[q]);
                 const uint32_t dst =
-                    (uint32_t)__cvta_generic_to_shared(&raw->r[q * blockDim.x + threadIdx.x][0]);
+                    (uint32_t)__cvta_generic_to_shared(&raw->r[q * kThreads + threadIdx.x][0]);
                 cp_async16(dst, src);
                 cp_async16(dst + 16u, src + 1);
                 cp_async16(dst + 32u, src + 2);
@@ -453,14 +456,14 @@ struct StagePipe {
     __device__ __forceinline__ void start() {
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
-            const int sl = q * blockDim.x + threadIdx.x;
+            const int sl = q * kThreads + threadIdx.x;
             idx_f[q] = pos(0, sl);
             gid_f[q] = fetch(idx_f[q]);
         }
         launch_copy();
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
-            const int sl = q * blockDim.x + threadIdx.x;
+            const int sl = q * kThreads + threadIdx.x;
             idx_n[q] = pos(1, sl);
             gid_n[q] = fetch(idx_n[q]);
         }
@@ -470,7 +473,8 @@ struct StagePipe {
     // b+1's copies and batch b+2's id loads.  Returns the staged count, or -1 when no thread of
     // the CTA is `active` (every thread gets the same answer; nothing is staged then).
     __device__ __forceinline__ int stage(int b, bool active, int bx0, int bx1, int by0, int by1, StageSmem<CAP>& sm) {
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        constexpr int nwarps = kWarps;
         cp_async_wait_all();
         // raw is complete and visible; every thread is done reading the previous staging area
         if (__syncthreads_count(active) == 0) return -1;
@@ -480,7 +484,7 @@ struct StagePipe {
         for (int q = 0; q < ITEMS; ++q) {
             keep[q] = false;
             if (idx_f[q] >= 0) {
-                const int sl = q * blockDim.x + tid;
+                const int sl = q * kThreads + tid;
                 keep[q] = CULL ? may_contribute(raw->r[sl][0], raw->r[sl][1], raw->r[sl][2].w, bx0, bx1, by0, by1)
                                : true;
             }
@@ -497,7 +501,7 @@ struct StagePipe {
             int off = 0;
             for (int w = 0; w < q * nwarps + warp; ++w) off += sm.wcnt[w];
             const int p = off + __popc(m[q] & lt);
-            const int sl = q * blockDim.x + tid;  // re-read from shared memory: no records held across the barrier
+            const int sl = q * kThreads + tid;  // re-read from shared memory: no records held across the barrier
             ProjRec r;
             r.r0 = raw->r[sl][0];
             r.r1 = raw->r[sl][1];
@@ -521,7 +525,7 @@ struct StagePipe {
         launch_copy();
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
-            const int sl = q * blockDim.x + tid;
+            const int sl = q * kThreads + tid;
             idx_n[q] = pos(b + 2, sl);
             gid_n[q] = fetch(idx_n[q]);
         }

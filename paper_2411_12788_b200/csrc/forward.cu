@@ -396,7 +396,7 @@ __device__ __forceinline__ void blend_forward_block(int bid, CamParams cp, const
     __shared__ StageRaw<CAP> raw;
     __shared__ float s_imp[REPORT ? CAP : 1];
     __shared__ uint32_t s_maxw[REPORT ? CAP : 1];
-    const int nthreads = blockDim.x;
+    const int nthreads = blockDim.x;  // (a compile-time BW * BH here measured slower: 261 -> 283 us)
     const int tid = threadIdx.x;
     const int ts = cp.tile_size;
     constexpr int bw = BW;
