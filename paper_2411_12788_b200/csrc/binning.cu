@@ -33,8 +33,9 @@ namespace {
 constexpr int kST = 4;              // supertile side in tiles
 constexpr int kSTT = kST * kST;     // tiles per supertile
 constexpr int kL2Threads = 512;     // level-2 CTA: one per piece of a supertile list
-constexpr int kStChunk = 128;       // depth-ordered survivors per warp of the supertile pass
-constexpr int kStWarps = 16;        // warps per supertile-count CTA (one count column per 2048 survivors)
+constexpr int kStChunk = 96;        // depth-ordered survivors per warp of the supertile pass (96: 0.6 % faster
+                                    // than 128, shorter emit warps, less wave tail; 64: the scan grows)
+constexpr int kStWarps = 16;        // warps per supertile-count CTA (one count column per 1536 survivors)
 constexpr int kEmitWarps = 1;       // warps per supertile-emit CTA (1: 60 us, 4 independent warps: 67 us)
 constexpr int kStChunkCta = kStChunk * kStWarps;  // survivors per CTA chunk (one count column)
 constexpr int kStMaxSmem = 3328;    // supertiles the chunked pass keeps in shared memory (x kStWarps rows)
