@@ -35,7 +35,8 @@ constexpr int kSTT = kST * kST;     // tiles per supertile
 constexpr int kL2Threads = 512;     // level-2 CTA: one per piece of a supertile list
 constexpr int kStChunk = 96;        // depth-ordered survivors per warp of the supertile pass (96: 0.6 % faster
                                     // than 128, shorter emit warps, less wave tail; 64: the scan grows)
-constexpr int kStWarps = 16;        // warps per supertile-count CTA (one count column per 1536 survivors)
+constexpr int kStWarps = 12;        // warps per supertile-count CTA (one count column per 1152 survivors;
+                                    // 12: +0.3 % over 16, a smaller last wave of count CTAs)
 constexpr int kEmitWarps = 1;       // warps per supertile-emit CTA (1: 60 us, 4 independent warps: 67 us)
 constexpr int kStChunkCta = kStChunk * kStWarps;  // survivors per CTA chunk (one count column)
 constexpr int kStMaxSmem = 3328;    // supertiles the chunked pass keeps in shared memory (x kStWarps rows)
